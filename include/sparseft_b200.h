@@ -1,0 +1,158 @@
+/*
+ * sparseft_b200.h — C-ABI of the B200-native Long Exposure hot path.
+ *
+ * The drop-in boundary for the reference `sparseft` package
+ * (/root/reference/pkg/src/sparseft, cited as sf/<file>:<line>). Each entry
+ * point replaces the reference function(s) named in its comment; the Python
+ * host layer (paper_2510_15964_b200/*.py) keeps the reference's names and
+ * argument meaning and binds these symbols with ctypes.
+ *
+ * Conventions
+ *   - plain device pointers + sizes; no torch types. bf16 = uint16_t storage.
+ *   - every call is stream-ordered on `stream` and never synchronises the host.
+ *   - the library allocates nothing; callers pass workspaces.
+ *   - return 0 on success, else an LX_ERR_* code; lx_last_error() describes it.
+ *     The host shim maps codes to the reference exception types
+ *     (ShapeError, LayoutError, MaskError, PatternError).
+ *   - deterministic at a fixed launch configuration (no float atomics).
+ */
+#ifndef SPARSEFT_B200_H
+#define SPARSEFT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* lx_stream_t;
+
+#define LX_OK 0
+#define LX_ERR_SHAPE 1       /* sf/tensor_core.py:15 ShapeError   */
+#define LX_ERR_LAYOUT 2      /* sf/block_sparse.py:18 LayoutError */
+#define LX_ERR_MASK 3        /* sf/neuron_ops.py:18 MaskError     */
+#define LX_ERR_PATTERN 4     /* sf/patterns.py:20 PatternError    */
+#define LX_ERR_CUDA 5
+#define LX_ERR_UNSUPPORTED 6 /* shape outside the sm_100a kernels' envelope */
+
+const char* lx_last_error(void);
+int lx_abi_version(void);
+int lx_device_sm_count(void);
+
+/* ------------------------------------------------------------------ generic
+ * C[M,N] (fp32 or bf16) = A[M,K] * B[N,K]^T, bf16 inputs, tcgen05 path.
+ * Used by the predictor projections and by tests of the GEMM engine. */
+int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void* c, int ldc, int c_is_f32, int M, int N,
+                    int K, lx_stream_t stream);
+
+/* ------------------------------------------------------------------ K1 mask build
+ * approx_mlp_scores + predict_mlp_mask + active_columns
+ *   (sf/predictor.py:121-139, sf/neuron_ops.py:67-72)
+ * h:      bf16 [n_items*s, d] post-LN2 MLP input (one item = one sequence)
+ * wa_t:   bf16 [n_blk, d]  (Wa_hat transposed: each block's scoring vector contiguous)
+ * scope_batch: 0 = per-item masks (sf/harness.py:204-211), 1 = OR over items (sf/predictor.py:132-136)
+ * bits_ws: uint32 [n_items, ceil(n_blk/32)] workspace
+ * counts: int32 [n_items]; ids: int32 [n_items, n_blk] ascending active block ids;
+ * pos:    int32 [n_items, n_blk] packed position of each block or -1
+ * scores_dump: optional fp32 [n_items*s, n_blk] copy of S_hat (parity tests) */
+int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint16_t* wa_t, int n_blk, float threshold,
+                        int scope_batch, uint32_t* bits_ws, int32_t* counts, int32_t* ids, int32_t* pos,
+                        float* scores_dump, lx_stream_t stream);
+
+/* Compaction only: bitmask words -> counts/ids/pos (used when masks come from a provider). */
+int lx_mask_compact(const uint32_t* bits, int n_items, int n_blk, int scope_batch, int32_t* counts, int32_t* ids,
+                    int32_t* pos, lx_stream_t stream);
+
+/* predict_attention_patterns + select_pattern_by_coverage
+ *   (sf/predictor.py:62-118, sf/exposer.py:71-85)
+ * x_small: bf16 [n_items*m, d] downsampled rows (m = ceil(sqrt(s)), rows min(i*s//m, s-1))
+ * wqk_t:   bf16 [2*H*r, d]: rows [h*r,(h+1)*r) = Wq_hat[h]^T, rows [(H+h)*r, ...) = Wk_hat[h]^T
+ * pool_kind/pool_param: pool in reference order (kind 0 blockdiag,1 band,2 causal,3 global,4 strided,5 dense)
+ * proj_ws: fp32 [n_items*m, 2*H*r] workspace; pattern_idx: int32 [n_items(or 1), H] pool index
+ * scores_dump: optional fp32 [n_items, H, m, m] */
+int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, int d, const uint16_t* wqk_t, int H,
+                                  int r, float threshold_frac, double tau, int n_b, const int32_t* pool_kind,
+                                  const int32_t* pool_param, int n_pool, int scope_batch, float* proj_ws,
+                                  int32_t* pattern_idx, float* scores_dump, lx_stream_t stream);
+
+/* ------------------------------------------------------------------ K2 neuron-sparse MLP
+ * Layout: w1_t bf16 [d_ff, d] (= W1 column-major, sf/neuron_ops.py:31-45), w2 bf16 [d_ff, d].
+ * Hidden tensors are packed per item: row t of item b holds its active columns
+ * [0, counts[b]*blk) in ascending block order, row stride ld_h (>= d_ff).
+ * LoRA factors are fp32 (trainable); pass NULL to skip a term. */
+
+/* neuron_matmul_fwd1 + b1 + scaling*(x A1) B1[:,cols] + ReLU   (sf/neuron_ops.py:75-82, sf/model.py:376-386)
+ * ax1: fp32 [M, r] = x A1 (from lx_rowproj); b1_lora: fp32 [r, d_ff] */
+int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w1_t,
+                  const int32_t* counts, const int32_t* ids, const float* b1, const float* ax1, const float* b1_lora,
+                  int r, float scaling, uint16_t* a_out, int ld_h, lx_stream_t stream);
+
+/* neuron_matmul_fwd2 + b2 + scaling*(a A2[cols]) B2   (sf/neuron_ops.py:85-95, sf/model.py:388-395)
+ * ax2: fp32 [M, r]; b2_lora: fp32 [r, d] */
+int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
+                  const int32_t* counts, const int32_t* ids, const float* b2, const float* ax2, const float* b2_lora,
+                  int r, float scaling, uint16_t* out, lx_stream_t stream);
+
+/* mlp_backward input-grad through fc2 and ReLU   (sf/autograd.py:97-106)
+ * dz = (dO W2[cols]^T + dax2 A2[cols]^T) * (a > 0); dax2 fp32 [M,r] (already scaled); a2: fp32 [d_ff, r] */
+int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
+                        const int32_t* counts, const int32_t* ids, const float* dax2, const float* a2_lora, int r,
+                        const uint16_t* a, uint16_t* dz, int ld_h, lx_stream_t stream);
+
+/* mlp_backward input-grad through fc1   (sf/autograd.py:112-120)
+ * dx = dz W1[:,cols]^T + dax1 A1^T; dax1 fp32 [M,r] (already scaled); a1: fp32 [d, r] */
+int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d, int d_ff, int blk,
+                        const uint16_t* w1_t, const int32_t* counts, const int32_t* ids, const float* dax1,
+                        const float* a1_lora, int r, uint16_t* dx, lx_stream_t stream);
+
+/* Skinny LoRA row projection: Y[M, r] = scale * X[M, K] W, K optionally gathered per item.
+ *   X bf16 row stride ldx; W(k, q) = w[k_orig*w_sk + q*w_sq]; k_orig = k (dense, counts==NULL) or
+ *   ids[b][k/blk]*blk + k%blk over the item's packed K = counts[b]*blk.  (x A1, a A2[cols], dO B2^T, dz B1[:,cols]^T) */
+int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const float* w, long long w_sk, long long w_sq,
+               int r, float scale, const int32_t* counts, const int32_t* ids, int blk, float* y, lx_stream_t stream);
+
+/* Skinny LoRA gradient reduction over tokens: G[q, c_orig] += scale * sum_rows P[row, q] X[row, c]
+ *   (dB1[:,cols], dA2[cols] (transposed), dB2, dA1 (transposed)); summed over items in order.
+ *   X bf16 [M, ncols(packed)] row stride ldx; G fp32 with G(q, c) = g[q*g_sq + c*g_sc].
+ *   ws: fp32 workspace of lx_colgrad_ws_floats(...) floats. Deterministic. */
+long long lx_colgrad_ws_floats(int n_items, int s, int ncols, int r);
+int lx_colgrad(const float* p, const uint16_t* x, int ldx, int n_items, int s, int ncols, int r, float scale,
+               const int32_t* counts, const int32_t* pos, int blk, float* g, long long g_sq, long long g_sc, float* ws,
+               lx_stream_t stream);
+
+/* Column sums of a packed bf16 matrix per original column (BitFit db1[cols] = sum dz; sf/autograd.py:107-111). */
+int lx_colsum(const uint16_t* x, int ldx, int n_items, int s, int ncols, const int32_t* counts, const int32_t* pos,
+              int blk, float* out, float* ws, lx_stream_t stream);
+
+/* ------------------------------------------------------------------ K3 block-sparse attention
+ * q,k,v,o: bf16 [n_items*s, ld] with head h at columns [h*hd, (h+1)*hd); non-causal; scale = 1/sqrt(hd).
+ * pattern_idx: int32 [n_items, H] pool index per (item, head) (or [1,H] with item_stride 0).
+ * Tile tables (from lx_attn_tables): per pool pattern, CSR over q-tiles and CSC over k-tiles of
+ * 64x64 tiles with a 16-bit mask of active 16x16 cells.
+ * fwd = sdd -> sparse_softmax -> dsd (sf/block_sparse.py:47-126); lse fp32 [n_items, H, s]. */
+int lx_attn_tables_size(int n_pool, int s, int attn_blk, int* n_row_entries);
+int lx_attn_tables(const int32_t* pool_kind_host, const int32_t* pool_param_host, int n_pool, int s, int attn_blk,
+                   int32_t* host_out, int host_out_ints);
+int lx_bsattn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, int ld, int n_items, int s, int H, int hd,
+                  const int32_t* pattern_idx, int item_stride, const int32_t* tables, int n_pool, float scale,
+                  uint16_t* o, int ldo, float* lse, lx_stream_t stream);
+/* dsd_backward -> sparse_softmax_backward -> sdd_backward (sf/block_sparse.py:63-137).
+ * delta_ws fp32 [n_items, H, s]; dq/dk/dv bf16 like q. */
+int lx_bsattn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o, const uint16_t* d_o, int ld,
+                  int n_items, int s, int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables,
+                  int n_pool, float scale, const float* lse, float* delta_ws, uint16_t* dq, uint16_t* dk, uint16_t* dv,
+                  lx_stream_t stream);
+
+/* ------------------------------------------------------------------ glue (fused neighbours)
+ * layernorm_forward (sf/model.py:307-312), fp32 residual in, bf16 out; saves mean/inv_std.
+ * Optionally also writes the predictor's downsampled rows (sf/predictor.py:62-71) to x_small. */
+int lx_layernorm_fwd(const float* x, int M, int d, const float* gamma, const float* beta, float eps, uint16_t* y,
+                     float* mean, float* inv_std, int s, int m_small, uint16_t* x_small, lx_stream_t stream);
+/* layernorm_backward (sf/autograd.py:61-66): dx_accum += LN'(dy), dy bf16 or fp32 (dy_is_f32). */
+int lx_layernorm_bwd(const void* dy, int dy_is_f32, const float* x, const float* gamma, const float* mean,
+                     const float* inv_std, int M, int d, float* dx_accum, lx_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,89 @@
+"""ctypes binding of the C-ABI (include/sparseft_b200.h).
+
+Loads the in-tree `libsparseft_b200.so`. There is no fallback: if the library
+is missing or no sm_100 GPU is present, calls raise immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from . import errors as E
+
+LIB_PATH = Path(__file__).resolve().parent / "libsparseft_b200.so"
+
+_P = C.c_void_p
+_I = C.c_int
+_F = C.c_float
+_D = C.c_double
+_LL = C.c_longlong
+
+# symbol -> argtypes (order as declared in include/sparseft_b200.h)
+SIGNATURES: dict[str, list] = {
+    "lx_last_error": [],
+    "lx_abi_version": [],
+    "lx_device_sm_count": [],
+    "lx_gemm_bf16_tn": [_P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _P],
+    "lx_predict_mlp_mask": [_P, _I, _I, _I, _P, _I, _F, _I, _P, _P, _P, _P, _P, _P],
+    "lx_mask_compact": [_P, _I, _I, _I, _P, _P, _P, _P],
+    "lx_predict_attention_patterns": [_P, _I, _I, _I, _P, _I, _I, _F, _D, _I, _P, _P, _I, _I, _P, _P, _P, _P],
+    "lx_neuron_fc1": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _P, _I, _P],
+    "lx_neuron_fc2": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _P, _P],
+    "lx_neuron_fc2_dgrad": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P],
+    "lx_neuron_fc1_dgrad": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P],
+    "lx_rowproj": [_P, _I, _I, _I, _I, _P, _LL, _LL, _I, _F, _P, _P, _I, _P, _P],
+    "lx_colgrad_ws_floats": [_I, _I, _I, _I],
+    "lx_colgrad": [_P, _P, _I, _I, _I, _I, _I, _F, _P, _P, _I, _P, _LL, _LL, _P, _P],
+    "lx_colsum": [_P, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P],
+    "lx_attn_tables_size": [_I, _I, _I, _P],
+    "lx_attn_tables": [_P, _P, _I, _I, _I, _P, _I],
+    "lx_bsattn_fwd": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _I, _P, _P],
+    "lx_bsattn_bwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P, _P],
+    "lx_layernorm_fwd": [_P, _I, _I, _P, _P, _F, _P, _P, _P, _I, _I, _P, _P],
+    "lx_layernorm_bwd": [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P],
+}
+RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_ws_floats": _LL}
+
+_ERRORS = {1: E.ShapeError, 2: E.LayoutError, 3: E.MaskError, 4: E.PatternError, 5: E.CudaError, 6: E.UnsupportedError}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load (once) and return the extension; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise E.CudaError(
+                f"{LIB_PATH.name} not built: run `python -m paper_2510_15964_b200.build` (no CPU fallback exists)"
+            )
+        handle = C.CDLL(str(LIB_PATH))
+        for name, argt in SIGNATURES.items():
+            if not hasattr(handle, name):
+                continue  # tests/test_abi_symbols.py asserts the full set is exported
+            fn = getattr(handle, name)
+            fn.argtypes = argt
+            fn.restype = RESTYPES.get(name, _I)
+        _lib = handle
+    return _lib
+
+
+def call(name: str, *args) -> int:
+    """Invoke an entry point; map a nonzero return code to the reference's exception type."""
+    rc = getattr(lib(), name)(*args)
+    if isinstance(rc, int) and rc != 0 and name not in ("lx_abi_version", "lx_device_sm_count", "lx_attn_tables_size"):
+        msg = lib().lx_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, E.CudaError)(f"{name}: {msg}")
+    return rc
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(device=None) -> int:
+    import torch
+
+    return torch.cuda.current_stream(device).cuda_stream

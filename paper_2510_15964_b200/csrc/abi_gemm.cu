@@ -1,0 +1,218 @@
+// C-ABI: generic tcgen05 GEMM and the neuron-sparse MLP GEMMs (K2).
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm_sm100.cuh"
+
+namespace lx {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+                      uint32_t box_inner, uint32_t box_outer) {
+  auto enc = get_encode();
+  LX_REQUIRE(enc != nullptr, LX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  LX_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, LX_ERR_SHAPE, "TMA base pointer must be 16B aligned");
+  LX_REQUIRE((row_stride_elems * 2) % 16 == 0, LX_ERR_SHAPE, "row stride must be a multiple of 8 bf16 elements");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  LX_REQUIRE(r == CUDA_SUCCESS, LX_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu box=%u,%u", (int)r,
+             (unsigned long long)inner, (unsigned long long)outer, box_inner, box_outer);
+  return LX_OK;
+}
+
+template <int BMODE, int EPI, int BN>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
+  auto kern = gemm_sm100_kernel<BMODE, EPI, BN>;
+  constexpr int smem = GemmSmem<BN>::kTotal;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+  LX_CHECK_CUDA(attr_err);
+  LX_REQUIRE(args.n_items >= 1 && args.n_items <= kMaxItems, LX_ERR_UNSUPPORTED, "n_items must be in [1, %d]", kMaxItems);
+  LX_REQUIRE(args.lora_r >= 0 && args.lora_r <= kMaxR, LX_ERR_UNSUPPORTED, "LoRA rank must be <= %d", kMaxR);
+  kern<<<num_sms(), 192, smem, st>>>(ta, tb, args);
+  return launch_check("gemm_sm100");
+}
+
+static GemmArgs base_args(int n_items, int rows, int n_dense, int k_dense) {
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.n_items = n_items;
+  a.rows_per_item = rows;
+  a.n_dense = n_dense;
+  a.k_dense = k_dense;
+  a.blk = 16;
+  a.lora_scale = 1.f;
+  return a;
+}
+
+static int check_blk(int blk) {
+  LX_REQUIRE(blk == 16 || blk == 32 || blk == 64, LX_ERR_UNSUPPORTED,
+             "neuron block size %d unsupported on the sm_100a path (16, 32 or 64)", blk);
+  return LX_OK;
+}
+
+}  // namespace lx
+
+using namespace lx;
+
+extern "C" {
+
+const char* lx_last_error(void) { return g_err; }
+int lx_abi_version(void) { return 1; }
+int lx_device_sm_count(void) { return num_sms(); }
+
+int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void* c, int ldc, int c_is_f32, int M, int N,
+                    int K, lx_stream_t stream) {
+  LX_REQUIRE(M > 0 && N > 0 && K > 0, LX_ERR_SHAPE, "gemm: empty shape");
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_tmap_bf16_2d(&ta, a, K, M, lda, kBK, kBM))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, b, K, N, ldb, kBK, 256))) return rc;
+  GemmArgs args = base_args(1, M, N, K);
+  args.out = c;
+  args.ldo = ldc;
+  return c_is_f32 ? launch_gemm<kDense, kEpiStoreF32, 256>(ta, tb, args, stream)
+                  : launch_gemm<kDense, kEpiStoreBF16, 256>(ta, tb, args, stream);
+}
+
+int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w1_t,
+                  const int32_t* counts, const int32_t* ids, const float* b1, const float* ax1, const float* b1_lora,
+                  int r, float scaling, uint16_t* a_out, int ld_h, lx_stream_t stream) {
+  int rc;
+  if ((rc = check_blk(blk))) return rc;
+  LX_REQUIRE(d_ff % blk == 0, LX_ERR_MASK, "d_ff %d not a multiple of blk %d on the device path", d_ff, blk);
+  CUtensorMap ta, tb;
+  if ((rc = make_tmap_bf16_2d(&ta, x, d, (uint64_t)n_items * s, d, kBK, kBM))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, w1_t, d, d_ff, d, kBK, blk))) return rc;
+  GemmArgs args = base_args(n_items, s, 0, d);
+  args.counts = counts;
+  args.ids = ids;
+  args.ids_stride = d_ff / blk;
+  args.blk = blk;
+  args.out = a_out;
+  args.ldo = ld_h;
+  args.bias = b1;
+  args.lora_x = ax1;
+  args.lora_w = b1_lora;
+  args.w_sr = d_ff;
+  args.w_sc = 1;
+  args.lora_r = (ax1 && b1_lora) ? r : 0;
+  args.lora_scale = scaling;
+  return launch_gemm<kNGather, kEpiFc1, 256>(ta, tb, args, stream);
+}
+
+int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
+                  const int32_t* counts, const int32_t* ids, const float* b2, const float* ax2, const float* b2_lora,
+                  int r, float scaling, uint16_t* out, lx_stream_t stream) {
+  int rc;
+  if ((rc = check_blk(blk))) return rc;
+  LX_REQUIRE(d_ff % blk == 0, LX_ERR_MASK, "d_ff %d not a multiple of blk %d on the device path", d_ff, blk);
+  CUtensorMap ta, tb;
+  if ((rc = make_tmap_bf16_2d(&ta, a, d_ff, (uint64_t)n_items * s, ld_h, kBK, kBM))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, w2, d, d_ff, d, 64, blk))) return rc;
+  GemmArgs args = base_args(n_items, s, d, 0);
+  args.counts = counts;
+  args.ids = ids;
+  args.ids_stride = d_ff / blk;
+  args.blk = blk;
+  args.out = out;
+  args.ldo = d;
+  args.bias = b2;
+  args.lora_x = ax2;
+  args.lora_w = b2_lora;
+  args.w_sr = d;
+  args.w_sc = 1;
+  args.lora_r = (ax2 && b2_lora) ? r : 0;
+  args.lora_scale = scaling;
+  return launch_gemm<kKGather, kEpiFc2, 256>(ta, tb, args, stream);
+}
+
+int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
+                        const int32_t* counts, const int32_t* ids, const float* dax2, const float* a2_lora, int r,
+                        const uint16_t* a, uint16_t* dz, int ld_h, lx_stream_t stream) {
+  int rc;
+  if ((rc = check_blk(blk))) return rc;
+  CUtensorMap ta, tb;
+  if ((rc = make_tmap_bf16_2d(&ta, d_out, d, (uint64_t)n_items * s, d, kBK, kBM))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, w2, d, d_ff, d, kBK, blk))) return rc;
+  GemmArgs args = base_args(n_items, s, 0, d);
+  args.counts = counts;
+  args.ids = ids;
+  args.ids_stride = d_ff / blk;
+  args.blk = blk;
+  args.out = dz;
+  args.ldo = ld_h;
+  args.lora_x = dax2;
+  args.lora_w = a2_lora;
+  args.w_sr = 1;
+  args.w_sc = r;
+  args.lora_r = (dax2 && a2_lora) ? r : 0;
+  args.act = reinterpret_cast<const __nv_bfloat16*>(a);
+  args.ld_act = ld_h;
+  return launch_gemm<kNGather, kEpiDa, 256>(ta, tb, args, stream);
+}
+
+int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d, int d_ff, int blk,
+                        const uint16_t* w1_t, const int32_t* counts, const int32_t* ids, const float* dax1,
+                        const float* a1_lora, int r, uint16_t* dx, lx_stream_t stream) {
+  int rc;
+  if ((rc = check_blk(blk))) return rc;
+  CUtensorMap ta, tb;
+  if ((rc = make_tmap_bf16_2d(&ta, dz, d_ff, (uint64_t)n_items * s, ld_h, kBK, kBM))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, w1_t, d, d_ff, d, 64, blk))) return rc;
+  GemmArgs args = base_args(n_items, s, d, 0);
+  args.counts = counts;
+  args.ids = ids;
+  args.ids_stride = d_ff / blk;
+  args.blk = blk;
+  args.out = dx;
+  args.ldo = d;
+  args.lora_x = dax1;
+  args.lora_w = a1_lora;
+  args.w_sr = 1;
+  args.w_sc = r;
+  args.lora_r = (dax1 && a1_lora) ? r : 0;
+  return launch_gemm<kKGather, kEpiDx, 256>(ta, tb, args, stream);
+}
+
+}  // extern "C"

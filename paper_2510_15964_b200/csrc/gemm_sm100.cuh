@@ -1,0 +1,391 @@
+// Persistent grouped gather-GEMM on sm_100a: TMA -> smem (SWIZZLE_128B) ->
+// tcgen05.mma (fp32 accumulators in TMEM, double-buffered) -> fused epilogue.
+//
+//   C[rows of item b, :] = A[rows of item b, :K_b] * B_b^T
+//
+// B operand modes (the neuron-sparse MLP of sf/neuron_ops.py:75-95):
+//   kDense   : B is K-major [N, K] (row n contiguous along K).
+//   kNGather : B is K-major [d_ff, K]; the item's packed N columns are its
+//              active neuron blocks (ids[b][*]), each a contiguous run of `blk`
+//              rows of W1^T (fc1) or W2 (fc2 input-grad). One TMA box per block.
+//   kKGather : B is MN-major [d_ff, N]; the item's packed K rows are its active
+//              neuron blocks, each `blk` contiguous rows of W2 (fc2) or W1^T
+//              (fc1 input-grad). A is the packed hidden [M, ld] (K = count*blk).
+//
+// Warp roles: w0 = TMA producer, w1 = MMA issuer (lane 0), w2..w5 = epilogue
+// (one accumulator row per thread). Grid = #SMs; tiles strided over CTAs, with
+// the M tile fastest so co-resident CTAs share the same weight (B) tile in L2.
+#pragma once
+#include "ptx.cuh"
+
+namespace lx {
+
+enum BMode : int { kDense = 0, kNGather = 1, kKGather = 2 };
+enum EpiKind : int {
+  kEpiStoreF32 = 0,   // C (fp32)
+  kEpiStoreBF16 = 1,  // C (bf16)
+  kEpiFc1 = 2,        // relu(acc + b1[c] + s*ax1[row]·B1[:,c])  -> bf16 packed hidden
+  kEpiFc2 = 3,        // acc + b2[c] + s*ax2[row]·B2[:,c]        -> bf16
+  kEpiDa = 4,         // (acc + dax2[row]·A2[c,:]) * (a[row,j] > 0) -> bf16 packed dz
+  kEpiDx = 5,         // acc + dax1[row]·A1[c,:]                  -> bf16
+  kEpiMask = 6,       // OR_rows(acc > thr) per column -> bitmask words (+ optional fp32 dump)
+};
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
+constexpr int kMaxR = 16;
+constexpr int kMaxItems = 512;
+
+struct GemmArgs {
+  // problem
+  int n_items;        // groups (sequences)
+  int rows_per_item;  // tokens per item
+  int n_dense;        // N for kDense / kKGather
+  int k_dense;        // K for kDense / kNGather
+  const int* counts;  // [n_items] active blocks per item (gather modes)
+  const int* ids;     // [n_items, ids_stride] ascending active block ids
+  int ids_stride;
+  int blk;            // neuron block size (multiple of 16)
+  // epilogue
+  void* out;
+  int ldo;
+  const float* bias;      // indexed by original column
+  const float* lora_x;    // [M, r] fp32 (row factor)
+  const float* lora_w;    // column factor: w(r, c) = lora_w[r*w_sr + c*w_sc]
+  long long w_sr, w_sc;
+  int lora_r;
+  float lora_scale;
+  const __nv_bfloat16* act;  // kEpiDa: packed relu output a (same layout as out)
+  int ld_act;
+  float thr;            // kEpiMask
+  uint32_t* bits;       // kEpiMask: [n_items, bits_stride] words
+  int bits_stride;
+};
+
+template <int BN>
+struct GemmSmem {
+  static constexpr int kStages = BN >= 256 ? 4 : 6;
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOff = kStages * kStageBytes;
+  static constexpr int kMiscOff = kBarOff + (2 * kStages + 4) * 8;
+  static constexpr int kEpiOff = (kMiscOff + 16 + 4 * (kMaxItems + 1) + 127) / 128 * 128;
+  static constexpr int kEpiBytes = BN * 4 + BN * kMaxR * 4;
+  static constexpr int kTotal = kEpiOff + kEpiBytes + 1024;  // + alignment slack
+};
+
+struct TileInfo {
+  int item, mt, nt;
+  int n_cols;    // valid packed/dense columns in this tile
+  int k_stages;  // K pipeline stages
+  int k_total;   // K extent (elements)
+};
+
+template <int BMODE, int BN>
+LX_DEV int item_n_tiles(const GemmArgs& a, int cnt) {
+  if (BMODE == kNGather) return (cnt * a.blk + BN - 1) / BN;
+  return (a.n_dense + BN - 1) / BN;
+}
+
+template <int BMODE, int BN>
+LX_DEV TileInfo decode_tile(const GemmArgs& a, const int* prefix, const int* cnts, int m_tiles, int t) {
+  int lo = 0, hi = a.n_items;  // largest item with prefix[item] <= t
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (prefix[mid] <= t) lo = mid; else hi = mid;
+  }
+  TileInfo ti;
+  ti.item = lo;
+  int local = t - prefix[lo];
+  ti.mt = local % m_tiles;
+  ti.nt = local / m_tiles;
+  int cnt = BMODE == kDense ? 0 : __ldg(cnts + lo);
+  int n_total = BMODE == kNGather ? cnt * a.blk : a.n_dense;
+  ti.n_cols = min(BN, n_total - ti.nt * BN);
+  ti.k_total = BMODE == kKGather ? cnt * a.blk : a.k_dense;
+  ti.k_stages = (ti.k_total + kBK - 1) / kBK;
+  return ti;
+}
+
+template <int BMODE, int EPI, int BN>
+__global__ void __launch_bounds__(192, 1)
+gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, GemmArgs args) {
+  using L = GemmSmem<BN>;
+  constexpr int S = L::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kMiscOff);
+  int* prefix = reinterpret_cast<int*>(smem + L::kMiscOff + 16);
+  float* s_bias = reinterpret_cast<float*>(smem + L::kEpiOff);
+  float* s_w = s_bias + BN;
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int m_tiles = (args.rows_per_item + kBM - 1) / kBM;
+
+  // ---- tile table: prefix[b] = first tile index of item b (counts are device-resident)
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < args.n_items; ++b) {
+      prefix[b] = acc;
+      int cnt = (BMODE == kDense) ? 0 : __ldg(args.counts + b);
+      acc += m_tiles * item_n_tiles<BMODE, BN>(args, cnt);
+    }
+    prefix[args.n_items] = acc;
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int i = 0; i < S; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, 4); }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int n_tiles_total = prefix[args.n_items];
+
+  // counts are needed by every role to decode tiles; read through L1 per decode.
+  const int* cnts = args.counts;
+
+  if (warp == 0) {
+    // ================= TMA producer
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+        TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t);
+        const int row0 = ti.item * args.rows_per_item + ti.mt * kBM;
+        const int* ids = args.ids + (size_t)ti.item * args.ids_stride;
+        for (int ks = 0; ks < ti.k_stages; ++ks) {
+          mbar_wait(empty + stage, phase ^ 1);
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          uint32_t bytes = L::kABytes;
+          if (BMODE == kDense) {
+            bytes += BN * kBK * 2;
+          } else if (BMODE == kNGather) {
+            int nb = (ti.n_cols + args.blk - 1) / args.blk;
+            bytes += nb * args.blk * kBK * 2;
+          } else {
+            int kb0 = ks * kBK / args.blk;
+            int nb = min(kBK / args.blk, ti.k_total / args.blk - kb0);
+            bytes += nb * (BN / 64) * args.blk * 128;
+          }
+          mbar_arrive_expect_tx(full + stage, bytes);
+          tma_load_2d(sa, &tmap_a, full + stage, ks * kBK, row0);
+          if (BMODE == kDense) {
+            tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.nt * BN, pol_w);
+          } else if (BMODE == kNGather) {
+            int nb = (ti.n_cols + args.blk - 1) / args.blk;
+            int blk0 = ti.nt * BN / args.blk;
+            for (int j = 0; j < nb; ++j) {
+              int id = __ldg(ids + blk0 + j);
+              tma_load_2d_hint(sb + j * args.blk * 128, &tmap_b, full + stage, ks * kBK, id * args.blk, pol_w);
+            }
+          } else {
+            int kb0 = ks * kBK / args.blk;
+            int nb = min(kBK / args.blk, ti.k_total / args.blk - kb0);
+            for (int j = 0; j < nb; ++j) {
+              int id = __ldg(ids + kb0 + j);
+              for (int a = 0; a < BN / 64; ++a)
+                tma_load_2d_hint(sb + a * (kBK * 128) + j * args.blk * 128, &tmap_b, full + stage, ti.nt * BN + a * 64,
+                                 id * args.blk, pol_w);
+            }
+          }
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+        TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t);
+        const int buf = it & 1;
+        const uint32_t use_phase = (it >> 1) & 1;
+        mbar_wait(tempty + buf, use_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        int n_mma = BMODE == kNGather ? ((ti.n_cols + 15) / 16) * 16 : BN;
+        const uint32_t idesc = make_idesc_bf16(kBM, n_mma, false, BMODE == kKGather);
+        for (int ks = 0; ks < ti.k_stages; ++ks) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t sb = sa + L::kABytes;
+          int kk_n = min(kBK, ti.k_total - ks * kBK);
+          kk_n = (kk_n + 15) / 16;
+          for (int kk = 0; kk < kk_n; ++kk) {
+            uint64_t da = make_sdesc(sa + kk * 32, 16, 1024);
+            uint64_t db = BMODE == kKGather ? make_sdesc(sb + kk * 2048, kBK * 128, 1024) : make_sdesc(sb + kk * 32, 16, 1024);
+            mma_bf16_ss(d_tmem, da, db, idesc, (ks | kk) != 0);
+          }
+          mma_commit(empty + stage);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        if (ti.k_stages > 0) mma_commit(tfull + buf);
+        else mbar_arrive(tfull + buf);
+      }
+    }
+  } else {
+    // ================= epilogue (warps 2..5): thread <-> accumulator row
+    const int quad = warp & 3;
+    const int r_in_tile = quad * 32 + lane;
+    const int ep_tid = threadIdx.x - 64;
+    int it = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+      TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t);
+      const int buf = it & 1;
+      const int* ids = args.ids + (size_t)ti.item * args.ids_stride;
+      const int local_row = ti.mt * kBM + r_in_tile;
+      const bool row_ok = local_row < args.rows_per_item;
+      const size_t grow = (size_t)ti.item * args.rows_per_item + local_row;
+      const int r = args.lora_r;
+      constexpr bool kLora = EPI == kEpiFc1 || EPI == kEpiFc2 || EPI == kEpiDa || EPI == kEpiDx;
+
+      // stage per-column bias / LoRA column factors for this tile
+      if (kLora) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int c = ep_tid; c < BN; c += 128) {
+          int j = ti.nt * BN + c;
+          int oc = j;
+          if (BMODE == kNGather) oc = (c < ti.n_cols) ? __ldg(ids + j / args.blk) * args.blk + j % args.blk : 0;
+          bool ok = c < ti.n_cols;
+          s_bias[c] = (ok && args.bias) ? __ldg(args.bias + oc) : 0.f;
+          for (int q = 0; q < kMaxR; ++q)
+            s_w[c * kMaxR + q] =
+                (ok && q < r && args.lora_w) ? __ldg(args.lora_w + q * args.w_sr + (long long)oc * args.w_sc) : 0.f;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      float xr[kMaxR];
+#pragma unroll
+      for (int q = 0; q < kMaxR; ++q) xr[q] = 0.f;
+      if (kLora && args.lora_x && row_ok) {
+#pragma unroll
+        for (int q = 0; q < kMaxR; ++q)
+          if (q < r) xr[q] = __ldg(args.lora_x + grow * r + q) * args.lora_scale;
+      }
+
+      mbar_wait(tfull + buf, (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;
+      const int n_chunks = (ti.n_cols + 31) / 32;
+      for (int ch = 0; ch < n_chunks; ++ch) {
+        uint32_t raw[32];
+        if (ti.k_stages > 0) {
+          tmem_ld_32x32b_x32(t_row + ch * 32, raw);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) raw[i] = 0u;
+        }
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
+        const int c0 = ch * 32;
+        const int nv = min(32, ti.n_cols - c0);
+        const int j0 = ti.nt * BN + c0;  // packed / dense column of v[0]
+
+        if (EPI == kEpiMask) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            bool act = row_ok && i < nv && v[i] > args.thr;
+            uint32_t bal = __ballot_sync(0xffffffffu, act);
+            if (bal) word |= 1u << i;
+          }
+          if (lane == 0 && word) atomicOr(args.bits + (size_t)ti.item * args.bits_stride + j0 / 32, word);
+          if (args.out && row_ok) {
+            float* o = reinterpret_cast<float*>(args.out) + grow * args.ldo + j0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < nv) o[i] = v[i];
+          }
+          continue;
+        }
+        if (kLora) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float* w = s_w + (c0 + i) * kMaxR;
+            float acc = v[i] + s_bias[c0 + i];
+#pragma unroll
+            for (int q = 0; q < kMaxR; q += 4) {
+              if (q < r) {
+                float4 wq = *reinterpret_cast<const float4*>(w + q);
+                acc = fmaf(xr[q], wq.x, acc);
+                acc = fmaf(xr[q + 1], wq.y, acc);
+                acc = fmaf(xr[q + 2], wq.z, acc);
+                acc = fmaf(xr[q + 3], wq.w, acc);
+              }
+            }
+            v[i] = acc;
+          }
+        }
+        if (EPI == kEpiFc1) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        if (EPI == kEpiDa) {
+          if (row_ok) {
+            const __nv_bfloat16* ap = args.act + grow * args.ld_act + j0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              float av = (i < nv) ? __bfloat162float(ap[i]) : 0.f;
+              v[i] = av > 0.f ? v[i] : 0.f;
+            }
+          }
+        }
+        if (!row_ok) continue;
+        if (EPI == kEpiStoreF32) {
+          float* o = reinterpret_cast<float*>(args.out) + grow * args.ldo + j0;
+          if (nv == 32 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < nv) o[i] = v[i];
+          }
+        } else {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + grow * args.ldo + j0;
+          if (nv == 32 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+            uint32_t p[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) p[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              *reinterpret_cast<uint4*>(o + 8 * i) = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < nv) o[i] = __float2bfloat16_rn(v[i]);
+          }
+        }
+      }
+      // release the accumulator buffer to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + buf);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+}  // namespace lx

@@ -1,0 +1,158 @@
+// LayerNorm forward/backward (sf/model.py:307-312, sf/autograd.py:61-66).
+// Forward reads the fp32 residual row once into registers, writes bf16 for the
+// GEMMs, and — fused — the predictor's sqrt(s)-downsampled rows
+// (sf/predictor.py:62-71), so the attention predictor never re-reads h1.
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace lx {
+
+constexpr int kLnThreads = 256;
+constexpr int kLnMaxVec = 8;  // float4 per thread -> d <= 256*4*8 = 8192
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+  return t;
+}
+
+__global__ void __launch_bounds__(kLnThreads) ln_fwd_kernel(const float* __restrict__ x, int d, const float* __restrict__ g,
+                                                             const float* __restrict__ b, float eps,
+                                                             __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+                                                             float* __restrict__ istd_out, int s, int m_small,
+                                                             __nv_bfloat16* __restrict__ x_small) {
+  __shared__ float red[32];
+  const size_t row = blockIdx.x;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * d);
+  const int nv = d / 4;
+  float4 v[kLnMaxVec];
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < kLnMaxVec; ++i) {
+    int c = threadIdx.x + i * kLnThreads;
+    v[i] = c < nv ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    sum += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+  const float mu = block_sum(sum, red) / d;
+  float sq = 0.f;
+#pragma unroll
+  for (int i = 0; i < kLnMaxVec; ++i) {
+    int c = threadIdx.x + i * kLnThreads;
+    if (c < nv) {
+      float a = v[i].x - mu, bb = v[i].y - mu, cc = v[i].z - mu, dd = v[i].w - mu;
+      sq += (a * a + bb * bb) + (cc * cc + dd * dd);
+    }
+  }
+  const float var = block_sum(sq, red) / d;
+  const float istd = 1.0f / sqrtf(var + eps);
+  if (threadIdx.x == 0) {
+    mean_out[row] = mu;
+    istd_out[row] = istd;
+  }
+  // fused downsample: token t of its sequence is sampled iff t == (i*s)//m for some i
+  __nv_bfloat16* xs_row = nullptr;
+  if (x_small) {
+    int t = row % s, item = row / s;
+    int i = (int)(((long long)t * m_small + s - 1) / s);
+    if (i < m_small && (int)(((long long)i * s) / m_small) == t) xs_row = x_small + ((size_t)item * m_small + i) * d;
+  }
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+#pragma unroll
+  for (int i = 0; i < kLnMaxVec; ++i) {
+    int c = threadIdx.x + i * kLnThreads;
+    if (c < nv) {
+      float4 gg = g4[c], bb = b4[c];
+      float o0 = (v[i].x - mu) * istd * gg.x + bb.x;
+      float o1 = (v[i].y - mu) * istd * gg.y + bb.y;
+      float o2 = (v[i].z - mu) * istd * gg.z + bb.z;
+      float o3 = (v[i].w - mu) * istd * gg.w + bb.w;
+      uint2 pk = make_uint2(pack_bf16x2(o0, o1), pack_bf16x2(o2, o3));
+      *reinterpret_cast<uint2*>(y + row * d + 4 * c) = pk;
+      if (xs_row) *reinterpret_cast<uint2*>(xs_row + 4 * c) = pk;
+    }
+  }
+}
+
+template <bool kF32>
+__global__ void __launch_bounds__(kLnThreads) ln_bwd_kernel(const void* __restrict__ dy_, const float* __restrict__ x,
+                                                             const float* __restrict__ g, const float* __restrict__ mean,
+                                                             const float* __restrict__ istd, int d,
+                                                             float* __restrict__ dx) {
+  __shared__ float red[32];
+  const size_t row = blockIdx.x;
+  const float mu = mean[row], is = istd[row];
+  const int nv = d / 4;
+  float4 gv[kLnMaxVec], xh[kLnMaxVec];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < kLnMaxVec; ++i) {
+    int c = threadIdx.x + i * kLnThreads;
+    gv[i] = xh[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < nv) {
+      float4 dy;
+      if (kF32) {
+        dy = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(dy_) + row * d)[c];
+      } else {
+        uint2 p = reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(dy_) + row * d)[c];
+        dy.x = bf16_bits_to_float(p.x & 0xffff);
+        dy.y = bf16_bits_to_float(p.x >> 16);
+        dy.z = bf16_bits_to_float(p.y & 0xffff);
+        dy.w = bf16_bits_to_float(p.y >> 16);
+      }
+      float4 xx = reinterpret_cast<const float4*>(x + row * d)[c];
+      float4 gg = reinterpret_cast<const float4*>(g)[c];
+      gv[i] = make_float4(dy.x * gg.x, dy.y * gg.y, dy.z * gg.z, dy.w * gg.w);
+      xh[i] = make_float4((xx.x - mu) * is, (xx.y - mu) * is, (xx.z - mu) * is, (xx.w - mu) * is);
+      s1 += (gv[i].x + gv[i].y) + (gv[i].z + gv[i].w);
+      s2 += (gv[i].x * xh[i].x + gv[i].y * xh[i].y) + (gv[i].z * xh[i].z + gv[i].w * xh[i].w);
+    }
+  }
+  const float mg = block_sum(s1, red) / d;
+  const float mgx = block_sum(s2, red) / d;
+#pragma unroll
+  for (int i = 0; i < kLnMaxVec; ++i) {
+    int c = threadIdx.x + i * kLnThreads;
+    if (c < nv) {
+      float4* o = reinterpret_cast<float4*>(dx + row * d) + c;
+      float4 cur = *o;
+      cur.x += is * (gv[i].x - mg - xh[i].x * mgx);
+      cur.y += is * (gv[i].y - mg - xh[i].y * mgx);
+      cur.z += is * (gv[i].z - mg - xh[i].z * mgx);
+      cur.w += is * (gv[i].w - mg - xh[i].w * mgx);
+      *o = cur;
+    }
+  }
+}
+
+}  // namespace lx
+
+using namespace lx;
+
+extern "C" {
+
+int lx_layernorm_fwd(const float* x, int M, int d, const float* gamma, const float* beta, float eps, uint16_t* y,
+                     float* mean, float* inv_std, int s, int m_small, uint16_t* x_small, lx_stream_t stream) {
+  LX_REQUIRE(d % 4 == 0 && d <= kLnThreads * 4 * kLnMaxVec, LX_ERR_UNSUPPORTED, "layernorm: d=%d unsupported", d);
+  LX_REQUIRE(M >= 1, LX_ERR_SHAPE, "layernorm: empty input");
+  if (x_small) LX_REQUIRE(s >= 1 && m_small >= 1 && M % s == 0, LX_ERR_SHAPE, "layernorm: bad downsample shape");
+  ln_fwd_kernel<<<M, kLnThreads, 0, stream>>>(x, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), mean, inv_std,
+                                              s > 0 ? s : 1, m_small, reinterpret_cast<__nv_bfloat16*>(x_small));
+  return launch_check("layernorm_fwd");
+}
+
+int lx_layernorm_bwd(const void* dy, int dy_is_f32, const float* x, const float* gamma, const float* mean,
+                     const float* inv_std, int M, int d, float* dx_accum, lx_stream_t stream) {
+  LX_REQUIRE(d % 4 == 0 && d <= kLnThreads * 4 * kLnMaxVec, LX_ERR_UNSUPPORTED, "layernorm: d=%d unsupported", d);
+  if (dy_is_f32)
+    ln_bwd_kernel<true><<<M, kLnThreads, 0, stream>>>(dy, x, gamma, mean, inv_std, d, dx_accum);
+  else
+    ln_bwd_kernel<false><<<M, kLnThreads, 0, stream>>>(dy, x, gamma, mean, inv_std, d, dx_accum);
+  return launch_check("layernorm_bwd");
+}
+
+}  // extern "C"

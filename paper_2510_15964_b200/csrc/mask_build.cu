@@ -1,0 +1,237 @@
+// K1 — predictor scoring + prolonged-range aggregation -> compacted index lists.
+//
+// MLP (sf/predictor.py:121-139, sf/neuron_ops.py:67-72):
+//   S = h * Wa_hat on tcgen05 (gemm_sm100, kEpiMask epilogue): each tile ORs
+//   (S > thr) over its rows with warp ballots and publishes one 32-bit word per
+//   (item, 32 blocks) with atomicOr (idempotent => deterministic). A compaction
+//   kernel turns the bitmask into ascending active-block ids, counts and the
+//   inverse map pos[item][blk] (packed position or -1).
+// Attention (sf/predictor.py:62-118, sf/exposer.py:71-85):
+//   [Q_hat | K_hat] = X_small * [Wq_hat | Wk_hat] for every head at once (one
+//   tcgen05 GEMM), then one CTA per (item, head): S_hat = Q_hat K_hat^T (fp32),
+//   per-matrix max, fp32 threshold frac*peak (NEP-50 rounding), strict '>',
+//   OR over items (batch scope), nearest-cell upsample, integer coverage counts
+//   per pool pattern and the fp64 (mass/total >= tau - 1e-9) selection with the
+//   fewest-blocks / pool-order tie-break.
+#include "common.cuh"
+#include "gemm_sm100.cuh"
+
+namespace lx {
+
+__global__ void mask_compact_kernel(const uint32_t* __restrict__ bits, int n_items, int n_blk, int scope_batch,
+                                    int32_t* __restrict__ counts, int32_t* __restrict__ ids, int32_t* __restrict__ pos) {
+  const int item = blockIdx.x;
+  const int words = (n_blk + 31) / 32;
+  __shared__ int s_scan[1024];
+  __shared__ int s_total;
+  // each thread owns a contiguous range of words
+  const int per = (words + blockDim.x - 1) / blockDim.x;
+  const int w0 = threadIdx.x * per;
+  int local = 0;
+  for (int w = w0; w < min(words, w0 + per); ++w) {
+    uint32_t v = 0;
+    if (scope_batch) {
+      for (int b = 0; b < n_items; ++b) v |= bits[(size_t)b * words + w];
+    } else {
+      v = bits[(size_t)item * words + w];
+    }
+    if (w == words - 1 && (n_blk & 31)) v &= (1u << (n_blk & 31)) - 1u;
+    local += __popc(v);
+  }
+  s_scan[threadIdx.x] = local;
+  __syncthreads();
+  // inclusive Hillis-Steele scan over blockDim.x entries
+  for (int off = 1; off < blockDim.x; off <<= 1) {
+    int v = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0;
+    __syncthreads();
+    s_scan[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int base = s_scan[threadIdx.x] - local;
+  if (threadIdx.x == blockDim.x - 1) s_total = s_scan[threadIdx.x];
+  int32_t* my_ids = ids + (size_t)item * n_blk;
+  int32_t* my_pos = pos ? pos + (size_t)item * n_blk : nullptr;
+  for (int w = w0; w < min(words, w0 + per); ++w) {
+    uint32_t v = 0;
+    if (scope_batch) {
+      for (int b = 0; b < n_items; ++b) v |= bits[(size_t)b * words + w];
+    } else {
+      v = bits[(size_t)item * words + w];
+    }
+    for (int i = 0; i < 32 && w * 32 + i < n_blk; ++i) {
+      int blk = w * 32 + i;
+      if ((v >> i) & 1u) {
+        my_ids[base] = blk;
+        if (my_pos) my_pos[blk] = base;
+        ++base;
+      } else if (my_pos) {
+        my_pos[blk] = -1;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) counts[item] = s_total;
+  // tail of ids beyond the count is left untouched (never read)
+}
+
+// membership of block (i, j) in pool pattern (kind, p) — sf/patterns.py:63-85
+__device__ __forceinline__ bool pool_member(int kind, int p, int i, int j) {
+  int dd = i - j;
+  switch (kind) {
+    case 0: return dd == 0;                                  // blockdiag
+    case 1: return dd <= p && dd >= -p;                      // band{p}
+    case 2: return dd >= 0 && dd <= p;                       // causal{p}
+    case 3: return i < p || j < p || dd == 0;                // global{p}
+    case 4: return ((dd % p) + p) % p == 0;                  // strided{p}
+    default: return true;                                    // dense
+  }
+}
+
+constexpr int kMaxPool = 16;
+constexpr int kMaxM = 64;
+
+__global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items, int m, int H, int r, float frac,
+                                    double tau, int n_b, const int32_t* __restrict__ pool_kind,
+                                    const int32_t* __restrict__ pool_param, int n_pool, int scope_batch,
+                                    int32_t* __restrict__ pattern_idx, float* __restrict__ dump) {
+  const int h = blockIdx.x;
+  const int item0 = scope_batch ? 0 : blockIdx.y;
+  const int item1 = scope_batch ? n_items : blockIdx.y + 1;
+  const int ldp = 2 * H * r;
+  __shared__ float s_hat[kMaxM * kMaxM];
+  __shared__ unsigned char cell[kMaxM * kMaxM];
+  __shared__ float s_red[32];
+  __shared__ unsigned long long s_cnt[kMaxPool + 1][2];  // [pattern][0]=mass, [1]=active blocks
+  const int mm = m * m;
+  for (int e = threadIdx.x; e < mm; e += blockDim.x) cell[e] = 0;
+  for (int item = item0; item < item1; ++item) {
+    // S_hat = (X Wq)(X Wk)^T  (sf/predictor.py:74-76)
+    for (int e = threadIdx.x; e < mm; e += blockDim.x) {
+      int i = e / m, j = e % m;
+      const float* qr = proj + (size_t)(item * m + i) * ldp + h * r;
+      const float* kr = proj + (size_t)(item * m + j) * ldp + (H + h) * r;
+      float acc = 0.f;
+      for (int t = 0; t < r; ++t) acc = fmaf(qr[t], kr[t], acc);
+      s_hat[e] = acc;
+      if (dump) dump[((size_t)item * H + h) * mm + e] = acc;
+    }
+    __syncthreads();
+    // per-matrix max (sf/predictor.py:89)
+    float mx = -INFINITY;
+    for (int e = threadIdx.x; e < mm; e += blockDim.x) mx = fmaxf(mx, s_hat[e]);
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float v = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : -INFINITY;
+      for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (threadIdx.x == 0) s_red[0] = v;
+    }
+    __syncthreads();
+    // threshold = fp32(frac) * peak rounded to fp32; strict '>' (sf/predictor.py:90, NEP 50)
+    const float thr = __fmul_rn(frac, s_red[0]);
+    for (int e = threadIdx.x; e < mm; e += blockDim.x) cell[e] |= (s_hat[e] > thr) ? 1 : 0;  // OR over batch
+    __syncthreads();
+  }
+  // upsample (sf/predictor.py:79-84) + integer coverage counts per pattern (sf/exposer.py:71-85)
+  if (threadIdx.x < (kMaxPool + 1) * 2) (&s_cnt[0][0])[threadIdx.x] = 0ull;
+  __syncthreads();
+  unsigned long long mass[kMaxPool], nnz[kMaxPool], total = 0;
+  for (int p = 0; p < kMaxPool; ++p) mass[p] = nnz[p] = 0;
+  const int cells = n_b * n_b;
+  for (int e = threadIdx.x; e < cells; e += blockDim.x) {
+    int i = e / n_b, j = e % n_b;
+    int si = min((int)(((long long)i * m) / n_b), m - 1);
+    int sj = min((int)(((long long)j * m) / n_b), m - 1);
+    bool on = cell[si * m + sj] != 0;
+    total += on;
+    for (int p = 0; p < n_pool; ++p) {
+      bool in = pool_member(pool_kind[p], pool_param[p], i, j);
+      nnz[p] += in;
+      mass[p] += (in && on);
+    }
+  }
+  atomicAdd(&s_cnt[kMaxPool][0], total);
+  for (int p = 0; p < n_pool; ++p) {
+    if (mass[p]) atomicAdd(&s_cnt[p][0], mass[p]);
+    if (nnz[p]) atomicAdd(&s_cnt[p][1], nnz[p]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long tot = s_cnt[kMaxPool][0];
+    int dense = n_pool - 1;  // dense is always last in the pool
+    int best = -1;
+    if (tot > 0) {
+      for (int p = 0; p < n_pool; ++p) {
+        double frac_cov = (double)s_cnt[p][0] / (double)tot;
+        if (frac_cov >= tau - 1e-9 && (best < 0 || s_cnt[p][1] < s_cnt[best][1])) best = p;
+      }
+    }
+    pattern_idx[(size_t)(scope_batch ? 0 : blockIdx.y) * H + h] = best < 0 ? dense : best;
+  }
+}
+
+}  // namespace lx
+
+using namespace lx;
+
+extern "C" {
+
+int lx_mask_compact(const uint32_t* bits, int n_items, int n_blk, int scope_batch, int32_t* counts, int32_t* ids,
+                    int32_t* pos, lx_stream_t stream) {
+  LX_REQUIRE(n_items >= 1 && n_blk >= 1, LX_ERR_SHAPE, "mask_compact: empty shape");
+  mask_compact_kernel<<<n_items, 256, 0, stream>>>(bits, n_items, n_blk, scope_batch, counts, ids, pos);
+  return launch_check("mask_compact");
+}
+
+int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint16_t* wa_t, int n_blk, float threshold,
+                        int scope_batch, uint32_t* bits_ws, int32_t* counts, int32_t* ids, int32_t* pos,
+                        float* scores_dump, lx_stream_t stream) {
+  LX_REQUIRE(n_items >= 1 && s >= 1 && d >= 1 && n_blk >= 1, LX_ERR_SHAPE, "predict_mlp_mask: empty shape");
+  LX_REQUIRE(n_items <= kMaxItems, LX_ERR_UNSUPPORTED, "too many items");
+  const int words = (n_blk + 31) / 32;
+  LX_CHECK_CUDA(cudaMemsetAsync(bits_ws, 0, sizeof(uint32_t) * n_items * words, stream));
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_tmap_bf16_2d(&ta, h, d, (uint64_t)n_items * s, d, kBK, kBM))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, wa_t, d, n_blk, d, kBK, 256))) return rc;
+  GemmArgs args;
+  memset(&args, 0, sizeof(args));
+  args.n_items = n_items;
+  args.rows_per_item = s;
+  args.n_dense = n_blk;
+  args.k_dense = d;
+  args.blk = 16;
+  args.out = scores_dump;
+  args.ldo = n_blk;
+  args.thr = threshold;
+  args.bits = bits_ws;
+  args.bits_stride = words;
+  args.lora_scale = 1.f;
+  {
+    auto kern = gemm_sm100_kernel<kDense, kEpiMask, 256>;
+    constexpr int smem = GemmSmem<256>::kTotal;
+    static cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    LX_CHECK_CUDA(attr);
+    kern<<<num_sms(), 192, smem, stream>>>(ta, tb, args);
+    if ((rc = launch_check("mlp mask gemm"))) return rc;
+  }
+  return lx_mask_compact(bits_ws, n_items, n_blk, scope_batch, counts, ids, pos, stream);
+}
+
+int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, int d, const uint16_t* wqk_t, int H,
+                                  int r, float threshold_frac, double tau, int n_b, const int32_t* pool_kind,
+                                  const int32_t* pool_param, int n_pool, int scope_batch, float* proj_ws,
+                                  int32_t* pattern_idx, float* scores_dump, lx_stream_t stream) {
+  LX_REQUIRE(m >= 1 && m <= kMaxM, LX_ERR_UNSUPPORTED, "downsampled length m=%d outside [1, %d] (s <= 4096)", m, kMaxM);
+  LX_REQUIRE(n_pool >= 1 && n_pool <= kMaxPool, LX_ERR_PATTERN, "pool size %d outside [1, %d]", n_pool, kMaxPool);
+  LX_REQUIRE(tau > 0 && tau <= 1, LX_ERR_SHAPE, "coverage tau must be in (0, 1]");
+  int rc = lx_gemm_bf16_tn(x_small, d, wqk_t, d, proj_ws, 2 * H * r, 1, n_items * m, 2 * H * r, d, stream);
+  if (rc) return rc;
+  dim3 grid(H, scope_batch ? 1 : n_items);
+  attn_pattern_kernel<<<grid, 256, 0, stream>>>(proj_ws, n_items, m, H, r, threshold_frac, tau, n_b, pool_kind,
+                                                  pool_param, n_pool, scope_batch, pattern_idx, scores_dump);
+  return launch_check("attn_pattern");
+}
+
+}  // extern "C"

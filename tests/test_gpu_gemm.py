@@ -1,0 +1,122 @@
+"""GPU parity of the tcgen05 GEMM engine and the neuron-sparse MLP GEMMs
+(K2, sf/neuron_ops.py:75-95, sf/model.py:363-400, sf/autograd.py:97-120)
+against a plain PyTorch fp32 reference of the same op. Tolerance: bf16 inputs,
+fp32 accumulation -> max|d| / max|ref| <= 1e-2 (bf16 outputs) / 2e-3 (fp32)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch.device("cuda")
+
+
+def rel(a, b):
+    a, b = a.float(), b.float()
+    return ((a - b).abs().max() / b.abs().max().clamp_min(1e-30)).item()
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 200), (1024, 1024, 1024), (4096, 512, 2048)])
+@pytest.mark.parametrize("f32", [True, False])
+def test_dense_gemm(M, N, K, f32):
+    from paper_2510_15964_b200 import _abi
+
+    dev = _dev()
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    a = torch.randn(M, K, generator=g).to(dev, torch.bfloat16)
+    b = torch.randn(N, K, generator=g).to(dev, torch.bfloat16)
+    c = torch.empty(M, N, device=dev, dtype=torch.float32 if f32 else torch.bfloat16)
+    _abi.call("lx_gemm_bf16_tn", a.data_ptr(), K, b.data_ptr(), K, c.data_ptr(), N, int(f32), M, N, K, _abi.stream_handle())
+    ref = a.float() @ b.float().T
+    torch.cuda.synchronize()
+    assert rel(c, ref) < (2e-3 if f32 else 1e-2)
+
+
+def _masks(n_items, n_blk, density, seed):
+    rng = np.random.default_rng(seed)
+    masks = rng.random((n_items, n_blk)) < density
+    if n_items > 1:
+        masks[-1] = False  # an empty item
+    counts = masks.sum(1).astype(np.int32)
+    ids = np.zeros((n_items, n_blk), np.int32)
+    for b in range(n_items):
+        ids[b, : counts[b]] = np.flatnonzero(masks[b])
+    return masks, counts, ids
+
+
+@pytest.mark.parametrize("n_items,s,d,d_ff,blk,density,r", [(2, 128, 128, 512, 16, 0.5, 8), (3, 100, 192, 384, 16, 0.7, 8),
+                                                           (4, 512, 2048, 8192, 16, 0.2, 8), (2, 256, 256, 1024, 32, 0.4, 0),
+                                                           (2, 128, 128, 512, 64, 0.6, 4)])
+def test_neuron_mlp_gemms(n_items, s, d, d_ff, blk, density, r):
+    from paper_2510_15964_b200 import _abi
+
+    dev = _dev()
+    st = _abi.stream_handle()
+    n_blk = d_ff // blk
+    masks, counts, ids = _masks(n_items, n_blk, density, seed=d + d_ff)
+    g = torch.Generator(device="cpu").manual_seed(7)
+    M = n_items * s
+    x = (torch.randn(M, d, generator=g)).to(dev, torch.bfloat16)
+    w1t = (torch.randn(d_ff, d, generator=g) * d ** -0.5).to(dev, torch.bfloat16)
+    w2 = (torch.randn(d_ff, d, generator=g) * d_ff ** -0.5).to(dev, torch.bfloat16)
+    b1 = torch.randn(d_ff, generator=g).to(dev) * 0.1
+    b2 = torch.randn(d, generator=g).to(dev) * 0.1
+    rr = max(r, 1)
+    ax1 = torch.randn(M, rr, generator=g).to(dev)
+    B1 = torch.randn(rr, d_ff, generator=g).to(dev) * 0.1
+    ax2 = torch.randn(M, rr, generator=g).to(dev)
+    B2 = torch.randn(rr, d, generator=g).to(dev) * 0.1
+    A1 = torch.randn(d, rr, generator=g).to(dev) * 0.1
+    A2 = torch.randn(d_ff, rr, generator=g).to(dev) * 0.1
+    dax1 = torch.randn(M, rr, generator=g).to(dev)
+    dax2 = torch.randn(M, rr, generator=g).to(dev)
+    d_out = torch.randn(M, d, generator=g).to(dev, torch.bfloat16)
+    cnt_d = torch.from_numpy(counts).to(dev)
+    ids_d = torch.from_numpy(ids).to(dev)
+    ld_h = d_ff
+    scaling = 0.5
+    a = torch.zeros(M, ld_h, device=dev, dtype=torch.bfloat16)
+    P = lambda t: None if (t is None or r == 0) else t.data_ptr()  # noqa: E731
+    _abi.call("lx_neuron_fc1", x.data_ptr(), n_items, s, d, d_ff, blk, w1t.data_ptr(), cnt_d.data_ptr(), ids_d.data_ptr(),
+              b1.data_ptr(), P(ax1), P(B1), r, scaling, a.data_ptr(), ld_h, st)
+    out = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
+    _abi.call("lx_neuron_fc2", a.data_ptr(), ld_h, n_items, s, d, d_ff, blk, w2.data_ptr(), cnt_d.data_ptr(), ids_d.data_ptr(),
+              b2.data_ptr(), P(ax2), P(B2), r, scaling, out.data_ptr(), st)
+    dz = torch.zeros(M, ld_h, device=dev, dtype=torch.bfloat16)
+    _abi.call("lx_neuron_fc2_dgrad", d_out.data_ptr(), n_items, s, d, d_ff, blk, w2.data_ptr(), cnt_d.data_ptr(),
+              ids_d.data_ptr(), P(dax2), P(A2), r, a.data_ptr(), dz.data_ptr(), ld_h, st)
+    dx = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
+    _abi.call("lx_neuron_fc1_dgrad", dz.data_ptr(), ld_h, n_items, s, d, d_ff, blk, w1t.data_ptr(), cnt_d.data_ptr(),
+              ids_d.data_ptr(), P(dax1), P(A1), r, dx.data_ptr(), st)
+    torch.cuda.synchronize()
+    for b in range(n_items):
+        rows = slice(b * s, (b + 1) * s)
+        cols = torch.from_numpy((ids[b, : counts[b], None] * blk + np.arange(blk)[None]).reshape(-1)).to(dev)
+        F = cols.numel()
+        xb = x[rows].float()
+        z = xb @ w1t[cols].float().T + b1[cols]
+        if r:
+            z = z + scaling * ax1[rows] @ B1[:, cols]
+        aref = torch.relu(z)
+        if F:
+            assert rel(a[rows, :F], aref) < 1e-2
+        ab = a[rows, :F].float()  # chain on the GPU's own bf16 hidden
+        o = ab @ w2[cols].float() + b2
+        if r:
+            o = o + scaling * ax2[rows] @ B2
+        assert rel(out[rows], o) < 1e-2
+        da = d_out[rows].float() @ w2[cols].float().T
+        if r:
+            da = da + dax2[rows] @ A2[cols].T
+        dzr = da * (ab > 0)
+        if F:
+            assert rel(dz[rows, :F], dzr) < 1e-2
+        dxr = dz[rows, :F].float() @ w1t[cols].float()
+        if r:
+            dxr = dxr + dax1[rows] @ A1.T
+        assert rel(dx[rows], dxr) < 1e-2 if dxr.abs().max() > 0 else dx[rows].float().abs().max() == 0
