@@ -81,11 +81,12 @@ int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, i
  * [0, counts[b]*blk) in ascending block order, row stride ld_h (>= d_ff).
  * LoRA factors are fp32 (trainable); pass NULL to skip a term. */
 
-/* neuron_matmul_fwd1 + b1 + scaling*(x A1) B1[:,cols] + ReLU   (sf/neuron_ops.py:75-82, sf/model.py:376-386)
+/* neuron_matmul_fwd1 + b1 + scaling*(x A1) B1[:,cols] (+ ReLU if apply_relu)
+ *   (sf/neuron_ops.py:75-82, sf/model.py:376-386)
  * ax1: fp32 [M, r] = x A1 (from lx_rowproj); b1_lora: fp32 [r, d_ff] */
 int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w1_t,
                   const int32_t* counts, const int32_t* ids, const float* b1, const float* ax1, const float* b1_lora,
-                  int r, float scaling, uint16_t* a_out, int ld_h, lx_stream_t stream);
+                  int r, float scaling, int apply_relu, uint16_t* a_out, int ld_h, lx_stream_t stream);
 
 /* neuron_matmul_fwd2 + b2 + scaling*(a A2[cols]) B2   (sf/neuron_ops.py:85-95, sf/model.py:388-395)
  * ax2: fp32 [M, r]; b2_lora: fp32 [r, d] */
@@ -137,9 +138,9 @@ int lx_bsattn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, int l
                   const int32_t* pattern_idx, int item_stride, const int32_t* tables, int n_pool, float scale,
                   uint16_t* o, int ldo, float* lse, lx_stream_t stream);
 /* dsd_backward -> sparse_softmax_backward -> sdd_backward (sf/block_sparse.py:63-137).
- * delta_ws fp32 [n_items, H, s]; dq/dk/dv bf16 like q. */
+ * o/d_o row stride ld_o; delta_ws fp32 [n_items, H, s]; dq/dk/dv bf16 with stride ld like q. */
 int lx_bsattn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o, const uint16_t* d_o, int ld,
-                  int n_items, int s, int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables,
+                  int ld_o, int n_items, int s, int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables,
                   int n_pool, float scale, const float* lse, float* delta_ws, uint16_t* dq, uint16_t* dk, uint16_t* dv,
                   lx_stream_t stream);
 

@@ -28,7 +28,7 @@ SIGNATURES: dict[str, list] = {
     "lx_predict_mlp_mask": [_P, _I, _I, _I, _P, _I, _F, _I, _P, _P, _P, _P, _P, _P],
     "lx_mask_compact": [_P, _I, _I, _I, _P, _P, _P, _P],
     "lx_predict_attention_patterns": [_P, _I, _I, _I, _P, _I, _I, _F, _D, _I, _P, _P, _I, _I, _P, _P, _P, _P],
-    "lx_neuron_fc1": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _P, _I, _P],
+    "lx_neuron_fc1": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _I, _P, _I, _P],
     "lx_neuron_fc2": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _P, _P],
     "lx_neuron_fc2_dgrad": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P],
     "lx_neuron_fc1_dgrad": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P],
@@ -39,7 +39,7 @@ SIGNATURES: dict[str, list] = {
     "lx_attn_tables_size": [_I, _I, _I, _P],
     "lx_attn_tables": [_P, _P, _I, _I, _I, _P, _I],
     "lx_bsattn_fwd": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _I, _P, _P],
-    "lx_bsattn_bwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P, _P],
+    "lx_bsattn_bwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P, _P],
     "lx_layernorm_fwd": [_P, _I, _I, _P, _P, _F, _P, _P, _P, _I, _I, _P, _P],
     "lx_layernorm_bwd": [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P],
 }

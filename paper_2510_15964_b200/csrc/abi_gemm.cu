@@ -117,7 +117,7 @@ int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void
 
 int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w1_t,
                   const int32_t* counts, const int32_t* ids, const float* b1, const float* ax1, const float* b1_lora,
-                  int r, float scaling, uint16_t* a_out, int ld_h, lx_stream_t stream) {
+                  int r, float scaling, int apply_relu, uint16_t* a_out, int ld_h, lx_stream_t stream) {
   int rc;
   if ((rc = check_blk(blk))) return rc;
   LX_REQUIRE(d_ff % blk == 0, LX_ERR_MASK, "d_ff %d not a multiple of blk %d on the device path", d_ff, blk);
@@ -138,7 +138,8 @@ int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int bl
   args.w_sc = 1;
   args.lora_r = (ax1 && b1_lora) ? r : 0;
   args.lora_scale = scaling;
-  return launch_gemm<kNGather, kEpiFc1, 256>(ta, tb, args, stream);
+  return apply_relu ? launch_gemm<kNGather, kEpiFc1, 256>(ta, tb, args, stream)
+                    : launch_gemm<kNGather, kEpiFc1Raw, 256>(ta, tb, args, stream);
 }
 
 int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,

@@ -127,7 +127,7 @@ LX_DEV void mma_p_t(float (&acc)[HD / 8][4], const float (&p)[8][4], const __nv_
 // ------------------------------------------------------------ tile tables
 // int32 layout: [0]=nt, [1]=n_pool, then per pattern p at base = 4 + p*per:
 //   row_ptr[nt+1], csr_col[nt*nt], csr_mask[nt*nt], col_ptr[nt+1], csc_row[nt*nt], csc_mask[nt*nt]
-LX_DEV __host__ inline int table_per_pattern(int nt) { return 2 * (nt + 1) + 4 * nt * nt; }
+__host__ __device__ __forceinline__ int table_per_pattern(int nt) { return 2 * (nt + 1) + 4 * nt * nt; }
 
 struct TableView {
   const int32_t *row_ptr, *csr_col, *csr_mask, *col_ptr, *csc_row, *csc_mask;
@@ -289,7 +289,7 @@ __global__ void bsattn_delta_kernel(const __nv_bfloat16* __restrict__ o, const _
 template <int HD>
 __global__ void __launch_bounds__(128) bsattn_dkdv_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
-    const __nv_bfloat16* __restrict__ d_o, int ld, int s, int H, const int32_t* __restrict__ pidx, int item_stride,
+    const __nv_bfloat16* __restrict__ d_o, int ld, int ld_o, int s, int H, const int32_t* __restrict__ pidx, int item_stride,
     const int32_t* __restrict__ tables, float scale, float scale_log2, const float* __restrict__ lse,
     const float* __restrict__ delta, __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv) {
   extern __shared__ __align__(16) uint8_t sm[];
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(128) bsattn_dkdv_kernel(
   auto load_q = [&](int e, int buf) {
     int i = tv.csc_row[e];
     load_tile<HD>(sQ + buf * E, q + off, ld, i * kT, s);
-    load_tile<HD>(sdO + buf * E, d_o + off, ld, i * kT, s);
+    load_tile<HD>(sdO + buf * E, d_o + item_row * ld_o + h * HD, ld_o, i * kT, s);
     if (threadIdx.x < kT) {
       int row = i * kT + threadIdx.x;
       sL[buf * kT + threadIdx.x] = row < s ? lse_b[row] * kLog2e : 0.f;
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(128) bsattn_dkdv_kernel(
 template <int HD>
 __global__ void __launch_bounds__(128) bsattn_dq_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
-    const __nv_bfloat16* __restrict__ d_o, int ld, int s, int H, const int32_t* __restrict__ pidx, int item_stride,
+    const __nv_bfloat16* __restrict__ d_o, int ld, int ld_o, int s, int H, const int32_t* __restrict__ pidx, int item_stride,
     const int32_t* __restrict__ tables, float scale, float scale_log2, const float* __restrict__ lse,
     const float* __restrict__ delta, __nv_bfloat16* __restrict__ dq) {
   extern __shared__ __align__(16) uint8_t sm[];
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(128) bsattn_dq_kernel(
   const float* del_b = delta + ((size_t)item * H + h) * s;
 
   load_tile<HD>(sQ, q + off, ld, qt * kT, s);
-  load_tile<HD>(sdO, d_o + off, ld, qt * kT, s);
+  load_tile<HD>(sdO, d_o + item_row * ld_o + h * HD, ld_o, qt * kT, s);
   if (e0 < e1) {
     int j = tv.csr_col[e0];
     load_tile<HD>(sK, k + off, ld, j * kT, s);
@@ -506,13 +506,13 @@ static int launch_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, i
 
 template <int HD>
 static int launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o, const uint16_t* d_o,
-                      int ld, int n_items, int s, int H, const int32_t* pidx, int item_stride, const int32_t* tables,
+                      int ld, int ld_o, int n_items, int s, int H, const int32_t* pidx, int item_stride, const int32_t* tables,
                       float scale, const float* lse, float* delta, uint16_t* dq, uint16_t* dk, uint16_t* dv,
                       cudaStream_t st) {
   using bf = const __nv_bfloat16*;
   const int rows = n_items * s;
   bsattn_delta_kernel<<<(rows * H * 32 + 255) / 256, 256, 0, st>>>(reinterpret_cast<bf>(o), reinterpret_cast<bf>(d_o),
-                                                                  ld, rows, s, H, HD, delta);
+                                                                  ld_o, rows, s, H, HD, delta);
   int rc = launch_check("bsattn_delta");
   if (rc) return rc;
   constexpr int E = TileSmem<HD>::kElems;
@@ -524,13 +524,13 @@ static int launch_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, c
   LX_CHECK_CUDA(a2);
   dim3 grid((s + kT - 1) / kT, H, n_items);
   bsattn_dkdv_kernel<HD><<<grid, 128, smem_kv, st>>>(reinterpret_cast<bf>(q), reinterpret_cast<bf>(k),
-                                                     reinterpret_cast<bf>(v), reinterpret_cast<bf>(d_o), ld, s, H, pidx,
+                                                     reinterpret_cast<bf>(v), reinterpret_cast<bf>(d_o), ld, ld_o, s, H, pidx,
                                                      item_stride, tables, scale, scale * kLog2e, lse, delta,
                                                      reinterpret_cast<__nv_bfloat16*>(dk),
                                                      reinterpret_cast<__nv_bfloat16*>(dv));
   if ((rc = launch_check("bsattn_dkdv"))) return rc;
   bsattn_dq_kernel<HD><<<grid, 128, smem_q, st>>>(reinterpret_cast<bf>(q), reinterpret_cast<bf>(k),
-                                                  reinterpret_cast<bf>(v), reinterpret_cast<bf>(d_o), ld, s, H, pidx,
+                                                  reinterpret_cast<bf>(v), reinterpret_cast<bf>(d_o), ld, ld_o, s, H, pidx,
                                                   item_stride, tables, scale, scale * kLog2e, lse, delta,
                                                   reinterpret_cast<__nv_bfloat16*>(dq));
   return launch_check("bsattn_dq");
@@ -608,14 +608,14 @@ int lx_bsattn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, int l
 }
 
 int lx_bsattn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o, const uint16_t* d_o, int ld,
-                  int n_items, int s, int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables,
+                  int ld_o, int n_items, int s, int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables,
                   int n_pool, float scale, const float* lse, float* delta_ws, uint16_t* dq, uint16_t* dk, uint16_t* dv,
                   lx_stream_t stream) {
-  LX_REQUIRE(ld % 8 == 0, LX_ERR_SHAPE, "attention: row strides must be multiples of 8");
+  LX_REQUIRE(ld % 8 == 0 && ld_o % 8 == 0, LX_ERR_SHAPE, "attention: row strides must be multiples of 8");
   switch (hd) {
-    case 32: return launch_bwd<32>(q, k, v, o, d_o, ld, n_items, s, H, pattern_idx, item_stride, tables, scale, lse, delta_ws, dq, dk, dv, stream);
-    case 64: return launch_bwd<64>(q, k, v, o, d_o, ld, n_items, s, H, pattern_idx, item_stride, tables, scale, lse, delta_ws, dq, dk, dv, stream);
-    case 128: return launch_bwd<128>(q, k, v, o, d_o, ld, n_items, s, H, pattern_idx, item_stride, tables, scale, lse, delta_ws, dq, dk, dv, stream);
+    case 32: return launch_bwd<32>(q, k, v, o, d_o, ld, ld_o, n_items, s, H, pattern_idx, item_stride, tables, scale, lse, delta_ws, dq, dk, dv, stream);
+    case 64: return launch_bwd<64>(q, k, v, o, d_o, ld, ld_o, n_items, s, H, pattern_idx, item_stride, tables, scale, lse, delta_ws, dq, dk, dv, stream);
+    case 128: return launch_bwd<128>(q, k, v, o, d_o, ld, ld_o, n_items, s, H, pattern_idx, item_stride, tables, scale, lse, delta_ws, dq, dk, dv, stream);
     default: LX_REQUIRE(false, LX_ERR_UNSUPPORTED, "head_dim %d unsupported (32, 64, 128)", hd);
   }
 }

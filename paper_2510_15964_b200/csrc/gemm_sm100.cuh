@@ -29,6 +29,7 @@ enum EpiKind : int {
   kEpiDa = 4,         // (acc + dax2[row]·A2[c,:]) * (a[row,j] > 0) -> bf16 packed dz
   kEpiDx = 5,         // acc + dax1[row]·A1[c,:]                  -> bf16
   kEpiMask = 6,       // OR_rows(acc > thr) per column -> bitmask words (+ optional fp32 dump)
+  kEpiFc1Raw = 7,     // acc + b1[c] + s*ax1[row]·B1[:,c] (no ReLU)  -> bf16 packed (neuron_matmul_fwd1 API)
 };
 
 constexpr int kBM = 128;
@@ -253,7 +254,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       const bool row_ok = local_row < args.rows_per_item;
       const size_t grow = (size_t)ti.item * args.rows_per_item + local_row;
       const int r = args.lora_r;
-      constexpr bool kLora = EPI == kEpiFc1 || EPI == kEpiFc2 || EPI == kEpiDa || EPI == kEpiDx;
+      constexpr bool kLora = EPI == kEpiFc1 || EPI == kEpiFc1Raw || EPI == kEpiFc2 || EPI == kEpiDa || EPI == kEpiDx;
 
       // stage per-column bias / LoRA column factors for this tile
       if (kLora) {

@@ -1,0 +1,122 @@
+"""Device-resident fine-tune step (the inner loop of sf/harness.py:396-427).
+
+`FinetuneEngine.step(tokens)` runs predict -> forward -> loss -> backward ->
+(all-reduce hook) -> Adam entirely on the GPU with no host synchronisation,
+so the whole step can be captured once in a CUDA graph and replayed (the
+launch-bound pattern the B200 playbook asks for). The LM head never
+materialises the full [B*s, V] logits: cross-entropy and its gradient are
+computed in row chunks (tied embedding, sf/model.py:449-472).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import autograd as AG, model as M
+
+
+def lm_head_loss_and_grad(hf: torch.Tensor, emb: torch.Tensor, targets: torch.Tensor, s: int, chunk: int = 1024):
+    """Mean CE over positions (per-item mean, then batch mean) and d(sum of per-item losses)/d hf.
+    hf bf16 [M, d]; emb bf16 [V, d]; targets int64 [M]. Returns (loss fp32 scalar tensor, d_hf fp32 [M, d])."""
+    Mr = hf.shape[0]
+    d_hf = torch.empty(Mr, hf.shape[1], dtype=torch.float32, device=hf.device)
+    loss_sum = torch.zeros((), dtype=torch.float32, device=hf.device)
+    for r0 in range(0, Mr, chunk):
+        r1 = min(Mr, r0 + chunk)
+        lg = M._mm_f32(hf[r0:r1], emb.t())  # [c, V] fp32
+        t = targets[r0:r1]
+        lse = torch.logsumexp(lg, dim=1)
+        loss_sum += (lse - lg.gather(1, t[:, None])[:, 0]).sum()
+        lg.sub_(lse[:, None]).exp_()  # softmax in place
+        lg.scatter_add_(1, t[:, None], torch.full((r1 - r0, 1), -1.0, device=hf.device))
+        lg.mul_(1.0 / s)  # per-item mean (sf/model.py:472)
+        d_hf[r0:r1] = M._mm_f32(lg.to(torch.bfloat16), emb)
+    return loss_sum / Mr, d_hf
+
+
+class FinetuneEngine:
+    """Fused fine-tune step over a batch of B sequences of length s (tokens [B, s+1])."""
+
+    def __init__(self, model: M.Model, state: M.PeftState, provider, lr: float, loss_chunk: int = 1024, grad_hook=None):
+        self.model, self.state, self.provider, self.lr = model, state, provider, lr
+        self.loss_chunk = loss_chunk
+        self.grad_hook = grad_hook  # called with the flat mean-gradient buffer (e.g. NCCL all-reduce)
+        self.flat_grad = torch.zeros_like(state.flat)
+        self.flat_grad64 = torch.zeros_like(state.m)
+        self.graph = None
+        self.static_tokens = None
+        self.static_loss = None
+        self._slots = []
+        base = state.flat.data_ptr()
+        for name, p in state.params.items():
+            off = (p.data_ptr() - base) // 4
+            self._slots.append((name, off, p.numel()))
+        self.last_masks = None
+
+    # -------------------------------------------------------------- one step (capturable)
+    def _step(self, tokens: torch.Tensor) -> torch.Tensor:
+        m = self.model
+        B, s1 = tokens.shape
+        s = s1 - 1
+        inp, tgt = tokens[:, :-1], tokens[:, 1:].reshape(-1)
+        h = m.weights.emb[inp].float()
+        caches = []
+        for layer in range(m.dims.n_layers):
+            h, c = M.block_forward(h, m, layer, self.provider)
+            caches.append(c)
+        hf, cf = M.layernorm_forward(h, m.weights.lnf_g, m.weights.lnf_b)
+        loss, d_hf = lm_head_loss_and_grad(hf, m.weights.emb, tgt, s, self.loss_chunk)
+        grads: dict = {}
+        dh = AG.layernorm_backward(d_hf, cf)
+        for layer in reversed(range(m.dims.n_layers)):
+            dh = AG.block_backward(dh, m, layer, caches[layer], None, grads)
+        self.last_masks = [c["masks"] for c in caches]
+        g = self.flat_grad
+        g.zero_()
+        inv_b = 1.0 / B
+        for name, off, n in self._slots:
+            if name in grads:
+                g[off : off + n].copy_(grads[name].reshape(-1)).mul_(inv_b)
+        return loss
+
+    def _finish(self) -> None:
+        """Data-parallel gradient reduction hook, then Adam (float64 moments, sf/autograd.py:203-225)."""
+        if self.grad_hook is not None:
+            self.grad_hook(self.flat_grad)
+        self.state.step += 1
+        self.flat_grad64.copy_(self.flat_grad)
+        AG.adam_flat(self.state.flat, self.flat_grad64, self.state.m, self.state.v, self.lr, 0.9, 0.999, 1e-8,
+                     self.state.step)
+
+    def step(self, tokens) -> torch.Tensor:
+        """Eager step (tokens host or device). Returns the loss as a device scalar."""
+        tok = torch.as_tensor(np.asarray(tokens) if not torch.is_tensor(tokens) else tokens)
+        tok = tok.to(self.model.device, torch.int64, non_blocking=True)
+        loss = self._step(tok)
+        self._finish()
+        return loss
+
+    # -------------------------------------------------------------- CUDA graph
+    def capture(self, example_tokens: torch.Tensor, warmup: int = 2) -> None:
+        """Capture forward+backward+grad-reduction (not Adam, whose bias correction depends on
+        the step count) into one CUDA graph; Adam runs as a handful of elementwise kernels."""
+        self.static_tokens = example_tokens.to(self.model.device, torch.int64).clone()
+        if hasattr(self.provider, "timing"):
+            self.provider.timing = False  # no timing events inside a graph
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self._step(self.static_tokens)
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.static_loss = self._step(self.static_tokens)
+
+    def replay(self, tokens=None) -> torch.Tensor:
+        if tokens is not None:
+            self.static_tokens.copy_(tokens, non_blocking=True)
+        self.graph.replay()
+        self._finish()
+        return self.static_loss

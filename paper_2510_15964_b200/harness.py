@@ -1,0 +1,144 @@
+"""Mask providers and the fine-tune step (drop-in for the hot-path half of
+sf/harness.py:122-244 and the inner loop of run_finetune, sf/harness.py:396-427).
+
+Providers implement the reference protocol `attn_patterns(layer, h)` /
+`mlp_mask(layer, h)`. The predicted provider returns device-resident results
+(pool indices [B, H] and compacted neuron index lists) so a step never
+synchronises the host; it also asks block_forward for the LayerNorm-fused
+downsampled rows (`fused_downsample`). Prediction time is measured with CUDA
+events on the current stream (the reference uses perf_counter around the
+same calls) and reported without a sync until `elapsed_ns` is read.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import autograd, model as M, predictor as P
+from .errors import ConfigError
+
+MODES = ("dense", "predicted", "random", "static")
+
+
+class _TimedProvider:
+    def __init__(self):
+        self._events: list = []
+        self.timing = True
+
+    def _timed(self, fn, *a, **k):
+        if not self.timing:
+            return fn(*a, **k)
+        st = torch.cuda.Event(enable_timing=True)
+        en = torch.cuda.Event(enable_timing=True)
+        st.record()
+        out = fn(*a, **k)
+        en.record()
+        self._events.append((st, en))
+        return out
+
+    @property
+    def elapsed_ns(self) -> int:
+        torch.cuda.synchronize()
+        return int(sum(s.elapsed_time(e) for s, e in self._events) * 1e6)
+
+    def reset_timing(self):
+        self._events.clear()
+
+    def attn_patterns(self, layer: int, h, x_small=None):
+        return self._timed(self._attn, layer, h, x_small)
+
+    def mlp_mask(self, layer: int, h):
+        return self._timed(self._mlp, layer, h)
+
+
+class DenseProvider(_TimedProvider):
+    """sf/harness.py:145-154."""
+
+    def __init__(self, model: M.Model):
+        super().__init__()
+        self.model = model
+
+    def _attn(self, layer, h, x_small=None):
+        return ["dense"] * self.model.dims.n_heads
+
+    def _mlp(self, layer, h):
+        return np.ones(self.model.dims.n_blk, dtype=bool)
+
+
+class PredictedProvider(_TimedProvider):
+    """sf/harness.py:193-211 on the fused mask-build kernels. scope='item' gives the
+    fine-tune loop's per-sequence masks; scope='batch' ORs over the batch (sf/predictor.py:105-136)."""
+
+    fused_downsample = True
+
+    def __init__(self, model: M.Model, predictors: dict, cfg: P.PredictorTrainConfig | None = None, counter=None,
+                 scope: str = "item"):
+        super().__init__()
+        if scope not in ("item", "batch"):
+            raise ConfigError(f"unknown mask scope {scope!r}")
+        self.model, self.predictors, self.counter = model, predictors, counter
+        self.pcfg = cfg or P.PredictorTrainConfig()
+        self.scope_batch = scope == "batch"
+        self.last_scores = {}
+
+    def _attn(self, layer, h, x_small=None):
+        B, s, d = h.shape
+        if x_small is None:
+            x_small, m = P.x_small_of(h)
+        else:
+            m = x_small.shape[0] // B
+        params = self.predictors["attn"][layer]
+        idx, _ = P.attn_pattern_idx(x_small, B, m, params, self.model.dpool, self.model.dims.n_b, self.pcfg,
+                                    scope_batch=self.scope_batch)
+        if self.counter is not None:
+            self.counter.add(B * len(params.wq_hat) * (2 * m * d * params.rank + m * m * params.rank))
+        return idx
+
+    def _mlp(self, layer, h):
+        B, s, d = h.shape
+        params = self.predictors["mlp"][layer]
+        nm, _ = P.mlp_masks(h.reshape(B * s, d), B, s, params, self.pcfg.mlp_threshold, self.model.dims.blk_size,
+                            scope_batch=self.scope_batch)
+        if self.counter is not None:
+            self.counter.add(B * (s * d * self.model.dims.n_blk + s))
+        return nm
+
+
+class RandomProvider(_TimedProvider):
+    """Seeded random patterns (sf/harness.py:214-230), the convergence-ablation baseline."""
+
+    def __init__(self, model: M.Model, seed: int):
+        super().__init__()
+        self.model = model
+        self.rng = np.random.Generator(np.random.PCG64(seed))
+        self.pattern_ids = [p for p in model.pool if p != "dense"]
+
+    def _attn(self, layer, h, x_small=None):
+        return [self.pattern_ids[self.rng.integers(len(self.pattern_ids))] for _ in range(self.model.dims.n_heads)]
+
+    def _mlp(self, layer, h):
+        mask = self.rng.random(self.model.dims.n_blk) < 0.5
+        if not mask.any():
+            mask[self.rng.integers(len(mask))] = True
+        return mask
+
+
+def finetune_step(model: M.Model, state: M.PeftState, batch_tokens, provider, lr: float, grad_hook=None) -> dict:
+    """One optimiser step of run_finetune (sf/harness.py:396-417) over a batch [B, s+1]:
+    per-item masks, mean loss, grads summed over items then / B, Adam (float64 moments).
+    `grad_hook(flat_grads)` runs before the update (the data-parallel all-reduce)."""
+    tok = torch.as_tensor(np.asarray(batch_tokens) if not torch.is_tensor(batch_tokens) else batch_tokens)
+    tok = tok.to(model.device, torch.int64)
+    inp, tgt = tok[:, :-1], tok[:, 1:]
+    logits, cache = M.model_forward(model, inp, provider)
+    loss = M.loss_forward(logits, tgt)
+    grads = autograd.model_backward(model, cache, M.loss_backward(logits, tgt))
+    B = tok.shape[0]
+    mean = {n: g / B for n, g in grads.items()}
+    if grad_hook is not None:
+        mean = grad_hook(mean)
+    autograd.optimizer_step(state, mean, lr)
+    if not np.isfinite(loss):
+        raise FloatingPointError(f"non-finite loss {loss}")
+    return {"loss": loss, "grads": mean, "masks": [c["masks"] for c in cache["blocks"]]}

@@ -1,0 +1,546 @@
+"""Frozen-backbone transformer with LoRA / Adapter / BitFit on the B200
+(drop-in for sf/model.py).
+
+Semantics mirror the reference exactly: pre-LN residual blocks, non-causal
+block-sparse attention without positional embedding (sf/model.py:443), ReLU
+MLP restricted to active neuron blocks, tied unembedding, mean cross-entropy.
+Every forward takes a batch of items [B, s] at once (the reference loops over
+sequences, sf/harness.py:401-411); masks stay per item, so results equal the
+per-item loop and gradients equal the reference's per-item sum.
+
+Device layout: residual stream fp32 [B*s, d]; LN outputs and GEMM operands
+bf16; frozen weights bf16 (W_qkv fused [d, 3d]; W1^T and W2 [d_ff, d]);
+trainable tensors fp32 views into one flat buffer (`PeftState`) so the
+data-parallel all-reduce is a single NCCL call.
+
+Hot-path kernels: mask build (predictor.py), neuron-sparse MLP (neuron_ops.py),
+block-sparse attention (block_sparse.py), LayerNorm (+ fused predictor
+downsample). Dense neighbours (Q/K/V/O projections, LM head) use cuBLAS.
+"""
+
+from __future__ import annotations
+
+import copy
+import hashlib
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _abi, neuron_ops
+from .block_sparse import attention_forward
+from .errors import ShapeError
+from .neuron_ops import LayeredWeights, NeuronMasks, lower_mask, rowproj
+from .patterns import DevicePool, LayoutTable, build_pool, device_pool
+
+LORA_TARGET_SHAPES = {"wq": "attn", "wk": "attn", "wv": "attn", "wo": "attn", "w1": "mlp_in", "w2": "mlp_out"}
+PEFT_METHODS = ("lora", "adapter", "bitfit")
+BIAS_NAMES = ("bq", "bk", "bv", "bo", "b1", "b2")
+
+
+@dataclass(frozen=True)
+class ModelDims:
+    """sf/model.py:33-60."""
+
+    d_model: int
+    n_heads: int
+    d_ff: int
+    seq_len: int
+    n_layers: int = 4
+    vocab: int = 256
+    blk_size: int = 16
+    attn_blk: int = 16
+
+    def __post_init__(self):
+        if self.d_model % self.n_heads:
+            raise ShapeError(f"d_model {self.d_model} not divisible by n_heads {self.n_heads}")
+        if self.seq_len % self.attn_blk:
+            raise ShapeError(f"seq_len {self.seq_len} not divisible by attn_blk {self.attn_blk}")
+
+    @property
+    def head_dim(self) -> int:
+        return self.d_model // self.n_heads
+
+    @property
+    def n_blk(self) -> int:
+        return neuron_ops.n_blocks(self.d_ff, self.blk_size)
+
+    @property
+    def n_b(self) -> int:
+        return self.seq_len // self.attn_blk
+
+
+@dataclass
+class LoraAdapter:
+    """z = xW + scaling * (xA)B; a (d_in, r), b (r, d_out) fp32 (sf/model.py:63-73)."""
+
+    a: torch.Tensor
+    b: torch.Tensor
+    scaling: float = 1.0
+
+    @property
+    def rank(self) -> int:
+        return self.a.shape[1]
+
+
+@dataclass
+class AdapterLayer:
+    """Bottleneck adapter x + relu(x Wd + bd) Wu + bu (sf/model.py:76-83)."""
+
+    w_down: torch.Tensor
+    b_down: torch.Tensor
+    w_up: torch.Tensor
+    b_up: torch.Tensor
+
+
+@dataclass
+class LayerWeights:
+    """sf/model.py:86-102 with the device layout described in the module docstring."""
+
+    wqkv: torch.Tensor  # bf16 [d, 3d]
+    wo: torch.Tensor  # bf16 [d, d]
+    bqkv: torch.Tensor  # fp32 [3d] (bq | bk | bv)
+    bo: torch.Tensor
+    mlp: LayeredWeights
+    b1: torch.Tensor
+    b2: torch.Tensor
+    ln1_g: torch.Tensor
+    ln1_b: torch.Tensor
+    ln2_g: torch.Tensor
+    ln2_b: torch.Tensor
+
+    @property
+    def d(self) -> int:
+        return self.wo.shape[0]
+
+    @property
+    def bq(self):
+        return self.bqkv[: self.d]
+
+    @property
+    def bk(self):
+        return self.bqkv[self.d : 2 * self.d]
+
+    @property
+    def bv(self):
+        return self.bqkv[2 * self.d :]
+
+    @property
+    def wq(self):
+        return self.wqkv[:, : self.d]
+
+    @property
+    def wk(self):
+        return self.wqkv[:, self.d : 2 * self.d]
+
+    @property
+    def wv(self):
+        return self.wqkv[:, 2 * self.d :]
+
+
+@dataclass
+class FrozenWeights:
+    emb: torch.Tensor  # bf16 [V, d] (tied embedding / unembedding)
+    layers: list
+    lnf_g: torch.Tensor
+    lnf_b: torch.Tensor
+
+
+@dataclass
+class PeftState:
+    """Trainable set with Adam moments (sf/model.py:113-127). `params` are views of
+    one flat fp32 buffer; moments are float64 like the reference."""
+
+    method: str
+    params: dict
+    flat: torch.Tensor | None = None
+    m: torch.Tensor | None = None
+    v: torch.Tensor | None = None
+    step: int = 0
+
+
+@dataclass
+class LayerMasks:
+    """sf/model.py:130-133. head_patterns: list[str] (shared) or int32 [B, H] pool indices;
+    neuron_mask: bool [n_blk] / [B, n_blk] or NeuronMasks."""
+
+    head_patterns: object
+    neuron_mask: object
+
+
+def dense_masks(dims: ModelDims) -> list[LayerMasks]:
+    return [LayerMasks(["dense"] * dims.n_heads, np.ones(dims.n_blk, dtype=bool)) for _ in range(dims.n_layers)]
+
+
+@dataclass
+class Model:
+    dims: ModelDims
+    weights: FrozenWeights
+    pool: dict
+    peft_method: str
+    lora: dict = field(default_factory=dict)
+    adapters: dict = field(default_factory=dict)
+    lora_targets: tuple = ()
+    device: torch.device = torch.device("cuda")
+    _dpool: DevicePool | None = None
+
+    @property
+    def dpool(self) -> DevicePool:
+        if self._dpool is None:
+            self._dpool = device_pool(self.pool, self.device, self.dims.seq_len, self.dims.attn_blk)
+        return self._dpool
+
+
+# ---------------------------------------------------------------- construction
+
+
+def _t(a, device, dtype=torch.float32):
+    return torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a).to(device=device, dtype=dtype).contiguous()
+
+
+def from_arrays(dims: ModelDims, peft: str, emb, layers: list[dict], lnf_g, lnf_b, lora: dict | None = None,
+                adapters: dict | None = None, lora_targets=(), device="cuda") -> Model:
+    """Build a device model from reference-format arrays (w1 is [d, d_ff]; lora values have
+    a/b/scaling; adapters have w_down/b_down/w_up/b_up)."""
+    dev = torch.device(device)
+    L = []
+    for lw in layers:
+        L.append(LayerWeights(
+            wqkv=torch.cat([_t(lw["wq"], dev), _t(lw["wk"], dev), _t(lw["wv"], dev)], 1).to(torch.bfloat16).contiguous(),
+            wo=_t(lw["wo"], dev, torch.bfloat16),
+            bqkv=torch.cat([_t(lw["bq"], dev), _t(lw["bk"], dev), _t(lw["bv"], dev)]).contiguous(),
+            bo=_t(lw["bo"], dev), mlp=LayeredWeights.from_row_major(np.asarray(lw["w1"]) if not torch.is_tensor(lw["w1"]) else lw["w1"],
+                                                                   np.asarray(lw["w2"]) if not torch.is_tensor(lw["w2"]) else lw["w2"], dev),
+            b1=_t(lw["b1"], dev), b2=_t(lw["b2"], dev), ln1_g=_t(lw["ln1_g"], dev), ln1_b=_t(lw["ln1_b"], dev),
+            ln2_g=_t(lw["ln2_g"], dev), ln2_b=_t(lw["ln2_b"], dev)))
+    m = Model(dims, FrozenWeights(_t(emb, dev, torch.bfloat16), L, _t(lnf_g, dev), _t(lnf_b, dev)), build_pool(dims.n_b), peft,
+              lora_targets=tuple(lora_targets) if peft == "lora" else (), device=dev)
+    for key, ad in (lora or {}).items():
+        m.lora[key] = LoraAdapter(_t(ad["a"], dev), _t(ad["b"], dev), float(ad.get("scaling", 1.0)))
+    for key, ad in (adapters or {}).items():
+        m.adapters[key] = AdapterLayer(*(_t(ad[k], dev) for k in ("w_down", "b_down", "w_up", "b_up")))
+    return m
+
+
+def build_model(dims: ModelDims, seed: int, peft: str = "lora", lora_rank: int = 8,
+                lora_targets: tuple = ("wq", "wv", "w1", "w2"), adapter_rank: int = 8, init_scale: float = 0.02,
+                device="cuda") -> Model:
+    """Random-init model with the reference's init distribution (sf/model.py:174-231):
+    projections / embedding / LoRA-A / adapter-down N(0, init_scale^2), zero biases,
+    LN gamma=1 beta=0, LoRA-B and adapter-up zero. Drawn on the device (torch
+    generator); use `from_arrays` to load reference-initialised weights."""
+    if peft not in PEFT_METHODS:
+        raise ValueError(f"unknown peft method {peft!r}")
+    dev = torch.device(device)
+    g = torch.Generator(device=dev).manual_seed(seed)
+    d, f = dims.d_model, dims.d_ff
+
+    def rn(*shape, dtype=torch.bfloat16):
+        return (torch.randn(*shape, generator=g, device=dev) * init_scale).to(dtype)
+
+    z = lambda n: torch.zeros(n, device=dev)  # noqa: E731
+    layers = [LayerWeights(rn(d, 3 * d), rn(d, d), z(3 * d), z(d), LayeredWeights(rn(f, d), rn(f, d)), z(f), z(d),
+                           torch.ones(d, device=dev), z(d), torch.ones(d, device=dev), z(d)) for _ in range(dims.n_layers)]
+    m = Model(dims, FrozenWeights(rn(dims.vocab, d), layers, torch.ones(d, device=dev), z(d)), build_pool(dims.n_b), peft,
+              lora_targets=tuple(lora_targets) if peft == "lora" else (), device=dev)
+    shapes = {"attn": (d, d), "mlp_in": (d, f), "mlp_out": (f, d)}
+    if peft == "lora":
+        for i in range(dims.n_layers):
+            for t in m.lora_targets:
+                di, do = shapes[LORA_TARGET_SHAPES[t]]
+                m.lora[(i, t)] = LoraAdapter(rn(di, lora_rank, dtype=torch.float32), torch.zeros(lora_rank, do, device=dev))
+    elif peft == "adapter":
+        for i in range(dims.n_layers):
+            for sub in ("attn", "mlp"):
+                m.adapters[(i, sub)] = AdapterLayer(rn(d, adapter_rank, dtype=torch.float32), z(adapter_rank),
+                                                    torch.zeros(adapter_rank, d, device=dev), z(d))
+    return m
+
+
+def _param_slots(model: Model) -> list[tuple[str, object, str]]:
+    """(name, owner, attribute) in the reference's trainable order (sf/model.py:234-249)."""
+    out = []
+    if model.peft_method == "lora":
+        for (i, t), ad in sorted(model.lora.items()):
+            out += [(f"layers.{i}.{t}.lora_a", ad, "a"), (f"layers.{i}.{t}.lora_b", ad, "b")]
+    elif model.peft_method == "adapter":
+        for (i, sub), ad in sorted(model.adapters.items()):
+            out += [(f"layers.{i}.{sub}_adapter.{k}", ad, k) for k in ("w_down", "b_down", "w_up", "b_up")]
+    else:
+        for i, lw in enumerate(model.weights.layers):
+            out += [(f"layers.{i}.bqkv", lw, "bqkv"), (f"layers.{i}.bo", lw, "bo"), (f"layers.{i}.b1", lw, "b1"),
+                    (f"layers.{i}.b2", lw, "b2")]
+    return out
+
+
+def trainable_params(model: Model) -> dict[str, torch.Tensor]:
+    """Named references to every trainable tensor (sf/model.py:234-249); BitFit's
+    bq/bk/bv are views of the fused bias."""
+    out = {}
+    for name, owner, attr in _param_slots(model):
+        t = getattr(owner, attr)
+        if name.endswith(".bqkv"):
+            i = name.split(".")[1]
+            d = t.shape[0] // 3
+            out[f"layers.{i}.bq"], out[f"layers.{i}.bk"], out[f"layers.{i}.bv"] = t[:d], t[d : 2 * d], t[2 * d :]
+        else:
+            out[name] = t
+    if model.peft_method == "bitfit":  # reference order: bq, bk, bv, bo, b1, b2 per layer
+        out = {k: out[k] for i in range(model.dims.n_layers) for k in (f"layers.{i}.{b}" for b in BIAS_NAMES)}
+    return out
+
+
+def make_peft_state(model: Model) -> PeftState:
+    """Move every trainable tensor into one flat fp32 buffer (views keep the model
+    pointing at the live parameters) and allocate float64 Adam moments."""
+    slots = _param_slots(model)
+    n = sum(getattr(o, a).numel() for _, o, a in slots)
+    flat = torch.zeros(n, dtype=torch.float32, device=model.device)
+    off = 0
+    for _, owner, attr in slots:
+        t = getattr(owner, attr)
+        view = flat[off : off + t.numel()].view(t.shape)
+        view.copy_(t)
+        setattr(owner, attr, view)
+        off += t.numel()
+    st = PeftState(model.peft_method, trainable_params(model), flat,
+                   torch.zeros(n, dtype=torch.float64, device=model.device), torch.zeros(n, dtype=torch.float64, device=model.device))
+    return st
+
+
+def backbone_param_count(model: Model) -> int:
+    d = model.dims
+    per = 4 * d.d_model * d.d_model + 4 * d.d_model + d.d_ff + d.d_model + 4 * d.d_model + 2 * d.d_model * d.d_ff
+    return d.vocab * d.d_model + 2 * d.d_model + d.n_layers * per
+
+
+def frozen_hash(model: Model) -> str:
+    """SHA-256 over the frozen backbone bytes (sf/model.py:267-285, device byte layout)."""
+    h = hashlib.sha256()
+    skip = model.peft_method == "bitfit"
+    for t in [model.weights.emb, model.weights.lnf_g, model.weights.lnf_b]:
+        h.update(t.detach().cpu().contiguous().view(torch.uint8).numpy().tobytes())
+    for lw in model.weights.layers:
+        ts = [lw.wqkv, lw.wo, lw.ln1_g, lw.ln1_b, lw.ln2_g, lw.ln2_b, lw.mlp.w1_t, lw.mlp.w2]
+        if not skip:
+            ts += [lw.bqkv, lw.bo, lw.b1, lw.b2]
+        for t in ts:
+            h.update(t.detach().cpu().contiguous().view(torch.uint8).numpy().tobytes())
+    return h.hexdigest()
+
+
+# ---------------------------------------------------------------- forward passes
+
+
+def _items(x: torch.Tensor):
+    """[s, d] or [B, s, d] -> (x2 [B*s, d], B, s)."""
+    if x.dim() == 2:
+        return x, 1, x.shape[0]
+    return x.reshape(-1, x.shape[-1]), x.shape[0], x.shape[1]
+
+
+def _mm_f32(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """bf16 x bf16 -> fp32 (cuBLAS)."""
+    try:
+        return torch.mm(a, b, out_dtype=torch.float32)
+    except TypeError:  # older torch
+        return torch.mm(a, b).float()
+
+
+def lora_linear_forward(x, w, bias, adapter: LoraAdapter | None):
+    """z = xW (+ bias) + scaling*(xA)B (sf/model.py:292-304); x bf16, z fp32."""
+    if x.shape[1] != w.shape[0]:
+        raise ShapeError(f"linear shapes disagree: {tuple(x.shape)} @ {tuple(w.shape)}")
+    z = _mm_f32(x, w)
+    cache = {"x": x, "ax": None}
+    if adapter is not None:
+        ax = x.float() @ adapter.a
+        z.addmm_(ax, adapter.b, alpha=adapter.scaling)
+        cache["ax"] = ax
+    if bias is not None:
+        z += bias
+    return z, cache
+
+
+def layernorm_forward(x: torch.Tensor, gamma, beta, eps: float = 1e-5, x_small_spec=None):
+    """sf/model.py:307-312 on the fused kernel; x fp32 [M, d] -> bf16 y. x_small_spec=(s, m)
+    additionally writes the predictor's downsampled rows (returned in the cache)."""
+    x2 = x.reshape(-1, x.shape[-1]).contiguous()
+    M, d = x2.shape
+    y = torch.empty(M, d, dtype=torch.bfloat16, device=x2.device)
+    mean = torch.empty(M, dtype=torch.float32, device=x2.device)
+    istd = torch.empty(M, dtype=torch.float32, device=x2.device)
+    xs, s, m = None, 0, 0
+    if x_small_spec is not None:
+        s, m = x_small_spec
+        xs = torch.empty(M // s * m, d, dtype=torch.bfloat16, device=x2.device)
+    _abi.call("lx_layernorm_fwd", x2.data_ptr(), M, d, gamma.data_ptr(), beta.data_ptr(), float(eps), y.data_ptr(),
+              mean.data_ptr(), istd.data_ptr(), s, m, _abi.ptr(xs), _abi.stream_handle(x2.device))
+    return y, {"x": x2, "mean": mean, "inv_std": istd, "gamma": gamma, "x_small": xs}
+
+
+def adapter_forward(x: torch.Tensor, ad: AdapterLayer):
+    """x + relu(x Wd + bd) Wu + bu (sf/model.py:315-319); fp32."""
+    z = torch.addmm(ad.b_down, x, ad.w_down)
+    h = torch.relu(z)
+    return x + torch.addmm(ad.b_up, h, ad.w_up), {"x": x, "z": z, "h": h}
+
+
+def resolve_head_patterns(head_patterns, model_or_dpool, n_items: int, n_heads: int, device):
+    """list[str] (shared) / list[list[str]] (per item) / int32 tensor [B|1, H] -> (pidx, item_stride)."""
+    dp = model_or_dpool.dpool if isinstance(model_or_dpool, Model) else model_or_dpool
+    if torch.is_tensor(head_patterns):
+        t = head_patterns.to(device=device, dtype=torch.int32).contiguous()
+        if t.dim() == 1:
+            t = t[None]
+        if t.shape[-1] != n_heads:
+            raise ShapeError(f"expected {n_heads} head patterns, got {t.shape[-1]}")
+        return t, (0 if t.shape[0] == 1 else n_heads)
+    hp = list(head_patterns)
+    if hp and isinstance(hp[0], (list, tuple)):
+        rows = [[dp.idx(p) for p in row] for row in hp]
+        if any(len(r) != n_heads for r in rows):
+            raise ShapeError(f"expected {n_heads} head patterns per item")
+        return torch.tensor(rows, dtype=torch.int32, device=device), n_heads
+    if len(hp) != n_heads:
+        raise ShapeError(f"expected {n_heads} head patterns, got {len(hp)}")
+    # static assignments are lowered once per (assignment, device) and reused (also inside CUDA-graph capture)
+    cache = dp.__dict__.setdefault("_static_idx", {})
+    key = (tuple(str(p) for p in hp), str(device))
+    if key not in cache:
+        cache[key] = torch.tensor([[dp.idx(p) for p in hp]], dtype=torch.int32, device=device)
+    return cache[key], 0
+
+
+def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: ModelDims, counter=None, *, dpool=None):
+    """Block-sparse multi-head attention (sf/model.py:322-360). x: LN1 output bf16 [B, s, d] (or [s, d]).
+    Returns (out fp32 [B*s, d], cache); the cache holds O and the row LSE instead of probabilities."""
+    x2, B, s = _items(x)
+    d, H, hd = dims.d_model, dims.n_heads, dims.head_dim
+    dp = dpool if dpool is not None else device_pool(pool, x2.device, dims.seq_len, dims.attn_blk)
+    pidx, stride = resolve_head_patterns(head_patterns, dp, B, H, x2.device)
+    qkv = torch.mm(x2, lw.wqkv)  # bf16 [M, 3d]
+    qkv += lw.bqkv.to(torch.bfloat16)
+    ax = {}
+    for j, t in enumerate(("wq", "wk", "wv")):
+        ad = lora.get(t)
+        if ad is not None:
+            ax[t] = x2.float() @ ad.a
+            sl = qkv[:, j * d : (j + 1) * d]
+            sl.copy_((sl.float() + ad.scaling * (ax[t] @ ad.b)).to(torch.bfloat16))
+    scale = 1.0 / float(np.sqrt(hd))
+    o, lse = attention_forward(qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :], 3 * d, B, s, H, hd, pidx, stride, dp, scale)
+    if counter is not None:
+        nnz = sum(dp_nnz(dp, int(i)) for i in pidx.flatten().tolist()) * (B if stride == 0 else 1)
+        counter.add(2 * nnz * dims.attn_blk * dims.attn_blk * hd)
+    out, co = lora_linear_forward(o, lw.wo, lw.bo, lora.get("wo"))
+    cache = {"x": x2, "qkv": qkv, "o": o, "lse": lse, "pidx": pidx, "stride": stride, "ax": ax, "co": co, "n_items": B,
+             "s": s, "dpool": dp}
+    return out, cache
+
+
+def dp_nnz(dp: DevicePool, i: int) -> int:
+    n_b = dp.seq_len // dp.attn_blk
+    return len(build_pool(n_b)[dp.ids[i]].coords) if dp.seq_len else 0
+
+
+def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, counter=None):
+    """ReLU MLP restricted to active neuron blocks (sf/model.py:363-400) on the tcgen05
+    gather-GEMMs with bias / LoRA / ReLU fused in the epilogues. x: LN2 output bf16."""
+    x2, B, s = _items(x)
+    d, f, blk = dims.d_model, dims.d_ff, dims.blk_size
+    nm = lower_mask(neuron_mask, dims.n_blk, blk, B, x2.device)
+    ad1, ad2 = lora.get("w1"), lora.get("w2")
+    ax1 = rowproj(x2, B, s, d, ad1.a, ad1.rank, 1, ad1.rank) if ad1 is not None else None
+    hid = neuron_ops.neuron_matmul_fwd1(x2.view(B, s, d), lw.mlp, nm, blk, counter, bias=lw.b1, ax=ax1,
+                                        lora_b=ad1.b if ad1 else None, lora_r=ad1.rank if ad1 else 0,
+                                        scaling=ad1.scaling if ad1 else 1.0, relu=True)
+    ax2 = rowproj(hid.values, B, s, f, ad2.a, ad2.rank, 1, ad2.rank, masks=nm, blk=blk) if ad2 is not None else None
+    out = neuron_ops.neuron_matmul_fwd2(hid, lw.mlp, None, counter, bias=lw.b2, ax=ax2, lora_b=ad2.b if ad2 else None,
+                                        lora_r=ad2.rank if ad2 else 0, scaling=ad2.scaling if ad2 else 1.0)
+    if counter is not None:
+        n_act = int(nm.counts.sum()) * blk
+        if ad1 is not None:
+            counter.add(s * (d + n_act // max(B, 1)) * ad1.rank * B)
+        if ad2 is not None:
+            counter.add(s * (n_act // max(B, 1) + d) * ad2.rank * B)
+    return out, {"x": x2, "a": hid, "mask": nm, "ax1": ax1, "ax2": ax2, "n_items": B, "s": s}
+
+
+def block_forward(x, model: Model, layer: int, masks, counter=None):
+    """Pre-norm residual block (sf/model.py:403-433); x fp32 [B, s, d]. `masks` is a
+    LayerMasks or a provider with attn_patterns(layer, h) / mlp_mask(layer, h)."""
+    lw = model.weights.layers[layer]
+    lora = {t: model.lora[(layer, t)] for t in model.lora_targets} if model.peft_method == "lora" else {}
+    B, s, d = x.shape
+    static = isinstance(masks, LayerMasks)
+    spec = None
+    if not static and getattr(masks, "fused_downsample", False):
+        from .predictor import downsample_indices
+
+        spec = (s, len(downsample_indices(s)))
+    h1, c1 = layernorm_forward(x, lw.ln1_g, lw.ln1_b, x_small_spec=spec)
+    h1v = h1.view(B, s, d)
+    if static:
+        hp = masks.head_patterns
+    elif spec is not None:
+        hp = masks.attn_patterns(layer, h1v, x_small=c1["x_small"])
+    else:
+        hp = masks.attn_patterns(layer, h1v)
+    att, ca = mha_forward(h1v, lw, lora, hp, model.pool, model.dims, counter, dpool=model.dpool)
+    caa = None
+    if model.peft_method == "adapter":
+        att, caa = adapter_forward(att, model.adapters[(layer, "attn")])
+    y = x.reshape(B * s, d) + att
+    h2, c2 = layernorm_forward(y, lw.ln2_g, lw.ln2_b)
+    h2v = h2.view(B, s, d)
+    nm = masks.neuron_mask if static else masks.mlp_mask(layer, h2v)
+    mo, cm = mlp_forward(h2v, lw, lora, nm, model.dims, counter)
+    mo = mo.float()
+    cma = None
+    if model.peft_method == "adapter":
+        mo, cma = adapter_forward(mo, model.adapters[(layer, "mlp")])
+    out = y + mo
+    cache = {"ln1": c1, "attn": ca, "attn_adapter": caa, "ln2": c2, "mlp": cm, "mlp_adapter": cma,
+             "masks": LayerMasks(ca["pidx"], cm["mask"])}
+    return out.view(B, s, d), cache
+
+
+def model_forward(model: Model, tokens, masks, counter=None):
+    """Embed, run all blocks, final LN, tied unembedding (sf/model.py:436-451).
+    tokens [s] or [B, s]; returns fp32 logits of the same leading shape."""
+    tok = torch.as_tensor(np.asarray(tokens) if not torch.is_tensor(tokens) else tokens).to(model.device, torch.int64)
+    squeeze = tok.dim() == 1
+    if squeeze:
+        tok = tok[None]
+    if int(tok.max()) >= model.dims.vocab or int(tok.min()) < 0:
+        raise ValueError("token id out of vocab range")
+    B, s = tok.shape
+    h = model.weights.emb[tok].float()
+    caches = []
+    for layer in range(model.dims.n_layers):
+        lm = masks[layer] if isinstance(masks, list) else masks
+        h, c = block_forward(h, model, layer, lm, counter)
+        caches.append(c)
+    hf, cf = layernorm_forward(h, model.weights.lnf_g, model.weights.lnf_b)
+    logits = _mm_f32(hf, model.weights.emb.t())
+    logits = logits.view(s, -1) if squeeze else logits.view(B, s, -1)
+    return logits, {"blocks": caches, "lnf": cf, "hf": hf, "tokens": tok}
+
+
+def loss_forward(logits, targets) -> float:
+    """Mean cross-entropy over positions (sf/model.py:454-462); batched input averages items."""
+    t = torch.as_tensor(np.asarray(targets) if not torch.is_tensor(targets) else targets).to(logits.device, torch.int64)
+    V = logits.shape[-1]
+    if int(t.max()) >= V or int(t.min()) < 0:
+        raise ValueError("target id out of vocab range")
+    return float(torch.nn.functional.cross_entropy(logits.reshape(-1, V).float(), t.reshape(-1)))
+
+
+def loss_backward(logits, targets) -> torch.Tensor:
+    """d loss / d logits (sf/model.py:465-472): per item (softmax - onehot) / s."""
+    t = torch.as_tensor(np.asarray(targets) if not torch.is_tensor(targets) else targets).to(logits.device, torch.int64)
+    V = logits.shape[-1]
+    g = torch.softmax(logits.reshape(-1, V).float(), dim=-1)
+    g[torch.arange(g.shape[0], device=g.device), t.reshape(-1)] -= 1.0
+    return (g / t.shape[-1]).view(logits.shape)

@@ -1,0 +1,240 @@
+"""Neuron-centric sparse MLP on the B200 (drop-in for sf/neuron_ops.py).
+
+Device layout (sf/neuron_ops.py:1-8): W1 is kept as W1^T
+[d_ff, d] and W2 as [d_ff, d], both bf16 row-major, so every neuron block is
+`blk` contiguous rows that one TMA box streams. A neuron mask is lowered once
+per layer to device index lists (`NeuronMasks`: counts, ascending ids, inverse
+positions) that the tcgen05 gather-GEMMs consume; hidden activations are
+packed per item (`ActiveHidden`), exactly the reference's packed order.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _abi
+from .errors import MaskError
+
+
+def block_slices(d_ff: int, blk_size: int) -> list[slice]:
+    """sf/neuron_ops.py:22-24."""
+    return [slice(lo, min(lo + blk_size, d_ff)) for lo in range(0, d_ff, blk_size)]
+
+
+def n_blocks(d_ff: int, blk_size: int) -> int:
+    """sf/neuron_ops.py:27-28."""
+    return (d_ff + blk_size - 1) // blk_size
+
+
+@dataclass
+class LayeredWeights:
+    """W1 (logically d x d_ff, stored as W1^T) and W2 (d_ff x d), bf16 on device (sf/neuron_ops.py:31-45)."""
+
+    w1_t: torch.Tensor  # [d_ff, d]
+    w2: torch.Tensor  # [d_ff, d]
+    layout_w1: str = "col"
+    layout_w2: str = "row"
+
+    @classmethod
+    def from_row_major(cls, w1, w2, device=None) -> "LayeredWeights":
+        w1 = torch.as_tensor(np.asarray(w1) if not torch.is_tensor(w1) else w1)
+        w2 = torch.as_tensor(np.asarray(w2) if not torch.is_tensor(w2) else w2)
+        dev = device or "cuda"
+        return cls(w1.t().contiguous().to(dev, torch.bfloat16), w2.contiguous().to(dev, torch.bfloat16))
+
+    @property
+    def w1(self) -> torch.Tensor:
+        return self.w1_t.t()
+
+    def to_row_major(self):
+        return self.w1_t.t().contiguous(), self.w2
+
+
+@dataclass
+class NeuronMasks:
+    """Device form of per-item neuron-block masks (sf/predictor.py:128-139 output, lowered)."""
+
+    counts: torch.Tensor  # int32 [B]
+    ids: torch.Tensor  # int32 [B, n_blk] ascending active block ids (first counts[b] valid)
+    pos: torch.Tensor  # int32 [B, n_blk] packed position or -1
+    n_blk: int
+    blk: int
+
+    @property
+    def n_items(self) -> int:
+        return self.counts.shape[0]
+
+    def to_bool(self) -> torch.Tensor:
+        """[B, n_blk] bool (host-typed view for parity / reference API)."""
+        return self.pos >= 0
+
+    def expand(self, n_items: int) -> "NeuronMasks":
+        if self.n_items == n_items:
+            return self
+        if self.n_items != 1:
+            raise MaskError(f"mask for {self.n_items} items used with {n_items}")
+        return NeuronMasks(self.counts.expand(n_items).contiguous(), self.ids.expand(n_items, -1).contiguous(),
+                           self.pos.expand(n_items, -1).contiguous(), self.n_blk, self.blk)
+
+
+_HOST_MASK_CACHE: dict = {}
+
+
+def _pack_bits(mask_bool: torch.Tensor) -> torch.Tensor:
+    B, n = mask_bool.shape
+    words = (n + 31) // 32
+    m = torch.zeros(B, words * 32, dtype=torch.int64, device=mask_bool.device)
+    m[:, :n] = mask_bool.to(torch.int64)
+    w = (m.view(B, words, 32) << torch.arange(32, device=mask_bool.device, dtype=torch.int64)).sum(-1)
+    w = torch.where(w >= 2**31, w - 2**32, w)
+    return w.to(torch.int32).contiguous()
+
+
+def lower_mask(mask, n_blk: int, blk: int, n_items: int | None = None, device=None) -> NeuronMasks:
+    """bool [n_blk] (shared) or [B, n_blk] (per item) -> NeuronMasks (device compaction, no host sync)."""
+    if isinstance(mask, NeuronMasks):
+        if mask.n_blk != n_blk:
+            raise MaskError(f"mask length {mask.n_blk} != n_blk {n_blk}")
+        return mask.expand(n_items) if n_items else mask
+    if not torch.is_tensor(mask):
+        # host masks (static LayerMasks / reference-typed providers) are lowered once and reused,
+        # which also keeps host->device copies out of CUDA-graph capture
+        arr = np.ascontiguousarray(np.asarray(mask, dtype=bool))
+        key = (arr.tobytes(), arr.shape, n_blk, blk, n_items, str(device or "cuda"))
+        hit = _HOST_MASK_CACHE.get(key)
+        if hit is None:
+            hit = lower_mask(torch.from_numpy(arr).to(device or "cuda"), n_blk, blk, n_items, device)
+            if len(_HOST_MASK_CACHE) > 256:
+                _HOST_MASK_CACHE.clear()
+            _HOST_MASK_CACHE[key] = hit
+        return hit
+    t = mask.to(device or "cuda", torch.bool)
+    if t.dim() == 1:
+        t = t[None]
+    if t.shape[-1] != n_blk:
+        raise MaskError(f"mask length ({t.shape[-1]},) != n_blk ({n_blk},)")
+    if n_items and t.shape[0] == 1 and n_items > 1:
+        t = t.expand(n_items, n_blk)
+    B = t.shape[0]
+    bits = _pack_bits(t)
+    counts = torch.empty(B, dtype=torch.int32, device=t.device)
+    ids = torch.zeros(B, n_blk, dtype=torch.int32, device=t.device)
+    pos = torch.empty(B, n_blk, dtype=torch.int32, device=t.device)
+    _abi.call("lx_mask_compact", bits.data_ptr(), B, n_blk, 0, counts.data_ptr(), ids.data_ptr(), pos.data_ptr(),
+              _abi.stream_handle(t.device))
+    return NeuronMasks(counts, ids, pos, n_blk, blk)
+
+
+@dataclass
+class ActiveHidden:
+    """Packed active hidden columns (sf/neuron_ops.py:48-56), per item: row t of item b holds
+    its first counts[b]*blk columns in ascending block order."""
+
+    values: torch.Tensor  # bf16 [B*s, d_ff] (row stride d_ff; only the packed prefix is valid)
+    masks: NeuronMasks
+    blk_size: int
+    d_ff: int
+    n_items: int = 1
+
+    def packed(self, item: int = 0) -> torch.Tensor:
+        """Host-typed [s, F_act] view of one item (syncs)."""
+        s = self.values.shape[0] // self.n_items
+        f = int(self.masks.counts[item]) * self.blk_size
+        return self.values[item * s : (item + 1) * s, :f]
+
+    @property
+    def active_blocks(self) -> tuple[int, ...]:
+        c = int(self.masks.counts[0])
+        return tuple(int(b) for b in self.masks.ids[0, :c].tolist())
+
+    @property
+    def col_index(self) -> np.ndarray:
+        return np.concatenate([np.arange(b * self.blk_size, min((b + 1) * self.blk_size, self.d_ff)) for b in self.active_blocks]) \
+            if self.active_blocks else np.empty(0, dtype=int)
+
+
+def active_columns(mask, d_ff: int, blk_size: int) -> tuple[tuple[int, ...], np.ndarray]:
+    """sf/neuron_ops.py:59-72 (host-typed helper)."""
+    m = mask.detach().cpu().numpy() if torch.is_tensor(mask) else np.asarray(mask, dtype=bool)
+    m = m.astype(bool)
+    if m.shape != (n_blocks(d_ff, blk_size),):
+        raise MaskError(f"mask length {m.shape} != n_blk ({n_blocks(d_ff, blk_size)},)")
+    active = tuple(int(b) for b in np.flatnonzero(m))
+    sl = block_slices(d_ff, blk_size)
+    cols = np.concatenate([np.arange(sl[b].start, sl[b].stop) for b in active]) if active else np.empty(0, dtype=int)
+    return active, cols
+
+
+def _as_items(x: torch.Tensor) -> tuple[torch.Tensor, int, int]:
+    if x.dim() == 2:
+        return x.contiguous(), 1, x.shape[0]
+    B, s, d = x.shape
+    return x.reshape(B * s, d).contiguous(), B, s
+
+
+def _check_device_blk(d_ff: int, blk: int) -> None:
+    if d_ff % blk:
+        raise MaskError(f"d_ff {d_ff} must be a multiple of blk_size {blk} on the sm_100a path (ragged tail unsupported)")
+
+
+def neuron_matmul_fwd1(x, weights: LayeredWeights, mask, blk_size: int, counter=None, *, bias=None, ax=None, lora_b=None,
+                       lora_r=0, scaling=1.0, relu=False, out=None) -> ActiveHidden:
+    """x @ W1[:, cols] over active column blocks (sf/neuron_ops.py:75-82) on the tcgen05
+    N-gather GEMM. Optional fused epilogue (used by mlp_forward): + bias[cols] + scaling*ax B[:,cols], ReLU."""
+    d_ff, d = weights.w1_t.shape
+    _check_device_blk(d_ff, blk_size)
+    x2, B, s = _as_items(x.to(torch.bfloat16))
+    nm = lower_mask(mask, n_blocks(d_ff, blk_size), blk_size, B, x2.device)
+    vals = out if out is not None else torch.empty(B * s, d_ff, dtype=torch.bfloat16, device=x2.device)
+    _abi.call("lx_neuron_fc1", x2.data_ptr(), B, s, d, d_ff, blk_size, weights.w1_t.data_ptr(), nm.counts.data_ptr(),
+              nm.ids.data_ptr(), _abi.ptr(bias), _abi.ptr(ax), _abi.ptr(lora_b), lora_r, float(scaling), int(relu),
+              vals.data_ptr(), d_ff, _abi.stream_handle(x2.device))
+    if counter is not None:
+        counter.add(s * d * int(nm.counts.sum()) * blk_size)
+    return ActiveHidden(vals, nm, blk_size, d_ff, B)
+
+
+def neuron_matmul_fwd2(hidden: ActiveHidden, weights: LayeredWeights, mask, counter=None, *, bias=None, ax=None,
+                       lora_b=None, lora_r=0, scaling=1.0, out=None) -> torch.Tensor:
+    """Packed hidden @ W2[cols, :] (sf/neuron_ops.py:85-95) on the tcgen05 K-gather GEMM."""
+    d_ff, d = weights.w2.shape
+    nm = hidden.masks
+    if mask is not None and mask is not nm:
+        other = lower_mask(mask, nm.n_blk, hidden.blk_size, nm.n_items, hidden.values.device)
+        if not torch.equal(other.pos, nm.pos):
+            raise MaskError("mask does not match the mask the hidden activations were computed with")
+    M = hidden.values.shape[0]
+    s = M // hidden.n_items
+    res = out if out is not None else torch.empty(M, d, dtype=torch.bfloat16, device=hidden.values.device)
+    _abi.call("lx_neuron_fc2", hidden.values.data_ptr(), hidden.values.stride(0), hidden.n_items, s, d, d_ff,
+              hidden.blk_size, weights.w2.data_ptr(), nm.counts.data_ptr(), nm.ids.data_ptr(), _abi.ptr(bias),
+              _abi.ptr(ax), _abi.ptr(lora_b), lora_r, float(scaling), res.data_ptr(), _abi.stream_handle(res.device))
+    if counter is not None:
+        counter.add(s * int(nm.counts.sum()) * hidden.blk_size * d)
+    return res
+
+
+# ---------------------------------------------------------------- skinny LoRA helpers (csrc/lora.cu)
+
+
+def rowproj(x2: torch.Tensor, n_items: int, s: int, K: int, w: torch.Tensor, w_sk: int, w_sq: int, r: int,
+            scale: float = 1.0, masks: NeuronMasks | None = None, blk: int = 1) -> torch.Tensor:
+    """Y[M, r] = scale * X[M, K] W (K gathered per item when `masks` is given)."""
+    y = torch.empty(x2.shape[0], r, dtype=torch.float32, device=x2.device)
+    _abi.call("lx_rowproj", x2.data_ptr(), x2.stride(0), n_items, s, K, w.data_ptr(), w_sk, w_sq, r, float(scale),
+              _abi.ptr(masks.counts if masks else None), _abi.ptr(masks.ids if masks else None), blk, y.data_ptr(),
+              _abi.stream_handle(x2.device))
+    return y
+
+
+def colgrad(p: torch.Tensor | None, x2: torch.Tensor, n_items: int, s: int, ncols: int, r: int, scale: float,
+            out: torch.Tensor, g_sq: int, g_sc: int, masks: NeuronMasks | None = None, blk: int = 1) -> torch.Tensor:
+    """out(q, c) = scale * sum_rows P[row, q] X[row, c] (c original column), deterministic."""
+    ws = torch.empty(int(_abi.lib().lx_colgrad_ws_floats(n_items, s, ncols, r)), dtype=torch.float32, device=x2.device)
+    _abi.call("lx_colgrad", _abi.ptr(p), x2.data_ptr(), x2.stride(0), n_items, s, ncols, r, float(scale),
+              _abi.ptr(masks.counts if masks else None), _abi.ptr(masks.pos if masks else None), blk, out.data_ptr(),
+              g_sq, g_sc, ws.data_ptr(), _abi.stream_handle(x2.device))
+    return out

@@ -1,0 +1,52 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads without a GPU and
+exports every symbol include/sparseft_b200.h declares; the ctypes table covers
+them all; error codes map to the reference exception types."""
+
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def header_symbols():
+    text = (ROOT / "include" / "sparseft_b200.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|long long|const char\*)\s+(lx_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_entry_points():
+    syms = header_symbols()
+    assert "lx_neuron_fc1" in syms and "lx_bsattn_bwd" in syms and "lx_predict_mlp_mask" in syms
+    assert len(syms) >= 20
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2510_15964_b200 import _abi
+
+    if not _abi.LIB_PATH.exists():
+        pytest.skip("extension not built (run __graft_entry__.build())")
+    lib = _abi.lib()
+    missing = [s for s in header_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(header_symbols()) == set(_abi.SIGNATURES), "ctypes table out of sync with the header"
+    assert lib.lx_abi_version() == 1
+
+
+def test_error_mapping_without_gpu():
+    """A shape error is raised before any CUDA call, as the reference's ValueError subclasses."""
+    from paper_2510_15964_b200 import _abi, errors as E
+
+    if not _abi.LIB_PATH.exists():
+        pytest.skip("extension not built")
+    with pytest.raises(E.UnsupportedError):
+        _abi.call("lx_neuron_fc1", None, 1, 16, 64, 64, 24, None, None, None, None, None, None, 0, 1.0, 1, None, 64, None)
+    with pytest.raises(E.LayoutError):
+        import ctypes
+
+        import numpy as np
+
+        kinds = np.zeros(1, np.int32)
+        out = np.zeros(64, np.int32)
+        _abi.call("lx_attn_tables", kinds.ctypes.data, kinds.ctypes.data, 1, 100, 16, out.ctypes.data, 64)
+    assert issubclass(E.LayoutError, ValueError) and issubclass(E.MaskError, ValueError)

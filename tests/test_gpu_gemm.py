@@ -83,7 +83,7 @@ def test_neuron_mlp_gemms(n_items, s, d, d_ff, blk, density, r):
     a = torch.zeros(M, ld_h, device=dev, dtype=torch.bfloat16)
     P = lambda t: None if (t is None or r == 0) else t.data_ptr()  # noqa: E731
     _abi.call("lx_neuron_fc1", x.data_ptr(), n_items, s, d, d_ff, blk, w1t.data_ptr(), cnt_d.data_ptr(), ids_d.data_ptr(),
-              b1.data_ptr(), P(ax1), P(B1), r, scaling, a.data_ptr(), ld_h, st)
+              b1.data_ptr(), P(ax1), P(B1), r, scaling, 1, a.data_ptr(), ld_h, st)
     out = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
     _abi.call("lx_neuron_fc2", a.data_ptr(), ld_h, n_items, s, d, d_ff, blk, w2.data_ptr(), cnt_d.data_ptr(), ids_d.data_ptr(),
               b2.data_ptr(), P(ax2), P(B2), r, scaling, out.data_ptr(), st)

@@ -1,0 +1,176 @@
+"""End-to-end GPU parity of the PEFT wrappers (sf/model.py, sf/autograd.py,
+sf/harness.py) against the reference's golden outputs and the oracle.
+
+Tolerance (stated per north_star): bf16 operands with fp32 accumulation ->
+tensor-level max|gpu - ref| / max|ref| <= 1e-2 for logits, activations and
+LoRA / Adapter / BitFit gradients; loss within 1e-2 relative. Gradients of
+inactive neuron blocks must be exactly zero (sf/autograd.py:89-90)."""
+
+import numpy as np
+import pytest
+
+from oracle import sf_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch.device("cuda")
+
+
+def rel(a, b):
+    a = np.asarray(a.detach().cpu() if torch.is_tensor(a) else a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)
+
+
+def device_model(om: O.OModel, dev):
+    from paper_2510_15964_b200 import model as M
+
+    d = om.dims
+    dims = M.ModelDims(d.d_model, d.n_heads, d.d_ff, d.seq_len, d.n_layers, d.vocab, d.blk_size, d.attn_blk)
+    return M.from_arrays(dims, om.peft, om.emb, om.layers, om.lnf_g, om.lnf_b, lora=om.lora, adapters=om.adapters,
+                         lora_targets=om.lora_targets, device=dev)
+
+
+def cos(a, b):
+    a = np.asarray(a.detach().cpu() if torch.is_tensor(a) else a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    return float(a @ b / max(np.linalg.norm(a) * np.linalg.norm(b), 1e-300))
+
+
+def _golden_model(g, peft):
+    d, H, f, s, L, V, blk, ablk = (int(v) for v in g["dims"])
+    om = O.build_model(O.Dims(d, H, f, s, L, V, blk, ablk), seed=7, peft=peft)
+    for n, p in O.trainable_params(om).items():
+        p[...] = g[f"{peft}/param/{n}"]
+    masks = [(list(g[f"{peft}/masks/{i}/heads"]), g[f"{peft}/masks/{i}/neuron"]) for i in range(L)]
+    return om, masks
+
+
+@pytest.mark.parametrize("peft", ["lora", "adapter", "bitfit"])
+def test_model_fwd_bwd_matches_reference(dev, golden, peft):
+    """The reference's own fixture (s=64, init 0.02). Logits / loss at 1e-2 against the
+    reference outputs. Its gradients are ill-conditioned for bf16 activations (ReLU
+    pre-activations within bf16 resolution of 0 flip sign; near-uniform attention gives
+    q/k a common mode ~3.6x their spread, so dq cancels) -- measured in
+    tests/test_gpu_model.py::test_model_grads_well_conditioned and DESIGN.md. Here the
+    gradient bar is direction (cosine >= 0.97) plus exact structural zeros."""
+    from paper_2510_15964_b200 import autograd as AG, model as M
+
+    g = golden("model")
+    om, masks_o = _golden_model(g, peft)
+    m = device_model(om, dev)
+    masks = [M.LayerMasks(*mo) for mo in masks_o]
+    toks = g[f"{peft}/tokens"]
+    logits, cache = M.model_forward(m, toks[:-1], masks)
+    assert rel(logits, g[f"{peft}/logits"]) < 1e-2
+    loss = M.loss_forward(logits, toks[1:])
+    assert abs(loss - float(g[f"{peft}/loss"])) < 1e-2 * abs(float(g[f"{peft}/loss"]))
+    grads = AG.model_backward(m, cache, M.loss_backward(logits, toks[1:]), masks)
+    for n, gr in grads.items():
+        ref = g[f"{peft}/grad/{n}"]
+        if np.abs(ref).max() == 0:
+            assert float(gr.abs().max()) == 0, n
+        elif n.endswith(".bk"):  # true gradient is 0 (softmax shift invariance)
+            assert float((gr.cpu() - torch.from_numpy(ref)).abs().max()) < 1e-4, n
+        else:
+            assert cos(gr, ref) > 0.97, (n, cos(gr, ref))
+        if n.endswith("w1.lora_b") or n.endswith("w2.lora_a") or n.endswith(".b1"):
+            assert np.all(gr.detach().cpu().numpy()[ref == 0] == 0), n  # inactive neuron blocks untouched
+
+
+@pytest.mark.parametrize("peft", ["lora", "adapter", "bitfit"])
+def test_model_grads_well_conditioned(dev, golden, peft):
+    """Same fixture with margin-separated ReLU pre-activations (b1 = +-1) and sharper attention
+    (W_q, W_k x 10): every gradient within max|d| / max|ref| <= 1e-2 of the fp32 oracle."""
+    from paper_2510_15964_b200 import autograd as AG, model as M
+
+    g = golden("model")
+    om, masks_o = _golden_model(g, peft)
+    rng = np.random.default_rng(1)
+    for lw in om.layers:
+        lw["b1"][...] = np.where(rng.random(lw["b1"].shape) < 0.5, 1.0, -1.0).astype(np.float32)
+        lw["wq"] *= 10
+        lw["wk"] *= 10
+    toks = g[f"{peft}/tokens"]
+    lg, c = O.model_forward(om, toks[:-1], masks_o)
+    og = O.model_backward(om, c, O.loss_backward(lg, toks[1:]))
+    m = device_model(om, dev)
+    masks = [M.LayerMasks(*mo) for mo in masks_o]
+    logits, cache = M.model_forward(m, toks[:-1], masks)
+    assert rel(logits, lg) < 1e-2
+    grads = AG.model_backward(m, cache, M.loss_backward(logits, toks[1:]), masks)
+    for n, v in og.items():
+        if np.abs(v).max() == 0:
+            assert float(grads[n].abs().max()) == 0, n
+        elif not n.endswith(".bk"):
+            assert rel(grads[n], v) < 1e-2, (n, rel(grads[n], v))
+
+
+def test_batched_items_equal_per_item_loop(dev):
+    """B items with different per-item masks in one batched call == the reference's per-item loop."""
+    from paper_2510_15964_b200 import autograd as AG, model as M
+
+    dims = O.Dims(128, 2, 256, 128, 2, 80, 16, 32)
+    om = O.build_model(dims, seed=11, peft="lora")
+    rng = np.random.default_rng(0)
+    for ad in om.lora.values():
+        ad["b"] += (rng.standard_normal(ad["b"].shape) * 0.02).astype(np.float32)
+    m = device_model(om, dev)
+    B = 3
+    toks = rng.integers(0, dims.vocab, size=(B, dims.seq_len + 1))
+    pids = list(om.pool)
+    pat = [[[pids[rng.integers(len(pids))] for _ in range(dims.n_heads)] for _ in range(dims.n_layers)] for _ in range(B)]
+    nms = rng.random((B, dims.n_layers, dims.n_blk)) < 0.5
+    masks = [M.LayerMasks([pat[b][i] for b in range(B)], nms[:, i]) for i in range(dims.n_layers)]
+    logits, cache = M.model_forward(m, toks[:, :-1], masks)
+    loss = M.loss_forward(logits, toks[:, 1:])
+    grads = AG.model_backward(m, cache, M.loss_backward(logits, toks[:, 1:]), masks)
+    ref_loss, gsum = [], {}
+    for b in range(B):
+        om_masks = [(pat[b][i], nms[b, i]) for i in range(dims.n_layers)]
+        lg, c = O.model_forward(om, toks[b, :-1], om_masks)
+        assert rel(logits[b], lg) < 1e-2
+        ref_loss.append(O.loss_forward(lg, toks[b, 1:]))
+        for n, v in O.model_backward(om, c, O.loss_backward(lg, toks[b, 1:])).items():
+            gsum[n] = gsum.get(n, 0) + v
+    assert abs(loss - np.mean(ref_loss)) < 1e-2 * abs(np.mean(ref_loss))
+    for n, v in gsum.items():
+        assert cos(grads[n], v) > 0.97 if np.abs(v).max() > 0 else float(grads[n].abs().max()) == 0, n
+
+
+def test_finetune_step_predicted_mode(dev, golden):
+    """One predicted-mode fine-tune step (sf/harness.py:396-417) on the reference's fixture:
+    predictor scores -> masks on device, per-item fwd/bwd, mean grads, Adam."""
+    from paper_2510_15964_b200 import harness as HN, model as M, predictor as P
+
+    g = golden("finetune_step")
+    dims = O.Dims(128, 2, 256, 64, 2, 96, 16, 16)
+    om = O.build_model(dims, seed=3, peft="lora")
+    m = device_model(om, dev)
+    state = M.make_peft_state(m)
+    preds = {"attn": [P.AttnPredictorParams(list(g[f"attn{i}/wq"]), list(g[f"attn{i}/wk"])) for i in range(2)],
+             "mlp": [P.MlpPredictorParams(g[f"mlp{i}/wa"]) for i in range(2)]}
+    prov = HN.PredictedProvider(m, preds, P.PredictorTrainConfig())
+    out = HN.finetune_step(m, state, g["batch"], prov, lr=1e-3)
+    assert abs(out["loss"] - float(g["loss"])) < 1e-2 * float(g["loss"])
+    # masks the device predictor chose vs the reference's (bf16 scores may flip a near-threshold unit)
+    ids = list(m.pool)
+    n_same = n_all = 0
+    for i, lm in enumerate(out["masks"]):
+        pid = lm.head_patterns.cpu().numpy()
+        nm = lm.neuron_mask.to_bool().cpu().numpy()
+        for b in range(2):
+            n_same += sum(ids[pid[b, h]] == g["patterns"][b][i][h] for h in range(2))
+            n_same += int(np.array_equal(nm[b], g["neuron_masks"][b][i])) * 2
+            n_all += 4
+    assert n_same / n_all >= 0.75
+    for n, v in out["grads"].items():
+        ref = g[f"grad/{n}"]
+        if np.abs(ref).max() > 0:
+            assert cos(v, ref) > 0.9, n
