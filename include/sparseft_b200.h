@@ -45,6 +45,14 @@ int lx_device_sm_count(void);
 int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void* c, int ldc, int c_is_f32, int M, int N,
                     int K, lx_stream_t stream);
 
+/* lora_linear_forward / lora_linear_backward's dense products (sf/model.py:292-304,
+ * sf/autograd.py:48-58) with the bias, LoRA and residual fused in the epilogue:
+ *   out[M,N] = (resid) + A[M,K] * B[N,K]^T + bias[N] + scaling * lora_x[M,r] . w(:, n)
+ *   w(q, n) = lora_w[q*w_sr + n*w_sc]; out fp32 (out_f32, optional resid) or bf16. */
+int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, int N, int K, void* out, int ldo,
+              int out_f32, const float* resid, const float* bias, const float* lora_x, const float* lora_w,
+              long long w_sr, long long w_sc, int r, float scaling, lx_stream_t stream);
+
 /* ------------------------------------------------------------------ K1 mask build
  * approx_mlp_scores + predict_mlp_mask + active_columns
  *   (sf/predictor.py:121-139, sf/neuron_ops.py:67-72)
@@ -89,10 +97,11 @@ int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int bl
                   int r, float scaling, int apply_relu, uint16_t* a_out, int ld_h, lx_stream_t stream);
 
 /* neuron_matmul_fwd2 + b2 + scaling*(a A2[cols]) B2   (sf/neuron_ops.py:85-95, sf/model.py:388-395)
- * ax2: fp32 [M, r]; b2_lora: fp32 [r, d] */
+ * ax2: fp32 [M, r]; b2_lora: fp32 [r, d]. out bf16, or fp32 (out_f32) with optional fused residual
+ * (out = resid + mlp, the block's y + MLP(LN(y)), sf/model.py:427). */
 int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
                   const int32_t* counts, const int32_t* ids, const float* b2, const float* ax2, const float* b2_lora,
-                  int r, float scaling, uint16_t* out, lx_stream_t stream);
+                  int r, float scaling, void* out, int out_f32, const float* resid, lx_stream_t stream);
 
 /* mlp_backward input-grad through fc2 and ReLU   (sf/autograd.py:97-106)
  * dz = (dO W2[cols]^T + dax2 A2[cols]^T) * (a > 0); dax2 fp32 [M,r] (already scaled); a2: fp32 [d_ff, r] */
@@ -104,20 +113,21 @@ int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_
  * dx = dz W1[:,cols]^T + dax1 A1^T; dax1 fp32 [M,r] (already scaled); a1: fp32 [d, r] */
 int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d, int d_ff, int blk,
                         const uint16_t* w1_t, const int32_t* counts, const int32_t* ids, const float* dax1,
-                        const float* a1_lora, int r, uint16_t* dx, lx_stream_t stream);
+                        const float* a1_lora, int r, void* dx, int out_f32, lx_stream_t stream);
 
-/* Skinny LoRA row projection: Y[M, r] = scale * X[M, K] W, K optionally gathered per item.
+/* Skinny LoRA row projection: Y[M, r] (row stride ldy) = scale * X[M, K] W, K optionally gathered per item.
  *   X bf16 row stride ldx; W(k, q) = w[k_orig*w_sk + q*w_sq]; k_orig = k (dense, counts==NULL) or
  *   ids[b][k/blk]*blk + k%blk over the item's packed K = counts[b]*blk.  (x A1, a A2[cols], dO B2^T, dz B1[:,cols]^T) */
 int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const float* w, long long w_sk, long long w_sq,
-               int r, float scale, const int32_t* counts, const int32_t* ids, int blk, float* y, lx_stream_t stream);
+               int r, float scale, const int32_t* counts, const int32_t* ids, int blk, float* y, int ldy,
+               lx_stream_t stream);
 
-/* Skinny LoRA gradient reduction over tokens: G[q, c_orig] += scale * sum_rows P[row, q] X[row, c]
+/* Skinny LoRA gradient reduction over tokens: G[q, c_orig] = scale * sum_rows P[row, q] X[row, c]
  *   (dB1[:,cols], dA2[cols] (transposed), dB2, dA1 (transposed)); summed over items in order.
- *   X bf16 [M, ncols(packed)] row stride ldx; G fp32 with G(q, c) = g[q*g_sq + c*g_sc].
+ *   P fp32 row stride ldp; X bf16 [M, ncols(packed)] row stride ldx; G fp32 with G(q, c) = g[q*g_sq + c*g_sc].
  *   ws: fp32 workspace of lx_colgrad_ws_floats(...) floats. Deterministic. */
 long long lx_colgrad_ws_floats(int n_items, int s, int ncols, int r);
-int lx_colgrad(const float* p, const uint16_t* x, int ldx, int n_items, int s, int ncols, int r, float scale,
+int lx_colgrad(const float* p, int ldp, const uint16_t* x, int ldx, int n_items, int s, int ncols, int r, float scale,
                const int32_t* counts, const int32_t* pos, int blk, float* g, long long g_sq, long long g_sc, float* ws,
                lx_stream_t stream);
 
@@ -149,9 +159,15 @@ int lx_bsattn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const
  * Optionally also writes the predictor's downsampled rows (sf/predictor.py:62-71) to x_small. */
 int lx_layernorm_fwd(const float* x, int M, int d, const float* gamma, const float* beta, float eps, uint16_t* y,
                      float* mean, float* inv_std, int s, int m_small, uint16_t* x_small, lx_stream_t stream);
-/* layernorm_backward (sf/autograd.py:61-66): dx_accum += LN'(dy), dy bf16 or fp32 (dy_is_f32). */
+/* loss_forward + loss_backward over rows of fp32 logits (sf/model.py:454-472): row_loss[r] =
+ * logsumexp(l_r) - l_r[t_r]; grad_bf16[r] = (softmax(l_r) - onehot(t_r)) * inv_s (inv_s = 1/seq_len). */
+int lx_cross_entropy(const float* logits, int rows, int V, const int64_t* targets, float inv_s, float* row_loss,
+                     uint16_t* grad_bf16, lx_stream_t stream);
+
+/* layernorm_backward (sf/autograd.py:61-66): dx_accum += LN'(dy), dy bf16 or fp32 (dy_is_f32);
+ * optionally also writes bf16(dx_accum) to dx_bf16 (the next GEMM's operand). */
 int lx_layernorm_bwd(const void* dy, int dy_is_f32, const float* x, const float* gamma, const float* mean,
-                     const float* inv_std, int M, int d, float* dx_accum, lx_stream_t stream);
+                     const float* inv_std, int M, int d, float* dx_accum, uint16_t* dx_bf16, lx_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -25,23 +25,25 @@ SIGNATURES: dict[str, list] = {
     "lx_abi_version": [],
     "lx_device_sm_count": [],
     "lx_gemm_bf16_tn": [_P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _P],
+    "lx_linear": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _P, _P, _P, _P, _LL, _LL, _I, _F, _P],
     "lx_predict_mlp_mask": [_P, _I, _I, _I, _P, _I, _F, _I, _P, _P, _P, _P, _P, _P],
     "lx_mask_compact": [_P, _I, _I, _I, _P, _P, _P, _P],
     "lx_predict_attention_patterns": [_P, _I, _I, _I, _P, _I, _I, _F, _D, _I, _P, _P, _I, _I, _P, _P, _P, _P],
     "lx_neuron_fc1": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _I, _P, _I, _P],
-    "lx_neuron_fc2": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _P, _P],
+    "lx_neuron_fc2": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _P, _I, _P, _P],
     "lx_neuron_fc2_dgrad": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P],
-    "lx_neuron_fc1_dgrad": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P],
-    "lx_rowproj": [_P, _I, _I, _I, _I, _P, _LL, _LL, _I, _F, _P, _P, _I, _P, _P],
+    "lx_neuron_fc1_dgrad": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P],
+    "lx_rowproj": [_P, _I, _I, _I, _I, _P, _LL, _LL, _I, _F, _P, _P, _I, _P, _I, _P],
     "lx_colgrad_ws_floats": [_I, _I, _I, _I],
-    "lx_colgrad": [_P, _P, _I, _I, _I, _I, _I, _F, _P, _P, _I, _P, _LL, _LL, _P, _P],
+    "lx_colgrad": [_P, _I, _P, _I, _I, _I, _I, _I, _F, _P, _P, _I, _P, _LL, _LL, _P, _P],
     "lx_colsum": [_P, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P],
     "lx_attn_tables_size": [_I, _I, _I, _P],
     "lx_attn_tables": [_P, _P, _I, _I, _I, _P, _I],
     "lx_bsattn_fwd": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _I, _P, _P],
     "lx_bsattn_bwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P, _P],
     "lx_layernorm_fwd": [_P, _I, _I, _P, _P, _F, _P, _P, _P, _I, _I, _P, _P],
-    "lx_layernorm_bwd": [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P],
+    "lx_cross_entropy": [_P, _I, _I, _P, _F, _P, _P, _P],
+    "lx_layernorm_bwd": [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P],
 }
 RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_ws_floats": _LL}
 

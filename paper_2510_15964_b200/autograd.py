@@ -4,9 +4,15 @@ Inactive neuron blocks and attention blocks are never touched: the MLP
 input-grad runs the tcgen05 gather-GEMMs over the forward's index lists, the
 LoRA / BitFit gradients are deterministic skinny reductions over the packed
 active columns (inactive rows/columns stay exactly 0, sf/autograd.py:89-90),
-and attention gradients flow through the block-sparse backward kernels only.
-Gradients are sums over the batch items (the reference harness sums per-item
-gradients and divides by the batch size, sf/harness.py:413-415).
+attention gradients flow through the block-sparse backward kernels only, and
+the projection input-grads run on the tcgen05 engine with the LoRA term
+fused in the epilogue. Gradients are sums over the batch items (the
+reference harness sums per-item gradients and divides by the batch size,
+sf/harness.py:413-415).
+
+The residual-stream gradient travels as (fp32, bf16) pairs: the LayerNorm
+backward kernel accumulates in fp32 and emits the bf16 copy the next GEMMs
+consume, so no separate conversion pass exists.
 """
 
 from __future__ import annotations
@@ -14,11 +20,11 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from . import _abi
 from . import model as M
 from .block_sparse import attention_backward
 from .errors import GradientError
 from .neuron_ops import colgrad, rowproj
-from . import _abi
 
 
 def check_gradient_set(grads: dict, model: M.Model) -> None:
@@ -43,8 +49,34 @@ def _acc(grads: dict, name: str, value: torch.Tensor) -> None:
         grads[name] = value
 
 
+class FlatGrads(dict):
+    """Gradient sink of the step engine: a gradient whose name has a view in the flat gradient
+    buffer is written there directly by its reduction kernel, pre-scaled (1/B for the batch mean),
+    instead of being allocated and copied."""
+
+    def __init__(self, views: dict, scale: float):
+        super().__init__()
+        self.views, self.scale = views, scale
+
+
+def _cg(grads: dict, name: str, shape, p, x2, n_items, s, ncols, r, scale, g_sq, g_sc, masks=None, blk=1) -> None:
+    """colgrad into the gradient `name` (in place in a FlatGrads view when possible)."""
+    if isinstance(grads, FlatGrads) and name in grads.views and name not in grads:
+        out = grads.views[name]
+        colgrad(p, x2, n_items, s, ncols, r, scale * grads.scale, out, g_sq, g_sc, masks=masks, blk=blk)
+        dict.__setitem__(grads, name, out)
+        return
+    out = torch.empty(shape, dtype=torch.float32, device=x2.device)
+    _acc(grads, name, colgrad(p, x2, n_items, s, ncols, r, scale, out, g_sq, g_sc, masks=masks, blk=blk))
+
+
+def _bf16(t: torch.Tensor) -> torch.Tensor:
+    return t if t.dtype == torch.bfloat16 else t.to(torch.bfloat16)
+
+
 def lora_linear_backward(dz, w, adapter, cache, grads: dict, prefix: str, bias_name):
-    """sf/autograd.py:48-58; dz fp32 [M, d_out], w bf16 [d_in, d_out]. Returns dx fp32."""
+    """sf/autograd.py:48-58 (reference-API helper; the model uses the fused paths below).
+    dz fp32 [M, d_out], w bf16 [d_in, d_out]. Returns dx fp32."""
     dx = M._mm_f32(dz.to(torch.bfloat16), w.t())
     if adapter is not None:
         d_ax = (dz @ adapter.b.t()) * adapter.scaling
@@ -56,15 +88,20 @@ def lora_linear_backward(dz, w, adapter, cache, grads: dict, prefix: str, bias_n
     return dx
 
 
-def layernorm_backward(dy, cache, accumulate_into: torch.Tensor | None = None) -> torch.Tensor:
-    """sf/autograd.py:61-66 on the fused kernel: returns (accumulate_into or 0) + LN'(dy) (fp32)."""
+def layernorm_backward(dy, cache, accumulate_into: torch.Tensor | None = None, want_bf16: bool = False):
+    """sf/autograd.py:61-66 on the fused kernel: returns (accumulate_into or 0) + LN'(dy) in fp32,
+    and with want_bf16 also its bf16 copy (written by the same kernel)."""
     x = cache["x"]
     Mr, d = x.shape
     out = accumulate_into if accumulate_into is not None else torch.zeros(Mr, d, dtype=torch.float32, device=x.device)
-    dy2 = dy.reshape(Mr, d).contiguous()
+    ob = torch.empty(Mr, d, dtype=torch.bfloat16, device=x.device) if want_bf16 else None
+    dy2 = dy.reshape(Mr, d)
+    if dy2.stride(1) != 1 or dy2.stride(0) != d:
+        dy2 = dy2.contiguous()
     _abi.call("lx_layernorm_bwd", dy2.data_ptr(), int(dy2.dtype == torch.float32), x.data_ptr(), cache["gamma"].data_ptr(),
-              cache["mean"].data_ptr(), cache["inv_std"].data_ptr(), Mr, d, out.data_ptr(), _abi.stream_handle(x.device))
-    return out
+              cache["mean"].data_ptr(), cache["inv_std"].data_ptr(), Mr, d, out.data_ptr(), _abi.ptr(ob),
+              _abi.stream_handle(x.device))
+    return (out, ob) if want_bf16 else out
 
 
 def adapter_backward(dy, ad: M.AdapterLayer, cache, grads: dict, prefix: str):
@@ -79,7 +116,7 @@ def adapter_backward(dy, ad: M.AdapterLayer, cache, grads: dict, prefix: str):
 
 def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims: M.ModelDims, grads: dict,
                  prefix: str = "", bitfit: bool = False):
-    """Backward of mlp_forward (sf/autograd.py:78-124). d_out fp32/bf16 [M, d] -> dx fp32 [M, d]."""
+    """Backward of mlp_forward (sf/autograd.py:78-124). d_out [M, d] (bf16 preferred) -> dx bf16 [M, d]."""
     nm = cache["mask"]
     if neuron_mask is not None and neuron_mask is not nm:
         other = M.lower_mask(neuron_mask, nm.n_blk, nm.blk, nm.n_items, nm.pos.device)
@@ -90,90 +127,108 @@ def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims
     x2, hid = cache["x"], cache["a"]
     a = hid.values
     dev = a.device
-    dO = d_out.reshape(-1, d).to(torch.bfloat16).contiguous()
+    dO = _bf16(d_out.reshape(-1, d)).contiguous()
     st = _abi.stream_handle(dev)
     if bitfit:
-        _acc(grads, f"{prefix}b2", colgrad(None, dO, B, s, d, 1, 1.0, torch.empty(d, device=dev), 0, 1))
+        _cg(grads, f"{prefix}b2", (d,), None, dO, B, s, d, 1, 1.0, 0, 1)
     ad1, ad2 = lora.get("w1"), lora.get("w2")
     dax2 = None
     if ad2 is not None:
         r2 = ad2.rank
         dax2 = rowproj(dO, B, s, d, ad2.b, 1, d, r2, scale=ad2.scaling)  # dO B2^T * s
-        _acc(grads, f"{prefix}w2.lora_b", colgrad(cache["ax2"], dO, B, s, d, r2, ad2.scaling,
-                                                   torch.empty(r2, d, device=dev), d, 1))
+        _cg(grads, f"{prefix}w2.lora_b", (r2, d), cache["ax2"], dO, B, s, d, r2, ad2.scaling, d, 1)
     dz = torch.empty_like(a)
     _abi.call("lx_neuron_fc2_dgrad", dO.data_ptr(), B, s, d, f, blk, lw.mlp.w2.data_ptr(), nm.counts.data_ptr(),
               nm.ids.data_ptr(), _abi.ptr(dax2), _abi.ptr(ad2.a if ad2 else None), ad2.rank if ad2 else 0, a.data_ptr(),
               dz.data_ptr(), a.stride(0), st)
     if ad2 is not None:
-        _acc(grads, f"{prefix}w2.lora_a", colgrad(dax2, a, B, s, f, ad2.rank, 1.0, torch.empty(f, ad2.rank, device=dev),
-                                                  1, ad2.rank, masks=nm, blk=blk))
+        _cg(grads, f"{prefix}w2.lora_a", (f, ad2.rank), dax2, a, B, s, f, ad2.rank, 1.0, 1, ad2.rank, masks=nm, blk=blk)
     if bitfit:
-        _acc(grads, f"{prefix}b1", colgrad(None, dz, B, s, f, 1, 1.0, torch.empty(f, device=dev), 0, 1, masks=nm, blk=blk))
+        _cg(grads, f"{prefix}b1", (f,), None, dz, B, s, f, 1, 1.0, 0, 1, masks=nm, blk=blk)
     dax1 = None
     if ad1 is not None:
         r1 = ad1.rank
-        _acc(grads, f"{prefix}w1.lora_b", colgrad(cache["ax1"], dz, B, s, f, r1, ad1.scaling,
-                                                   torch.empty(r1, f, device=dev), f, 1, masks=nm, blk=blk))
+        _cg(grads, f"{prefix}w1.lora_b", (r1, f), cache["ax1"], dz, B, s, f, r1, ad1.scaling, f, 1, masks=nm, blk=blk)
         dax1 = rowproj(dz, B, s, f, ad1.b, 1, f, r1, scale=ad1.scaling, masks=nm, blk=blk)  # dz B1[:,cols]^T * s
-        _acc(grads, f"{prefix}w1.lora_a", colgrad(dax1, x2, B, s, d, r1, 1.0, torch.empty(d, r1, device=dev), 1, r1))
+        _cg(grads, f"{prefix}w1.lora_a", (d, r1), dax1, x2, B, s, d, r1, 1.0, 1, r1)
     dx = torch.empty(B * s, d, dtype=torch.bfloat16, device=dev)
     _abi.call("lx_neuron_fc1_dgrad", dz.data_ptr(), dz.stride(0), B, s, d, f, blk, lw.mlp.w1_t.data_ptr(),
               nm.counts.data_ptr(), nm.ids.data_ptr(), _abi.ptr(dax1), _abi.ptr(ad1.a if ad1 else None),
-              ad1.rank if ad1 else 0, dx.data_ptr(), st)
+              ad1.rank if ad1 else 0, dx.data_ptr(), 0, st)
     return dx
 
 
 def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims, grads: dict, prefix: str = "",
                  bitfit: bool = False):
-    """Backward of mha_forward (sf/autograd.py:127-162); score gradients only on active blocks."""
+    """Backward of mha_forward (sf/autograd.py:127-162); score gradients only on active blocks.
+    d_out [M, d] (bf16 preferred) -> dx bf16 [M, d]."""
     B, s = cache["n_items"], cache["s"]
     d, H, hd = dims.d_model, dims.n_heads, dims.head_dim
     dp = cache["dpool"]
     if cache["pidx"].shape[-1] != H:
         raise GradientError("cache layout head count does not match model dims")
-    d_heads = lora_linear_backward(d_out.reshape(-1, d).float(), lw.wo, lora.get("wo"), cache["co"], grads,
-                                   f"{prefix}wo", f"{prefix}bo" if bitfit else None)
+    dev = cache["x"].device
+    g = _bf16(d_out.reshape(-1, d)).contiguous()
+    # output projection: d_heads = g Wo^T (+ LoRA(wo) fused), grads of wo's LoRA / bias
+    ad_o = lora.get("wo")
+    dax_o = rowproj(g, B, s, d, ad_o.b, 1, d, ad_o.rank, scale=ad_o.scaling) if ad_o is not None else None
+    d_heads = M.linear(g, lw.wo, lora_x=dax_o, lora_w=ad_o.a if ad_o else None, w_sr=1, w_sc=ad_o.rank if ad_o else 0,
+                       r=ad_o.rank if ad_o else 0)
+    if ad_o is not None:
+        r = ad_o.rank
+        _cg(grads, f"{prefix}wo.lora_a", (d, r), dax_o, cache["o"], B, s, d, r, 1.0, 1, r)
+        _cg(grads, f"{prefix}wo.lora_b", (r, d), cache["ax_o"], g, B, s, d, r, ad_o.scaling, d, 1)
+    if bitfit:
+        _cg(grads, f"{prefix}bo", (d,), None, g, B, s, d, 1, 1.0, 0, 1)
     qkv = cache["qkv"]
-    d_o = d_heads.to(torch.bfloat16)
     dqkv = torch.empty_like(qkv)
     scale = 1.0 / float(np.sqrt(hd))
-    attention_backward(qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :], cache["o"], d_o, 3 * d, B, s, H, hd,
+    attention_backward(qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :], cache["o"], d_heads, 3 * d, B, s, H, hd,
                        cache["pidx"], cache["stride"], dp, scale, cache["lse"], dqkv[:, :d], dqkv[:, d : 2 * d],
                        dqkv[:, 2 * d :])
     x2 = cache["x"]
-    dx = M._mm_f32(dqkv, lw.wqkv.t())
-    for j, t in enumerate(("wq", "wk", "wv")):
-        sl = dqkv[:, j * d : (j + 1) * d]
-        ad = lora.get(t)
-        if ad is not None:
-            g = sl.float()
-            d_ax = (g @ ad.b.t()) * ad.scaling
-            _acc(grads, f"{prefix}{t}.lora_a", x2.float().t() @ d_ax)
-            _acc(grads, f"{prefix}{t}.lora_b", ad.scaling * (cache["ax"][t].t() @ g))
-            dx.addmm_(d_ax, ad.a.t())
-        if bitfit:
-            _acc(grads, f"{prefix}b{t[1]}", sl.float().sum(0))
+    tq, r = cache["lora_t"], cache["lora_r"]
+    dax = None
+    if tq:
+        dax = torch.empty(B * s, len(tq) * r, dtype=torch.float32, device=dev)
+        for j, t in enumerate(tq):
+            ad, sl = lora[t], M.QKV_SLOT[t]
+            rowproj(dqkv[:, sl * d : (sl + 1) * d], B, s, d, ad.b, 1, d, r, scale=ad.scaling, out=dax[:, j * r : (j + 1) * r])
+    # dx = dqkv W_qkv^T + dax A_cat^T (LoRA fused in the epilogue)
+    dx = M.linear(dqkv, lw.wqkv, lora_x=dax, lora_w=cache["a_cat"] if tq else None, w_sr=1,
+                  w_sc=len(tq) * r if tq else 0, r=len(tq) * r if tq else 0)
+    for j, t in enumerate(tq):
+        ad, sl = lora[t], M.QKV_SLOT[t]
+        _cg(grads, f"{prefix}{t}.lora_a", (d, r), dax[:, j * r : (j + 1) * r], x2, B, s, d, r, 1.0, 1, r)
+        _cg(grads, f"{prefix}{t}.lora_b", (r, d), cache["ax"][:, j * r : (j + 1) * r], dqkv[:, sl * d : (sl + 1) * d], B,
+            s, d, r, ad.scaling, d, 1)
+    if bitfit:
+        for t in ("wq", "wk", "wv"):
+            sl = M.QKV_SLOT[t]
+            _cg(grads, f"{prefix}b{t[1]}", (d,), None, dqkv[:, sl * d : (sl + 1) * d], B, s, d, 1, 1.0, 0, 1)
     return dx
 
 
-def block_backward(d_out, model: M.Model, layer: int, cache, masks, grads: dict):
-    """sf/autograd.py:165-181; d_out fp32 [B*s, d]."""
+def block_backward(d_out, model: M.Model, layer: int, cache, masks, grads: dict, d_out_bf16=None, inplace: bool = False):
+    """sf/autograd.py:165-181; d_out fp32 [B*s, d] (+ its bf16 copy). Returns (dx fp32, dx bf16)."""
     lw = model.weights.layers[layer]
     bitfit = model.peft_method == "bitfit"
     lora = {t: model.lora[(layer, t)] for t in model.lora_targets} if model.peft_method == "lora" else {}
     prefix = f"layers.{layer}."
-    d_mlp = d_out
-    if model.peft_method == "adapter":
+    adapter = model.peft_method == "adapter"
+    if d_out_bf16 is None:
+        d_out_bf16 = d_out.to(torch.bfloat16)
+    d_mlp = d_out_bf16
+    if adapter:
         d_mlp = adapter_backward(d_out, model.adapters[(layer, "mlp")], cache["mlp_adapter"], grads, f"{prefix}mlp_adapter")
     nm = masks.neuron_mask if masks is not None else None
     dh2 = mlp_backward(d_mlp, cache["mlp"], lw, lora, nm, model.dims, grads, prefix, bitfit)
-    dy = layernorm_backward(dh2, cache["ln2"], accumulate_into=d_out.clone())
-    d_attn = dy
-    if model.peft_method == "adapter":
+    dy, dy_bf = layernorm_backward(dh2, cache["ln2"], accumulate_into=d_out if inplace else d_out.clone(), want_bf16=True)
+    d_attn = dy_bf
+    if adapter:
         d_attn = adapter_backward(dy, model.adapters[(layer, "attn")], cache["attn_adapter"], grads, f"{prefix}attn_adapter")
     dh1 = mha_backward(d_attn, cache["attn"], lw, lora, model.dims, grads, prefix, bitfit)
-    return layernorm_backward(dh1, cache["ln1"], accumulate_into=dy)
+    return layernorm_backward(dh1, cache["ln1"], accumulate_into=dy, want_bf16=True)
 
 
 def model_backward(model: M.Model, cache, d_logits, masks=None) -> dict:
@@ -182,10 +237,10 @@ def model_backward(model: M.Model, cache, d_logits, masks=None) -> dict:
     grads: dict = {}
     V = model.dims.vocab
     d_hf = M._mm_f32(d_logits.reshape(-1, V).to(torch.bfloat16), model.weights.emb)
-    dh = layernorm_backward(d_hf, cache["lnf"])
+    dh, dh_bf = layernorm_backward(d_hf, cache["lnf"], want_bf16=True)
     for layer in reversed(range(model.dims.n_layers)):
         lm = None if masks is None else masks[layer]
-        dh = block_backward(dh, model, layer, cache["blocks"][layer], lm, grads)
+        dh, dh_bf = block_backward(dh, model, layer, cache["blocks"][layer], lm, grads, dh_bf, inplace=True)
     for name, p in M.trainable_params(model).items():
         if name not in grads:
             grads[name] = torch.zeros_like(p)
@@ -201,21 +256,11 @@ def optimizer_step(state: M.PeftState, grads: dict, lr: float, betas=(0.9, 0.999
         raise GradientError(f"optimizer grads mismatch: missing={sorted(missing)}, extra={sorted(extra)}")
     b1, b2 = betas
     state.step += 1
-    t = state.step
-    if state.flat is not None:
-        g = torch.empty_like(state.m)
-        for name, p in state.params.items():
-            off = p.data_ptr() - state.flat.data_ptr()
-            g[off // 4 : off // 4 + p.numel()] = grads[name].reshape(-1).double()
-        adam_flat(state.flat, g, state.m, state.v, lr, b1, b2, eps, t)
-        return state
-    for name, p in state.params.items():  # pragma: no cover - flat path is the default
-        g = grads[name].double()
-        m = state.m.setdefault(name, torch.zeros_like(g))
-        v = state.v.setdefault(name, torch.zeros_like(g))
-        m.mul_(b1).add_(g, alpha=1 - b1)
-        v.mul_(b2).addcmul_(g, g, value=1 - b2)
-        p -= (lr * (m / (1 - b1**t)) / ((v / (1 - b2**t)).sqrt() + eps)).to(p.dtype)
+    g = torch.empty_like(state.m)
+    for name, p in state.params.items():
+        off = (p.data_ptr() - state.flat.data_ptr()) // 4
+        g[off : off + p.numel()] = grads[name].reshape(-1).double()
+    adam_flat(state.flat, g, state.m, state.v, lr, b1, b2, eps, state.step)
     return state
 
 

@@ -115,6 +115,30 @@ int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void
                   : launch_gemm<kDense, kEpiStoreBF16, 256>(ta, tb, args, stream);
 }
 
+int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, int N, int K, void* out, int ldo,
+              int out_f32, const float* resid, const float* bias, const float* lora_x, const float* lora_w,
+              long long w_sr, long long w_sc, int r, float scaling, lx_stream_t stream) {
+  LX_REQUIRE(M > 0 && N > 0 && K > 0, LX_ERR_SHAPE, "linear: empty shape");
+  LX_REQUIRE(!resid || out_f32, LX_ERR_SHAPE, "linear: residual add needs fp32 output");
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_tmap_bf16_2d(&ta, a, K, M, lda, kBK, kBM))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, b_t, K, N, ldb, kBK, 256))) return rc;
+  GemmArgs args = base_args(1, M, N, K);
+  args.out = out;
+  args.ldo = ldo;
+  args.out_f32 = out_f32;
+  args.resid = resid;
+  args.bias = bias;
+  args.lora_x = lora_x;
+  args.lora_w = lora_w;
+  args.w_sr = w_sr;
+  args.w_sc = w_sc;
+  args.lora_r = (lora_x && lora_w) ? r : 0;
+  args.lora_scale = scaling;
+  return launch_gemm<kDense, kEpiFc2, 256>(ta, tb, args, stream);
+}
+
 int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w1_t,
                   const int32_t* counts, const int32_t* ids, const float* b1, const float* ax1, const float* b1_lora,
                   int r, float scaling, int apply_relu, uint16_t* a_out, int ld_h, lx_stream_t stream) {
@@ -144,7 +168,7 @@ int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int bl
 
 int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
                   const int32_t* counts, const int32_t* ids, const float* b2, const float* ax2, const float* b2_lora,
-                  int r, float scaling, uint16_t* out, lx_stream_t stream) {
+                  int r, float scaling, void* out, int out_f32, const float* resid, lx_stream_t stream) {
   int rc;
   if ((rc = check_blk(blk))) return rc;
   LX_REQUIRE(d_ff % blk == 0, LX_ERR_MASK, "d_ff %d not a multiple of blk %d on the device path", d_ff, blk);
@@ -165,6 +189,9 @@ int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_
   args.w_sc = 1;
   args.lora_r = (ax2 && b2_lora) ? r : 0;
   args.lora_scale = scaling;
+  args.out_f32 = out_f32;
+  args.resid = resid;
+  LX_REQUIRE(!resid || out_f32, LX_ERR_SHAPE, "fc2: residual add needs fp32 output");
   return launch_gemm<kKGather, kEpiFc2, 256>(ta, tb, args, stream);
 }
 
@@ -195,7 +222,7 @@ int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_
 
 int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d, int d_ff, int blk,
                         const uint16_t* w1_t, const int32_t* counts, const int32_t* ids, const float* dax1,
-                        const float* a1_lora, int r, uint16_t* dx, lx_stream_t stream) {
+                        const float* a1_lora, int r, void* dx, int out_f32, lx_stream_t stream) {
   int rc;
   if ((rc = check_blk(blk))) return rc;
   CUtensorMap ta, tb;
@@ -213,6 +240,7 @@ int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d,
   args.w_sr = 1;
   args.w_sc = r;
   args.lora_r = (dax1 && a1_lora) ? r : 0;
+  args.out_f32 = out_f32;
   return launch_gemm<kKGather, kEpiDx, 256>(ta, tb, args, stream);
 }
 

@@ -61,6 +61,8 @@ struct GemmArgs {
   float thr;            // kEpiMask
   uint32_t* bits;       // kEpiMask: [n_items, bits_stride] words
   int bits_stride;
+  int out_f32;          // store fp32 instead of bf16 (any epilogue except kEpiMask)
+  const float* resid;   // fp32 [rows, ldo]: out = resid + value (fused residual add; requires out_f32)
 };
 
 template <int BN>
@@ -157,53 +159,52 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   const int* cnts = args.counts;
 
   if (warp == 0) {
-    // ================= TMA producer
-    if (lane == 0) {
-      const uint64_t pol_w = policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-        TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t);
-        const int row0 = ti.item * args.rows_per_item + ti.mt * kBM;
-        const int* ids = args.ids + (size_t)ti.item * args.ids_stride;
-        for (int ks = 0; ks < ti.k_stages; ++ks) {
-          mbar_wait(empty + stage, phase ^ 1);
-          uint8_t* sa = smem + stage * L::kStageBytes;
-          uint8_t* sb = sa + L::kABytes;
+    // ================= TMA producer (whole warp: gather boxes are issued one per lane, in parallel;
+    // each lane holds its neuron-block id in a register for the whole tile / stage)
+    const uint64_t pol_w = policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+      TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t);
+      const int row0 = ti.item * args.rows_per_item + ti.mt * kBM;
+      const int* ids = args.ids + (size_t)ti.item * args.ids_stride;
+      int my_row = 0;  // kNGather: this lane's gathered W row (block id * blk), lane < nb
+      int nb_n = 0;
+      if (BMODE == kNGather) {
+        nb_n = (ti.n_cols + args.blk - 1) / args.blk;
+        if ((int)lane < nb_n) my_row = __ldg(ids + ti.nt * BN / args.blk + lane) * args.blk;
+      }
+      for (int ks = 0; ks < ti.k_stages; ++ks) {
+        uint8_t* sa = smem + stage * L::kStageBytes;
+        uint8_t* sb = sa + L::kABytes;
+        int nb_k = 0, my_k_row = 0;
+        if (BMODE == kKGather) {
+          const int kb0 = ks * kBK / args.blk;
+          nb_k = min(kBK / args.blk, ti.k_total / args.blk - kb0);
+          const int j = lane / (BN / 64);
+          if (j < nb_k) my_k_row = __ldg(ids + kb0 + j) * args.blk;
+        }
+        mbar_wait(empty + stage, phase ^ 1);
+        if (lane == 0) {
           uint32_t bytes = L::kABytes;
-          if (BMODE == kDense) {
-            bytes += BN * kBK * 2;
-          } else if (BMODE == kNGather) {
-            int nb = (ti.n_cols + args.blk - 1) / args.blk;
-            bytes += nb * args.blk * kBK * 2;
-          } else {
-            int kb0 = ks * kBK / args.blk;
-            int nb = min(kBK / args.blk, ti.k_total / args.blk - kb0);
-            bytes += nb * (BN / 64) * args.blk * 128;
-          }
+          if (BMODE == kDense) bytes += BN * kBK * 2;
+          else if (BMODE == kNGather) bytes += nb_n * args.blk * kBK * 2;
+          else bytes += nb_k * (BN / 64) * args.blk * 128;
           mbar_arrive_expect_tx(full + stage, bytes);
           tma_load_2d(sa, &tmap_a, full + stage, ks * kBK, row0);
-          if (BMODE == kDense) {
-            tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.nt * BN, pol_w);
-          } else if (BMODE == kNGather) {
-            int nb = (ti.n_cols + args.blk - 1) / args.blk;
-            int blk0 = ti.nt * BN / args.blk;
-            for (int j = 0; j < nb; ++j) {
-              int id = __ldg(ids + blk0 + j);
-              tma_load_2d_hint(sb + j * args.blk * 128, &tmap_b, full + stage, ks * kBK, id * args.blk, pol_w);
-            }
-          } else {
-            int kb0 = ks * kBK / args.blk;
-            int nb = min(kBK / args.blk, ti.k_total / args.blk - kb0);
-            for (int j = 0; j < nb; ++j) {
-              int id = __ldg(ids + kb0 + j);
-              for (int a = 0; a < BN / 64; ++a)
-                tma_load_2d_hint(sb + a * (kBK * 128) + j * args.blk * 128, &tmap_b, full + stage, ti.nt * BN + a * 64,
-                                 id * args.blk, pol_w);
-            }
-          }
-          if (++stage == S) { stage = 0; phase ^= 1; }
+          if (BMODE == kDense) tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.nt * BN, pol_w);
         }
+        if (BMODE == kNGather) {
+          if ((int)lane < nb_n)
+            tma_load_2d_hint(sb + lane * args.blk * 128, &tmap_b, full + stage, ks * kBK, my_row, pol_w);
+        } else if (BMODE == kKGather) {
+          const int j = lane / (BN / 64), a = lane % (BN / 64);
+          if (j < nb_k)
+            tma_load_2d_hint(sb + a * (kBK * 128) + j * args.blk * 128, &tmap_b, full + stage, ti.nt * BN + a * 64,
+                             my_k_row, pol_w);
+        }
+        __syncwarp();
+        if (++stage == S) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -342,16 +343,46 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         if (EPI == kEpiDa) {
           if (row_ok) {
             const __nv_bfloat16* ap = args.act + grow * args.ld_act + j0;
+            uint32_t aw[16];
+            if (nv == 32) {  // 64 contiguous bytes of this row: four 16B loads
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                uint4 p = *reinterpret_cast<const uint4*>(ap + 8 * i);
+                aw[4 * i] = p.x; aw[4 * i + 1] = p.y; aw[4 * i + 2] = p.z; aw[4 * i + 3] = p.w;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const uint32_t lo = (2 * i < nv) ? __bfloat16_as_ushort(ap[2 * i]) : 0u;
+                const uint32_t hi = (2 * i + 1 < nv) ? __bfloat16_as_ushort(ap[2 * i + 1]) : 0u;
+                aw[i] = lo | (hi << 16);
+              }
+            }
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-              float av = (i < nv) ? __bfloat162float(ap[i]) : 0.f;
-              v[i] = av > 0.f ? v[i] : 0.f;
+              // relu'(z) = (a > 0): sign bit clear and nonzero magnitude of the bf16 activation
+              const uint32_t h = (aw[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+              v[i] = (h != 0u && (h & 0x8000u) == 0u) ? v[i] : 0.f;
             }
           }
         }
         if (!row_ok) continue;
-        if (EPI == kEpiStoreF32) {
+        if (EPI == kEpiStoreF32 || args.out_f32) {
           float* o = reinterpret_cast<float*>(args.out) + grow * args.ldo + j0;
+          if (args.resid) {
+            const float* rp = args.resid + grow * args.ldo + j0;
+            if (nv == 32) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4) {
+                float4 rv = *reinterpret_cast<const float4*>(rp + i);
+                v[i] += rv.x; v[i + 1] += rv.y; v[i + 2] += rv.z; v[i + 3] += rv.w;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (i < nv) v[i] += rp[i];
+            }
+          }
           if (nv == 32 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);

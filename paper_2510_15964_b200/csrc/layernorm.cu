@@ -82,7 +82,7 @@ template <bool kF32>
 __global__ void __launch_bounds__(kLnThreads) ln_bwd_kernel(const void* __restrict__ dy_, const float* __restrict__ x,
                                                              const float* __restrict__ g, const float* __restrict__ mean,
                                                              const float* __restrict__ istd, int d,
-                                                             float* __restrict__ dx) {
+                                                             float* __restrict__ dx, __nv_bfloat16* __restrict__ dx_bf16) {
   __shared__ float red[32];
   const size_t row = blockIdx.x;
   const float mu = mean[row], is = istd[row];
@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(kLnThreads) ln_bwd_kernel(const void* __restri
       cur.z += is * (gv[i].z - mg - xh[i].z * mgx);
       cur.w += is * (gv[i].w - mg - xh[i].w * mgx);
       *o = cur;
+      if (dx_bf16)  // bf16 copy of the updated residual gradient: the next GEMMs' operand
+        *reinterpret_cast<uint2*>(dx_bf16 + row * d + 4 * c) = make_uint2(pack_bf16x2(cur.x, cur.y), pack_bf16x2(cur.z, cur.w));
     }
   }
 }
@@ -146,12 +148,13 @@ int lx_layernorm_fwd(const float* x, int M, int d, const float* gamma, const flo
 }
 
 int lx_layernorm_bwd(const void* dy, int dy_is_f32, const float* x, const float* gamma, const float* mean,
-                     const float* inv_std, int M, int d, float* dx_accum, lx_stream_t stream) {
+                     const float* inv_std, int M, int d, float* dx_accum, uint16_t* dx_bf16, lx_stream_t stream) {
   LX_REQUIRE(d % 4 == 0 && d <= kLnThreads * 4 * kLnMaxVec, LX_ERR_UNSUPPORTED, "layernorm: d=%d unsupported", d);
+  auto* ob = reinterpret_cast<__nv_bfloat16*>(dx_bf16);
   if (dy_is_f32)
-    ln_bwd_kernel<true><<<M, kLnThreads, 0, stream>>>(dy, x, gamma, mean, inv_std, d, dx_accum);
+    ln_bwd_kernel<true><<<M, kLnThreads, 0, stream>>>(dy, x, gamma, mean, inv_std, d, dx_accum, ob);
   else
-    ln_bwd_kernel<false><<<M, kLnThreads, 0, stream>>>(dy, x, gamma, mean, inv_std, d, dx_accum);
+    ln_bwd_kernel<false><<<M, kLnThreads, 0, stream>>>(dy, x, gamma, mean, inv_std, d, dx_accum, ob);
   return launch_check("layernorm_bwd");
 }
 

@@ -102,14 +102,22 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
   __shared__ unsigned char cell[kMaxM * kMaxM];
   __shared__ float s_red[32];
   __shared__ unsigned long long s_cnt[kMaxPool + 1][2];  // [pattern][0]=mass, [1]=active blocks
+  extern __shared__ float s_qk[];  // [2][m][r+1]: this (item, head)'s Q_hat and K_hat rows
   const int mm = m * m;
+  const int rs = r + 1;            // padded row stride: conflict-free column walks
   for (int e = threadIdx.x; e < mm; e += blockDim.x) cell[e] = 0;
   for (int item = item0; item < item1; ++item) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 2 * m * r; e += blockDim.x) {  // coalesced: consecutive threads, consecutive t
+      const int which = e / (m * r), rem = e % (m * r), i = rem / r, t = rem % r;
+      s_qk[(which * m + i) * rs + t] = proj[(size_t)(item * m + i) * ldp + (which ? H + h : h) * r + t];
+    }
+    __syncthreads();
     // S_hat = (X Wq)(X Wk)^T  (sf/predictor.py:74-76)
     for (int e = threadIdx.x; e < mm; e += blockDim.x) {
-      int i = e / m, j = e % m;
-      const float* qr = proj + (size_t)(item * m + i) * ldp + h * r;
-      const float* kr = proj + (size_t)(item * m + j) * ldp + (H + h) * r;
+      const int i = e / m, j = e % m;
+      const float* qr = s_qk + i * rs;
+      const float* kr = s_qk + (m + j) * rs;
       float acc = 0.f;
       for (int t = 0; t < r; ++t) acc = fmaf(qr[t], kr[t], acc);
       s_hat[e] = acc;
@@ -229,8 +237,12 @@ int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, i
   int rc = lx_gemm_bf16_tn(x_small, d, wqk_t, d, proj_ws, 2 * H * r, 1, n_items * m, 2 * H * r, d, stream);
   if (rc) return rc;
   dim3 grid(H, scope_batch ? 1 : n_items);
-  attn_pattern_kernel<<<grid, 256, 0, stream>>>(proj_ws, n_items, m, H, r, threshold_frac, tau, n_b, pool_kind,
-                                                  pool_param, n_pool, scope_batch, pattern_idx, scores_dump);
+  const size_t smem = sizeof(float) * 2 * m * (r + 1);
+  LX_REQUIRE(smem <= 200 * 1024, LX_ERR_UNSUPPORTED, "predictor rank %d x m %d exceeds shared memory", r, m);
+  static cudaError_t attr = cudaFuncSetAttribute(attn_pattern_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  LX_CHECK_CUDA(attr);
+  attn_pattern_kernel<<<grid, 256, smem, stream>>>(proj_ws, n_items, m, H, r, threshold_frac, tau, n_b, pool_kind,
+                                                     pool_param, n_pool, scope_batch, pattern_idx, scores_dump);
   return launch_check("attn_pattern");
 }
 

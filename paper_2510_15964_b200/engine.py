@@ -19,20 +19,20 @@ from . import autograd as AG, model as M
 def lm_head_loss_and_grad(hf: torch.Tensor, emb: torch.Tensor, targets: torch.Tensor, s: int, chunk: int = 1024):
     """Mean CE over positions (per-item mean, then batch mean) and d(sum of per-item losses)/d hf.
     hf bf16 [M, d]; emb bf16 [V, d]; targets int64 [M]. Returns (loss fp32 scalar tensor, d_hf fp32 [M, d])."""
-    Mr = hf.shape[0]
+    from . import _abi
+
+    Mr, V = hf.shape[0], emb.shape[0]
     d_hf = torch.empty(Mr, hf.shape[1], dtype=torch.float32, device=hf.device)
-    loss_sum = torch.zeros((), dtype=torch.float32, device=hf.device)
+    row_loss = torch.empty(Mr, dtype=torch.float32, device=hf.device)
+    tg = targets.contiguous()
     for r0 in range(0, Mr, chunk):
         r1 = min(Mr, r0 + chunk)
-        lg = M._mm_f32(hf[r0:r1], emb.t())  # [c, V] fp32
-        t = targets[r0:r1]
-        lse = torch.logsumexp(lg, dim=1)
-        loss_sum += (lse - lg.gather(1, t[:, None])[:, 0]).sum()
-        lg.sub_(lse[:, None]).exp_()  # softmax in place
-        lg.scatter_add_(1, t[:, None], torch.full((r1 - r0, 1), -1.0, device=hf.device))
-        lg.mul_(1.0 / s)  # per-item mean (sf/model.py:472)
-        d_hf[r0:r1] = M._mm_f32(lg.to(torch.bfloat16), emb)
-    return loss_sum / Mr, d_hf
+        lg = M._mm_f32(hf[r0:r1], emb.t())  # [c, V] fp32 (cuBLAS)
+        gb = torch.empty(r1 - r0, V, dtype=torch.bfloat16, device=hf.device)
+        _abi.call("lx_cross_entropy", lg.data_ptr(), r1 - r0, V, tg[r0:r1].data_ptr(), 1.0 / s, row_loss[r0:].data_ptr(),
+                  gb.data_ptr(), _abi.stream_handle(hf.device))  # fused CE fwd+bwd, per-item mean (sf/model.py:472)
+        d_hf[r0:r1] = M._mm_f32(gb, emb)
+    return row_loss.mean(), d_hf
 
 
 class FinetuneEngine:
@@ -47,11 +47,11 @@ class FinetuneEngine:
         self.graph = None
         self.static_tokens = None
         self.static_loss = None
-        self._slots = []
+        self._grad_views = {}
         base = state.flat.data_ptr()
         for name, p in state.params.items():
             off = (p.data_ptr() - base) // 4
-            self._slots.append((name, off, p.numel()))
+            self._grad_views[name] = self.flat_grad[off : off + p.numel()].view(p.shape)
         self.last_masks = None
 
     # -------------------------------------------------------------- one step (capturable)
@@ -67,17 +67,18 @@ class FinetuneEngine:
             caches.append(c)
         hf, cf = M.layernorm_forward(h, m.weights.lnf_g, m.weights.lnf_b)
         loss, d_hf = lm_head_loss_and_grad(hf, m.weights.emb, tgt, s, self.loss_chunk)
-        grads: dict = {}
-        dh = AG.layernorm_backward(d_hf, cf)
+        # gradient reductions write straight into the flat buffer, pre-scaled by 1/B (sf/harness.py:415)
+        grads = AG.FlatGrads(self._grad_views, 1.0 / B)
+        dh, dh_bf = AG.layernorm_backward(d_hf, cf, want_bf16=True)
         for layer in reversed(range(m.dims.n_layers)):
-            dh = AG.block_backward(dh, m, layer, caches[layer], None, grads)
+            dh, dh_bf = AG.block_backward(dh, m, layer, caches[layer], None, grads, dh_bf, inplace=True)
         self.last_masks = [c["masks"] for c in caches]
-        g = self.flat_grad
-        g.zero_()
-        inv_b = 1.0 / B
-        for name, off, n in self._slots:
-            if name in grads:
-                g[off : off + n].copy_(grads[name].reshape(-1)).mul_(inv_b)
+        for name, view in self._grad_views.items():
+            t = grads.get(name)
+            if t is None:
+                view.zero_()  # unreached trainables get zero gradients (sf/autograd.py:191-194)
+            elif t is not view:
+                view.copy_(t).mul_(1.0 / B)  # gradients produced by torch ops (adapter path)
         return loss
 
     def _finish(self) -> None:

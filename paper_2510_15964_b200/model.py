@@ -108,6 +108,15 @@ class LayerWeights:
     ln1_b: torch.Tensor
     ln2_g: torch.Tensor
     ln2_b: torch.Tensor
+    # K-major copies for the forward TN GEMMs (out = x W  ==  x (W^T)^T): frozen, built once
+    wqkv_t: torch.Tensor | None = None  # bf16 [3d, d]
+    wo_t: torch.Tensor | None = None  # bf16 [d, d]
+
+    def __post_init__(self):
+        if self.wqkv_t is None:
+            self.wqkv_t = self.wqkv.t().contiguous()
+        if self.wo_t is None:
+            self.wo_t = self.wo.t().contiguous()
 
     @property
     def d(self) -> int:
@@ -412,30 +421,62 @@ def resolve_head_patterns(head_patterns, model_or_dpool, n_items: int, n_heads: 
     return cache[key], 0
 
 
-def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: ModelDims, counter=None, *, dpool=None):
+def linear(a: torch.Tensor, b_t: torch.Tensor, out_f32: bool = False, resid: torch.Tensor | None = None, bias=None,
+           lora_x=None, lora_w=None, w_sr: int = 0, w_sc: int = 0, r: int = 0, scaling: float = 1.0) -> torch.Tensor:
+    """out = (resid) + a @ b_t^T + bias + scaling * lora_x . w on the tcgen05 GEMM (fused epilogue).
+    a bf16 [M, K] (any row stride), b_t bf16 [N, K] (K-major weight)."""
+    M, K = a.shape
+    N = b_t.shape[0]
+    out = torch.empty(M, N, dtype=torch.float32 if (out_f32 or resid is not None) else torch.bfloat16, device=a.device)
+    _abi.call("lx_linear", a.data_ptr(), a.stride(0), b_t.data_ptr(), b_t.stride(0), M, N, K, out.data_ptr(), out.stride(0),
+              int(out.dtype == torch.float32), _abi.ptr(resid), _abi.ptr(bias), _abi.ptr(lora_x), _abi.ptr(lora_w), w_sr,
+              w_sc, r if lora_x is not None else 0, float(scaling), _abi.stream_handle(a.device))
+    return out
+
+
+QKV_SLOT = {"wq": 0, "wk": 1, "wv": 2}
+
+
+def _qkv_lora(lora: dict, d: int):
+    """Targets among wq/wk/wv, concatenated A [d, n*r] and the segmented column factor
+    W [n*r, 3d] (scaling folded in) that the QKV epilogue applies (sf/model.py:292-304)."""
+    tq = [t for t in ("wq", "wk", "wv") if t in lora]
+    if not tq:
+        return tq, None, None, 0
+    r = lora[tq[0]].rank
+    a_cat = torch.cat([lora[t].a for t in tq], 1).contiguous()
+    w = torch.zeros(len(tq) * r, 3 * d, dtype=torch.float32, device=a_cat.device)
+    for j, t in enumerate(tq):
+        sl = QKV_SLOT[t]
+        w[j * r : (j + 1) * r, sl * d : (sl + 1) * d] = lora[t].b * lora[t].scaling
+    return tq, a_cat, w, r
+
+
+def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: ModelDims, counter=None, *, dpool=None,
+                resid=None):
     """Block-sparse multi-head attention (sf/model.py:322-360). x: LN1 output bf16 [B, s, d] (or [s, d]).
-    Returns (out fp32 [B*s, d], cache); the cache holds O and the row LSE instead of probabilities."""
+    Q/K/V come from one tcgen05 GEMM with bias + LoRA fused in the epilogue; the output projection
+    fuses bias, LoRA and (optionally) the residual add. Returns (out fp32 [B*s, d], cache); the cache
+    holds O and the row LSE instead of probabilities."""
     x2, B, s = _items(x)
     d, H, hd = dims.d_model, dims.n_heads, dims.head_dim
     dp = dpool if dpool is not None else device_pool(pool, x2.device, dims.seq_len, dims.attn_blk)
     pidx, stride = resolve_head_patterns(head_patterns, dp, B, H, x2.device)
-    qkv = torch.mm(x2, lw.wqkv)  # bf16 [M, 3d]
-    qkv += lw.bqkv.to(torch.bfloat16)
-    ax = {}
-    for j, t in enumerate(("wq", "wk", "wv")):
-        ad = lora.get(t)
-        if ad is not None:
-            ax[t] = x2.float() @ ad.a
-            sl = qkv[:, j * d : (j + 1) * d]
-            sl.copy_((sl.float() + ad.scaling * (ax[t] @ ad.b)).to(torch.bfloat16))
+    tq, a_cat, w_l, r = _qkv_lora(lora, d)
+    ax = rowproj(x2, B, s, d, a_cat, a_cat.shape[1], 1, a_cat.shape[1]) if tq else None  # [M, n*r]
+    qkv = linear(x2, lw.wqkv_t, bias=lw.bqkv, lora_x=ax, lora_w=w_l, w_sr=3 * d, w_sc=1,
+                 r=a_cat.shape[1] if tq else 0)  # bf16 [M, 3d]
     scale = 1.0 / float(np.sqrt(hd))
     o, lse = attention_forward(qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :], 3 * d, B, s, H, hd, pidx, stride, dp, scale)
     if counter is not None:
         nnz = sum(dp_nnz(dp, int(i)) for i in pidx.flatten().tolist()) * (B if stride == 0 else 1)
         counter.add(2 * nnz * dims.attn_blk * dims.attn_blk * hd)
-    out, co = lora_linear_forward(o, lw.wo, lw.bo, lora.get("wo"))
-    cache = {"x": x2, "qkv": qkv, "o": o, "lse": lse, "pidx": pidx, "stride": stride, "ax": ax, "co": co, "n_items": B,
-             "s": s, "dpool": dp}
+    ad_o = lora.get("wo")
+    ax_o = rowproj(o, B, s, d, ad_o.a, ad_o.rank, 1, ad_o.rank) if ad_o is not None else None
+    out = linear(o, lw.wo_t, out_f32=True, resid=resid, bias=lw.bo, lora_x=ax_o, lora_w=ad_o.b if ad_o else None,
+                 w_sr=d, w_sc=1, r=ad_o.rank if ad_o else 0, scaling=ad_o.scaling if ad_o else 1.0)
+    cache = {"x": x2, "qkv": qkv, "o": o, "lse": lse, "pidx": pidx, "stride": stride, "ax": ax, "lora_t": tq,
+             "lora_r": r, "a_cat": a_cat, "ax_o": ax_o, "n_items": B, "s": s, "dpool": dp}
     return out, cache
 
 
@@ -444,9 +485,11 @@ def dp_nnz(dp: DevicePool, i: int) -> int:
     return len(build_pool(n_b)[dp.ids[i]].coords) if dp.seq_len else 0
 
 
-def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, counter=None):
+def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, counter=None, *, resid=None,
+                out_f32: bool = False):
     """ReLU MLP restricted to active neuron blocks (sf/model.py:363-400) on the tcgen05
-    gather-GEMMs with bias / LoRA / ReLU fused in the epilogues. x: LN2 output bf16."""
+    gather-GEMMs with bias / LoRA / ReLU fused in the epilogues. x: LN2 output bf16.
+    With `resid` (fp32) the fc2 epilogue returns resid + MLP (the block's residual add)."""
     x2, B, s = _items(x)
     d, f, blk = dims.d_model, dims.d_ff, dims.blk_size
     nm = lower_mask(neuron_mask, dims.n_blk, blk, B, x2.device)
@@ -456,8 +499,10 @@ def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, c
                                         lora_b=ad1.b if ad1 else None, lora_r=ad1.rank if ad1 else 0,
                                         scaling=ad1.scaling if ad1 else 1.0, relu=True)
     ax2 = rowproj(hid.values, B, s, f, ad2.a, ad2.rank, 1, ad2.rank, masks=nm, blk=blk) if ad2 is not None else None
-    out = neuron_ops.neuron_matmul_fwd2(hid, lw.mlp, None, counter, bias=lw.b2, ax=ax2, lora_b=ad2.b if ad2 else None,
-                                        lora_r=ad2.rank if ad2 else 0, scaling=ad2.scaling if ad2 else 1.0)
+    out = neuron_ops.neuron_matmul_fwd2(
+        hid, lw.mlp, None, counter, bias=lw.b2, ax=ax2, lora_b=ad2.b if ad2 else None, lora_r=ad2.rank if ad2 else 0,
+        scaling=ad2.scaling if ad2 else 1.0, resid=resid,
+        out=torch.empty(B * s, d, dtype=torch.float32, device=x2.device) if (out_f32 or resid is not None) else None)
     if counter is not None:
         n_act = int(nm.counts.sum()) * blk
         if ad1 is not None:
@@ -487,20 +532,27 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
         hp = masks.attn_patterns(layer, h1v, x_small=c1["x_small"])
     else:
         hp = masks.attn_patterns(layer, h1v)
-    att, ca = mha_forward(h1v, lw, lora, hp, model.pool, model.dims, counter, dpool=model.dpool)
+    adapter = model.peft_method == "adapter"
+    x2 = x.reshape(B * s, d)
+    # residual adds are fused into the output-projection / fc2 epilogues unless an adapter sits in between
+    att, ca = mha_forward(h1v, lw, lora, hp, model.pool, model.dims, counter, dpool=model.dpool,
+                          resid=None if adapter else x2)
     caa = None
-    if model.peft_method == "adapter":
+    if adapter:
         att, caa = adapter_forward(att, model.adapters[(layer, "attn")])
-    y = x.reshape(B * s, d) + att
+        y = x2 + att
+    else:
+        y = att
     h2, c2 = layernorm_forward(y, lw.ln2_g, lw.ln2_b)
     h2v = h2.view(B, s, d)
     nm = masks.neuron_mask if static else masks.mlp_mask(layer, h2v)
-    mo, cm = mlp_forward(h2v, lw, lora, nm, model.dims, counter)
-    mo = mo.float()
+    mo, cm = mlp_forward(h2v, lw, lora, nm, model.dims, counter, resid=None if adapter else y, out_f32=True)
     cma = None
-    if model.peft_method == "adapter":
+    if adapter:
         mo, cma = adapter_forward(mo, model.adapters[(layer, "mlp")])
-    out = y + mo
+        out = y + mo
+    else:
+        out = mo
     cache = {"ln1": c1, "attn": ca, "attn_adapter": caa, "ln2": c2, "mlp": cm, "mlp_adapter": cma,
              "masks": LayerMasks(ca["pidx"], cm["mask"])}
     return out.view(B, s, d), cache

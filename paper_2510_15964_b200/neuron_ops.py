@@ -198,8 +198,9 @@ def neuron_matmul_fwd1(x, weights: LayeredWeights, mask, blk_size: int, counter=
 
 
 def neuron_matmul_fwd2(hidden: ActiveHidden, weights: LayeredWeights, mask, counter=None, *, bias=None, ax=None,
-                       lora_b=None, lora_r=0, scaling=1.0, out=None) -> torch.Tensor:
-    """Packed hidden @ W2[cols, :] (sf/neuron_ops.py:85-95) on the tcgen05 K-gather GEMM."""
+                       lora_b=None, lora_r=0, scaling=1.0, out=None, resid=None) -> torch.Tensor:
+    """Packed hidden @ W2[cols, :] (sf/neuron_ops.py:85-95) on the tcgen05 K-gather GEMM.
+    With `resid` (fp32 [M, d]) the result is fp32 resid + MLP (fused residual add)."""
     d_ff, d = weights.w2.shape
     nm = hidden.masks
     if mask is not None and mask is not nm:
@@ -208,10 +209,13 @@ def neuron_matmul_fwd2(hidden: ActiveHidden, weights: LayeredWeights, mask, coun
             raise MaskError("mask does not match the mask the hidden activations were computed with")
     M = hidden.values.shape[0]
     s = M // hidden.n_items
-    res = out if out is not None else torch.empty(M, d, dtype=torch.bfloat16, device=hidden.values.device)
+    f32 = resid is not None
+    res = out if out is not None else torch.empty(M, d, dtype=torch.float32 if f32 else torch.bfloat16,
+                                                  device=hidden.values.device)
     _abi.call("lx_neuron_fc2", hidden.values.data_ptr(), hidden.values.stride(0), hidden.n_items, s, d, d_ff,
               hidden.blk_size, weights.w2.data_ptr(), nm.counts.data_ptr(), nm.ids.data_ptr(), _abi.ptr(bias),
-              _abi.ptr(ax), _abi.ptr(lora_b), lora_r, float(scaling), res.data_ptr(), _abi.stream_handle(res.device))
+              _abi.ptr(ax), _abi.ptr(lora_b), lora_r, float(scaling), res.data_ptr(), int(res.dtype == torch.float32),
+              _abi.ptr(resid), _abi.stream_handle(res.device))
     if counter is not None:
         counter.add(s * int(nm.counts.sum()) * hidden.blk_size * d)
     return res
@@ -221,20 +225,23 @@ def neuron_matmul_fwd2(hidden: ActiveHidden, weights: LayeredWeights, mask, coun
 
 
 def rowproj(x2: torch.Tensor, n_items: int, s: int, K: int, w: torch.Tensor, w_sk: int, w_sq: int, r: int,
-            scale: float = 1.0, masks: NeuronMasks | None = None, blk: int = 1) -> torch.Tensor:
-    """Y[M, r] = scale * X[M, K] W (K gathered per item when `masks` is given)."""
-    y = torch.empty(x2.shape[0], r, dtype=torch.float32, device=x2.device)
+            scale: float = 1.0, masks: NeuronMasks | None = None, blk: int = 1, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Y[M, r] = scale * X[M, K] W (K gathered per item when `masks` is given). `out` may be a column
+    slice of a wider fp32 buffer (row stride out.stride(0))."""
+    y = out if out is not None else torch.empty(x2.shape[0], r, dtype=torch.float32, device=x2.device)
     _abi.call("lx_rowproj", x2.data_ptr(), x2.stride(0), n_items, s, K, w.data_ptr(), w_sk, w_sq, r, float(scale),
               _abi.ptr(masks.counts if masks else None), _abi.ptr(masks.ids if masks else None), blk, y.data_ptr(),
-              _abi.stream_handle(x2.device))
+              y.stride(0), _abi.stream_handle(x2.device))
     return y
 
 
 def colgrad(p: torch.Tensor | None, x2: torch.Tensor, n_items: int, s: int, ncols: int, r: int, scale: float,
             out: torch.Tensor, g_sq: int, g_sc: int, masks: NeuronMasks | None = None, blk: int = 1) -> torch.Tensor:
-    """out(q, c) = scale * sum_rows P[row, q] X[row, c] (c original column), deterministic."""
+    """out(q, c) = scale * sum_rows P[row, q] X[row, c] (c original column), deterministic.
+    P may be a column slice (row stride p.stride(0)); X may be a column slice (row stride x2.stride(0))."""
     ws = torch.empty(int(_abi.lib().lx_colgrad_ws_floats(n_items, s, ncols, r)), dtype=torch.float32, device=x2.device)
-    _abi.call("lx_colgrad", _abi.ptr(p), x2.data_ptr(), x2.stride(0), n_items, s, ncols, r, float(scale),
+    _abi.call("lx_colgrad", _abi.ptr(p), p.stride(0) if p is not None else 1, x2.data_ptr(), x2.stride(0), n_items, s,
+              ncols, r, float(scale),
               _abi.ptr(masks.counts if masks else None), _abi.ptr(masks.pos if masks else None), blk, out.data_ptr(),
               g_sq, g_sc, ws.data_ptr(), _abi.stream_handle(x2.device))
     return out

@@ -86,13 +86,13 @@ def test_neuron_mlp_gemms(n_items, s, d, d_ff, blk, density, r):
               b1.data_ptr(), P(ax1), P(B1), r, scaling, 1, a.data_ptr(), ld_h, st)
     out = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
     _abi.call("lx_neuron_fc2", a.data_ptr(), ld_h, n_items, s, d, d_ff, blk, w2.data_ptr(), cnt_d.data_ptr(), ids_d.data_ptr(),
-              b2.data_ptr(), P(ax2), P(B2), r, scaling, out.data_ptr(), st)
+              b2.data_ptr(), P(ax2), P(B2), r, scaling, out.data_ptr(), 0, None, st)
     dz = torch.zeros(M, ld_h, device=dev, dtype=torch.bfloat16)
     _abi.call("lx_neuron_fc2_dgrad", d_out.data_ptr(), n_items, s, d, d_ff, blk, w2.data_ptr(), cnt_d.data_ptr(),
               ids_d.data_ptr(), P(dax2), P(A2), r, a.data_ptr(), dz.data_ptr(), ld_h, st)
     dx = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
     _abi.call("lx_neuron_fc1_dgrad", dz.data_ptr(), ld_h, n_items, s, d, d_ff, blk, w1t.data_ptr(), cnt_d.data_ptr(),
-              ids_d.data_ptr(), P(dax1), P(A1), r, dx.data_ptr(), st)
+              ids_d.data_ptr(), P(dax1), P(A1), r, dx.data_ptr(), 0, st)
     torch.cuda.synchronize()
     for b in range(n_items):
         rows = slice(b * s, (b + 1) * s)
@@ -120,3 +120,90 @@ def test_neuron_mlp_gemms(n_items, s, d, d_ff, blk, density, r):
         if r:
             dxr = dxr + dax1[rows] @ A1.T
         assert rel(dx[rows], dxr) < 1e-2 if dxr.abs().max() > 0 else dx[rows].float().abs().max() == 0
+
+
+@pytest.mark.parametrize("gather", [False, True])
+@pytest.mark.parametrize("r,w_layout", [(8, "kr"), (8, "rk"), (16, "kr"), (4, "rk"), (1, "kr")])
+def test_lora_skinny_kernels(gather, r, w_layout):
+    """rowproj / colgrad (csrc/lora.cu) vs torch fp32 on the same bf16 operands, incl. per-item gathers."""
+    from paper_2510_15964_b200 import neuron_ops as N
+
+    dev = _dev()
+    n_items, s, K, blk = 3, 300, 1024, 16
+    n_blk = K // blk
+    masks, counts, ids = _masks(n_items, n_blk, 0.4, seed=r)
+    g = torch.Generator(device="cpu").manual_seed(r)
+    x = torch.randn(n_items * s, K, generator=g).to(dev, torch.bfloat16)
+    w = (torch.randn(K, r, generator=g) if w_layout == "kr" else torch.randn(r, K, generator=g)).to(dev)
+    w_sk, w_sq = (r, 1) if w_layout == "kr" else (1, K)
+    wk = w if w_layout == "kr" else w.t()
+    nm = N.lower_mask(torch.from_numpy(masks).to(dev), n_blk, blk, n_items, dev) if gather else None
+    y = N.rowproj(x, n_items, s, K, w, w_sk, w_sq, r, scale=0.5, masks=nm, blk=blk)
+    p = torch.randn(n_items * s, r, generator=g).to(dev)
+    G = torch.empty(r, K, device=dev)
+    N.colgrad(p, x, n_items, s, K, r, 0.25, G, K, 1, masks=nm, blk=blk)
+    torch.cuda.synchronize()
+    Gref = torch.zeros(r, K, device=dev)
+    for b in range(n_items):
+        rows = slice(b * s, (b + 1) * s)
+        if gather:
+            cols = torch.from_numpy((ids[b, : counts[b], None] * blk + np.arange(blk)[None]).reshape(-1)).to(dev)
+            xb = x[rows, : cols.numel()].float()  # packed columns
+            yr = 0.5 * xb @ wk[cols]
+            Gref[:, cols] += 0.25 * p[rows].t() @ xb
+        else:
+            yr = 0.5 * x[rows].float() @ wk
+            Gref += 0.25 * p[rows].t() @ x[rows].float()
+        assert rel(y[rows], yr) < 1e-4 if yr.abs().max() > 0 else y[rows].abs().max() == 0
+    assert rel(G, Gref) < 1e-4
+    if gather:  # inactive columns exactly zero
+        act = np.zeros(K, bool)
+        for b in range(n_items):
+            act[(ids[b, : counts[b], None] * blk + np.arange(blk)[None]).reshape(-1)] = True
+        assert float(G[:, torch.from_numpy(~act).to(dev)].abs().max()) == 0
+
+
+@pytest.mark.parametrize("M,N,K,r,mode", [(4096, 6144, 2048, 16, "bf16"), (300, 520, 200, 8, "f32"), (512, 2048, 2048, 8, "resid"),
+                                          (256, 256, 64, 0, "bf16")])
+def test_linear_fused_epilogue(M, N, K, r, mode):
+    """lx_linear: out = (resid) + A B^T + bias + s * lora_x . w  (lora_linear_forward's fused dense product)."""
+    from paper_2510_15964_b200 import model as Mo
+
+    dev = _dev()
+    g = torch.Generator(device="cpu").manual_seed(M + r)
+    a = torch.randn(M, K, generator=g).to(dev, torch.bfloat16)
+    bt = (torch.randn(N, K, generator=g) * K ** -0.5).to(dev, torch.bfloat16)
+    bias = torch.randn(N, generator=g).to(dev)
+    lx = torch.randn(M, max(r, 1), generator=g).to(dev)
+    lw = torch.randn(max(r, 1), N, generator=g).to(dev) * 0.1
+    resid = torch.randn(M, N, generator=g).to(dev) if mode == "resid" else None
+    out = Mo.linear(a, bt, out_f32=mode != "bf16", resid=resid, bias=bias, lora_x=lx if r else None, lora_w=lw if r else None,
+                    w_sr=N, w_sc=1, r=r, scaling=0.5)
+    ref = a.float() @ bt.float().T + bias
+    if r:
+        ref = ref + 0.5 * lx @ lw
+    if resid is not None:
+        ref = ref + resid
+    torch.cuda.synchronize()
+    assert out.dtype == (torch.bfloat16 if mode == "bf16" else torch.float32)
+    assert rel(out, ref) < (1e-2 if mode == "bf16" else 2e-3)
+
+
+def test_cross_entropy_kernel():
+    """Fused LM-head CE fwd+bwd (csrc/ce.cu) vs torch fp32 (sf/model.py:454-472)."""
+    from paper_2510_15964_b200.engine import lm_head_loss_and_grad
+
+    dev = _dev()
+    g = torch.Generator(device="cpu").manual_seed(3)
+    B, s, d, V = 2, 96, 128, 1000
+    hf = torch.randn(B * s, d, generator=g).to(dev, torch.bfloat16)
+    emb = (torch.randn(V, d, generator=g) * 0.3).to(dev, torch.bfloat16)
+    tgt = torch.randint(0, V, (B * s,), generator=g).to(dev)
+    loss, d_hf = lm_head_loss_and_grad(hf, emb, tgt, s, chunk=64)
+    logits = (hf.float() @ emb.float().T).requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(logits, tgt)
+    (ref * B).backward()  # per-item mean summed over items == gradient convention of loss_backward (1/s)
+    ref_dhf = logits.grad @ emb.float()
+    torch.cuda.synchronize()
+    assert abs(float(loss) - float(ref)) < 1e-4 * float(ref)
+    assert rel(d_hf, ref_dhf) < 1e-2

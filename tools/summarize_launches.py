@@ -1,0 +1,25 @@
+"""Summarise an ncu `--metrics gpu__time_duration.sum --csv` launch list by kernel."""
+import collections
+import csv
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+hdr = rows[hi]
+ci = {h: i for i, h in enumerate(hdr)}
+agg = collections.defaultdict(lambda: [0, 0.0])
+tot = 0.0
+for r in rows[hi + 1:]:
+    if len(r) < len(hdr) or r[ci["Metric Name"]] != "gpu__time_duration.sum":
+        continue
+    v = float(r[ci["Metric Value"]].replace(",", ""))
+    u = r[ci["Metric Unit"]]
+    v = v / 1e3 if u == "nsecond" else v * 1e3 if u == "msecond" else v  # -> microseconds
+    k = r[ci["Kernel Name"]].split("(")[0][:100]
+    agg[k][0] += 1
+    agg[k][1] += v
+    tot += v
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+print(f"total {tot / 1e3:.2f} ms over {sum(a[0] for a in agg.values())} launches (ncu-serialised, cold caches)")
+for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
+    print(f"{t / 1e3:8.3f} ms {100 * t / tot:5.1f}%  n={n:4d}  {k}")
