@@ -119,8 +119,10 @@ int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d,
  *   X bf16 row stride ldx; W(k, q) = w[k_orig*w_sk + q*w_sq]; k_orig = k (dense, counts==NULL) or
  *   ids[b][k/blk]*blk + k%blk over the item's packed K = counts[b]*blk.  (x A1, a A2[cols], dO B2^T, dz B1[:,cols]^T) */
 int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const float* w, long long w_sk, long long w_sq,
-               int r, float scale, const int32_t* counts, const int32_t* ids, int blk, float* y, int ldy,
+               int r, float scale, const int32_t* counts, const int32_t* ids, int blk, float* y, int ldy, void* wpack_ws,
                lx_stream_t stream);
+/* Workspace for lx_rowproj's tensor-core path: W packed as bf16 hi/lo [items][2][R'][K] (gathered per item). */
+long long lx_rowproj_ws_bytes(int n_items, int K, int r, int gathered);
 
 /* Skinny LoRA gradient reduction over tokens: G[q, c_orig] = scale * sum_rows P[row, q] X[row, c]
  *   (dB1[:,cols], dA2[cols] (transposed), dB2, dA1 (transposed)); summed over items in order.
@@ -157,8 +159,10 @@ int lx_bsattn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const
 /* ------------------------------------------------------------------ glue (fused neighbours)
  * layernorm_forward (sf/model.py:307-312), fp32 residual in, bf16 out; saves mean/inv_std.
  * Optionally also writes the predictor's downsampled rows (sf/predictor.py:62-71) to x_small. */
-int lx_layernorm_fwd(const float* x, int M, int d, const float* gamma, const float* beta, float eps, uint16_t* y,
-                     float* mean, float* inv_std, int s, int m_small, uint16_t* x_small, lx_stream_t stream);
+int lx_layernorm_fwd(const float* x, const uint16_t* delta, float* resid_out, int M, int d, const float* gamma,
+                     const float* beta, float eps, uint16_t* y, float* mean, float* inv_std, int s, int m_small,
+                     uint16_t* x_small, lx_stream_t stream);
+/* (delta != NULL: fused residual add — resid_out = x + delta (fp32) is normalised and returned.) */
 /* loss_forward + loss_backward over rows of fp32 logits (sf/model.py:454-472): row_loss[r] =
  * logsumexp(l_r) - l_r[t_r]; grad_bf16[r] = (softmax(l_r) - onehot(t_r)) * inv_s (inv_s = 1/seq_len). */
 int lx_cross_entropy(const float* logits, int rows, int V, const int64_t* targets, float inv_s, float* row_loss,

@@ -33,7 +33,8 @@ SIGNATURES: dict[str, list] = {
     "lx_neuron_fc2": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _P, _I, _P, _P],
     "lx_neuron_fc2_dgrad": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P],
     "lx_neuron_fc1_dgrad": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P],
-    "lx_rowproj": [_P, _I, _I, _I, _I, _P, _LL, _LL, _I, _F, _P, _P, _I, _P, _I, _P],
+    "lx_rowproj": [_P, _I, _I, _I, _I, _P, _LL, _LL, _I, _F, _P, _P, _I, _P, _I, _P, _P],
+    "lx_rowproj_ws_bytes": [_I, _I, _I, _I],
     "lx_colgrad_ws_floats": [_I, _I, _I, _I],
     "lx_colgrad": [_P, _I, _P, _I, _I, _I, _I, _I, _F, _P, _P, _I, _P, _LL, _LL, _P, _P],
     "lx_colsum": [_P, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P],
@@ -41,11 +42,11 @@ SIGNATURES: dict[str, list] = {
     "lx_attn_tables": [_P, _P, _I, _I, _I, _P, _I],
     "lx_bsattn_fwd": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _I, _P, _P],
     "lx_bsattn_bwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P, _P],
-    "lx_layernorm_fwd": [_P, _I, _I, _P, _P, _F, _P, _P, _P, _I, _I, _P, _P],
+    "lx_layernorm_fwd": [_P, _P, _P, _I, _I, _P, _P, _F, _P, _P, _P, _I, _I, _P, _P],
     "lx_cross_entropy": [_P, _I, _I, _P, _F, _P, _P, _P],
     "lx_layernorm_bwd": [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P],
 }
-RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_ws_floats": _LL}
+RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_ws_floats": _LL, "lx_rowproj_ws_bytes": _LL}
 
 _ERRORS = {1: E.ShapeError, 2: E.LayoutError, 3: E.MaskError, 4: E.PatternError, 5: E.CudaError, 6: E.UnsupportedError}
 

@@ -171,9 +171,11 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
     g = _bf16(d_out.reshape(-1, d)).contiguous()
     # output projection: d_heads = g Wo^T (+ LoRA(wo) fused), grads of wo's LoRA / bias
     ad_o = lora.get("wo")
-    dax_o = rowproj(g, B, s, d, ad_o.b, 1, d, ad_o.rank, scale=ad_o.scaling) if ad_o is not None else None
-    d_heads = M.linear(g, lw.wo, lora_x=dax_o, lora_w=ad_o.a if ad_o else None, w_sr=1, w_sc=ad_o.rank if ad_o else 0,
-                       r=ad_o.rank if ad_o else 0)
+    d_heads = torch.mm(g, lw.wo.t())  # plain library GEMM (cuBLAS), bf16
+    dax_o = None
+    if ad_o is not None:
+        dax_o = rowproj(g, B, s, d, ad_o.b, 1, d, ad_o.rank, scale=ad_o.scaling)
+        d_heads.addmm_(dax_o.to(torch.bfloat16), ad_o.a.t().to(torch.bfloat16))
     if ad_o is not None:
         r = ad_o.rank
         _cg(grads, f"{prefix}wo.lora_a", (d, r), dax_o, cache["o"], B, s, d, r, 1.0, 1, r)
@@ -194,9 +196,10 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
         for j, t in enumerate(tq):
             ad, sl = lora[t], M.QKV_SLOT[t]
             rowproj(dqkv[:, sl * d : (sl + 1) * d], B, s, d, ad.b, 1, d, r, scale=ad.scaling, out=dax[:, j * r : (j + 1) * r])
-    # dx = dqkv W_qkv^T + dax A_cat^T (LoRA fused in the epilogue)
-    dx = M.linear(dqkv, lw.wqkv, lora_x=dax, lora_w=cache["a_cat"] if tq else None, w_sr=1,
-                  w_sc=len(tq) * r if tq else 0, r=len(tq) * r if tq else 0)
+    # dx = dqkv W_qkv^T (cuBLAS) + dax A_cat^T (rank-n*r update)
+    dx = torch.mm(dqkv, lw.wqkv.t())
+    if tq:
+        dx.addmm_(dax.to(torch.bfloat16), cache["a_cat"].t().to(torch.bfloat16))
     for j, t in enumerate(tq):
         ad, sl = lora[t], M.QKV_SLOT[t]
         _cg(grads, f"{prefix}{t}.lora_a", (d, r), dax[:, j * r : (j + 1) * r], x2, B, s, d, r, 1.0, 1, r)

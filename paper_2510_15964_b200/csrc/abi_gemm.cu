@@ -120,10 +120,18 @@ int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, i
               long long w_sr, long long w_sc, int r, float scaling, lx_stream_t stream) {
   LX_REQUIRE(M > 0 && N > 0 && K > 0, LX_ERR_SHAPE, "linear: empty shape");
   LX_REQUIRE(!resid || out_f32, LX_ERR_SHAPE, "linear: residual add needs fp32 output");
+  // tile width: 128x256 tiles unless that leaves fewer than ~3 tiles per SM, then 128x128
+  // (more tiles per persistent CTA -> epilogues overlap the next tile's mainloop, smaller tail wave)
+  static int forced_bn = [] { const char* e = getenv("LX_LINEAR_BN"); return e ? atoi(e) : 0; }();
+  const long long tiles256 = (long long)((M + kBM - 1) / kBM) * ((N + 255) / 256);
+  // measured (tools/linear_probe.py): 128-wide tiles are A-operand smem-bound with 1-SM MMA, so 256
+  // wins even at 1.7 waves; LX_LINEAR_BN=128 keeps the variant reachable for experiments
+  (void)tiles256;
+  const int bn = forced_bn ? forced_bn : 256;
   CUtensorMap ta, tb;
   int rc;
   if ((rc = make_tmap_bf16_2d(&ta, a, K, M, lda, kBK, kBM))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, b_t, K, N, ldb, kBK, 256))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, b_t, K, N, ldb, kBK, bn))) return rc;
   GemmArgs args = base_args(1, M, N, K);
   args.out = out;
   args.ldo = ldo;
@@ -136,7 +144,8 @@ int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, i
   args.w_sc = w_sc;
   args.lora_r = (lora_x && lora_w) ? r : 0;
   args.lora_scale = scaling;
-  return launch_gemm<kDense, kEpiFc2, 256>(ta, tb, args, stream);
+  return bn == 128 ? launch_gemm<kDense, kEpiFc2, 128>(ta, tb, args, stream)
+                   : launch_gemm<kDense, kEpiFc2, 256>(ta, tb, args, stream);
 }
 
 int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w1_t,

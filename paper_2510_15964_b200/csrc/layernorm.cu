@@ -24,7 +24,9 @@ __global__ void __launch_bounds__(kLnThreads) ln_fwd_kernel(const float* __restr
                                                              const float* __restrict__ b, float eps,
                                                              __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
                                                              float* __restrict__ istd_out, int s, int m_small,
-                                                             __nv_bfloat16* __restrict__ x_small) {
+                                                             __nv_bfloat16* __restrict__ x_small,
+                                                             const __nv_bfloat16* __restrict__ delta,
+                                                             float* __restrict__ resid_out) {
   __shared__ float red[32];
   const size_t row = blockIdx.x;
   const float4* xr = reinterpret_cast<const float4*>(x + row * d);
@@ -35,6 +37,14 @@ __global__ void __launch_bounds__(kLnThreads) ln_fwd_kernel(const float* __restr
   for (int i = 0; i < kLnMaxVec; ++i) {
     int c = threadIdx.x + i * kLnThreads;
     v[i] = c < nv ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (delta && c < nv) {  // fused residual add: y = x + delta (sf/model.py:420, 427), y kept in fp32
+      const uint2 p = reinterpret_cast<const uint2*>(delta + row * d)[c];
+      v[i].x += bf16_bits_to_float(p.x & 0xffff);
+      v[i].y += bf16_bits_to_float(p.x >> 16);
+      v[i].z += bf16_bits_to_float(p.y & 0xffff);
+      v[i].w += bf16_bits_to_float(p.y >> 16);
+      reinterpret_cast<float4*>(resid_out + row * d)[c] = v[i];
+    }
     sum += (v[i].x + v[i].y) + (v[i].z + v[i].w);
   }
   const float mu = block_sum(sum, red) / d;
@@ -137,13 +147,16 @@ using namespace lx;
 
 extern "C" {
 
-int lx_layernorm_fwd(const float* x, int M, int d, const float* gamma, const float* beta, float eps, uint16_t* y,
-                     float* mean, float* inv_std, int s, int m_small, uint16_t* x_small, lx_stream_t stream) {
+int lx_layernorm_fwd(const float* x, const uint16_t* delta, float* resid_out, int M, int d, const float* gamma,
+                     const float* beta, float eps, uint16_t* y, float* mean, float* inv_std, int s, int m_small,
+                     uint16_t* x_small, lx_stream_t stream) {
   LX_REQUIRE(d % 4 == 0 && d <= kLnThreads * 4 * kLnMaxVec, LX_ERR_UNSUPPORTED, "layernorm: d=%d unsupported", d);
   LX_REQUIRE(M >= 1, LX_ERR_SHAPE, "layernorm: empty input");
+  LX_REQUIRE(!delta || resid_out, LX_ERR_SHAPE, "layernorm: residual add needs resid_out");
   if (x_small) LX_REQUIRE(s >= 1 && m_small >= 1 && M % s == 0, LX_ERR_SHAPE, "layernorm: bad downsample shape");
   ln_fwd_kernel<<<M, kLnThreads, 0, stream>>>(x, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), mean, inv_std,
-                                              s > 0 ? s : 1, m_small, reinterpret_cast<__nv_bfloat16*>(x_small));
+                                              s > 0 ? s : 1, m_small, reinterpret_cast<__nv_bfloat16*>(x_small),
+                                              reinterpret_cast<const __nv_bfloat16*>(delta), resid_out);
   return launch_check("layernorm_fwd");
 }
 

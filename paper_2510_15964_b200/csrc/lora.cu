@@ -107,8 +107,195 @@ __global__ void __launch_bounds__(256) rowproj_kernel(const __nv_bfloat16* __res
   }
 }
 
+// ---------------------------------------------------------------- rowproj on tensor cores
+// Y[M, R] = X[M, K] W[K, R] with mma.sync m16n8k16 (bf16 in, fp32 accumulate): a warp owns
+// 16 rows and walks K in steps of 16; A fragments come straight from global (X rows are
+// contiguous along K), B fragments from the W chunk staged in shared memory as bf16 [n][k].
+// The CUDA-core form is shared-memory-bandwidth bound (R*4 bytes of W per X element).
+LX_DEV void mma16816_rp(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+constexpr int kRmRows = 16;    // rows per CTA; its 4 warps split K and reduce through shared memory
+constexpr int kRmChunk = 256;  // K per staged W chunk
+constexpr int kRmStride = kRmChunk + 8;  // bf16 elements per n-row in smem (conflict-free 32-bit reads)
+
+template <int NT>  // NT n8-tiles: R <= 8*NT
+__global__ void __launch_bounds__(128) rowproj_mma_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int s, int K,
+                                                          const float* __restrict__ w, long long w_sk, long long w_sq,
+                                                          int r, float scale, const int32_t* __restrict__ counts,
+                                                          const int32_t* __restrict__ ids, int ids_stride, int blk,
+                                                          float* __restrict__ y, int ldy) {
+  // W chunk as a bf16 (hi, lo) pair: W ~= hi + lo to ~2^-17 relative, so X (exact bf16) . W keeps
+  // fp32-level accuracy with two MMAs per step
+  __shared__ __align__(16) __nv_bfloat16 s_hi[8 * NT * kRmStride];
+  __shared__ __align__(16) __nv_bfloat16 s_lo[8 * NT * kRmStride];
+  __shared__ float s_red[4][16][8 * NT + 1];
+  const int item = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = blockIdx.x * kRmRows;
+  const int k_item = counts ? __ldg(counts + item) * blk : K;
+  const int32_t* my_ids = ids ? ids + (size_t)item * ids_stride : nullptr;
+  const int ra = row0 + (lane >> 2), rb = ra + 8;
+  const uint32_t* xa = reinterpret_cast<const uint32_t*>(x + ((size_t)item * s + min(ra, s - 1)) * ldx) + (lane & 3);
+  const uint32_t* xb = reinterpret_cast<const uint32_t*>(x + ((size_t)item * s + min(rb, s - 1)) * ldx) + (lane & 3);
+  float acc[NT][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+  const bool k_fast = (w_sk == 1);
+  for (int k0 = 0; k0 < k_item; k0 += kRmChunk) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 8 * NT * kRmChunk; e += 128) {
+      int kk, q;
+      if (k_fast) { q = e / kRmChunk; kk = e % kRmChunk; } else { kk = e / (8 * NT); q = e % (8 * NT); }
+      const int k = k0 + kk;
+      float val = 0.f;
+      if (k < k_item && q < r) {
+        long long ko = my_ids ? (long long)__ldg(my_ids + k / blk) * blk + k % blk : k;
+        val = __ldg(w + ko * w_sk + q * w_sq);
+      }
+      const __nv_bfloat16 hi = __float2bfloat16_rn(val);
+      s_hi[q * kRmStride + kk] = hi;
+      s_lo[q * kRmStride + kk] = __float2bfloat16_rn(val - __bfloat162float(hi));
+    }
+    __syncthreads();
+    const int kn = min(kRmChunk, k_item - k0);  // multiple of 16
+    // warp w takes k-steps w, w+4, ...: all four A-fragment loads of two steps are in flight together
+    for (int ks = warp * 16; ks < kn; ks += 128) {
+      const int kw = (k0 + ks) >> 1;
+      const bool two = ks + 64 < kn;
+      uint32_t a[4] = {__ldg(xa + kw), __ldg(xb + kw), __ldg(xa + kw + 4), __ldg(xb + kw + 4)};
+      uint32_t a2[4] = {0u, 0u, 0u, 0u};
+      if (two) {
+        a2[0] = __ldg(xa + kw + 32); a2[1] = __ldg(xb + kw + 32); a2[2] = __ldg(xa + kw + 36); a2[3] = __ldg(xb + kw + 36);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !two) break;
+        const int kk = ks + h * 64;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int off = (t * 8 + (lane >> 2)) * kRmStride + kk + (lane & 3) * 2;
+          const uint32_t h0 = *reinterpret_cast<const uint32_t*>(s_hi + off);
+          const uint32_t h1 = *reinterpret_cast<const uint32_t*>(s_hi + off + 8);
+          const uint32_t l0 = *reinterpret_cast<const uint32_t*>(s_lo + off);
+          const uint32_t l1 = *reinterpret_cast<const uint32_t*>(s_lo + off + 8);
+          mma16816_rp(acc[t], h ? a2 : a, h0, h1);
+          mma16816_rp(acc[t], h ? a2 : a, l0, l1);
+        }
+      }
+    }
+  }
+  // reduce the four warps' partial sums
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const int q = t * 8 + (lane & 3) * 2;
+    s_red[warp][lane >> 2][q] = acc[t][0];
+    s_red[warp][lane >> 2][q + 1] = acc[t][1];
+    s_red[warp][(lane >> 2) + 8][q] = acc[t][2];
+    s_red[warp][(lane >> 2) + 8][q + 1] = acc[t][3];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 16 * 8 * NT; e += 128) {
+    const int rr = e / (8 * NT), q = e % (8 * NT), row = row0 + rr;
+    if (q < r && row < s)
+      y[((size_t)item * s + row) * ldy + q] = (s_red[0][rr][q] + s_red[1][rr][q] + s_red[2][rr][q] + s_red[3][rr][q]) * scale;
+  }
+}
+
+// W packed once per call: wp[item][hl][q][k] bf16 (hl = 0: hi, 1: lo), k over the item's packed K
+// (gathered through ids), rows q >= r and columns k >= k_item zero. Kp = K rounded up to 16.
+__global__ void rowproj_wpack_kernel(const float* __restrict__ w, long long w_sk, long long w_sq, int r, int RP, int K,
+                                     int Kp, const int32_t* __restrict__ counts, const int32_t* __restrict__ ids,
+                                     int ids_stride, int blk, __nv_bfloat16* __restrict__ wp) {
+  const int item = blockIdx.y;
+  const int k_item = counts ? __ldg(counts + item) * blk : K;
+  const int32_t* my_ids = ids ? ids + (size_t)item * ids_stride : nullptr;
+  __nv_bfloat16* out = wp + (size_t)item * 2 * RP * Kp;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < RP * Kp; e += gridDim.x * blockDim.x) {
+    const int q = e / Kp, k = e % Kp;
+    float val = 0.f;
+    if (k < k_item && q < r) {
+      const long long ko = my_ids ? (long long)__ldg(my_ids + k / blk) * blk + k % blk : k;
+      val = __ldg(w + ko * w_sk + q * w_sq);
+    }
+    const __nv_bfloat16 hi = __float2bfloat16_rn(val);
+    out[e] = hi;
+    out[(size_t)RP * Kp + e] = __float2bfloat16_rn(val - __bfloat162float(hi));
+  }
+}
+
+// Y[M, R] = X W on tensor cores, A and B fragments straight from global (L2-resident W pack);
+// a CTA owns 16 rows, its 4 warps interleave k-steps and reduce through shared memory.
+template <int NT>
+__global__ void __launch_bounds__(128) rowproj_mma2_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int s, int K,
+                                                           int Kp, int r, float scale, const int32_t* __restrict__ counts,
+                                                           int blk, const __nv_bfloat16* __restrict__ wp,
+                                                           float* __restrict__ y, int ldy) {
+  constexpr int RP = 8 * NT;
+  __shared__ float s_red[4][16][RP + 1];
+  const int item = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = blockIdx.x * 16;
+  const int k_item = counts ? __ldg(counts + item) * blk : K;
+  const int ra = row0 + (lane >> 2), rb = ra + 8;
+  const uint32_t* xa = reinterpret_cast<const uint32_t*>(x + ((size_t)item * s + min(ra, s - 1)) * ldx) + (lane & 3);
+  const uint32_t* xb = reinterpret_cast<const uint32_t*>(x + ((size_t)item * s + min(rb, s - 1)) * ldx) + (lane & 3);
+  const uint32_t* wh = reinterpret_cast<const uint32_t*>(wp + (size_t)item * 2 * RP * Kp + (lane >> 2) * Kp) + (lane & 3);
+  const uint32_t* wl = wh + (size_t)RP * Kp / 2;
+  float acc[NT][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+  constexpr int U = 4;  // k-steps in flight per warp
+  for (int kb = warp * 16; kb < k_item; kb += 64 * U) {
+    uint32_t a[U][4], bh[U][NT][2], bl[U][NT][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int ks = kb + u * 64;
+      const bool ok = ks < k_item;
+      const int kw = ks >> 1;
+      a[u][0] = ok ? __ldg(xa + kw) : 0u;
+      a[u][1] = ok ? __ldg(xb + kw) : 0u;
+      a[u][2] = ok ? __ldg(xa + kw + 4) : 0u;
+      a[u][3] = ok ? __ldg(xb + kw + 4) : 0u;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const size_t o = (size_t)t * 8 * Kp / 2 + kw;
+        bh[u][t][0] = ok ? __ldg(wh + o) : 0u;
+        bh[u][t][1] = ok ? __ldg(wh + o + 4) : 0u;
+        bl[u][t][0] = ok ? __ldg(wl + o) : 0u;
+        bl[u][t][1] = ok ? __ldg(wl + o + 4) : 0u;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        mma16816_rp(acc[t], a[u], bh[u][t][0], bh[u][t][1]);
+        mma16816_rp(acc[t], a[u], bl[u][t][0], bl[u][t][1]);
+      }
+  }
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const int q = t * 8 + (lane & 3) * 2;
+    s_red[warp][lane >> 2][q] = acc[t][0];
+    s_red[warp][lane >> 2][q + 1] = acc[t][1];
+    s_red[warp][(lane >> 2) + 8][q] = acc[t][2];
+    s_red[warp][(lane >> 2) + 8][q + 1] = acc[t][3];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 16 * RP; e += 128) {
+    const int rr = e / RP, q = e % RP, row = row0 + rr;
+    if (q < r && row < s)
+      y[((size_t)item * s + row) * ldy + q] = (s_red[0][rr][q] + s_red[1][rr][q] + s_red[2][rr][q] + s_red[3][rr][q]) * scale;
+  }
+}
+
 constexpr int kCgCols = 256;  // 32 lanes x 8 columns
-constexpr int kCgRows = 256;  // rows per split (8 warps x 32 rows)
+constexpr int kCgRows = 128;  // rows per split (8 warps x 16 rows)
 
 // partial[item][split][q][col] over the item's packed columns (dynamic smem: s_p | s_red)
 template <int R>
@@ -139,17 +326,17 @@ __global__ void __launch_bounds__(256) colgrad_partial_kernel(const float* __res
     for (int q = 0; q < R; ++q) acc[j][q] = 0.f;
   const int nrows = min(kCgRows, s - r0);
   if (c0 < n_item) {
-    // warp w owns rows w, w+8, ...; 4 rows in flight per lane
-    for (int i0 = warp; i0 < nrows; i0 += 32) {
-      uint4 pk[4];
+    // warp w owns rows w, w+8, ...; 8 rows in flight per lane
+    for (int i0 = warp; i0 < nrows; i0 += 64) {
+      uint4 pk[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int i = i0 + u * 8;
         pk[u] = i < nrows ? *reinterpret_cast<const uint4*>(x + ((size_t)item * s + r0 + i) * ldx + c0)
                           : make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int i = i0 + u * 8;
         if (i >= nrows) break;
         const uint32_t pw[4] = {pk[u].x, pk[u].y, pk[u].z, pk[u].w};
@@ -188,14 +375,31 @@ __global__ void colgrad_final_kernel(const float* __restrict__ ws, int n_items, 
   const int q = blockIdx.y;
   if (c >= ncols || q >= r) return;
   float acc = 0.f;
-  for (int b = 0; b < n_items; ++b) {
-    int pc = c;
-    if (pos) {
-      int pb = __ldg(pos + (size_t)b * (ncols / blk) + c / blk);
-      if (pb < 0) continue;
-      pc = pb * blk + c % blk;
+  // items in groups of 8: all position lookups, then all partial loads, are independent (in flight together);
+  // the summation order stays fixed (item-major, split-minor) -> deterministic
+  for (int b0 = 0; b0 < n_items; b0 += 8) {
+    int pcs[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int b = b0 + u;
+      pcs[u] = -1;
+      if (b < n_items) {
+        if (pos) {
+          const int pb = __ldg(pos + (size_t)b * (ncols / blk) + c / blk);
+          pcs[u] = pb < 0 ? -1 : pb * blk + c % blk;
+        } else {
+          pcs[u] = c;
+        }
+      }
     }
-    for (int sp = 0; sp < n_splits; ++sp) acc += ws[(((size_t)b * n_splits + sp) * R + q) * ncols + pc];
+    for (int sp = 0; sp < n_splits; ++sp) {
+      float vals[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        vals[u] = pcs[u] >= 0 ? ws[(((size_t)(b0 + u) * n_splits + sp) * R + q) * ncols + pcs[u]] : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += vals[u];
+    }
   }
   g[(long long)q * g_sq + (long long)c * g_sc] = acc * scale;
 }
@@ -225,8 +429,13 @@ using namespace lx;
 
 extern "C" {
 
+long long lx_rowproj_ws_bytes(int n_items, int K, int r, int gathered) {
+  const int RP = r <= 8 ? 8 : 16;
+  return (long long)(gathered ? n_items : 1) * 2 * RP * K * 2;
+}
+
 int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const float* w, long long w_sk, long long w_sq,
-               int r, float scale, const int32_t* counts, const int32_t* ids, int blk, float* y, int ldy,
+               int r, float scale, const int32_t* counts, const int32_t* ids, int blk, float* y, int ldy, void* wpack_ws,
                lx_stream_t stream) {
   LX_REQUIRE(ldy >= r, LX_ERR_SHAPE, "rowproj: ldy < r");
   LX_REQUIRE(r >= 1 && r <= kRpMaxR, LX_ERR_UNSUPPORTED, "rowproj: rank %d outside [1, %d]", r, kRpMaxR);
@@ -234,9 +443,34 @@ int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const floa
              "rowproj: 16B-aligned rows required (row stride multiple of 8)");
   LX_REQUIRE(!counts || K % blk == 0, LX_ERR_MASK, "rowproj: K not a multiple of blk");
   LX_REQUIRE(ldx >= ((K + 15) / 16) * 16, LX_ERR_SHAPE, "rowproj: row stride must cover K rounded up to 16");
-  dim3 grid((s + kRpRows - 1) / kRpRows, n_items);
   const auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
   const int ids_stride = counts ? K / blk : 0, b = counts ? blk : 1;
+  if (K % 16 == 0 && wpack_ws) {  // tensor-core path (K and every item's packed K are multiples of 16)
+    const int NT = r <= 8 ? 1 : 2, RP = 8 * NT;
+    const int items_w = counts ? n_items : 1;
+    const int Kp = K;
+    dim3 gp((RP * Kp + 255) / 256 < 64 ? (RP * Kp + 255) / 256 : 64, items_w);
+    rowproj_wpack_kernel<<<gp, 256, 0, stream>>>(w, w_sk, w_sq, r, RP, K, Kp, counts, ids, ids_stride, b,
+                                                 reinterpret_cast<__nv_bfloat16*>(wpack_ws));
+    int rc = launch_check("rowproj_wpack");
+    if (rc) return rc;
+    dim3 grid((s + 15) / 16, n_items);
+    const auto* wpb = reinterpret_cast<const __nv_bfloat16*>(wpack_ws);
+    if (!counts && n_items > 1) {
+      // dense W is shared by all items: index it as item 0 by treating the batch as one item
+      grid = dim3((n_items * s + 15) / 16, 1);
+      if (NT == 1)
+        rowproj_mma2_kernel<1><<<grid, 128, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb, y, ldy);
+      else
+        rowproj_mma2_kernel<2><<<grid, 128, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb, y, ldy);
+    } else if (NT == 1) {
+      rowproj_mma2_kernel<1><<<grid, 128, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, y, ldy);
+    } else {
+      rowproj_mma2_kernel<2><<<grid, 128, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, y, ldy);
+    }
+    return launch_check("rowproj_mma");
+  }
+  dim3 grid((s + kRpRows - 1) / kRpRows, n_items);
   if (r <= 8)
     rowproj_kernel<8><<<grid, 256, 0, stream>>>(xb, ldx, s, K, w, w_sk, w_sq, r, scale, counts, ids, ids_stride, b, y, ldy);
   else

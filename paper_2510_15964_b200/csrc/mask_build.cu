@@ -159,10 +159,18 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
       mass[p] += (in && on);
     }
   }
-  atomicAdd(&s_cnt[kMaxPool][0], total);
-  for (int p = 0; p < n_pool; ++p) {
-    if (mass[p]) atomicAdd(&s_cnt[p][0], mass[p]);
-    if (nnz[p]) atomicAdd(&s_cnt[p][1], nnz[p]);
+  // warp-reduce the integer counts, then one shared atomic per warp and counter
+  {
+    const unsigned t32 = __reduce_add_sync(0xffffffffu, (unsigned)total);
+    if ((threadIdx.x & 31) == 0 && t32) atomicAdd(&s_cnt[kMaxPool][0], (unsigned long long)t32);
+    for (int p = 0; p < n_pool; ++p) {
+      const unsigned m32 = __reduce_add_sync(0xffffffffu, (unsigned)mass[p]);
+      const unsigned n32 = __reduce_add_sync(0xffffffffu, (unsigned)nnz[p]);
+      if ((threadIdx.x & 31) == 0) {
+        if (m32) atomicAdd(&s_cnt[p][0], (unsigned long long)m32);
+        if (n32) atomicAdd(&s_cnt[p][1], (unsigned long long)n32);
+      }
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -108,16 +108,6 @@ class LayerWeights:
     ln1_b: torch.Tensor
     ln2_g: torch.Tensor
     ln2_b: torch.Tensor
-    # K-major copies for the forward TN GEMMs (out = x W  ==  x (W^T)^T): frozen, built once
-    wqkv_t: torch.Tensor | None = None  # bf16 [3d, d]
-    wo_t: torch.Tensor | None = None  # bf16 [d, d]
-
-    def __post_init__(self):
-        if self.wqkv_t is None:
-            self.wqkv_t = self.wqkv.t().contiguous()
-        if self.wo_t is None:
-            self.wo_t = self.wo.t().contiguous()
-
     @property
     def d(self) -> int:
         return self.wo.shape[0]
@@ -371,21 +361,24 @@ def lora_linear_forward(x, w, bias, adapter: LoraAdapter | None):
     return z, cache
 
 
-def layernorm_forward(x: torch.Tensor, gamma, beta, eps: float = 1e-5, x_small_spec=None):
+def layernorm_forward(x: torch.Tensor, gamma, beta, eps: float = 1e-5, x_small_spec=None, delta=None):
     """sf/model.py:307-312 on the fused kernel; x fp32 [M, d] -> bf16 y. x_small_spec=(s, m)
-    additionally writes the predictor's downsampled rows (returned in the cache)."""
+    additionally writes the predictor's downsampled rows (returned in the cache). With `delta`
+    (bf16 [M, d]) the residual add x + delta is fused: the fp32 sum is normalised and returned
+    as cache["x"] (the block's y, sf/model.py:420)."""
     x2 = x.reshape(-1, x.shape[-1]).contiguous()
     M, d = x2.shape
     y = torch.empty(M, d, dtype=torch.bfloat16, device=x2.device)
     mean = torch.empty(M, dtype=torch.float32, device=x2.device)
     istd = torch.empty(M, dtype=torch.float32, device=x2.device)
+    resid = torch.empty(M, d, dtype=torch.float32, device=x2.device) if delta is not None else None
     xs, s, m = None, 0, 0
     if x_small_spec is not None:
         s, m = x_small_spec
         xs = torch.empty(M // s * m, d, dtype=torch.bfloat16, device=x2.device)
-    _abi.call("lx_layernorm_fwd", x2.data_ptr(), M, d, gamma.data_ptr(), beta.data_ptr(), float(eps), y.data_ptr(),
-              mean.data_ptr(), istd.data_ptr(), s, m, _abi.ptr(xs), _abi.stream_handle(x2.device))
-    return y, {"x": x2, "mean": mean, "inv_std": istd, "gamma": gamma, "x_small": xs}
+    _abi.call("lx_layernorm_fwd", x2.data_ptr(), _abi.ptr(delta), _abi.ptr(resid), M, d, gamma.data_ptr(), beta.data_ptr(),
+              float(eps), y.data_ptr(), mean.data_ptr(), istd.data_ptr(), s, m, _abi.ptr(xs), _abi.stream_handle(x2.device))
+    return y, {"x": resid if resid is not None else x2, "mean": mean, "inv_std": istd, "gamma": gamma, "x_small": xs}
 
 
 def adapter_forward(x: torch.Tensor, ad: AdapterLayer):
@@ -452,29 +445,36 @@ def _qkv_lora(lora: dict, d: int):
     return tq, a_cat, w, r
 
 
-def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: ModelDims, counter=None, *, dpool=None,
-                resid=None):
+def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: ModelDims, counter=None, *, dpool=None):
     """Block-sparse multi-head attention (sf/model.py:322-360). x: LN1 output bf16 [B, s, d] (or [s, d]).
-    Q/K/V come from one tcgen05 GEMM with bias + LoRA fused in the epilogue; the output projection
-    fuses bias, LoRA and (optionally) the residual add. Returns (out fp32 [B*s, d], cache); the cache
-    holds O and the row LSE instead of probabilities."""
+    The dense projections are plain library GEMMs (cuBLAS, bias in the addmm); each LoRA delta
+    s*(xA)B is a rank-r cuBLAS update of its column slice with xA from the skinny rowproj kernel.
+    Returns (out bf16 [B*s, d] = O Wo + bo (+ LoRA), cache); the cache holds O and the row LSE
+    instead of probabilities. The residual add is fused into the next LayerNorm kernel."""
     x2, B, s = _items(x)
     d, H, hd = dims.d_model, dims.n_heads, dims.head_dim
     dp = dpool if dpool is not None else device_pool(pool, x2.device, dims.seq_len, dims.attn_blk)
     pidx, stride = resolve_head_patterns(head_patterns, dp, B, H, x2.device)
-    tq, a_cat, w_l, r = _qkv_lora(lora, d)
-    ax = rowproj(x2, B, s, d, a_cat, a_cat.shape[1], 1, a_cat.shape[1]) if tq else None  # [M, n*r]
-    qkv = linear(x2, lw.wqkv_t, bias=lw.bqkv, lora_x=ax, lora_w=w_l, w_sr=3 * d, w_sc=1,
-                 r=a_cat.shape[1] if tq else 0)  # bf16 [M, 3d]
+    tq, a_cat, _, r = _qkv_lora(lora, d)
+    qkv = torch.addmm(lw.bqkv.to(torch.bfloat16), x2, lw.wqkv)  # bf16 [M, 3d]
+    ax = None
+    if tq:
+        ax = rowproj(x2, B, s, d, a_cat, a_cat.shape[1], 1, a_cat.shape[1])  # fp32 [M, n*r] (kept for the LoRA grads)
+        axb = ax.to(torch.bfloat16)
+        for j, t in enumerate(tq):
+            sl = QKV_SLOT[t]
+            qkv[:, sl * d : (sl + 1) * d].addmm_(axb[:, j * r : (j + 1) * r], (lora[t].b * lora[t].scaling).to(torch.bfloat16))
     scale = 1.0 / float(np.sqrt(hd))
     o, lse = attention_forward(qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :], 3 * d, B, s, H, hd, pidx, stride, dp, scale)
     if counter is not None:
         nnz = sum(dp_nnz(dp, int(i)) for i in pidx.flatten().tolist()) * (B if stride == 0 else 1)
         counter.add(2 * nnz * dims.attn_blk * dims.attn_blk * hd)
+    out = torch.addmm(lw.bo.to(torch.bfloat16), o, lw.wo)  # bf16 [M, d]
     ad_o = lora.get("wo")
-    ax_o = rowproj(o, B, s, d, ad_o.a, ad_o.rank, 1, ad_o.rank) if ad_o is not None else None
-    out = linear(o, lw.wo_t, out_f32=True, resid=resid, bias=lw.bo, lora_x=ax_o, lora_w=ad_o.b if ad_o else None,
-                 w_sr=d, w_sc=1, r=ad_o.rank if ad_o else 0, scaling=ad_o.scaling if ad_o else 1.0)
+    ax_o = None
+    if ad_o is not None:
+        ax_o = rowproj(o, B, s, d, ad_o.a, ad_o.rank, 1, ad_o.rank)
+        out.addmm_(ax_o.to(torch.bfloat16), (ad_o.b * ad_o.scaling).to(torch.bfloat16))
     cache = {"x": x2, "qkv": qkv, "o": o, "lse": lse, "pidx": pidx, "stride": stride, "ax": ax, "lora_t": tq,
              "lora_r": r, "a_cat": a_cat, "ax_o": ax_o, "n_items": B, "s": s, "dpool": dp}
     return out, cache
@@ -534,16 +534,15 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
         hp = masks.attn_patterns(layer, h1v)
     adapter = model.peft_method == "adapter"
     x2 = x.reshape(B * s, d)
-    # residual adds are fused into the output-projection / fc2 epilogues unless an adapter sits in between
-    att, ca = mha_forward(h1v, lw, lora, hp, model.pool, model.dims, counter, dpool=model.dpool,
-                          resid=None if adapter else x2)
+    att, ca = mha_forward(h1v, lw, lora, hp, model.pool, model.dims, counter, dpool=model.dpool)
     caa = None
     if adapter:
-        att, caa = adapter_forward(att, model.adapters[(layer, "attn")])
-        y = x2 + att
+        att, caa = adapter_forward(att.float(), model.adapters[(layer, "attn")])
+        h2, c2 = layernorm_forward(x2 + att, lw.ln2_g, lw.ln2_b)
     else:
-        y = att
-    h2, c2 = layernorm_forward(y, lw.ln2_g, lw.ln2_b)
+        # y = x + attn fused into the LN2 kernel (fp32 y returned as the LN cache input)
+        h2, c2 = layernorm_forward(x2, lw.ln2_g, lw.ln2_b, delta=att)
+    y = c2["x"]
     h2v = h2.view(B, s, d)
     nm = masks.neuron_mask if static else masks.mlp_mask(layer, h2v)
     mo, cm = mlp_forward(h2v, lw, lora, nm, model.dims, counter, resid=None if adapter else y, out_f32=True)

@@ -229,9 +229,11 @@ def rowproj(x2: torch.Tensor, n_items: int, s: int, K: int, w: torch.Tensor, w_s
     """Y[M, r] = scale * X[M, K] W (K gathered per item when `masks` is given). `out` may be a column
     slice of a wider fp32 buffer (row stride out.stride(0))."""
     y = out if out is not None else torch.empty(x2.shape[0], r, dtype=torch.float32, device=x2.device)
+    nbytes = int(_abi.lib().lx_rowproj_ws_bytes(n_items, K, r, int(masks is not None)))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=x2.device)
     _abi.call("lx_rowproj", x2.data_ptr(), x2.stride(0), n_items, s, K, w.data_ptr(), w_sk, w_sq, r, float(scale),
               _abi.ptr(masks.counts if masks else None), _abi.ptr(masks.ids if masks else None), blk, y.data_ptr(),
-              y.stride(0), _abi.stream_handle(x2.device))
+              y.stride(0), ws.data_ptr(), _abi.stream_handle(x2.device))
     return y
 
 
