@@ -43,7 +43,7 @@ CONFIGS = {
 # kernels of ours launched per C-ABI call (for gpu_launches)
 KERNELS_PER_CALL = {
     "lx_gemm_bf16_tn": 1, "lx_linear": 1, "lx_cross_entropy": 1, "lx_predict_mlp_mask": 2, "lx_mask_compact": 1, "lx_predict_attention_patterns": 2,
-    "lx_neuron_fc1": 1, "lx_neuron_fc2": 1, "lx_neuron_fc2_dgrad": 1, "lx_neuron_fc1_dgrad": 1, "lx_rowproj": 2,
+    "lx_neuron_fc1": 1, "lx_neuron_fc2": 1, "lx_neuron_fc2_dgrad": 1, "lx_neuron_fc1_dgrad": 1, "lx_rowproj": 2, "lx_pack_active_rows": 1,
     "lx_colgrad": 2, "lx_colsum": 2, "lx_bsattn_fwd": 1, "lx_bsattn_bwd": 3, "lx_layernorm_fwd": 1, "lx_layernorm_bwd": 1,
 }
 
@@ -213,11 +213,15 @@ def fc1_roofline(model, engine, peaks: dict, reps: int = 20) -> dict:
     lw = model.weights.layers[0]
     ad = model.lora[(0, "w1")]
     ax = torch.randn(B * s, ad.rank, device="cuda")
+    from paper_2510_15964_b200.neuron_ops import pack_active_rows
+
+    w1p = pack_active_rows(lw.mlp.w1_t, nm)  # the step packs active W1^T rows per item (as here)
+    wp = w1p.data_ptr()
     st = _abi.stream_handle()
 
     def launch():
         _abi.call("lx_neuron_fc1", x.data_ptr(), B, s, d, f, dims.blk_size, lw.mlp.w1_t.data_ptr(), nm.counts.data_ptr(),
-                  nm.ids.data_ptr(), lw.b1.data_ptr(), ax.data_ptr(), ad.b.data_ptr(), ad.rank, 1.0, 1, out.data_ptr(), f, st)
+                  nm.ids.data_ptr(), lw.b1.data_ptr(), ax.data_ptr(), ad.b.data_ptr(), ad.rank, 1.0, 1, out.data_ptr(), f, wp, st)
 
     for _ in range(3):
         launch()
@@ -236,7 +240,7 @@ def fc1_roofline(model, engine, peaks: dict, reps: int = 20) -> dict:
     prof = ROOT / "profiles" / "r01_fc1_ncu.json"
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-    return {"kernel": "gemm_sm100_kernel<kNGather,kEpiFc1> (neuron_matmul_fwd1+b1+LoRA+ReLU)", "bound": "tensor",
+    return {"kernel": "gemm_sm100_kernel<kPackedN,kEpiFc1> (neuron_matmul_fwd1+b1+LoRA+ReLU over packed active W1 rows)", "bound": "tensor",
             "achieved": round(ach, 1), "peak": peaks["bf16"], "unit": "TFLOP/s", "frac": round(ach / peaks["bf16"], 4),
             "traffic": traffic, "peak_src": f"{peaks['src']} burst bf16 (kernel timed alone)", "ms_per_launch": round(ms, 4),
             "flops_per_launch": flops}

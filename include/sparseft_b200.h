@@ -85,6 +85,8 @@ int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, i
 
 /* ------------------------------------------------------------------ K2 neuron-sparse MLP
  * Layout: w1_t bf16 [d_ff, d] (= W1 column-major, sf/neuron_ops.py:31-45), w2 bf16 [d_ff, d].
+ * w*_packed (optional, from lx_pack_active_rows): the item-packed active rows of the same weight;
+ * when given, the GEMM streams them with one TMA box per 256 rows / 64x64 tile instead of one per block.
  * Hidden tensors are packed per item: row t of item b holds its active columns
  * [0, counts[b]*blk) in ascending block order, row stride ld_h (>= d_ff).
  * LoRA factors are fp32 (trainable); pass NULL to skip a term. */
@@ -94,26 +96,34 @@ int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, i
  * ax1: fp32 [M, r] = x A1 (from lx_rowproj); b1_lora: fp32 [r, d_ff] */
 int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w1_t,
                   const int32_t* counts, const int32_t* ids, const float* b1, const float* ax1, const float* b1_lora,
-                  int r, float scaling, int apply_relu, uint16_t* a_out, int ld_h, lx_stream_t stream);
+                  int r, float scaling, int apply_relu, uint16_t* a_out, int ld_h, const uint16_t* w1_packed,
+                  lx_stream_t stream);
 
 /* neuron_matmul_fwd2 + b2 + scaling*(a A2[cols]) B2   (sf/neuron_ops.py:85-95, sf/model.py:388-395)
  * ax2: fp32 [M, r]; b2_lora: fp32 [r, d]. out bf16, or fp32 (out_f32) with optional fused residual
  * (out = resid + mlp, the block's y + MLP(LN(y)), sf/model.py:427). */
 int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
                   const int32_t* counts, const int32_t* ids, const float* b2, const float* ax2, const float* b2_lora,
-                  int r, float scaling, void* out, int out_f32, const float* resid, lx_stream_t stream);
+                  int r, float scaling, void* out, int out_f32, const float* resid, const uint16_t* w2_packed,
+                  lx_stream_t stream);
 
 /* mlp_backward input-grad through fc2 and ReLU   (sf/autograd.py:97-106)
  * dz = (dO W2[cols]^T + dax2 A2[cols]^T) * (a > 0); dax2 fp32 [M,r] (already scaled); a2: fp32 [d_ff, r] */
 int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
                         const int32_t* counts, const int32_t* ids, const float* dax2, const float* a2_lora, int r,
-                        const uint16_t* a, uint16_t* dz, int ld_h, lx_stream_t stream);
+                        const uint16_t* a, uint16_t* dz, int ld_h, const uint16_t* w2_packed, lx_stream_t stream);
 
 /* mlp_backward input-grad through fc1   (sf/autograd.py:112-120)
  * dx = dz W1[:,cols]^T + dax1 A1^T; dax1 fp32 [M,r] (already scaled); a1: fp32 [d, r] */
 int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d, int d_ff, int blk,
                         const uint16_t* w1_t, const int32_t* counts, const int32_t* ids, const float* dax1,
-                        const float* a1_lora, int r, void* dx, int out_f32, lx_stream_t stream);
+                        const float* a1_lora, int r, void* dx, int out_f32, const uint16_t* w1_packed,
+                        lx_stream_t stream);
+
+/* Copy each item's active neuron-block rows of a [d_ff, d] weight (W1^T or W2), in ascending block
+ * order, into packed [n_items, d_ff, d] rows [0, counts[b]*blk) (sf/neuron_ops.py:67-72 columns). */
+int lx_pack_active_rows(const uint16_t* w, int d_ff, int d, int blk, int n_items, const int32_t* counts,
+                        const int32_t* ids, uint16_t* packed, lx_stream_t stream);
 
 /* Skinny LoRA row projection: Y[M, r] (row stride ldy) = scale * X[M, K] W, K optionally gathered per item.
  *   X bf16 row stride ldx; W(k, q) = w[k_orig*w_sk + q*w_sq]; k_orig = k (dense, counts==NULL) or

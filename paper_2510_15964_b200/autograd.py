@@ -140,7 +140,7 @@ def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims
     dz = torch.empty_like(a)
     _abi.call("lx_neuron_fc2_dgrad", dO.data_ptr(), B, s, d, f, blk, lw.mlp.w2.data_ptr(), nm.counts.data_ptr(),
               nm.ids.data_ptr(), _abi.ptr(dax2), _abi.ptr(ad2.a if ad2 else None), ad2.rank if ad2 else 0, a.data_ptr(),
-              dz.data_ptr(), a.stride(0), st)
+              dz.data_ptr(), a.stride(0), _abi.ptr(cache.get("w2p")), st)
     if ad2 is not None:
         _cg(grads, f"{prefix}w2.lora_a", (f, ad2.rank), dax2, a, B, s, f, ad2.rank, 1.0, 1, ad2.rank, masks=nm, blk=blk)
     if bitfit:
@@ -154,7 +154,7 @@ def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims
     dx = torch.empty(B * s, d, dtype=torch.bfloat16, device=dev)
     _abi.call("lx_neuron_fc1_dgrad", dz.data_ptr(), dz.stride(0), B, s, d, f, blk, lw.mlp.w1_t.data_ptr(),
               nm.counts.data_ptr(), nm.ids.data_ptr(), _abi.ptr(dax1), _abi.ptr(ad1.a if ad1 else None),
-              ad1.rank if ad1 else 0, dx.data_ptr(), 0, st)
+              ad1.rank if ad1 else 0, dx.data_ptr(), 0, _abi.ptr(cache.get("w1p")), st)
     return dx
 
 

@@ -85,6 +85,20 @@ static GemmArgs base_args(int n_items, int rows, int n_dense, int k_dense) {
   return a;
 }
 
+// copy item b's active neuron-block rows (ascending) of a [d_ff, d] weight into packed[b][0 : count*blk]
+// one warp per packed row, 16-byte loads/stores
+__global__ void __launch_bounds__(256) pack_rows_kernel(const uint4* __restrict__ w, int d16, int d_ff, int blk,
+                                                        const int32_t* __restrict__ counts, const int32_t* __restrict__ ids,
+                                                        uint4* __restrict__ packed) {
+  const int item = blockIdx.y;
+  const int prow = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (prow >= __ldg(counts + item) * blk) return;
+  const int src = __ldg(ids + (size_t)item * (d_ff / blk) + prow / blk) * blk + prow % blk;
+  const uint4* sp = w + (size_t)src * d16;
+  uint4* dp = packed + ((size_t)item * d_ff + prow) * d16;
+  for (int i = threadIdx.x & 31; i < d16; i += 32) dp[i] = __ldg(sp + i);
+}
+
 static int check_blk(int blk) {
   LX_REQUIRE(blk == 16 || blk == 32 || blk == 64, LX_ERR_UNSUPPORTED,
              "neuron block size %d unsupported on the sm_100a path (16, 32 or 64)", blk);
@@ -148,20 +162,31 @@ int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, i
                    : launch_gemm<kDense, kEpiFc2, 256>(ta, tb, args, stream);
 }
 
+// B-operand tensor map of an MLP GEMM: gathered blocks of the full weight, or the item-packed copy.
+// N side: K-major boxes [64 K x blk rows] (gather) / [64 K x 256 rows] (packed).
+// K side: MN-major boxes [64 N x blk rows] (gather) / [64 N x 64 rows] (packed).
+static int mlp_tmap_b(CUtensorMap* tb, const uint16_t* w, const uint16_t* wp, int n_items, int d, int d_ff, int blk,
+                      bool n_side) {
+  if (wp) return make_tmap_bf16_2d(tb, wp, d, (uint64_t)n_items * d_ff, d, kBK, n_side ? 256 : 64);
+  return make_tmap_bf16_2d(tb, w, d, d_ff, d, kBK, blk);
+}
+
 int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w1_t,
                   const int32_t* counts, const int32_t* ids, const float* b1, const float* ax1, const float* b1_lora,
-                  int r, float scaling, int apply_relu, uint16_t* a_out, int ld_h, lx_stream_t stream) {
+                  int r, float scaling, int apply_relu, uint16_t* a_out, int ld_h, const uint16_t* w1_packed,
+                  lx_stream_t stream) {
   int rc;
   if ((rc = check_blk(blk))) return rc;
   LX_REQUIRE(d_ff % blk == 0, LX_ERR_MASK, "d_ff %d not a multiple of blk %d on the device path", d_ff, blk);
   CUtensorMap ta, tb;
   if ((rc = make_tmap_bf16_2d(&ta, x, d, (uint64_t)n_items * s, d, kBK, kBM))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, w1_t, d, d_ff, d, kBK, blk))) return rc;
+  if ((rc = mlp_tmap_b(&tb, w1_t, w1_packed, n_items, d, d_ff, blk, true))) return rc;
   GemmArgs args = base_args(n_items, s, 0, d);
   args.counts = counts;
   args.ids = ids;
   args.ids_stride = d_ff / blk;
   args.blk = blk;
+  args.packed_stride = d_ff;
   args.out = a_out;
   args.ldo = ld_h;
   args.bias = b1;
@@ -171,24 +196,30 @@ int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int bl
   args.w_sc = 1;
   args.lora_r = (ax1 && b1_lora) ? r : 0;
   args.lora_scale = scaling;
+  if (w1_packed)
+    return apply_relu ? launch_gemm<kPackedN, kEpiFc1, 256>(ta, tb, args, stream)
+                      : launch_gemm<kPackedN, kEpiFc1Raw, 256>(ta, tb, args, stream);
   return apply_relu ? launch_gemm<kNGather, kEpiFc1, 256>(ta, tb, args, stream)
                     : launch_gemm<kNGather, kEpiFc1Raw, 256>(ta, tb, args, stream);
 }
 
 int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
                   const int32_t* counts, const int32_t* ids, const float* b2, const float* ax2, const float* b2_lora,
-                  int r, float scaling, void* out, int out_f32, const float* resid, lx_stream_t stream) {
+                  int r, float scaling, void* out, int out_f32, const float* resid, const uint16_t* w2_packed,
+                  lx_stream_t stream) {
   int rc;
   if ((rc = check_blk(blk))) return rc;
   LX_REQUIRE(d_ff % blk == 0, LX_ERR_MASK, "d_ff %d not a multiple of blk %d on the device path", d_ff, blk);
+  LX_REQUIRE(!resid || out_f32, LX_ERR_SHAPE, "fc2: residual add needs fp32 output");
   CUtensorMap ta, tb;
   if ((rc = make_tmap_bf16_2d(&ta, a, d_ff, (uint64_t)n_items * s, ld_h, kBK, kBM))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, w2, d, d_ff, d, 64, blk))) return rc;
+  if ((rc = mlp_tmap_b(&tb, w2, w2_packed, n_items, d, d_ff, blk, false))) return rc;
   GemmArgs args = base_args(n_items, s, d, 0);
   args.counts = counts;
   args.ids = ids;
   args.ids_stride = d_ff / blk;
   args.blk = blk;
+  args.packed_stride = d_ff;
   args.out = out;
   args.ldo = d;
   args.bias = b2;
@@ -200,23 +231,24 @@ int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_
   args.lora_scale = scaling;
   args.out_f32 = out_f32;
   args.resid = resid;
-  LX_REQUIRE(!resid || out_f32, LX_ERR_SHAPE, "fc2: residual add needs fp32 output");
+  if (w2_packed) return launch_gemm<kPackedK, kEpiFc2, 256>(ta, tb, args, stream);
   return launch_gemm<kKGather, kEpiFc2, 256>(ta, tb, args, stream);
 }
 
 int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
                         const int32_t* counts, const int32_t* ids, const float* dax2, const float* a2_lora, int r,
-                        const uint16_t* a, uint16_t* dz, int ld_h, lx_stream_t stream) {
+                        const uint16_t* a, uint16_t* dz, int ld_h, const uint16_t* w2_packed, lx_stream_t stream) {
   int rc;
   if ((rc = check_blk(blk))) return rc;
   CUtensorMap ta, tb;
   if ((rc = make_tmap_bf16_2d(&ta, d_out, d, (uint64_t)n_items * s, d, kBK, kBM))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, w2, d, d_ff, d, kBK, blk))) return rc;
+  if ((rc = mlp_tmap_b(&tb, w2, w2_packed, n_items, d, d_ff, blk, true))) return rc;
   GemmArgs args = base_args(n_items, s, 0, d);
   args.counts = counts;
   args.ids = ids;
   args.ids_stride = d_ff / blk;
   args.blk = blk;
+  args.packed_stride = d_ff;
   args.out = dz;
   args.ldo = ld_h;
   args.lora_x = dax2;
@@ -226,22 +258,25 @@ int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_
   args.lora_r = (dax2 && a2_lora) ? r : 0;
   args.act = reinterpret_cast<const __nv_bfloat16*>(a);
   args.ld_act = ld_h;
+  if (w2_packed) return launch_gemm<kPackedN, kEpiDa, 256>(ta, tb, args, stream);
   return launch_gemm<kNGather, kEpiDa, 256>(ta, tb, args, stream);
 }
 
 int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d, int d_ff, int blk,
                         const uint16_t* w1_t, const int32_t* counts, const int32_t* ids, const float* dax1,
-                        const float* a1_lora, int r, void* dx, int out_f32, lx_stream_t stream) {
+                        const float* a1_lora, int r, void* dx, int out_f32, const uint16_t* w1_packed,
+                        lx_stream_t stream) {
   int rc;
   if ((rc = check_blk(blk))) return rc;
   CUtensorMap ta, tb;
   if ((rc = make_tmap_bf16_2d(&ta, dz, d_ff, (uint64_t)n_items * s, ld_h, kBK, kBM))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, w1_t, d, d_ff, d, 64, blk))) return rc;
+  if ((rc = mlp_tmap_b(&tb, w1_t, w1_packed, n_items, d, d_ff, blk, false))) return rc;
   GemmArgs args = base_args(n_items, s, d, 0);
   args.counts = counts;
   args.ids = ids;
   args.ids_stride = d_ff / blk;
   args.blk = blk;
+  args.packed_stride = d_ff;
   args.out = dx;
   args.ldo = d;
   args.lora_x = dax1;
@@ -250,7 +285,17 @@ int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d,
   args.w_sc = r;
   args.lora_r = (dax1 && a1_lora) ? r : 0;
   args.out_f32 = out_f32;
+  if (w1_packed) return launch_gemm<kPackedK, kEpiDx, 256>(ta, tb, args, stream);
   return launch_gemm<kKGather, kEpiDx, 256>(ta, tb, args, stream);
+}
+
+int lx_pack_active_rows(const uint16_t* w, int d_ff, int d, int blk, int n_items, const int32_t* counts,
+                        const int32_t* ids, uint16_t* packed, lx_stream_t stream) {
+  LX_REQUIRE(d % 8 == 0 && d_ff % blk == 0, LX_ERR_SHAPE, "pack_active_rows: d %% 8 and d_ff %% blk required");
+  dim3 grid((d_ff + 7) / 8, n_items);
+  pack_rows_kernel<<<grid, 256, 0, stream>>>(reinterpret_cast<const uint4*>(w), d / 8, d_ff, blk, counts, ids,
+                                             reinterpret_cast<uint4*>(packed));
+  return launch_check("pack_active_rows");
 }
 
 }  // extern "C"

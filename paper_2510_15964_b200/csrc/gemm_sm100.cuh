@@ -20,7 +20,14 @@
 
 namespace lx {
 
-enum BMode : int { kDense = 0, kNGather = 1, kKGather = 2 };
+// kPackedN / kPackedK: the same two gathers, but over an item-packed copy of the active rows
+// ([n_items, packed_stride, K|N], built once per layer by lx_pack_active_rows): one 256-row box
+// (N side) or four 64x64 boxes (K side) per stage instead of one 2 KB box per neuron block.
+enum BMode : int { kDense = 0, kNGather = 1, kKGather = 2, kPackedN = 3, kPackedK = 4 };
+template <int BMODE>
+LX_DEV constexpr bool is_ng() { return BMODE == kNGather || BMODE == kPackedN; }
+template <int BMODE>
+LX_DEV constexpr bool is_kg() { return BMODE == kKGather || BMODE == kPackedK; }
 enum EpiKind : int {
   kEpiStoreF32 = 0,   // C (fp32)
   kEpiStoreBF16 = 1,  // C (bf16)
@@ -63,6 +70,7 @@ struct GemmArgs {
   int bits_stride;
   int out_f32;          // store fp32 instead of bf16 (any epilogue except kEpiMask)
   const float* resid;   // fp32 [rows, ldo]: out = resid + value (fused residual add; requires out_f32)
+  int packed_stride;    // kPacked*: rows per item in the packed weight copy
 };
 
 template <int BN>
@@ -87,7 +95,7 @@ struct TileInfo {
 
 template <int BMODE, int BN>
 LX_DEV int item_n_tiles(const GemmArgs& a, int cnt) {
-  if (BMODE == kNGather) return (cnt * a.blk + BN - 1) / BN;
+  if (is_ng<BMODE>()) return (cnt * a.blk + BN - 1) / BN;
   return (a.n_dense + BN - 1) / BN;
 }
 
@@ -104,9 +112,9 @@ LX_DEV TileInfo decode_tile(const GemmArgs& a, const int* prefix, const int* cnt
   ti.mt = local % m_tiles;
   ti.nt = local / m_tiles;
   int cnt = BMODE == kDense ? 0 : __ldg(cnts + lo);
-  int n_total = BMODE == kNGather ? cnt * a.blk : a.n_dense;
+  int n_total = is_ng<BMODE>() ? cnt * a.blk : a.n_dense;
   ti.n_cols = min(BN, n_total - ti.nt * BN);
-  ti.k_total = BMODE == kKGather ? cnt * a.blk : a.k_dense;
+  ti.k_total = is_kg<BMODE>() ? cnt * a.blk : a.k_dense;
   ti.k_stages = (ti.k_total + kBK - 1) / kBK;
   return ti;
 }
@@ -187,12 +195,18 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         mbar_wait(empty + stage, phase ^ 1);
         if (lane == 0) {
           uint32_t bytes = L::kABytes;
-          if (BMODE == kDense) bytes += BN * kBK * 2;
+          if (BMODE == kDense || BMODE == kPackedN || BMODE == kPackedK) bytes += BN * kBK * 2;
           else if (BMODE == kNGather) bytes += nb_n * args.blk * kBK * 2;
           else bytes += nb_k * (BN / 64) * args.blk * 128;
           mbar_arrive_expect_tx(full + stage, bytes);
           tma_load_2d(sa, &tmap_a, full + stage, ks * kBK, row0);
           if (BMODE == kDense) tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.nt * BN, pol_w);
+          if (BMODE == kPackedN)  // rows [nt*BN, nt*BN+BN) of this item's packed copy, one box
+            tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.item * args.packed_stride + ti.nt * BN, pol_w);
+          if (BMODE == kPackedK)  // 64 packed K-rows x BN columns: one box per 64-column atom
+            for (int a = 0; a < BN / 64; ++a)
+              tma_load_2d_hint(sb + a * (kBK * 128), &tmap_b, full + stage, ti.nt * BN + a * 64,
+                               ti.item * args.packed_stride + ks * kBK, pol_w);
         }
         if (BMODE == kNGather) {
           if ((int)lane < nb_n)
@@ -220,8 +234,8 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         mbar_wait(tempty + buf, use_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
-        int n_mma = BMODE == kNGather ? ((ti.n_cols + 15) / 16) * 16 : BN;
-        const uint32_t idesc = make_idesc_bf16(kBM, n_mma, false, BMODE == kKGather);
+        int n_mma = is_ng<BMODE>() ? ((ti.n_cols + 15) / 16) * 16 : BN;
+        const uint32_t idesc = make_idesc_bf16(kBM, n_mma, false, is_kg<BMODE>());
         for (int ks = 0; ks < ti.k_stages; ++ks) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
@@ -231,7 +245,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           kk_n = (kk_n + 15) / 16;
           for (int kk = 0; kk < kk_n; ++kk) {
             uint64_t da = make_sdesc(sa + kk * 32, 16, 1024);
-            uint64_t db = BMODE == kKGather ? make_sdesc(sb + kk * 2048, kBK * 128, 1024) : make_sdesc(sb + kk * 32, 16, 1024);
+            uint64_t db = is_kg<BMODE>() ? make_sdesc(sb + kk * 2048, kBK * 128, 1024) : make_sdesc(sb + kk * 32, 16, 1024);
             mma_bf16_ss(d_tmem, da, db, idesc, (ks | kk) != 0);
           }
           mma_commit(empty + stage);
@@ -263,7 +277,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         for (int c = ep_tid; c < BN; c += 128) {
           int j = ti.nt * BN + c;
           int oc = j;
-          if (BMODE == kNGather) oc = (c < ti.n_cols) ? __ldg(ids + j / args.blk) * args.blk + j % args.blk : 0;
+          if (is_ng<BMODE>()) oc = (c < ti.n_cols) ? __ldg(ids + j / args.blk) * args.blk + j % args.blk : 0;
           bool ok = c < ti.n_cols;
           s_bias[c] = (ok && args.bias) ? __ldg(args.bias + oc) : 0.f;
           for (int q = 0; q < kMaxR; ++q)

@@ -494,14 +494,17 @@ def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, c
     d, f, blk = dims.d_model, dims.d_ff, dims.blk_size
     nm = lower_mask(neuron_mask, dims.n_blk, blk, B, x2.device)
     ad1, ad2 = lora.get("w1"), lora.get("w2")
+    # active rows of W1^T and W2 packed per item once per layer; reused by the backward's input-grads
+    w1p = neuron_ops.pack_active_rows(lw.mlp.w1_t, nm)
+    w2p = neuron_ops.pack_active_rows(lw.mlp.w2, nm)
     ax1 = rowproj(x2, B, s, d, ad1.a, ad1.rank, 1, ad1.rank) if ad1 is not None else None
     hid = neuron_ops.neuron_matmul_fwd1(x2.view(B, s, d), lw.mlp, nm, blk, counter, bias=lw.b1, ax=ax1,
                                         lora_b=ad1.b if ad1 else None, lora_r=ad1.rank if ad1 else 0,
-                                        scaling=ad1.scaling if ad1 else 1.0, relu=True)
+                                        scaling=ad1.scaling if ad1 else 1.0, relu=True, w_packed=w1p)
     ax2 = rowproj(hid.values, B, s, f, ad2.a, ad2.rank, 1, ad2.rank, masks=nm, blk=blk) if ad2 is not None else None
     out = neuron_ops.neuron_matmul_fwd2(
         hid, lw.mlp, None, counter, bias=lw.b2, ax=ax2, lora_b=ad2.b if ad2 else None, lora_r=ad2.rank if ad2 else 0,
-        scaling=ad2.scaling if ad2 else 1.0, resid=resid,
+        scaling=ad2.scaling if ad2 else 1.0, resid=resid, w_packed=w2p,
         out=torch.empty(B * s, d, dtype=torch.float32, device=x2.device) if (out_f32 or resid is not None) else None)
     if counter is not None:
         n_act = int(nm.counts.sum()) * blk
@@ -509,7 +512,7 @@ def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, c
             counter.add(s * (d + n_act // max(B, 1)) * ad1.rank * B)
         if ad2 is not None:
             counter.add(s * (n_act // max(B, 1) + d) * ad2.rank * B)
-    return out, {"x": x2, "a": hid, "mask": nm, "ax1": ax1, "ax2": ax2, "n_items": B, "s": s}
+    return out, {"x": x2, "a": hid, "mask": nm, "ax1": ax1, "ax2": ax2, "n_items": B, "s": s, "w1p": w1p, "w2p": w2p}
 
 
 def block_forward(x, model: Model, layer: int, masks, counter=None):

@@ -181,7 +181,7 @@ def _check_device_blk(d_ff: int, blk: int) -> None:
 
 
 def neuron_matmul_fwd1(x, weights: LayeredWeights, mask, blk_size: int, counter=None, *, bias=None, ax=None, lora_b=None,
-                       lora_r=0, scaling=1.0, relu=False, out=None) -> ActiveHidden:
+                       lora_r=0, scaling=1.0, relu=False, out=None, w_packed=None) -> ActiveHidden:
     """x @ W1[:, cols] over active column blocks (sf/neuron_ops.py:75-82) on the tcgen05
     N-gather GEMM. Optional fused epilogue (used by mlp_forward): + bias[cols] + scaling*ax B[:,cols], ReLU."""
     d_ff, d = weights.w1_t.shape
@@ -191,14 +191,14 @@ def neuron_matmul_fwd1(x, weights: LayeredWeights, mask, blk_size: int, counter=
     vals = out if out is not None else torch.empty(B * s, d_ff, dtype=torch.bfloat16, device=x2.device)
     _abi.call("lx_neuron_fc1", x2.data_ptr(), B, s, d, d_ff, blk_size, weights.w1_t.data_ptr(), nm.counts.data_ptr(),
               nm.ids.data_ptr(), _abi.ptr(bias), _abi.ptr(ax), _abi.ptr(lora_b), lora_r, float(scaling), int(relu),
-              vals.data_ptr(), d_ff, _abi.stream_handle(x2.device))
+              vals.data_ptr(), d_ff, _abi.ptr(w_packed), _abi.stream_handle(x2.device))
     if counter is not None:
         counter.add(s * d * int(nm.counts.sum()) * blk_size)
     return ActiveHidden(vals, nm, blk_size, d_ff, B)
 
 
 def neuron_matmul_fwd2(hidden: ActiveHidden, weights: LayeredWeights, mask, counter=None, *, bias=None, ax=None,
-                       lora_b=None, lora_r=0, scaling=1.0, out=None, resid=None) -> torch.Tensor:
+                       lora_b=None, lora_r=0, scaling=1.0, out=None, resid=None, w_packed=None) -> torch.Tensor:
     """Packed hidden @ W2[cols, :] (sf/neuron_ops.py:85-95) on the tcgen05 K-gather GEMM.
     With `resid` (fp32 [M, d]) the result is fp32 resid + MLP (fused residual add)."""
     d_ff, d = weights.w2.shape
@@ -215,10 +215,20 @@ def neuron_matmul_fwd2(hidden: ActiveHidden, weights: LayeredWeights, mask, coun
     _abi.call("lx_neuron_fc2", hidden.values.data_ptr(), hidden.values.stride(0), hidden.n_items, s, d, d_ff,
               hidden.blk_size, weights.w2.data_ptr(), nm.counts.data_ptr(), nm.ids.data_ptr(), _abi.ptr(bias),
               _abi.ptr(ax), _abi.ptr(lora_b), lora_r, float(scaling), res.data_ptr(), int(res.dtype == torch.float32),
-              _abi.ptr(resid), _abi.stream_handle(res.device))
+              _abi.ptr(resid), _abi.ptr(w_packed), _abi.stream_handle(res.device))
     if counter is not None:
         counter.add(s * int(nm.counts.sum()) * hidden.blk_size * d)
     return res
+
+
+def pack_active_rows(w: torch.Tensor, masks: NeuronMasks) -> torch.Tensor:
+    """Item-packed copy [B, d_ff, d] of a [d_ff, d] weight's active block rows (ascending), so the
+    tcgen05 GEMMs stream them with large TMA boxes (csrc/abi_gemm.cu lx_pack_active_rows)."""
+    d_ff, d = w.shape
+    out = torch.empty(masks.n_items, d_ff, d, dtype=w.dtype, device=w.device)
+    _abi.call("lx_pack_active_rows", w.data_ptr(), d_ff, d, masks.blk, masks.n_items, masks.counts.data_ptr(),
+              masks.ids.data_ptr(), out.data_ptr(), _abi.stream_handle(w.device))
+    return out
 
 
 # ---------------------------------------------------------------- skinny LoRA helpers (csrc/lora.cu)

@@ -40,7 +40,8 @@ def test_error_mapping_without_gpu():
     if not _abi.LIB_PATH.exists():
         pytest.skip("extension not built")
     with pytest.raises(E.UnsupportedError):
-        _abi.call("lx_neuron_fc1", None, 1, 16, 64, 64, 24, None, None, None, None, None, None, 0, 1.0, 1, None, 64, None)
+        _abi.call("lx_neuron_fc1", None, 1, 16, 64, 64, 24, None, None, None, None, None, None, 0, 1.0, 1, None, 64, None,
+                  None)
     with pytest.raises(E.LayoutError):
         import ctypes
 

@@ -52,7 +52,8 @@ def _masks(n_items, n_blk, density, seed):
 @pytest.mark.parametrize("n_items,s,d,d_ff,blk,density,r", [(2, 128, 128, 512, 16, 0.5, 8), (3, 100, 192, 384, 16, 0.7, 8),
                                                            (4, 512, 2048, 8192, 16, 0.2, 8), (2, 256, 256, 1024, 32, 0.4, 0),
                                                            (2, 128, 128, 512, 64, 0.6, 4)])
-def test_neuron_mlp_gemms(n_items, s, d, d_ff, blk, density, r):
+@pytest.mark.parametrize("packed", [False, True])
+def test_neuron_mlp_gemms(n_items, s, d, d_ff, blk, density, r, packed):
     from paper_2510_15964_b200 import _abi
 
     dev = _dev()
@@ -82,17 +83,25 @@ def test_neuron_mlp_gemms(n_items, s, d, d_ff, blk, density, r):
     scaling = 0.5
     a = torch.zeros(M, ld_h, device=dev, dtype=torch.bfloat16)
     P = lambda t: None if (t is None or r == 0) else t.data_ptr()  # noqa: E731
+    WP1 = WP2 = None
+    if packed:  # item-packed active rows (lx_pack_active_rows) -> kPackedN / kPackedK GEMMs
+        w1p = torch.empty(n_items, d_ff, d, device=dev, dtype=torch.bfloat16)
+        w2p = torch.empty(n_items, d_ff, d, device=dev, dtype=torch.bfloat16)
+        for src, dst in ((w1t, w1p), (w2, w2p)):
+            _abi.call("lx_pack_active_rows", src.data_ptr(), d_ff, d, blk, n_items, cnt_d.data_ptr(), ids_d.data_ptr(),
+                      dst.data_ptr(), st)
+        WP1, WP2 = w1p.data_ptr(), w2p.data_ptr()
     _abi.call("lx_neuron_fc1", x.data_ptr(), n_items, s, d, d_ff, blk, w1t.data_ptr(), cnt_d.data_ptr(), ids_d.data_ptr(),
-              b1.data_ptr(), P(ax1), P(B1), r, scaling, 1, a.data_ptr(), ld_h, st)
+              b1.data_ptr(), P(ax1), P(B1), r, scaling, 1, a.data_ptr(), ld_h, WP1, st)
     out = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
     _abi.call("lx_neuron_fc2", a.data_ptr(), ld_h, n_items, s, d, d_ff, blk, w2.data_ptr(), cnt_d.data_ptr(), ids_d.data_ptr(),
-              b2.data_ptr(), P(ax2), P(B2), r, scaling, out.data_ptr(), 0, None, st)
+              b2.data_ptr(), P(ax2), P(B2), r, scaling, out.data_ptr(), 0, None, WP2, st)
     dz = torch.zeros(M, ld_h, device=dev, dtype=torch.bfloat16)
     _abi.call("lx_neuron_fc2_dgrad", d_out.data_ptr(), n_items, s, d, d_ff, blk, w2.data_ptr(), cnt_d.data_ptr(),
-              ids_d.data_ptr(), P(dax2), P(A2), r, a.data_ptr(), dz.data_ptr(), ld_h, st)
+              ids_d.data_ptr(), P(dax2), P(A2), r, a.data_ptr(), dz.data_ptr(), ld_h, WP2, st)
     dx = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
     _abi.call("lx_neuron_fc1_dgrad", dz.data_ptr(), ld_h, n_items, s, d, d_ff, blk, w1t.data_ptr(), cnt_d.data_ptr(),
-              ids_d.data_ptr(), P(dax1), P(A1), r, dx.data_ptr(), 0, st)
+              ids_d.data_ptr(), P(dax1), P(A1), r, dx.data_ptr(), 0, WP1, st)
     torch.cuda.synchronize()
     for b in range(n_items):
         rows = slice(b * s, (b + 1) * s)

@@ -38,6 +38,6 @@ for dens in (0.15, 1.0):
         ids = torch.zeros(B, n_blk, dtype=torch.int32, device="cuda")
         ids[:, : len(act)] = torch.from_numpy(act).cuda().int()
         fl = 2 * B * s * d * len(act) * blk
-        t1 = timeit(lambda: _abi.call("lx_neuron_fc1", x.data_ptr(), B, s, d, f, blk, w1t.data_ptr(), counts.data_ptr(), ids.data_ptr(), None, None, None, 0, 1.0, 1, out.data_ptr(), f, st))
-        t2 = timeit(lambda: _abi.call("lx_neuron_fc2", a.data_ptr(), f, B, s, d, f, blk, w2.data_ptr(), counts.data_ptr(), ids.data_ptr(), None, None, None, 0, 1.0, o2.data_ptr(), 0, None, st))
+        t1 = timeit(lambda: _abi.call("lx_neuron_fc1", x.data_ptr(), B, s, d, f, blk, w1t.data_ptr(), counts.data_ptr(), ids.data_ptr(), None, None, None, 0, 1.0, 1, out.data_ptr(), f, None, st))
+        t2 = timeit(lambda: _abi.call("lx_neuron_fc2", a.data_ptr(), f, B, s, d, f, blk, w2.data_ptr(), counts.data_ptr(), ids.data_ptr(), None, None, None, 0, 1.0, o2.data_ptr(), 0, None, None, st))
         print(f"density {dens} blk {blk}: fc1 {t1:.4f} ms {fl / t1 / 1e9:.0f} TF/s | fc2 {t2:.4f} ms {fl / t2 / 1e9:.0f} TF/s")
