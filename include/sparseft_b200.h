@@ -159,6 +159,17 @@ int lx_attn_tables(const int32_t* pool_kind_host, const int32_t* pool_param_host
 int lx_bsattn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, int ld, int n_items, int s, int H, int hd,
                   const int32_t* pattern_idx, int item_stride, const int32_t* tables, int n_pool, float scale,
                   uint16_t* o, int ldo, float* lse, lx_stream_t stream);
+/* Same forward on tcgen05 (hd 64 or 128) over the fused projection output qkv [n_items*s, 3*H*hd]
+ * (q | k | v column blocks) and 128x128-tile tables (64-bit cell masks, patterns.tables128_from_grids). */
+int lx_bsattn_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H, int hd, const int32_t* pattern_idx,
+                     int item_stride, const int32_t* tables128, float scale, uint16_t* o, int ldo, float* lse,
+                     lx_stream_t stream);
+/* Backward on tcgen05 (hd 64 or 128): dqkv [n_items*s, 3*H*hd] (same fused layout as qkv) from
+ * d_o [n_items*s, ld_o] and the forward's o / lse; delta_ws fp32 [n_items, H, s]. dK/dV walk the
+ * CSC of each 128-key tile, dQ the CSR of each 128-query tile (sf/block_sparse.py:63-137). */
+int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
+                     int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128, float scale,
+                     const float* lse, float* delta_ws, uint16_t* dqkv, lx_stream_t stream);
 /* dsd_backward -> sparse_softmax_backward -> sdd_backward (sf/block_sparse.py:63-137).
  * o/d_o row stride ld_o; delta_ws fp32 [n_items, H, s]; dq/dk/dv bf16 with stride ld like q. */
 int lx_bsattn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o, const uint16_t* d_o, int ld,

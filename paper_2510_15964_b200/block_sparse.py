@@ -24,6 +24,9 @@ from .patterns import DevicePool
 
 Coord = tuple[int, int]
 
+# tcgen05 kernels for hd in {64, 128} on the fused QKV layout; the warp-MMA kernels cover the rest
+USE_TCGEN05 = True
+
 
 # ---------------------------------------------------------------- fused hot path
 
@@ -36,6 +39,14 @@ def attention_forward(q, k, v, ld: int, n_items: int, s: int, H: int, hd: int, p
     dev = q.device
     o = out if out is not None else torch.empty(n_items * s, H * hd, dtype=torch.bfloat16, device=dev)
     lse = torch.empty(n_items, H, s, dtype=torch.float32, device=dev)
+    d = H * hd
+    fused = (ld == 3 * d and k.data_ptr() == q.data_ptr() + 2 * d and v.data_ptr() == q.data_ptr() + 4 * d)
+    if fused and hd in (64, 128) and dpool.tables128 is not None and USE_TCGEN05:
+        # tcgen05 flash kernel over 128x128 tiles (csrc/attn_sm100.cu)
+        _abi.call("lx_bsattn_fwd_tc", q.data_ptr(), ld, n_items, s, H, hd, pidx.data_ptr(), item_stride,
+                  dpool.tables128.data_ptr(), float(scale), o.data_ptr(), o.stride(0), lse.data_ptr(),
+                  _abi.stream_handle(dev))
+        return o, lse
     _abi.call("lx_bsattn_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), ld, n_items, s, H, hd, pidx.data_ptr(), item_stride,
               dpool.tables.data_ptr(), len(dpool.ids), float(scale), o.data_ptr(), o.stride(0), lse.data_ptr(),
               _abi.stream_handle(dev))
@@ -49,6 +60,15 @@ def attention_backward(q, k, v, o, d_o, ld: int, n_items: int, s: int, H: int, h
     delta = torch.empty(n_items, H, s, dtype=torch.float32, device=dev)
     if d_o.stride(0) != o.stride(0):
         raise LayoutError("attention_backward expects o and d_o with the same row stride")
+    d = H * hd
+    fused = (ld == 3 * d and k.data_ptr() == q.data_ptr() + 2 * d and v.data_ptr() == q.data_ptr() + 4 * d
+             and dk.data_ptr() == dq.data_ptr() + 2 * d and dv.data_ptr() == dq.data_ptr() + 4 * d and dq.stride(0) == ld)
+    if fused and hd in (64, 128) and dpool.tables128 is not None and USE_TCGEN05:
+        # tcgen05 dK/dV (CSC walk) + dQ (CSR walk) over 128x128 tiles (csrc/attn_sm100.cu)
+        _abi.call("lx_bsattn_bwd_tc", q.data_ptr(), ld, o.data_ptr(), d_o.data_ptr(), o.stride(0), n_items, s, H, hd,
+                  pidx.data_ptr(), item_stride, dpool.tables128.data_ptr(), float(scale), lse.data_ptr(),
+                  delta.data_ptr(), dq.data_ptr(), _abi.stream_handle(dev))
+        return
     _abi.call("lx_bsattn_bwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), d_o.data_ptr(), ld, o.stride(0),
               n_items, s, H, hd,
               pidx.data_ptr(), item_stride, dpool.tables.data_ptr(), len(dpool.ids), float(scale), lse.data_ptr(),

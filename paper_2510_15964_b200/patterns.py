@@ -143,10 +143,11 @@ class DevicePool:
     ids: list[str]
     kinds: object  # torch int32 [P]
     params: object  # torch int32 [P]
-    tables: object | None  # torch int32 attention tile tables (None until built for a seq_len)
+    tables: object | None  # torch int32 attention tile tables, 64x64 tiles (None until built for a seq_len)
     seq_len: int = 0
     attn_blk: int = 0
     index: dict = field(default_factory=dict)
+    tables128: object | None = None  # 128x128-tile tables for the tcgen05 attention kernels
 
     def idx(self, pid: str) -> int:
         if pid not in self.index:
@@ -202,6 +203,62 @@ def tables_from_grids(grids: np.ndarray, seq_len: int, attn_blk: int) -> np.ndar
     return out
 
 
+def tables128_from_grids(grids: np.ndarray, seq_len: int, attn_blk: int) -> np.ndarray:
+    """128x128-tile tables for the tcgen05 attention kernels (csrc/attn_sm100.cu): per pattern
+    row_ptr, csr_col, csr_lo, csr_hi, col_ptr, csc_row, csc_lo, csc_hi; a tile's 64-bit mask has
+    bit (ci*8 + cj) set when its 16x16 cell (ci, cj) is active."""
+    from .errors import LayoutError, UnsupportedError
+
+    if attn_blk % 16 or attn_blk < 16:
+        raise UnsupportedError(f"attn_blk {attn_blk} unsupported on the sm_100a path (multiple of 16)")
+    if seq_len % attn_blk:
+        raise LayoutError(f"sequence length {seq_len} != n_b*blk")
+    T = 128
+    P = grids.shape[0]
+    nt = -(-seq_len // T)
+    per = 2 * (nt + 1) + 6 * nt * nt
+    out = np.zeros(4 + P * per, np.int64)
+    out[:4] = (nt, P, seq_len, attn_blk)
+    nc = seq_len // 16
+    ci = np.arange(nc)
+    for p in range(P):
+        cells = grids[p][np.ix_(ci * 16 // attn_blk, ci * 16 // attn_blk)]
+        tm = np.zeros((nt, nt), np.uint64)
+        a_idx, b_idx = np.nonzero(cells)
+        for a, b in zip(a_idx, b_idx):
+            tm[a // 8, b // 8] |= np.uint64(1) << np.uint64((a % 8) * 8 + b % 8)
+        base = 4 + p * per
+        rp, cc, clo, chi = base, base + nt + 1, base + nt + 1 + nt * nt, base + nt + 1 + 2 * nt * nt
+        cp = base + nt + 1 + 3 * nt * nt
+        cr, rlo, rhi = cp + nt + 1, cp + nt + 1 + nt * nt, cp + nt + 1 + 2 * nt * nt
+        n = 0
+        for i in range(nt):
+            out[rp + i] = n
+            for j in np.flatnonzero(tm[i]):
+                out[cc + n], out[clo + n], out[chi + n] = j, int(tm[i, j]) & 0xFFFFFFFF, int(tm[i, j]) >> 32
+                n += 1
+        out[rp + nt] = n
+        n = 0
+        for j in range(nt):
+            out[cp + j] = n
+            for i in np.flatnonzero(tm[:, j]):
+                out[cr + n], out[rlo + n], out[rhi + n] = i, int(tm[i, j]) & 0xFFFFFFFF, int(tm[i, j]) >> 32
+                n += 1
+        out[cp + nt] = n
+        if np.any(out[rp + 1 : rp + nt + 1] == out[rp : rp + nt]):
+            raise LayoutError("a block-row has no active blocks (pattern pool violation)")
+    return out.astype(np.uint32).view(np.int32)
+
+
+def pool_grids(pool: dict[str, LayoutTable]) -> np.ndarray:
+    n_b = next(iter(pool.values())).n_b
+    grids = np.zeros((len(pool), n_b, n_b), bool)
+    for i, t in enumerate(pool.values()):
+        c = np.asarray(t.coords, dtype=np.int64).reshape(-1, 2)
+        grids[i, c[:, 0], c[:, 1]] = True
+    return grids
+
+
 def device_pool(pool: dict[str, LayoutTable], device, seq_len: int | None = None, attn_blk: int | None = None) -> DevicePool:
     import torch
 
@@ -220,5 +277,6 @@ def device_pool(pool: dict[str, LayoutTable], device, seq_len: int | None = None
         host = np.zeros(n.value, np.int32)
         _abi.call("lx_attn_tables", kinds.ctypes.data, params.ctypes.data, len(ids), seq_len, attn_blk, host.ctypes.data, n.value)
         dp.tables = torch.from_numpy(host).to(device)
+        dp.tables128 = torch.from_numpy(tables128_from_grids(pool_grids(pool), seq_len, attn_blk)).to(device)
         dp.seq_len, dp.attn_blk = seq_len, attn_blk
     return dp

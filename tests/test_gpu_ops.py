@@ -215,3 +215,82 @@ def test_pool_tables_match_python(dev):
             c = np.array(t.coords)
             grids[i, c[:, 0], c[:, 1]] = True
         np.testing.assert_array_equal(dp.tables.cpu().numpy(), PT.tables_from_grids(grids, s, ab))
+
+
+@pytest.mark.parametrize("n_items,s,H,hd,attn_blk", [(2, 256, 2, 64, 16), (1, 384, 3, 64, 32), (2, 512, 4, 64, 64),
+                                                      (1, 256, 2, 128, 64), (2, 240, 2, 64, 48), (3, 1024, 2, 64, 128)])
+def test_bsattn_tcgen05_fwd(dev, n_items, s, H, hd, attn_blk):
+    """tcgen05 forward (csrc/attn_sm100.cu, 128x128 tiles) on the fused QKV layout vs the oracle
+    (sdd -> sparse_softmax -> dsd) and vs the warp-MMA kernel; LSE vs the fp64 reference."""
+    from paper_2510_15964_b200 import block_sparse as BS, patterns as PT
+
+    q, k, v, do, grids, pidx, dp = _attn_case(dev, n_items, s, H, hd, attn_blk, seed=s + hd + attn_blk)
+    dp.tables128 = torch.from_numpy(PT.tables128_from_grids(grids, s, attn_blk)).to(dev)
+    d = H * hd
+    qkv = torch.from_numpy(np.concatenate([q, k, v], 1)).to(dev, torch.bfloat16)
+    scale = 1.0 / np.sqrt(hd)
+    o, lse = BS.attention_forward(qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :], 3 * d, n_items, s, H, hd, pidx, H, dp, scale)
+    BS.USE_TCGEN05 = False
+    try:
+        o2, lse2 = BS.attention_forward(qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :], 3 * d, n_items, s, H, hd, pidx, H, dp,
+                                        scale)
+    finally:
+        BS.USE_TCGEN05 = True
+    torch.cuda.synchronize()
+    o, o2, lse, lse2 = o.float().cpu().numpy(), o2.float().cpu().numpy(), lse.cpu().numpy(), lse2.cpu().numpy()
+    assert rel(o, o2) < 1e-2
+    n_b = s // attn_blk
+    for b in range(n_items):
+        rows = slice(b * s, (b + 1) * s)
+        for h in range(H):
+            cols = slice(h * hd, (h + 1) * hd)
+            coords = np.argwhere(grids[b * H + h])
+            qq, kk, vv = (bf(a[rows, cols]) for a in (q, k, v))
+            p = O.sparse_softmax(O.sdd(qq, kk, coords, attn_blk, scale), coords, n_b)
+            assert rel(o[rows, cols], O.dsd(p, vv, coords, n_b)) < 1e-2, (b, h)
+    assert np.abs(lse - lse2).max() < 2e-2
+
+
+@pytest.mark.parametrize("n_items,s,H,hd,attn_blk", [(2, 256, 2, 64, 16), (1, 384, 3, 64, 32), (2, 512, 4, 64, 64),
+                                                      (1, 256, 2, 128, 64), (2, 240, 2, 64, 48), (3, 1024, 2, 64, 128)])
+def test_bsattn_tcgen05_bwd(dev, n_items, s, H, hd, attn_blk):
+    """tcgen05 backward (dK/dV over the CSC walk, dQ over the CSR walk) on the fused dQKV layout vs
+    the oracle chain dsd_backward -> sparse_softmax_backward -> sdd_backward and the warp-MMA kernel."""
+    from paper_2510_15964_b200 import block_sparse as BS, patterns as PT
+
+    q, k, v, do, grids, pidx, dp = _attn_case(dev, n_items, s, H, hd, attn_blk, seed=3 * s + hd + attn_blk)
+    dp.tables128 = torch.from_numpy(PT.tables128_from_grids(grids, s, attn_blk)).to(dev)
+    d = H * hd
+    qkv = torch.from_numpy(np.concatenate([q, k, v], 1)).to(dev, torch.bfloat16)
+    dod = torch.from_numpy(do).to(dev, torch.bfloat16)
+    scale = 1.0 / np.sqrt(hd)
+    Q, K, V = qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :]
+    o, lse = BS.attention_forward(Q, K, V, 3 * d, n_items, s, H, hd, pidx, H, dp, scale)
+    dqkv = torch.full_like(qkv, float("nan"))
+    BS.attention_backward(Q, K, V, o, dod, 3 * d, n_items, s, H, hd, pidx, H, dp, scale, lse,
+                          dqkv[:, :d], dqkv[:, d : 2 * d], dqkv[:, 2 * d :])
+    BS.USE_TCGEN05 = False
+    try:
+        dqkv2 = torch.zeros_like(qkv)
+        BS.attention_backward(Q, K, V, o, dod, 3 * d, n_items, s, H, hd, pidx, H, dp, scale, lse,
+                              dqkv2[:, :d], dqkv2[:, d : 2 * d], dqkv2[:, 2 * d :])
+    finally:
+        BS.USE_TCGEN05 = True
+    torch.cuda.synchronize()
+    g, g2 = dqkv.float().cpu().numpy(), dqkv2.float().cpu().numpy()
+    assert np.isfinite(g).all()
+    assert rel(g, g2) < 2e-2
+    n_b = s // attn_blk
+    for b in range(n_items):
+        rows = slice(b * s, (b + 1) * s)
+        for h in range(H):
+            cols = slice(h * hd, (h + 1) * hd)
+            coords = np.argwhere(grids[b * H + h])
+            qq, kk, vv, dd = (bf(a[rows, cols]) for a in (q, k, v, do))
+            p = O.sparse_softmax(O.sdd(qq, kk, coords, attn_blk, scale), coords, n_b)
+            db, ref_dv = O.dsd_backward(p, vv, dd, coords, n_b)
+            ds = O.sparse_softmax_backward(p, db, coords, n_b)
+            ref_dq, ref_dk = O.sdd_backward(ds, qq, kk, coords, attn_blk, scale)
+            assert rel(g[rows, 2 * d + h * hd : 2 * d + (h + 1) * hd], ref_dv) < 1e-2, (b, h)
+            assert rel(g[rows, cols], ref_dq) < 2e-2, (b, h)
+            assert rel(g[rows, d + h * hd : d + (h + 1) * hd], ref_dk) < 2e-2, (b, h)
