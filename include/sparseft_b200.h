@@ -165,11 +165,13 @@ int lx_bsattn_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H, int
                      int item_stride, const int32_t* tables128, float scale, uint16_t* o, int ldo, float* lse,
                      lx_stream_t stream);
 /* Backward on tcgen05 (hd 64 or 128): dqkv [n_items*s, 3*H*hd] (same fused layout as qkv) from
- * d_o [n_items*s, ld_o] and the forward's o / lse; delta_ws fp32 [n_items, H, s]. dK/dV walk the
- * CSC of each 128-key tile, dQ the CSR of each 128-query tile (sf/block_sparse.py:63-137). */
+ * d_o [n_items*s, ld_o] and the forward's o / lse; delta_ws fp32 [n_items, H, s]; ksum_ws fp32
+ * [n_items, H, ceil(s/128), hd] (per-key-tile column sums of K, used by dQ to cancel the bf16
+ * row-sum residual of dS against the keys' common mode). dK/dV walk the CSC of each 128-key tile,
+ * dQ the CSR of each 128-query tile (sf/block_sparse.py:63-137). */
 int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                      int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128, float scale,
-                     const float* lse, float* delta_ws, uint16_t* dqkv, lx_stream_t stream);
+                     const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv, lx_stream_t stream);
 /* dsd_backward -> sparse_softmax_backward -> sdd_backward (sf/block_sparse.py:63-137).
  * o/d_o row stride ld_o; delta_ws fp32 [n_items, H, s]; dq/dk/dv bf16 with stride ld like q. */
 int lx_bsattn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o, const uint16_t* d_o, int ld,

@@ -65,9 +65,10 @@ def attention_backward(q, k, v, o, d_o, ld: int, n_items: int, s: int, H: int, h
              and dk.data_ptr() == dq.data_ptr() + 2 * d and dv.data_ptr() == dq.data_ptr() + 4 * d and dq.stride(0) == ld)
     if fused and hd in (64, 128) and dpool.tables128 is not None and USE_TCGEN05:
         # tcgen05 dK/dV (CSC walk) + dQ (CSR walk) over 128x128 tiles (csrc/attn_sm100.cu)
+        ksum = torch.empty(n_items, H, (s + 127) // 128, hd, dtype=torch.float32, device=dev)
         _abi.call("lx_bsattn_bwd_tc", q.data_ptr(), ld, o.data_ptr(), d_o.data_ptr(), o.stride(0), n_items, s, H, hd,
                   pidx.data_ptr(), item_stride, dpool.tables128.data_ptr(), float(scale), lse.data_ptr(),
-                  delta.data_ptr(), dq.data_ptr(), _abi.stream_handle(dev))
+                  delta.data_ptr(), ksum.data_ptr(), dq.data_ptr(), _abi.stream_handle(dev))
         return
     _abi.call("lx_bsattn_bwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), d_o.data_ptr(), ld, o.stride(0),
               n_items, s, H, hd,

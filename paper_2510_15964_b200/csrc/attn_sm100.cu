@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(192, 1)
 bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, int s, int H,
                       int d_model, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                       float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
-                      __nv_bfloat16* __restrict__ dkv, int ld_dkv) {
+                      __nv_bfloat16* __restrict__ dkv, int ld_dkv, float* __restrict__ ksum) {
   using L = AttnBwdSmem<HD>;
   constexpr int A = HD / 64;
   extern __shared__ uint8_t smem_raw[];
@@ -494,6 +494,28 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
         }
       }
     }
+    // column sums of this key tile (keys < s) -> ksum[item, h, kt, :], the common mode the dQ
+    // kernel removes (see bsattn_dq_tc_kernel)
+    {
+      constexpr int G = 128 / HD;  // row groups
+      const int col = ep_tid % HD, grp = ep_tid / HD, rows = kAT / G;
+      const uint8_t* katom = sm + (col >> 6) * (kAT * 128);
+      float acc = 0.f;
+      for (int rr = 0; rr < rows; ++rr) {
+        const int r = grp * rows + rr;
+        if (kt * kAT + r < s) {
+          const __nv_bfloat16 kv =
+              *reinterpret_cast<const __nv_bfloat16*>(katom + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4) + (col & 7) * 2);
+          acc += __bfloat162float(kv);
+        }
+      }
+      sL[ep_tid] = acc;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (grp == 0) {
+        for (int g2 = 1; g2 < G; ++g2) acc += sL[g2 * HD + col];
+        ksum[(((size_t)item * H + h) * gridDim.x + kt) * HD + col] = acc;
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -508,7 +530,7 @@ __global__ void __launch_bounds__(192, 1)
 bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, int s, int H,
                     int d_model, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                     float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
-                    __nv_bfloat16* __restrict__ dq, int ld_dq) {
+                    __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ ksum) {
   using L = AttnBwdSmem<HD>;  // [Q | dO | 2 x (K | V) | - | dS]
   constexpr int A = HD / 64;
   extern __shared__ uint8_t smem_raw[];
@@ -598,6 +620,10 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
     const float l2 = __ldg(lse + lrow) * 1.4426950408889634f, dl = __ldg(delta + lrow);
     uint8_t* tDS = sm + L::kOffDS;
     const int ci = r >> 4;
+    // eps = row sum of the bf16 dS fed to the MMA. Exactly, sum_j dS_ij = 0 (softmax Jacobian), so
+    // dq_i = sum_j dS_ij (k_j - kbar) for any kbar; rounding leaves eps != 0, whose product with
+    // the keys' common mode kbar is removed in the epilogue.
+    float eps = 0.f;
     for (int e = 0; e < n; ++e) {
       const uint32_t lo = (uint32_t)__ldg(tv.csr_lo + e0 + e), hi = (uint32_t)__ldg(tv.csr_hi + e0 + e);
       const uint32_t mrow = (uint32_t)((((uint64_t)hi << 32) | lo) >> (ci * 8)) & 0xffu;
@@ -621,6 +647,8 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
             d2[w] = p * (__uint_as_float(dv_[2 * u + w]) - dl);
           }
           dd[u] = pack_bf16x2(d2[0], d2[1]);
+          const __nv_bfloat162 rb = *reinterpret_cast<const __nv_bfloat162*>(&dd[u]);
+          eps += __low2float(rb) + __high2float(rb);
         }
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4)
@@ -631,6 +659,15 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive(p_ready);
     }
+    // kbar = mean over the item's keys (column sums from the dK/dV kernel)
+    float* kbar = reinterpret_cast<float*>(sm + L::kOffP);
+    if (r < HD) {
+      const float* ks = ksum + ((size_t)item * H + h) * gridDim.x * HD + r;
+      float acc = 0.f;
+      for (int t = 0; t < (int)gridDim.x; ++t) acc += __ldg(ks + t * HD);
+      kbar[r] = acc / (float)s;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
     mbar_wait(done, 0);
     tc_fence_after();
 #pragma unroll
@@ -639,14 +676,15 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
       tmem_ld_32x32b_x32(t_dq + lane_base + c * 32, ov);
       tmem_ld_wait();
       if (row < s) {
+        float f[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) f[i] = (__uint_as_float(ov[i]) - eps * kbar[c * 32 + i]) * scale;
         __nv_bfloat16* op = dq + ((size_t)row_base + row) * ld_dq + h * HD + c * 32;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          *reinterpret_cast<uint4*>(op + 8 * i) = make_uint4(
-              pack_bf16x2(__uint_as_float(ov[8 * i]) * scale, __uint_as_float(ov[8 * i + 1]) * scale),
-              pack_bf16x2(__uint_as_float(ov[8 * i + 2]) * scale, __uint_as_float(ov[8 * i + 3]) * scale),
-              pack_bf16x2(__uint_as_float(ov[8 * i + 4]) * scale, __uint_as_float(ov[8 * i + 5]) * scale),
-              pack_bf16x2(__uint_as_float(ov[8 * i + 6]) * scale, __uint_as_float(ov[8 * i + 7]) * scale));
+          *reinterpret_cast<uint4*>(op + 8 * i) =
+              make_uint4(pack_bf16x2(f[8 * i], f[8 * i + 1]), pack_bf16x2(f[8 * i + 2], f[8 * i + 3]),
+                         pack_bf16x2(f[8 * i + 4], f[8 * i + 5]), pack_bf16x2(f[8 * i + 6], f[8 * i + 7]));
       }
     }
   }
@@ -680,7 +718,7 @@ __global__ void bsattn_delta_tc_kernel(const __nv_bfloat16* __restrict__ o, cons
 template <int HD>
 static int launch_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                          int H, const int32_t* pidx, int item_stride, const int32_t* tables128, float scale,
-                         const float* lse, float* delta, uint16_t* dqkv, cudaStream_t st) {
+                         const float* lse, float* delta, float* ksum, uint16_t* dqkv, cudaStream_t st) {
   const int rows = n_items * s;
   bsattn_delta_tc_kernel<<<(rows * H * 32 + 255) / 256, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                                         reinterpret_cast<const __nv_bfloat16*>(d_o), ld_o,
@@ -698,10 +736,10 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const u
   dim3 grid((s + kAT - 1) / kAT, H, n_items);
   const float sl2 = scale * 1.4426950408889634f;
   bsattn_dkdv_tc_kernel<HD><<<grid, 192, smem, st>>>(tm_qkv, tm_do, s, H, ld / 3, pidx, item_stride, tables128, scale, sl2,
-                                                     lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld);
+                                                     lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld, ksum);
   if ((rc = launch_check("bsattn_dkdv_tc"))) return rc;
   bsattn_dq_tc_kernel<HD><<<grid, 192, smem, st>>>(tm_qkv, tm_do, s, H, ld / 3, pidx, item_stride, tables128, scale, sl2,
-                                                   lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld);
+                                                   lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld, ksum);
   return launch_check("bsattn_dq_tc");
 }
 
@@ -713,12 +751,12 @@ extern "C" {
 
 int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                      int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128, float scale,
-                     const float* lse, float* delta_ws, uint16_t* dqkv, lx_stream_t stream) {
+                     const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv, lx_stream_t stream) {
   LX_REQUIRE(ld == 3 * H * hd && ld % 8 == 0 && ld_o % 8 == 0, LX_ERR_SHAPE,
              "attention bwd (tcgen05): qkv / dqkv must be fused [M, 3*H*hd]");
   switch (hd) {
-    case 64: return launch_bwd_tc<64>(qkv, ld, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, dqkv, stream);
-    case 128: return launch_bwd_tc<128>(qkv, ld, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, dqkv, stream);
+    case 64: return launch_bwd_tc<64>(qkv, ld, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, ksum_ws, dqkv, stream);
+    case 128: return launch_bwd_tc<128>(qkv, ld, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, ksum_ws, dqkv, stream);
     default: LX_REQUIRE(false, LX_ERR_UNSUPPORTED, "tcgen05 attention: head_dim %d unsupported (64, 128)", hd);
   }
 }
