@@ -258,11 +258,10 @@ def run_ours(args, cfg, rank, world, dist):
     peaks = load_peaks()
     model, state, provider = build_workload(cfg, dev, seed=args.seed, mlp_sparsity=args.mlp_sparsity,
                                             local_frac=args.local_frac)
-    hook = None
-    if dist is not None and world > 1:
-        def hook(g):
-            dist.all_reduce(g)
-            g.mul_(1.0 / world)
+    from paper_2510_15964_b200.dp import make_grad_hook
+
+    # weak scaling: each rank runs its own B-sequence shard of a global batch of B*world
+    hook = make_grad_hook(dist, cfg["B"] * world, rank, world) if dist is not None else None
     eng = FinetuneEngine(model, state, provider, lr=1e-4, grad_hook=hook)
     B, s, V = cfg["B"], cfg["s"], cfg["V"]
     gen = torch.Generator().manual_seed(args.seed + 2 + rank)  # synthetic uniform tokens, per-rank shard

@@ -1,0 +1,101 @@
+"""Data-parallel step logic (paper_2510_15964_b200/dp.py) on CPU with gloo, world size 2.
+
+Each rank computes the shard-mean gradients of its contiguous batch shard with the oracle
+(the per-sequence fwd/bwd of sf/harness.py:401-411), packs them into a flat fp32 buffer, runs
+the product hook (one all-reduce) and the product's flat Adam (autograd.adam_flat). The result
+must equal the single-process full-batch step (oracle finetune_step): same mean gradients and,
+on every rank, the same updated parameters."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import sf_oracle as O
+
+B_GLOBAL = 3  # ragged shards: 2 + 1
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem():
+    dims = O.Dims(32, 2, 64, 16, 2, 40, 8, 8)
+    m = O.build_model(dims, seed=5, peft="lora")
+    rng = np.random.default_rng(3)
+    for ad in m.lora.values():
+        ad["b"] += (rng.standard_normal(ad["b"].shape) * 0.02).astype(np.float32)
+    toks = rng.integers(0, dims.vocab, size=(B_GLOBAL, dims.seq_len + 1))
+    nm = np.ones(dims.n_blk, bool)
+    nm[[1, 4, 5]] = False
+    masks = [(["blockdiag", "dense"], nm), (["dense", "band1"], ~nm)]  # fixed sparse masks per layer
+    return m, toks, masks
+
+
+def _flat(grads: dict, names) -> torch.Tensor:
+    return torch.from_numpy(np.concatenate([grads[n].ravel() for n in names]).astype(np.float32))
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2510_15964_b200 import autograd as AG
+    from paper_2510_15964_b200.dp import make_grad_hook, shard_range
+
+    m, toks, prov = _problem()
+    names = list(O.trainable_params(m))
+    a, b = shard_range(B_GLOBAL, rank, world)
+    gsum = None
+    for seq in toks[a:b]:
+        logits, cache = O.model_forward(m, seq[:-1], prov)
+        g = O.model_backward(m, cache, O.loss_backward(logits, seq[1:]))
+        f = _flat(g, names)
+        gsum = f if gsum is None else gsum + f
+    flat = gsum / (b - a)  # the engine's shard mean
+    make_grad_hook(dist, B_GLOBAL, rank, world)(flat)
+    p = torch.from_numpy(np.concatenate([O.trainable_params(m)[n].ravel() for n in names]).astype(np.float32))
+    mom, vel = torch.zeros_like(flat, dtype=torch.float64), torch.zeros_like(flat, dtype=torch.float64)
+    AG.adam_flat(p, flat.double(), mom, vel, 1e-3, 0.9, 0.999, 1e-8, 1)
+    out[rank] = (flat.numpy().copy(), p.numpy().copy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_dp_allreduce_equals_full_batch_step():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    m, toks, prov = _problem()
+    names = list(O.trainable_params(m))
+    params = O.trainable_params(m)
+    _, gmean, _ = O.finetune_step(m, toks, prov, params, {}, {}, 0, 1e-3)
+    ref_g = _flat(gmean, names).numpy()
+    ref_p = np.concatenate([params[n].ravel() for n in names])
+    g0, p0 = out[0]
+    g1, p1 = out[1]
+    np.testing.assert_array_equal(g0, g1)  # all-reduce leaves identical buffers
+    np.testing.assert_array_equal(p0, p1)  # replicated Adam stays bit-identical
+    np.testing.assert_allclose(g0, ref_g, rtol=1e-5, atol=1e-6 * np.abs(ref_g).max())  # fp32 summation order
+    np.testing.assert_allclose(p0, ref_p, rtol=1e-6, atol=1e-7)
+
+
+def test_shard_range():
+    from paper_2510_15964_b200.dp import shard_range
+    from paper_2510_15964_b200.errors import ConfigError
+
+    assert [shard_range(8, r, 4) for r in range(4)] == [(0, 2), (2, 4), (4, 6), (6, 8)]
+    assert [shard_range(5, r, 2) for r in range(2)] == [(0, 3), (3, 5)]
+    with pytest.raises(ConfigError):
+        shard_range(1, 0, 2)
+    with pytest.raises(ConfigError):
+        shard_range(4, 2, 2)
