@@ -1,17 +1,15 @@
 // K3 on tcgen05 — block-sparse flash attention forward for sm_100a
 // (sf/block_sparse.py:47-126 fused: SDD -> sparse softmax -> DSD, sf/model.py:343-353).
 //
-// One CTA per (128-query tile, head, item), walking the CSR list of its pool
-// pattern over 128x128 tiles (64-bit masks of active 16x16 cells):
-//   warp 0      TMA producer: Q once, then K_j / V_j tiles into a 2-stage ring
-//   warp 1      MMA issuer (lane 0): S_j = Q K_j^T into TMEM (double-buffered),
-//               then O += P_{j-1} V_{j-1} (software-pipelined one tile behind)
-//   warps 2..5  softmax: thread <-> query row; tcgen05.ld of the S row, -inf on
-//               inactive cells, online max/sum (no shuffles: a thread owns its row),
-//               O rescale in TMEM, P (bf16) into shared memory in the UMMA K-major
-//               SWIZZLE_128B layout, then O / l and the row LSE at the end.
-// Q/K are K-major operands (rows of hd), V is the MN-major B operand of P.V
-// (rows of hd, K = keys) — all three straight from the projection output by TMA.
+// Forward: one CTA per (128-query tile, head, item) walking the CSR list of its pool pattern
+// over 128x128 tiles (64-bit masks of active 16x16 cells); backward: dK/dV per 128-key tile over
+// the CSC list, dQ per 128-query tile over the CSR list. Warp roles in every kernel:
+//   warp 0      TMA producer (Q/K/V/dO tiles straight from the fused projection output)
+//   warp 1      MMA issuer (lane 0)
+//   warps 2..5  softmax: thread <-> tile row (TMEM lane); no shuffles, a thread owns its row
+// P and dS never touch shared memory: they are written as bf16 into TMEM and consumed as the
+// A operand of the next MMA (TS form). Q/K are K-major operands (rows of hd); V, dO, Q, K also
+// serve as MN-major B operands (K = rows) of P.V, P^T.dO, dS^T.Q and dS.K from the same tiles.
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -50,23 +48,48 @@ LX_DEV void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
       "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
 }
+LX_DEV void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
 LX_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// Smem tiles are 128 rows x HD bf16 as [HD/64 atoms][128 rows][128B] (SWIZZLE_128B), used as a
+// K-major operand (rows = M/N, K = hd) or as an MN-major B operand (K = rows, N = hd).
+LX_DEV uint64_t desc_kmajor(uint32_t base, int kk) {  // K = hd step kk (16 elements)
+  return make_sdesc(base + (kk >> 2) * (kAT * 128) + (kk & 3) * 32, 16, 1024);
+}
+LX_DEV uint64_t desc_mnmajor(uint32_t base, int kk) {  // K = rows step kk (16 rows), N = hd atoms at 16KB
+  return make_sdesc(base + kk * 16 * 128, kAT * 128, 1024);
+}
+__host__ __device__ constexpr int tmem_cols_pow2(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+
+// ============================================================================ forward
+// One CTA per (128-query tile, head, item); 2 CTAs per SM at hd=64 (TMEM 256 columns: S/P [0,128),
+// O [128, 128+hd); smem Q + a 2-stage K/V ring = 80 KB), so one CTA's softmax overlaps the other's
+// MMAs, loads and epilogue. Per CSR entry e (key tile j):
+//   MMA:     S = Q K_j^T -> TMEM S region                          (commit s_full)
+//   softmax: mask, online max, rescale O in TMEM when the max moved, P = 2^(S*c - m) as bf16
+//            into the S region's first 64 columns (tcgen05.st)     (arrive p_full)
+//   MMA:     O += P V_j with P read from TMEM (TS form), then S_{e+1} (in issue order, so it may
+//            overwrite P)                                          (commit kv_empty)
 template <int HD>
 struct AttnFwdSmem {
   static constexpr int kAtoms = HD / 64;
-  static constexpr int kQ = kAtoms * kAT * 128;   // [atoms][128 rows][128B]
-  static constexpr int kKV = kAtoms * kAT * 128;  // one K or V tile
-  static constexpr int kP = 2 * kAT * 128;        // [2 key atoms][128 rows][128B]
-  static constexpr int kOffK = kQ;
-  static constexpr int kOffV = kOffK + 2 * kKV;
-  static constexpr int kOffP = kOffV + 2 * kKV;
-  static constexpr int kOffBar = kOffP + kP;
-  static constexpr int kTotal = kOffBar + 256 + 1024;
+  static constexpr int kT = kAtoms * kAT * 128;  // one 128 x HD tile
+  static constexpr int kOffK = kT;
+  static constexpr int kOffV = kOffK + 2 * kT;
+  static constexpr int kOffBar = kOffV + 2 * kT;
+  static constexpr int kTotal = kOffBar + 128 + 1024;
+  static constexpr int kCtas = HD == 64 ? 2 : 1;
+  static constexpr int kTmem = tmem_cols_pow2(kAT + HD);
 };
 
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, AttnFwdSmem<HD>::kCtas)
 bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, int d_model,
                      const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                      float scale_log2, __nv_bfloat16* __restrict__ o, int ldo, float* __restrict__ lse) {
@@ -78,18 +101,16 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_free = bars + 7;    // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* o_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_full = bars + 6;
+  uint64_t* o_done = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
 
   const int qt = blockIdx.x, h = blockIdx.y, item = blockIdx.z;
   const uint32_t warp = warp_id(), lane = lane_id();
   const Tab128 tv = tab128(tables, __ldg(pidx + item * item_stride + h));
-  const int e0 = __ldg(tv.row_ptr + qt), e1 = __ldg(tv.row_ptr + qt + 1);
-  const int n = e1 - e0;
-  const int row_base = item * s;  // first token row of this item in qkv
+  const int e0 = __ldg(tv.row_ptr + qt), n = __ldg(tv.row_ptr + qt + 1) - e0;
+  const int row_base = item * s;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
@@ -97,33 +118,31 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
     for (int i = 0; i < 2; ++i) {
       mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 1);
-      mbar_init(s_full + i, 1);
-      mbar_init(s_free + i, 4);
     }
+    mbar_init(s_full, 1);
     mbar_init(p_full, 4);
     mbar_init(o_done, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 2) tmem_alloc<L::kTmem>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_o = tmem + 2 * kAT;  // O accumulator columns [256, 256+HD)
+  const uint32_t t_s = tmem, t_o = tmem + kAT;
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
       const int qcol = h * HD, kcol = d_model + h * HD, vcol = 2 * d_model + h * HD;
-      mbar_arrive_expect_tx(q_full, L::kQ);
+      mbar_arrive_expect_tx(q_full, L::kT);
       for (int a = 0; a < A; ++a) tma_load_2d(sm + a * kAT * 128, &tm_qkv, q_full, qcol + a * 64, row_base + qt * kAT);
       for (int e = 0; e < n; ++e) {
         const int st = e & 1;
         mbar_wait(kv_empty + st, ((e >> 1) & 1) ^ 1);
         const int j = __ldg(tv.csr_col + e0 + e);
-        mbar_arrive_expect_tx(kv_full + st, 2 * L::kKV);
-        uint8_t* sk = sm + L::kOffK + st * L::kKV;
-        uint8_t* sv = sm + L::kOffV + st * L::kKV;
+        mbar_arrive_expect_tx(kv_full + st, 2 * L::kT);
+        uint8_t* sk = sm + L::kOffK + st * L::kT;
+        uint8_t* sv = sm + L::kOffV + st * L::kT;
         for (int a = 0; a < A; ++a) {
           tma_load_2d(sk + a * kAT * 128, &tm_qkv, kv_full + st, kcol + a * 64, row_base + j * kAT);
           tma_load_2d(sv + a * kAT * 128, &tm_qkv, kv_full + st, vcol + a * 64, row_base + j * kAT);
@@ -131,124 +150,94 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
       }
     }
   } else if (warp == 1) {
-    // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      const uint32_t idesc_s = make_idesc_bf16(kAT, kAT, false, false);  // S = Q K^T: both K-major
-      const uint32_t idesc_o = make_idesc_bf16(kAT, HD, false, true);    // O += P V: V is MN-major
-      const uint32_t sq = smem_u32(sm), sp = smem_u32(sm + L::kOffP);
+      const uint32_t idesc_s = make_idesc_bf16(kAT, kAT, false, false);  // S = Q K^T
+      const uint32_t idesc_o = make_idesc_bf16(kAT, HD, false, true);    // O += P V (V MN-major)
+      const uint32_t sq = smem_u32(sm);
       mbar_wait(q_full, 0);
-      auto issue_pv = [&](int e) {  // O += P_e V_e
+      auto issue_pv = [&](int e) {
         const int st = e & 1;
         mbar_wait(p_full, e & 1);
         tc_fence_after();
-        const uint32_t sv = smem_u32(sm + L::kOffV + st * L::kKV);
-        for (int kk = 0; kk < kAT / 16; ++kk) {
-          const uint64_t da = make_sdesc(sp + (kk >> 2) * (kAT * 128) + (kk & 3) * 32, 16, 1024);
-          const uint64_t db = make_sdesc(sv + kk * 16 * 128, kAT * 128, 1024);
-          mma_bf16_ss(t_o, da, db, idesc_o, (e | kk) != 0);
-        }
-        mma_commit(o_done);
+        const uint32_t sv = smem_u32(sm + L::kOffV + st * L::kT);
+        for (int kk = 0; kk < kAT / 16; ++kk) mma_bf16_ts(t_o, t_s + kk * 8, desc_mnmajor(sv, kk), idesc_o, (e | kk) != 0);
         mma_commit(kv_empty + st);
       };
       for (int e = 0; e < n; ++e) {
         const int st = e & 1;
         mbar_wait(kv_full + st, (e >> 1) & 1);
-        mbar_wait(s_free + st, ((e >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t sk = smem_u32(sm + L::kOffK + st * L::kKV);
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * (kAT * 128) + (kk & 3) * 32;
-          mma_bf16_ss(tmem + st * kAT, make_sdesc(sq + off, 16, 1024), make_sdesc(sk + off, 16, 1024), idesc_s, kk != 0);
-        }
-        mma_commit(s_full + st);
         if (e >= 1) issue_pv(e - 1);
+        tc_fence_after();
+        const uint32_t sk = smem_u32(sm + L::kOffK + st * L::kT);
+        for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_s, desc_kmajor(sq, kk), desc_kmajor(sk, kk), idesc_s, kk != 0);
+        mma_commit(s_full);
       }
       if (n >= 1) issue_pv(n - 1);
+      mma_commit(o_done);
     }
   } else {
-    // ---------------------------------------------------------------- softmax warps
     const int quad = warp & 3;
     const int r = quad * 32 + lane;  // query row within the tile
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     float m = -INFINITY, l = 0.f;
-    uint8_t* prow = sm + L::kOffP + r * 128;
     for (int e = 0; e < n; ++e) {
-      const int st = e & 1;
       const uint32_t lo = (uint32_t)__ldg(tv.csr_lo + e0 + e), hi = (uint32_t)__ldg(tv.csr_hi + e0 + e);
-      const uint64_t mask = ((uint64_t)hi << 32) | lo;
-      const uint32_t mrow = (uint32_t)(mask >> ((r >> 4) * 8)) & 0xffu;  // active 16-key groups of this row
-      mbar_wait(s_full + st, (e >> 1) & 1);
+      const uint32_t mrow = (uint32_t)((((uint64_t)hi << 32) | lo) >> ((r >> 4) * 8)) & 0xffu;  // 16-key groups
+      mbar_wait(s_full, e & 1);
       tc_fence_after();
-      uint32_t sr[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tmem + lane_base + st * kAT + c * 32, sr[c]);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_free + st);
+      // pass 1: row max over the active keys
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < 4; ++c) {
+        uint32_t sv[32];
+        tmem_ld_32x32b_x32(t_s + lane_base + c * 32, sv);
+        tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const bool on = (mrow >> (c * 2 + (i >> 4))) & 1u;
-          float v = on ? __uint_as_float(sr[c][i]) * scale_log2 : -INFINITY;
-          sr[c][i] = __float_as_uint(v);
-          mx = fmaxf(mx, v);
-        }
-      const float m_new = fmaxf(m, mx);
+        for (int i = 0; i < 32; ++i)
+          if ((mrow >> (c * 2 + (i >> 4))) & 1u) mx = fmaxf(mx, __uint_as_float(sv[i]));
+      }
+      const float m_new = fmaxf(m, mx * scale_log2);
       const float use = m_new == -INFINITY ? 0.f : m_new;
-      const float alpha = exp2f(m - use);
+      const float alpha = ex2(m - use);
       m = m_new;
-      float rs = 0.f;
-      uint32_t pk[4][16];
+      // O is stable: s_full(e) was committed after O += P_{e-1} V_{e-1}
+      if (e >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t ov[32];
+          tmem_ld_32x32b_x32(t_o + lane_base + c * 32, ov);
+          tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float p0 = exp2f(__uint_as_float(sr[c][2 * i]) - use);
-          const float p1 = exp2f(__uint_as_float(sr[c][2 * i + 1]) - use);
-          rs += p0 + p1;
-          pk[c][i] = pack_bf16x2(p0, p1);
-        }
-      l = l * alpha + rs;
-      // P_{e-1} V_{e-1} must be complete before P is overwritten and O rescaled
-      if (e >= 1) {
-        mbar_wait(o_done, (e - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll
-          for (int c = 0; c < HD / 32; ++c) {
-            uint32_t ov[32];
-            tmem_ld_32x32b_x32(t_o + lane_base + c * 32, ov);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-            tmem_st_32x32b_x32(t_o + lane_base + c * 32, ov);
-          }
-          tmem_st_wait();
+          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+          tmem_st_32x32b_x32(t_o + lane_base + c * 32, ov);
         }
       }
-      // P row -> shared memory, K-major SWIZZLE_128B: 16B chunk cc of row r at (cc ^ (r & 7))
+      // pass 2: P = 2^(S*c - m) (bf16 pairs) into S columns [0, 64): chunk c -> [16c, 16c+16)
+      float rs = 0.f;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+        uint32_t sv[32];
+        tmem_ld_32x32b_x32(t_s + lane_base + c * 32, sv);
+        tmem_ld_wait();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int chunk = c * 4 + q;  // 16B chunk over the 128 keys (8 keys each)
-          const int atom = chunk >> 3, cc = chunk & 7;
-          *reinterpret_cast<uint4*>(prow + atom * (kAT * 128) + ((cc ^ (r & 7)) << 4)) =
-              make_uint4(pk[c][4 * q], pk[c][4 * q + 1], pk[c][4 * q + 2], pk[c][4 * q + 3]);
+        for (int i = 0; i < 16; ++i) {
+          const bool on = (mrow >> (c * 2 + (i >> 3))) & 1u;
+          const float p0 = on ? ex2(fmaf(__uint_as_float(sv[2 * i]), scale_log2, -use)) : 0.f;
+          const float p1 = on ? ex2(fmaf(__uint_as_float(sv[2 * i + 1]), scale_log2, -use)) : 0.f;
+          rs += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
         }
-      fence_proxy_async_smem();
+        tmem_st_32x32b_x16(t_s + lane_base + c * 16, pk);  // S chunk c/2 already consumed
+      }
+      l = l * alpha + rs;
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
     }
-    // epilogue: O / l -> bf16 rows, LSE
-    if (n >= 1) {
-      mbar_wait(o_done, (n - 1) & 1);
-      tc_fence_after();
-    }
+    mbar_wait(o_done, 0);
+    tc_fence_after();
     const int row = qt * kAT + r;
     const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll
@@ -259,21 +248,22 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
       if (row < s) {
         __nv_bfloat16* op = o + ((size_t)row_base + row) * ldo + h * HD + c * 32;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          *reinterpret_cast<uint4*>(op + 8 * i) = make_uint4(
-              pack_bf16x2(__uint_as_float(ov[8 * i]) * inv, __uint_as_float(ov[8 * i + 1]) * inv),
-              pack_bf16x2(__uint_as_float(ov[8 * i + 2]) * inv, __uint_as_float(ov[8 * i + 3]) * inv),
-              pack_bf16x2(__uint_as_float(ov[8 * i + 4]) * inv, __uint_as_float(ov[8 * i + 5]) * inv),
-              pack_bf16x2(__uint_as_float(ov[8 * i + 6]) * inv, __uint_as_float(ov[8 * i + 7]) * inv));
+        for (int i = 0; i < 4; ++i) {
+          float f[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) f[k] = n > 0 ? __uint_as_float(ov[8 * i + k]) * inv : 0.f;
+          *reinterpret_cast<uint4*>(op + 8 * i) = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                                                             pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+        }
       }
     }
-    if (row < s) lse[((size_t)item * H + h) * s + row] = (m + log2f(l)) * 0.6931471805599453f;
+    if (row < s) lse[((size_t)item * H + h) * s + row] = (m + __log2f(l)) * 0.6931471805599453f;
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<L::kTmem>(tmem);
   }
 }
 
@@ -293,122 +283,125 @@ static int launch_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H,
 }
 
 // ============================================================================ backward
-// Shared pieces: smem tiles of 128 rows x HD (A atoms of [128 rows x 128B]), used either as a
-// K-major operand (rows = M/N, K = hd) or as an MN-major B operand (K = rows, N = hd).
-LX_DEV uint64_t desc_kmajor(uint32_t base, int kk) {  // K = hd step kk (16 elements)
-  return make_sdesc(base + (kk >> 2) * (kAT * 128) + (kk & 3) * 32, 16, 1024);
-}
-LX_DEV uint64_t desc_mnmajor(uint32_t base, int kk) {  // K = rows step kk (16 rows), N = hd atoms at 16KB
-  return make_sdesc(base + kk * 16 * 128, kAT * 128, 1024);
-}
-// bf16x8 chunk (16B) of a 128-wide K-major SWIZZLE_128B row written by the thread owning row r
-LX_DEV void st_swz_chunk(uint8_t* tile, int r, int chunk, uint4 v) {
-  const int atom = chunk >> 3, cc = chunk & 7;
-  *reinterpret_cast<uint4*>(tile + atom * (kAT * 128) + r * 128 + ((cc ^ (r & 7)) << 4)) = v;
-}
-
+// Both kernels keep one 128-column TMEM region R that is reused, in MMA issue order, for
+// S (S^T), dP (dP^T) and -- as bf16 A operands in its first 64 columns -- P (P^T) and dS (dS^T).
+// P stays in registers (bf16) between the two softmax phases of an entry.
 template <int HD>
 struct AttnBwdSmem {
-  static constexpr int kTile = (HD / 64) * kAT * 128;  // 128 rows x HD
-  static constexpr int kPS = 2 * kAT * 128;            // 128 x 128 bf16 operand
-  // dkdv: [K | V | 2 x (Q | dO) | P^T | dS^T | lse2[2][128] | delta[2][128]]
-  static constexpr int kSt = HD == 128 ? 1 : 2;  // Q/dO (dkdv) or K/V (dq) ring stages
-  static constexpr int kOffQ = 2 * kTile;
-  static constexpr int kOffP = kOffQ + 2 * kSt * kTile;
-  static constexpr int kOffDS = kOffP + kPS;
-  static constexpr int kOffL = kOffDS + kPS;
-  static constexpr int kOffBar = kOffL + 4 * kAT * 4;
+  static constexpr int kT = (HD / 64) * kAT * 128;  // 128 rows x HD
+  static constexpr int kSt = 2;                     // Q/dO (dkdv) or K/V (dq) ring stages
+  // [fixed pair (K|V) or (Q|dO)] [kSt x ring pair] [lse2 [kSt][128]] [delta [kSt][128]] [bars]
+  static constexpr int kOffRing = 2 * kT;
+  static constexpr int kOffL = kOffRing + 2 * kSt * kT;
+  static constexpr int kOffBar = kOffL + 2 * kSt * kAT * 4;
   static constexpr int kTotal = kOffBar + 256 + 1024;
+  static constexpr int kCtas = HD == 64 ? 2 : 1;
 };
 
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, AttnBwdSmem<HD>::kCtas)
 bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, int s, int H,
                       int d_model, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                       float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
                       __nv_bfloat16* __restrict__ dkv, int ld_dkv, float* __restrict__ ksum) {
   using L = AttnBwdSmem<HD>;
   constexpr int A = HD / 64;
+  constexpr int kTmem = tmem_cols_pow2(kAT + 2 * HD);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
   uint64_t* kv_full = bars + 0;
-  uint64_t* qd_full = bars + 1;   // [2]
+  uint64_t* qd_full = bars + 1;   // [2]: TMA (1 arrive + tx) + 32 producer lanes (lse/delta)
   uint64_t* qd_empty = bars + 3;  // [2]
-  uint64_t* st_full = bars + 5;
+  uint64_t* s_full = bars + 5;
   uint64_t* p_ready = bars + 6;
-  uint64_t* done = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
-  float* sL = reinterpret_cast<float*>(sm + L::kOffL);  // [2][128] lse * log2(e)
-  float* sD = sL + 2 * kAT;                             // [2][128] delta
+  uint64_t* dp_full = bars + 7;
+  uint64_t* ds_ready = bars + 8;
+  uint64_t* done = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  float* sL = reinterpret_cast<float*>(sm + L::kOffL);  // [kSt][128] lse * log2(e) (+inf past s)
+  float* sD = sL + L::kSt * kAT;                        // [kSt][128] delta
 
   const int kt = blockIdx.x, h = blockIdx.y, item = blockIdx.z;
   const uint32_t warp = warp_id(), lane = lane_id();
   const Tab128 tv = tab128(tables, __ldg(pidx + item * item_stride + h));
   const int e0 = __ldg(tv.col_ptr + kt), n = __ldg(tv.col_ptr + kt + 1) - e0;
   const int row_base = item * s;
-  const float* lse_b = lse + ((size_t)item * H + h) * s;
-  const float* del_b = delta + ((size_t)item * H + h) * s;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
     tma_prefetch_desc(&tm_do);
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(qd_full + i, 1); mbar_init(qd_empty + i, 1); }
-    mbar_init(st_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(qd_full + i, 33);
+      mbar_init(qd_empty + i, 1);
+    }
+    mbar_init(s_full, 1);
     mbar_init(p_ready, 4);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_ready, 4);
     mbar_init(done, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 2) tmem_alloc<kTmem>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s = tmem, t_dp = tmem + kAT, t_dv = tmem + 2 * kAT, t_dk = tmem + 2 * kAT + HD;
+  const uint32_t t_r = tmem, t_dv = tmem + kAT, t_dk = tmem + kAT + HD;
 
   if (warp == 0) {
+    const float* lse_b = lse + ((size_t)item * H + h) * s;
+    const float* del_b = delta + ((size_t)item * H + h) * s;
+    const int qcol = h * HD, kcol = d_model + h * HD, vcol = 2 * d_model + h * HD;
     if (lane == 0) {
-      const int qcol = h * HD, kcol = d_model + h * HD, vcol = 2 * d_model + h * HD;
-      mbar_arrive_expect_tx(kv_full, 2 * L::kTile);
+      mbar_arrive_expect_tx(kv_full, 2 * L::kT);
       for (int a = 0; a < A; ++a) {
         tma_load_2d(sm + a * kAT * 128, &tm_qkv, kv_full, kcol + a * 64, row_base + kt * kAT);
-        tma_load_2d(sm + L::kTile + a * kAT * 128, &tm_qkv, kv_full, vcol + a * 64, row_base + kt * kAT);
+        tma_load_2d(sm + L::kT + a * kAT * 128, &tm_qkv, kv_full, vcol + a * 64, row_base + kt * kAT);
       }
-      for (int e = 0; e < n; ++e) {
-        const int st = e % L::kSt;
-        mbar_wait(qd_empty + st, ((e / L::kSt) & 1) ^ 1);
-        const int i = __ldg(tv.csc_row + e0 + e);
-        uint8_t* sq = sm + L::kOffQ + st * 2 * L::kTile;
-        mbar_arrive_expect_tx(qd_full + st, 2 * L::kTile);
+    }
+    for (int e = 0; e < n; ++e) {
+      const int st = e % L::kSt;
+      mbar_wait(qd_empty + st, ((e / L::kSt) & 1) ^ 1);
+      const int i = __ldg(tv.csc_row + e0 + e);
+      if (lane == 0) {
+        uint8_t* sq = sm + L::kOffRing + st * 2 * L::kT;
+        mbar_arrive_expect_tx(qd_full + st, 2 * L::kT);
         for (int a = 0; a < A; ++a) {
           tma_load_2d(sq + a * kAT * 128, &tm_qkv, qd_full + st, qcol + a * 64, row_base + i * kAT);
-          tma_load_2d(sq + L::kTile + a * kAT * 128, &tm_do, qd_full + st, h * HD + a * 64, row_base + i * kAT);
+          tma_load_2d(sq + L::kT + a * kAT * 128, &tm_do, qd_full + st, h * HD + a * 64, row_base + i * kAT);
         }
       }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int qi = lane * 4 + k, q = i * kAT + qi;
+        sL[st * kAT + qi] = q < s ? __ldg(lse_b + q) * 1.4426950408889634f : INFINITY;
+        sD[st * kAT + qi] = q < s ? __ldg(del_b + q) : 0.f;
+      }
+      mbar_arrive(qd_full + st);
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t id_s = make_idesc_bf16(kAT, kAT, false, false);  // S^T, dP^T: B K-major
       const uint32_t id_g = make_idesc_bf16(kAT, HD, false, true);    // dV, dK: B MN-major
-      const uint32_t sk = smem_u32(sm), sv = sk + L::kTile;
-      const uint32_t sp = smem_u32(sm + L::kOffP), sds = smem_u32(sm + L::kOffDS);
+      const uint32_t sk = smem_u32(sm), sv = sk + L::kT;
       mbar_wait(kv_full, 0);
       for (int e = 0; e < n; ++e) {
         const int st = e % L::kSt;
-        const uint32_t sq = smem_u32(sm + L::kOffQ + st * 2 * L::kTile), sdo = sq + L::kTile;
+        const uint32_t sq = smem_u32(sm + L::kOffRing + st * 2 * L::kT), sdo = sq + L::kT;
         mbar_wait(qd_full + st, (e / L::kSt) & 1);
         tc_fence_after();
-        for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_s, desc_kmajor(sk, kk), desc_kmajor(sq, kk), id_s, kk != 0);
-        for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_dp, desc_kmajor(sv, kk), desc_kmajor(sdo, kk), id_s, kk != 0);
-        mma_commit(st_full);
+        for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_r, desc_kmajor(sk, kk), desc_kmajor(sq, kk), id_s, kk != 0);
+        mma_commit(s_full);
         mbar_wait(p_ready, e & 1);
         tc_fence_after();
-        for (int kk = 0; kk < kAT / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * (kAT * 128) + (kk & 3) * 32;
-          mma_bf16_ss(t_dv, make_sdesc(sp + off, 16, 1024), desc_mnmajor(sdo, kk), id_g, (e | kk) != 0);
-          mma_bf16_ss(t_dk, make_sdesc(sds + off, 16, 1024), desc_mnmajor(sq, kk), id_g, (e | kk) != 0);
-        }
+        for (int kk = 0; kk < kAT / 16; ++kk) mma_bf16_ts(t_dv, t_r + kk * 8, desc_mnmajor(sdo, kk), id_g, (e | kk) != 0);
+        for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_r, desc_kmajor(sv, kk), desc_kmajor(sdo, kk), id_s, kk != 0);
+        mma_commit(dp_full);
+        mbar_wait(ds_ready, e & 1);
+        tc_fence_after();
+        for (int kk = 0; kk < kAT / 16; ++kk) mma_bf16_ts(t_dk, t_r + kk * 8, desc_mnmajor(sq, kk), id_g, (e | kk) != 0);
         mma_commit(qd_empty + st);
       }
       mma_commit(done);
@@ -418,53 +411,56 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
     const int kr = quad * 32 + lane;  // key row within the tile
     const int ep_tid = threadIdx.x - 64;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    uint8_t* tP = sm + L::kOffP;
-    uint8_t* tDS = sm + L::kOffDS;
+    const int cj = kr >> 4;
     for (int e = 0; e < n; ++e) {
-      const int st = e & 1;  // lse/delta slot: entries e and e+2 are separated by the named barrier of e+1
-      const int i = __ldg(tv.csc_row + e0 + e);
-      {
-        const int q = i * kAT + ep_tid;
-        sL[st * kAT + ep_tid] = q < s ? __ldg(lse_b + q) * 1.4426950408889634f : INFINITY;
-        sD[st * kAT + ep_tid] = q < s ? __ldg(del_b + q) : 0.f;
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int st = e % L::kSt;
       const uint32_t lo = (uint32_t)__ldg(tv.csc_lo + e0 + e), hi = (uint32_t)__ldg(tv.csc_hi + e0 + e);
       const uint64_t mask = ((uint64_t)hi << 32) | lo;
-      const int cj = kr >> 4;
-      mbar_wait(st_full, e & 1);
+      const float* l2 = sL + st * kAT;
+      const float* dl = sD + st * kAT;
+      mbar_wait(qd_full + st, (e / L::kSt) & 1);  // lse / delta staged with the tiles
+      mbar_wait(s_full, e & 1);
       tc_fence_after();
+      uint32_t pp[4][16];  // P^T (bf16 pairs) for the whole row, reused by dS^T
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t sv_[32], dv_[32];
-        tmem_ld_32x32b_x32(t_s + lane_base + c * 32, sv_);
-        tmem_ld_32x32b_x32(t_dp + lane_base + c * 32, dv_);
+        uint32_t sv_[32];
+        tmem_ld_32x32b_x32(t_r + lane_base + c * 32, sv_);
         tmem_ld_wait();
-        uint32_t pp[16], dd[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
-          float p2[2], d2[2];
-#pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            const int qi = c * 32 + 2 * u + w;
-            const bool on = (mask >> ((qi >> 4) * 8 + cj)) & 1ull;
-            const float p = on ? exp2f(__uint_as_float(sv_[2 * u + w]) * scale_log2 - sL[st * kAT + qi]) : 0.f;
-            p2[w] = p;
-            d2[w] = p * (__uint_as_float(dv_[2 * u + w]) - sD[st * kAT + qi]);
-          }
-          pp[u] = pack_bf16x2(p2[0], p2[1]);
-          dd[u] = pack_bf16x2(d2[0], d2[1]);
+          const int qi = c * 32 + 2 * u;
+          const bool on = (mask >> ((qi >> 4) * 8 + cj)) & 1ull;
+          const float p0 = on ? ex2(fmaf(__uint_as_float(sv_[2 * u]), scale_log2, -l2[qi])) : 0.f;
+          const float p1 = on ? ex2(fmaf(__uint_as_float(sv_[2 * u + 1]), scale_log2, -l2[qi + 1])) : 0.f;
+          pp[c][u] = pack_bf16x2(p0, p1);
         }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          st_swz_chunk(tP, kr, c * 4 + q4, make_uint4(pp[4 * q4], pp[4 * q4 + 1], pp[4 * q4 + 2], pp[4 * q4 + 3]));
-          st_swz_chunk(tDS, kr, c * 4 + q4, make_uint4(dd[4 * q4], dd[4 * q4 + 1], dd[4 * q4 + 2], dd[4 * q4 + 3]));
-        }
+        tmem_st_32x32b_x16(t_r + lane_base + c * 16, pp[c]);  // S^T chunk c/2 already consumed
       }
-      fence_proxy_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_ready);
+      mbar_wait(dp_full, e & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t dv_[32], dd[16];
+        tmem_ld_32x32b_x32(t_r + lane_base + c * 32, dv_);
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int qi = c * 32 + 2 * u;
+          const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pp[c][u]);
+          dd[u] = pack_bf16x2(__low2float(pb) * (__uint_as_float(dv_[2 * u]) - dl[qi]),
+                              __high2float(pb) * (__uint_as_float(dv_[2 * u + 1]) - dl[qi + 1]));
+        }
+        tmem_st_32x32b_x16(t_r + lane_base + c * 16, dd);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_ready);
     }
     mbar_wait(done, 0);
     tc_fence_after();
@@ -478,24 +474,21 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
         uint32_t ov[32];
         tmem_ld_32x32b_x32(tcol + lane_base + c * 32, ov);
         tmem_ld_wait();
-        if (key < s && n > 0) {
+        if (key < s) {  // n == 0: no query tile attends to this key tile -> zero gradient
           __nv_bfloat16* op = dkv + ((size_t)row_base + key) * ld_dkv + (which + 1) * d_model + h * HD + c * 32;
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            *reinterpret_cast<uint4*>(op + 8 * i) = make_uint4(
-                pack_bf16x2(__uint_as_float(ov[8 * i]) * mul, __uint_as_float(ov[8 * i + 1]) * mul),
-                pack_bf16x2(__uint_as_float(ov[8 * i + 2]) * mul, __uint_as_float(ov[8 * i + 3]) * mul),
-                pack_bf16x2(__uint_as_float(ov[8 * i + 4]) * mul, __uint_as_float(ov[8 * i + 5]) * mul),
-                pack_bf16x2(__uint_as_float(ov[8 * i + 6]) * mul, __uint_as_float(ov[8 * i + 7]) * mul));
-        } else if (key < s) {  // no query tile attends to this key tile: zero gradient
-          __nv_bfloat16* op = dkv + ((size_t)row_base + key) * ld_dkv + (which + 1) * d_model + h * HD + c * 32;
+          for (int i = 0; i < 4; ++i) {
+            float f[8];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) *reinterpret_cast<uint4*>(op + 8 * i) = make_uint4(0u, 0u, 0u, 0u);
+            for (int k = 0; k < 8; ++k) f[k] = n > 0 ? __uint_as_float(ov[8 * i + k]) * mul : 0.f;
+            *reinterpret_cast<uint4*>(op + 8 * i) = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                                                               pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+          }
         }
       }
     }
-    // column sums of this key tile (keys < s) -> ksum[item, h, kt, :], the common mode the dQ
-    // kernel removes (see bsattn_dq_tc_kernel)
+    // column sums of this key tile (keys < s) -> ksum[item, h, kt, :]: the common mode the dQ
+    // kernel removes (see bsattn_dq_tc_kernel). K is still resident; sL is free now.
     {
       constexpr int G = 128 / HD;  // row groups
       const int col = ep_tid % HD, grp = ep_tid / HD, rows = kAT / G;
@@ -503,11 +496,9 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       float acc = 0.f;
       for (int rr = 0; rr < rows; ++rr) {
         const int r = grp * rows + rr;
-        if (kt * kAT + r < s) {
-          const __nv_bfloat16 kv =
-              *reinterpret_cast<const __nv_bfloat16*>(katom + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4) + (col & 7) * 2);
-          acc += __bfloat162float(kv);
-        }
+        if (kt * kAT + r < s)
+          acc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+              katom + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4) + (col & 7) * 2));
       }
       sL[ep_tid] = acc;
       asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -521,28 +512,32 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<kTmem>(tmem);
   }
 }
 
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, AttnBwdSmem<HD>::kCtas)
 bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, int s, int H,
                     int d_model, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                     float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
                     __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ ksum) {
-  using L = AttnBwdSmem<HD>;  // [Q | dO | 2 x (K | V) | - | dS]
+  using L = AttnBwdSmem<HD>;  // [Q | dO] [kSt x (K | V)] [kbar]
   constexpr int A = HD / 64;
+  constexpr int kTmem = tmem_cols_pow2(kAT + HD);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* st_full = bars + 5;
-  uint64_t* p_ready = bars + 6;
-  uint64_t* done = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_done = bars + 6;
+  uint64_t* dp_full = bars + 7;
+  uint64_t* ds_ready = bars + 8;
+  uint64_t* done = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  float* kbar = reinterpret_cast<float*>(sm + L::kOffL);
 
   const int qt = blockIdx.x, h = blockIdx.y, item = blockIdx.z;
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -554,36 +549,41 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
     tma_prefetch_desc(&tm_qkv);
     tma_prefetch_desc(&tm_do);
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
-    mbar_init(st_full, 1);
-    mbar_init(p_ready, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_done, 4);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_ready, 4);
     mbar_init(done, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 2) tmem_alloc<kTmem>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s = tmem, t_dp = tmem + kAT, t_dq = tmem + 2 * kAT;
+  const uint32_t t_r = tmem, t_dq = tmem + kAT;
 
   if (warp == 0) {
     if (lane == 0) {
       const int qcol = h * HD, kcol = d_model + h * HD, vcol = 2 * d_model + h * HD;
-      mbar_arrive_expect_tx(q_full, 2 * L::kTile);
+      mbar_arrive_expect_tx(q_full, 2 * L::kT);
       for (int a = 0; a < A; ++a) {
         tma_load_2d(sm + a * kAT * 128, &tm_qkv, q_full, qcol + a * 64, row_base + qt * kAT);
-        tma_load_2d(sm + L::kTile + a * kAT * 128, &tm_do, q_full, h * HD + a * 64, row_base + qt * kAT);
+        tma_load_2d(sm + L::kT + a * kAT * 128, &tm_do, q_full, h * HD + a * 64, row_base + qt * kAT);
       }
       for (int e = 0; e < n; ++e) {
         const int st = e % L::kSt;
         mbar_wait(kv_empty + st, ((e / L::kSt) & 1) ^ 1);
         const int j = __ldg(tv.csr_col + e0 + e);
-        uint8_t* skv = sm + L::kOffQ + st * 2 * L::kTile;
-        mbar_arrive_expect_tx(kv_full + st, 2 * L::kTile);
+        uint8_t* skv = sm + L::kOffRing + st * 2 * L::kT;
+        mbar_arrive_expect_tx(kv_full + st, 2 * L::kT);
         for (int a = 0; a < A; ++a) {
           tma_load_2d(skv + a * kAT * 128, &tm_qkv, kv_full + st, kcol + a * 64, row_base + j * kAT);
-          tma_load_2d(skv + L::kTile + a * kAT * 128, &tm_qkv, kv_full + st, vcol + a * 64, row_base + j * kAT);
+          tma_load_2d(skv + L::kT + a * kAT * 128, &tm_qkv, kv_full + st, vcol + a * 64, row_base + j * kAT);
         }
       }
     }
@@ -591,22 +591,22 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
     if (lane == 0) {
       const uint32_t id_s = make_idesc_bf16(kAT, kAT, false, false);
       const uint32_t id_g = make_idesc_bf16(kAT, HD, false, true);
-      const uint32_t sq = smem_u32(sm), sdo = sq + L::kTile, sds = smem_u32(sm + L::kOffDS);
+      const uint32_t sq = smem_u32(sm), sdo = sq + L::kT;
       mbar_wait(q_full, 0);
       for (int e = 0; e < n; ++e) {
         const int st = e % L::kSt;
-        const uint32_t sk = smem_u32(sm + L::kOffQ + st * 2 * L::kTile), sv = sk + L::kTile;
+        const uint32_t sk = smem_u32(sm + L::kOffRing + st * 2 * L::kT), sv = sk + L::kT;
         mbar_wait(kv_full + st, (e / L::kSt) & 1);
         tc_fence_after();
-        for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_s, desc_kmajor(sq, kk), desc_kmajor(sk, kk), id_s, kk != 0);
-        for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_dp, desc_kmajor(sdo, kk), desc_kmajor(sv, kk), id_s, kk != 0);
-        mma_commit(st_full);
-        mbar_wait(p_ready, e & 1);
+        for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_r, desc_kmajor(sq, kk), desc_kmajor(sk, kk), id_s, kk != 0);
+        mma_commit(s_full);
+        mbar_wait(p_done, e & 1);
         tc_fence_after();
-        for (int kk = 0; kk < kAT / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * (kAT * 128) + (kk & 3) * 32;
-          mma_bf16_ss(t_dq, make_sdesc(sds + off, 16, 1024), desc_mnmajor(sk, kk), id_g, (e | kk) != 0);
-        }
+        for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_r, desc_kmajor(sdo, kk), desc_kmajor(sv, kk), id_s, kk != 0);
+        mma_commit(dp_full);
+        mbar_wait(ds_ready, e & 1);
+        tc_fence_after();
+        for (int kk = 0; kk < kAT / 16; ++kk) mma_bf16_ts(t_dq, t_r + kk * 8, desc_mnmajor(sk, kk), id_g, (e | kk) != 0);
         mma_commit(kv_empty + st);
       }
       mma_commit(done);
@@ -618,7 +618,6 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
     const int row = qt * kAT + r;
     const size_t lrow = ((size_t)item * H + h) * s + (row < s ? row : 0);
     const float l2 = __ldg(lse + lrow) * 1.4426950408889634f, dl = __ldg(delta + lrow);
-    uint8_t* tDS = sm + L::kOffDS;
     const int ci = r >> 4;
     // eps = row sum of the bf16 dS fed to the MMA. Exactly, sum_j dS_ij = 0 (softmax Jacobian), so
     // dq_i = sum_j dS_ij (k_j - kbar) for any kbar; rounding leaves eps != 0, whose product with
@@ -627,40 +626,48 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
     for (int e = 0; e < n; ++e) {
       const uint32_t lo = (uint32_t)__ldg(tv.csr_lo + e0 + e), hi = (uint32_t)__ldg(tv.csr_hi + e0 + e);
       const uint32_t mrow = (uint32_t)((((uint64_t)hi << 32) | lo) >> (ci * 8)) & 0xffu;
-      mbar_wait(st_full, e & 1);
+      mbar_wait(s_full, e & 1);
+      tc_fence_after();
+      uint32_t pp[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t sv_[32];
+        tmem_ld_32x32b_x32(t_r + lane_base + c * 32, sv_);
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const bool on = (mrow >> (c * 2 + (u >> 3))) & 1u;
+          const float p0 = on ? ex2(fmaf(__uint_as_float(sv_[2 * u]), scale_log2, -l2)) : 0.f;
+          const float p1 = on ? ex2(fmaf(__uint_as_float(sv_[2 * u + 1]), scale_log2, -l2)) : 0.f;
+          pp[c][u] = pack_bf16x2(p0, p1);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_done);
+      mbar_wait(dp_full, e & 1);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t sv_[32], dv_[32];
-        tmem_ld_32x32b_x32(t_s + lane_base + c * 32, sv_);
-        tmem_ld_32x32b_x32(t_dp + lane_base + c * 32, dv_);
+        uint32_t dv_[32], dd[16];
+        tmem_ld_32x32b_x32(t_r + lane_base + c * 32, dv_);
         tmem_ld_wait();
-        uint32_t dd[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
-          float d2[2];
-#pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            const int ki = c * 32 + 2 * u + w;
-            const bool on = (mrow >> (ki >> 4)) & 1u;
-            const float p = on ? exp2f(__uint_as_float(sv_[2 * u + w]) * scale_log2 - l2) : 0.f;
-            d2[w] = p * (__uint_as_float(dv_[2 * u + w]) - dl);
-          }
-          dd[u] = pack_bf16x2(d2[0], d2[1]);
+          const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pp[c][u]);
+          dd[u] = pack_bf16x2(__low2float(pb) * (__uint_as_float(dv_[2 * u]) - dl),
+                              __high2float(pb) * (__uint_as_float(dv_[2 * u + 1]) - dl));
           const __nv_bfloat162 rb = *reinterpret_cast<const __nv_bfloat162*>(&dd[u]);
           eps += __low2float(rb) + __high2float(rb);
         }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          st_swz_chunk(tDS, r, c * 4 + q4, make_uint4(dd[4 * q4], dd[4 * q4 + 1], dd[4 * q4 + 2], dd[4 * q4 + 3]));
+        tmem_st_32x32b_x16(t_r + lane_base + c * 16, dd);  // dP chunk c/2 already consumed
       }
-      fence_proxy_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_ready);
+      if (lane == 0) mbar_arrive(ds_ready);
     }
     // kbar = mean over the item's keys (column sums from the dK/dV kernel)
-    float* kbar = reinterpret_cast<float*>(sm + L::kOffP);
     if (r < HD) {
       const float* ks = ksum + ((size_t)item * H + h) * gridDim.x * HD + r;
       float acc = 0.f;
@@ -678,7 +685,7 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
       if (row < s) {
         float f[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] = (__uint_as_float(ov[i]) - eps * kbar[c * 32 + i]) * scale;
+        for (int i = 0; i < 32; ++i) f[i] = n > 0 ? (__uint_as_float(ov[i]) - eps * kbar[c * 32 + i]) * scale : 0.f;
         __nv_bfloat16* op = dq + ((size_t)row_base + row) * ld_dq + h * HD + c * 32;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -692,7 +699,7 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<kTmem>(tmem);
   }
 }
 

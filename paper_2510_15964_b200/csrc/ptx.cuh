@@ -102,6 +102,22 @@ LX_DEV void mma_bf16_ss(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint3
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
 }
+// D[tmem] (+)= A[tmem] * B[smem]^T (A K-major in TMEM: row m in lane m, bf16 pairs per 32-bit
+// column, a K=16 step = 8 columns). MMAs of one thread execute in issue order, so a later MMA
+// may overwrite the A columns an earlier one reads.
+LX_DEV void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
+}
+// 2^x on the MUFU without exp2f's denormal range fix-up (ftz; 2^-inf = +0).
+LX_DEV float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 // Arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete.
 LX_DEV void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
