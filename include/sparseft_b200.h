@@ -172,6 +172,9 @@ int lx_bsattn_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H, int
 int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                      int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128, float scale,
                      const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv, lx_stream_t stream);
+/* Debug only: per-CTA clock64 phase stamps of the tcgen05 attention kernels into buf
+ * [n_ctas][32] (slot 31 = SM id); NULL disables. Used by tools/attn_trace.py. */
+int lx_debug_set_attn_trace(unsigned long long* buf);
 /* dsd_backward -> sparse_softmax_backward -> sdd_backward (sf/block_sparse.py:63-137).
  * o/d_o row stride ld_o; delta_ws fp32 [n_items, H, s]; dq/dk/dv bf16 with stride ld like q. */
 int lx_bsattn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o, const uint16_t* d_o, int ld,

@@ -43,6 +43,7 @@ SIGNATURES: dict[str, list] = {
     "lx_attn_tables": [_P, _P, _I, _I, _I, _P, _I],
     "lx_bsattn_fwd": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _I, _P, _P],
     "lx_bsattn_fwd_tc": [_P, _I, _I, _I, _I, _I, _P, _I, _P, _F, _P, _I, _P, _P],
+    "lx_debug_set_attn_trace": [_P],
     "lx_bsattn_bwd_tc": [_P, _I, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _F, _P, _P, _P, _P, _P],
     "lx_bsattn_bwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P, _P],
     "lx_layernorm_fwd": [_P, _P, _P, _I, _I, _P, _P, _F, _P, _P, _P, _I, _I, _P, _P],

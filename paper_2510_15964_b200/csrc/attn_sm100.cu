@@ -17,6 +17,23 @@ namespace lx {
 
 constexpr int kAT = 128;  // query / key tile edge
 
+// Debug-only phase trace (lx_debug_set_attn_trace): per CTA 32 clock64 stamps, NULL in production.
+__device__ unsigned long long* g_attn_trace = nullptr;
+LX_DEV void trace_stamp(int slot) {
+  unsigned long long* t = g_attn_trace;
+  if (t != nullptr) {
+    const size_t cta = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    t[cta * 32 + slot] = c;
+    if (slot == 0) {
+      unsigned smid;
+      asm("mov.u32 %0, %%smid;" : "=r"(smid));
+      t[cta * 32 + 31] = smid;
+    }
+  }
+}
+
 // 128x128 tile tables (built by patterns.tables_from_grids(tile=128)): per pattern
 // row_ptr[nt+1] csr_col[nt2] csr_lo[nt2] csr_hi[nt2] col_ptr[nt+1] csc_row[nt2] csc_lo[nt2] csc_hi[nt2]
 struct Tab128 {
@@ -113,6 +130,7 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
   const int row_base = item * s;
 
   if (warp == 0 && lane == 0) {
+    trace_stamp(0);
     tma_prefetch_desc(&tm_qkv);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
@@ -154,7 +172,9 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
       const uint32_t idesc_s = make_idesc_bf16(kAT, kAT, false, false);  // S = Q K^T
       const uint32_t idesc_o = make_idesc_bf16(kAT, HD, false, true);    // O += P V (V MN-major)
       const uint32_t sq = smem_u32(sm);
+      trace_stamp(1);
       mbar_wait(q_full, 0);
+      trace_stamp(2);
       auto issue_pv = [&](int e) {
         const int st = e & 1;
         mbar_wait(p_full, e & 1);
@@ -166,6 +186,7 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
       for (int e = 0; e < n; ++e) {
         const int st = e & 1;
         mbar_wait(kv_full + st, (e >> 1) & 1);
+        if (e < 4) trace_stamp(4 + e);
         if (e >= 1) issue_pv(e - 1);
         tc_fence_after();
         const uint32_t sk = smem_u32(sm + L::kOffK + st * L::kT);
@@ -184,22 +205,38 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
       const uint32_t lo = (uint32_t)__ldg(tv.csr_lo + e0 + e), hi = (uint32_t)__ldg(tv.csr_hi + e0 + e);
       const uint32_t mrow = (uint32_t)((((uint64_t)hi << 32) | lo) >> ((r >> 4) * 8)) & 0xffu;  // 16-key groups
       mbar_wait(s_full, e & 1);
+      if (r == 0 && e < 4) trace_stamp(8 + e);
       tc_fence_after();
-      // pass 1: row max over the active keys
+      // the whole S row in registers (one wait), row max over the active keys
+      uint32_t sv[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + lane_base + c * 32, sv[c]);
+      tmem_ld_wait();
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t sv[32];
-        tmem_ld_32x32b_x32(t_s + lane_base + c * 32, sv);
-        tmem_ld_wait();
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if ((mrow >> (c * 2 + (i >> 4))) & 1u) mx = fmaxf(mx, __uint_as_float(sv[i]));
-      }
+          if ((mrow >> (c * 2 + (i >> 4))) & 1u) mx = fmaxf(mx, __uint_as_float(sv[c][i]));
       const float m_new = fmaxf(m, mx * scale_log2);
       const float use = m_new == -INFINITY ? 0.f : m_new;
       const float alpha = ex2(m - use);
       m = m_new;
+      // P = 2^(S*c - m) (bf16 pairs) into S columns [0, 64): chunk c -> [16c, 16c+16)
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const bool on = (mrow >> (c * 2 + (i >> 3))) & 1u;
+          const float p0 = on ? ex2(fmaf(__uint_as_float(sv[c][2 * i]), scale_log2, -use)) : 0.f;
+          const float p1 = on ? ex2(fmaf(__uint_as_float(sv[c][2 * i + 1]), scale_log2, -use)) : 0.f;
+          rs += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+        tmem_st_32x32b_x16(t_s + lane_base + c * 16, pk);
+      }
       // O is stable: s_full(e) was committed after O += P_{e-1} V_{e-1}
       if (e >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
@@ -212,31 +249,15 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
           tmem_st_32x32b_x32(t_o + lane_base + c * 32, ov);
         }
       }
-      // pass 2: P = 2^(S*c - m) (bf16 pairs) into S columns [0, 64): chunk c -> [16c, 16c+16)
-      float rs = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
-        uint32_t sv[32];
-        tmem_ld_32x32b_x32(t_s + lane_base + c * 32, sv);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const bool on = (mrow >> (c * 2 + (i >> 3))) & 1u;
-          const float p0 = on ? ex2(fmaf(__uint_as_float(sv[2 * i]), scale_log2, -use)) : 0.f;
-          const float p1 = on ? ex2(fmaf(__uint_as_float(sv[2 * i + 1]), scale_log2, -use)) : 0.f;
-          rs += p0 + p1;
-          pk[i] = pack_bf16x2(p0, p1);
-        }
-        tmem_st_32x32b_x16(t_s + lane_base + c * 16, pk);  // S chunk c/2 already consumed
-      }
       l = l * alpha + rs;
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      if (r == 0 && e < 4) trace_stamp(12 + e);
     }
     mbar_wait(o_done, 0);
+    if (r == 0) trace_stamp(16);
     tc_fence_after();
     const int row = qt * kAT + r;
     const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -258,12 +279,14 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
       }
     }
     if (row < s) lse[((size_t)item * H + h) * s + row] = (m + __log2f(l)) * 0.6931471805599453f;
+    if (r == 0) trace_stamp(17);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<L::kTmem>(tmem);
+    if (lane == 0) trace_stamp(18);
   }
 }
 
@@ -423,19 +446,24 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       tc_fence_after();
       uint32_t pp[4][16];  // P^T (bf16 pairs) for the whole row, reused by dS^T
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t sv_[32];
-        tmem_ld_32x32b_x32(t_r + lane_base + c * 32, sv_);
+      for (int h2 = 0; h2 < 2; ++h2) {
+        uint32_t sv_[2][32];
+        tmem_ld_32x32b_x32(t_r + lane_base + h2 * 64, sv_[0]);
+        tmem_ld_32x32b_x32(t_r + lane_base + h2 * 64 + 32, sv_[1]);
         tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int qi = c * 32 + 2 * u;
-          const bool on = (mask >> ((qi >> 4) * 8 + cj)) & 1ull;
-          const float p0 = on ? ex2(fmaf(__uint_as_float(sv_[2 * u]), scale_log2, -l2[qi])) : 0.f;
-          const float p1 = on ? ex2(fmaf(__uint_as_float(sv_[2 * u + 1]), scale_log2, -l2[qi + 1])) : 0.f;
-          pp[c][u] = pack_bf16x2(p0, p1);
+        for (int c2 = 0; c2 < 2; ++c2) {
+          const int c = h2 * 2 + c2;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int qi = c * 32 + 2 * u;
+            const bool on = (mask >> ((qi >> 4) * 8 + cj)) & 1ull;
+            const float p0 = on ? ex2(fmaf(__uint_as_float(sv_[c2][2 * u]), scale_log2, -l2[qi])) : 0.f;
+            const float p1 = on ? ex2(fmaf(__uint_as_float(sv_[c2][2 * u + 1]), scale_log2, -l2[qi + 1])) : 0.f;
+            pp[c][u] = pack_bf16x2(p0, p1);
+          }
+          tmem_st_32x32b_x16(t_r + lane_base + c * 16, pp[c]);  // S^T chunk c/2 already consumed
         }
-        tmem_st_32x32b_x16(t_r + lane_base + c * 16, pp[c]);  // S^T chunk c/2 already consumed
       }
       tmem_st_wait();
       tc_fence_before();
@@ -755,6 +783,13 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const u
 using namespace lx;
 
 extern "C" {
+
+// Debug: route the tcgen05 attention kernels' per-CTA phase stamps to a device buffer of
+// [n_ctas][32] uint64 (NULL disables). Not part of the production path.
+int lx_debug_set_attn_trace(unsigned long long* buf) {
+  LX_CHECK_CUDA(cudaMemcpyToSymbol(g_attn_trace, &buf, sizeof(buf)));
+  return 0;
+}
 
 int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                      int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128, float scale,
