@@ -119,92 +119,6 @@ LX_DEV void mma16816_rp(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-constexpr int kRmRows = 16;    // rows per CTA; its 4 warps split K and reduce through shared memory
-constexpr int kRmChunk = 256;  // K per staged W chunk
-constexpr int kRmStride = kRmChunk + 8;  // bf16 elements per n-row in smem (conflict-free 32-bit reads)
-
-template <int NT>  // NT n8-tiles: R <= 8*NT
-__global__ void __launch_bounds__(128) rowproj_mma_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int s, int K,
-                                                          const float* __restrict__ w, long long w_sk, long long w_sq,
-                                                          int r, float scale, const int32_t* __restrict__ counts,
-                                                          const int32_t* __restrict__ ids, int ids_stride, int blk,
-                                                          float* __restrict__ y, int ldy) {
-  // W chunk as a bf16 (hi, lo) pair: W ~= hi + lo to ~2^-17 relative, so X (exact bf16) . W keeps
-  // fp32-level accuracy with two MMAs per step
-  __shared__ __align__(16) __nv_bfloat16 s_hi[8 * NT * kRmStride];
-  __shared__ __align__(16) __nv_bfloat16 s_lo[8 * NT * kRmStride];
-  __shared__ float s_red[4][16][8 * NT + 1];
-  const int item = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = blockIdx.x * kRmRows;
-  const int k_item = counts ? __ldg(counts + item) * blk : K;
-  const int32_t* my_ids = ids ? ids + (size_t)item * ids_stride : nullptr;
-  const int ra = row0 + (lane >> 2), rb = ra + 8;
-  const uint32_t* xa = reinterpret_cast<const uint32_t*>(x + ((size_t)item * s + min(ra, s - 1)) * ldx) + (lane & 3);
-  const uint32_t* xb = reinterpret_cast<const uint32_t*>(x + ((size_t)item * s + min(rb, s - 1)) * ldx) + (lane & 3);
-  float acc[NT][4];
-#pragma unroll
-  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
-  const bool k_fast = (w_sk == 1);
-  for (int k0 = 0; k0 < k_item; k0 += kRmChunk) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < 8 * NT * kRmChunk; e += 128) {
-      int kk, q;
-      if (k_fast) { q = e / kRmChunk; kk = e % kRmChunk; } else { kk = e / (8 * NT); q = e % (8 * NT); }
-      const int k = k0 + kk;
-      float val = 0.f;
-      if (k < k_item && q < r) {
-        long long ko = my_ids ? (long long)__ldg(my_ids + k / blk) * blk + k % blk : k;
-        val = __ldg(w + ko * w_sk + q * w_sq);
-      }
-      const __nv_bfloat16 hi = __float2bfloat16_rn(val);
-      s_hi[q * kRmStride + kk] = hi;
-      s_lo[q * kRmStride + kk] = __float2bfloat16_rn(val - __bfloat162float(hi));
-    }
-    __syncthreads();
-    const int kn = min(kRmChunk, k_item - k0);  // multiple of 16
-    // warp w takes k-steps w, w+4, ...: all four A-fragment loads of two steps are in flight together
-    for (int ks = warp * 16; ks < kn; ks += 128) {
-      const int kw = (k0 + ks) >> 1;
-      const bool two = ks + 64 < kn;
-      uint32_t a[4] = {__ldg(xa + kw), __ldg(xb + kw), __ldg(xa + kw + 4), __ldg(xb + kw + 4)};
-      uint32_t a2[4] = {0u, 0u, 0u, 0u};
-      if (two) {
-        a2[0] = __ldg(xa + kw + 32); a2[1] = __ldg(xb + kw + 32); a2[2] = __ldg(xa + kw + 36); a2[3] = __ldg(xb + kw + 36);
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h == 1 && !two) break;
-        const int kk = ks + h * 64;
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int off = (t * 8 + (lane >> 2)) * kRmStride + kk + (lane & 3) * 2;
-          const uint32_t h0 = *reinterpret_cast<const uint32_t*>(s_hi + off);
-          const uint32_t h1 = *reinterpret_cast<const uint32_t*>(s_hi + off + 8);
-          const uint32_t l0 = *reinterpret_cast<const uint32_t*>(s_lo + off);
-          const uint32_t l1 = *reinterpret_cast<const uint32_t*>(s_lo + off + 8);
-          mma16816_rp(acc[t], h ? a2 : a, h0, h1);
-          mma16816_rp(acc[t], h ? a2 : a, l0, l1);
-        }
-      }
-    }
-  }
-  // reduce the four warps' partial sums
-#pragma unroll
-  for (int t = 0; t < NT; ++t) {
-    const int q = t * 8 + (lane & 3) * 2;
-    s_red[warp][lane >> 2][q] = acc[t][0];
-    s_red[warp][lane >> 2][q + 1] = acc[t][1];
-    s_red[warp][(lane >> 2) + 8][q] = acc[t][2];
-    s_red[warp][(lane >> 2) + 8][q + 1] = acc[t][3];
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < 16 * 8 * NT; e += 128) {
-    const int rr = e / (8 * NT), q = e % (8 * NT), row = row0 + rr;
-    if (q < r && row < s)
-      y[((size_t)item * s + row) * ldy + q] = (s_red[0][rr][q] + s_red[1][rr][q] + s_red[2][rr][q] + s_red[3][rr][q]) * scale;
-  }
-}
 
 // W packed once per call: wp[item][hl][q][k] bf16 (hl = 0: hi, 1: lo), k over the item's packed K
 // (gathered through ids), rows q >= r and columns k >= k_item zero. Kp = K rounded up to 16.
@@ -229,139 +143,207 @@ __global__ void rowproj_wpack_kernel(const float* __restrict__ w, long long w_sk
 }
 
 // Y[M, R] = X W on tensor cores, A and B fragments straight from global (L2-resident W pack);
-// a CTA owns 16 rows, its 4 warps interleave k-steps and reduce through shared memory.
+// a CTA owns 16 rows, its kRpWarps warps interleave k-steps (kRpU in flight each: ~64 KB of X
+// in flight per SM, enough to stream at HBM rate) and reduce through shared memory.
+// Y[M, R] = X W on tensor cores (mma.sync m16n8k16), streaming X once at HBM rate.
+// K is summed over, so the MMA's k-slots may be mapped to any permutation of the physical k applied
+// to both X and W: within each 32-wide k block, lane t (= lane % 4) owns physical k [8t, 8t+8) and
+// feeds MMA step j (0, 1) with k 8t+4j+{0,1} (slots 2t, 2t+1) and 8t+4j+{2,3} (slots 2t+8, 2t+9).
+// One 16B load per row (g, g+8) then serves two MMA steps, and the packed W ([q][k], hi/lo bf16)
+// is read the same way. A CTA owns 16 rows; kRpWarps warps take interleaved 32-k blocks (kRpU in
+// flight each) and reduce through shared memory.
+constexpr int kRpWarps = 8, kRpU = 8;
+
 template <int NT>
-__global__ void __launch_bounds__(128) rowproj_mma2_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int s, int K,
+__global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int s, int K,
                                                            int Kp, int r, float scale, const int32_t* __restrict__ counts,
                                                            int blk, const __nv_bfloat16* __restrict__ wp,
                                                            float* __restrict__ y, int ldy) {
   constexpr int RP = 8 * NT;
-  __shared__ float s_red[4][16][RP + 1];
+  __shared__ float s_red[kRpWarps][16][RP + 1];
   const int item = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
   const int row0 = blockIdx.x * 16;
   const int k_item = counts ? __ldg(counts + item) * blk : K;
-  const int ra = row0 + (lane >> 2), rb = ra + 8;
-  const uint32_t* xa = reinterpret_cast<const uint32_t*>(x + ((size_t)item * s + min(ra, s - 1)) * ldx) + (lane & 3);
-  const uint32_t* xb = reinterpret_cast<const uint32_t*>(x + ((size_t)item * s + min(rb, s - 1)) * ldx) + (lane & 3);
-  const uint32_t* wh = reinterpret_cast<const uint32_t*>(wp + (size_t)item * 2 * RP * Kp + (lane >> 2) * Kp) + (lane & 3);
-  const uint32_t* wl = wh + (size_t)RP * Kp / 2;
+  const int ra = row0 + g, rb = ra + 8;
+  const __nv_bfloat16* xa = x + ((size_t)item * s + min(ra, s - 1)) * ldx + 8 * t;
+  const __nv_bfloat16* xb = x + ((size_t)item * s + min(rb, s - 1)) * ldx + 8 * t;
+  const __nv_bfloat16* wh = wp + (size_t)item * 2 * RP * Kp + (size_t)g * Kp + 8 * t;  // row q = g (+8 per n-tile)
+  const __nv_bfloat16* wl = wh + (size_t)RP * Kp;
   float acc[NT][4];
 #pragma unroll
-  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
-  constexpr int U = 4;  // k-steps in flight per warp
-  for (int kb = warp * 16; kb < k_item; kb += 64 * U) {
-    uint32_t a[U][4], bh[U][NT][2], bl[U][NT][2];
+  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+  for (int kb = warp * 32; kb < k_item; kb += 32 * kRpWarps * kRpU) {
+    uint4 va[kRpU], vb[kRpU], vh[kRpU][NT], vl[kRpU][NT];
+    // all loads of the round issued before any MMA (unconditional, clamped addresses; out-of-range
+    // lanes are zeroed afterwards): kRpU x 1 KB of X per warp in flight
+    uint32_t okm = 0;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int ks = kb + u * 64;
-      const bool ok = ks < k_item;
-      const int kw = ks >> 1;
-      a[u][0] = ok ? __ldg(xa + kw) : 0u;
-      a[u][1] = ok ? __ldg(xb + kw) : 0u;
-      a[u][2] = ok ? __ldg(xa + kw + 4) : 0u;
-      a[u][3] = ok ? __ldg(xb + kw + 4) : 0u;
+    for (int u = 0; u < kRpU; ++u) {
+      const int k0 = kb + u * 32 * kRpWarps;
+      const bool ok = k0 + 8 * t < k_item;  // k_item is a multiple of 16: a lane's 8 k are all in or all out
+      okm |= ok ? 1u << u : 0u;
+      const int kl = ok ? k0 : 0;
+      va[u] = __ldg(reinterpret_cast<const uint4*>(xa + kl));
+      vb[u] = __ldg(reinterpret_cast<const uint4*>(xb + kl));
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const size_t o = (size_t)t * 8 * Kp / 2 + kw;
-        bh[u][t][0] = ok ? __ldg(wh + o) : 0u;
-        bh[u][t][1] = ok ? __ldg(wh + o + 4) : 0u;
-        bl[u][t][0] = ok ? __ldg(wl + o) : 0u;
-        bl[u][t][1] = ok ? __ldg(wl + o + 4) : 0u;
+      for (int n = 0; n < NT; ++n) {
+        vh[u][n] = __ldg(reinterpret_cast<const uint4*>(wh + (size_t)n * 8 * Kp + kl));
+        vl[u][n] = __ldg(reinterpret_cast<const uint4*>(wl + (size_t)n * 8 * Kp + kl));
+      }
+    }
+    asm volatile("" ::: "memory");
+#pragma unroll
+    for (int u = 0; u < kRpU; ++u) {
+      if (!((okm >> u) & 1u)) {
+        va[u] = vb[u] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int n = 0; n < NT; ++n) vh[u][n] = vl[u][n] = make_uint4(0u, 0u, 0u, 0u);
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+    for (int u = 0; u < kRpU; ++u) {
+      const uint32_t a0[4] = {va[u].x, vb[u].x, va[u].y, vb[u].y};  // step 0
+      const uint32_t a1[4] = {va[u].z, vb[u].z, va[u].w, vb[u].w};  // step 1
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        mma16816_rp(acc[t], a[u], bh[u][t][0], bh[u][t][1]);
-        mma16816_rp(acc[t], a[u], bl[u][t][0], bl[u][t][1]);
+      for (int n = 0; n < NT; ++n) {
+        mma16816_rp(acc[n], a0, vh[u][n].x, vh[u][n].y);
+        mma16816_rp(acc[n], a0, vl[u][n].x, vl[u][n].y);
+        mma16816_rp(acc[n], a1, vh[u][n].z, vh[u][n].w);
+        mma16816_rp(acc[n], a1, vl[u][n].z, vl[u][n].w);
       }
+    }
   }
 #pragma unroll
-  for (int t = 0; t < NT; ++t) {
-    const int q = t * 8 + (lane & 3) * 2;
-    s_red[warp][lane >> 2][q] = acc[t][0];
-    s_red[warp][lane >> 2][q + 1] = acc[t][1];
-    s_red[warp][(lane >> 2) + 8][q] = acc[t][2];
-    s_red[warp][(lane >> 2) + 8][q + 1] = acc[t][3];
+  for (int n = 0; n < NT; ++n) {
+    const int q = n * 8 + t * 2;
+    s_red[warp][g][q] = acc[n][0];
+    s_red[warp][g][q + 1] = acc[n][1];
+    s_red[warp][g + 8][q] = acc[n][2];
+    s_red[warp][g + 8][q + 1] = acc[n][3];
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < 16 * RP; e += 128) {
+  for (int e = threadIdx.x; e < 16 * RP; e += 32 * kRpWarps) {
     const int rr = e / RP, q = e % RP, row = row0 + rr;
-    if (q < r && row < s)
-      y[((size_t)item * s + row) * ldy + q] = (s_red[0][rr][q] + s_red[1][rr][q] + s_red[2][rr][q] + s_red[3][rr][q]) * scale;
+    if (q < r && row < s) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < kRpWarps; ++w) v += s_red[w][rr][q];
+      y[((size_t)item * s + row) * ldy + q] = v * scale;
+    }
   }
 }
 
-constexpr int kCgCols = 256;  // 32 lanes x 8 columns
-constexpr int kCgRows = 128;  // rows per split (8 warps x 16 rows)
+constexpr int kCgCols = 128;  // 32 lanes x 4 columns
+constexpr int kCgRows = 512;  // rows per CTA (one split)
 
-// partial[item][split][q][col] over the item's packed columns (dynamic smem: s_p | s_red)
+// partial[item][split][q][col] = sum over the split's rows of P[row, q] X[row, col] over the item's
+// packed columns. A CTA owns 128 columns x kCgRows rows: warp 8 streams [32 rows x 128 cols] tiles
+// (two SWIZZLE_128B boxes of 64 columns) through a kCgSt-stage TMA ring, 64 KB in flight; the P rows
+// of the split are staged in shared memory once; consumer warp w accumulates rows 4w..4w+3 of each
+// tile, lane l columns 4l..4l+3 (R <= 8; P rows read as 8 floats: ldp % 4 == 0, ldp >= 8; columns
+// q >= r are ignored by the final kernel). The ring is reused for the cross-warp reduction.
+constexpr int kCgSt = 8, kCgTile = 32 * kCgCols * 2;  // bytes per stage (2 atoms of [32][128B])
+
+struct CgSmem {
+  static constexpr int kOffP = kCgSt * kCgTile;       // s_p [kCgRows][8] fp32
+  static constexpr int kOffBar = kOffP + kCgRows * 8 * 4;
+  static constexpr int kTotal = kOffBar + 2 * kCgSt * 8 + 1024;
+};
+
 template <int R>
-__global__ void __launch_bounds__(256) colgrad_partial_kernel(const float* __restrict__ p, int ldp,
-                                                              const __nv_bfloat16* __restrict__ x, int ldx, int s, int ncols,
-                                                              int r, const int32_t* __restrict__ counts, int blk,
+__global__ void __launch_bounds__(288) colgrad_partial_kernel(const __grid_constant__ CUtensorMap tm_x, const float* __restrict__ p,
+                                                              int ldp, int s, int ncols, int r,
+                                                              const int32_t* __restrict__ counts, int blk,
                                                               float* __restrict__ ws) {
-  extern __shared__ float cg_smem[];
-  float* s_p = cg_smem;                          // [kCgRows][R]
-  float* s_red = cg_smem + kCgRows * R;          // [8][R][kCgCols + 4]
-  constexpr int kRedStride = kCgCols + 4;
+  extern __shared__ uint8_t cg_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(cg_raw) + 1023) & ~uintptr_t(1023));
+  float* s_p = reinterpret_cast<float*>(sm + CgSmem::kOffP);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + CgSmem::kOffBar);
+  uint64_t* empty = full + kCgSt;
   const int item = blockIdx.z, split = blockIdx.y;
   const int n_splits = gridDim.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_item = counts ? __ldg(counts + item) * blk : ncols;
-  const int c0 = blockIdx.x * kCgCols + lane * 8;
-  const int r0 = split * kCgRows;
   if (blockIdx.x * kCgCols >= n_item) return;  // beyond the item's packed width: never read
-  for (int e = threadIdx.x; e < kCgRows * R; e += 256) {
-    const int lr = r0 + e / R, q = e % R;
-    s_p[e] = (lr < s && q < r) ? (p ? __ldg(p + ((size_t)item * s + lr) * ldp + q) : 1.f) : 0.f;
+  const int r0 = split * kCgRows;
+  const int nrows = min(kCgRows, s - r0);
+  const int n_tiles = (nrows + 31) / 32;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kCgSt; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 8);
+    }
+    fence_mbar_init();
   }
   __syncthreads();
-  float acc[8][R];
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-#pragma unroll
-    for (int q = 0; q < R; ++q) acc[j][q] = 0.f;
-  const int nrows = min(kCgRows, s - r0);
-  if (c0 < n_item) {
-    // warp w owns rows w, w+8, ...; 8 rows in flight per lane
-    for (int i0 = warp; i0 < nrows; i0 += 64) {
-      uint4 pk[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + u * 8;
-        pk[u] = i < nrows ? *reinterpret_cast<const uint4*>(x + ((size_t)item * s + r0 + i) * ldx + c0)
-                          : make_uint4(0u, 0u, 0u, 0u);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + u * 8;
-        if (i >= nrows) break;
-        const uint32_t pw[4] = {pk[u].x, pk[u].y, pk[u].z, pk[u].w};
-        const float* pp = s_p + i * R;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float xv = bf16_bits_to_float((pw[j >> 1] >> ((j & 1) * 16)) & 0xffff);
-#pragma unroll
-          for (int q = 0; q < R; ++q) acc[j][q] = fmaf(pp[q], xv, acc[j][q]);
-        }
+  if (warp == 8) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_x);
+      for (int t = 0; t < n_tiles; ++t) {
+        const int st = t % kCgSt;
+        mbar_wait(empty + st, ((t / kCgSt) & 1) ^ 1);
+        mbar_arrive_expect_tx(full + st, kCgTile);
+        uint8_t* dst = sm + st * kCgTile;
+        const int row = item * s + r0 + t * 32;
+        tma_load_2d(dst, &tm_x, full + st, blockIdx.x * kCgCols, row);
+        tma_load_2d(dst + kCgTile / 2, &tm_x, full + st, blockIdx.x * kCgCols + 64, row);
       }
     }
+    return;
   }
+  // P rows of this split -> smem (p == NULL: column sums, P = 1); rows past nrows are zero
+  for (int e = threadIdx.x; e < kCgRows * 2; e += 256) {
+    const int i = e >> 1, h = e & 1;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < nrows) v = p ? __ldg(reinterpret_cast<const float4*>(p + ((size_t)item * s + r0 + i) * ldp) + h)
+                         : make_float4(1.f, 1.f, 1.f, 1.f);
+    *reinterpret_cast<float4*>(s_p + i * 8 + h * 4) = v;
+  }
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  float acc[4][R];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int q = 0; q < R; ++q) acc[j][q] = 0.f;
+  const int atom = lane >> 4, chunk = (lane & 15) >> 1, half = lane & 1;  // columns 4*lane .. 4*lane+3
+  for (int t = 0; t < n_tiles; ++t) {
+    const int st = t % kCgSt;
+    mbar_wait(full + st, (t / kCgSt) & 1);
+    const uint8_t* tile = sm + st * kCgTile + atom * (kCgTile / 2);
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const int row = warp * 4 + rr;  // rows past nrows: P is zero (X finite: next item / zero fill)
+      const uint2 xv = *reinterpret_cast<const uint2*>(tile + row * 128 + ((chunk ^ (row & 7)) << 4) + half * 8);
+      const float* pp = s_p + (t * 32 + row) * 8;
+      const float xf[4] = {bf16_bits_to_float(xv.x & 0xffff), bf16_bits_to_float(xv.x >> 16),
+                           bf16_bits_to_float(xv.y & 0xffff), bf16_bits_to_float(xv.y >> 16)};
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const float pq = pp[q];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j][q] = fmaf(pq, xf[j], acc[j][q]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
+  }
+  // every tile consumed (each consumer waited all full barriers) -> the ring is free for the reduction
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  float* s_red = reinterpret_cast<float*>(sm);  // [8 warps][R][kCgCols + 4]
+  constexpr int kRs = kCgCols + 4;
 #pragma unroll
   for (int q = 0; q < R; ++q)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) s_red[(warp * R + q) * kRedStride + lane * 8 + j] = acc[j][q];
-  __syncthreads();
+    *reinterpret_cast<float4*>(s_red + (warp * R + q) * kRs + lane * 4) = make_float4(acc[0][q], acc[1][q], acc[2][q], acc[3][q]);
+  asm volatile("bar.sync 1, 256;" ::: "memory");
   float* out = ws + (((size_t)item * n_splits + split) * R) * ncols;
   for (int e = threadIdx.x; e < R * kCgCols; e += 256) {
     const int q = e / kCgCols, cc = e % kCgCols, c = blockIdx.x * kCgCols + cc;
     if (q >= r || c >= ncols) continue;
     float v = 0.f;
 #pragma unroll
-    for (int w2 = 0; w2 < 8; ++w2) v += s_red[(w2 * R + q) * kRedStride + cc];
+    for (int w2 = 0; w2 < 8; ++w2) v += s_red[(w2 * R + q) * kRs + cc];
     out[(size_t)q * ncols + c] = v;
   }
 }
@@ -392,13 +374,19 @@ __global__ void colgrad_final_kernel(const float* __restrict__ ws, int n_items, 
         }
       }
     }
-    for (int sp = 0; sp < n_splits; ++sp) {
-      float vals[8];
+    for (int sp0 = 0; sp0 < n_splits; sp0 += 4) {
+      float vals[8][4];
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        vals[u] = pcs[u] >= 0 ? ws[(((size_t)(b0 + u) * n_splits + sp) * R + q) * ncols + pcs[u]] : 0.f;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc += vals[u];
+        for (int t = 0; t < 4; ++t)
+          vals[u][t] = (pcs[u] >= 0 && sp0 + t < n_splits)
+                           ? __ldg(ws + (((size_t)(b0 + u) * n_splits + sp0 + t) * R + q) * ncols + pcs[u])
+                           : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc += vals[u][t];
     }
   }
   g[(long long)q * g_sq + (long long)c * g_sc] = acc * scale;
@@ -408,17 +396,24 @@ template <int R>
 static int colgrad_impl(const float* p, int ldp, const uint16_t* x, int ldx, int n_items, int s, int ncols, int r,
                         float scale, const int32_t* counts, const int32_t* pos, int blk, float* g, long long g_sq,
                         long long g_sc, float* ws, cudaStream_t stream) {
-  const int splits = (s + kCgRows - 1) / kCgRows;
-  dim3 g1((ncols + kCgCols - 1) / kCgCols, splits, n_items);
-  const int smem = (kCgRows * R + 8 * R * (kCgCols + 4)) * 4;
+  // shared columns (no counts): every item reads the same columns -> one item of n_items * s rows
+  const int items = counts ? n_items : 1, rows = counts ? s : n_items * s;
+  const int splits = (rows + kCgRows - 1) / kCgRows;
+  dim3 g1((ncols + kCgCols - 1) / kCgCols, splits, items);
+  static_assert(8 * 8 * (kCgCols + 4) * 4 <= kCgSt * kCgTile, "reduction must fit in the ring");
+  constexpr int smem = CgSmem::kTotal;
   static cudaError_t attr = cudaFuncSetAttribute(colgrad_partial_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   LX_CHECK_CUDA(attr);
-  colgrad_partial_kernel<R><<<g1, 256, smem, stream>>>(p, ldp, reinterpret_cast<const __nv_bfloat16*>(x), ldx, s, ncols, r,
-                                                    counts, counts ? blk : 1, ws);
+  // X as [n_items*s, ldx]: boxes of 64 columns x 32 rows (columns past ncols / the item's width are
+  // never combined; rows past an item's split are weighted by P = 0)
+  CUtensorMap tm;
+  int rc0 = make_tmap_bf16_2d(&tm, x, (uint64_t)ldx, (uint64_t)n_items * s, (uint64_t)ldx, 64, 32);
+  if (rc0) return rc0;
+  colgrad_partial_kernel<R><<<g1, 288, smem, stream>>>(tm, p, ldp, rows, ncols, r, counts, counts ? blk : 1, ws);
   int rc = launch_check("colgrad_partial");
   if (rc) return rc;
   dim3 g2((ncols + 255) / 256, r);
-  colgrad_final_kernel<R><<<g2, 256, 0, stream>>>(ws, n_items, splits, ncols, r, counts ? pos : nullptr,
+  colgrad_final_kernel<R><<<g2, 256, 0, stream>>>(ws, items, splits, ncols, r, counts ? pos : nullptr,
                                                   counts ? blk : 1, scale, g, g_sq, g_sc);
   return launch_check("colgrad_final");
 }
@@ -460,13 +455,13 @@ int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const floa
       // dense W is shared by all items: index it as item 0 by treating the batch as one item
       grid = dim3((n_items * s + 15) / 16, 1);
       if (NT == 1)
-        rowproj_mma2_kernel<1><<<grid, 128, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb, y, ldy);
+        rowproj_mma2_kernel<1><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb, y, ldy);
       else
-        rowproj_mma2_kernel<2><<<grid, 128, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb, y, ldy);
+        rowproj_mma2_kernel<2><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb, y, ldy);
     } else if (NT == 1) {
-      rowproj_mma2_kernel<1><<<grid, 128, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, y, ldy);
+      rowproj_mma2_kernel<1><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, y, ldy);
     } else {
-      rowproj_mma2_kernel<2><<<grid, 128, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, y, ldy);
+      rowproj_mma2_kernel<2><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, y, ldy);
     }
     return launch_check("rowproj_mma");
   }
@@ -479,21 +474,23 @@ int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const floa
 }
 
 long long lx_colgrad_ws_floats(int n_items, int s, int ncols, int r) {
+  // bound for both layouts: per item (gathered) or one item of n_items * s rows (shared columns)
   long long splits = (s + kCgRows - 1) / kCgRows;
-  int rr = r <= 1 ? 1 : (r <= 8 ? 8 : 16);
+  int rr = r <= 1 ? 1 : 8;
   return (long long)n_items * splits * rr * ncols;
 }
 
 int lx_colgrad(const float* p, int ldp, const uint16_t* x, int ldx, int n_items, int s, int ncols, int r, float scale,
                const int32_t* counts, const int32_t* pos, int blk, float* g, long long g_sq, long long g_sc, float* ws,
                lx_stream_t stream) {
-  LX_REQUIRE(r >= 1 && r <= 16, LX_ERR_UNSUPPORTED, "colgrad: rank %d outside [1, 16]", r);
-  LX_REQUIRE(!p || ldp >= r, LX_ERR_SHAPE, "colgrad: ldp < r");
+  LX_REQUIRE(r >= 1 && r <= 8, LX_ERR_UNSUPPORTED, "colgrad: rank %d outside [1, 8]", r);
+  LX_REQUIRE(!p || (ldp >= 8 && ldp % 4 == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0), LX_ERR_SHAPE,
+             "colgrad: P rows must be 16B-aligned and padded to 8 floats (ldp >= 8, ldp %% 4 == 0)");
+  LX_REQUIRE(ncols % 4 == 0, LX_ERR_SHAPE, "colgrad: ncols must be a multiple of 4");
   LX_REQUIRE(!counts || (pos && ncols % blk == 0), LX_ERR_MASK, "colgrad: gathered columns need pos and ncols %% blk == 0");
   LX_REQUIRE(ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0, LX_ERR_SHAPE, "colgrad: 16B-aligned rows required");
   if (r == 1) return colgrad_impl<1>(p, ldp, x, ldx, n_items, s, ncols, r, scale, counts, pos, blk, g, g_sq, g_sc, ws, stream);
-  if (r <= 8) return colgrad_impl<8>(p, ldp, x, ldx, n_items, s, ncols, r, scale, counts, pos, blk, g, g_sq, g_sc, ws, stream);
-  return colgrad_impl<16>(p, ldp, x, ldx, n_items, s, ncols, r, scale, counts, pos, blk, g, g_sq, g_sc, ws, stream);
+  return colgrad_impl<8>(p, ldp, x, ldx, n_items, s, ncols, r, scale, counts, pos, blk, g, g_sq, g_sc, ws, stream);
 }
 
 int lx_colsum(const uint16_t* x, int ldx, int n_items, int s, int ncols, const int32_t* counts, const int32_t* pos,
