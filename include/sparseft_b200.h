@@ -38,6 +38,11 @@ typedef struct CUstream_st* lx_stream_t;
 const char* lx_last_error(void);
 int lx_abi_version(void);
 int lx_device_sm_count(void);
+/* GEMM engine variant for the dense / item-packed modes: 1 = CTA pairs (tcgen05.mma.cta_group::2,
+ * 256-row tiles), 0 (default) = single-CTA 128-row tiles. Returns the previous value. */
+int lx_gemm_set_cta_pair(int on);
+/* Debug only: per-CTA clock64 phase stamps of the GEMM engine into buf [grid][32]; NULL disables. */
+int lx_debug_set_gemm_trace(unsigned long long* buf);
 
 /* ------------------------------------------------------------------ generic
  * C[M,N] (fp32 or bf16) = A[M,K] * B[N,K]^T, bf16 inputs, tcgen05 path.

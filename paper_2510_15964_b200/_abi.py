@@ -24,6 +24,8 @@ SIGNATURES: dict[str, list] = {
     "lx_last_error": [],
     "lx_abi_version": [],
     "lx_device_sm_count": [],
+    "lx_gemm_set_cta_pair": [_I],
+    "lx_debug_set_gemm_trace": [_P],
     "lx_gemm_bf16_tn": [_P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _P],
     "lx_linear": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _P, _P, _P, _P, _LL, _LL, _I, _F, _P],
     "lx_predict_mlp_mask": [_P, _I, _I, _I, _P, _I, _F, _I, _P, _P, _P, _P, _P, _P],
@@ -79,7 +81,7 @@ def lib() -> C.CDLL:
 def call(name: str, *args) -> int:
     """Invoke an entry point; map a nonzero return code to the reference's exception type."""
     rc = getattr(lib(), name)(*args)
-    if isinstance(rc, int) and rc != 0 and name not in ("lx_abi_version", "lx_device_sm_count", "lx_attn_tables_size"):
+    if isinstance(rc, int) and rc != 0 and name not in ("lx_abi_version", "lx_device_sm_count", "lx_attn_tables_size", "lx_gemm_set_cta_pair"):
         msg = lib().lx_last_error().decode(errors="replace")
         raise _ERRORS.get(rc, E.CudaError)(f"{name}: {msg}")
     return rc

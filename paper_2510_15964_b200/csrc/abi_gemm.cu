@@ -59,18 +59,47 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
   return LX_OK;
 }
 
-template <int BMODE, int EPI, int BN>
+// CTA pairs (cta_group::2) for the dense / item-packed modes, selectable with lx_gemm_set_cta_pair.
+// Default single-CTA: at the MLP shapes (about one tile per CTA) the pair's cluster launch delays the
+// first stage by ~1.4k cycles and costs more than its halved B traffic saves (tools/gemm_trace.py).
+static int g_cta_pair = 0;
+
+template <int BMODE, int EPI, int BN, int CTAS = 1>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
-  auto kern = gemm_sm100_kernel<BMODE, EPI, BN>;
-  constexpr int smem = GemmSmem<BN>::kTotal;
+  auto kern = gemm_sm100_kernel<BMODE, EPI, BN, CTAS>;
+  constexpr int smem = GemmSmem<BN, CTAS>::kTotal;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
   LX_CHECK_CUDA(attr_err);
   LX_REQUIRE(args.n_items >= 1 && args.n_items <= kMaxItems, LX_ERR_UNSUPPORTED, "n_items must be in [1, %d]", kMaxItems);
   LX_REQUIRE(args.lora_r >= 0 && args.lora_r <= kMaxR, LX_ERR_UNSUPPORTED, "LoRA rank must be <= %d", kMaxR);
-  kern<<<num_sms(), 192, smem, st>>>(ta, tb, args);
-  return launch_check("gemm_sm100");
+  if (CTAS == 1) {
+    kern<<<num_sms(), kGemmThreads, smem, st>>>(ta, tb, args);
+    return launch_check("gemm_sm100");
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms() & ~1);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LX_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, args));
+  return launch_check("gemm_sm100 (cta pair)");
+}
+
+// dense / packed B: pick the CTA-pair engine when enabled (B boxes are then BN/2 rows on the N side)
+template <int BMODE, int EPI>
+static int launch_gemm_auto(const CUtensorMap& ta, const CUtensorMap& tb1, const CUtensorMap& tb2, const GemmArgs& args,
+                            cudaStream_t st) {
+  if (g_cta_pair) return launch_gemm<BMODE, EPI, 256, 2>(ta, tb2, args, st);
+  return launch_gemm<BMODE, EPI, 256, 1>(ta, tb1, args, st);
 }
 
 static GemmArgs base_args(int n_items, int rows, int n_dense, int k_dense) {
@@ -114,6 +143,16 @@ extern "C" {
 const char* lx_last_error(void) { return g_err; }
 int lx_abi_version(void) { return 1; }
 int lx_device_sm_count(void) { return num_sms(); }
+int lx_debug_set_gemm_trace(unsigned long long* buf) {
+  LX_CHECK_CUDA(cudaMemcpyToSymbol(g_gemm_trace, &buf, sizeof(buf)));
+  return 0;
+}
+
+int lx_gemm_set_cta_pair(int on) {
+  const int prev = g_cta_pair;
+  g_cta_pair = on ? 1 : 0;
+  return prev;
+}
 
 int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void* c, int ldc, int c_is_f32, int M, int N,
                     int K, lx_stream_t stream) {
@@ -121,12 +160,14 @@ int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void
   CUtensorMap ta, tb;
   int rc;
   if ((rc = make_tmap_bf16_2d(&ta, a, K, M, lda, kBK, kBM))) return rc;
+  CUtensorMap tb2;
   if ((rc = make_tmap_bf16_2d(&tb, b, K, N, ldb, kBK, 256))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb2, b, K, N, ldb, kBK, 128))) return rc;
   GemmArgs args = base_args(1, M, N, K);
   args.out = c;
   args.ldo = ldc;
-  return c_is_f32 ? launch_gemm<kDense, kEpiStoreF32, 256>(ta, tb, args, stream)
-                  : launch_gemm<kDense, kEpiStoreBF16, 256>(ta, tb, args, stream);
+  return c_is_f32 ? launch_gemm_auto<kDense, kEpiStoreF32>(ta, tb, tb2, args, stream)
+                  : launch_gemm_auto<kDense, kEpiStoreBF16>(ta, tb, tb2, args, stream);
 }
 
 int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, int N, int K, void* out, int ldo,
@@ -166,8 +207,8 @@ int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, i
 // N side: K-major boxes [64 K x blk rows] (gather) / [64 K x 256 rows] (packed).
 // K side: MN-major boxes [64 N x blk rows] (gather) / [64 N x 64 rows] (packed).
 static int mlp_tmap_b(CUtensorMap* tb, const uint16_t* w, const uint16_t* wp, int n_items, int d, int d_ff, int blk,
-                      bool n_side) {
-  if (wp) return make_tmap_bf16_2d(tb, wp, d, (uint64_t)n_items * d_ff, d, kBK, n_side ? 256 : 64);
+                      bool n_side, int n_rows = 256) {
+  if (wp) return make_tmap_bf16_2d(tb, wp, d, (uint64_t)n_items * d_ff, d, kBK, n_side ? n_rows : 64);
   return make_tmap_bf16_2d(tb, w, d, d_ff, d, kBK, blk);
 }
 
@@ -196,9 +237,12 @@ int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int bl
   args.w_sc = 1;
   args.lora_r = (ax1 && b1_lora) ? r : 0;
   args.lora_scale = scaling;
-  if (w1_packed)
-    return apply_relu ? launch_gemm<kPackedN, kEpiFc1, 256>(ta, tb, args, stream)
-                      : launch_gemm<kPackedN, kEpiFc1Raw, 256>(ta, tb, args, stream);
+  if (w1_packed) {
+    CUtensorMap tb2;
+    if ((rc = mlp_tmap_b(&tb2, w1_t, w1_packed, n_items, d, d_ff, blk, true, 128))) return rc;
+    return apply_relu ? launch_gemm_auto<kPackedN, kEpiFc1>(ta, tb, tb2, args, stream)
+                      : launch_gemm_auto<kPackedN, kEpiFc1Raw>(ta, tb, tb2, args, stream);
+  }
   return apply_relu ? launch_gemm<kNGather, kEpiFc1, 256>(ta, tb, args, stream)
                     : launch_gemm<kNGather, kEpiFc1Raw, 256>(ta, tb, args, stream);
 }
@@ -231,7 +275,7 @@ int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_
   args.lora_scale = scaling;
   args.out_f32 = out_f32;
   args.resid = resid;
-  if (w2_packed) return launch_gemm<kPackedK, kEpiFc2, 256>(ta, tb, args, stream);
+  if (w2_packed) return launch_gemm_auto<kPackedK, kEpiFc2>(ta, tb, tb, args, stream);
   return launch_gemm<kKGather, kEpiFc2, 256>(ta, tb, args, stream);
 }
 
@@ -258,7 +302,11 @@ int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_
   args.lora_r = (dax2 && a2_lora) ? r : 0;
   args.act = reinterpret_cast<const __nv_bfloat16*>(a);
   args.ld_act = ld_h;
-  if (w2_packed) return launch_gemm<kPackedN, kEpiDa, 256>(ta, tb, args, stream);
+  if (w2_packed) {
+    CUtensorMap tb2;
+    if ((rc = mlp_tmap_b(&tb2, w2, w2_packed, n_items, d, d_ff, blk, true, 128))) return rc;
+    return launch_gemm_auto<kPackedN, kEpiDa>(ta, tb, tb2, args, stream);
+  }
   return launch_gemm<kNGather, kEpiDa, 256>(ta, tb, args, stream);
 }
 
@@ -285,7 +333,7 @@ int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d,
   args.w_sc = r;
   args.lora_r = (dax1 && a1_lora) ? r : 0;
   args.out_f32 = out_f32;
-  if (w1_packed) return launch_gemm<kPackedK, kEpiDx, 256>(ta, tb, args, stream);
+  if (w1_packed) return launch_gemm_auto<kPackedK, kEpiDx>(ta, tb, tb, args, stream);
   return launch_gemm<kKGather, kEpiDx, 256>(ta, tb, args, stream);
 }
 

@@ -113,7 +113,7 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
   using L = AttnFwdSmem<HD>;
   constexpr int A = L::kAtoms;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sm = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;   // [2]
@@ -331,7 +331,7 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
   constexpr int A = HD / 64;
   constexpr int kTmem = tmem_cols_pow2(kAT + 2 * HD);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sm = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
   uint64_t* kv_full = bars + 0;
   uint64_t* qd_full = bars + 1;   // [2]: TMA (1 arrive + tx) + 32 producer lanes (lse/delta)
@@ -554,7 +554,7 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
   constexpr int A = HD / 64;
   constexpr int kTmem = tmem_cols_pow2(kAT + HD);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sm = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;   // [2]

@@ -12,9 +12,17 @@
 //              neuron blocks, each `blk` contiguous rows of W2 (fc2) or W1^T
 //              (fc1 input-grad). A is the packed hidden [M, ld] (K = count*blk).
 //
-// Warp roles: w0 = TMA producer, w1 = MMA issuer (lane 0), w2..w5 = epilogue
-// (one accumulator row per thread). Grid = #SMs; tiles strided over CTAs, with
+// Warp roles: w0 = TMA producer, w1 = MMA issuer (lane 0), w2..w9 = epilogue
+// (one accumulator row per thread, half of the tile's columns per warp). Grid = #SMs; tiles strided over CTAs, with
 // the M tile fastest so co-resident CTAs share the same weight (B) tile in L2.
+//
+// CTAS = 2 (dense and item-packed modes): a cluster pair owns a 256 x BN tile and issues
+// tcgen05.mma.cta_group::2 (M = 256) from the even CTA. Each CTA loads its 128 rows of A and its
+// half of B (BN/2 rows, or BN/2 columns for the MN-major K-side), so a stage is 32 KB instead of
+// 48 KB (6 stages) and L2 -> SM traffic per FLOP drops by 1.5x. Both CTAs' TMA count bytes on the
+// leader's full barrier; the MMA commits multicast to both CTAs' empty / accumulator barriers;
+// both CTAs' epilogue warps release the leader's accumulator barrier. Each CTA's TMEM holds its
+// 128 rows x BN columns, so the epilogue is the 1-CTA one.
 #pragma once
 #include "ptx.cuh"
 
@@ -39,8 +47,23 @@ enum EpiKind : int {
   kEpiFc1Raw = 7,     // acc + b1[c] + s*ax1[row]·B1[:,c] (no ReLU)  -> bf16 packed (neuron_matmul_fwd1 API)
 };
 
+// Debug-only phase trace (lx_debug_set_gemm_trace): per CTA 32 clock64 stamps, NULL in production.
+__device__ unsigned long long* g_gemm_trace = nullptr;
+LX_DEV void gemm_stamp(int slot) {
+  unsigned long long* t = g_gemm_trace;
+  if (t != nullptr) {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    t[blockIdx.x * 32 + slot] = c;
+  }
+}
+
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
+// epilogue: 8 warps = the 4 TMEM lane groups twice; warps 2..5 take columns [0, BN/2) of their rows,
+// warps 6..9 columns [BN/2, BN) (two warps per SM sub-partition hide each other's latency)
+constexpr int kEpiWarps = 8;
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr int kMaxR = 16;
 constexpr int kMaxItems = 512;
 
@@ -73,17 +96,20 @@ struct GemmArgs {
   int packed_stride;    // kPacked*: rows per item in the packed weight copy
 };
 
-template <int BN>
+constexpr int kStgPitch = 80;  // bytes per staged row: 64 B of bf16 + 16 B pad (conflict-free 16 B writes)
+
+template <int BN, int CTAS = 1>
 struct GemmSmem {
-  static constexpr int kStages = BN >= 256 ? 4 : 6;
+  static constexpr int kStages = CTAS == 2 ? 5 : (BN >= 256 ? 3 : 5);
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kBBytes = (BN / CTAS) * kBK * 2;  // this CTA's share of the B tile
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOff = kStages * kStageBytes;
   static constexpr int kMiscOff = kBarOff + (2 * kStages + 4) * 8;
   static constexpr int kEpiOff = (kMiscOff + 16 + 4 * (kMaxItems + 1) + 127) / 128 * 128;
   static constexpr int kEpiBytes = BN * 4 + BN * kMaxR * 4;
-  static constexpr int kTotal = kEpiOff + kEpiBytes + 1024;  // + alignment slack
+  static constexpr int kStgOff = kEpiOff + kEpiBytes;  // per epilogue warp: 32 rows x kStgPitch
+  static constexpr int kTotal = kStgOff + kEpiWarps * 32 * kStgPitch + 1024;  // + alignment slack
 };
 
 struct TileInfo {
@@ -101,6 +127,7 @@ LX_DEV int item_n_tiles(const GemmArgs& a, int cnt) {
 
 template <int BMODE, int BN>
 LX_DEV TileInfo decode_tile(const GemmArgs& a, const int* prefix, const int* cnts, int m_tiles, int t) {
+  // m_tiles counts tiles of kBM * CTAS rows (the caller's choice)
   int lo = 0, hi = a.n_items;  // largest item with prefix[item] <= t
   while (hi - lo > 1) {
     int mid = (lo + hi) >> 1;
@@ -119,13 +146,16 @@ LX_DEV TileInfo decode_tile(const GemmArgs& a, const int* prefix, const int* cnt
   return ti;
 }
 
-template <int BMODE, int EPI, int BN>
-__global__ void __launch_bounds__(192, 1)
+template <int BMODE, int EPI, int BN, int CTAS = 1>
+__global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, GemmArgs args) {
-  using L = GemmSmem<BN>;
+  static_assert(CTAS == 1 || (BMODE == kDense || BMODE == kPackedN || BMODE == kPackedK), "CTA pairs: dense / packed B only");
+  using L = GemmSmem<BN, CTAS>;
+  constexpr int TM = kBM * CTAS;  // rows per (pair) tile
+  constexpr int BNC = BN / CTAS;  // this CTA's share of the N tile
   constexpr int S = L::kStages;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
@@ -137,7 +167,10 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int m_tiles = (args.rows_per_item + kBM - 1) / kBM;
+  const uint32_t rank = CTAS == 2 ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int m_tiles = (args.rows_per_item + TM - 1) / TM;
+  const int t0 = blockIdx.x / CTAS, t_step = gridDim.x / CTAS;
 
   // ---- tile table: prefix[b] = first tile index of item b (counts are device-resident)
   if (threadIdx.x == 0) {
@@ -150,15 +183,20 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     prefix[args.n_items] = acc;
   }
   if (warp == 0 && lane == 0) {
+    gemm_stamp(0);
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
     for (int i = 0; i < S; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, kEpiWarps * CTAS); }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 2) {
+    if (CTAS == 2) tmem_alloc_cg2<512>(tmem_slot);
+    else tmem_alloc<512>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
+  if (CTAS == 2) cluster_sync();  // both CTAs' barriers initialised before any cross-CTA signal
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int n_tiles_total = prefix[args.n_items];
@@ -172,9 +210,9 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     const uint64_t pol_w = policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+    for (int t = t0; t < n_tiles_total; t += t_step) {
       TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t);
-      const int row0 = ti.item * args.rows_per_item + ti.mt * kBM;
+      const int row0 = ti.item * args.rows_per_item + ti.mt * TM + rank * kBM;
       const int* ids = args.ids + (size_t)ti.item * args.ids_stride;
       int my_row = 0;  // kNGather: this lane's gathered W row (block id * blk), lane < nb
       int nb_n = 0;
@@ -193,6 +231,23 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           if (j < nb_k) my_k_row = __ldg(ids + kb0 + j) * args.blk;
         }
         mbar_wait(empty + stage, phase ^ 1);
+        if (CTAS == 2) {
+          // pair: this CTA's A rows and half of B; bytes of both halves counted on the leader's barrier
+          if (lane == 0) {
+            if (leader) mbar_arrive_expect_tx(full + stage, 2 * (L::kABytes + L::kBBytes));
+            tma_load_2d_cg2(sa, &tmap_a, full + stage, ks * kBK, row0, pol_w);
+            if (BMODE == kDense) tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.nt * BN + rank * BNC, pol_w);
+            if (BMODE == kPackedN)
+              tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.item * args.packed_stride + ti.nt * BN + rank * BNC, pol_w);
+            if (BMODE == kPackedK)
+              for (int a = 0; a < BNC / 64; ++a)
+                tma_load_2d_cg2(sb + a * (kBK * 128), &tmap_b, full + stage, ti.nt * BN + rank * BNC + a * 64,
+                                ti.item * args.packed_stride + ks * kBK, pol_w);
+          }
+          __syncwarp();
+          if (++stage == S) { stage = 0; phase ^= 1; }
+          continue;
+        }
         if (lane == 0) {
           uint32_t bytes = L::kABytes;
           if (BMODE == kDense || BMODE == kPackedN || BMODE == kPackedK) bytes += BN * kBK * 2;
@@ -223,21 +278,23 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     }
   } else if (warp == 1) {
     // ================= MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+      for (int t = t0; t < n_tiles_total; t += t_step, ++it) {
         TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t);
         const int buf = it & 1;
         const uint32_t use_phase = (it >> 1) & 1;
         mbar_wait(tempty + buf, use_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
-        int n_mma = is_ng<BMODE>() ? ((ti.n_cols + 15) / 16) * 16 : BN;
-        const uint32_t idesc = make_idesc_bf16(kBM, n_mma, false, is_kg<BMODE>());
+        // pairs always run the full N (each CTA holds BN/2 of B; columns past n_cols are discarded)
+        int n_mma = (is_ng<BMODE>() && CTAS == 1) ? ((ti.n_cols + 15) / 16) * 16 : BN;
+        const uint32_t idesc = make_idesc_bf16(TM, n_mma, false, is_kg<BMODE>());
         for (int ks = 0; ks < ti.k_stages; ++ks) {
           mbar_wait(full + stage, phase);
+          if (ks == 0 && it < 3) gemm_stamp(2 + 4 * it);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
           const uint32_t sb = sa + L::kABytes;
@@ -246,26 +303,32 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           for (int kk = 0; kk < kk_n; ++kk) {
             uint64_t da = make_sdesc(sa + kk * 32, 16, 1024);
             uint64_t db = is_kg<BMODE>() ? make_sdesc(sb + kk * 2048, kBK * 128, 1024) : make_sdesc(sb + kk * 32, 16, 1024);
-            mma_bf16_ss(d_tmem, da, db, idesc, (ks | kk) != 0);
+            if (CTAS == 2) mma_bf16_ss_cg2(d_tmem, da, db, idesc, (ks | kk) != 0);
+            else mma_bf16_ss(d_tmem, da, db, idesc, (ks | kk) != 0);
           }
-          mma_commit(empty + stage);
+          if (CTAS == 2) mma_commit_cg2(empty + stage);
+          else mma_commit(empty + stage);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        if (ti.k_stages > 0) mma_commit(tfull + buf);
+        if (it < 3) gemm_stamp(3 + 4 * it);
+        if (CTAS == 2) mma_commit_cg2(tfull + buf);  // also fine with no MMA issued (arrives at once)
+        else if (ti.k_stages > 0) mma_commit(tfull + buf);
         else mbar_arrive(tfull + buf);
       }
     }
   } else {
-    // ================= epilogue (warps 2..5): thread <-> accumulator row
+    // ================= epilogue (warps 2..9): thread <-> accumulator row, half of the columns
     const int quad = warp & 3;
     const int r_in_tile = quad * 32 + lane;
     const int ep_tid = threadIdx.x - 64;
+    const int col_half = (warp - 2) / 4;
+    uint8_t* stg = smem + L::kStgOff + (warp - 2) * 32 * kStgPitch;
     int it = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+    for (int t = t0; t < n_tiles_total; t += t_step, ++it) {
       TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t);
       const int buf = it & 1;
       const int* ids = args.ids + (size_t)ti.item * args.ids_stride;
-      const int local_row = ti.mt * kBM + r_in_tile;
+      const int local_row = ti.mt * TM + rank * kBM + r_in_tile;
       const bool row_ok = local_row < args.rows_per_item;
       const size_t grow = (size_t)ti.item * args.rows_per_item + local_row;
       const int r = args.lora_r;
@@ -273,8 +336,8 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
 
       // stage per-column bias / LoRA column factors for this tile
       if (kLora) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        for (int c = ep_tid; c < BN; c += 128) {
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        for (int c = ep_tid; c < BN; c += 32 * kEpiWarps) {
           int j = ti.nt * BN + c;
           int oc = j;
           if (is_ng<BMODE>()) oc = (c < ti.n_cols) ? __ldg(ids + j / args.blk) * args.blk + j % args.blk : 0;
@@ -284,7 +347,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             s_w[c * kMaxR + q] =
                 (ok && q < r && args.lora_w) ? __ldg(args.lora_w + q * args.w_sr + (long long)oc * args.w_sc) : 0.f;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
       }
       float xr[kMaxR];
 #pragma unroll
@@ -296,10 +359,12 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       }
 
       mbar_wait(tfull + buf, (it >> 1) & 1);
+      if (ep_tid == 0 && it < 3) gemm_stamp(4 + 4 * it);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;
       const int n_chunks = (ti.n_cols + 31) / 32;
-      for (int ch = 0; ch < n_chunks; ++ch) {
+      constexpr int kHalf = BN / 64;  // 32-column chunks per column half
+      for (int ch = col_half * kHalf; ch < min(n_chunks, (col_half + 1) * kHalf); ++ch) {
         uint32_t raw[32];
         if (ti.k_stages > 0) {
           tmem_ld_32x32b_x32(t_row + ch * 32, raw);
@@ -332,7 +397,10 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           }
           continue;
         }
-        if (kLora) {
+        if (kLora && r == 0) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += s_bias[c0 + i];
+        } else if (kLora) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const float* w = s_w + (c0 + i) * kMaxR;
@@ -380,7 +448,10 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             }
           }
         }
-        if (!row_ok) continue;
+        // bf16 full chunks go through the warp's staging rows (all lanes take part); else per-row stores
+        const bool stg_ok = !(EPI == kEpiStoreF32 || args.out_f32) && nv == 32 && (args.ldo % 8) == 0 &&
+                            (reinterpret_cast<uintptr_t>(args.out) & 15) == 0;
+        if (!row_ok && !stg_ok) continue;
         if (EPI == kEpiStoreF32 || args.out_f32) {
           float* o = reinterpret_cast<float*>(args.out) + grow * args.ldo + j0;
           if (args.resid) {
@@ -405,6 +476,29 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             for (int i = 0; i < 32; ++i)
               if (i < nv) o[i] = v[i];
           }
+        } else if (stg_ok) {
+          // bf16 chunk through shared memory: this thread's 64 B row segment in, then lane l stores
+          // row 8p + l/4, bytes 16(l%4).. : each warp store covers 8 rows x 64 B instead of 32 x 16 B
+          uint32_t p[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) p[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+          uint8_t* mine = stg + lane * kStgPitch;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<uint4*>(mine + 16 * i) = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int pss = 0; pss < 4; ++pss) {
+            const int rr = pss * 8 + (lane >> 2), q = lane & 3;
+            const int lrow = ti.mt * TM + rank * kBM + quad * 32 + rr;
+            if (lrow < args.rows_per_item) {
+              const uint4 val = *reinterpret_cast<const uint4*>(stg + rr * kStgPitch + 16 * q);
+              __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                 ((size_t)ti.item * args.rows_per_item + lrow) * args.ldo + j0 + 8 * q;
+              *reinterpret_cast<uint4*>(o) = val;
+            }
+          }
+          __syncwarp();
         } else {
           __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + grow * args.ldo + j0;
           if (nv == 32 && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
@@ -424,13 +518,21 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       // release the accumulator buffer to the MMA warp
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + buf);
+      if (lane == 0) {
+        if (CTAS == 2) mbar_arrive_leader(tempty + buf);
+        else mbar_arrive(tempty + buf);
+      }
+      if (ep_tid == 0 && it < 3) gemm_stamp(5 + 4 * it);
     }
   }
+  tc_fence_before();
   __syncthreads();
+  if (CTAS == 2) cluster_sync();  // the peer's TMEM / barriers stay valid until the leader is done
+  if (threadIdx.x == 0) gemm_stamp(1);
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem_base);
+    if (CTAS == 2) tmem_dealloc_cg2<512>(tmem_base);
+    else tmem_dealloc<512>(tmem_base);
   }
 }
 

@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(288) colgrad_partial_kernel(const __grid_const
                                                               const int32_t* __restrict__ counts, int blk,
                                                               float* __restrict__ ws) {
   extern __shared__ uint8_t cg_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(cg_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sm = align_smem_1024(cg_raw);
   float* s_p = reinterpret_cast<float*>(sm + CgSmem::kOffP);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + CgSmem::kOffBar);
   uint64_t* empty = full + kCgSt;

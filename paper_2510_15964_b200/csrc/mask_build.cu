@@ -229,7 +229,7 @@ int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint
     constexpr int smem = GemmSmem<256>::kTotal;
     static cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     LX_CHECK_CUDA(attr);
-    kern<<<num_sms(), 192, smem, stream>>>(ta, tb, args);
+    kern<<<num_sms(), kGemmThreads, smem, stream>>>(ta, tb, args);
     if ((rc = launch_check("mlp mask gemm"))) return rc;
   }
   return lx_mask_compact(bits_ws, n_items, n_blk, scope_batch, counts, ids, pos, stream);

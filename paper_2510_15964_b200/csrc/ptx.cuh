@@ -67,6 +67,59 @@ LX_DEV void tma_load_2d_hint(void* smem_dst, const void* desc, uint64_t* bar, in
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(hint)
       : "memory");
 }
+// Dynamic shared memory rounded up to 1024 B (SWIZZLE_128B atoms) by integer offset, so the
+// result stays a shared-space pointer (a uintptr_t round-trip would turn every access generic).
+LX_DEV uint8_t* align_smem_1024(uint8_t* raw) { return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u); }
+
+// ---------------------------------------------------------------- CTA pairs (cta_group::2)
+// The pair's shared::cluster window: clearing bit 24 of a shared::cta address names the same
+// offset in the even (leader) CTA of the pair.
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
+LX_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+LX_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load into this CTA's smem whose completion (bytes) is counted on the LEADER's mbarrier.
+LX_DEV void tma_load_2d_cg2(void* smem_dst, const void* desc, uint64_t* bar, int32_t c0, int32_t c1, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "l"(hint)
+      : "memory");
+}
+// Arrive (release, cluster scope) on the leader CTA's copy of this barrier.
+LX_DEV void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask) : "memory");
+}
+template <uint32_t kCols>
+LX_DEV void tmem_alloc_cg2(uint32_t* dst_smem) {  // one warp in each CTA of the pair (same warp id)
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)), "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+template <uint32_t kCols>
+LX_DEV void tmem_dealloc_cg2(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
+}
+// D[tmem of both CTAs] (+)= A[smem of both] * B[smem of both]^T, M = 256 (128 rows per CTA), B split by N.
+LX_DEV void mma_bf16_ss_cg2(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
+}
+// Arrive on this barrier offset in BOTH CTAs of the pair once the issued MMAs complete.
+LX_DEV void mma_commit_cg2(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
 // L2 cache-policy descriptors (createpolicy): weights are re-read by many CTAs.
 LX_DEV uint64_t policy_evict_last() {
   uint64_t p;

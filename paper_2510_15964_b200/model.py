@@ -361,11 +361,30 @@ def lora_linear_forward(x, w, bias, adapter: LoraAdapter | None):
     return z, cache
 
 
-def layernorm_forward(x: torch.Tensor, gamma, beta, eps: float = 1e-5, x_small_spec=None, delta=None):
+class PendingResidual:
+    """A block output whose residual add is deferred to the next LayerNorm: value = base + delta
+    (fp32 base, bf16 delta [M, d]). The LN kernel materialises the fp32 sum it normalises."""
+
+    __slots__ = ("base", "delta")
+
+    def __init__(self, base: torch.Tensor, delta: torch.Tensor):
+        self.base, self.delta = base, delta
+
+    @property
+    def shape(self):
+        return self.base.shape
+
+    def materialize(self) -> torch.Tensor:
+        return (self.base.reshape(-1, self.base.shape[-1]) + self.delta.float()).view(self.base.shape)
+
+
+def layernorm_forward(x, gamma, beta, eps: float = 1e-5, x_small_spec=None, delta=None):
     """sf/model.py:307-312 on the fused kernel; x fp32 [M, d] -> bf16 y. x_small_spec=(s, m)
     additionally writes the predictor's downsampled rows (returned in the cache). With `delta`
-    (bf16 [M, d]) the residual add x + delta is fused: the fp32 sum is normalised and returned
-    as cache["x"] (the block's y, sf/model.py:420)."""
+    (bf16 [M, d]) -- or x a PendingResidual -- the residual add x + delta is fused: the fp32 sum
+    is normalised and returned as cache["x"] (the block's y, sf/model.py:420)."""
+    if isinstance(x, PendingResidual):
+        x, delta = x.base, x.delta
     x2 = x.reshape(-1, x.shape[-1]).contiguous()
     M, d = x2.shape
     y = torch.empty(M, d, dtype=torch.bfloat16, device=x2.device)
@@ -520,7 +539,7 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
     LayerMasks or a provider with attn_patterns(layer, h) / mlp_mask(layer, h)."""
     lw = model.weights.layers[layer]
     lora = {t: model.lora[(layer, t)] for t in model.lora_targets} if model.peft_method == "lora" else {}
-    B, s, d = x.shape
+    B, s, d = x.shape  # x: fp32 [B, s, d] or a PendingResidual (previous block's y + MLP)
     static = isinstance(masks, LayerMasks)
     spec = None
     if not static and getattr(masks, "fused_downsample", False):
@@ -536,7 +555,7 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
     else:
         hp = masks.attn_patterns(layer, h1v)
     adapter = model.peft_method == "adapter"
-    x2 = x.reshape(B * s, d)
+    x2 = c1["x"]  # the block input (materialised by LN1 when x was a pending residual)
     att, ca = mha_forward(h1v, lw, lora, hp, model.pool, model.dims, counter, dpool=model.dpool)
     caa = None
     if adapter:
@@ -548,16 +567,17 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
     y = c2["x"]
     h2v = h2.view(B, s, d)
     nm = masks.neuron_mask if static else masks.mlp_mask(layer, h2v)
-    mo, cm = mlp_forward(h2v, lw, lora, nm, model.dims, counter, resid=None if adapter else y, out_f32=True)
+    # the MLP's residual add (y + MLP) is deferred into the next LayerNorm: fc2 stores bf16 only
+    mo, cm = mlp_forward(h2v, lw, lora, nm, model.dims, counter, out_f32=adapter)
     cma = None
     if adapter:
         mo, cma = adapter_forward(mo, model.adapters[(layer, "mlp")])
-        out = y + mo
+        out = (y + mo).view(B, s, d)
     else:
-        out = mo
+        out = PendingResidual(y.view(B, s, d), mo)
     cache = {"ln1": c1, "attn": ca, "attn_adapter": caa, "ln2": c2, "mlp": cm, "mlp_adapter": cma,
              "masks": LayerMasks(ca["pidx"], cm["mask"])}
-    return out.view(B, s, d), cache
+    return out, cache
 
 
 def model_forward(model: Model, tokens, masks, counter=None):

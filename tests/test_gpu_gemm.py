@@ -21,9 +21,19 @@ def rel(a, b):
     return ((a - b).abs().max() / b.abs().max().clamp_min(1e-30)).item()
 
 
+@pytest.fixture(params=[1, 0], ids=["cta_pair", "single_cta"])
+def engine(request):
+    """Both GEMM engine variants: CTA pairs (tcgen05.mma.cta_group::2) and single-CTA tiles."""
+    from paper_2510_15964_b200 import _abi
+
+    prev = _abi.lib().lx_gemm_set_cta_pair(request.param)
+    yield request.param
+    _abi.lib().lx_gemm_set_cta_pair(prev)
+
+
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 200), (1024, 1024, 1024), (4096, 512, 2048)])
 @pytest.mark.parametrize("f32", [True, False])
-def test_dense_gemm(M, N, K, f32):
+def test_dense_gemm(M, N, K, f32, engine):
     from paper_2510_15964_b200 import _abi
 
     dev = _dev()
@@ -53,7 +63,7 @@ def _masks(n_items, n_blk, density, seed):
                                                            (4, 512, 2048, 8192, 16, 0.2, 8), (2, 256, 256, 1024, 32, 0.4, 0),
                                                            (2, 128, 128, 512, 64, 0.6, 4)])
 @pytest.mark.parametrize("packed", [False, True])
-def test_neuron_mlp_gemms(n_items, s, d, d_ff, blk, density, r, packed):
+def test_neuron_mlp_gemms(n_items, s, d, d_ff, blk, density, r, packed, engine):
     from paper_2510_15964_b200 import _abi
 
     dev = _dev()
