@@ -38,9 +38,10 @@ typedef struct CUstream_st* lx_stream_t;
 const char* lx_last_error(void);
 int lx_abi_version(void);
 int lx_device_sm_count(void);
-/* GEMM engine variant for the dense / item-packed modes: 1 = CTA pairs (tcgen05.mma.cta_group::2,
- * 256-row tiles), 0 (default) = single-CTA 128-row tiles. Returns the previous value. */
-int lx_gemm_set_cta_pair(int on);
+/* GEMM engine variant for the dense / item-packed modes: 0 (default) = single-CTA 128 x 256 tiles,
+ * 1 = CTA pairs (tcgen05.mma.cta_group::2) with 256 x 256 tiles, 2 = CTA pairs with 256 x 128 tiles.
+ * Returns the previous value. */
+int lx_gemm_set_cta_pair(int mode);
 /* Debug only: per-CTA clock64 phase stamps of the GEMM engine into buf [grid][32]; NULL disables. */
 int lx_debug_set_gemm_trace(unsigned long long* buf);
 

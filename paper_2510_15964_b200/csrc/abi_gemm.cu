@@ -95,10 +95,12 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
 }
 
 // dense / packed B: pick the CTA-pair engine when enabled (B boxes are then BN/2 rows on the N side)
+// tb1: B boxes for 1-CTA 256-wide tiles; tb2: 128-row boxes (pair, BN 256); tb4: 64-row boxes (pair, BN 128)
 template <int BMODE, int EPI>
-static int launch_gemm_auto(const CUtensorMap& ta, const CUtensorMap& tb1, const CUtensorMap& tb2, const GemmArgs& args,
-                            cudaStream_t st) {
-  if (g_cta_pair) return launch_gemm<BMODE, EPI, 256, 2>(ta, tb2, args, st);
+static int launch_gemm_auto(const CUtensorMap& ta, const CUtensorMap& tb1, const CUtensorMap& tb2, const CUtensorMap& tb4,
+                            const GemmArgs& args, cudaStream_t st) {
+  if (g_cta_pair == 2) return launch_gemm<BMODE, EPI, 128, 2>(ta, tb4, args, st);
+  if (g_cta_pair == 1) return launch_gemm<BMODE, EPI, 256, 2>(ta, tb2, args, st);
   return launch_gemm<BMODE, EPI, 256, 1>(ta, tb1, args, st);
 }
 
@@ -148,9 +150,9 @@ int lx_debug_set_gemm_trace(unsigned long long* buf) {
   return 0;
 }
 
-int lx_gemm_set_cta_pair(int on) {
+int lx_gemm_set_cta_pair(int mode) {
   const int prev = g_cta_pair;
-  g_cta_pair = on ? 1 : 0;
+  g_cta_pair = (mode == 1 || mode == 2) ? mode : 0;
   return prev;
 }
 
@@ -160,14 +162,15 @@ int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void
   CUtensorMap ta, tb;
   int rc;
   if ((rc = make_tmap_bf16_2d(&ta, a, K, M, lda, kBK, kBM))) return rc;
-  CUtensorMap tb2;
+  CUtensorMap tb2, tb4;
   if ((rc = make_tmap_bf16_2d(&tb, b, K, N, ldb, kBK, 256))) return rc;
   if ((rc = make_tmap_bf16_2d(&tb2, b, K, N, ldb, kBK, 128))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb4, b, K, N, ldb, kBK, 64))) return rc;
   GemmArgs args = base_args(1, M, N, K);
   args.out = c;
   args.ldo = ldc;
-  return c_is_f32 ? launch_gemm_auto<kDense, kEpiStoreF32>(ta, tb, tb2, args, stream)
-                  : launch_gemm_auto<kDense, kEpiStoreBF16>(ta, tb, tb2, args, stream);
+  return c_is_f32 ? launch_gemm_auto<kDense, kEpiStoreF32>(ta, tb, tb2, tb4, args, stream)
+                  : launch_gemm_auto<kDense, kEpiStoreBF16>(ta, tb, tb2, tb4, args, stream);
 }
 
 int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, int N, int K, void* out, int ldo,
@@ -238,10 +241,11 @@ int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int bl
   args.lora_r = (ax1 && b1_lora) ? r : 0;
   args.lora_scale = scaling;
   if (w1_packed) {
-    CUtensorMap tb2;
+    CUtensorMap tb2, tb4;
     if ((rc = mlp_tmap_b(&tb2, w1_t, w1_packed, n_items, d, d_ff, blk, true, 128))) return rc;
-    return apply_relu ? launch_gemm_auto<kPackedN, kEpiFc1>(ta, tb, tb2, args, stream)
-                      : launch_gemm_auto<kPackedN, kEpiFc1Raw>(ta, tb, tb2, args, stream);
+    if ((rc = mlp_tmap_b(&tb4, w1_t, w1_packed, n_items, d, d_ff, blk, true, 64))) return rc;
+    return apply_relu ? launch_gemm_auto<kPackedN, kEpiFc1>(ta, tb, tb2, tb4, args, stream)
+                      : launch_gemm_auto<kPackedN, kEpiFc1Raw>(ta, tb, tb2, tb4, args, stream);
   }
   return apply_relu ? launch_gemm<kNGather, kEpiFc1, 256>(ta, tb, args, stream)
                     : launch_gemm<kNGather, kEpiFc1Raw, 256>(ta, tb, args, stream);
@@ -275,7 +279,7 @@ int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_
   args.lora_scale = scaling;
   args.out_f32 = out_f32;
   args.resid = resid;
-  if (w2_packed) return launch_gemm_auto<kPackedK, kEpiFc2>(ta, tb, tb, args, stream);
+  if (w2_packed) return launch_gemm_auto<kPackedK, kEpiFc2>(ta, tb, tb, tb, args, stream);
   return launch_gemm<kKGather, kEpiFc2, 256>(ta, tb, args, stream);
 }
 
@@ -303,9 +307,10 @@ int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_
   args.act = reinterpret_cast<const __nv_bfloat16*>(a);
   args.ld_act = ld_h;
   if (w2_packed) {
-    CUtensorMap tb2;
+    CUtensorMap tb2, tb4;
     if ((rc = mlp_tmap_b(&tb2, w2, w2_packed, n_items, d, d_ff, blk, true, 128))) return rc;
-    return launch_gemm_auto<kPackedN, kEpiDa>(ta, tb, tb2, args, stream);
+    if ((rc = mlp_tmap_b(&tb4, w2, w2_packed, n_items, d, d_ff, blk, true, 64))) return rc;
+    return launch_gemm_auto<kPackedN, kEpiDa>(ta, tb, tb2, tb4, args, stream);
   }
   return launch_gemm<kNGather, kEpiDa, 256>(ta, tb, args, stream);
 }
@@ -333,7 +338,7 @@ int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d,
   args.w_sc = r;
   args.lora_r = (dax1 && a1_lora) ? r : 0;
   args.out_f32 = out_f32;
-  if (w1_packed) return launch_gemm_auto<kPackedK, kEpiDx>(ta, tb, tb, args, stream);
+  if (w1_packed) return launch_gemm_auto<kPackedK, kEpiDx>(ta, tb, tb, tb, args, stream);
   return launch_gemm<kKGather, kEpiDx, 256>(ta, tb, args, stream);
 }
 

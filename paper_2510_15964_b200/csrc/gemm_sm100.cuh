@@ -100,7 +100,7 @@ constexpr int kStgPitch = 80;  // bytes per staged row: 64 B of bf16 + 16 B pad 
 
 template <int BN, int CTAS = 1>
 struct GemmSmem {
-  static constexpr int kStages = CTAS == 2 ? 5 : (BN >= 256 ? 3 : 5);
+  static constexpr int kStages = CTAS == 2 ? (BN >= 256 ? 5 : 7) : (BN >= 256 ? 3 : 5);
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = (BN / CTAS) * kBK * 2;  // this CTA's share of the B tile
   static constexpr int kStageBytes = kABytes + kBBytes;

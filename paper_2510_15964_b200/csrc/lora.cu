@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_
 }
 
 constexpr int kCgCols = 128;  // 32 lanes x 4 columns
-constexpr int kCgRows = 512;  // rows per CTA (one split)
+constexpr int kCgRows = 256;  // rows per CTA (one split): 2 CTAs per SM keep ~128 KB of X in flight
 
 // partial[item][split][q][col] = sum over the split's rows of P[row, q] X[row, col] over the item's
 // packed columns. A CTA owns 128 columns x kCgRows rows: warp 8 streams [32 rows x 128 cols] tiles
@@ -246,6 +246,18 @@ constexpr int kCgRows = 512;  // rows per CTA (one split)
 // q >= r are ignored by the final kernel). The ring is reused for the cross-warp reduction.
 constexpr int kCgSt = 8, kCgTile = 32 * kCgCols * 2;  // bytes per stage (2 atoms of [32][128B])
 
+// Debug-only phase trace (lx_debug_set_colgrad_trace): per CTA 8 clock64 stamps, NULL in production.
+__device__ unsigned long long* g_cg_trace = nullptr;
+LX_DEV void cg_stamp(int slot) {
+  unsigned long long* t = g_cg_trace;
+  if (t != nullptr) {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    const size_t cta = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+    t[cta * 8 + slot] = c;
+  }
+}
+
 struct CgSmem {
   static constexpr int kOffP = kCgSt * kCgTile;       // s_p [kCgRows][8] fp32
   static constexpr int kOffBar = kOffP + kCgRows * 8 * 4;
@@ -253,7 +265,7 @@ struct CgSmem {
 };
 
 template <int R>
-__global__ void __launch_bounds__(288) colgrad_partial_kernel(const __grid_constant__ CUtensorMap tm_x, const float* __restrict__ p,
+__global__ void __launch_bounds__(288, 2) colgrad_partial_kernel(const __grid_constant__ CUtensorMap tm_x, const float* __restrict__ p,
                                                               int ldp, int s, int ncols, int r,
                                                               const int32_t* __restrict__ counts, int blk,
                                                               float* __restrict__ ws) {
@@ -271,6 +283,7 @@ __global__ void __launch_bounds__(288) colgrad_partial_kernel(const __grid_const
   const int nrows = min(kCgRows, s - r0);
   const int n_tiles = (nrows + 31) / 32;
   if (threadIdx.x == 0) {
+    cg_stamp(0);
     for (int i = 0; i < kCgSt; ++i) {
       mbar_init(full + i, 1);
       mbar_init(empty + i, 8);
@@ -302,6 +315,7 @@ __global__ void __launch_bounds__(288) colgrad_partial_kernel(const __grid_const
     *reinterpret_cast<float4*>(s_p + i * 8 + h * 4) = v;
   }
   asm volatile("bar.sync 1, 256;" ::: "memory");
+  if (threadIdx.x == 0) cg_stamp(1);
   float acc[4][R];
 #pragma unroll
   for (int j = 0; j < 4; ++j)
@@ -311,6 +325,7 @@ __global__ void __launch_bounds__(288) colgrad_partial_kernel(const __grid_const
   for (int t = 0; t < n_tiles; ++t) {
     const int st = t % kCgSt;
     mbar_wait(full + st, (t / kCgSt) & 1);
+    if (threadIdx.x == 0 && t == 0) cg_stamp(2);
     const uint8_t* tile = sm + st * kCgTile + atom * (kCgTile / 2);
 #pragma unroll
     for (int rr = 0; rr < 4; ++rr) {
@@ -330,6 +345,7 @@ __global__ void __launch_bounds__(288) colgrad_partial_kernel(const __grid_const
     if (lane == 0) mbar_arrive(empty + st);
   }
   // every tile consumed (each consumer waited all full barriers) -> the ring is free for the reduction
+  if (threadIdx.x == 0) cg_stamp(3);
   asm volatile("bar.sync 1, 256;" ::: "memory");
   float* s_red = reinterpret_cast<float*>(sm);  // [8 warps][R][kCgCols + 4]
   constexpr int kRs = kCgCols + 4;
@@ -346,6 +362,7 @@ __global__ void __launch_bounds__(288) colgrad_partial_kernel(const __grid_const
     for (int w2 = 0; w2 < 8; ++w2) v += s_red[(w2 * R + q) * kRs + cc];
     out[(size_t)q * ncols + c] = v;
   }
+  if (threadIdx.x == 0) cg_stamp(4);
 }
 
 // G(q, c_orig) = scale * sum_items sum_splits partial[item][split][q][pos_item(c_orig)]
@@ -471,6 +488,11 @@ int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const floa
   else
     rowproj_kernel<16><<<grid, 256, 0, stream>>>(xb, ldx, s, K, w, w_sk, w_sq, r, scale, counts, ids, ids_stride, b, y, ldy);
   return launch_check("rowproj");
+}
+
+int lx_debug_set_colgrad_trace(unsigned long long* buf) {
+  LX_CHECK_CUDA(cudaMemcpyToSymbol(g_cg_trace, &buf, sizeof(buf)));
+  return 0;
 }
 
 long long lx_colgrad_ws_floats(int n_items, int s, int ncols, int r) {

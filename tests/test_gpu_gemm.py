@@ -21,9 +21,9 @@ def rel(a, b):
     return ((a - b).abs().max() / b.abs().max().clamp_min(1e-30)).item()
 
 
-@pytest.fixture(params=[1, 0], ids=["cta_pair", "single_cta"])
+@pytest.fixture(params=[0, 1, 2], ids=["single_cta", "cta_pair_256", "cta_pair_128"])
 def engine(request):
-    """Both GEMM engine variants: CTA pairs (tcgen05.mma.cta_group::2) and single-CTA tiles."""
+    """All GEMM engine variants: single-CTA tiles and CTA pairs (tcgen05.mma.cta_group::2), N 256 / 128."""
     from paper_2510_15964_b200 import _abi
 
     prev = _abi.lib().lx_gemm_set_cta_pair(request.param)
