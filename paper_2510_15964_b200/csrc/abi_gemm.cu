@@ -169,6 +169,11 @@ int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void
   GemmArgs args = base_args(1, M, N, K);
   args.out = c;
   args.ldo = ldc;
+  // under-filled single-CTA problems (e.g. the predictor projection, M = B*m = 184): 128-wide tiles
+  const long long tiles256 = (long long)((M + kBM - 1) / kBM) * ((N + 255) / 256);
+  if (g_cta_pair == 0 && tiles256 < num_sms())
+    return c_is_f32 ? launch_gemm<kDense, kEpiStoreF32, 128, 1>(ta, tb2, args, stream)
+                    : launch_gemm<kDense, kEpiStoreBF16, 128, 1>(ta, tb2, args, stream);
   return c_is_f32 ? launch_gemm_auto<kDense, kEpiStoreF32>(ta, tb, tb2, tb4, args, stream)
                   : launch_gemm_auto<kDense, kEpiStoreBF16>(ta, tb, tb2, tb4, args, stream);
 }

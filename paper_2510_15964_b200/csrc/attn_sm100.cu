@@ -731,23 +731,50 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
   }
 }
 
-// delta[item, h, row] = sum_c dO[row, c] * O[row, c]  (== rowsum(dP * P), sf/block_sparse.py:102-113)
-__global__ void bsattn_delta_tc_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ d_o, int ld,
-                                       int n_rows_total, int s, int H, int hd, float* __restrict__ delta) {
-  const int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// delta[item, h, row] = sum_c dO[row, c] * O[row, c]  (== rowsum(dP * P), sf/block_sparse.py:102-113).
+// One warp per token row: lane l reads 16 B chunks l, l+32, ... of O and dO (all in flight), a group of
+// HD/8 lanes holds one head per pass and reduces it with shuffles.
+template <int HD>
+__global__ void __launch_bounds__(256) bsattn_delta_tc_kernel(const __nv_bfloat16* __restrict__ o,
+                                                              const __nv_bfloat16* __restrict__ d_o, int ld,
+                                                              int n_rows_total, int s, int H, float* __restrict__ delta) {
+  constexpr int G = HD / 8;  // lanes per head
+  constexpr int kIt = 8;     // 16 B chunks per lane per pass (2048 columns)
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp_g >= n_rows_total * H) return;
-  const int row = warp_g / H, h = warp_g % H;
-  const __nv_bfloat16* a = o + (size_t)row * ld + h * hd;
-  const __nv_bfloat16* b = d_o + (size_t)row * ld + h * hd;
-  float acc = 0.f;
-  for (int c = lane * 2; c < hd; c += 64) {
-    __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(a + c);
-    __nv_bfloat162 y = *reinterpret_cast<const __nv_bfloat162*>(b + c);
-    acc += __bfloat162float(x.x) * __bfloat162float(y.x) + __bfloat162float(x.y) * __bfloat162float(y.y);
+  if (row >= n_rows_total) return;
+  const int d = H * HD, n_it = (d + 255) / 256;
+  const uint4* a = reinterpret_cast<const uint4*>(o + (size_t)row * ld);
+  const uint4* b = reinterpret_cast<const uint4*>(d_o + (size_t)row * ld);
+  const size_t out_row = (size_t)(row / s) * H * s + row % s;
+  for (int base = 0; base < n_it; base += kIt) {
+  uint4 va[kIt], vb[kIt];
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {
+    const int c = (base + i) * 32 + lane;
+    const bool ok = base + i < n_it && c * 8 < d;
+    va[i] = ok ? __ldg(a + c) : make_uint4(0u, 0u, 0u, 0u);
+    vb[i] = ok ? __ldg(b + c) : make_uint4(0u, 0u, 0u, 0u);
   }
-  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) delta[((size_t)(row / s) * H + h) * s + row % s] = acc;
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {
+    const int it = base + i;
+    if (it >= n_it) break;
+    const uint32_t xa[4] = {va[i].x, va[i].y, va[i].z, va[i].w}, xb[4] = {vb[i].x, vb[i].y, vb[i].z, vb[i].w};
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __nv_bfloat162 p = *reinterpret_cast<const __nv_bfloat162*>(&xa[k]);
+      const __nv_bfloat162 q = *reinterpret_cast<const __nv_bfloat162*>(&xb[k]);
+      acc = fmaf(__low2float(p), __low2float(q), acc);
+      acc = fmaf(__high2float(p), __high2float(q), acc);
+    }
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    const int h = (it * 32 + lane) * 8 / HD;
+    if ((lane % G) == 0 && h < H) delta[out_row + (size_t)h * s] = acc;
+  }
+  }
 }
 
 template <int HD>
@@ -755,9 +782,10 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const u
                          int H, const int32_t* pidx, int item_stride, const int32_t* tables128, float scale,
                          const float* lse, float* delta, float* ksum, uint16_t* dqkv, cudaStream_t st) {
   const int rows = n_items * s;
-  bsattn_delta_tc_kernel<<<(rows * H * 32 + 255) / 256, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(o),
-                                                                        reinterpret_cast<const __nv_bfloat16*>(d_o), ld_o,
-                                                                        rows, s, H, HD, delta);
+  LX_REQUIRE(ld_o % 8 == 0, LX_ERR_SHAPE, "attention bwd: O / dO row stride must be a multiple of 8");
+  bsattn_delta_tc_kernel<HD><<<(rows * 32 + 255) / 256, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(o),
+                                                                      reinterpret_cast<const __nv_bfloat16*>(d_o), ld_o,
+                                                                      rows, s, H, delta);
   int rc = launch_check("bsattn_delta_tc");
   if (rc) return rc;
   CUtensorMap tm_qkv, tm_do;

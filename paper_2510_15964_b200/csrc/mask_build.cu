@@ -207,10 +207,13 @@ int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint
   LX_REQUIRE(n_items <= kMaxItems, LX_ERR_UNSUPPORTED, "too many items");
   const int words = (n_blk + 31) / 32;
   LX_CHECK_CUDA(cudaMemsetAsync(bits_ws, 0, sizeof(uint32_t) * n_items * words, stream));
+  // 128-wide tiles when 256-wide ones would leave SMs idle (n_blk = 512: 64 tiles at B = 8 x 512 tokens)
+  const long long tiles256 = (long long)n_items * ((s + kBM - 1) / kBM) * ((n_blk + 255) / 256);
+  const int bn = tiles256 < num_sms() ? 128 : 256;
   CUtensorMap ta, tb;
   int rc;
   if ((rc = make_tmap_bf16_2d(&ta, h, d, (uint64_t)n_items * s, d, kBK, kBM))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, wa_t, d, n_blk, d, kBK, 256))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, wa_t, d, n_blk, d, kBK, bn))) return rc;
   GemmArgs args;
   memset(&args, 0, sizeof(args));
   args.n_items = n_items;
@@ -224,14 +227,20 @@ int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint
   args.bits = bits_ws;
   args.bits_stride = words;
   args.lora_scale = 1.f;
-  {
+  if (bn == 128) {
+    auto kern = gemm_sm100_kernel<kDense, kEpiMask, 128>;
+    constexpr int smem = GemmSmem<128>::kTotal;
+    static cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    LX_CHECK_CUDA(attr);
+    kern<<<num_sms(), kGemmThreads, smem, stream>>>(ta, tb, args);
+  } else {
     auto kern = gemm_sm100_kernel<kDense, kEpiMask, 256>;
     constexpr int smem = GemmSmem<256>::kTotal;
     static cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     LX_CHECK_CUDA(attr);
     kern<<<num_sms(), kGemmThreads, smem, stream>>>(ta, tb, args);
-    if ((rc = launch_check("mlp mask gemm"))) return rc;
   }
+  if ((rc = launch_check("mlp mask gemm"))) return rc;
   return lx_mask_compact(bits_ws, n_items, n_blk, scope_batch, counts, ids, pos, stream);
 }
 
