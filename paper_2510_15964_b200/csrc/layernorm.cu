@@ -141,6 +141,162 @@ __global__ void __launch_bounds__(kLnThreads) ln_bwd_kernel(const void* __restri
   }
 }
 
+// ---------------------------------------------------------------- warp-per-row variants (d <= 2048)
+// One warp owns a row: lane l holds float4 chunks l, l+32, ... (VEC of them) in registers, both
+// reductions are warp shuffles (no block barriers), and 8 rows per CTA keep ~64-160 KB in flight per SM.
+LX_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const float* __restrict__ x, int M, int d,
+                                                          const float* __restrict__ g, const float* __restrict__ b,
+                                                          float eps, __nv_bfloat16* __restrict__ y,
+                                                          float* __restrict__ mean_out, float* __restrict__ istd_out, int s,
+                                                          int m_small, __nv_bfloat16* __restrict__ x_small,
+                                                          const __nv_bfloat16* __restrict__ delta,
+                                                          float* __restrict__ resid_out) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const int nv = d / 4;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * d);
+  const uint2* dr = delta ? reinterpret_cast<const uint2*>(delta + (size_t)row * d) : nullptr;
+  float4 v[VEC];
+  uint2 dv[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = lane + 32 * i;
+    v[i] = c < nv ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    dv[i] = (dr && c < nv) ? __ldg(dr + c) : make_uint2(0u, 0u);
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = lane + 32 * i;
+    if (dr && c < nv) {  // fused residual add: y = x + delta (sf/model.py:420, 427), y kept in fp32
+      v[i].x += bf16_bits_to_float(dv[i].x & 0xffff);
+      v[i].y += bf16_bits_to_float(dv[i].x >> 16);
+      v[i].z += bf16_bits_to_float(dv[i].y & 0xffff);
+      v[i].w += bf16_bits_to_float(dv[i].y >> 16);
+      reinterpret_cast<float4*>(resid_out + (size_t)row * d)[c] = v[i];
+    }
+    sum += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+  const float mu = warp_sum(sum) / d;
+  float sq = 0.f;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nv) {
+      const float a = v[i].x - mu, bb = v[i].y - mu, cc = v[i].z - mu, dd = v[i].w - mu;
+      sq += (a * a + bb * bb) + (cc * cc + dd * dd);
+    }
+  }
+  const float istd = 1.0f / sqrtf(warp_sum(sq) / d + eps);
+  if (lane == 0) {
+    mean_out[row] = mu;
+    istd_out[row] = istd;
+  }
+  __nv_bfloat16* xs_row = nullptr;  // fused downsample: token t is sampled iff t == (i*s)//m for some i
+  if (x_small) {
+    const int t = row % s, item = row / s;
+    const int i = (int)(((long long)t * m_small + s - 1) / s);
+    if (i < m_small && (int)(((long long)i * s) / m_small) == t) xs_row = x_small + ((size_t)item * m_small + i) * d;
+  }
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nv) {
+      const float4 gg = __ldg(g4 + c), bb = __ldg(b4 + c);
+      const uint2 pk = make_uint2(pack_bf16x2((v[i].x - mu) * istd * gg.x + bb.x, (v[i].y - mu) * istd * gg.y + bb.y),
+                                  pack_bf16x2((v[i].z - mu) * istd * gg.z + bb.z, (v[i].w - mu) * istd * gg.w + bb.w));
+      *reinterpret_cast<uint2*>(y + (size_t)row * d + 4 * c) = pk;
+      if (xs_row) *reinterpret_cast<uint2*>(xs_row + 4 * c) = pk;
+    }
+  }
+}
+
+template <bool kF32, int VEC>
+__global__ void __launch_bounds__(256) ln_bwd_warp_kernel(const void* __restrict__ dy_, const float* __restrict__ x,
+                                                          const float* __restrict__ g, const float* __restrict__ mean,
+                                                          const float* __restrict__ istd, int M, int d,
+                                                          float* __restrict__ dx, __nv_bfloat16* __restrict__ dx_bf16) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const int nv = d / 4;
+  const float mu = __ldg(mean + row), is = __ldg(istd + row);
+  float4 gv[VEC], xh[VEC];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = lane + 32 * i;
+    float4 dy = make_float4(0.f, 0.f, 0.f, 0.f), xx = dy, gg = dy;
+    if (c < nv) {
+      if (kF32) {
+        dy = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(dy_) + (size_t)row * d) + c);
+      } else {
+        const uint2 p = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(dy_) + (size_t)row * d) + c);
+        dy = make_float4(bf16_bits_to_float(p.x & 0xffff), bf16_bits_to_float(p.x >> 16), bf16_bits_to_float(p.y & 0xffff),
+                         bf16_bits_to_float(p.y >> 16));
+      }
+      xx = __ldg(reinterpret_cast<const float4*>(x + (size_t)row * d) + c);
+      gg = __ldg(reinterpret_cast<const float4*>(g) + c);
+    }
+    gv[i] = make_float4(dy.x * gg.x, dy.y * gg.y, dy.z * gg.z, dy.w * gg.w);
+    xh[i] = c < nv ? make_float4((xx.x - mu) * is, (xx.y - mu) * is, (xx.z - mu) * is, (xx.w - mu) * is)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    s1 += (gv[i].x + gv[i].y) + (gv[i].z + gv[i].w);
+    s2 += (gv[i].x * xh[i].x + gv[i].y * xh[i].y) + (gv[i].z * xh[i].z + gv[i].w * xh[i].w);
+  }
+  const float mg = warp_sum(s1) / d, mgx = warp_sum(s2) / d;
+  float4* o = reinterpret_cast<float4*>(dx + (size_t)row * d);
+  float4 cur[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = lane + 32 * i;
+    cur[i] = c < nv ? o[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nv) {
+      cur[i].x += is * (gv[i].x - mg - xh[i].x * mgx);
+      cur[i].y += is * (gv[i].y - mg - xh[i].y * mgx);
+      cur[i].z += is * (gv[i].z - mg - xh[i].z * mgx);
+      cur[i].w += is * (gv[i].w - mg - xh[i].w * mgx);
+      o[c] = cur[i];
+      if (dx_bf16)  // bf16 copy of the updated residual gradient: the next GEMMs' operand
+        *reinterpret_cast<uint2*>(dx_bf16 + (size_t)row * d + 4 * c) =
+            make_uint2(pack_bf16x2(cur[i].x, cur[i].y), pack_bf16x2(cur[i].z, cur[i].w));
+    }
+  }
+}
+
+template <int VEC>
+static void ln_fwd_warp(const float* x, const uint16_t* delta, float* resid_out, int M, int d, const float* gamma,
+                        const float* beta, float eps, uint16_t* y, float* mean, float* inv_std, int s, int m_small,
+                        uint16_t* x_small, cudaStream_t st) {
+  ln_fwd_warp_kernel<VEC><<<(M + 7) / 8, 256, 0, st>>>(x, M, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), mean,
+                                                       inv_std, s > 0 ? s : 1, m_small,
+                                                       reinterpret_cast<__nv_bfloat16*>(x_small),
+                                                       reinterpret_cast<const __nv_bfloat16*>(delta), resid_out);
+}
+
+template <int VEC>
+static void ln_bwd_warp(const void* dy, int dy_is_f32, const float* x, const float* gamma, const float* mean,
+                        const float* inv_std, int M, int d, float* dx, __nv_bfloat16* ob, cudaStream_t st) {
+  if (dy_is_f32)
+    ln_bwd_warp_kernel<true, VEC><<<(M + 7) / 8, 256, 0, st>>>(dy, x, gamma, mean, inv_std, M, d, dx, ob);
+  else
+    ln_bwd_warp_kernel<false, VEC><<<(M + 7) / 8, 256, 0, st>>>(dy, x, gamma, mean, inv_std, M, d, dx, ob);
+}
+
 }  // namespace lx
 
 using namespace lx;
@@ -154,6 +310,13 @@ int lx_layernorm_fwd(const float* x, const uint16_t* delta, float* resid_out, in
   LX_REQUIRE(M >= 1, LX_ERR_SHAPE, "layernorm: empty input");
   LX_REQUIRE(!delta || resid_out, LX_ERR_SHAPE, "layernorm: residual add needs resid_out");
   if (x_small) LX_REQUIRE(s >= 1 && m_small >= 1 && M % s == 0, LX_ERR_SHAPE, "layernorm: bad downsample shape");
+  const int per_lane = (d / 4 + 31) / 32;  // float4 chunks per lane in the warp-per-row kernel
+  if (per_lane <= 16) {
+    if (per_lane <= 4) ln_fwd_warp<4>(x, delta, resid_out, M, d, gamma, beta, eps, y, mean, inv_std, s, m_small, x_small, stream);
+    else if (per_lane <= 8) ln_fwd_warp<8>(x, delta, resid_out, M, d, gamma, beta, eps, y, mean, inv_std, s, m_small, x_small, stream);
+    else ln_fwd_warp<16>(x, delta, resid_out, M, d, gamma, beta, eps, y, mean, inv_std, s, m_small, x_small, stream);
+    return launch_check("layernorm_fwd");
+  }
   ln_fwd_kernel<<<M, kLnThreads, 0, stream>>>(x, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), mean, inv_std,
                                               s > 0 ? s : 1, m_small, reinterpret_cast<__nv_bfloat16*>(x_small),
                                               reinterpret_cast<const __nv_bfloat16*>(delta), resid_out);
@@ -164,6 +327,13 @@ int lx_layernorm_bwd(const void* dy, int dy_is_f32, const float* x, const float*
                      const float* inv_std, int M, int d, float* dx_accum, uint16_t* dx_bf16, lx_stream_t stream) {
   LX_REQUIRE(d % 4 == 0 && d <= kLnThreads * 4 * kLnMaxVec, LX_ERR_UNSUPPORTED, "layernorm: d=%d unsupported", d);
   auto* ob = reinterpret_cast<__nv_bfloat16*>(dx_bf16);
+  const int per_lane = (d / 4 + 31) / 32;
+  if (per_lane <= 16) {
+    if (per_lane <= 4) ln_bwd_warp<4>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
+    else if (per_lane <= 8) ln_bwd_warp<8>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
+    else ln_bwd_warp<16>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
+    return launch_check("layernorm_bwd");
+  }
   if (dy_is_f32)
     ln_bwd_kernel<true><<<M, kLnThreads, 0, stream>>>(dy, x, gamma, mean, inv_std, d, dx_accum, ob);
   else

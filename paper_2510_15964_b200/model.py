@@ -450,18 +450,14 @@ QKV_SLOT = {"wq": 0, "wk": 1, "wv": 2}
 
 
 def _qkv_lora(lora: dict, d: int):
-    """Targets among wq/wk/wv, concatenated A [d, n*r] and the segmented column factor
-    W [n*r, 3d] (scaling folded in) that the QKV epilogue applies (sf/model.py:292-304)."""
+    """Targets among wq/wk/wv and their concatenated A [d, n*r] (sf/model.py:292-304): one rowproj
+    computes x A for all of them."""
     tq = [t for t in ("wq", "wk", "wv") if t in lora]
     if not tq:
-        return tq, None, None, 0
+        return tq, None, 0
     r = lora[tq[0]].rank
-    a_cat = torch.cat([lora[t].a for t in tq], 1).contiguous()
-    w = torch.zeros(len(tq) * r, 3 * d, dtype=torch.float32, device=a_cat.device)
-    for j, t in enumerate(tq):
-        sl = QKV_SLOT[t]
-        w[j * r : (j + 1) * r, sl * d : (sl + 1) * d] = lora[t].b * lora[t].scaling
-    return tq, a_cat, w, r
+    a_cat = lora[tq[0]].a if len(tq) == 1 else torch.cat([lora[t].a for t in tq], 1).contiguous()
+    return tq, a_cat, r
 
 
 def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: ModelDims, counter=None, *, dpool=None):
@@ -474,7 +470,7 @@ def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: Mode
     d, H, hd = dims.d_model, dims.n_heads, dims.head_dim
     dp = dpool if dpool is not None else device_pool(pool, x2.device, dims.seq_len, dims.attn_blk)
     pidx, stride = resolve_head_patterns(head_patterns, dp, B, H, x2.device)
-    tq, a_cat, _, r = _qkv_lora(lora, d)
+    tq, a_cat, r = _qkv_lora(lora, d)
     qkv = torch.addmm(lw.bqkv.to(torch.bfloat16), x2, lw.wqkv)  # bf16 [M, 3d]
     ax = None
     if tq:
