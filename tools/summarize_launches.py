@@ -14,7 +14,7 @@ for r in rows[hi + 1:]:
         continue
     v = float(r[ci["Metric Value"]].replace(",", ""))
     u = r[ci["Metric Unit"]]
-    v = v / 1e3 if u == "nsecond" else v * 1e3 if u == "msecond" else v  # -> microseconds
+    v = v / 1e3 if u in ("nsecond", "ns") else v * 1e3 if u in ("msecond", "ms") else v  # -> microseconds
     k = r[ci["Kernel Name"]].split("(")[0][:100]
     agg[k][0] += 1
     agg[k][1] += v
@@ -22,4 +22,4 @@ for r in rows[hi + 1:]:
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 print(f"total {tot / 1e3:.2f} ms over {sum(a[0] for a in agg.values())} launches (ncu-serialised, cold caches)")
 for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
-    print(f"{t / 1e3:8.3f} ms {100 * t / tot:5.1f}%  n={n:4d}  {k}")
+    print(f"{t / 1e3:8.3f} ms {100 * t / tot:5.1f}%  n={n:4d}  {t / n:8.1f} us/launch  {k}")
