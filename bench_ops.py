@@ -118,7 +118,7 @@ def sweep_mlp(args, timer, peak):
         def fwd():
             w1p = N.pack_active_rows(lw.w1_t, nm)
             w2p = N.pack_active_rows(lw.w2, nm)
-            hid = N.neuron_matmul_fwd1(x, lw, nm, blk, bias=b1, relu=True, out=hid_buf, w_packed=w1p)
+            hid = N.neuron_matmul_fwd1(x.view(B, s, d), lw, nm, blk, bias=b1, relu=True, out=hid_buf, w_packed=w1p)
             N.neuron_matmul_fwd2(hid, lw, None, out=out, w_packed=w2p)
             state.update(w1p=w1p, w2p=w2p, hid=hid)
 

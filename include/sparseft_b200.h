@@ -142,7 +142,7 @@ long long lx_rowproj_ws_bytes(int n_items, int K, int r, int gathered);
 
 /* Skinny LoRA gradient reduction over tokens: G[q, c_orig] = scale * sum_rows P[row, q] X[row, c]
  *   (dB1[:,cols], dA2[cols] (transposed), dB2, dA1 (transposed)); summed over items in order.
- *   P fp32 row stride ldp; X bf16 [M, ncols(packed)] row stride ldx; G fp32 with G(q, c) = g[q*g_sq + c*g_sc].
+ *   P fp32 row stride ldp (r <= 16); X bf16 [M, ncols(packed)] row stride ldx; G fp32 with G(q, c) = g[q*g_sq + c*g_sc].
  *   ws: fp32 workspace of lx_colgrad_ws_floats(...) floats. Deterministic. */
 long long lx_colgrad_ws_floats(int n_items, int s, int ncols, int r);
 int lx_colgrad(const float* p, int ldp, const uint16_t* x, int ldx, int n_items, int s, int ncols, int r, float scale,

@@ -235,16 +235,20 @@ __global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_
   }
 }
 
-constexpr int kCgCols = 128;  // 32 lanes x 4 columns
+constexpr int kCgCols = 128;  // columns per CTA: 8 consumer warps x 16 columns
 constexpr int kCgRows = 256;  // rows per CTA (one split): 2 CTAs per SM keep ~128 KB of X in flight
 
 // partial[item][split][q][col] = sum over the split's rows of P[row, q] X[row, col] over the item's
-// packed columns. A CTA owns 128 columns x kCgRows rows: warp 8 streams [32 rows x 128 cols] tiles
-// (two SWIZZLE_128B boxes of 64 columns) through a kCgSt-stage TMA ring, 64 KB in flight; the P rows
-// of the split are staged in shared memory once; consumer warp w accumulates rows 4w..4w+3 of each
-// tile, lane l columns 4l..4l+3 (R <= 8; P rows read as 8 floats: ldp % 4 == 0, ldp >= 8; columns
-// q >= r are ignored by the final kernel). The ring is reused for the cross-warp reduction.
+// packed columns, on tensor cores: it is the GEMM D[col][q] = X^T[col][row] P[row][q] with
+// m = column, n = q, k = row (mma.sync m16n8k16, bf16 in, fp32 accumulate). Warp 8 streams
+// [32 rows x 128 cols] X tiles (two SWIZZLE_128B boxes of 64 columns) through a kCgSt-stage TMA
+// ring (the whole 256-row split in flight); consumer warp w owns columns 16w..16w+15 and takes its
+// A fragments with ldmatrix.trans straight from the swizzled tile. P is staged once per split as
+// bf16 hi + lo ([q][row], padded rows: conflict-free B fragment loads), so X (P_hi + P_lo) keeps
+// ~16 mantissa bits of P. No cross-warp reduction: every warp owns distinct output columns.
+// The CUDA-core form of this kernel was FMA-bound (R FMAs per X element).
 constexpr int kCgSt = 8, kCgTile = 32 * kCgCols * 2;  // bytes per stage (2 atoms of [32][128B])
+constexpr int kCgPStride = kCgRows + 8;               // bf16 elements per staged P row
 
 // Debug-only phase trace (lx_debug_set_colgrad_trace): per CTA 8 clock64 stamps, NULL in production.
 __device__ unsigned long long* g_cg_trace = nullptr;
@@ -258,21 +262,29 @@ LX_DEV void cg_stamp(int slot) {
   }
 }
 
+template <int RN>
 struct CgSmem {
-  static constexpr int kOffP = kCgSt * kCgTile;       // s_p [kCgRows][8] fp32
-  static constexpr int kOffBar = kOffP + kCgRows * 8 * 4;
+  static constexpr int kOffP = kCgSt * kCgTile;  // s_pt [2][RN][kCgPStride] bf16
+  static constexpr int kOffBar = kOffP + 2 * RN * kCgPStride * 2;
   static constexpr int kTotal = kOffBar + 2 * kCgSt * 8 + 1024;
 };
 
-template <int R>
+LX_DEV void ldsm_x4_trans(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+template <int RN>
 __global__ void __launch_bounds__(288, 2) colgrad_partial_kernel(const __grid_constant__ CUtensorMap tm_x, const float* __restrict__ p,
                                                               int ldp, int s, int ncols, int r,
                                                               const int32_t* __restrict__ counts, int blk,
                                                               float* __restrict__ ws) {
+  constexpr int NT = RN / 8;
   extern __shared__ uint8_t cg_raw[];
   uint8_t* sm = align_smem_1024(cg_raw);
-  float* s_p = reinterpret_cast<float*>(sm + CgSmem::kOffP);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + CgSmem::kOffBar);
+  __nv_bfloat16* s_pt = reinterpret_cast<__nv_bfloat16*>(sm + CgSmem<RN>::kOffP);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + CgSmem<RN>::kOffBar);
   uint64_t* empty = full + kCgSt;
   const int item = blockIdx.z, split = blockIdx.y;
   const int n_splits = gridDim.y;
@@ -306,67 +318,74 @@ __global__ void __launch_bounds__(288, 2) colgrad_partial_kernel(const __grid_co
     }
     return;
   }
-  // P rows of this split -> smem (p == NULL: column sums, P = 1); rows past nrows are zero
-  for (int e = threadIdx.x; e < kCgRows * 2; e += 256) {
-    const int i = e >> 1, h = e & 1;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < nrows) v = p ? __ldg(reinterpret_cast<const float4*>(p + ((size_t)item * s + r0 + i) * ldp) + h)
-                         : make_float4(1.f, 1.f, 1.f, 1.f);
-    *reinterpret_cast<float4*>(s_p + i * 8 + h * 4) = v;
+  // P rows of this split -> smem as bf16 hi/lo, transposed (p == NULL: column sums, P[:, 0] = 1);
+  // rows past nrows and columns q >= r are zero
+  for (int e = threadIdx.x; e < kCgRows * RN; e += 256) {
+    const int i = e / RN, q = e % RN;
+    float v = 0.f;
+    if (i < nrows && q < r) v = p ? __ldg(p + ((size_t)item * s + r0 + i) * ldp + q) : 1.f;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    s_pt[q * kCgPStride + i] = hi;
+    s_pt[(RN + q) * kCgPStride + i] = __float2bfloat16_rn(v - __bfloat162float(hi));
   }
   asm volatile("bar.sync 1, 256;" ::: "memory");
   if (threadIdx.x == 0) cg_stamp(1);
-  float acc[4][R];
+  float acc[NT][4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int q = 0; q < R; ++q) acc[j][q] = 0.f;
-  const int atom = lane >> 4, chunk = (lane & 15) >> 1, half = lane & 1;  // columns 4*lane .. 4*lane+3
+  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+  const int g = lane >> 2, t4 = lane & 3;
+  // ldmatrix.trans: lane L addresses row (L & 7) of matrix L >> 3; matrices (rows k0.., cols 16w..),
+  // (k0.., 16w+8..), (k0+8.., 16w..), (k0+8.., 16w+8..) = the A fragment a0..a3 of m16 x k16
+  const int mi = lane >> 3, ri = lane & 7;
+  const int ld_row = ri + ((mi >> 1) << 3);
+  const int ld_chunk = 2 * (warp & 3) + (mi & 1);
+  const uint32_t sm_base = smem_u32(sm) + (warp >> 2) * (kCgTile / 2);
+  const uint32_t pt_base = smem_u32(s_pt) + (g * kCgPStride + 2 * t4) * 2;
   for (int t = 0; t < n_tiles; ++t) {
     const int st = t % kCgSt;
     mbar_wait(full + st, (t / kCgSt) & 1);
     if (threadIdx.x == 0 && t == 0) cg_stamp(2);
-    const uint8_t* tile = sm + st * kCgTile + atom * (kCgTile / 2);
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      const int row = warp * 4 + rr;  // rows past nrows: P is zero (X finite: next item / zero fill)
-      const uint2 xv = *reinterpret_cast<const uint2*>(tile + row * 128 + ((chunk ^ (row & 7)) << 4) + half * 8);
-      const float* pp = s_p + (t * 32 + row) * 8;
-      const float xf[4] = {bf16_bits_to_float(xv.x & 0xffff), bf16_bits_to_float(xv.x >> 16),
-                           bf16_bits_to_float(xv.y & 0xffff), bf16_bits_to_float(xv.y >> 16)};
+    for (int k0 = 0; k0 < 32; k0 += 16) {
+      const int row = k0 + ld_row;
+      uint32_t a[4];
+      ldsm_x4_trans(sm_base + st * kCgTile + row * 128 + ((ld_chunk ^ (row & 7)) << 4), a);
+      const int kk = t * 32 + k0;
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const float pq = pp[q];
+      for (int n = 0; n < NT; ++n) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j][q] = fmaf(pq, xf[j], acc[j][q]);
+        for (int hl = 0; hl < 2; ++hl) {
+          const uint32_t pb = pt_base + ((hl * RN + 8 * n) * kCgPStride + kk) * 2;
+          uint32_t b0, b1;
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b0) : "r"(pb));
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b1) : "r"(pb + 16));
+          mma16816_rp(acc[n], a, b0, b1);
+        }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
   }
-  // every tile consumed (each consumer waited all full barriers) -> the ring is free for the reduction
   if (threadIdx.x == 0) cg_stamp(3);
-  asm volatile("bar.sync 1, 256;" ::: "memory");
-  float* s_red = reinterpret_cast<float*>(sm);  // [8 warps][R][kCgCols + 4]
-  constexpr int kRs = kCgCols + 4;
+  // D[m = column][n = q]: d0 (col g, q 2t), d1 (g, 2t+1), d2 (g+8, 2t), d3 (g+8, 2t+1)
+  float* out = ws + ((size_t)item * n_splits + split) * r * (size_t)ncols;
+  const int c = blockIdx.x * kCgCols + warp * 16 + g;
 #pragma unroll
-  for (int q = 0; q < R; ++q)
-    *reinterpret_cast<float4*>(s_red + (warp * R + q) * kRs + lane * 4) = make_float4(acc[0][q], acc[1][q], acc[2][q], acc[3][q]);
-  asm volatile("bar.sync 1, 256;" ::: "memory");
-  float* out = ws + (((size_t)item * n_splits + split) * R) * ncols;
-  for (int e = threadIdx.x; e < R * kCgCols; e += 256) {
-    const int q = e / kCgCols, cc = e % kCgCols, c = blockIdx.x * kCgCols + cc;
-    if (q >= r || c >= ncols) continue;
-    float v = 0.f;
-#pragma unroll
-    for (int w2 = 0; w2 < 8; ++w2) v += s_red[(w2 * R + q) * kRs + cc];
-    out[(size_t)q * ncols + c] = v;
+  for (int n = 0; n < NT; ++n) {
+    const int q = 8 * n + 2 * t4;
+    if (q < r) {
+      if (c < ncols) out[(size_t)q * ncols + c] = acc[n][0];
+      if (c + 8 < ncols) out[(size_t)q * ncols + c + 8] = acc[n][2];
+    }
+    if (q + 1 < r) {
+      if (c < ncols) out[(size_t)(q + 1) * ncols + c] = acc[n][1];
+      if (c + 8 < ncols) out[(size_t)(q + 1) * ncols + c + 8] = acc[n][3];
+    }
   }
   if (threadIdx.x == 0) cg_stamp(4);
 }
 
 // G(q, c_orig) = scale * sum_items sum_splits partial[item][split][q][pos_item(c_orig)]
-template <int R>
 __global__ void colgrad_final_kernel(const float* __restrict__ ws, int n_items, int n_splits, int ncols, int r,
                                      const int32_t* __restrict__ pos, int blk, float scale, float* __restrict__ g,
                                      long long g_sq, long long g_sc) {
@@ -398,7 +417,7 @@ __global__ void colgrad_final_kernel(const float* __restrict__ ws, int n_items, 
 #pragma unroll
         for (int t = 0; t < 4; ++t)
           vals[u][t] = (pcs[u] >= 0 && sp0 + t < n_splits)
-                           ? __ldg(ws + (((size_t)(b0 + u) * n_splits + sp0 + t) * R + q) * ncols + pcs[u])
+                           ? __ldg(ws + (((size_t)(b0 + u) * n_splits + sp0 + t) * r + q) * ncols + pcs[u])
                            : 0.f;
 #pragma unroll
       for (int u = 0; u < 8; ++u)
@@ -409,7 +428,7 @@ __global__ void colgrad_final_kernel(const float* __restrict__ ws, int n_items, 
   g[(long long)q * g_sq + (long long)c * g_sc] = acc * scale;
 }
 
-template <int R>
+template <int RN>
 static int colgrad_impl(const float* p, int ldp, const uint16_t* x, int ldx, int n_items, int s, int ncols, int r,
                         float scale, const int32_t* counts, const int32_t* pos, int blk, float* g, long long g_sq,
                         long long g_sc, float* ws, cudaStream_t stream) {
@@ -417,20 +436,19 @@ static int colgrad_impl(const float* p, int ldp, const uint16_t* x, int ldx, int
   const int items = counts ? n_items : 1, rows = counts ? s : n_items * s;
   const int splits = (rows + kCgRows - 1) / kCgRows;
   dim3 g1((ncols + kCgCols - 1) / kCgCols, splits, items);
-  static_assert(8 * 8 * (kCgCols + 4) * 4 <= kCgSt * kCgTile, "reduction must fit in the ring");
-  constexpr int smem = CgSmem::kTotal;
-  static cudaError_t attr = cudaFuncSetAttribute(colgrad_partial_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  constexpr int smem = CgSmem<RN>::kTotal;
+  static cudaError_t attr = cudaFuncSetAttribute(colgrad_partial_kernel<RN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   LX_CHECK_CUDA(attr);
   // X as [n_items*s, ldx]: boxes of 64 columns x 32 rows (columns past ncols / the item's width are
   // never combined; rows past an item's split are weighted by P = 0)
   CUtensorMap tm;
   int rc0 = make_tmap_bf16_2d(&tm, x, (uint64_t)ldx, (uint64_t)n_items * s, (uint64_t)ldx, 64, 32);
   if (rc0) return rc0;
-  colgrad_partial_kernel<R><<<g1, 288, smem, stream>>>(tm, p, ldp, rows, ncols, r, counts, counts ? blk : 1, ws);
+  colgrad_partial_kernel<RN><<<g1, 288, smem, stream>>>(tm, p, ldp, rows, ncols, r, counts, counts ? blk : 1, ws);
   int rc = launch_check("colgrad_partial");
   if (rc) return rc;
   dim3 g2((ncols + 255) / 256, r);
-  colgrad_final_kernel<R><<<g2, 256, 0, stream>>>(ws, items, splits, ncols, r, counts ? pos : nullptr,
+  colgrad_final_kernel<<<g2, 256, 0, stream>>>(ws, items, splits, ncols, r, counts ? pos : nullptr,
                                                   counts ? blk : 1, scale, g, g_sq, g_sc);
   return launch_check("colgrad_final");
 }
@@ -498,20 +516,18 @@ int lx_debug_set_colgrad_trace(unsigned long long* buf) {
 long long lx_colgrad_ws_floats(int n_items, int s, int ncols, int r) {
   // bound for both layouts: per item (gathered) or one item of n_items * s rows (shared columns)
   long long splits = (s + kCgRows - 1) / kCgRows;
-  int rr = r <= 1 ? 1 : 8;
-  return (long long)n_items * splits * rr * ncols;
+  return (long long)n_items * splits * r * ncols;
 }
 
 int lx_colgrad(const float* p, int ldp, const uint16_t* x, int ldx, int n_items, int s, int ncols, int r, float scale,
                const int32_t* counts, const int32_t* pos, int blk, float* g, long long g_sq, long long g_sc, float* ws,
                lx_stream_t stream) {
-  LX_REQUIRE(r >= 1 && r <= 8, LX_ERR_UNSUPPORTED, "colgrad: rank %d outside [1, 8]", r);
-  LX_REQUIRE(!p || (ldp >= 8 && ldp % 4 == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0), LX_ERR_SHAPE,
-             "colgrad: P rows must be 16B-aligned and padded to 8 floats (ldp >= 8, ldp %% 4 == 0)");
+  LX_REQUIRE(r >= 1 && r <= 16, LX_ERR_UNSUPPORTED, "colgrad: rank %d outside [1, 16]", r);
+  LX_REQUIRE(!p || ldp >= r, LX_ERR_SHAPE, "colgrad: ldp < r");
   LX_REQUIRE(ncols % 4 == 0, LX_ERR_SHAPE, "colgrad: ncols must be a multiple of 4");
   LX_REQUIRE(!counts || (pos && ncols % blk == 0), LX_ERR_MASK, "colgrad: gathered columns need pos and ncols %% blk == 0");
   LX_REQUIRE(ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0, LX_ERR_SHAPE, "colgrad: 16B-aligned rows required");
-  if (r == 1) return colgrad_impl<1>(p, ldp, x, ldx, n_items, s, ncols, r, scale, counts, pos, blk, g, g_sq, g_sc, ws, stream);
+  if (r > 8) return colgrad_impl<16>(p, ldp, x, ldx, n_items, s, ncols, r, scale, counts, pos, blk, g, g_sq, g_sc, ws, stream);
   return colgrad_impl<8>(p, ldp, x, ldx, n_items, s, ncols, r, scale, counts, pos, blk, g, g_sq, g_sc, ws, stream);
 }
 

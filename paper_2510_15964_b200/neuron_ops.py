@@ -263,21 +263,15 @@ def colgrad(p: torch.Tensor | None, x2: torch.Tensor, n_items: int, s: int, ncol
             out: torch.Tensor, g_sq: int, g_sc: int, masks: NeuronMasks | None = None, blk: int = 1) -> torch.Tensor:
     """out(q, c) = scale * sum_rows P[row, q] X[row, c] (c original column), deterministic.
     P may be a column slice (row stride p.stride(0)); X may be a column slice (row stride x2.stride(0))."""
-    if p is not None:
-        # the kernel reads P rows as 8 floats (16B-aligned, row stride >= 8, multiple of 4) and up to 8 ranks
-        # per call: pad / chunk otherwise
-        rp = 8 * ((r + 7) // 8)
-        if not (p.stride(0) >= rp and p.stride(0) % 4 == 0 and p.stride(1) == 1 and p.data_ptr() % 16 == 0):
-            pp = torch.zeros(p.shape[0], rp, dtype=torch.float32, device=p.device)
-            pp[:, :r] = p
-            p = pp
-        if r > 8:
-            for q0 in range(0, r, 8):
-                colgrad(p[:, q0:], x2, n_items, s, ncols, min(8, r - q0), scale,
-                        out.view(-1)[q0 * g_sq:] if g_sq else out, g_sq, g_sc, masks, blk)
-            return out
+    if p is not None and p.stride(1) != 1:
+        p = p.contiguous()
+    if p is not None and r > 16:  # the kernel takes up to 16 ranks per call
+        for q0 in range(0, r, 16):
+            colgrad(p[:, q0:], x2, n_items, s, ncols, min(16, r - q0), scale,
+                    out.view(-1)[q0 * g_sq:] if g_sq else out, g_sq, g_sc, masks, blk)
+        return out
     ws = torch.empty(int(_abi.lib().lx_colgrad_ws_floats(n_items, s, ncols, r)), dtype=torch.float32, device=x2.device)
-    _abi.call("lx_colgrad", _abi.ptr(p), p.stride(0) if p is not None else 8, x2.data_ptr(), x2.stride(0), n_items, s,
+    _abi.call("lx_colgrad", _abi.ptr(p), p.stride(0) if p is not None else 1, x2.data_ptr(), x2.stride(0), n_items, s,
               ncols, r, float(scale),
               _abi.ptr(masks.counts if masks else None), _abi.ptr(masks.pos if masks else None), blk, out.data_ptr(),
               g_sq, g_sc, ws.data_ptr(), _abi.stream_handle(x2.device))

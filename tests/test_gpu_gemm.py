@@ -142,7 +142,7 @@ def test_neuron_mlp_gemms(n_items, s, d, d_ff, blk, density, r, packed, engine):
 
 
 @pytest.mark.parametrize("gather", [False, True])
-@pytest.mark.parametrize("r,w_layout", [(8, "kr"), (8, "rk"), (16, "kr"), (4, "rk"), (1, "kr")])
+@pytest.mark.parametrize("r,w_layout", [(8, "kr"), (8, "rk"), (16, "kr"), (12, "rk"), (4, "rk"), (1, "kr")])
 def test_lora_skinny_kernels(gather, r, w_layout):
     """rowproj / colgrad (csrc/lora.cu) vs torch fp32 on the same bf16 operands, incl. per-item gathers."""
     from paper_2510_15964_b200 import neuron_ops as N
