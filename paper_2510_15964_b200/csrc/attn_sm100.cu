@@ -85,61 +85,83 @@ LX_DEV uint64_t desc_mnmajor(uint32_t base, int kk) {  // K = rows step kk (16 r
 __host__ __device__ constexpr int tmem_cols_pow2(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
 // ============================================================================ forward
-// One CTA per (128-query tile, head, item); 2 CTAs per SM at hd=64 (TMEM 256 columns: S/P [0,128),
-// O [128, 128+hd); smem Q + a 2-stage K/V ring = 80 KB), so one CTA's softmax overlaps the other's
-// MMAs, loads and epilogue. Per CSR entry e (key tile j):
-//   MMA:     S = Q K_j^T -> TMEM S region                          (commit s_full)
-//   softmax: mask, online max, rescale O in TMEM when the max moved, P = 2^(S*c - m) as bf16
-//            into the S region's first 64 columns (tcgen05.st)     (arrive p_full)
-//   MMA:     O += P V_j with P read from TMEM (TS form), then S_{e+1} (in issue order, so it may
-//            overwrite P)                                          (commit kv_empty)
+// Persistent: grid = min(#units, kCtas x #SMs); CTA c walks units u = c, c + G, ... with
+// u = (item * H + h) * nqt + qt, so the CTAs resident at a time cover consecutive (item, head)s
+// and share their K/V tiles in L2. TMEM per CTA: S [0,128) | P [128,192) (bf16 pairs) | O.
+// Q is double-buffered across units and K/V stream through a 2-stage ring indexed by a running
+// entry counter g, so the next unit's Q and first K/V load under the current unit's tail.
+// Per entry g (key tile j of the unit's CSR list):
+//   MMA      S(g) = Q K_j^T as soon as the softmax has pulled S(g-1) into registers (s_free),
+//            then O += P(g-1) V_{j'} once P(g-1) is in TMEM (p_full)
+//   softmax  S(g) -> registers, release S; row max; lazy rescale (the running max only moves
+//            when it grows by > 2^8, FA4-style, so O is rarely touched); P(g) = 2^(S c - m) as bf16
+//            into the P region after PV(g-1) completed (pv_done)
+// so S(g+1) runs on the tensor core while the softmax of g runs. A unit's epilogue reads O
+// after its last PV and releases it (o_free) before the next unit's first PV overwrites it.
 template <int HD>
 struct AttnFwdSmem {
   static constexpr int kAtoms = HD / 64;
   static constexpr int kT = kAtoms * kAT * 128;  // one 128 x HD tile
-  static constexpr int kOffK = kT;
-  static constexpr int kOffV = kOffK + 2 * kT;
-  static constexpr int kOffBar = kOffV + 2 * kT;
-  static constexpr int kTotal = kOffBar + 128 + 1024;
+  static constexpr int kOffQ = 0;                // Q[2]
+  static constexpr int kOffK = 2 * kT;           // K[2]
+  static constexpr int kOffV = 4 * kT;           // V[2]
+  static constexpr int kOffRed = 6 * kT;        // softmax pair exchange [2][2][128] max + [2][128] sum
+  static constexpr int kOffBar = kOffRed + 768 * 4;
+  static constexpr int kTotal = kOffBar + 256 + 1024;
   static constexpr int kCtas = HD == 64 ? 2 : 1;
-  static constexpr int kTmem = tmem_cols_pow2(kAT + HD);
+  static constexpr int kTmem = tmem_cols_pow2(kAT + 64 + HD);
+  static constexpr int kThreads = 320;  // TMA warp, MMA warp, 8 softmax warps
 };
 
+LX_DEV void decode_unit(int u, int nqt, int H, int& qt, int& h, int& item) {
+  qt = u % nqt;
+  const int r = u / nqt;
+  h = r % H;
+  item = r / H;
+}
+
 template <int HD>
-__global__ void __launch_bounds__(192, AttnFwdSmem<HD>::kCtas)
+__global__ void __launch_bounds__(AttnFwdSmem<HD>::kThreads, AttnFwdSmem<HD>::kCtas)
 bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, int d_model,
                      const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
-                     float scale_log2, __nv_bfloat16* __restrict__ o, int ldo, float* __restrict__ lse) {
+                     float scale_log2, __nv_bfloat16* __restrict__ o, int ldo, float* __restrict__ lse, int n_units) {
   using L = AttnFwdSmem<HD>;
   constexpr int A = L::kAtoms;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
-  uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_full = bars + 6;
-  uint64_t* o_done = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* q_full = bars + 0;    // [2]
+  uint64_t* q_empty = bars + 2;   // [2]
+  uint64_t* k_full = bars + 4;    // [2]  K and V have separate barriers: K(g)'s stage is refilled as
+  uint64_t* k_empty = bars + 6;   // [2]  soon as S(g) completes, V(g)'s once PV(g) completes
+  uint64_t* v_full = bars + 8;    // [2]
+  uint64_t* v_empty = bars + 10;  // [2]
+  uint64_t* s_full = bars + 12;
+  uint64_t* s_free = bars + 13;
+  uint64_t* p_full = bars + 14;
+  uint64_t* pv_done = bars + 15;
+  uint64_t* o_free = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
-  const int qt = blockIdx.x, h = blockIdx.y, item = blockIdx.z;
   const uint32_t warp = warp_id(), lane = lane_id();
-  const Tab128 tv = tab128(tables, __ldg(pidx + item * item_stride + h));
-  const int e0 = __ldg(tv.row_ptr + qt), n = __ldg(tv.row_ptr + qt + 1) - e0;
-  const int row_base = item * s;
+  const int nqt = (s + kAT - 1) / kAT;
 
   if (warp == 0 && lane == 0) {
     trace_stamp(0);
     tma_prefetch_desc(&tm_qkv);
-    mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(kv_full + i, 1);
-      mbar_init(kv_empty + i, 1);
+      mbar_init(q_full + i, 1);
+      mbar_init(q_empty + i, 1);
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
-    mbar_init(o_done, 1);
+    mbar_init(s_free, 8);
+    mbar_init(p_full, 8);
+    mbar_init(pv_done, 1);
+    mbar_init(o_free, 8);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<L::kTmem>(tmem_slot);
@@ -147,146 +169,222 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s = tmem, t_o = tmem + kAT;
+  const uint32_t t_s = tmem, t_p = tmem + kAT, t_o = tmem + kAT + 64;
 
   if (warp == 0) {
     if (lane == 0) {
-      const int qcol = h * HD, kcol = d_model + h * HD, vcol = 2 * d_model + h * HD;
-      mbar_arrive_expect_tx(q_full, L::kT);
-      for (int a = 0; a < A; ++a) tma_load_2d(sm + a * kAT * 128, &tm_qkv, q_full, qcol + a * 64, row_base + qt * kAT);
-      for (int e = 0; e < n; ++e) {
-        const int st = e & 1;
-        mbar_wait(kv_empty + st, ((e >> 1) & 1) ^ 1);
-        const int j = __ldg(tv.csr_col + e0 + e);
-        mbar_arrive_expect_tx(kv_full + st, 2 * L::kT);
-        uint8_t* sk = sm + L::kOffK + st * L::kT;
-        uint8_t* sv = sm + L::kOffV + st * L::kT;
-        for (int a = 0; a < A; ++a) {
-          tma_load_2d(sk + a * kAT * 128, &tm_qkv, kv_full + st, kcol + a * 64, row_base + j * kAT);
-          tma_load_2d(sv + a * kAT * 128, &tm_qkv, kv_full + st, vcol + a * 64, row_base + j * kAT);
+      int g = 0, ul = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int qt, h, item;
+        decode_unit(u, nqt, H, qt, h, item);
+        const Tab128 tv = tab128(tables, __ldg(pidx + item * item_stride + h));
+        const int e0 = __ldg(tv.row_ptr + qt), n = __ldg(tv.row_ptr + qt + 1) - e0;
+        if (n == 0) continue;
+        const int row_base = item * s;
+        const int qcol = h * HD, kcol = d_model + h * HD, vcol = 2 * d_model + h * HD;
+        const int qb = ul & 1;
+        mbar_wait(q_empty + qb, ((ul >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full + qb, L::kT);
+        for (int a = 0; a < A; ++a)
+          tma_load_2d(sm + L::kOffQ + qb * L::kT + a * kAT * 128, &tm_qkv, q_full + qb, qcol + a * 64, row_base + qt * kAT);
+        for (int e = 0; e < n; ++e, ++g) {
+          const int st = g & 1;
+          const int j = __ldg(tv.csr_col + e0 + e);
+          uint8_t* sk = sm + L::kOffK + st * L::kT;
+          uint8_t* sv = sm + L::kOffV + st * L::kT;
+          mbar_wait(k_empty + st, ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(k_full + st, L::kT);
+          for (int a = 0; a < A; ++a) tma_load_2d(sk + a * kAT * 128, &tm_qkv, k_full + st, kcol + a * 64, row_base + j * kAT);
+          mbar_wait(v_empty + st, ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(v_full + st, L::kT);
+          for (int a = 0; a < A; ++a) tma_load_2d(sv + a * kAT * 128, &tm_qkv, v_full + st, vcol + a * 64, row_base + j * kAT);
         }
+        ++ul;
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc_s = make_idesc_bf16(kAT, kAT, false, false);  // S = Q K^T
       const uint32_t idesc_o = make_idesc_bf16(kAT, HD, false, true);    // O += P V (V MN-major)
-      const uint32_t sq = smem_u32(sm);
-      trace_stamp(1);
-      mbar_wait(q_full, 0);
-      trace_stamp(2);
-      auto issue_pv = [&](int e) {
-        const int st = e & 1;
-        mbar_wait(p_full, e & 1);
+      // deferred PV of the previous entry: (entry index, kv stage, first entry of its unit, unit ordinal)
+      int pv_g = -1, pv_st = 0, pv_first = 0, pv_ul = 0;
+      auto issue_pv = [&]() {
+        if (pv_first && pv_ul >= 1) mbar_wait(o_free, (pv_ul - 1) & 1);  // previous unit's O read out
+        mbar_wait(v_full + pv_st, (pv_g >> 1) & 1);
+        mbar_wait(p_full, pv_g & 1);
         tc_fence_after();
-        const uint32_t sv = smem_u32(sm + L::kOffV + st * L::kT);
-        for (int kk = 0; kk < kAT / 16; ++kk) mma_bf16_ts(t_o, t_s + kk * 8, desc_mnmajor(sv, kk), idesc_o, (e | kk) != 0);
-        mma_commit(kv_empty + st);
+        const uint32_t sv = smem_u32(sm + L::kOffV + pv_st * L::kT);
+        for (int kk = 0; kk < kAT / 16; ++kk)
+          mma_bf16_ts(t_o, t_p + kk * 8, desc_mnmajor(sv, kk), idesc_o, !(pv_first && kk == 0));
+        mma_commit(pv_done);
+        mma_commit(v_empty + pv_st);
       };
-      for (int e = 0; e < n; ++e) {
-        const int st = e & 1;
-        mbar_wait(kv_full + st, (e >> 1) & 1);
-        if (e < 4) trace_stamp(4 + e);
-        if (e >= 1) issue_pv(e - 1);
-        tc_fence_after();
-        const uint32_t sk = smem_u32(sm + L::kOffK + st * L::kT);
-        for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_s, desc_kmajor(sq, kk), desc_kmajor(sk, kk), idesc_s, kk != 0);
-        mma_commit(s_full);
+      int g = 0, ul = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int qt, h, item;
+        decode_unit(u, nqt, H, qt, h, item);
+        const Tab128 tv = tab128(tables, __ldg(pidx + item * item_stride + h));
+        const int n = __ldg(tv.row_ptr + qt + 1) - __ldg(tv.row_ptr + qt);
+        if (n == 0) continue;
+        const int qb = ul & 1;
+        const uint32_t sq = smem_u32(sm + L::kOffQ + qb * L::kT);
+        mbar_wait(q_full + qb, (ul >> 1) & 1);
+        for (int e = 0; e < n; ++e, ++g) {
+          const int st = g & 1;
+          mbar_wait(k_full + st, (g >> 1) & 1);
+          if (g >= 1) mbar_wait(s_free, (g - 1) & 1);  // S(g-1) is in the softmax registers
+          tc_fence_after();
+          const uint32_t sk = smem_u32(sm + L::kOffK + st * L::kT);
+          for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_s, desc_kmajor(sq, kk), desc_kmajor(sk, kk), idesc_s, kk != 0);
+          mma_commit(s_full);
+          mma_commit(k_empty + st);
+          if (e == n - 1) mma_commit(q_empty + qb);
+          if (pv_g >= 0) issue_pv();
+          pv_g = g;
+          pv_st = st;
+          pv_first = e == 0;
+          pv_ul = ul;
+        }
+        ++ul;
       }
-      if (n >= 1) issue_pv(n - 1);
-      mma_commit(o_done);
+      if (pv_g >= 0) issue_pv();
     }
   } else {
-    const int quad = warp & 3;
+    // 8 softmax warps: warp w owns TMEM lanes 32*(w%4).. (query rows) and S columns [64*half, +64),
+    // half = (w-2)/4; the two warps of a row exchange their partial row max through shared memory
+    // (pair barrier 1 + quad) so both apply the same max; row sums stay partial until the epilogue.
+    const int quad = warp & 3, half = (warp - 2) >> 2;
     const int r = quad * 32 + lane;  // query row within the tile
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    float m = -INFINITY, l = 0.f;
-    for (int e = 0; e < n; ++e) {
-      const uint32_t lo = (uint32_t)__ldg(tv.csr_lo + e0 + e), hi = (uint32_t)__ldg(tv.csr_hi + e0 + e);
-      const uint32_t mrow = (uint32_t)((((uint64_t)hi << 32) | lo) >> ((r >> 4) * 8)) & 0xffu;  // 16-key groups
-      mbar_wait(s_full, e & 1);
-      if (r == 0 && e < 4) trace_stamp(8 + e);
+    float* red = reinterpret_cast<float*>(sm + L::kOffRed);  // [2 parity][2 half][128]
+    const uint32_t bar_id = 1 + quad;
+    int g = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int qt, h, item;
+      decode_unit(u, nqt, H, qt, h, item);
+      const Tab128 tv = tab128(tables, __ldg(pidx + item * item_stride + h));
+      const int e0 = __ldg(tv.row_ptr + qt), n = __ldg(tv.row_ptr + qt + 1) - e0;
+      const int row = qt * kAT + r;
+      const int row_base = item * s;
+      float m = -INFINITY, l = 0.f;  // running max (log2 domain, scaled) and this half's row sum
+      for (int e = 0; e < n; ++e, ++g) {
+        const uint32_t lo = (uint32_t)__ldg(tv.csr_lo + e0 + e), hi = (uint32_t)__ldg(tv.csr_hi + e0 + e);
+        // 16-key groups 4*half .. 4*half+3 of this row's 16-row group
+        const uint32_t mrow = (uint32_t)((((uint64_t)hi << 32) | lo) >> ((r >> 4) * 8 + 4 * half)) & 0xfu;
+        const bool full = __all_sync(0xffffffffu, mrow == 0xfu);
+        mbar_wait(s_full, g & 1);
+        tc_fence_after();
+        uint32_t sv[2][32];
+        tmem_ld_32x32b_x32(t_s + lane_base + half * 64, sv[0]);
+        tmem_ld_32x32b_x32(t_s + lane_base + half * 64 + 32, sv[1]);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);
+        float mx = -INFINITY;
+        if (full) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(sv[c][i]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if ((mrow >> (c * 2 + (i >> 4))) & 1u) mx = fmaxf(mx, __uint_as_float(sv[c][i]));
+        }
+        float* rp = red + (g & 1) * 256;
+        rp[half * 128 + r] = mx;
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        mx = fmaxf(mx, rp[(half ^ 1) * 128 + r]);
+        const float mxs = mx * scale_log2;
+        const float m_new = mxs > m + 8.f ? mxs : m;  // lazy: keep the stale max while P <= 2^8
+        const float alpha = m_new == m ? 1.f : ex2(m - m_new);
+        const float use = m_new == -INFINITY ? 0.f : m_new;
+        m = m_new;
+        // P region free and O stable: PV(g-1) completed (by now, usually)
+        if (g >= 1) mbar_wait(pv_done, (g - 1) & 1);
+        tc_fence_after();
+        float rs = 0.f;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float p0 = ex2(fmaf(__uint_as_float(sv[c][2 * i]), scale_log2, -use));
+            float p1 = ex2(fmaf(__uint_as_float(sv[c][2 * i + 1]), scale_log2, -use));
+            if (!full && !((mrow >> (c * 2 + (i >> 3))) & 1u)) p0 = p1 = 0.f;
+            rs += p0 + p1;
+            pk[i] = pack_bf16x2(p0, p1);
+          }
+          tmem_st_32x32b_x16(t_p + lane_base + half * 32 + c * 16, pk);
+        }
+        // O rescale (this warp's half of the O columns), rare with the lazy max
+        if (e >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < HD / 64; ++c) {
+            uint32_t ov[32];
+            const uint32_t ta = t_o + lane_base + half * (HD / 2) + c * 32;
+            tmem_ld_32x32b_x32(ta, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            tmem_st_32x32b_x32(ta, ov);
+          }
+        }
+        l = l * alpha + rs;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+      }
+      if (n == 0) {  // no key tile for this query tile: zero output (never for pool patterns)
+        if (row < s) {
+          __nv_bfloat16* op = o + ((size_t)row_base + row) * ldo + h * HD + half * (HD / 2);
+          for (int c = 0; c < HD / 2; c += 8) *reinterpret_cast<uint4*>(op + c) = make_uint4(0u, 0u, 0u, 0u);
+          if (half == 0) lse[((size_t)item * H + h) * s + row] = -INFINITY;
+        }
+        continue;
+      }
+      mbar_wait(pv_done, (g - 1) & 1);  // the unit's last PV
       tc_fence_after();
-      // the whole S row in registers (one wait), row max over the active keys
-      uint32_t sv[4][32];
+      uint32_t ov[HD / 64][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + lane_base + c * 32, sv[c]);
+      for (int c = 0; c < HD / 64; ++c) tmem_ld_32x32b_x32(t_o + lane_base + half * (HD / 2) + c * 32, ov[c]);
       tmem_ld_wait();
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if ((mrow >> (c * 2 + (i >> 4))) & 1u) mx = fmaxf(mx, __uint_as_float(sv[c][i]));
-      const float m_new = fmaxf(m, mx * scale_log2);
-      const float use = m_new == -INFINITY ? 0.f : m_new;
-      const float alpha = ex2(m - use);
-      m = m_new;
-      // P = 2^(S*c - m) (bf16 pairs) into S columns [0, 64): chunk c -> [16c, 16c+16)
-      float rs = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const bool on = (mrow >> (c * 2 + (i >> 3))) & 1u;
-          const float p0 = on ? ex2(fmaf(__uint_as_float(sv[c][2 * i]), scale_log2, -use)) : 0.f;
-          const float p1 = on ? ex2(fmaf(__uint_as_float(sv[c][2 * i + 1]), scale_log2, -use)) : 0.f;
-          rs += p0 + p1;
-          pk[i] = pack_bf16x2(p0, p1);
-        }
-        tmem_st_32x32b_x16(t_s + lane_base + c * 16, pk);
-      }
-      // O is stable: s_full(e) was committed after O += P_{e-1} V_{e-1}
-      if (e >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
-          uint32_t ov[32];
-          tmem_ld_32x32b_x32(t_o + lane_base + c * 32, ov);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-          tmem_st_32x32b_x32(t_o + lane_base + c * 32, ov);
-        }
-      }
-      l = l * alpha + rs;
-      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
-      if (r == 0 && e < 4) trace_stamp(12 + e);
-    }
-    mbar_wait(o_done, 0);
-    if (r == 0) trace_stamp(16);
-    tc_fence_after();
-    const int row = qt * kAT + r;
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t ov[32];
-      tmem_ld_32x32b_x32(t_o + lane_base + c * 32, ov);
-      tmem_ld_wait();
+      if (lane == 0) mbar_arrive(o_free);
+      // total row sum = both halves' partial sums (same max, same alpha history)
+      float* rl = red + 512;
+      rl[half * 128 + r] = l;
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      l += rl[(half ^ 1) * 128 + r];
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // rl reusable by the next unit
+      const float inv = l > 0.f ? 1.f / l : 0.f;
       if (row < s) {
-        __nv_bfloat16* op = o + ((size_t)row_base + row) * ldo + h * HD + c * 32;
+        __nv_bfloat16* op = o + ((size_t)row_base + row) * ldo + h * HD + half * (HD / 2);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float f[8];
+        for (int c = 0; c < HD / 64; ++c) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) f[k] = n > 0 ? __uint_as_float(ov[8 * i + k]) * inv : 0.f;
-          *reinterpret_cast<uint4*>(op + 8 * i) = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
-                                                             pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+          for (int i = 0; i < 4; ++i) {
+            float f[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) f[k] = __uint_as_float(ov[c][8 * i + k]) * inv;
+            *reinterpret_cast<uint4*>(op + c * 32 + 8 * i) = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                                                                        pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+          }
         }
+        if (half == 0) lse[((size_t)item * H + h) * s + row] = (m + __log2f(l)) * 0.6931471805599453f;
       }
     }
-    if (row < s) lse[((size_t)item * H + h) * s + row] = (m + __log2f(l)) * 0.6931471805599453f;
-    if (r == 0) trace_stamp(17);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<L::kTmem>(tmem);
-    if (lane == 0) trace_stamp(18);
   }
 }
 
@@ -299,9 +397,11 @@ static int launch_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H,
   constexpr int smem = AttnFwdSmem<HD>::kTotal;
   static cudaError_t attr = cudaFuncSetAttribute(bsattn_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   LX_CHECK_CUDA(attr);
-  dim3 grid((s + kAT - 1) / kAT, H, n_items);
-  bsattn_fwd_tc_kernel<HD><<<grid, 192, smem, st>>>(tm, s, H, ld / 3, pidx, item_stride, tables128, scale * 1.4426950408889634f,
-                                                    reinterpret_cast<__nv_bfloat16*>(o), ldo, lse);
+  const int n_units = ((s + kAT - 1) / kAT) * H * n_items;
+  const int grid = n_units < AttnFwdSmem<HD>::kCtas * num_sms() ? n_units : AttnFwdSmem<HD>::kCtas * num_sms();
+  bsattn_fwd_tc_kernel<HD><<<grid, AttnFwdSmem<HD>::kThreads, smem, st>>>(tm, s, H, H * HD, pidx, item_stride, tables128,
+                                                    scale * 1.4426950408889634f, reinterpret_cast<__nv_bfloat16*>(o), ldo,
+                                                    lse, n_units);
   return launch_check("bsattn_fwd_tc");
 }
 
@@ -798,10 +898,10 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const u
   LX_CHECK_CUDA(a2);
   dim3 grid((s + kAT - 1) / kAT, H, n_items);
   const float sl2 = scale * 1.4426950408889634f;
-  bsattn_dkdv_tc_kernel<HD><<<grid, 192, smem, st>>>(tm_qkv, tm_do, s, H, ld / 3, pidx, item_stride, tables128, scale, sl2,
+  bsattn_dkdv_tc_kernel<HD><<<grid, 192, smem, st>>>(tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
                                                      lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld, ksum);
   if ((rc = launch_check("bsattn_dkdv_tc"))) return rc;
-  bsattn_dq_tc_kernel<HD><<<grid, 192, smem, st>>>(tm_qkv, tm_do, s, H, ld / 3, pidx, item_stride, tables128, scale, sl2,
+  bsattn_dq_tc_kernel<HD><<<grid, 192, smem, st>>>(tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
                                                    lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld, ksum);
   return launch_check("bsattn_dq_tc");
 }
@@ -822,8 +922,8 @@ int lx_debug_set_attn_trace(unsigned long long* buf) {
 int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                      int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128, float scale,
                      const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv, lx_stream_t stream) {
-  LX_REQUIRE(ld == 3 * H * hd && ld % 8 == 0 && ld_o % 8 == 0, LX_ERR_SHAPE,
-             "attention bwd (tcgen05): qkv / dqkv must be fused [M, 3*H*hd]");
+  LX_REQUIRE(ld >= 3 * H * hd && ld % 8 == 0 && ld_o % 8 == 0, LX_ERR_SHAPE,
+             "attention bwd (tcgen05): qkv / dqkv must be fused [M, >= 3*H*hd] with 16B-aligned rows");
   switch (hd) {
     case 64: return launch_bwd_tc<64>(qkv, ld, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, ksum_ws, dqkv, stream);
     case 128: return launch_bwd_tc<128>(qkv, ld, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, ksum_ws, dqkv, stream);
@@ -834,8 +934,8 @@ int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const uint1
 int lx_bsattn_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H, int hd, const int32_t* pattern_idx,
                      int item_stride, const int32_t* tables128, float scale, uint16_t* o, int ldo, float* lse,
                      lx_stream_t stream) {
-  LX_REQUIRE(ld % 8 == 0 && ldo % 8 == 0 && ld == 3 * H * hd, LX_ERR_SHAPE,
-             "attention (tcgen05): qkv must be the fused [M, 3*H*hd] projection output");
+  LX_REQUIRE(ld % 8 == 0 && ldo % 8 == 0 && ld >= 3 * H * hd, LX_ERR_SHAPE,
+             "attention (tcgen05): qkv must be the fused [M, >= 3*H*hd] projection output (16B-aligned rows)");
   LX_REQUIRE(n_items >= 1 && n_items < 65536 && H >= 1 && H < 65536, LX_ERR_SHAPE, "attention: bad grid");
   switch (hd) {
     case 64: return launch_fwd_tc<64>(qkv, ld, n_items, s, H, pattern_idx, item_stride, tables128, scale, o, ldo, lse, stream);
