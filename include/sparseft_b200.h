@@ -140,18 +140,32 @@ int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const floa
 /* Workspace for lx_rowproj's tensor-core path: W packed as bf16 hi/lo [items][2][R'][K] (gathered per item). */
 long long lx_rowproj_ws_bytes(int n_items, int K, int r, int gathered);
 
-/* Skinny LoRA gradient reduction over tokens: G[q, c_orig] = scale * sum_rows P[row, q] X[row, c]
- *   (dB1[:,cols], dA2[cols] (transposed), dB2, dA1 (transposed)); summed over items in order.
- *   P fp32 row stride ldp (r <= 16); X bf16 [M, ncols(packed)] row stride ldx; G fp32 with G(q, c) = g[q*g_sq + c*g_sc].
- *   ws: fp32 workspace of lx_colgrad_ws_floats(...) floats. Deterministic. */
-long long lx_colgrad_ws_floats(int n_items, int s, int ncols, int r);
-int lx_colgrad(const float* p, int ldp, const uint16_t* x, int ldx, int n_items, int s, int ncols, int r, float scale,
-               const int32_t* counts, const int32_t* pos, int blk, float* g, long long g_sq, long long g_sc, float* ws,
-               lx_stream_t stream);
-
-/* Column sums of a packed bf16 matrix per original column (BitFit db1[cols] = sum dz; sf/autograd.py:107-111). */
-int lx_colsum(const uint16_t* x, int ldx, int n_items, int s, int ncols, const int32_t* counts, const int32_t* pos,
-              int blk, float* out, float* ws, lx_stream_t stream);
+/* Skinny LoRA / BitFit gradient reductions over tokens, up to 8 per launch (one sublayer's backward):
+ *   G(q, c) = scale * sum_rows P[row, q] X[row, c]     c = original column
+ * replacing lora_linear_backward's xᵀ·dAx / axᵀ·dz and mlp_backward's dB2, dA2[cols], dB1[:,cols], dA1
+ * (sf/autograd.py:50-58,97-120) and BitFit's column sums (p == NULL, r = 1; sf/autograd.py:56-57,95-96,107-111).
+ *   P fp32 [n_items*s, >= r] row stride ldp (r <= 16); X bf16 row stride ldx (16B-aligned rows).
+ *   pos == NULL: X columns are the original columns [0, ncols).
+ *   pos != NULL: X holds each item's active neuron blocks packed in ascending order; pos[b][block] is the
+ *                block's packed index or -1 (NeuronMasks.pos); inactive columns of G are written 0.
+ *   G(q, c) = g[q*g_sq + c*g_sc]. Summed over items in a fixed order: deterministic.
+ *   ws: fp32 workspace of lx_colgrad_group_ws_floats floats (split partials). */
+typedef struct lx_colgrad_problem {
+  const float* p;
+  int ldp;
+  const uint16_t* x;
+  int ldx;
+  int ncols;
+  int r;
+  float scale;
+  const int32_t* pos;
+  int blk;
+  float* g;
+  long long g_sq;
+  long long g_sc;
+} lx_colgrad_problem;
+long long lx_colgrad_group_ws_floats(const lx_colgrad_problem* probs, int n_probs, int n_items, int s);
+int lx_colgrad_group(const lx_colgrad_problem* probs, int n_probs, int n_items, int s, float* ws, lx_stream_t stream);
 
 /* ------------------------------------------------------------------ K3 block-sparse attention
  * q,k,v,o: bf16 [n_items*s, ld] with head h at columns [h*hd, (h+1)*hd); non-causal; scale = 1/sqrt(hd).

@@ -38,9 +38,8 @@ SIGNATURES: dict[str, list] = {
     "lx_neuron_fc1_dgrad": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P],
     "lx_rowproj": [_P, _I, _I, _I, _I, _P, _LL, _LL, _I, _F, _P, _P, _I, _P, _I, _P, _P],
     "lx_rowproj_ws_bytes": [_I, _I, _I, _I],
-    "lx_colgrad_ws_floats": [_I, _I, _I, _I],
-    "lx_colgrad": [_P, _I, _P, _I, _I, _I, _I, _I, _F, _P, _P, _I, _P, _LL, _LL, _P, _P],
-    "lx_colsum": [_P, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P],
+    "lx_colgrad_group_ws_floats": [_P, _I, _I, _I],
+    "lx_colgrad_group": [_P, _I, _I, _I, _P, _P],
     "lx_attn_tables_size": [_I, _I, _I, _P],
     "lx_attn_tables": [_P, _P, _I, _I, _I, _P, _I],
     "lx_bsattn_fwd": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _I, _P, _P],
@@ -52,7 +51,16 @@ SIGNATURES: dict[str, list] = {
     "lx_cross_entropy": [_P, _I, _I, _P, _F, _P, _P, _P],
     "lx_layernorm_bwd": [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P],
 }
-RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_ws_floats": _LL, "lx_rowproj_ws_bytes": _LL}
+RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_group_ws_floats": _LL, "lx_rowproj_ws_bytes": _LL}
+
+
+
+class ColgradProblem(C.Structure):
+    """lx_colgrad_problem (include/sparseft_b200.h)."""
+
+    _fields_ = [("p", _P), ("ldp", _I), ("x", _P), ("ldx", _I), ("ncols", _I), ("r", _I), ("scale", _F), ("pos", _P),
+                ("blk", _I), ("g", _P), ("g_sq", _LL), ("g_sc", _LL)]
+
 
 _ERRORS = {1: E.ShapeError, 2: E.LayoutError, 3: E.MaskError, 4: E.PatternError, 5: E.CudaError, 6: E.UnsupportedError}
 

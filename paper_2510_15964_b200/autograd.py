@@ -24,7 +24,7 @@ from . import _abi
 from . import model as M
 from .block_sparse import attention_backward
 from .errors import GradientError
-from .neuron_ops import colgrad, rowproj
+from .neuron_ops import colgrad_group, colgrad_problem, rowproj
 
 
 def check_gradient_set(grads: dict, model: M.Model) -> None:
@@ -59,15 +59,32 @@ class FlatGrads(dict):
         self.views, self.scale = views, scale
 
 
-def _cg(grads: dict, name: str, shape, p, x2, n_items, s, ncols, r, scale, g_sq, g_sc, masks=None, blk=1) -> None:
-    """colgrad into the gradient `name` (in place in a FlatGrads view when possible)."""
-    if isinstance(grads, FlatGrads) and name in grads.views and name not in grads:
-        out = grads.views[name]
-        colgrad(p, x2, n_items, s, ncols, r, scale * grads.scale, out, g_sq, g_sc, masks=masks, blk=blk)
-        dict.__setitem__(grads, name, out)
-        return
-    out = torch.empty(shape, dtype=torch.float32, device=x2.device)
-    _acc(grads, name, colgrad(p, x2, n_items, s, ncols, r, scale, out, g_sq, g_sc, masks=masks, blk=blk))
+class _CgBatch:
+    """The LoRA / BitFit column reductions of one sublayer's backward, collected and run as one
+    deterministic lx_colgrad_group launch. A gradient with a view in a FlatGrads buffer is written
+    there directly (pre-scaled by the batch mean); others are accumulated after the launch."""
+
+    def __init__(self, grads: dict, n_items: int, s: int):
+        self.grads, self.n_items, self.s = grads, n_items, s
+        self.probs, self.post = [], []
+
+    def add(self, name, shape, p, x2, ncols, r, scale, g_sq, g_sc, masks=None, blk=1) -> None:
+        g = self.grads
+        if isinstance(g, FlatGrads) and name in g.views and name not in g:
+            out = g.views[name]
+            scale = scale * g.scale
+            dict.__setitem__(g, name, out)
+        else:
+            out = torch.empty(shape, dtype=torch.float32, device=x2.device)
+            self.post.append((name, out))
+        self.probs.append(colgrad_problem(p, x2, ncols, r, scale, out, g_sq, g_sc, masks=masks, blk=blk))
+
+    def flush(self) -> None:
+        if self.probs:
+            colgrad_group(self.probs, self.n_items, self.s)
+        for name, out in self.post:
+            _acc(self.grads, name, out)
+        self.probs, self.post = [], []
 
 
 def _bf16(t: torch.Tensor) -> torch.Tensor:
@@ -129,32 +146,34 @@ def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims
     dev = a.device
     dO = _bf16(d_out.reshape(-1, d)).contiguous()
     st = _abi.stream_handle(dev)
+    cg = _CgBatch(grads, B, s)
     if bitfit:
-        _cg(grads, f"{prefix}b2", (d,), None, dO, B, s, d, 1, 1.0, 0, 1)
+        cg.add(f"{prefix}b2", (d,), None, dO, d, 1, 1.0, 0, 1)
     ad1, ad2 = lora.get("w1"), lora.get("w2")
     dax2 = None
     if ad2 is not None:
         r2 = ad2.rank
         dax2 = rowproj(dO, B, s, d, ad2.b, 1, d, r2, scale=ad2.scaling)  # dO B2^T * s
-        _cg(grads, f"{prefix}w2.lora_b", (r2, d), cache["ax2"], dO, B, s, d, r2, ad2.scaling, d, 1)
+        cg.add(f"{prefix}w2.lora_b", (r2, d), cache["ax2"], dO, d, r2, ad2.scaling, d, 1)
     dz = torch.empty_like(a)
     _abi.call("lx_neuron_fc2_dgrad", dO.data_ptr(), B, s, d, f, blk, lw.mlp.w2.data_ptr(), nm.counts.data_ptr(),
               nm.ids.data_ptr(), _abi.ptr(dax2), _abi.ptr(ad2.a if ad2 else None), ad2.rank if ad2 else 0, a.data_ptr(),
               dz.data_ptr(), a.stride(0), _abi.ptr(cache.get("w2p")), st)
     if ad2 is not None:
-        _cg(grads, f"{prefix}w2.lora_a", (f, ad2.rank), dax2, a, B, s, f, ad2.rank, 1.0, 1, ad2.rank, masks=nm, blk=blk)
+        cg.add(f"{prefix}w2.lora_a", (f, ad2.rank), dax2, a, f, ad2.rank, 1.0, 1, ad2.rank, masks=nm, blk=blk)
     if bitfit:
-        _cg(grads, f"{prefix}b1", (f,), None, dz, B, s, f, 1, 1.0, 0, 1, masks=nm, blk=blk)
+        cg.add(f"{prefix}b1", (f,), None, dz, f, 1, 1.0, 0, 1, masks=nm, blk=blk)
     dax1 = None
     if ad1 is not None:
         r1 = ad1.rank
-        _cg(grads, f"{prefix}w1.lora_b", (r1, f), cache["ax1"], dz, B, s, f, r1, ad1.scaling, f, 1, masks=nm, blk=blk)
+        cg.add(f"{prefix}w1.lora_b", (r1, f), cache["ax1"], dz, f, r1, ad1.scaling, f, 1, masks=nm, blk=blk)
         dax1 = rowproj(dz, B, s, f, ad1.b, 1, f, r1, scale=ad1.scaling, masks=nm, blk=blk)  # dz B1[:,cols]^T * s
-        _cg(grads, f"{prefix}w1.lora_a", (d, r1), dax1, x2, B, s, d, r1, 1.0, 1, r1)
+        cg.add(f"{prefix}w1.lora_a", (d, r1), dax1, x2, d, r1, 1.0, 1, r1)
     dx = torch.empty(B * s, d, dtype=torch.bfloat16, device=dev)
     _abi.call("lx_neuron_fc1_dgrad", dz.data_ptr(), dz.stride(0), B, s, d, f, blk, lw.mlp.w1_t.data_ptr(),
               nm.counts.data_ptr(), nm.ids.data_ptr(), _abi.ptr(dax1), _abi.ptr(ad1.a if ad1 else None),
               ad1.rank if ad1 else 0, dx.data_ptr(), 0, _abi.ptr(cache.get("w1p")), st)
+    cg.flush()
     return dx
 
 
@@ -176,12 +195,13 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
     if ad_o is not None:
         dax_o = rowproj(g, B, s, d, ad_o.b, 1, d, ad_o.rank, scale=ad_o.scaling)
         d_heads.addmm_(dax_o.to(torch.bfloat16), ad_o.a.t().to(torch.bfloat16))
+    cg = _CgBatch(grads, B, s)
     if ad_o is not None:
         r = ad_o.rank
-        _cg(grads, f"{prefix}wo.lora_a", (d, r), dax_o, cache["o"], B, s, d, r, 1.0, 1, r)
-        _cg(grads, f"{prefix}wo.lora_b", (r, d), cache["ax_o"], g, B, s, d, r, ad_o.scaling, d, 1)
+        cg.add(f"{prefix}wo.lora_a", (d, r), dax_o, cache["o"], d, r, 1.0, 1, r)
+        cg.add(f"{prefix}wo.lora_b", (r, d), cache["ax_o"], g, d, r, ad_o.scaling, d, 1)
     if bitfit:
-        _cg(grads, f"{prefix}bo", (d,), None, g, B, s, d, 1, 1.0, 0, 1)
+        cg.add(f"{prefix}bo", (d,), None, g, d, 1, 1.0, 0, 1)
     qkv = cache["qkv"]
     dqkv = torch.empty_like(qkv)
     scale = 1.0 / float(np.sqrt(hd))
@@ -202,13 +222,14 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
         dx.addmm_(dax.to(torch.bfloat16), cache["a_cat"].t().to(torch.bfloat16))
     for j, t in enumerate(tq):
         ad, sl = lora[t], M.QKV_SLOT[t]
-        _cg(grads, f"{prefix}{t}.lora_a", (d, r), dax[:, j * r : (j + 1) * r], x2, B, s, d, r, 1.0, 1, r)
-        _cg(grads, f"{prefix}{t}.lora_b", (r, d), cache["ax"][:, j * r : (j + 1) * r], dqkv[:, sl * d : (sl + 1) * d], B,
-            s, d, r, ad.scaling, d, 1)
+        cg.add(f"{prefix}{t}.lora_a", (d, r), dax[:, j * r : (j + 1) * r], x2, d, r, 1.0, 1, r)
+        cg.add(f"{prefix}{t}.lora_b", (r, d), cache["ax"][:, j * r : (j + 1) * r], dqkv[:, sl * d : (sl + 1) * d], d, r,
+               ad.scaling, d, 1)
     if bitfit:
         for t in ("wq", "wk", "wv"):
             sl = M.QKV_SLOT[t]
-            _cg(grads, f"{prefix}b{t[1]}", (d,), None, dqkv[:, sl * d : (sl + 1) * d], B, s, d, 1, 1.0, 0, 1)
+            cg.add(f"{prefix}b{t[1]}", (d,), None, dqkv[:, sl * d : (sl + 1) * d], d, 1, 1.0, 0, 1)
+    cg.flush()
     return dx
 
 

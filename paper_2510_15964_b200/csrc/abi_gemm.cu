@@ -43,6 +43,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
                       uint32_t box_inner, uint32_t box_outer) {
+  return make_tmap_bf16_2d_sw(map, ptr, inner, outer, row_stride_elems, box_inner, box_outer, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+int make_tmap_bf16_2d_sw(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+                         uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
   auto enc = get_encode();
   LX_REQUIRE(enc != nullptr, LX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   LX_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, LX_ERR_SHAPE, "TMA base pointer must be 16B aligned");
@@ -52,7 +57,7 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   LX_REQUIRE(r == CUDA_SUCCESS, LX_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu box=%u,%u", (int)r,
              (unsigned long long)inner, (unsigned long long)outer, box_inner, box_outer);

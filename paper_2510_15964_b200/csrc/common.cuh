@@ -36,6 +36,10 @@ void set_error(const char* fmt, ...);
 int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
                       uint32_t box_inner, uint32_t box_outer);
 
+// same with an explicit swizzle (CU_TENSOR_MAP_SWIZZLE_*)
+int make_tmap_bf16_2d_sw(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+                         uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz);
+
 int num_sms();
 
 inline int launch_check(const char* what) {

@@ -11,10 +11,10 @@
 // the chunk of W (gathered through the item's block ids) is staged once in
 // shared memory with coalesced loads and reused by all 32 rows; each lane
 // consumes 16 contiguous bf16 per row per chunk (two 16B loads).
-// colgrad: a CTA owns 256 columns x 256 rows; a lane owns 8 adjacent
-// columns (one 16B load per row), warps split the rows and reduce through
-// shared memory; one partial per (item, 256-row split) is written and a fixed-
-// order final pass sums partials over splits and items (deterministic).
+// colgrad: one grouped launch per sublayer backward over 64-column chunks x
+// row splits on mma.sync (see colgrad_group_kernel below).
+#include <algorithm>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -235,38 +235,69 @@ __global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_
   }
 }
 
-constexpr int kCgCols = 128;  // columns per CTA: 8 consumer warps x 16 columns
-constexpr int kCgRows = 256;  // rows per CTA (one split): 2 CTAs per SM keep ~128 KB of X in flight
+// ---------------------------------------------------------------- colgrad (grouped)
+// G_i(q, c) = scale_i * sum_rows P_i[row, q] X_i[row, c] for up to kCgMaxProbs problems per launch (all
+// LoRA / BitFit column reductions of one sublayer's backward). It is the GEMM D[q][c] = P^T X with
+// m = q, n = column, k = row, on mma.sync m16n8k16 (bf16 in, fp32 accumulate): the 16 m-rows of one
+// MMA carry P_hi (rows 0..7) and P_lo (rows 8..15) of 8 ranks, so X (P_hi + P_lo) keeps ~16 mantissa
+// bits of P at no extra MMA cost. A prep launch writes each P once as that fragment-ready bf16 hi/lo
+// transpose Pt[16*MT][M].
+//
+// HBM-bound streaming: persistent CTAs (2 per SM); one producer thread walks the CTA's units and
+// TMA-loads [128 rows x 64 columns] X stages (16 KB) plus the matching Pt tile through a
+// kCgStages-deep mbarrier ring that crosses unit boundaries; consumer warp w owns columns 8w..8w+7
+// of the chunk (ldmatrix.trans B fragments, no cross-warp reduction), so the steady state has no
+// CTA-wide barrier and ~6 stages x 16 KB per SM in flight.
+//
+// Unit = (problem, 64-column chunk, row split). Dense problems (pos == NULL) treat the batch as one item
+// of n_items*s rows; gathered problems (per-item packed columns, pos[b][block] >= 0 when active) take the
+// chunk in ORIGINAL columns, loop over the items whose blocks in the chunk are active (one TMA box per
+// active 16-column sub-block, addressed through pos), so the partials of every item line up and inactive
+// columns come out exactly 0. A unit writes its partial [r][64] (or G itself when it is the only split);
+// a final launch sums the splits in order: deterministic, no float atomics.
+constexpr int kCgMaxProbs = 8;
+constexpr int kCgChunk = 64;
+constexpr int kCgConsumers = 8;
+constexpr int kCgThreads = 32 * (kCgConsumers + 1);
+constexpr int kCgRows = 128;  // rows per stage = rows per split of a gathered problem
+constexpr int kCgStages = 4;
+constexpr int kCgMaxSlots = 32;  // units per CTA
+constexpr int kCgMaxItems = 16;  // items of a gathered problem
+constexpr int kCgRowsDense = 512;
+constexpr int kCgXBytes = kCgRows * 128;
+constexpr int kCgPBytes = 2 * 32 * 128;  // two 64-row halves of Pt, up to 32 q-rows (MT = 2)
+constexpr int kCgStageBytes = kCgXBytes + kCgPBytes;
+enum : int { kCgLast = 1, kCgEmpty = 2, kCgGath = 4 };
 
-// partial[item][split][q][col] = sum over the split's rows of P[row, q] X[row, col] over the item's
-// packed columns, on tensor cores: it is the GEMM D[col][q] = X^T[col][row] P[row][q] with
-// m = column, n = q, k = row (mma.sync m16n8k16, bf16 in, fp32 accumulate). Warp 8 streams
-// [32 rows x 128 cols] X tiles (two SWIZZLE_128B boxes of 64 columns) through a kCgSt-stage TMA
-// ring (the whole 256-row split in flight); consumer warp w owns columns 16w..16w+15 and takes its
-// A fragments with ldmatrix.trans straight from the swizzled tile. P is staged once per split as
-// bf16 hi + lo ([q][row], padded rows: conflict-free B fragment loads), so X (P_hi + P_lo) keeps
-// ~16 mantissa bits of P. No cross-warp reduction: every warp owns distinct output columns.
-// The CUDA-core form of this kernel was FMA-bound (R FMAs per X element).
-constexpr int kCgSt = 8, kCgTile = 32 * kCgCols * 2;  // bytes per stage (2 atoms of [32][128B])
-constexpr int kCgPStride = kCgRows + 8;               // bf16 elements per staged P row
+struct CgProb {
+  const float* p;
+  __nv_bfloat16* pt;  // [16*MT][mpad] bf16 hi/lo transpose of P (NULL: column sums)
+  const int32_t* pos;
+  float* g;
+  float* ws;  // partials [chunks][splits][r][64] (splits > 1)
+  long long g_sq, g_sc;
+  int ldp, ncols, r, blk, chunks, splits, rows_per_split, rows_eff, unit0, mpad;
+  int pt_item;  // gathered: Pt columns per item (s rounded up to 8: TMA inner coordinates stay 16B-aligned)
+  float scale;
+};
+struct CgGroup {
+  CUtensorMap tx[kCgMaxProbs];  // X: dense box 64 x 128 (SWIZZLE_128B); gathered box 16 x 128 (SWIZZLE_32B)
+  CUtensorMap tp[kCgMaxProbs];  // Pt: box 64 x 16*MT (SWIZZLE_128B)
+  CgProb pr[kCgMaxProbs];
+  int n_probs, n_items, s, n_units, mt;
+};
 
-// Debug-only phase trace (lx_debug_set_colgrad_trace): per CTA 8 clock64 stamps, NULL in production.
-__device__ unsigned long long* g_cg_trace = nullptr;
-LX_DEV void cg_stamp(int slot) {
-  unsigned long long* t = g_cg_trace;
-  if (t != nullptr) {
-    unsigned long long c;
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
-    const size_t cta = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
-    t[cta * 8 + slot] = c;
-  }
-}
+struct CgSlot {
+  int prob, chunk, split, items;  // items: bitmask of the items with work (bit 0 for dense problems)
+};
 
-template <int RN>
-struct CgSmem {
-  static constexpr int kOffP = kCgSt * kCgTile;  // s_pt [2][RN][kCgPStride] bf16
-  static constexpr int kOffBar = kOffP + 2 * RN * kCgPStride * 2;
-  static constexpr int kTotal = kOffBar + 2 * kCgSt * 8 + 1024;
+struct CgSmemL {
+  static constexpr int kRing = kCgStages * kCgStageBytes;
+  static constexpr int kBar = kRing;                                   // full[S], empty[S]
+  static constexpr int kMeta = kBar + 2 * kCgStages * 8;               // int4 per stage
+  static constexpr int kSlots = kMeta + kCgStages * 16;                // (kCgMaxSlots + 1) slots (+ sentinel)
+  static constexpr int kPos = kSlots + (kCgMaxSlots + 1) * 16;         // [slot][item][4] packed column starts
+  static constexpr int kTotal = kPos + kCgMaxSlots * kCgMaxItems * 4 * 4 + 1024;
 };
 
 LX_DEV void ldsm_x4_trans(uint32_t addr, uint32_t (&r)[4]) {
@@ -274,183 +305,273 @@ LX_DEV void ldsm_x4_trans(uint32_t addr, uint32_t (&r)[4]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(addr));
 }
+LX_DEV uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+// zero the bf16 halves whose k row is past the unit's valid rows (lo half = row k, hi half = row k+1)
+LX_DEV uint32_t cg_mask_rows(uint32_t v, int k, int nvalid) {
+  if (k + 1 < nvalid) return v;
+  return k < nvalid ? (v & 0xffffu) : 0u;
+}
 
-template <int RN>
-__global__ void __launch_bounds__(288, 2) colgrad_partial_kernel(const __grid_constant__ CUtensorMap tm_x, const float* __restrict__ p,
-                                                              int ldp, int s, int ncols, int r,
-                                                              const int32_t* __restrict__ counts, int blk,
-                                                              float* __restrict__ ws) {
-  constexpr int NT = RN / 8;
+template <int MT>
+__global__ void __launch_bounds__(kCgThreads, 2) colgrad_group_kernel(const __grid_constant__ CgGroup grp) {
   extern __shared__ uint8_t cg_raw[];
   uint8_t* sm = align_smem_1024(cg_raw);
-  __nv_bfloat16* s_pt = reinterpret_cast<__nv_bfloat16*>(sm + CgSmem<RN>::kOffP);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + CgSmem<RN>::kOffBar);
-  uint64_t* empty = full + kCgSt;
-  const int item = blockIdx.z, split = blockIdx.y;
-  const int n_splits = gridDim.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_item = counts ? __ldg(counts + item) * blk : ncols;
-  if (blockIdx.x * kCgCols >= n_item) return;  // beyond the item's packed width: never read
-  const int r0 = split * kCgRows;
-  const int nrows = min(kCgRows, s - r0);
-  const int n_tiles = (nrows + 31) / 32;
-  if (threadIdx.x == 0) {
-    cg_stamp(0);
-    for (int i = 0; i < kCgSt; ++i) {
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + CgSmemL::kBar);
+  uint64_t* empty = full + kCgStages;
+  int4* meta = reinterpret_cast<int4*>(sm + CgSmemL::kMeta);
+  CgSlot* slots = reinterpret_cast<CgSlot*>(sm + CgSmemL::kSlots);
+  int* postab = reinterpret_cast<int*>(sm + CgSmemL::kPos);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---- this CTA's units (round robin) and, for gathered problems, each (unit, item)'s packed column
+  // starts of the chunk's four 16-column sub-blocks (-1 inactive): one parallel lookup round
+  const int n_slots = (grp.n_units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  if (tid <= n_slots) {
+    CgSlot sl = {0, 0, 0, 0};
+    if (tid < n_slots) {
+      const int u = blockIdx.x + tid * gridDim.x;
+      int pi = 0;
+      while (pi + 1 < grp.n_probs && u >= grp.pr[pi + 1].unit0) ++pi;
+      const CgProb& P = grp.pr[pi];
+      const int local = u - P.unit0;
+      sl.prob = pi;
+      sl.chunk = local / P.splits;
+      sl.split = local % P.splits;
+      sl.items = P.pos ? 0 : 1;
+    }
+    slots[tid] = sl;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kCgStages; ++i) {
       mbar_init(full + i, 1);
-      mbar_init(empty + i, 8);
+      mbar_init(empty + i, kCgConsumers);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == 8) {
-    if (lane == 0) {
-      tma_prefetch_desc(&tm_x);
-      for (int t = 0; t < n_tiles; ++t) {
-        const int st = t % kCgSt;
-        mbar_wait(empty + st, ((t / kCgSt) & 1) ^ 1);
-        mbar_arrive_expect_tx(full + st, kCgTile);
-        uint8_t* dst = sm + st * kCgTile;
-        const int row = item * s + r0 + t * 32;
-        tma_load_2d(dst, &tm_x, full + st, blockIdx.x * kCgCols, row);
-        tma_load_2d(dst + kCgTile / 2, &tm_x, full + st, blockIdx.x * kCgCols + 64, row);
+  for (int e = tid; e < n_slots * kCgMaxItems * 4; e += kCgThreads) {
+    const int k = e / (kCgMaxItems * 4), item = (e / 4) % kCgMaxItems, sb = e % 4;
+    const CgSlot sl = slots[k];
+    const CgProb& P = grp.pr[sl.prob];
+    int v = -1;
+    if (P.pos && item < grp.n_items) {
+      const int oc = sl.chunk * kCgChunk + sb * 16;
+      if (oc < P.ncols) {
+        const int pb = __ldg(P.pos + (size_t)item * (P.ncols / P.blk) + oc / P.blk);
+        if (pb >= 0) v = pb * P.blk + oc % P.blk;
+      }
+    }
+    postab[e] = v;
+    if (v >= 0) atomicOr(&slots[k].items, 1 << item);
+  }
+  __syncthreads();
+
+  if (warp == kCgConsumers) {
+    // ================= producer (one thread)
+    if (lane == 0 && n_slots > 0) {
+      for (int i = 0; i < grp.n_probs; ++i) {
+        tma_prefetch_desc(&grp.tx[i]);
+        if (grp.pr[i].pt) tma_prefetch_desc(&grp.tp[i]);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      auto emit = [&](int slot, int prob, int chunk, int row0, int nvalid, int flags, int subs, int item) {
+        mbar_wait(empty + stage, phase ^ 1);
+        meta[stage] = make_int4(slot, nvalid, flags | (subs << 4), item);
+        uint8_t* xs = sm + stage * kCgStageBytes;
+        if (flags & kCgEmpty) {
+          mbar_arrive(full + stage);
+        } else {
+          const CgProb& P = grp.pr[prob];
+          const int pbytes = P.pt ? 2 * 16 * grp.mt * 128 : 0;
+          if (flags & kCgGath) {
+            mbar_arrive_expect_tx(full + stage, __popc(subs) * (kCgXBytes / 4) + pbytes);
+            for (int sb = 0; sb < 4; ++sb)
+              if ((subs >> sb) & 1)
+                tma_load_2d(xs + sb * (kCgXBytes / 4), &grp.tx[prob], full + stage,
+                            postab[(slot * kCgMaxItems + item) * 4 + sb], row0);
+          } else {
+            mbar_arrive_expect_tx(full + stage, kCgXBytes + pbytes);
+            tma_load_2d(xs, &grp.tx[prob], full + stage, chunk * kCgChunk, row0);
+          }
+          if (P.pt) {
+            const int pc = (flags & kCgGath) ? item * P.pt_item + (row0 - item * grp.s) : row0;
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d(xs + kCgXBytes + h * 16 * grp.mt * 128, &grp.tp[prob], full + stage, pc + 64 * h, 0);
+          }
+        }
+        if (++stage == kCgStages) { stage = 0; phase ^= 1; }
+      };
+      for (int k = 0; k < n_slots; ++k) {
+        const CgSlot sl = slots[k];
+        const CgProb& P = grp.pr[sl.prob];
+        const int nr = min(P.rows_per_split, P.rows_eff - sl.split * P.rows_per_split);
+        if (P.pos == nullptr) {
+          const int nst = (nr + kCgRows - 1) / kCgRows;
+          for (int st = 0; st < nst; ++st)
+            emit(k, sl.prob, sl.chunk, sl.split * P.rows_per_split + st * kCgRows, min(kCgRows, nr - st * kCgRows),
+                 st == nst - 1 ? kCgLast : 0, 0xF, 0);
+        } else if (sl.items == 0) {
+          emit(k, sl.prob, sl.chunk, 0, 0, kCgLast | kCgEmpty, 0, 0);
+        } else {
+          for (int m = sl.items; m; m &= m - 1) {
+            const int item = __ffs(m) - 1;
+            int subs = 0;
+            for (int sb = 0; sb < 4; ++sb) subs |= (postab[(k * kCgMaxItems + item) * 4 + sb] >= 0) << sb;
+            emit(k, sl.prob, sl.chunk, item * grp.s + sl.split * P.rows_per_split, nr,
+                 kCgGath | ((m & (m - 1)) == 0 ? kCgLast : 0), subs, item);
+          }
+        }
       }
     }
     return;
   }
-  // P rows of this split -> smem as bf16 hi/lo, transposed (p == NULL: column sums, P[:, 0] = 1);
-  // rows past nrows and columns q >= r are zero
-  for (int e = threadIdx.x; e < kCgRows * RN; e += 256) {
-    const int i = e / RN, q = e % RN;
-    float v = 0.f;
-    if (i < nrows && q < r) v = p ? __ldg(p + ((size_t)item * s + r0 + i) * ldp + q) : 1.f;
-    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-    s_pt[q * kCgPStride + i] = hi;
-    s_pt[(RN + q) * kCgPStride + i] = __float2bfloat16_rn(v - __bfloat162float(hi));
-  }
-  asm volatile("bar.sync 1, 256;" ::: "memory");
-  if (threadIdx.x == 0) cg_stamp(1);
-  float acc[NT][4];
+
+  // ================= consumers: warp w owns columns 8w .. 8w+7 of the chunk
+  const int g = lane >> 2, t = lane & 3;
+  const int lm_row = (lane >> 3) * 8 + (lane & 7);  // ldmatrix.trans: matrix lane/8 = k rows 8*(lane/8)..
+  float acc[MT][4];
 #pragma unroll
-  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
-  const int g = lane >> 2, t4 = lane & 3;
-  // ldmatrix.trans: lane L addresses row (L & 7) of matrix L >> 3; matrices (rows k0.., cols 16w..),
-  // (k0.., 16w+8..), (k0+8.., 16w..), (k0+8.., 16w+8..) = the A fragment a0..a3 of m16 x k16
-  const int mi = lane >> 3, ri = lane & 7;
-  const int ld_row = ri + ((mi >> 1) << 3);
-  const int ld_chunk = 2 * (warp & 3) + (mi & 1);
-  const uint32_t sm_base = smem_u32(sm) + (warp >> 2) * (kCgTile / 2);
-  const uint32_t pt_base = smem_u32(s_pt) + (g * kCgPStride + 2 * t4) * 2;
-  for (int t = 0; t < n_tiles; ++t) {
-    const int st = t % kCgSt;
-    mbar_wait(full + st, (t / kCgSt) & 1);
-    if (threadIdx.x == 0 && t == 0) cg_stamp(2);
+  for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+  int stage = 0;
+  uint32_t phase = 0;
+  const int pq = 16 * grp.mt * 128;  // bytes per Pt half
+#pragma unroll 1
+  for (int k = 0; k < n_slots;) {
+    mbar_wait(full + stage, phase);
+    const int4 mt4 = meta[stage];
+    const int flags = mt4.z & 0xF, subs = mt4.z >> 4, nvalid = mt4.y;
+    const CgSlot sl = slots[mt4.x];
+    const CgProb& P = grp.pr[sl.prob];
+    const uint32_t xs = smem_u32(sm + stage * kCgStageBytes);
+    const uint32_t ps = xs + kCgXBytes;
+    const bool active = !(flags & kCgEmpty) &&
+                        ((flags & kCgGath) ? ((subs >> (warp >> 1)) & 1) : (sl.chunk * kCgChunk + 8 * warp < P.ncols));
+    if (active) {
+      const bool has_p = P.pt != nullptr;
 #pragma unroll
-    for (int k0 = 0; k0 < 32; k0 += 16) {
-      const int row = k0 + ld_row;
-      uint32_t a[4];
-      ldsm_x4_trans(sm_base + st * kCgTile + row * 128 + ((ld_chunk ^ (row & 7)) << 4), a);
-      const int kk = t * 32 + k0;
+      for (int h = 0; h < 4; ++h) {  // 32-row quarters: one ldmatrix.x4.trans = B of two k-steps
+        const int row = h * 32 + lm_row;
+        uint32_t b[4];
+        const uint32_t xa = (flags & kCgGath)
+                                ? xs + (warp >> 1) * (kCgXBytes / 4) + row * 32 + (((warp & 1) ^ ((row >> 2) & 1)) << 4)
+                                : xs + row * 128 + ((warp ^ (row & 7)) << 4);
+        ldsm_x4_trans(xa, b);
 #pragma unroll
-      for (int n = 0; n < NT; ++n) {
+        for (int kk = 0; kk < 2; ++kk) {
+          const int k0 = h * 32 + kk * 16;
+          const int kl = k0 & 63;
+          const uint32_t pbase = ps + (k0 >> 6) * pq;
 #pragma unroll
-        for (int hl = 0; hl < 2; ++hl) {
-          const uint32_t pb = pt_base + ((hl * RN + 8 * n) * kCgPStride + kk) * 2;
-          uint32_t b0, b1;
-          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b0) : "r"(pb));
-          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b1) : "r"(pb + 16));
-          mma16816_rp(acc[n], a, b0, b1);
+          for (int m = 0; m < MT; ++m) {
+            uint32_t a[4];
+            if (has_p) {
+              const int qh = 16 * m + g, ql = qh + 8;
+              a[0] = lds32(pbase + qh * 128 + (((kl >> 3) ^ (qh & 7)) << 4) + 4 * t);
+              a[1] = lds32(pbase + ql * 128 + (((kl >> 3) ^ (ql & 7)) << 4) + 4 * t);
+              a[2] = lds32(pbase + qh * 128 + ((((kl >> 3) + 1) ^ (qh & 7)) << 4) + 4 * t);
+              a[3] = lds32(pbase + ql * 128 + ((((kl >> 3) + 1) ^ (ql & 7)) << 4) + 4 * t);
+            } else {  // column sums: P[:, 0] = 1
+              const uint32_t one = (m == 0 && g == 0) ? 0x3f803f80u : 0u;
+              a[0] = one; a[1] = 0u; a[2] = one; a[3] = 0u;
+            }
+            if (nvalid < kCgRows) {
+              a[0] = cg_mask_rows(a[0], k0 + 2 * t, nvalid);
+              a[1] = cg_mask_rows(a[1], k0 + 2 * t, nvalid);
+              a[2] = cg_mask_rows(a[2], k0 + 2 * t + 8, nvalid);
+              a[3] = cg_mask_rows(a[3], k0 + 2 * t + 8, nvalid);
+            }
+            mma16816_rp(acc[m], a, b[2 * kk], b[2 * kk + 1]);
+          }
         }
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + st);
-  }
-  if (threadIdx.x == 0) cg_stamp(3);
-  // D[m = column][n = q]: d0 (col g, q 2t), d1 (g, 2t+1), d2 (g+8, 2t), d3 (g+8, 2t+1)
-  float* out = ws + ((size_t)item * n_splits + split) * r * (size_t)ncols;
-  const int c = blockIdx.x * kCgCols + warp * 16 + g;
+    if (lane == 0) mbar_arrive(empty + stage);
+    if (++stage == kCgStages) { stage = 0; phase ^= 1; }
+    if (flags & kCgLast) {
+      // unit done: rows g (hi) and g+8 (lo) of m-tile m are rank q = g + 8m; columns 8w + 2t, +1
+      const int col = sl.chunk * kCgChunk + 8 * warp + 2 * t;
 #pragma unroll
-  for (int n = 0; n < NT; ++n) {
-    const int q = 8 * n + 2 * t4;
-    if (q < r) {
-      if (c < ncols) out[(size_t)q * ncols + c] = acc[n][0];
-      if (c + 8 < ncols) out[(size_t)q * ncols + c + 8] = acc[n][2];
-    }
-    if (q + 1 < r) {
-      if (c < ncols) out[(size_t)(q + 1) * ncols + c] = acc[n][1];
-      if (c + 8 < ncols) out[(size_t)(q + 1) * ncols + c + 8] = acc[n][3];
-    }
-  }
-  if (threadIdx.x == 0) cg_stamp(4);
-}
-
-// G(q, c_orig) = scale * sum_items sum_splits partial[item][split][q][pos_item(c_orig)]
-__global__ void colgrad_final_kernel(const float* __restrict__ ws, int n_items, int n_splits, int ncols, int r,
-                                     const int32_t* __restrict__ pos, int blk, float scale, float* __restrict__ g,
-                                     long long g_sq, long long g_sc) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int q = blockIdx.y;
-  if (c >= ncols || q >= r) return;
-  float acc = 0.f;
-  // items in groups of 8: all position lookups, then all partial loads, are independent (in flight together);
-  // the summation order stays fixed (item-major, split-minor) -> deterministic
-  for (int b0 = 0; b0 < n_items; b0 += 8) {
-    int pcs[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int b = b0 + u;
-      pcs[u] = -1;
-      if (b < n_items) {
-        if (pos) {
-          const int pb = __ldg(pos + (size_t)b * (ncols / blk) + c / blk);
-          pcs[u] = pb < 0 ? -1 : pb * blk + c % blk;
+      for (int m = 0; m < MT; ++m) {
+        const int q = g + 8 * m;
+        const float v0 = acc[m][0] + acc[m][2], v1 = acc[m][1] + acc[m][3];
+        acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+        if (q >= P.r || col >= P.ncols) continue;
+        if (P.splits == 1) {
+          P.g[(long long)q * P.g_sq + (long long)col * P.g_sc] = v0 * P.scale;
+          P.g[(long long)q * P.g_sq + (long long)(col + 1) * P.g_sc] = v1 * P.scale;
         } else {
-          pcs[u] = c;
+          float* part = P.ws + (((size_t)sl.chunk * P.splits + sl.split) * P.r + q) * kCgChunk + 8 * warp + 2 * t;
+          *reinterpret_cast<float2*>(part) = make_float2(v0, v1);
         }
       }
-    }
-    for (int sp0 = 0; sp0 < n_splits; sp0 += 4) {
-      float vals[8][4];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          vals[u][t] = (pcs[u] >= 0 && sp0 + t < n_splits)
-                           ? __ldg(ws + (((size_t)(b0 + u) * n_splits + sp0 + t) * r + q) * ncols + pcs[u])
-                           : 0.f;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) acc += vals[u][t];
+      ++k;
     }
   }
-  g[(long long)q * g_sq + (long long)c * g_sc] = acc * scale;
 }
 
-template <int RN>
-static int colgrad_impl(const float* p, int ldp, const uint16_t* x, int ldx, int n_items, int s, int ncols, int r,
-                        float scale, const int32_t* counts, const int32_t* pos, int blk, float* g, long long g_sq,
-                        long long g_sc, float* ws, cudaStream_t stream) {
-  // shared columns (no counts): every item reads the same columns -> one item of n_items * s rows
-  const int items = counts ? n_items : 1, rows = counts ? s : n_items * s;
-  const int splits = (rows + kCgRows - 1) / kCgRows;
-  dim3 g1((ncols + kCgCols - 1) / kCgCols, splits, items);
-  constexpr int smem = CgSmem<RN>::kTotal;
-  static cudaError_t attr = cudaFuncSetAttribute(colgrad_partial_kernel<RN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  LX_CHECK_CUDA(attr);
-  // X as [n_items*s, ldx]: boxes of 64 columns x 32 rows (columns past ncols / the item's width are
-  // never combined; rows past an item's split are weighted by P = 0)
-  CUtensorMap tm;
-  int rc0 = make_tmap_bf16_2d(&tm, x, (uint64_t)ldx, (uint64_t)n_items * s, (uint64_t)ldx, 64, 32);
-  if (rc0) return rc0;
-  colgrad_partial_kernel<RN><<<g1, 288, smem, stream>>>(tm, p, ldp, rows, ncols, r, counts, counts ? blk : 1, ws);
-  int rc = launch_check("colgrad_partial");
-  if (rc) return rc;
-  dim3 g2((ncols + 255) / 256, r);
-  colgrad_final_kernel<<<g2, 256, 0, stream>>>(ws, items, splits, ncols, r, counts ? pos : nullptr,
-                                                  counts ? blk : 1, scale, g, g_sq, g_sc);
-  return launch_check("colgrad_final");
+// Pt[qrow][row] (bf16): qrow = 16m + j (j < 8: hi of rank 8m + j; j >= 8: lo of rank 8m + j - 8)
+__global__ void colgrad_prep_kernel(const __grid_constant__ CgGroup grp) {
+  const CgProb& P = grp.pr[blockIdx.z];
+  if (P.pt == nullptr) return;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  const int qrow = blockIdx.y;
+  if (row >= P.mpad || qrow >= 16 * grp.mt) return;
+  const int q = (qrow >> 4) * 8 + (qrow & 7);
+  const int M = grp.n_items * grp.s;
+  int src = row;  // Pt column -> activation row
+  if (P.pos) src = (row % P.pt_item < grp.s) ? (row / P.pt_item) * grp.s + row % P.pt_item : M;
+  const float v = (q < P.r && src < M) ? __ldg(P.p + (size_t)src * P.ldp + q) : 0.f;
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  P.pt[(size_t)qrow * P.mpad + row] = (qrow & 8) ? __float2bfloat16_rn(v - __bfloat162float(hi)) : hi;
+}
+
+// G(q, c) = scale * sum over splits (in order) of the partials, for the problems with splits > 1
+__global__ void colgrad_final_kernel(const __grid_constant__ CgGroup grp) {
+  const CgProb& P = grp.pr[blockIdx.y];
+  if (P.splits == 1) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= P.chunks * P.r * kCgChunk) return;
+  const int chunk = e / (P.r * kCgChunk), q = (e / kCgChunk) % P.r, c = e % kCgChunk;
+  const int col = chunk * kCgChunk + c;
+  if (col >= P.ncols) return;
+  const float* src = P.ws + ((size_t)chunk * P.splits * P.r + q) * kCgChunk + c;
+  float v = 0.f;
+#pragma unroll 4
+  for (int sp = 0; sp < P.splits; ++sp) v += src[(size_t)sp * P.r * kCgChunk];
+  P.g[(long long)q * P.g_sq + (long long)col * P.g_sc] = v * P.scale;
+}
+
+// host-side layout of one problem (shared by the workspace query and the launch)
+static void cg_layout(const lx_colgrad_problem& q, int n_items, int s, CgProb& o) {
+  o.chunks = (q.ncols + kCgChunk - 1) / kCgChunk;
+  const bool gathered = q.pos != nullptr;
+  o.rows_eff = gathered ? s : n_items * s;
+  o.rows_per_split = gathered ? kCgRows : kCgRowsDense;
+  o.splits = (o.rows_eff + o.rows_per_split - 1) / o.rows_per_split;
+  o.pt_item = (s + 7) / 8 * 8;
+  o.mpad = gathered ? n_items * o.pt_item : (n_items * s + 7) / 8 * 8;
+}
+
+static int cg_mt(const lx_colgrad_problem* probs, int n) {
+  int mr = 0;
+  for (int i = 0; i < n; ++i) mr = probs[i].r > mr ? probs[i].r : mr;
+  return mr > 8 ? 2 : 1;
+}
+
+// floats: Pt (16*MT*mpad bf16 = 8*MT*mpad floats) + partials, each rounded to 64 floats (256 B)
+static long long cg_ws_floats(const lx_colgrad_problem& q, int n_items, int s, int mt, long long* pt_floats) {
+  CgProb o;
+  cg_layout(q, n_items, s, o);
+  const long long pt = q.p ? (8LL * mt * o.mpad + 63) / 64 * 64 : 0;
+  const long long part = o.splits > 1 ? ((long long)o.chunks * o.splits * q.r * kCgChunk + 63) / 64 * 64 : 0;
+  if (pt_floats) *pt_floats = pt;
+  return pt + part;
 }
 
 }  // namespace lx
@@ -508,32 +629,90 @@ int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const floa
   return launch_check("rowproj");
 }
 
-int lx_debug_set_colgrad_trace(unsigned long long* buf) {
-  LX_CHECK_CUDA(cudaMemcpyToSymbol(g_cg_trace, &buf, sizeof(buf)));
-  return 0;
+long long lx_colgrad_group_ws_floats(const lx_colgrad_problem* probs, int n_probs, int n_items, int s) {
+  const int mt = cg_mt(probs, n_probs);
+  long long tot = 0;
+  for (int i = 0; i < n_probs; ++i) tot += cg_ws_floats(probs[i], n_items, s, mt, nullptr);
+  return tot;
 }
 
-long long lx_colgrad_ws_floats(int n_items, int s, int ncols, int r) {
-  // bound for both layouts: per item (gathered) or one item of n_items * s rows (shared columns)
-  long long splits = (s + kCgRows - 1) / kCgRows;
-  return (long long)n_items * splits * r * ncols;
-}
-
-int lx_colgrad(const float* p, int ldp, const uint16_t* x, int ldx, int n_items, int s, int ncols, int r, float scale,
-               const int32_t* counts, const int32_t* pos, int blk, float* g, long long g_sq, long long g_sc, float* ws,
-               lx_stream_t stream) {
-  LX_REQUIRE(r >= 1 && r <= 16, LX_ERR_UNSUPPORTED, "colgrad: rank %d outside [1, 16]", r);
-  LX_REQUIRE(!p || ldp >= r, LX_ERR_SHAPE, "colgrad: ldp < r");
-  LX_REQUIRE(ncols % 4 == 0, LX_ERR_SHAPE, "colgrad: ncols must be a multiple of 4");
-  LX_REQUIRE(!counts || (pos && ncols % blk == 0), LX_ERR_MASK, "colgrad: gathered columns need pos and ncols %% blk == 0");
-  LX_REQUIRE(ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0, LX_ERR_SHAPE, "colgrad: 16B-aligned rows required");
-  if (r > 8) return colgrad_impl<16>(p, ldp, x, ldx, n_items, s, ncols, r, scale, counts, pos, blk, g, g_sq, g_sc, ws, stream);
-  return colgrad_impl<8>(p, ldp, x, ldx, n_items, s, ncols, r, scale, counts, pos, blk, g, g_sq, g_sc, ws, stream);
-}
-
-int lx_colsum(const uint16_t* x, int ldx, int n_items, int s, int ncols, const int32_t* counts, const int32_t* pos,
-              int blk, float* out, float* ws, lx_stream_t stream) {
-  return lx_colgrad(nullptr, 1, x, ldx, n_items, s, ncols, 1, 1.f, counts, pos, blk, out, 0, 1, ws, stream);
+int lx_colgrad_group(const lx_colgrad_problem* probs, int n_probs, int n_items, int s, float* ws, lx_stream_t stream) {
+  LX_REQUIRE(n_probs >= 1 && n_probs <= kCgMaxProbs, LX_ERR_UNSUPPORTED, "colgrad_group: 1..%d problems", kCgMaxProbs);
+  LX_REQUIRE(n_items >= 1 && s >= 1, LX_ERR_SHAPE, "colgrad_group: empty batch");
+  LX_REQUIRE(ws != nullptr && (reinterpret_cast<uintptr_t>(ws) & 255) == 0, LX_ERR_SHAPE,
+             "colgrad_group: 256B-aligned workspace required");
+  CgGroup grp;
+  memset(&grp, 0, sizeof(grp));
+  grp.n_probs = n_probs;
+  grp.n_items = n_items;
+  grp.s = s;
+  grp.mt = cg_mt(probs, n_probs);
+  const int M = n_items * s;
+  int units = 0, max_final = 0, max_mpad = 0;
+  long long ws_off = 0;
+  for (int i = 0; i < n_probs; ++i) {
+    const lx_colgrad_problem& q = probs[i];
+    LX_REQUIRE(q.r >= 1 && q.r <= 16, LX_ERR_UNSUPPORTED, "colgrad: rank %d outside [1, 16]", q.r);
+    LX_REQUIRE(!q.p || q.ldp >= q.r, LX_ERR_SHAPE, "colgrad: ldp < r");
+    LX_REQUIRE(q.ncols % 8 == 0, LX_ERR_SHAPE, "colgrad: ncols must be a multiple of 8");
+    LX_REQUIRE(!q.pos || (q.blk % 16 == 0 && q.ncols % q.blk == 0), LX_ERR_MASK,
+               "colgrad: gathered columns need blk %% 16 == 0 and ncols %% blk == 0");
+    LX_REQUIRE(!q.pos || n_items <= kCgMaxItems, LX_ERR_UNSUPPORTED, "colgrad: gathered problems take <= %d items",
+               kCgMaxItems);
+    LX_REQUIRE(q.ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(q.x) & 15) == 0, LX_ERR_SHAPE,
+               "colgrad: 16B-aligned rows required");
+    CgProb& o = grp.pr[i];
+    cg_layout(q, n_items, s, o);
+    long long pt_floats = 0;
+    const long long need = cg_ws_floats(q, n_items, s, grp.mt, &pt_floats);
+    o.p = q.p;
+    o.pt = q.p ? reinterpret_cast<__nv_bfloat16*>(ws + ws_off) : nullptr;
+    o.ws = ws + ws_off + pt_floats;
+    ws_off += need;
+    o.pos = q.pos;
+    o.g = q.g;
+    o.g_sq = q.g_sq;
+    o.g_sc = q.g_sc;
+    o.ldp = q.ldp;
+    o.ncols = q.ncols;
+    o.r = q.r;
+    o.blk = q.pos ? q.blk : 1;
+    o.scale = q.scale;
+    o.unit0 = units;
+    units += o.chunks * o.splits;
+    if (o.splits > 1) max_final = std::max(max_final, o.chunks * q.r * kCgChunk);
+    max_mpad = std::max(max_mpad, o.mpad);
+    int rc = q.pos ? make_tmap_bf16_2d_sw(&grp.tx[i], q.x, (uint64_t)q.ldx, (uint64_t)M, (uint64_t)q.ldx, 16, kCgRows,
+                                          CU_TENSOR_MAP_SWIZZLE_32B)
+                   : make_tmap_bf16_2d_sw(&grp.tx[i], q.x, (uint64_t)q.ncols, (uint64_t)M, (uint64_t)q.ldx, 64, kCgRows,
+                                          CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    if (q.p) {
+      rc = make_tmap_bf16_2d_sw(&grp.tp[i], o.pt, (uint64_t)o.mpad, (uint64_t)(16 * grp.mt), (uint64_t)o.mpad, 64,
+                                16 * grp.mt, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (rc) return rc;
+    }
+  }
+  grp.n_units = units;
+  const int grid = std::max(std::min(units, 2 * num_sms()), (units + kCgMaxSlots - 1) / kCgMaxSlots);
+  LX_REQUIRE((units + grid - 1) / grid <= kCgMaxSlots, LX_ERR_UNSUPPORTED, "colgrad_group: too many units");
+  colgrad_prep_kernel<<<dim3((max_mpad + 255) / 256, 16 * grp.mt, n_probs), 256, 0, stream>>>(grp);
+  int rc = launch_check("colgrad_prep");
+  if (rc) return rc;
+  constexpr int smem = CgSmemL::kTotal;
+  if (grp.mt == 2) {
+    static cudaError_t attr = cudaFuncSetAttribute(colgrad_group_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    LX_CHECK_CUDA(attr);
+    colgrad_group_kernel<2><<<grid, kCgThreads, smem, stream>>>(grp);
+  } else {
+    static cudaError_t attr = cudaFuncSetAttribute(colgrad_group_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    LX_CHECK_CUDA(attr);
+    colgrad_group_kernel<1><<<grid, kCgThreads, smem, stream>>>(grp);
+  }
+  rc = launch_check("colgrad_group");
+  if (rc || max_final == 0) return rc;
+  colgrad_final_kernel<<<dim3((max_final + 255) / 256, n_probs), 256, 0, stream>>>(grp);
+  return launch_check("colgrad_final");
 }
 
 }  // extern "C"

@@ -259,20 +259,47 @@ def rowproj(x2: torch.Tensor, n_items: int, s: int, K: int, w: torch.Tensor, w_s
     return y
 
 
-def colgrad(p: torch.Tensor | None, x2: torch.Tensor, n_items: int, s: int, ncols: int, r: int, scale: float,
-            out: torch.Tensor, g_sq: int, g_sc: int, masks: NeuronMasks | None = None, blk: int = 1) -> torch.Tensor:
-    """out(q, c) = scale * sum_rows P[row, q] X[row, c] (c original column), deterministic.
+def colgrad_problem(p: torch.Tensor | None, x2: torch.Tensor, ncols: int, r: int, scale: float, out: torch.Tensor,
+                    g_sq: int, g_sc: int, masks: NeuronMasks | None = None, blk: int = 1):
+    """One G(q, c) = scale * sum_rows P[row, q] X[row, c] problem (c original column) for colgrad_group.
     P may be a column slice (row stride p.stride(0)); X may be a column slice (row stride x2.stride(0))."""
     if p is not None and p.stride(1) != 1:
         p = p.contiguous()
-    if p is not None and r > 16:  # the kernel takes up to 16 ranks per call
-        for q0 in range(0, r, 16):
-            colgrad(p[:, q0:], x2, n_items, s, ncols, min(16, r - q0), scale,
-                    out.view(-1)[q0 * g_sq:] if g_sq else out, g_sq, g_sc, masks, blk)
-        return out
-    ws = torch.empty(int(_abi.lib().lx_colgrad_ws_floats(n_items, s, ncols, r)), dtype=torch.float32, device=x2.device)
-    _abi.call("lx_colgrad", _abi.ptr(p), p.stride(0) if p is not None else 1, x2.data_ptr(), x2.stride(0), n_items, s,
-              ncols, r, float(scale),
-              _abi.ptr(masks.counts if masks else None), _abi.ptr(masks.pos if masks else None), blk, out.data_ptr(),
-              g_sq, g_sc, ws.data_ptr(), _abi.stream_handle(x2.device))
+    return dict(p=p, x=x2, ncols=ncols, r=r, scale=float(scale), out=out, g_sq=g_sq, g_sc=g_sc, masks=masks,
+                blk=blk if masks is not None else 1)
+
+
+def colgrad_group(problems: list, n_items: int, s: int) -> None:
+    """All problems in one deterministic launch (lx_colgrad_group, up to 8; ranks above 16 split)."""
+    flat = []
+    for pr in problems:
+        r = pr["r"]
+        if pr["p"] is not None and r > 16:  # the kernel takes up to 16 ranks per problem
+            for q0 in range(0, r, 16):
+                sub = dict(pr, p=pr["p"][:, q0:], r=min(16, r - q0))
+                sub["out"] = pr["out"].view(-1)[q0 * pr["g_sq"]:] if pr["g_sq"] else pr["out"]
+                flat.append(sub)
+        else:
+            flat.append(pr)
+    for i in range(0, len(flat), 8):
+        chunk = flat[i : i + 8]
+        arr = (_abi.ColgradProblem * len(chunk))()
+        keep = []
+        for j, pr in enumerate(chunk):
+            p, x, m = pr["p"], pr["x"], pr["masks"]
+            arr[j] = _abi.ColgradProblem(_abi.ptr(p), p.stride(0) if p is not None else 1, x.data_ptr(), x.stride(0),
+                                         pr["ncols"], pr["r"], pr["scale"], _abi.ptr(m.pos if m is not None else None),
+                                         pr["blk"], pr["out"].data_ptr(), pr["g_sq"], pr["g_sc"])
+            keep.append(p)
+        lib = _abi.lib()
+        dev = chunk[0]["x"].device
+        nws = int(lib.lx_colgrad_group_ws_floats(arr, len(chunk), n_items, s))
+        ws = torch.empty(max(nws, 1), dtype=torch.float32, device=dev)
+        _abi.call("lx_colgrad_group", arr, len(chunk), n_items, s, ws.data_ptr(), _abi.stream_handle(dev))
+
+
+def colgrad(p: torch.Tensor | None, x2: torch.Tensor, n_items: int, s: int, ncols: int, r: int, scale: float,
+            out: torch.Tensor, g_sq: int, g_sc: int, masks: NeuronMasks | None = None, blk: int = 1) -> torch.Tensor:
+    """out(q, c) = scale * sum_rows P[row, q] X[row, c] (c original column), deterministic (one problem)."""
+    colgrad_group([colgrad_problem(p, x2, ncols, r, scale, out, g_sq, g_sc, masks, blk)], n_items, s)
     return out
