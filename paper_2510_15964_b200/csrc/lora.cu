@@ -240,12 +240,14 @@ __global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_
 // LoRA / BitFit column reductions of one sublayer's backward). It is the GEMM D[q][c] = P^T X with
 // m = q, n = column, k = row, on mma.sync m16n8k16 (bf16 in, fp32 accumulate): the 16 m-rows of one
 // MMA carry P_hi (rows 0..7) and P_lo (rows 8..15) of 8 ranks, so X (P_hi + P_lo) keeps ~16 mantissa
-// bits of P at no extra MMA cost. A prep launch writes each P once as that fragment-ready bf16 hi/lo
-// transpose Pt[16*MT][M].
+// bits of P at no extra MMA cost. A prep launch writes each P once in fragment order: per 128-row block
+// and lane, the lane's A fragments of the block's 8 k-steps as 8*MT contiguous 16-byte chunks (rotated
+// by lane: conflict-free LDS.128), fetched per stage with one 1-D bulk copy. Column sums (P == NULL)
+// use an all-ones P. Rows past a unit (ragged items) carry P = 0, so no masking is needed.
 //
 // HBM-bound streaming: persistent CTAs (2 per SM); one producer thread walks the CTA's units and
 // TMA-loads [128 rows x 64 columns] X stages (16 KB) plus the matching Pt tile through a
-// kCgStages-deep mbarrier ring that crosses unit boundaries; consumer warp w owns columns 8w..8w+7
+// 4-5 stage mbarrier ring that crosses unit boundaries; consumer warp w owns columns 8w..8w+7
 // of the chunk (ldmatrix.trans B fragments, no cross-warp reduction), so the steady state has no
 // CTA-wide barrier and ~6 stages x 16 KB per SM in flight.
 //
@@ -260,29 +262,25 @@ constexpr int kCgChunk = 64;
 constexpr int kCgConsumers = 8;
 constexpr int kCgThreads = 32 * (kCgConsumers + 1);
 constexpr int kCgRows = 128;  // rows per stage = rows per split of a gathered problem
-constexpr int kCgStages = 4;
 constexpr int kCgMaxSlots = 32;  // units per CTA
 constexpr int kCgMaxItems = 16;  // items of a gathered problem
-constexpr int kCgRowsDense = 512;
+constexpr int kCgRowsDense = 256;
 constexpr int kCgXBytes = kCgRows * 128;
-constexpr int kCgPBytes = 2 * 32 * 128;  // two 64-row halves of Pt, up to 32 q-rows (MT = 2)
-constexpr int kCgStageBytes = kCgXBytes + kCgPBytes;
 enum : int { kCgLast = 1, kCgEmpty = 2, kCgGath = 4 };
 
 struct CgProb {
   const float* p;
-  __nv_bfloat16* pt;  // [16*MT][mpad] bf16 hi/lo transpose of P (NULL: column sums)
+  uint32_t* pt;       // fragment blocks [nblocks][32 lanes][8*MT chunks][4 words]
   const int32_t* pos;
   float* g;
   float* ws;  // partials [chunks][splits][r][64] (splits > 1)
   long long g_sq, g_sc;
-  int ldp, ncols, r, blk, chunks, splits, rows_per_split, rows_eff, unit0, mpad;
-  int pt_item;  // gathered: Pt columns per item (s rounded up to 8: TMA inner coordinates stay 16B-aligned)
+  int ldp, ncols, r, blk, chunks, splits, rows_per_split, rows_eff, unit0;
+  int nblocks;  // 128-row fragment blocks (gathered: per item ceil(s/128), item-major)
   float scale;
 };
 struct CgGroup {
   CUtensorMap tx[kCgMaxProbs];  // X: dense box 64 x 128 (SWIZZLE_128B); gathered box 16 x 128 (SWIZZLE_32B)
-  CUtensorMap tp[kCgMaxProbs];  // Pt: box 64 x 16*MT (SWIZZLE_128B)
   CgProb pr[kCgMaxProbs];
   int n_probs, n_items, s, n_units, mt;
 };
@@ -291,12 +289,15 @@ struct CgSlot {
   int prob, chunk, split, items;  // items: bitmask of the items with work (bit 0 for dense problems)
 };
 
+template <int MT>
 struct CgSmemL {
-  static constexpr int kRing = kCgStages * kCgStageBytes;
-  static constexpr int kBar = kRing;                                   // full[S], empty[S]
-  static constexpr int kMeta = kBar + 2 * kCgStages * 8;               // int4 per stage
-  static constexpr int kSlots = kMeta + kCgStages * 16;                // (kCgMaxSlots + 1) slots (+ sentinel)
-  static constexpr int kPos = kSlots + (kCgMaxSlots + 1) * 16;         // [slot][item][4] packed column starts
+  static constexpr int kStages = MT == 1 ? 5 : 4;
+  static constexpr int kStageBytes = kCgXBytes + 32 * 8 * MT * 16;  // X tile + fragment block (32 lanes x 8*MT x 16 B)
+  static constexpr int kRing = kStages * kStageBytes;
+  static constexpr int kBar = kRing;                                // full[S], empty[S]
+  static constexpr int kMeta = kBar + 2 * kStages * 8;              // int4 per stage
+  static constexpr int kSlots = kMeta + kStages * 16;               // (kCgMaxSlots + 1) slots (+ sentinel)
+  static constexpr int kPos = kSlots + (kCgMaxSlots + 1) * 16;      // [slot][item][4] packed column starts
   static constexpr int kTotal = kPos + kCgMaxSlots * kCgMaxItems * 4 * 4 + 1024;
 };
 
@@ -305,26 +306,24 @@ LX_DEV void ldsm_x4_trans(uint32_t addr, uint32_t (&r)[4]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(addr));
 }
-LX_DEV uint32_t lds32(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
-}
-// zero the bf16 halves whose k row is past the unit's valid rows (lo half = row k, hi half = row k+1)
-LX_DEV uint32_t cg_mask_rows(uint32_t v, int k, int nvalid) {
-  if (k + 1 < nvalid) return v;
-  return k < nvalid ? (v & 0xffffu) : 0u;
+LX_DEV void bulk_load(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 template <int MT>
 __global__ void __launch_bounds__(kCgThreads, 2) colgrad_group_kernel(const __grid_constant__ CgGroup grp) {
+  using L = CgSmemL<MT>;
+  constexpr int kCgStages = L::kStages, kCgStageBytes = L::kStageBytes;
   extern __shared__ uint8_t cg_raw[];
   uint8_t* sm = align_smem_1024(cg_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + CgSmemL::kBar);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::kBar);
   uint64_t* empty = full + kCgStages;
-  int4* meta = reinterpret_cast<int4*>(sm + CgSmemL::kMeta);
-  CgSlot* slots = reinterpret_cast<CgSlot*>(sm + CgSmemL::kSlots);
-  int* postab = reinterpret_cast<int*>(sm + CgSmemL::kPos);
+  int4* meta = reinterpret_cast<int4*>(sm + L::kMeta);
+  CgSlot* slots = reinterpret_cast<CgSlot*>(sm + L::kSlots);
+  int* postab = reinterpret_cast<int*>(sm + L::kPos);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // ---- this CTA's units (round robin) and, for gathered problems, each (unit, item)'s packed column
@@ -375,7 +374,6 @@ __global__ void __launch_bounds__(kCgThreads, 2) colgrad_group_kernel(const __gr
     if (lane == 0 && n_slots > 0) {
       for (int i = 0; i < grp.n_probs; ++i) {
         tma_prefetch_desc(&grp.tx[i]);
-        if (grp.pr[i].pt) tma_prefetch_desc(&grp.tp[i]);
       }
       int stage = 0;
       uint32_t phase = 0;
@@ -387,7 +385,7 @@ __global__ void __launch_bounds__(kCgThreads, 2) colgrad_group_kernel(const __gr
           mbar_arrive(full + stage);
         } else {
           const CgProb& P = grp.pr[prob];
-          const int pbytes = P.pt ? 2 * 16 * grp.mt * 128 : 0;
+          const int pbytes = 32 * 8 * grp.mt * 16;
           if (flags & kCgGath) {
             mbar_arrive_expect_tx(full + stage, __popc(subs) * (kCgXBytes / 4) + pbytes);
             for (int sb = 0; sb < 4; ++sb)
@@ -398,11 +396,9 @@ __global__ void __launch_bounds__(kCgThreads, 2) colgrad_group_kernel(const __gr
             mbar_arrive_expect_tx(full + stage, kCgXBytes + pbytes);
             tma_load_2d(xs, &grp.tx[prob], full + stage, chunk * kCgChunk, row0);
           }
-          if (P.pt) {
-            const int pc = (flags & kCgGath) ? item * P.pt_item + (row0 - item * grp.s) : row0;
-            for (int h = 0; h < 2; ++h)
-              tma_load_2d(xs + kCgXBytes + h * 16 * grp.mt * 128, &grp.tp[prob], full + stage, pc + 64 * h, 0);
-          }
+          const int blk_i = (flags & kCgGath) ? item * ((grp.s + kCgRows - 1) / kCgRows) + (row0 - item * grp.s) / kCgRows
+                                              : row0 / kCgRows;
+          bulk_load(xs + kCgXBytes, P.pt + (size_t)blk_i * 32 * 8 * grp.mt * 4, pbytes, full + stage);
         }
         if (++stage == kCgStages) { stage = 0; phase ^= 1; }
       };
@@ -439,20 +435,19 @@ __global__ void __launch_bounds__(kCgThreads, 2) colgrad_group_kernel(const __gr
   for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
   int stage = 0;
   uint32_t phase = 0;
-  const int pq = 16 * grp.mt * 128;  // bytes per Pt half
 #pragma unroll 1
   for (int k = 0; k < n_slots;) {
     mbar_wait(full + stage, phase);
     const int4 mt4 = meta[stage];
-    const int flags = mt4.z & 0xF, subs = mt4.z >> 4, nvalid = mt4.y;
+    const int flags = mt4.z & 0xF, subs = mt4.z >> 4;
     const CgSlot sl = slots[mt4.x];
     const CgProb& P = grp.pr[sl.prob];
     const uint32_t xs = smem_u32(sm + stage * kCgStageBytes);
-    const uint32_t ps = xs + kCgXBytes;
     const bool active = !(flags & kCgEmpty) &&
                         ((flags & kCgGath) ? ((subs >> (warp >> 1)) & 1) : (sl.chunk * kCgChunk + 8 * warp < P.ncols));
     if (active) {
-      const bool has_p = P.pt != nullptr;
+      // this lane's A fragments of the block: chunk j at rotated position (j + lane) % (8*MT)
+      const uint32_t pa = xs + kCgXBytes + lane * (8 * MT * 16);
 #pragma unroll
       for (int h = 0; h < 4; ++h) {  // 32-row quarters: one ldmatrix.x4.trans = B of two k-steps
         const int row = h * 32 + lm_row;
@@ -463,28 +458,13 @@ __global__ void __launch_bounds__(kCgThreads, 2) colgrad_group_kernel(const __gr
         ldsm_x4_trans(xa, b);
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
-          const int k0 = h * 32 + kk * 16;
-          const int kl = k0 & 63;
-          const uint32_t pbase = ps + (k0 >> 6) * pq;
 #pragma unroll
           for (int m = 0; m < MT; ++m) {
+            const int j = (h * 2 + kk) * MT + m;
             uint32_t a[4];
-            if (has_p) {
-              const int qh = 16 * m + g, ql = qh + 8;
-              a[0] = lds32(pbase + qh * 128 + (((kl >> 3) ^ (qh & 7)) << 4) + 4 * t);
-              a[1] = lds32(pbase + ql * 128 + (((kl >> 3) ^ (ql & 7)) << 4) + 4 * t);
-              a[2] = lds32(pbase + qh * 128 + ((((kl >> 3) + 1) ^ (qh & 7)) << 4) + 4 * t);
-              a[3] = lds32(pbase + ql * 128 + ((((kl >> 3) + 1) ^ (ql & 7)) << 4) + 4 * t);
-            } else {  // column sums: P[:, 0] = 1
-              const uint32_t one = (m == 0 && g == 0) ? 0x3f803f80u : 0u;
-              a[0] = one; a[1] = 0u; a[2] = one; a[3] = 0u;
-            }
-            if (nvalid < kCgRows) {
-              a[0] = cg_mask_rows(a[0], k0 + 2 * t, nvalid);
-              a[1] = cg_mask_rows(a[1], k0 + 2 * t, nvalid);
-              a[2] = cg_mask_rows(a[2], k0 + 2 * t + 8, nvalid);
-              a[3] = cg_mask_rows(a[3], k0 + 2 * t + 8, nvalid);
-            }
+            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+                         : "r"(pa + (((j + lane) & (8 * MT - 1)) << 4)));
             mma16816_rp(acc[m], a, b[2 * kk], b[2 * kk + 1]);
           }
         }
@@ -515,20 +495,41 @@ __global__ void __launch_bounds__(kCgThreads, 2) colgrad_group_kernel(const __gr
   }
 }
 
-// Pt[qrow][row] (bf16): qrow = 16m + j (j < 8: hi of rank 8m + j; j >= 8: lo of rank 8m + j - 8)
+// fragment blocks: block bi, lane (g, t), chunk j = k-step * MT + m holds the m16n8k16 A fragment of
+// k-step rows 16*ks + {2t, 2t+1, 2t+8, 2t+9}: regs (hi, lo, hi, lo) of rank q = 8m + g
 __global__ void colgrad_prep_kernel(const __grid_constant__ CgGroup grp) {
-  const CgProb& P = grp.pr[blockIdx.z];
-  if (P.pt == nullptr) return;
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  const int qrow = blockIdx.y;
-  if (row >= P.mpad || qrow >= 16 * grp.mt) return;
-  const int q = (qrow >> 4) * 8 + (qrow & 7);
-  const int M = grp.n_items * grp.s;
-  int src = row;  // Pt column -> activation row
-  if (P.pos) src = (row % P.pt_item < grp.s) ? (row / P.pt_item) * grp.s + row % P.pt_item : M;
-  const float v = (q < P.r && src < M) ? __ldg(P.p + (size_t)src * P.ldp + q) : 0.f;
-  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-  P.pt[(size_t)qrow * P.mpad + row] = (qrow & 8) ? __float2bfloat16_rn(v - __bfloat162float(hi)) : hi;
+  const CgProb& P = grp.pr[blockIdx.y];
+  const int MT = grp.mt, nw = 32 * 8 * MT * 4;  // words per block
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= P.nblocks * nw) return;
+  const int bi = e / nw, w = e % nw;
+  const int lane = w / (8 * MT * 4), pos = (w / 4) % (8 * MT), reg = w % 4;
+  const int j = (pos - lane) & (8 * MT - 1);  // logical chunk stored at rotated position pos
+  const int ks = j / MT, m = j % MT, g = lane >> 2, t = lane & 3;
+  const int q = 8 * m + g;
+  // block rows -> activation rows
+  int row_base, nvalid;
+  if (P.pos) {
+    const int nsb = (grp.s + kCgRows - 1) / kCgRows;
+    const int item = bi / nsb, sb = bi % nsb;
+    row_base = item * grp.s + sb * kCgRows;
+    nvalid = min(kCgRows, grp.s - sb * kCgRows);
+  } else {
+    row_base = bi * kCgRows;
+    nvalid = min(kCgRows, grp.n_items * grp.s - row_base);
+  }
+  const int k0 = ks * 16 + 2 * t + (reg >= 2 ? 8 : 0);
+  uint32_t word = 0;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int k = k0 + half;
+    float v = 0.f;
+    if (k < nvalid && q < P.r) v = P.p ? __ldg(P.p + (size_t)(row_base + k) * P.ldp + q) : 1.f;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    const __nv_bfloat16 out = (reg & 1) ? __float2bfloat16_rn(v - __bfloat162float(hi)) : hi;
+    word |= (uint32_t)__bfloat16_as_ushort(out) << (16 * half);
+  }
+  P.pt[e] = word;
 }
 
 // G(q, c) = scale * sum over splits (in order) of the partials, for the problems with splits > 1
@@ -554,8 +555,7 @@ static void cg_layout(const lx_colgrad_problem& q, int n_items, int s, CgProb& o
   o.rows_eff = gathered ? s : n_items * s;
   o.rows_per_split = gathered ? kCgRows : kCgRowsDense;
   o.splits = (o.rows_eff + o.rows_per_split - 1) / o.rows_per_split;
-  o.pt_item = (s + 7) / 8 * 8;
-  o.mpad = gathered ? n_items * o.pt_item : (n_items * s + 7) / 8 * 8;
+  o.nblocks = gathered ? n_items * ((s + kCgRows - 1) / kCgRows) : (n_items * s + kCgRows - 1) / kCgRows;
 }
 
 static int cg_mt(const lx_colgrad_problem* probs, int n) {
@@ -564,11 +564,11 @@ static int cg_mt(const lx_colgrad_problem* probs, int n) {
   return mr > 8 ? 2 : 1;
 }
 
-// floats: Pt (16*MT*mpad bf16 = 8*MT*mpad floats) + partials, each rounded to 64 floats (256 B)
+// floats: fragment blocks (32 * 8 * MT * 4 words per block) + partials, each rounded to 64 floats (256 B)
 static long long cg_ws_floats(const lx_colgrad_problem& q, int n_items, int s, int mt, long long* pt_floats) {
   CgProb o;
   cg_layout(q, n_items, s, o);
-  const long long pt = q.p ? (8LL * mt * o.mpad + 63) / 64 * 64 : 0;
+  const long long pt = (long long)o.nblocks * 32 * 8 * mt * 4;
   const long long part = o.splits > 1 ? ((long long)o.chunks * o.splits * q.r * kCgChunk + 63) / 64 * 64 : 0;
   if (pt_floats) *pt_floats = pt;
   return pt + part;
@@ -648,7 +648,7 @@ int lx_colgrad_group(const lx_colgrad_problem* probs, int n_probs, int n_items, 
   grp.s = s;
   grp.mt = cg_mt(probs, n_probs);
   const int M = n_items * s;
-  int units = 0, max_final = 0, max_mpad = 0;
+  int units = 0, max_final = 0, max_blk_words = 0;
   long long ws_off = 0;
   for (int i = 0; i < n_probs; ++i) {
     const lx_colgrad_problem& q = probs[i];
@@ -666,7 +666,7 @@ int lx_colgrad_group(const lx_colgrad_problem* probs, int n_probs, int n_items, 
     long long pt_floats = 0;
     const long long need = cg_ws_floats(q, n_items, s, grp.mt, &pt_floats);
     o.p = q.p;
-    o.pt = q.p ? reinterpret_cast<__nv_bfloat16*>(ws + ws_off) : nullptr;
+    o.pt = reinterpret_cast<uint32_t*>(ws + ws_off);
     o.ws = ws + ws_off + pt_floats;
     ws_off += need;
     o.pos = q.pos;
@@ -681,30 +681,26 @@ int lx_colgrad_group(const lx_colgrad_problem* probs, int n_probs, int n_items, 
     o.unit0 = units;
     units += o.chunks * o.splits;
     if (o.splits > 1) max_final = std::max(max_final, o.chunks * q.r * kCgChunk);
-    max_mpad = std::max(max_mpad, o.mpad);
+    max_blk_words = std::max(max_blk_words, o.nblocks * 32 * 8 * grp.mt * 4);
     int rc = q.pos ? make_tmap_bf16_2d_sw(&grp.tx[i], q.x, (uint64_t)q.ldx, (uint64_t)M, (uint64_t)q.ldx, 16, kCgRows,
                                           CU_TENSOR_MAP_SWIZZLE_32B)
                    : make_tmap_bf16_2d_sw(&grp.tx[i], q.x, (uint64_t)q.ncols, (uint64_t)M, (uint64_t)q.ldx, 64, kCgRows,
                                           CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
-    if (q.p) {
-      rc = make_tmap_bf16_2d_sw(&grp.tp[i], o.pt, (uint64_t)o.mpad, (uint64_t)(16 * grp.mt), (uint64_t)o.mpad, 64,
-                                16 * grp.mt, CU_TENSOR_MAP_SWIZZLE_128B);
-      if (rc) return rc;
-    }
   }
   grp.n_units = units;
   const int grid = std::max(std::min(units, 2 * num_sms()), (units + kCgMaxSlots - 1) / kCgMaxSlots);
   LX_REQUIRE((units + grid - 1) / grid <= kCgMaxSlots, LX_ERR_UNSUPPORTED, "colgrad_group: too many units");
-  colgrad_prep_kernel<<<dim3((max_mpad + 255) / 256, 16 * grp.mt, n_probs), 256, 0, stream>>>(grp);
+  colgrad_prep_kernel<<<dim3((max_blk_words + 255) / 256, n_probs), 256, 0, stream>>>(grp);
   int rc = launch_check("colgrad_prep");
   if (rc) return rc;
-  constexpr int smem = CgSmemL::kTotal;
   if (grp.mt == 2) {
+    constexpr int smem = CgSmemL<2>::kTotal;
     static cudaError_t attr = cudaFuncSetAttribute(colgrad_group_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     LX_CHECK_CUDA(attr);
     colgrad_group_kernel<2><<<grid, kCgThreads, smem, stream>>>(grp);
   } else {
+    constexpr int smem = CgSmemL<1>::kTotal;
     static cudaError_t attr = cudaFuncSetAttribute(colgrad_group_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     LX_CHECK_CUDA(attr);
     colgrad_group_kernel<1><<<grid, kCgThreads, smem, stream>>>(grp);
