@@ -137,6 +137,33 @@ int lx_pack_active_rows(const uint16_t* w, int d_ff, int d, int blk, int n_items
 int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const float* w, long long w_sk, long long w_sq,
                int r, float scale, const int32_t* counts, const int32_t* ids, int blk, float* y, int ldy, void* wpack_ws,
                lx_stream_t stream);
+/* lx_rowproj over a pre-packed W (lx_pack_params): wpack = [2][RP][K_full] bf16 (hi rows, then lo rows),
+ * W(k, q) = hi[q][k] + lo[q][k]; RP = 8 or 16 (r <= RP). Gathered (counts != NULL): packed k of item b maps to
+ * column ids[b][k/blk]*blk + k%blk of the full pack. yb (optional): bf16 copy of Y with row stride ldyb — the
+ * LoRA columns of a K-extended projection operand (lora_linear_forward's x A, sf/model.py:296-300). */
+int lx_rowproj_packed(const uint16_t* x, int ldx, int n_items, int s, int K, const uint16_t* wpack, int K_full, int RP,
+                      int r, float scale, const int32_t* counts, const int32_t* ids, int blk, float* y, int ldy,
+                      uint16_t* yb, int ldyb, lx_stream_t stream);
+
+/* Parameter packing after the optimizer step (sf/autograd.py:203-225 updates the fp32 trainables):
+ *   dst[i*dst_sr + j*dst_sc] = bf16(scale * src[i*src_sr + j*src_sc]),  i < rows, j < cols (element strides);
+ *   lo_off != 0 also writes the bf16 residual at dst + lo_off (hi/lo split of an fp32 factor).
+ * segs is a DEVICE array of n_segs segments (built once; the pointers stay valid across steps). */
+typedef struct lx_pack_segment {
+  const float* src;
+  long long src_sr;
+  long long src_sc;
+  int rows;
+  int cols;
+  uint16_t* dst;
+  long long dst_sr;
+  long long dst_sc;
+  long long lo_off;
+  float scale;
+  int pad_;
+} lx_pack_segment;
+int lx_pack_params(const lx_pack_segment* segs, int n_segs, lx_stream_t stream);
+
 /* Workspace for lx_rowproj's tensor-core path: W packed as bf16 hi/lo [items][2][R'][K] (gathered per item). */
 long long lx_rowproj_ws_bytes(int n_items, int K, int r, int gathered);
 
@@ -189,7 +216,8 @@ int lx_bsattn_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H, int
  * [n_items, H, ceil(s/128), hd] (per-key-tile column sums of K, used by dQ to cancel the bf16
  * row-sum residual of dS against the keys' common mode). dK/dV walk the CSC of each 128-key tile,
  * dQ the CSR of each 128-query tile (sf/block_sparse.py:63-137). */
-int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
+/* (ld: row stride of the fused qkv input; ld_d: row stride of the fused dqkv output.) */
+int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                      int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128, float scale,
                      const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv, lx_stream_t stream);
 /* Debug only: per-CTA clock64 phase stamps of the tcgen05 attention kernels into buf
@@ -206,7 +234,7 @@ int lx_bsattn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const
  * layernorm_forward (sf/model.py:307-312), fp32 residual in, bf16 out; saves mean/inv_std.
  * Optionally also writes the predictor's downsampled rows (sf/predictor.py:62-71) to x_small. */
 int lx_layernorm_fwd(const float* x, const uint16_t* delta, float* resid_out, int M, int d, const float* gamma,
-                     const float* beta, float eps, uint16_t* y, float* mean, float* inv_std, int s, int m_small,
+                     const float* beta, float eps, uint16_t* y, int ldy, float* mean, float* inv_std, int s, int m_small,
                      uint16_t* x_small, lx_stream_t stream);
 /* (delta != NULL: fused residual add — resid_out = x + delta (fp32) is normalised and returned.) */
 /* loss_forward + loss_backward over rows of fp32 logits (sf/model.py:454-472): row_loss[r] =

@@ -38,6 +38,8 @@ SIGNATURES: dict[str, list] = {
     "lx_neuron_fc1_dgrad": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P],
     "lx_rowproj": [_P, _I, _I, _I, _I, _P, _LL, _LL, _I, _F, _P, _P, _I, _P, _I, _P, _P],
     "lx_rowproj_ws_bytes": [_I, _I, _I, _I],
+    "lx_rowproj_packed": [_P, _I, _I, _I, _I, _P, _I, _I, _I, _F, _P, _P, _I, _P, _I, _P, _I, _P],
+    "lx_pack_params": [_P, _I, _P],
     "lx_colgrad_group_ws_floats": [_P, _I, _I, _I],
     "lx_colgrad_group": [_P, _I, _I, _I, _P, _P],
     "lx_attn_tables_size": [_I, _I, _I, _P],
@@ -45,9 +47,9 @@ SIGNATURES: dict[str, list] = {
     "lx_bsattn_fwd": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _I, _P, _P],
     "lx_bsattn_fwd_tc": [_P, _I, _I, _I, _I, _I, _P, _I, _P, _F, _P, _I, _P, _P],
     "lx_debug_set_attn_trace": [_P],
-    "lx_bsattn_bwd_tc": [_P, _I, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _F, _P, _P, _P, _P, _P],
+    "lx_bsattn_bwd_tc": [_P, _I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _F, _P, _P, _P, _P, _P],
     "lx_bsattn_bwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P, _P],
-    "lx_layernorm_fwd": [_P, _P, _P, _I, _I, _P, _P, _F, _P, _P, _P, _I, _I, _P, _P],
+    "lx_layernorm_fwd": [_P, _P, _P, _I, _I, _P, _P, _F, _P, _I, _P, _P, _I, _I, _P, _P],
     "lx_cross_entropy": [_P, _I, _I, _P, _F, _P, _P, _P],
     "lx_layernorm_bwd": [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P],
 }
@@ -60,6 +62,13 @@ class ColgradProblem(C.Structure):
 
     _fields_ = [("p", _P), ("ldp", _I), ("x", _P), ("ldx", _I), ("ncols", _I), ("r", _I), ("scale", _F), ("pos", _P),
                 ("blk", _I), ("g", _P), ("g_sq", _LL), ("g_sc", _LL)]
+
+
+class PackSegment(C.Structure):
+    """lx_pack_segment (include/sparseft_b200.h)."""
+
+    _fields_ = [("src", _P), ("src_sr", _LL), ("src_sc", _LL), ("rows", _I), ("cols", _I), ("dst", _P), ("dst_sr", _LL),
+                ("dst_sc", _LL), ("lo_off", _LL), ("scale", _F), ("pad_", _I)]
 
 
 _ERRORS = {1: E.ShapeError, 2: E.LayoutError, 3: E.MaskError, 4: E.PatternError, 5: E.CudaError, 6: E.UnsupportedError}

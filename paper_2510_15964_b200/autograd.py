@@ -24,7 +24,7 @@ from . import _abi
 from . import model as M
 from .block_sparse import attention_backward
 from .errors import GradientError
-from .neuron_ops import colgrad_group, colgrad_problem, rowproj
+from .neuron_ops import colgrad_group, colgrad_problem, rowproj, rowproj_packed
 
 
 def check_gradient_set(grads: dict, model: M.Model) -> None:
@@ -150,10 +150,14 @@ def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims
     if bitfit:
         cg.add(f"{prefix}b2", (d,), None, dO, d, 1, 1.0, 0, 1)
     ad1, ad2 = lora.get("w1"), lora.get("w2")
+    lp = lw.lora_pack or {}
     dax2 = None
     if ad2 is not None:
         r2 = ad2.rank
-        dax2 = rowproj(dO, B, s, d, ad2.b, 1, d, r2, scale=ad2.scaling)  # dO B2^T * s
+        if lp.get("b2") is not None:
+            dax2 = rowproj_packed(dO, B, s, d, lp["b2"], r2, scale=ad2.scaling)  # dO B2^T * s
+        else:
+            dax2 = rowproj(dO, B, s, d, ad2.b, 1, d, r2, scale=ad2.scaling)
         cg.add(f"{prefix}w2.lora_b", (r2, d), cache["ax2"], dO, d, r2, ad2.scaling, d, 1)
     dz = torch.empty_like(a)
     _abi.call("lx_neuron_fc2_dgrad", dO.data_ptr(), B, s, d, f, blk, lw.mlp.w2.data_ptr(), nm.counts.data_ptr(),
@@ -167,7 +171,10 @@ def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims
     if ad1 is not None:
         r1 = ad1.rank
         cg.add(f"{prefix}w1.lora_b", (r1, f), cache["ax1"], dz, f, r1, ad1.scaling, f, 1, masks=nm, blk=blk)
-        dax1 = rowproj(dz, B, s, f, ad1.b, 1, f, r1, scale=ad1.scaling, masks=nm, blk=blk)  # dz B1[:,cols]^T * s
+        if lp.get("b1") is not None:  # dz B1[:,cols]^T * s
+            dax1 = rowproj_packed(dz, B, s, f, lp["b1"], r1, scale=ad1.scaling, masks=nm, blk=blk)
+        else:
+            dax1 = rowproj(dz, B, s, f, ad1.b, 1, f, r1, scale=ad1.scaling, masks=nm, blk=blk)
         cg.add(f"{prefix}w1.lora_a", (d, r1), dax1, x2, d, r1, 1.0, 1, r1)
     dx = torch.empty(B * s, d, dtype=torch.bfloat16, device=dev)
     _abi.call("lx_neuron_fc1_dgrad", dz.data_ptr(), dz.stride(0), B, s, d, f, blk, lw.mlp.w1_t.data_ptr(),
@@ -203,23 +210,35 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
     if bitfit:
         cg.add(f"{prefix}bo", (d,), None, g, d, 1, 1.0, 0, 1)
     qkv = cache["qkv"]
-    dqkv = torch.empty_like(qkv)
+    ext = cache.get("ext", False)
+    tq, r = cache["lora_t"], cache["lora_r"]
+    kx = lw.lora_pack["kx"] if ext else 0
+    # K-extended: dqkv_ext = [dq dk dv | dAx (bf16)], so one GEMM gives dqkv W^T + dAx A_cat^T
+    dqkv_full = torch.empty(B * s, 3 * d + kx, dtype=torch.bfloat16, device=dev)
+    dqkv = dqkv_full[:, : 3 * d] if ext else dqkv_full
     scale = 1.0 / float(np.sqrt(hd))
     attention_backward(qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :], cache["o"], d_heads, 3 * d, B, s, H, hd,
                        cache["pidx"], cache["stride"], dp, scale, cache["lse"], dqkv[:, :d], dqkv[:, d : 2 * d],
                        dqkv[:, 2 * d :])
     x2 = cache["x"]
-    tq, r = cache["lora_t"], cache["lora_r"]
     dax = None
     if tq:
         dax = torch.empty(B * s, len(tq) * r, dtype=torch.float32, device=dev)
         for j, t in enumerate(tq):
             ad, sl = lora[t], M.QKV_SLOT[t]
-            rowproj(dqkv[:, sl * d : (sl + 1) * d], B, s, d, ad.b, 1, d, r, scale=ad.scaling, out=dax[:, j * r : (j + 1) * r])
-    # dx = dqkv W_qkv^T (cuBLAS) + dax A_cat^T (rank-n*r update)
-    dx = torch.mm(dqkv, lw.wqkv.t())
-    if tq:
-        dx.addmm_(dax.to(torch.bfloat16), cache["a_cat"].t().to(torch.bfloat16))
+            if ext:
+                rowproj_packed(dqkv[:, sl * d : (sl + 1) * d], B, s, d, lw.lora_pack["b"][t], r, scale=ad.scaling,
+                               out=dax[:, j * r : (j + 1) * r], out_bf16=dqkv_full[:, 3 * d + j * r : 3 * d + (j + 1) * r])
+            else:
+                rowproj(dqkv[:, sl * d : (sl + 1) * d], B, s, d, ad.b, 1, d, r, scale=ad.scaling,
+                        out=dax[:, j * r : (j + 1) * r])
+    if ext:
+        dx = torch.mm(dqkv_full, lw.wqkv_ext[:d, :].t())
+    else:
+        # dx = dqkv W_qkv^T (cuBLAS) + dax A_cat^T (rank-n*r update)
+        dx = torch.mm(dqkv, lw.wqkv.t())
+        if tq:
+            dx.addmm_(dax.to(torch.bfloat16), cache["a_cat"].t().to(torch.bfloat16))
     for j, t in enumerate(tq):
         ad, sl = lora[t], M.QKV_SLOT[t]
         cg.add(f"{prefix}{t}.lora_a", (d, r), dax[:, j * r : (j + 1) * r], x2, d, r, 1.0, 1, r)

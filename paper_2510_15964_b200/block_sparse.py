@@ -62,14 +62,18 @@ def attention_backward(q, k, v, o, d_o, ld: int, n_items: int, s: int, H: int, h
         raise LayoutError("attention_backward expects o and d_o with the same row stride")
     d = H * hd
     fused = (ld == 3 * d and k.data_ptr() == q.data_ptr() + 2 * d and v.data_ptr() == q.data_ptr() + 4 * d
-             and dk.data_ptr() == dq.data_ptr() + 2 * d and dv.data_ptr() == dq.data_ptr() + 4 * d and dq.stride(0) == ld)
+             and dk.data_ptr() == dq.data_ptr() + 2 * d and dv.data_ptr() == dq.data_ptr() + 4 * d
+             and dk.stride(0) == dq.stride(0) == dv.stride(0) >= 3 * d)
     if fused and hd in (64, 128) and dpool.tables128 is not None and USE_TCGEN05:
-        # tcgen05 dK/dV (CSC walk) + dQ (CSR walk) over 128x128 tiles (csrc/attn_sm100.cu)
+        # tcgen05 dK/dV (CSC walk) + dQ (CSR walk) over 128x128 tiles (csrc/attn_sm100.cu); dqkv may be the
+        # K-extended [M, 3d + kx] operand of the projection input-grad GEMM (row stride dq.stride(0))
         ksum = torch.empty(n_items, H, (s + 127) // 128, hd, dtype=torch.float32, device=dev)
-        _abi.call("lx_bsattn_bwd_tc", q.data_ptr(), ld, o.data_ptr(), d_o.data_ptr(), o.stride(0), n_items, s, H, hd,
+        _abi.call("lx_bsattn_bwd_tc", q.data_ptr(), ld, dq.stride(0), o.data_ptr(), d_o.data_ptr(), o.stride(0), n_items, s, H, hd,
                   pidx.data_ptr(), item_stride, dpool.tables128.data_ptr(), float(scale), lse.data_ptr(),
                   delta.data_ptr(), ksum.data_ptr(), dq.data_ptr(), _abi.stream_handle(dev))
         return
+    if dq.stride(0) != ld or dk.stride(0) != ld or dv.stride(0) != ld:
+        raise LayoutError("attention_backward (warp-MMA path) expects dq/dk/dv with the row stride of q")
     _abi.call("lx_bsattn_bwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), d_o.data_ptr(), ld, o.stride(0),
               n_items, s, H, hd,
               pidx.data_ptr(), item_stride, dpool.tables.data_ptr(), len(dpool.ids), float(scale), lse.data_ptr(),

@@ -878,7 +878,7 @@ __global__ void __launch_bounds__(256) bsattn_delta_tc_kernel(const __nv_bfloat1
 }
 
 template <int HD>
-static int launch_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
+static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                          int H, const int32_t* pidx, int item_stride, const int32_t* tables128, float scale,
                          const float* lse, float* delta, float* ksum, uint16_t* dqkv, cudaStream_t st) {
   const int rows = n_items * s;
@@ -899,10 +899,10 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const u
   dim3 grid((s + kAT - 1) / kAT, H, n_items);
   const float sl2 = scale * 1.4426950408889634f;
   bsattn_dkdv_tc_kernel<HD><<<grid, 192, smem, st>>>(tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
-                                                     lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld, ksum);
+                                                     lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);
   if ((rc = launch_check("bsattn_dkdv_tc"))) return rc;
   bsattn_dq_tc_kernel<HD><<<grid, 192, smem, st>>>(tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
-                                                   lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld, ksum);
+                                                   lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);
   return launch_check("bsattn_dq_tc");
 }
 
@@ -919,14 +919,14 @@ int lx_debug_set_attn_trace(unsigned long long* buf) {
   return 0;
 }
 
-int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
-                     int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128, float scale,
-                     const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv, lx_stream_t stream) {
-  LX_REQUIRE(ld >= 3 * H * hd && ld % 8 == 0 && ld_o % 8 == 0, LX_ERR_SHAPE,
+int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items,
+                     int s, int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128,
+                     float scale, const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv, lx_stream_t stream) {
+  LX_REQUIRE(ld >= 3 * H * hd && ld_d >= 3 * H * hd && ld % 8 == 0 && ld_d % 8 == 0 && ld_o % 8 == 0, LX_ERR_SHAPE,
              "attention bwd (tcgen05): qkv / dqkv must be fused [M, >= 3*H*hd] with 16B-aligned rows");
   switch (hd) {
-    case 64: return launch_bwd_tc<64>(qkv, ld, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, ksum_ws, dqkv, stream);
-    case 128: return launch_bwd_tc<128>(qkv, ld, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, ksum_ws, dqkv, stream);
+    case 64: return launch_bwd_tc<64>(qkv, ld, ld_d, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, ksum_ws, dqkv, stream);
+    case 128: return launch_bwd_tc<128>(qkv, ld, ld_d, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, ksum_ws, dqkv, stream);
     default: LX_REQUIRE(false, LX_ERR_UNSUPPORTED, "tcgen05 attention: head_dim %d unsupported (64, 128)", hd);
   }
 }

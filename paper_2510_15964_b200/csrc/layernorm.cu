@@ -153,15 +153,15 @@ LX_DEV float warp_sum(float v) {
 template <int VEC>
 __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const float* __restrict__ x, int M, int d,
                                                           const float* __restrict__ g, const float* __restrict__ b,
-                                                          float eps, __nv_bfloat16* __restrict__ y,
+                                                          float eps, __nv_bfloat16* __restrict__ y, int ldy,
                                                           float* __restrict__ mean_out, float* __restrict__ istd_out, int s,
                                                           int m_small, __nv_bfloat16* __restrict__ x_small,
                                                           const __nv_bfloat16* __restrict__ delta,
                                                           float* __restrict__ resid_out) {
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= M) return;
   const int nv = d / 4;
+#pragma unroll 1
+  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < M; row += gridDim.x * 8) {
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * d);
   const uint2* dr = delta ? reinterpret_cast<const uint2*>(delta + (size_t)row * d) : nullptr;
   float4 v[VEC];
@@ -215,9 +215,10 @@ __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const float* __restric
       const float4 gg = __ldg(g4 + c), bb = __ldg(b4 + c);
       const uint2 pk = make_uint2(pack_bf16x2((v[i].x - mu) * istd * gg.x + bb.x, (v[i].y - mu) * istd * gg.y + bb.y),
                                   pack_bf16x2((v[i].z - mu) * istd * gg.z + bb.z, (v[i].w - mu) * istd * gg.w + bb.w));
-      *reinterpret_cast<uint2*>(y + (size_t)row * d + 4 * c) = pk;
+      *reinterpret_cast<uint2*>(y + (size_t)row * ldy + 4 * c) = pk;
       if (xs_row) *reinterpret_cast<uint2*>(xs_row + 4 * c) = pk;
     }
+  }
   }
 }
 
@@ -226,11 +227,18 @@ __global__ void __launch_bounds__(256) ln_bwd_warp_kernel(const void* __restrict
                                                           const float* __restrict__ g, const float* __restrict__ mean,
                                                           const float* __restrict__ istd, int M, int d,
                                                           float* __restrict__ dx, __nv_bfloat16* __restrict__ dx_bf16) {
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= M) return;
   const int nv = d / 4;
+#pragma unroll 1
+  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < M; row += gridDim.x * 8) {
   const float mu = __ldg(mean + row), is = __ldg(istd + row);
+  float4* o = reinterpret_cast<float4*>(dx + (size_t)row * d);
+  float4 cur[VEC];  // the accumulator row is loaded with the inputs: one round trip per row
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = lane + 32 * i;
+    cur[i] = c < nv ? o[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   float4 gv[VEC], xh[VEC];
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -255,13 +263,6 @@ __global__ void __launch_bounds__(256) ln_bwd_warp_kernel(const void* __restrict
     s2 += (gv[i].x * xh[i].x + gv[i].y * xh[i].y) + (gv[i].z * xh[i].z + gv[i].w * xh[i].w);
   }
   const float mg = warp_sum(s1) / d, mgx = warp_sum(s2) / d;
-  float4* o = reinterpret_cast<float4*>(dx + (size_t)row * d);
-  float4 cur[VEC];
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) {
-    const int c = lane + 32 * i;
-    cur[i] = c < nv ? o[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
     const int c = lane + 32 * i;
@@ -276,13 +277,23 @@ __global__ void __launch_bounds__(256) ln_bwd_warp_kernel(const void* __restrict
             make_uint2(pack_bf16x2(cur[i].x, cur[i].y), pack_bf16x2(cur[i].z, cur[i].w));
     }
   }
+  }
+}
+
+// persistent grid for the warp-per-row kernels: as many 8-row CTAs as fit at once (no partial last wave)
+template <typename K>
+static int ln_grid(K kern, int M) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+  const int ctas = (M + 7) / 8;
+  return ctas < per_sm * num_sms() ? ctas : per_sm * num_sms();
 }
 
 template <int VEC>
 static void ln_fwd_warp(const float* x, const uint16_t* delta, float* resid_out, int M, int d, const float* gamma,
-                        const float* beta, float eps, uint16_t* y, float* mean, float* inv_std, int s, int m_small,
+                        const float* beta, float eps, uint16_t* y, int ldy, float* mean, float* inv_std, int s, int m_small,
                         uint16_t* x_small, cudaStream_t st) {
-  ln_fwd_warp_kernel<VEC><<<(M + 7) / 8, 256, 0, st>>>(x, M, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), mean,
+  ln_fwd_warp_kernel<VEC><<<ln_grid(ln_fwd_warp_kernel<VEC>, M), 256, 0, st>>>(x, M, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), ldy, mean,
                                                        inv_std, s > 0 ? s : 1, m_small,
                                                        reinterpret_cast<__nv_bfloat16*>(x_small),
                                                        reinterpret_cast<const __nv_bfloat16*>(delta), resid_out);
@@ -292,9 +303,9 @@ template <int VEC>
 static void ln_bwd_warp(const void* dy, int dy_is_f32, const float* x, const float* gamma, const float* mean,
                         const float* inv_std, int M, int d, float* dx, __nv_bfloat16* ob, cudaStream_t st) {
   if (dy_is_f32)
-    ln_bwd_warp_kernel<true, VEC><<<(M + 7) / 8, 256, 0, st>>>(dy, x, gamma, mean, inv_std, M, d, dx, ob);
+    ln_bwd_warp_kernel<true, VEC><<<ln_grid(ln_bwd_warp_kernel<true, VEC>, M), 256, 0, st>>>(dy, x, gamma, mean, inv_std, M, d, dx, ob);
   else
-    ln_bwd_warp_kernel<false, VEC><<<(M + 7) / 8, 256, 0, st>>>(dy, x, gamma, mean, inv_std, M, d, dx, ob);
+    ln_bwd_warp_kernel<false, VEC><<<ln_grid(ln_bwd_warp_kernel<false, VEC>, M), 256, 0, st>>>(dy, x, gamma, mean, inv_std, M, d, dx, ob);
 }
 
 }  // namespace lx
@@ -304,19 +315,21 @@ using namespace lx;
 extern "C" {
 
 int lx_layernorm_fwd(const float* x, const uint16_t* delta, float* resid_out, int M, int d, const float* gamma,
-                     const float* beta, float eps, uint16_t* y, float* mean, float* inv_std, int s, int m_small,
+                     const float* beta, float eps, uint16_t* y, int ldy, float* mean, float* inv_std, int s, int m_small,
                      uint16_t* x_small, lx_stream_t stream) {
   LX_REQUIRE(d % 4 == 0 && d <= kLnThreads * 4 * kLnMaxVec, LX_ERR_UNSUPPORTED, "layernorm: d=%d unsupported", d);
   LX_REQUIRE(M >= 1, LX_ERR_SHAPE, "layernorm: empty input");
   LX_REQUIRE(!delta || resid_out, LX_ERR_SHAPE, "layernorm: residual add needs resid_out");
   if (x_small) LX_REQUIRE(s >= 1 && m_small >= 1 && M % s == 0, LX_ERR_SHAPE, "layernorm: bad downsample shape");
+  LX_REQUIRE(ldy >= d && ldy % 4 == 0, LX_ERR_SHAPE, "layernorm: output row stride %d < d or not a multiple of 4", ldy);
   const int per_lane = (d / 4 + 31) / 32;  // float4 chunks per lane in the warp-per-row kernel
   if (per_lane <= 16) {
-    if (per_lane <= 4) ln_fwd_warp<4>(x, delta, resid_out, M, d, gamma, beta, eps, y, mean, inv_std, s, m_small, x_small, stream);
-    else if (per_lane <= 8) ln_fwd_warp<8>(x, delta, resid_out, M, d, gamma, beta, eps, y, mean, inv_std, s, m_small, x_small, stream);
-    else ln_fwd_warp<16>(x, delta, resid_out, M, d, gamma, beta, eps, y, mean, inv_std, s, m_small, x_small, stream);
+    if (per_lane <= 4) ln_fwd_warp<4>(x, delta, resid_out, M, d, gamma, beta, eps, y, ldy, mean, inv_std, s, m_small, x_small, stream);
+    else if (per_lane <= 8) ln_fwd_warp<8>(x, delta, resid_out, M, d, gamma, beta, eps, y, ldy, mean, inv_std, s, m_small, x_small, stream);
+    else ln_fwd_warp<16>(x, delta, resid_out, M, d, gamma, beta, eps, y, ldy, mean, inv_std, s, m_small, x_small, stream);
     return launch_check("layernorm_fwd");
   }
+  LX_REQUIRE(ldy == d, LX_ERR_UNSUPPORTED, "layernorm: strided output needs d <= 2048");
   ln_fwd_kernel<<<M, kLnThreads, 0, stream>>>(x, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), mean, inv_std,
                                               s > 0 ? s : 1, m_small, reinterpret_cast<__nv_bfloat16*>(x_small),
                                               reinterpret_cast<const __nv_bfloat16*>(delta), resid_out);

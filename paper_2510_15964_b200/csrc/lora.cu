@@ -154,11 +154,16 @@ __global__ void rowproj_wpack_kernel(const float* __restrict__ w, long long w_sk
 // flight each) and reduce through shared memory.
 constexpr int kRpWarps = 8, kRpU = 8;
 
+// W pack: wp + item * w_item_stride holds [2][RP][Kp] (hi, lo); with `ids` the pack is the FULL W
+// (shared by the items, w_item_stride 0) and packed k maps to ids[item][k / blk] * blk + k % blk.
+// yb (optional): bf16 copy of Y (the LoRA rows of a K-extended projection GEMM operand).
 template <int NT>
 __global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int s, int K,
                                                            int Kp, int r, float scale, const int32_t* __restrict__ counts,
                                                            int blk, const __nv_bfloat16* __restrict__ wp,
-                                                           float* __restrict__ y, int ldy) {
+                                                           long long w_item_stride, const int32_t* __restrict__ ids,
+                                                           int ids_stride, float* __restrict__ y, int ldy,
+                                                           __nv_bfloat16* __restrict__ yb, int ldyb) {
   constexpr int RP = 8 * NT;
   __shared__ float s_red[kRpWarps][16][RP + 1];
   const int item = blockIdx.y;
@@ -169,8 +174,9 @@ __global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_
   const int ra = row0 + g, rb = ra + 8;
   const __nv_bfloat16* xa = x + ((size_t)item * s + min(ra, s - 1)) * ldx + 8 * t;
   const __nv_bfloat16* xb = x + ((size_t)item * s + min(rb, s - 1)) * ldx + 8 * t;
-  const __nv_bfloat16* wh = wp + (size_t)item * 2 * RP * Kp + (size_t)g * Kp + 8 * t;  // row q = g (+8 per n-tile)
+  const __nv_bfloat16* wh = wp + (size_t)item * w_item_stride + (size_t)g * Kp;  // row q = g (+8 per n-tile)
   const __nv_bfloat16* wl = wh + (size_t)RP * Kp;
+  const int32_t* my_ids = ids ? ids + (size_t)item * ids_stride : nullptr;
   float acc[NT][4];
 #pragma unroll
   for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
@@ -187,10 +193,12 @@ __global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_
       const int kl = ok ? k0 : 0;
       va[u] = __ldg(reinterpret_cast<const uint4*>(xa + kl));
       vb[u] = __ldg(reinterpret_cast<const uint4*>(xb + kl));
+      int kw = kl + 8 * t;  // this lane's first k (8 consecutive k stay inside one neuron block)
+      if (my_ids) kw = ok ? __ldg(my_ids + kw / blk) * blk + kw % blk : 0;
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
-        vh[u][n] = __ldg(reinterpret_cast<const uint4*>(wh + (size_t)n * 8 * Kp + kl));
-        vl[u][n] = __ldg(reinterpret_cast<const uint4*>(wl + (size_t)n * 8 * Kp + kl));
+        vh[u][n] = __ldg(reinterpret_cast<const uint4*>(wh + (size_t)n * 8 * Kp + kw));
+        vl[u][n] = __ldg(reinterpret_cast<const uint4*>(wl + (size_t)n * 8 * Kp + kw));
       }
     }
     asm volatile("" ::: "memory");
@@ -231,7 +239,25 @@ __global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_
 #pragma unroll
       for (int w = 0; w < kRpWarps; ++w) v += s_red[w][rr][q];
       y[((size_t)item * s + row) * ldy + q] = v * scale;
+      if (yb) yb[((size_t)item * s + row) * ldyb + q] = __float2bfloat16_rn(v * scale);
     }
+  }
+}
+
+// ---------------------------------------------------------------- parameter packing
+// dst[i*dst_sr + j*dst_sc] = bf16(scale * src[i*src_sr + j*src_sc]) over a segment table (device memory);
+// lo_off != 0 also writes the bf16 residual (hi/lo split) at dst + lo_off. One launch refreshes every
+// LoRA factor's rowproj pack and K-extended projection rows after the optimizer step.
+__global__ void pack_params_kernel(const lx_pack_segment* __restrict__ segs) {
+  const lx_pack_segment sg = segs[blockIdx.y];
+  const long long n = (long long)sg.rows * sg.cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / sg.cols, j = e % sg.cols;
+    const float v = sg.scale * __ldg(sg.src + i * sg.src_sr + j * sg.src_sc);
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(sg.dst) + i * sg.dst_sr + j * sg.dst_sc;
+    *d = hi;
+    if (sg.lo_off) d[sg.lo_off] = __float2bfloat16_rn(v - __bfloat162float(hi));
   }
 }
 
@@ -611,13 +637,17 @@ int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const floa
       // dense W is shared by all items: index it as item 0 by treating the batch as one item
       grid = dim3((n_items * s + 15) / 16, 1);
       if (NT == 1)
-        rowproj_mma2_kernel<1><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb, y, ldy);
+        rowproj_mma2_kernel<1><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb,
+                                                                   2LL * 8 * Kp, nullptr, 0, y, ldy, nullptr, 0);
       else
-        rowproj_mma2_kernel<2><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb, y, ldy);
+        rowproj_mma2_kernel<2><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb,
+                                                                   2LL * 16 * Kp, nullptr, 0, y, ldy, nullptr, 0);
     } else if (NT == 1) {
-      rowproj_mma2_kernel<1><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, y, ldy);
+      rowproj_mma2_kernel<1><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, 2LL * 8 * Kp,
+                                                                 nullptr, 0, y, ldy, nullptr, 0);
     } else {
-      rowproj_mma2_kernel<2><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, y, ldy);
+      rowproj_mma2_kernel<2><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, 2LL * 16 * Kp,
+                                                                 nullptr, 0, y, ldy, nullptr, 0);
     }
     return launch_check("rowproj_mma");
   }
@@ -627,6 +657,38 @@ int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const floa
   else
     rowproj_kernel<16><<<grid, 256, 0, stream>>>(xb, ldx, s, K, w, w_sk, w_sq, r, scale, counts, ids, ids_stride, b, y, ldy);
   return launch_check("rowproj");
+}
+
+int lx_rowproj_packed(const uint16_t* x, int ldx, int n_items, int s, int K, const uint16_t* wpack, int K_full, int RP,
+                      int r, float scale, const int32_t* counts, const int32_t* ids, int blk, float* y, int ldy,
+                      uint16_t* yb, int ldyb, lx_stream_t stream) {
+  LX_REQUIRE(RP == 8 || RP == 16, LX_ERR_UNSUPPORTED, "rowproj_packed: RP must be 8 or 16");
+  LX_REQUIRE(r >= 1 && r <= RP, LX_ERR_UNSUPPORTED, "rowproj_packed: rank %d outside [1, RP]", r);
+  LX_REQUIRE(ldy >= r && (!yb || ldyb >= r), LX_ERR_SHAPE, "rowproj_packed: output stride < r");
+  LX_REQUIRE(K % 16 == 0 && K_full % 8 == 0 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                 (reinterpret_cast<uintptr_t>(wpack) & 15) == 0,
+             LX_ERR_SHAPE, "rowproj_packed: K % 16, 16B-aligned rows and pack required");
+  LX_REQUIRE(!counts || (ids && blk % 8 == 0 && K % blk == 0), LX_ERR_MASK, "rowproj_packed: gathered K needs ids, blk % 8");
+  LX_REQUIRE(counts || K <= K_full, LX_ERR_SHAPE, "rowproj_packed: K exceeds the pack");
+  const auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  const auto* wp = reinterpret_cast<const __nv_bfloat16*>(wpack);
+  auto* ybf = reinterpret_cast<__nv_bfloat16*>(yb);
+  const int items = counts ? n_items : 1, rows = counts ? s : n_items * s;
+  dim3 grid((rows + 15) / 16, items);
+  if (RP == 8)
+    rowproj_mma2_kernel<1><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, rows, K, K_full, r, scale, counts, counts ? blk : 1, wp,
+                                                               0, counts ? ids : nullptr, counts ? K / blk : 0, y, ldy, ybf, ldyb);
+  else
+    rowproj_mma2_kernel<2><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, rows, K, K_full, r, scale, counts, counts ? blk : 1, wp,
+                                                               0, counts ? ids : nullptr, counts ? K / blk : 0, y, ldy, ybf, ldyb);
+  return launch_check("rowproj_packed");
+}
+
+int lx_pack_params(const lx_pack_segment* segs, int n_segs, lx_stream_t stream) {
+  LX_REQUIRE(n_segs >= 0, LX_ERR_SHAPE, "pack_params: negative segment count");
+  if (n_segs == 0) return LX_OK;
+  pack_params_kernel<<<dim3(64, n_segs), 256, 0, stream>>>(segs);
+  return launch_check("pack_params");
 }
 
 long long lx_colgrad_group_ws_floats(const lx_colgrad_problem* probs, int n_probs, int n_items, int s) {

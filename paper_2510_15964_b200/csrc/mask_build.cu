@@ -108,9 +108,34 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
   for (int e = threadIdx.x; e < mm; e += blockDim.x) cell[e] = 0;
   for (int item = item0; item < item1; ++item) {
     __syncthreads();
-    for (int e = threadIdx.x; e < 2 * m * r; e += blockDim.x) {  // coalesced: consecutive threads, consecutive t
-      const int which = e / (m * r), rem = e % (m * r), i = rem / r, t = rem % r;
-      s_qk[(which * m + i) * rs + t] = proj[(size_t)(item * m + i) * ldp + (which ? H + h : h) * r + t];
+    if ((r & 3) == 0) {
+      // float4 loads, issued in batches of 8 before any store (one round trip per batch)
+      const int nq = 2 * m * (r / 4);
+      for (int e0 = threadIdx.x; e0 < nq; e0 += 8 * blockDim.x) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * blockDim.x;
+          if (e < nq) {
+            const int which = e / (m * (r / 4)), rem = e % (m * (r / 4)), i = rem / (r / 4), t4 = rem % (r / 4);
+            v[u] = __ldg(reinterpret_cast<const float4*>(proj + (size_t)(item * m + i) * ldp + (which ? H + h : h) * r) + t4);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * blockDim.x;
+          if (e < nq) {
+            const int which = e / (m * (r / 4)), rem = e % (m * (r / 4)), i = rem / (r / 4), t = 4 * (rem % (r / 4));
+            float* dst = s_qk + (which * m + i) * rs + t;
+            dst[0] = v[u].x; dst[1] = v[u].y; dst[2] = v[u].z; dst[3] = v[u].w;
+          }
+        }
+      }
+    } else {
+      for (int e = threadIdx.x; e < 2 * m * r; e += blockDim.x) {  // coalesced: consecutive threads, consecutive t
+        const int which = e / (m * r), rem = e % (m * r), i = rem / r, t = rem % r;
+        s_qk[(which * m + i) * rs + t] = proj[(size_t)(item * m + i) * ldp + (which ? H + h : h) * r + t];
+      }
     }
     __syncthreads();
     // S_hat = (X Wq)(X Wk)^T  (sf/predictor.py:74-76)
@@ -118,8 +143,17 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
       const int i = e / m, j = e % m;
       const float* qr = s_qk + i * rs;
       const float* kr = s_qk + (m + j) * rs;
-      float acc = 0.f;
-      for (int t = 0; t < r; ++t) acc = fmaf(qr[t], kr[t], acc);
+      // four independent partial sums (ILP); fixed combination order -> deterministic
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      int t = 0;
+      for (; t + 4 <= r; t += 4) {
+        a0 = fmaf(qr[t], kr[t], a0);
+        a1 = fmaf(qr[t + 1], kr[t + 1], a1);
+        a2 = fmaf(qr[t + 2], kr[t + 2], a2);
+        a3 = fmaf(qr[t + 3], kr[t + 3], a3);
+      }
+      for (; t < r; ++t) a0 = fmaf(qr[t], kr[t], a0);
+      const float acc = (a0 + a1) + (a2 + a3);
       s_hat[e] = acc;
       if (dump) dump[((size_t)item * H + h) * mm + e] = acc;
     }
@@ -141,34 +175,31 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
     for (int e = threadIdx.x; e < mm; e += blockDim.x) cell[e] |= (s_hat[e] > thr) ? 1 : 0;  // OR over batch
     __syncthreads();
   }
-  // upsample (sf/predictor.py:79-84) + integer coverage counts per pattern (sf/exposer.py:71-85)
+  // upsample (sf/predictor.py:79-84) + integer coverage counts per pattern (sf/exposer.py:71-85):
+  // block-wide predicate counts (__syncthreads_count), cells in chunks of blockDim
   if (threadIdx.x < (kMaxPool + 1) * 2) (&s_cnt[0][0])[threadIdx.x] = 0ull;
   __syncthreads();
-  unsigned long long mass[kMaxPool], nnz[kMaxPool], total = 0;
-  for (int p = 0; p < kMaxPool; ++p) mass[p] = nnz[p] = 0;
   const int cells = n_b * n_b;
-  for (int e = threadIdx.x; e < cells; e += blockDim.x) {
-    int i = e / n_b, j = e % n_b;
-    int si = min((int)(((long long)i * m) / n_b), m - 1);
-    int sj = min((int)(((long long)j * m) / n_b), m - 1);
-    bool on = cell[si * m + sj] != 0;
-    total += on;
-    for (int p = 0; p < n_pool; ++p) {
-      bool in = pool_member(pool_kind[p], pool_param[p], i, j);
-      nnz[p] += in;
-      mass[p] += (in && on);
+  for (int e0 = 0; e0 < cells; e0 += blockDim.x) {
+    const int e = e0 + threadIdx.x;
+    bool on = false;
+    int i = 0, j = 0;
+    if (e < cells) {
+      i = e / n_b;
+      j = e % n_b;
+      const int si = min((int)(((long long)i * m) / n_b), m - 1);
+      const int sj = min((int)(((long long)j * m) / n_b), m - 1);
+      on = cell[si * m + sj] != 0;
     }
-  }
-  // warp-reduce the integer counts, then one shared atomic per warp and counter
-  {
-    const unsigned t32 = __reduce_add_sync(0xffffffffu, (unsigned)total);
-    if ((threadIdx.x & 31) == 0 && t32) atomicAdd(&s_cnt[kMaxPool][0], (unsigned long long)t32);
+    const int tot_c = __syncthreads_count(on);
+    if (threadIdx.x == 0) s_cnt[kMaxPool][0] += (unsigned long long)tot_c;
     for (int p = 0; p < n_pool; ++p) {
-      const unsigned m32 = __reduce_add_sync(0xffffffffu, (unsigned)mass[p]);
-      const unsigned n32 = __reduce_add_sync(0xffffffffu, (unsigned)nnz[p]);
-      if ((threadIdx.x & 31) == 0) {
-        if (m32) atomicAdd(&s_cnt[p][0], (unsigned long long)m32);
-        if (n32) atomicAdd(&s_cnt[p][1], (unsigned long long)n32);
+      const bool in = e < cells && pool_member(__ldg(pool_kind + p), __ldg(pool_param + p), i, j);
+      const int n_in = __syncthreads_count(in);
+      const int n_mass = __syncthreads_count(in && on);
+      if (threadIdx.x == 0) {
+        s_cnt[p][0] += (unsigned long long)n_mass;
+        s_cnt[p][1] += (unsigned long long)n_in;
       }
     }
   }

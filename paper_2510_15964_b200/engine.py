@@ -53,6 +53,7 @@ class FinetuneEngine:
             off = (p.data_ptr() - base) // 4
             self._grad_views[name] = self.flat_grad[off : off + p.numel()].view(p.shape)
         self.last_masks = None
+        M.ensure_lora_packs(model)  # packed LoRA operands, refreshed at the start of every step
 
     # -------------------------------------------------------------- one step (capturable)
     def _step(self, tokens: torch.Tensor) -> torch.Tensor:
@@ -60,6 +61,7 @@ class FinetuneEngine:
         B, s1 = tokens.shape
         s = s1 - 1
         inp, tgt = tokens[:, :-1], tokens[:, 1:].reshape(-1)
+        M.refresh_lora_packs(m)  # one launch: LoRA factors (updated by Adam) -> bf16 packs / K-extended rows
         h = m.weights.emb[inp].float()
         caches = []
         for layer in range(m.dims.n_layers):

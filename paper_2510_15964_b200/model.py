@@ -30,7 +30,7 @@ import torch
 from . import _abi, neuron_ops
 from .block_sparse import attention_forward
 from .errors import ShapeError
-from .neuron_ops import LayeredWeights, NeuronMasks, lower_mask, rowproj
+from .neuron_ops import LayeredWeights, NeuronMasks, lower_mask, rowproj, rowproj_packed
 from .patterns import DevicePool, LayoutTable, build_pool, device_pool
 
 LORA_TARGET_SHAPES = {"wq": "attn", "wk": "attn", "wv": "attn", "wo": "attn", "w1": "mlp_in", "w2": "mlp_out"}
@@ -108,6 +108,12 @@ class LayerWeights:
     ln1_b: torch.Tensor
     ln2_g: torch.Tensor
     ln2_b: torch.Tensor
+    # K-extended q/k/v projection [d + kx, 3d + kx] (wqkv is its [:d, :3d] view): rows d.. hold s*B of the
+    # LoRA targets, columns 3d.. hold their A, so one GEMM applies x W + s (xA) B and one dx GEMM adds
+    # dAx A^T (sf/model.py:292-304, sf/autograd.py:48-58). Set by ensure_lora_packs.
+    wqkv_ext: torch.Tensor | None = None
+    lora_pack: dict | None = None
+
     @property
     def d(self) -> int:
         return self.wo.shape[0]
@@ -328,6 +334,91 @@ def frozen_hash(model: Model) -> str:
     return h.hexdigest()
 
 
+# ---------------------------------------------------------------- LoRA packs
+
+
+def _rp(r: int) -> int:
+    return 8 if r <= 8 else 16
+
+
+def ensure_lora_packs(model: Model) -> bool:
+    """Build (once per parameter storage) the packed LoRA operands of every layer: rowproj packs
+    (bf16 hi/lo [2][RP][K], lx_pack_params layout) of A_cat (q/k/v targets), each q/k/v B, A1, A2, B1, B2,
+    and the K-extended q/k/v weight. Returns True when packs are live (refresh_lora_packs fills them).
+    The fused q/k/v path needs equal ranks r % 8 == 0 with n * r <= 16 (cfg3: wq, wv at r = 8)."""
+    if model.peft_method != "lora" or not model.lora:
+        return False
+    keys = sorted(model.lora)
+    ptrs = tuple((model.lora[k].a.data_ptr(), model.lora[k].b.data_ptr()) for k in keys)
+    st = model.__dict__.get("_lora_packs")
+    if st is not None and st["ptrs"] == ptrs:
+        return True
+    if torch.cuda.is_available() and torch.cuda.is_current_stream_capturing():
+        raise RuntimeError("ensure_lora_packs must run before CUDA-graph capture")
+    dev, d = model.device, model.dims.d_model
+    segs = []
+
+    def seg(src: torch.Tensor, src_sr, src_sc, rows, cols, dst: torch.Tensor, dst_off, dst_sr, dst_sc, lo_off, scale=1.0):
+        segs.append(_abi.PackSegment(src.data_ptr(), src_sr, src_sc, rows, cols, dst.data_ptr() + 2 * dst_off, dst_sr,
+                                     dst_sc, lo_off, float(scale), 0))
+
+    def pack_a(a: torch.Tensor, K: int):  # W(k, q) = A[k][q], A [K, r]
+        r = a.shape[1]
+        rp = _rp(r)
+        t = torch.zeros(2, rp, K, dtype=torch.bfloat16, device=dev)
+        seg(a, 1, r, r, K, t, 0, K, 1, rp * K)
+        return t
+
+    def pack_b(b: torch.Tensor, K: int):  # W(k, q) = B[q][k], B [r, K]
+        r = b.shape[0]
+        rp = _rp(r)
+        t = torch.zeros(2, rp, K, dtype=torch.bfloat16, device=dev)
+        seg(b, K, 1, r, K, t, 0, K, 1, rp * K)
+        return t
+
+    for i, lw in enumerate(model.weights.layers):
+        lora = {t: model.lora[(i, t)] for t in model.lora_targets if (i, t) in model.lora}
+        tq = tuple(t for t in ("wq", "wk", "wv") if t in lora)
+        ranks = {lora[t].rank for t in tq}
+        kx = 0
+        if tq and len(ranks) == 1 and next(iter(ranks)) % 8 == 0 and len(tq) * next(iter(ranks)) <= 16:
+            kx = len(tq) * next(iter(ranks))
+        lp = {"kx": kx, "tq": tq, "b": {}}
+        if kx:
+            r = kx // len(tq)
+            if lw.wqkv_ext is None or lw.wqkv_ext.shape != (d + kx, 3 * d + kx):
+                ext = torch.zeros(d + kx, 3 * d + kx, dtype=torch.bfloat16, device=dev)
+                ext[:d, : 3 * d] = lw.wqkv
+                lw.wqkv_ext, lw.wqkv = ext, ext[:d, : 3 * d]
+            ext, ld = lw.wqkv_ext, 3 * d + kx
+            a_qkv = torch.zeros(2, kx, d, dtype=torch.bfloat16, device=dev)
+            for j, t in enumerate(tq):
+                ad, sl = lora[t], QKV_SLOT[t]
+                seg(ad.a, 1, r, r, d, a_qkv, j * r * d, d, 1, kx * d)  # rowproj pack rows j*r..
+                seg(ad.b, d, 1, r, d, ext, (d + j * r) * ld + sl * d, ld, 1, 0, ad.scaling)  # s * B_j rows
+                seg(ad.a, r, 1, d, r, ext, 3 * d + j * r, ld, 1, 0)  # A_j columns (input-grad GEMM)
+                lp["b"][t] = pack_b(ad.b, d)
+            lp["a_qkv"] = a_qkv
+        if "w1" in lora and lora["w1"].rank <= 16:
+            lp["a1"] = pack_a(lora["w1"].a, d)
+            lp["b1"] = pack_b(lora["w1"].b, model.dims.d_ff)
+        if "w2" in lora and lora["w2"].rank <= 16:
+            lp["a2"] = pack_a(lora["w2"].a, model.dims.d_ff)
+            lp["b2"] = pack_b(lora["w2"].b, d)
+        lw.lora_pack = lp
+    arr = (_abi.PackSegment * max(len(segs), 1))(*segs)
+    host = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8)
+    model.__dict__["_lora_packs"] = {"ptrs": ptrs, "segs": host.to(dev), "n": len(segs)}
+    return True
+
+
+def refresh_lora_packs(model: Model) -> None:
+    """One launch: re-pack every LoRA factor after the optimizer step (stream-ordered, graph-capturable)."""
+    st = model.__dict__.get("_lora_packs")
+    if st is not None and st["n"]:
+        _abi.call("lx_pack_params", st["segs"].data_ptr(), st["n"], _abi.stream_handle(model.device))
+
+
 # ---------------------------------------------------------------- forward passes
 
 
@@ -378,7 +469,7 @@ class PendingResidual:
         return (self.base.reshape(-1, self.base.shape[-1]) + self.delta.float()).view(self.base.shape)
 
 
-def layernorm_forward(x, gamma, beta, eps: float = 1e-5, x_small_spec=None, delta=None):
+def layernorm_forward(x, gamma, beta, eps: float = 1e-5, x_small_spec=None, delta=None, ext_cols: int = 0):
     """sf/model.py:307-312 on the fused kernel; x fp32 [M, d] -> bf16 y. x_small_spec=(s, m)
     additionally writes the predictor's downsampled rows (returned in the cache). With `delta`
     (bf16 [M, d]) -- or x a PendingResidual -- the residual add x + delta is fused: the fp32 sum
@@ -387,7 +478,8 @@ def layernorm_forward(x, gamma, beta, eps: float = 1e-5, x_small_spec=None, delt
         x, delta = x.base, x.delta
     x2 = x.reshape(-1, x.shape[-1]).contiguous()
     M, d = x2.shape
-    y = torch.empty(M, d, dtype=torch.bfloat16, device=x2.device)
+    y_ext = torch.empty(M, d + ext_cols, dtype=torch.bfloat16, device=x2.device)  # + LoRA columns of a K-extended GEMM
+    y = y_ext[:, :d] if ext_cols else y_ext
     mean = torch.empty(M, dtype=torch.float32, device=x2.device)
     istd = torch.empty(M, dtype=torch.float32, device=x2.device)
     resid = torch.empty(M, d, dtype=torch.float32, device=x2.device) if delta is not None else None
@@ -396,8 +488,10 @@ def layernorm_forward(x, gamma, beta, eps: float = 1e-5, x_small_spec=None, delt
         s, m = x_small_spec
         xs = torch.empty(M // s * m, d, dtype=torch.bfloat16, device=x2.device)
     _abi.call("lx_layernorm_fwd", x2.data_ptr(), _abi.ptr(delta), _abi.ptr(resid), M, d, gamma.data_ptr(), beta.data_ptr(),
-              float(eps), y.data_ptr(), mean.data_ptr(), istd.data_ptr(), s, m, _abi.ptr(xs), _abi.stream_handle(x2.device))
-    return y, {"x": resid if resid is not None else x2, "mean": mean, "inv_std": istd, "gamma": gamma, "x_small": xs}
+              float(eps), y.data_ptr(), y_ext.stride(0), mean.data_ptr(), istd.data_ptr(), s, m, _abi.ptr(xs),
+              _abi.stream_handle(x2.device))
+    return y, {"x": resid if resid is not None else x2, "mean": mean, "inv_std": istd, "gamma": gamma, "x_small": xs,
+               "y_ext": y_ext if ext_cols else None}
 
 
 def adapter_forward(x: torch.Tensor, ad: AdapterLayer):
@@ -460,7 +554,8 @@ def _qkv_lora(lora: dict, d: int):
     return tq, a_cat, r
 
 
-def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: ModelDims, counter=None, *, dpool=None):
+def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: ModelDims, counter=None, *, dpool=None,
+                x_ext=None):
     """Block-sparse multi-head attention (sf/model.py:322-360). x: LN1 output bf16 [B, s, d] (or [s, d]).
     The dense projections are plain library GEMMs (cuBLAS, bias in the addmm); each LoRA delta
     s*(xA)B is a rank-r cuBLAS update of its column slice with xA from the skinny rowproj kernel.
@@ -471,9 +566,17 @@ def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: Mode
     dp = dpool if dpool is not None else device_pool(pool, x2.device, dims.seq_len, dims.attn_blk)
     pidx, stride = resolve_head_patterns(head_patterns, dp, B, H, x2.device)
     tq, a_cat, r = _qkv_lora(lora, d)
-    qkv = torch.addmm(lw.bqkv.to(torch.bfloat16), x2, lw.wqkv)  # bf16 [M, 3d]
+    lp = lw.lora_pack
+    ext = bool(tq) and x_ext is not None and lp is not None and lp["kx"] > 0 and lp["tq"] == tuple(tq)
     ax = None
-    if tq:
+    if ext:
+        # K-extended projection: x_ext = [x | xA_cat] (bf16 LoRA columns written by the rowproj), W_ext rows d.. = s*B
+        kx = lp["kx"]
+        ax = rowproj_packed(x_ext, B, s, d, lp["a_qkv"], kx, out_bf16=x_ext[:, d:])  # fp32 [M, n*r] for the LoRA grads
+        qkv = torch.addmm(lw.bqkv.to(torch.bfloat16), x_ext, lw.wqkv_ext[: d + kx, : 3 * d])
+    else:
+        qkv = torch.addmm(lw.bqkv.to(torch.bfloat16), x2, lw.wqkv)  # bf16 [M, 3d]
+    if tq and not ext:
         ax = rowproj(x2, B, s, d, a_cat, a_cat.shape[1], 1, a_cat.shape[1])  # fp32 [M, n*r] (kept for the LoRA grads)
         axb = ax.to(torch.bfloat16)
         for j, t in enumerate(tq):
@@ -491,7 +594,7 @@ def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: Mode
         ax_o = rowproj(o, B, s, d, ad_o.a, ad_o.rank, 1, ad_o.rank)
         out.addmm_(ax_o.to(torch.bfloat16), (ad_o.b * ad_o.scaling).to(torch.bfloat16))
     cache = {"x": x2, "qkv": qkv, "o": o, "lse": lse, "pidx": pidx, "stride": stride, "ax": ax, "lora_t": tq,
-             "lora_r": r, "a_cat": a_cat, "ax_o": ax_o, "n_items": B, "s": s, "dpool": dp}
+             "lora_r": r, "a_cat": a_cat, "ax_o": ax_o, "n_items": B, "s": s, "dpool": dp, "ext": ext}
     return out, cache
 
 
@@ -512,11 +615,22 @@ def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, c
     # active rows of W1^T and W2 packed per item once per layer; reused by the backward's input-grads
     w1p = neuron_ops.pack_active_rows(lw.mlp.w1_t, nm)
     w2p = neuron_ops.pack_active_rows(lw.mlp.w2, nm)
-    ax1 = rowproj(x2, B, s, d, ad1.a, ad1.rank, 1, ad1.rank) if ad1 is not None else None
+    lp = lw.lora_pack
+    if ad1 is None:
+        ax1 = None
+    elif lp is not None and lp.get("a1") is not None:
+        ax1 = rowproj_packed(x2, B, s, d, lp["a1"], ad1.rank)
+    else:
+        ax1 = rowproj(x2, B, s, d, ad1.a, ad1.rank, 1, ad1.rank)
     hid = neuron_ops.neuron_matmul_fwd1(x2.view(B, s, d), lw.mlp, nm, blk, counter, bias=lw.b1, ax=ax1,
                                         lora_b=ad1.b if ad1 else None, lora_r=ad1.rank if ad1 else 0,
                                         scaling=ad1.scaling if ad1 else 1.0, relu=True, w_packed=w1p)
-    ax2 = rowproj(hid.values, B, s, f, ad2.a, ad2.rank, 1, ad2.rank, masks=nm, blk=blk) if ad2 is not None else None
+    if ad2 is None:
+        ax2 = None
+    elif lp is not None and lp.get("a2") is not None:
+        ax2 = rowproj_packed(hid.values, B, s, f, lp["a2"], ad2.rank, masks=nm, blk=blk)
+    else:
+        ax2 = rowproj(hid.values, B, s, f, ad2.a, ad2.rank, 1, ad2.rank, masks=nm, blk=blk)
     out = neuron_ops.neuron_matmul_fwd2(
         hid, lw.mlp, None, counter, bias=lw.b2, ax=ax2, lora_b=ad2.b if ad2 else None, lora_r=ad2.rank if ad2 else 0,
         scaling=ad2.scaling if ad2 else 1.0, resid=resid, w_packed=w2p,
@@ -542,7 +656,8 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
         from .predictor import downsample_indices
 
         spec = (s, len(downsample_indices(s)))
-    h1, c1 = layernorm_forward(x, lw.ln1_g, lw.ln1_b, x_small_spec=spec)
+    kx = lw.lora_pack["kx"] if (model.peft_method == "lora" and lw.lora_pack is not None) else 0
+    h1, c1 = layernorm_forward(x, lw.ln1_g, lw.ln1_b, x_small_spec=spec, ext_cols=kx)
     h1v = h1.view(B, s, d)
     if static:
         hp = masks.head_patterns
@@ -552,7 +667,7 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
         hp = masks.attn_patterns(layer, h1v)
     adapter = model.peft_method == "adapter"
     x2 = c1["x"]  # the block input (materialised by LN1 when x was a pending residual)
-    att, ca = mha_forward(h1v, lw, lora, hp, model.pool, model.dims, counter, dpool=model.dpool)
+    att, ca = mha_forward(h1v, lw, lora, hp, model.pool, model.dims, counter, dpool=model.dpool, x_ext=c1["y_ext"])
     caa = None
     if adapter:
         att, caa = adapter_forward(att.float(), model.adapters[(layer, "attn")])
@@ -586,6 +701,8 @@ def model_forward(model: Model, tokens, masks, counter=None):
     if int(tok.max()) >= model.dims.vocab or int(tok.min()) < 0:
         raise ValueError("token id out of vocab range")
     B, s = tok.shape
+    if ensure_lora_packs(model):
+        refresh_lora_packs(model)
     h = model.weights.emb[tok].float()
     caches = []
     for layer in range(model.dims.n_layers):

@@ -259,6 +259,20 @@ def rowproj(x2: torch.Tensor, n_items: int, s: int, K: int, w: torch.Tensor, w_s
     return y
 
 
+def rowproj_packed(x2: torch.Tensor, n_items: int, s: int, K: int, wpack: torch.Tensor, r: int, scale: float = 1.0,
+                   masks: NeuronMasks | None = None, blk: int = 1, out: torch.Tensor | None = None,
+                   out_bf16: torch.Tensor | None = None) -> torch.Tensor:
+    """Y[M, r] = scale * X[M, K] W over a pre-packed W (lx_pack_params layout [2][RP][K_full], hi then lo);
+    K gathered per item through `masks` (packed k -> ids[b][k/blk]*blk + k%blk of the full pack).
+    `out_bf16` (optional, row-strided) receives a bf16 copy of Y."""
+    y = out if out is not None else torch.empty(x2.shape[0], r, dtype=torch.float32, device=x2.device)
+    _abi.call("lx_rowproj_packed", x2.data_ptr(), x2.stride(0), n_items, s, K, wpack.data_ptr(), wpack.shape[2],
+              wpack.shape[1], r, float(scale), _abi.ptr(masks.counts if masks else None),
+              _abi.ptr(masks.ids if masks else None), blk, y.data_ptr(), y.stride(0), _abi.ptr(out_bf16),
+              out_bf16.stride(0) if out_bf16 is not None else 0, _abi.stream_handle(x2.device))
+    return y
+
+
 def colgrad_problem(p: torch.Tensor | None, x2: torch.Tensor, ncols: int, r: int, scale: float, out: torch.Tensor,
                     g_sq: int, g_sc: int, masks: NeuronMasks | None = None, blk: int = 1):
     """One G(q, c) = scale * sum_rows P[row, q] X[row, c] problem (c original column) for colgrad_group.
