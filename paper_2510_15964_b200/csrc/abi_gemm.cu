@@ -1,4 +1,5 @@
 // C-ABI: generic tcgen05 GEMM and the neuron-sparse MLP GEMMs (K2).
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -13,6 +14,14 @@ void set_error(const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("LX_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 int num_sms() {
@@ -80,7 +89,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   LX_REQUIRE(args.n_items >= 1 && args.n_items <= kMaxItems, LX_ERR_UNSUPPORTED, "n_items must be in [1, %d]", kMaxItems);
   LX_REQUIRE(args.lora_r >= 0 && args.lora_r <= kMaxR, LX_ERR_UNSUPPORTED, "LoRA rank must be <= %d", kMaxR);
   if (CTAS == 1) {
-    kern<<<num_sms(), kGemmThreads, smem, st>>>(ta, tb, args);
+    launch_k(kern, num_sms(), kGemmThreads, smem, st, ta, tb, args);
     return launch_check("gemm_sm100");
   }
   cudaLaunchConfig_t cfg = {};
@@ -88,13 +97,15 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   LX_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, args));
   return launch_check("gemm_sm100 (cta pair)");
 }
@@ -126,6 +137,7 @@ static GemmArgs base_args(int n_items, int rows, int n_dense, int k_dense) {
 __global__ void __launch_bounds__(256) pack_rows_kernel(const uint4* __restrict__ w, int d16, int d_ff, int blk,
                                                         const int32_t* __restrict__ counts, const int32_t* __restrict__ ids,
                                                         uint4* __restrict__ packed) {
+  pdl_wait_trigger();
   const int item = blockIdx.y;
   const int prow = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (prow >= __ldg(counts + item) * blk) return;
@@ -356,7 +368,7 @@ int lx_pack_active_rows(const uint16_t* w, int d_ff, int d, int blk, int n_items
                         const int32_t* ids, uint16_t* packed, lx_stream_t stream) {
   LX_REQUIRE(d % 8 == 0 && d_ff % blk == 0, LX_ERR_SHAPE, "pack_active_rows: d %% 8 and d_ff %% blk required");
   dim3 grid((d_ff + 7) / 8, n_items);
-  pack_rows_kernel<<<grid, 256, 0, stream>>>(reinterpret_cast<const uint4*>(w), d / 8, d_ff, blk, counts, ids,
+  launch_k(pack_rows_kernel, grid, 256, 0, stream, reinterpret_cast<const uint4*>(w), d / 8, d_ff, blk, counts, ids,
                                              reinterpret_cast<uint4*>(packed));
   return launch_check("pack_active_rows");
 }

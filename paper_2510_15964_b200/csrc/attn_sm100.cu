@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(AttnFwdSmem<HD>::kThreads, AttnFwdSmem<HD>::kC
 bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, int d_model,
                      const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                      float scale_log2, __nv_bfloat16* __restrict__ o, int ldo, float* __restrict__ lse, int n_units) {
+  pdl_wait_trigger();
   using L = AttnFwdSmem<HD>;
   constexpr int A = L::kAtoms;
   extern __shared__ uint8_t smem_raw[];
@@ -399,7 +400,7 @@ static int launch_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H,
   LX_CHECK_CUDA(attr);
   const int n_units = ((s + kAT - 1) / kAT) * H * n_items;
   const int grid = n_units < AttnFwdSmem<HD>::kCtas * num_sms() ? n_units : AttnFwdSmem<HD>::kCtas * num_sms();
-  bsattn_fwd_tc_kernel<HD><<<grid, AttnFwdSmem<HD>::kThreads, smem, st>>>(tm, s, H, H * HD, pidx, item_stride, tables128,
+  launch_k(bsattn_fwd_tc_kernel<HD>, grid, AttnFwdSmem<HD>::kThreads, smem, st, tm, s, H, H * HD, pidx, item_stride, tables128,
                                                     scale * 1.4426950408889634f, reinterpret_cast<__nv_bfloat16*>(o), ldo,
                                                     lse, n_units);
   return launch_check("bsattn_fwd_tc");
@@ -427,6 +428,7 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
                       int d_model, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                       float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
                       __nv_bfloat16* __restrict__ dkv, int ld_dkv, float* __restrict__ ksum) {
+  pdl_wait_trigger();
   using L = AttnBwdSmem<HD>;
   constexpr int A = HD / 64;
   constexpr int kTmem = tmem_cols_pow2(kAT + 2 * HD);
@@ -650,6 +652,7 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
                     int d_model, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                     float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
                     __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ ksum) {
+  pdl_wait_trigger();
   using L = AttnBwdSmem<HD>;  // [Q | dO] [kSt x (K | V)] [kbar]
   constexpr int A = HD / 64;
   constexpr int kTmem = tmem_cols_pow2(kAT + HD);
@@ -838,6 +841,7 @@ template <int HD>
 __global__ void __launch_bounds__(256) bsattn_delta_tc_kernel(const __nv_bfloat16* __restrict__ o,
                                                               const __nv_bfloat16* __restrict__ d_o, int ld,
                                                               int n_rows_total, int s, int H, float* __restrict__ delta) {
+  pdl_wait_trigger();
   constexpr int G = HD / 8;  // lanes per head
   constexpr int kIt = 8;     // 16 B chunks per lane per pass (2048 columns)
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -883,7 +887,7 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
                          const float* lse, float* delta, float* ksum, uint16_t* dqkv, cudaStream_t st) {
   const int rows = n_items * s;
   LX_REQUIRE(ld_o % 8 == 0, LX_ERR_SHAPE, "attention bwd: O / dO row stride must be a multiple of 8");
-  bsattn_delta_tc_kernel<HD><<<(rows * 32 + 255) / 256, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(o),
+  launch_k(bsattn_delta_tc_kernel<HD>, (rows * 32 + 255) / 256, 256, 0, st, reinterpret_cast<const __nv_bfloat16*>(o),
                                                                       reinterpret_cast<const __nv_bfloat16*>(d_o), ld_o,
                                                                       rows, s, H, delta);
   int rc = launch_check("bsattn_delta_tc");
@@ -898,10 +902,10 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
   LX_CHECK_CUDA(a2);
   dim3 grid((s + kAT - 1) / kAT, H, n_items);
   const float sl2 = scale * 1.4426950408889634f;
-  bsattn_dkdv_tc_kernel<HD><<<grid, 192, smem, st>>>(tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
+  launch_k(bsattn_dkdv_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
                                                      lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);
   if ((rc = launch_check("bsattn_dkdv_tc"))) return rc;
-  bsattn_dq_tc_kernel<HD><<<grid, 192, smem, st>>>(tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
+  launch_k(bsattn_dq_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
                                                    lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);
   return launch_check("bsattn_dq_tc");
 }

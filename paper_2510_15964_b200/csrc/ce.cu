@@ -15,6 +15,7 @@ __device__ __forceinline__ void online_merge(float& m, float& sum, float m2, flo
 
 __global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logits, int V, const int64_t* __restrict__ tgt,
                                                  float inv_s, float* __restrict__ row_loss, __nv_bfloat16* __restrict__ grad) {
+  pdl_wait_trigger();
   const size_t row = blockIdx.x;
   const float4* l4 = reinterpret_cast<const float4*>(logits + row * V);
   const int nv = V / 4;
@@ -70,7 +71,7 @@ int lx_cross_entropy(const float* logits, int rows, int V, const int64_t* target
                      uint16_t* grad_bf16, lx_stream_t stream) {
   LX_REQUIRE(rows >= 1 && V >= 1, LX_ERR_SHAPE, "cross_entropy: empty shape");
   LX_REQUIRE(V % 4 == 0, LX_ERR_UNSUPPORTED, "cross_entropy: vocab must be a multiple of 4");
-  ce_kernel<<<rows, 256, 0, stream>>>(logits, V, targets, inv_s, row_loss, reinterpret_cast<__nv_bfloat16*>(grad_bf16));
+  launch_k(ce_kernel, rows, 256, 0, stream, logits, V, targets, inv_s, row_loss, reinterpret_cast<__nv_bfloat16*>(grad_bf16));
   return launch_check("cross_entropy");
 }
 

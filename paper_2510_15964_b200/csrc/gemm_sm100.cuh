@@ -172,16 +172,6 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   const int m_tiles = (args.rows_per_item + TM - 1) / TM;
   const int t0 = blockIdx.x / CTAS, t_step = gridDim.x / CTAS;
 
-  // ---- tile table: prefix[b] = first tile index of item b (counts are device-resident)
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int b = 0; b < args.n_items; ++b) {
-      prefix[b] = acc;
-      int cnt = (BMODE == kDense) ? 0 : __ldg(args.counts + b);
-      acc += m_tiles * item_n_tiles<BMODE, BN>(args, cnt);
-    }
-    prefix[args.n_items] = acc;
-  }
   if (warp == 0 && lane == 0) {
     gemm_stamp(0);
     tma_prefetch_desc(&tmap_a);
@@ -193,6 +183,18 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   if (warp == 2) {
     if (CTAS == 2) tmem_alloc_cg2<512>(tmem_slot);
     else tmem_alloc<512>(tmem_slot);
+  }
+  // prologue above overlaps the predecessor kernel's tail (programmatic dependent launch)
+  pdl_wait_trigger();
+  // ---- tile table: prefix[b] = first tile index of item b (counts are device-resident)
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < args.n_items; ++b) {
+      prefix[b] = acc;
+      int cnt = (BMODE == kDense) ? 0 : __ldg(args.counts + b);
+      acc += m_tiles * item_n_tiles<BMODE, BN>(args, cnt);
+    }
+    prefix[args.n_items] = acc;
   }
   tc_fence_before();
   __syncthreads();

@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(kLnThreads) ln_fwd_kernel(const float* __restr
                                                              __nv_bfloat16* __restrict__ x_small,
                                                              const __nv_bfloat16* __restrict__ delta,
                                                              float* __restrict__ resid_out) {
+  pdl_wait_trigger();
   __shared__ float red[32];
   const size_t row = blockIdx.x;
   const float4* xr = reinterpret_cast<const float4*>(x + row * d);
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(kLnThreads) ln_bwd_kernel(const void* __restri
                                                              const float* __restrict__ g, const float* __restrict__ mean,
                                                              const float* __restrict__ istd, int d,
                                                              float* __restrict__ dx, __nv_bfloat16* __restrict__ dx_bf16) {
+  pdl_wait_trigger();
   __shared__ float red[32];
   const size_t row = blockIdx.x;
   const float mu = mean[row], is = istd[row];
@@ -158,6 +160,7 @@ __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const float* __restric
                                                           int m_small, __nv_bfloat16* __restrict__ x_small,
                                                           const __nv_bfloat16* __restrict__ delta,
                                                           float* __restrict__ resid_out) {
+  pdl_wait_trigger();
   const int lane = threadIdx.x & 31;
   const int nv = d / 4;
 #pragma unroll 1
@@ -227,6 +230,7 @@ __global__ void __launch_bounds__(256) ln_bwd_warp_kernel(const void* __restrict
                                                           const float* __restrict__ g, const float* __restrict__ mean,
                                                           const float* __restrict__ istd, int M, int d,
                                                           float* __restrict__ dx, __nv_bfloat16* __restrict__ dx_bf16) {
+  pdl_wait_trigger();
   const int lane = threadIdx.x & 31;
   const int nv = d / 4;
 #pragma unroll 1
@@ -293,7 +297,7 @@ template <int VEC>
 static void ln_fwd_warp(const float* x, const uint16_t* delta, float* resid_out, int M, int d, const float* gamma,
                         const float* beta, float eps, uint16_t* y, int ldy, float* mean, float* inv_std, int s, int m_small,
                         uint16_t* x_small, cudaStream_t st) {
-  ln_fwd_warp_kernel<VEC><<<ln_grid(ln_fwd_warp_kernel<VEC>, M), 256, 0, st>>>(x, M, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), ldy, mean,
+  launch_k(ln_fwd_warp_kernel<VEC>, ln_grid(ln_fwd_warp_kernel<VEC>, M), 256, 0, st, x, M, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), ldy, mean,
                                                        inv_std, s > 0 ? s : 1, m_small,
                                                        reinterpret_cast<__nv_bfloat16*>(x_small),
                                                        reinterpret_cast<const __nv_bfloat16*>(delta), resid_out);
@@ -303,9 +307,9 @@ template <int VEC>
 static void ln_bwd_warp(const void* dy, int dy_is_f32, const float* x, const float* gamma, const float* mean,
                         const float* inv_std, int M, int d, float* dx, __nv_bfloat16* ob, cudaStream_t st) {
   if (dy_is_f32)
-    ln_bwd_warp_kernel<true, VEC><<<ln_grid(ln_bwd_warp_kernel<true, VEC>, M), 256, 0, st>>>(dy, x, gamma, mean, inv_std, M, d, dx, ob);
+    launch_k(ln_bwd_warp_kernel<true, VEC>, ln_grid(ln_bwd_warp_kernel<true, VEC>, M), 256, 0, st, dy, x, gamma, mean, inv_std, M, d, dx, ob);
   else
-    ln_bwd_warp_kernel<false, VEC><<<ln_grid(ln_bwd_warp_kernel<false, VEC>, M), 256, 0, st>>>(dy, x, gamma, mean, inv_std, M, d, dx, ob);
+    launch_k(ln_bwd_warp_kernel<false, VEC>, ln_grid(ln_bwd_warp_kernel<false, VEC>, M), 256, 0, st, dy, x, gamma, mean, inv_std, M, d, dx, ob);
 }
 
 }  // namespace lx
@@ -330,7 +334,7 @@ int lx_layernorm_fwd(const float* x, const uint16_t* delta, float* resid_out, in
     return launch_check("layernorm_fwd");
   }
   LX_REQUIRE(ldy == d, LX_ERR_UNSUPPORTED, "layernorm: strided output needs d <= 2048");
-  ln_fwd_kernel<<<M, kLnThreads, 0, stream>>>(x, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), mean, inv_std,
+  launch_k(ln_fwd_kernel, M, kLnThreads, 0, stream, x, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), mean, inv_std,
                                               s > 0 ? s : 1, m_small, reinterpret_cast<__nv_bfloat16*>(x_small),
                                               reinterpret_cast<const __nv_bfloat16*>(delta), resid_out);
   return launch_check("layernorm_fwd");
@@ -348,9 +352,9 @@ int lx_layernorm_bwd(const void* dy, int dy_is_f32, const float* x, const float*
     return launch_check("layernorm_bwd");
   }
   if (dy_is_f32)
-    ln_bwd_kernel<true><<<M, kLnThreads, 0, stream>>>(dy, x, gamma, mean, inv_std, d, dx_accum, ob);
+    launch_k(ln_bwd_kernel<true>, M, kLnThreads, 0, stream, dy, x, gamma, mean, inv_std, d, dx_accum, ob);
   else
-    ln_bwd_kernel<false><<<M, kLnThreads, 0, stream>>>(dy, x, gamma, mean, inv_std, d, dx_accum, ob);
+    launch_k(ln_bwd_kernel<false>, M, kLnThreads, 0, stream, dy, x, gamma, mean, inv_std, d, dx_accum, ob);
   return launch_check("layernorm_bwd");
 }
 

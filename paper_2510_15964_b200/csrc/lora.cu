@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(256) rowproj_kernel(const __nv_bfloat16* __res
                                                       float scale, const int32_t* __restrict__ counts,
                                                       const int32_t* __restrict__ ids, int ids_stride, int blk,
                                                       float* __restrict__ y, int ldy) {
+  pdl_wait_trigger();
   // staged W chunk [kRpChunk][RS]: RS = R + 4 so the 8 lanes of a quarter-warp, reading 8 consecutive
   // k-rows with float4 loads, hit 8 distinct 4-bank groups (conflict-free)
   constexpr int RS = R + 4;
@@ -125,6 +126,7 @@ LX_DEV void mma16816_rp(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint
 __global__ void rowproj_wpack_kernel(const float* __restrict__ w, long long w_sk, long long w_sq, int r, int RP, int K,
                                      int Kp, const int32_t* __restrict__ counts, const int32_t* __restrict__ ids,
                                      int ids_stride, int blk, __nv_bfloat16* __restrict__ wp) {
+  pdl_wait_trigger();
   const int item = blockIdx.y;
   const int k_item = counts ? __ldg(counts + item) * blk : K;
   const int32_t* my_ids = ids ? ids + (size_t)item * ids_stride : nullptr;
@@ -164,6 +166,7 @@ __global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_
                                                            long long w_item_stride, const int32_t* __restrict__ ids,
                                                            int ids_stride, float* __restrict__ y, int ldy,
                                                            __nv_bfloat16* __restrict__ yb, int ldyb) {
+  pdl_wait_trigger();
   constexpr int RP = 8 * NT;
   __shared__ float s_red[kRpWarps][16][RP + 1];
   const int item = blockIdx.y;
@@ -249,6 +252,7 @@ __global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_
 // lo_off != 0 also writes the bf16 residual (hi/lo split) at dst + lo_off. One launch refreshes every
 // LoRA factor's rowproj pack and K-extended projection rows after the optimizer step.
 __global__ void pack_params_kernel(const lx_pack_segment* __restrict__ segs) {
+  pdl_wait_trigger();
   const lx_pack_segment sg = segs[blockIdx.y];
   const long long n = (long long)sg.rows * sg.cols;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
@@ -341,6 +345,7 @@ LX_DEV void bulk_load(void* smem_dst, const void* src, uint32_t bytes, uint64_t*
 
 template <int MT>
 __global__ void __launch_bounds__(kCgThreads, 2) colgrad_group_kernel(const __grid_constant__ CgGroup grp) {
+  pdl_wait_trigger();
   using L = CgSmemL<MT>;
   constexpr int kCgStages = L::kStages, kCgStageBytes = L::kStageBytes;
   extern __shared__ uint8_t cg_raw[];
@@ -524,6 +529,7 @@ __global__ void __launch_bounds__(kCgThreads, 2) colgrad_group_kernel(const __gr
 // fragment blocks: block bi, lane (g, t), chunk j = k-step * MT + m holds the m16n8k16 A fragment of
 // k-step rows 16*ks + {2t, 2t+1, 2t+8, 2t+9}: regs (hi, lo, hi, lo) of rank q = 8m + g
 __global__ void colgrad_prep_kernel(const __grid_constant__ CgGroup grp) {
+  pdl_wait_trigger();
   const CgProb& P = grp.pr[blockIdx.y];
   const int MT = grp.mt, nw = 32 * 8 * MT * 4;  // words per block
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -560,6 +566,7 @@ __global__ void colgrad_prep_kernel(const __grid_constant__ CgGroup grp) {
 
 // G(q, c) = scale * sum over splits (in order) of the partials, for the problems with splits > 1
 __global__ void colgrad_final_kernel(const __grid_constant__ CgGroup grp) {
+  pdl_wait_trigger();
   const CgProb& P = grp.pr[blockIdx.y];
   if (P.splits == 1) return;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -627,7 +634,7 @@ int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const floa
     const int items_w = counts ? n_items : 1;
     const int Kp = K;
     dim3 gp((RP * Kp + 255) / 256 < 64 ? (RP * Kp + 255) / 256 : 64, items_w);
-    rowproj_wpack_kernel<<<gp, 256, 0, stream>>>(w, w_sk, w_sq, r, RP, K, Kp, counts, ids, ids_stride, b,
+    launch_k(rowproj_wpack_kernel, gp, 256, 0, stream, w, w_sk, w_sq, r, RP, K, Kp, counts, ids, ids_stride, b,
                                                  reinterpret_cast<__nv_bfloat16*>(wpack_ws));
     int rc = launch_check("rowproj_wpack");
     if (rc) return rc;
@@ -637,25 +644,25 @@ int lx_rowproj(const uint16_t* x, int ldx, int n_items, int s, int K, const floa
       // dense W is shared by all items: index it as item 0 by treating the batch as one item
       grid = dim3((n_items * s + 15) / 16, 1);
       if (NT == 1)
-        rowproj_mma2_kernel<1><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb,
+        launch_k(rowproj_mma2_kernel<1>, grid, 32 * kRpWarps, 0, stream, xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb,
                                                                    2LL * 8 * Kp, nullptr, 0, y, ldy, nullptr, 0);
       else
-        rowproj_mma2_kernel<2><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb,
+        launch_k(rowproj_mma2_kernel<2>, grid, 32 * kRpWarps, 0, stream, xb, ldx, n_items * s, K, Kp, r, scale, nullptr, b, wpb,
                                                                    2LL * 16 * Kp, nullptr, 0, y, ldy, nullptr, 0);
     } else if (NT == 1) {
-      rowproj_mma2_kernel<1><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, 2LL * 8 * Kp,
+      launch_k(rowproj_mma2_kernel<1>, grid, 32 * kRpWarps, 0, stream, xb, ldx, s, K, Kp, r, scale, counts, b, wpb, 2LL * 8 * Kp,
                                                                  nullptr, 0, y, ldy, nullptr, 0);
     } else {
-      rowproj_mma2_kernel<2><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, s, K, Kp, r, scale, counts, b, wpb, 2LL * 16 * Kp,
+      launch_k(rowproj_mma2_kernel<2>, grid, 32 * kRpWarps, 0, stream, xb, ldx, s, K, Kp, r, scale, counts, b, wpb, 2LL * 16 * Kp,
                                                                  nullptr, 0, y, ldy, nullptr, 0);
     }
     return launch_check("rowproj_mma");
   }
   dim3 grid((s + kRpRows - 1) / kRpRows, n_items);
   if (r <= 8)
-    rowproj_kernel<8><<<grid, 256, 0, stream>>>(xb, ldx, s, K, w, w_sk, w_sq, r, scale, counts, ids, ids_stride, b, y, ldy);
+    launch_k(rowproj_kernel<8>, grid, 256, 0, stream, xb, ldx, s, K, w, w_sk, w_sq, r, scale, counts, ids, ids_stride, b, y, ldy);
   else
-    rowproj_kernel<16><<<grid, 256, 0, stream>>>(xb, ldx, s, K, w, w_sk, w_sq, r, scale, counts, ids, ids_stride, b, y, ldy);
+    launch_k(rowproj_kernel<16>, grid, 256, 0, stream, xb, ldx, s, K, w, w_sk, w_sq, r, scale, counts, ids, ids_stride, b, y, ldy);
   return launch_check("rowproj");
 }
 
@@ -676,10 +683,10 @@ int lx_rowproj_packed(const uint16_t* x, int ldx, int n_items, int s, int K, con
   const int items = counts ? n_items : 1, rows = counts ? s : n_items * s;
   dim3 grid((rows + 15) / 16, items);
   if (RP == 8)
-    rowproj_mma2_kernel<1><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, rows, K, K_full, r, scale, counts, counts ? blk : 1, wp,
+    launch_k(rowproj_mma2_kernel<1>, grid, 32 * kRpWarps, 0, stream, xb, ldx, rows, K, K_full, r, scale, counts, counts ? blk : 1, wp,
                                                                0, counts ? ids : nullptr, counts ? K / blk : 0, y, ldy, ybf, ldyb);
   else
-    rowproj_mma2_kernel<2><<<grid, 32 * kRpWarps, 0, stream>>>(xb, ldx, rows, K, K_full, r, scale, counts, counts ? blk : 1, wp,
+    launch_k(rowproj_mma2_kernel<2>, grid, 32 * kRpWarps, 0, stream, xb, ldx, rows, K, K_full, r, scale, counts, counts ? blk : 1, wp,
                                                                0, counts ? ids : nullptr, counts ? K / blk : 0, y, ldy, ybf, ldyb);
   return launch_check("rowproj_packed");
 }
@@ -687,7 +694,7 @@ int lx_rowproj_packed(const uint16_t* x, int ldx, int n_items, int s, int K, con
 int lx_pack_params(const lx_pack_segment* segs, int n_segs, lx_stream_t stream) {
   LX_REQUIRE(n_segs >= 0, LX_ERR_SHAPE, "pack_params: negative segment count");
   if (n_segs == 0) return LX_OK;
-  pack_params_kernel<<<dim3(64, n_segs), 256, 0, stream>>>(segs);
+  launch_k(pack_params_kernel, dim3(64, n_segs), 256, 0, stream, segs);
   return launch_check("pack_params");
 }
 
@@ -753,23 +760,23 @@ int lx_colgrad_group(const lx_colgrad_problem* probs, int n_probs, int n_items, 
   grp.n_units = units;
   const int grid = std::max(std::min(units, 2 * num_sms()), (units + kCgMaxSlots - 1) / kCgMaxSlots);
   LX_REQUIRE((units + grid - 1) / grid <= kCgMaxSlots, LX_ERR_UNSUPPORTED, "colgrad_group: too many units");
-  colgrad_prep_kernel<<<dim3((max_blk_words + 255) / 256, n_probs), 256, 0, stream>>>(grp);
+  launch_k(colgrad_prep_kernel, dim3((max_blk_words + 255) / 256, n_probs), 256, 0, stream, grp);
   int rc = launch_check("colgrad_prep");
   if (rc) return rc;
   if (grp.mt == 2) {
     constexpr int smem = CgSmemL<2>::kTotal;
     static cudaError_t attr = cudaFuncSetAttribute(colgrad_group_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     LX_CHECK_CUDA(attr);
-    colgrad_group_kernel<2><<<grid, kCgThreads, smem, stream>>>(grp);
+    launch_k(colgrad_group_kernel<2>, grid, kCgThreads, smem, stream, grp);
   } else {
     constexpr int smem = CgSmemL<1>::kTotal;
     static cudaError_t attr = cudaFuncSetAttribute(colgrad_group_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     LX_CHECK_CUDA(attr);
-    colgrad_group_kernel<1><<<grid, kCgThreads, smem, stream>>>(grp);
+    launch_k(colgrad_group_kernel<1>, grid, kCgThreads, smem, stream, grp);
   }
   rc = launch_check("colgrad_group");
   if (rc || max_final == 0) return rc;
-  colgrad_final_kernel<<<dim3((max_final + 255) / 256, n_probs), 256, 0, stream>>>(grp);
+  launch_k(colgrad_final_kernel, dim3((max_final + 255) / 256, n_probs), 256, 0, stream, grp);
   return launch_check("colgrad_final");
 }
 

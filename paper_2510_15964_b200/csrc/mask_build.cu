@@ -20,6 +20,7 @@ namespace lx {
 
 __global__ void mask_compact_kernel(const uint32_t* __restrict__ bits, int n_items, int n_blk, int scope_batch,
                                     int32_t* __restrict__ counts, int32_t* __restrict__ ids, int32_t* __restrict__ pos) {
+  pdl_wait_trigger();
   const int item = blockIdx.x;
   const int words = (n_blk + 31) / 32;
   __shared__ int s_scan[1024];
@@ -94,6 +95,7 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
                                     double tau, int n_b, const int32_t* __restrict__ pool_kind,
                                     const int32_t* __restrict__ pool_param, int n_pool, int scope_batch,
                                     int32_t* __restrict__ pattern_idx, float* __restrict__ dump) {
+  pdl_wait_trigger();
   const int h = blockIdx.x;
   const int item0 = scope_batch ? 0 : blockIdx.y;
   const int item1 = scope_batch ? n_items : blockIdx.y + 1;
@@ -227,7 +229,7 @@ extern "C" {
 int lx_mask_compact(const uint32_t* bits, int n_items, int n_blk, int scope_batch, int32_t* counts, int32_t* ids,
                     int32_t* pos, lx_stream_t stream) {
   LX_REQUIRE(n_items >= 1 && n_blk >= 1, LX_ERR_SHAPE, "mask_compact: empty shape");
-  mask_compact_kernel<<<n_items, 256, 0, stream>>>(bits, n_items, n_blk, scope_batch, counts, ids, pos);
+  launch_k(mask_compact_kernel, n_items, 256, 0, stream, bits, n_items, n_blk, scope_batch, counts, ids, pos);
   return launch_check("mask_compact");
 }
 
@@ -263,13 +265,13 @@ int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint
     constexpr int smem = GemmSmem<128>::kTotal;
     static cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     LX_CHECK_CUDA(attr);
-    kern<<<num_sms(), kGemmThreads, smem, stream>>>(ta, tb, args);
+    launch_k(kern, num_sms(), kGemmThreads, smem, stream, ta, tb, args);
   } else {
     auto kern = gemm_sm100_kernel<kDense, kEpiMask, 256>;
     constexpr int smem = GemmSmem<256>::kTotal;
     static cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     LX_CHECK_CUDA(attr);
-    kern<<<num_sms(), kGemmThreads, smem, stream>>>(ta, tb, args);
+    launch_k(kern, num_sms(), kGemmThreads, smem, stream, ta, tb, args);
   }
   if ((rc = launch_check("mlp mask gemm"))) return rc;
   return lx_mask_compact(bits_ws, n_items, n_blk, scope_batch, counts, ids, pos, stream);
@@ -289,7 +291,7 @@ int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, i
   LX_REQUIRE(smem <= 200 * 1024, LX_ERR_UNSUPPORTED, "predictor rank %d x m %d exceeds shared memory", r, m);
   static cudaError_t attr = cudaFuncSetAttribute(attn_pattern_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   LX_CHECK_CUDA(attr);
-  attn_pattern_kernel<<<grid, 256, smem, stream>>>(proj_ws, n_items, m, H, r, threshold_frac, tau, n_b, pool_kind,
+  launch_k(attn_pattern_kernel, grid, 256, smem, stream, proj_ws, n_items, m, H, r, threshold_frac, tau, n_b, pool_kind,
                                                      pool_param, n_pool, scope_batch, pattern_idx, scores_dump);
   return launch_check("attn_pattern");
 }

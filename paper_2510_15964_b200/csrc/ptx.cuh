@@ -10,6 +10,19 @@
 
 namespace lx {
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every hot-path kernel is launched with programmatic stream serialization (launch_k): it may start
+// while its predecessor drains, so it first waits for the predecessor grid's completion (and memory
+// flush) before touching global memory, then lets its own dependents launch.
+LX_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+LX_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+LX_DEV void pdl_wait_trigger() {
+  pdl_wait();
+#ifdef LX_PDL_EARLY_TRIGGER
+  pdl_trigger();
+#endif
+}
+
 LX_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
 LX_DEV uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x / 32, 0); }

@@ -49,6 +49,24 @@ for pair in (2, 1, 0):
         b.record()
         torch.cuda.synchronize()
         us = a.elapsed_time(b) / 20 * 1e3
+        gr = torch.cuda.CUDAGraph()  # device-side per-launch time (no host launch overhead)
+        s2 = torch.cuda.Stream()
+        s2.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s2):
+            st_prev = st
+            globals()["st"] = _abi.stream_handle()
+            with torch.cuda.graph(gr, stream=s2):
+                for _ in range(20):
+                    fn()
+            globals()["st"] = st_prev
+        torch.cuda.current_stream().wait_stream(s2)
+        gr.replay()
+        torch.cuda.synchronize()
+        a.record()
+        gr.replay()
+        b.record()
+        torch.cuda.synchronize()
+        us_graph = a.elapsed_time(b) / 20 * 1e3
         buf.zero_()
         _abi.call("lx_debug_set_gemm_trace", buf.data_ptr())
         fn()
@@ -58,7 +76,7 @@ for pair in (2, 1, 0):
         act = t[:, 2] > 0
         base = t[:, 0:1]
         rel = np.where(t > 0, t - base, 0)
-        print(f"{name} pair={pair}: {us:.1f} us/launch, CTAs with a tile {act.sum()}; lifetime mean "
+        print(f"{name} pair={pair}: {us:.1f} us/launch (graph {us_graph:.1f}), CTAs with a tile {act.sum()}; lifetime mean "
               f"{(t[:, 1] - t[:, 0]).mean():.0f} cyc")
         for i in range(2):
             sel = t[:, 2 + 4 * i] > 0
