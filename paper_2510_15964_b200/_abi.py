@@ -11,7 +11,10 @@ from pathlib import Path
 
 from . import errors as E
 
-LIB_PATH = Path(__file__).resolve().parent / "libsparseft_b200.so"
+import os
+
+# LX_LIB: an alternative build of the same library (experiments only; tests record which .so loaded)
+LIB_PATH = Path(os.environ.get("LX_LIB") or Path(__file__).resolve().parent / "libsparseft_b200.so")
 
 _P = C.c_void_p
 _I = C.c_int

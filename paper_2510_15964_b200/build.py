@@ -17,14 +17,15 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-OBJ = PKG / "build"
-LIB = PKG / "libsparseft_b200.so"
+OBJ = Path(os.environ.get("LX_BUILD_DIR", PKG / "build"))
+LIB = Path(os.environ.get("LX_LIB_OUT", PKG / "libsparseft_b200.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v,-warn-spills",
     f"-I{ROOT / 'include'}", f"-I{CSRC}",
+    *os.environ.get("LX_NVCC_EXTRA", "").split(),
 ]
 
 

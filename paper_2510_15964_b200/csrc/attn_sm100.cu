@@ -429,6 +429,7 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
                       float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
                       __nv_bfloat16* __restrict__ dkv, int ld_dkv, float* __restrict__ ksum) {
   pdl_wait_trigger();
+  if (threadIdx.x == 0) trace_stamp(0);
   using L = AttnBwdSmem<HD>;
   constexpr int A = HD / 64;
   constexpr int kTmem = tmem_cols_pow2(kAT + 2 * HD);
@@ -512,10 +513,12 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       const uint32_t id_g = make_idesc_bf16(kAT, HD, false, true);    // dV, dK: B MN-major
       const uint32_t sk = smem_u32(sm), sv = sk + L::kT;
       mbar_wait(kv_full, 0);
+      trace_stamp(1);
       for (int e = 0; e < n; ++e) {
         const int st = e % L::kSt;
         const uint32_t sq = smem_u32(sm + L::kOffRing + st * 2 * L::kT), sdo = sq + L::kT;
         mbar_wait(qd_full + st, (e / L::kSt) & 1);
+        if (e < 4) trace_stamp(2 + 6 * e);  // q/dO tile landed, S MMA issued next
         tc_fence_after();
         for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(t_r, desc_kmajor(sk, kk), desc_kmajor(sq, kk), id_s, kk != 0);
         mma_commit(s_full);
@@ -545,6 +548,7 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       const float* dl = sD + st * kAT;
       mbar_wait(qd_full + st, (e / L::kSt) & 1);  // lse / delta staged with the tiles
       mbar_wait(s_full, e & 1);
+      if (e < 4 && ep_tid == 0) trace_stamp(3 + 6 * e);  // S in TMEM
       tc_fence_after();
       uint32_t pp[4][16];  // P^T (bf16 pairs) for the whole row, reused by dS^T
 #pragma unroll
@@ -571,7 +575,9 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_ready);
+      if (e < 4 && ep_tid == 0) trace_stamp(4 + 6 * e);  // P stored
       mbar_wait(dp_full, e & 1);
+      if (e < 4 && ep_tid == 0) trace_stamp(5 + 6 * e);  // dP in TMEM
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -591,8 +597,10 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_ready);
+      if (e < 4 && ep_tid == 0) trace_stamp(6 + 6 * e);  // dS stored
     }
     mbar_wait(done, 0);
+    if (ep_tid == 0) trace_stamp(26);
     tc_fence_after();
     const int key = kt * kAT + kr;
 #pragma unroll
@@ -638,6 +646,7 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       }
     }
   }
+  if (threadIdx.x == 64) trace_stamp(27);
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {

@@ -49,7 +49,20 @@ LX_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 LX_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef LX_MBAR_SUSPEND_NS
+#define LX_MBAR_SUSPEND_NS 0x989680u
+#endif
 LX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if LX_MBAR_SPIN
+  // pure polling: the waiter resumes the cycle the phase flips (no suspend/wake latency)
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra LAB_WAIT;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "LAB_WAIT:\n\t"
@@ -57,8 +70,9 @@ LX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@P1 bra DONE;\n\t"
       "bra LAB_WAIT;\n\t"
       "DONE:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680u)
+      "r"(parity), "r"(LX_MBAR_SUSPEND_NS)
       : "memory");
+#endif
 }
 
 // ---------------------------------------------------------------- TMA
