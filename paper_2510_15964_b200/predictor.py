@@ -22,6 +22,14 @@ from .neuron_ops import NeuronMasks
 from .patterns import DevicePool, LayoutTable, device_pool
 
 
+def _dev_key(device) -> str:
+    """Cache key of a device ('cuda' and 'cuda:<current>' are the same device)."""
+    dv = torch.device(device)
+    if dv.type == "cuda" and dv.index is None:
+        dv = torch.device("cuda", torch.cuda.current_device())
+    return str(dv)
+
+
 @dataclass
 class AttnPredictorParams:
     """One (wq_hat, wk_hat) low-rank pair per head, each (d, r) (sf/predictor.py:28-37)."""
@@ -36,7 +44,7 @@ class AttnPredictorParams:
 
     def packed_t(self, device) -> torch.Tensor:
         """bf16 [2*H*r, d]: rows [h*r, (h+1)*r) = Wq_hat[h]^T, then the Wk_hat[h]^T blocks."""
-        key = str(device)
+        key = _dev_key(device)
         if key not in self._dev:
             def t(w):
                 return torch.as_tensor(np.asarray(w) if not torch.is_tensor(w) else w).float().t()
@@ -53,7 +61,7 @@ class MlpPredictorParams:
     _dev: dict = field(default_factory=dict, repr=False)
 
     def packed_t(self, device) -> torch.Tensor:
-        key = str(device)
+        key = _dev_key(device)
         if key not in self._dev:
             w = torch.as_tensor(np.asarray(self.wa_hat) if not torch.is_tensor(self.wa_hat) else self.wa_hat)
             self._dev[key] = w.float().t().contiguous().to(device, torch.bfloat16)

@@ -226,3 +226,86 @@ def test_cross_entropy_kernel():
     torch.cuda.synchronize()
     assert abs(float(loss) - float(ref)) < 1e-4 * float(ref)
     assert rel(d_hf, ref_dhf) < 1e-2
+
+
+@pytest.mark.parametrize("gather", [False, True])
+@pytest.mark.parametrize("r,rp", [(8, 8), (16, 16), (4, 8), (12, 16)])
+def test_rowproj_packed_and_pack_params(gather, r, rp):
+    """lx_pack_params (fp32 LoRA factor -> bf16 hi/lo pack) feeding lx_rowproj_packed, dense and gathered
+    through the item's active block ids, with the optional bf16 copy of Y (K-extended GEMM columns)."""
+    from paper_2510_15964_b200 import _abi, neuron_ops as N
+
+    dev = _dev()
+    n_items, s, K, blk = 3, 300, 1024, 16
+    n_blk = K // blk
+    masks, counts, ids = _masks(n_items, n_blk, 0.4, seed=r + rp)
+    g = torch.Generator(device="cpu").manual_seed(r)
+    x = torch.randn(n_items * s, K + 16, generator=g).to(dev, torch.bfloat16)[:, :K]  # row stride K + 16
+    a = torch.randn(K, r, generator=g).to(dev)  # W(k, q) = A[k][q]
+    wp = torch.zeros(2, rp, K, dtype=torch.bfloat16, device=dev)
+    seg = _abi.PackSegment(a.data_ptr(), 1, r, r, K, wp.data_ptr(), K, 1, rp * K, 1.0, 0)
+    segs = torch.frombuffer(bytearray(bytes(seg)), dtype=torch.uint8).to(dev)
+    _abi.call("lx_pack_params", segs.data_ptr(), 1, _abi.stream_handle())
+    torch.cuda.synchronize()
+    assert rel(wp[0, :r].float() + wp[1, :r].float(), a.t()) < 1e-5  # hi + lo keeps ~16 mantissa bits
+    nm = N.lower_mask(torch.from_numpy(masks).to(dev), n_blk, blk, n_items, dev) if gather else None
+    yb = torch.zeros(n_items * s, 24, dtype=torch.bfloat16, device=dev)
+    y = N.rowproj_packed(x, n_items, s, K, wp, r, scale=0.5, masks=nm, blk=blk, out_bf16=yb[:, 3 : 3 + r])
+    torch.cuda.synchronize()
+    for b in range(n_items):
+        rows = slice(b * s, (b + 1) * s)
+        if gather:
+            cols = torch.from_numpy((ids[b, : counts[b], None] * blk + np.arange(blk)[None]).reshape(-1)).to(dev)
+            ref = 0.5 * x[rows, : cols.numel()].float() @ a[cols]
+        else:
+            ref = 0.5 * x[rows].float() @ a
+        assert rel(y[rows], ref) < 1e-4 if ref.abs().max() > 0 else y[rows].abs().max() == 0
+        assert rel(yb[rows, 3 : 3 + r], ref) < 1e-2 if ref.abs().max() > 0 else True
+    assert yb[:, :3].abs().max() == 0 and yb[:, 3 + r :].abs().max() == 0  # only the r columns are written
+
+
+def test_colgrad_group_mixed_problems():
+    """One lx_colgrad_group launch over dense, gathered (packed per-item columns), column-sum and
+    rank-16 problems with strided X / P / G — each equal to its own torch fp32 reduction."""
+    from paper_2510_15964_b200 import neuron_ops as N
+
+    dev = _dev()
+    n_items, s, d, f, blk = 4, 320, 512, 2048, 16
+    n_blk = f // blk
+    masks, counts, ids = _masks(n_items, n_blk, 0.3, seed=5)
+    nm = N.lower_mask(torch.from_numpy(masks).to(dev), n_blk, blk, n_items, dev)
+    g = torch.Generator(device="cpu").manual_seed(11)
+    M = n_items * s
+    xw = torch.randn(M, 3 * d + 16, generator=g).to(dev, torch.bfloat16)  # dense X: a column slice, row stride 3d+16
+    xd = xw[:, d : 2 * d]
+    fa = int(counts.max()) * blk
+    xp = torch.randn(M, fa + 8, generator=g).to(dev, torch.bfloat16)  # packed X
+    p16 = torch.randn(M, 24, generator=g).to(dev)
+    g1 = torch.empty(8, d, device=dev)          # G(q, c) = g[q*d + c]
+    g2 = torch.empty(f, 8, device=dev)          # transposed: G(q, c) = g[c*8 + q]
+    g3 = torch.empty(d, device=dev)             # column sums
+    g4 = torch.empty(16, d, device=dev)         # rank 16
+    probs = [N.colgrad_problem(p16[:, :8], xd, d, 8, 0.5, g1, d, 1),
+             N.colgrad_problem(p16[:, 8:16], xp, f, 8, 1.0, g2, 1, 8, masks=nm, blk=blk),
+             N.colgrad_problem(None, xd, d, 1, 1.0, g3, 0, 1),
+             N.colgrad_problem(p16[:, 4:20], xd, d, 16, 2.0, g4, d, 1)]
+    N.colgrad_group(probs, n_items, s)
+    torch.cuda.synchronize()
+    assert rel(g1, 0.5 * p16[:, :8].t() @ xd.float()) < 1e-4
+    ref2 = torch.zeros(8, f, device=dev)
+    for b in range(n_items):
+        rows = slice(b * s, (b + 1) * s)
+        cols = torch.from_numpy((ids[b, : counts[b], None] * blk + np.arange(blk)[None]).reshape(-1)).to(dev)
+        ref2[:, cols] += p16[rows, 8:16].t() @ xp[rows, : cols.numel()].float()
+    assert rel(g2.t(), ref2) < 1e-4
+    act = np.zeros(f, bool)
+    for b in range(n_items):
+        act[(ids[b, : counts[b], None] * blk + np.arange(blk)[None]).reshape(-1)] = True
+    assert float(g2[torch.from_numpy(~act).to(dev)].abs().max()) == 0  # inactive columns exactly 0
+    assert rel(g3, xd.float().sum(0)) < 1e-4
+    assert rel(g4, 2.0 * p16[:, 4:20].t() @ xd.float()) < 1e-4
+    # deterministic: a second launch gives identical bits
+    g1b = g1.clone()
+    N.colgrad_group(probs, n_items, s)
+    torch.cuda.synchronize()
+    assert torch.equal(g1, g1b)

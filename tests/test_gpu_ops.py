@@ -294,3 +294,28 @@ def test_bsattn_tcgen05_bwd(dev, n_items, s, H, hd, attn_blk):
             assert rel(g[rows, 2 * d + h * hd : 2 * d + (h + 1) * hd], ref_dv) < 1e-2, (b, h)
             assert rel(g[rows, cols], ref_dq) < 2e-2, (b, h)
             assert rel(g[rows, d + h * hd : d + (h + 1) * hd], ref_dk) < 2e-2, (b, h)
+
+
+def test_bsattn_tcgen05_bwd_extended_dqkv(dev):
+    """The tcgen05 backward writing into a K-extended [M, 3d + kx] dQKV operand (row stride != the qkv
+    stride, the layout the q/k/v input-grad GEMM consumes) gives the same bits as the fused [M, 3d] layout
+    and leaves the extra columns untouched."""
+    from paper_2510_15964_b200 import block_sparse as BS, patterns as PT
+
+    n_items, s, H, hd, attn_blk = 2, 512, 4, 64, 64
+    q, k, v, do, grids, pidx, dp = _attn_case(dev, n_items, s, H, hd, attn_blk, seed=77)
+    dp.tables128 = torch.from_numpy(PT.tables128_from_grids(grids, s, attn_blk)).to(dev)
+    d = H * hd
+    qkv = torch.from_numpy(np.concatenate([q, k, v], 1)).to(dev, torch.bfloat16)
+    dod = torch.from_numpy(do).to(dev, torch.bfloat16)
+    Q, K, V = qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :]
+    o, lse = BS.attention_forward(Q, K, V, 3 * d, n_items, s, H, hd, pidx, H, dp, 0.125)
+    ref = torch.empty_like(qkv)
+    BS.attention_backward(Q, K, V, o, dod, 3 * d, n_items, s, H, hd, pidx, H, dp, 0.125, lse,
+                          ref[:, :d], ref[:, d : 2 * d], ref[:, 2 * d :])
+    ext = torch.full((n_items * s, 3 * d + 16), 7.0, dtype=torch.bfloat16, device=dev)
+    BS.attention_backward(Q, K, V, o, dod, 3 * d, n_items, s, H, hd, pidx, H, dp, 0.125, lse,
+                          ext[:, :d], ext[:, d : 2 * d], ext[:, 2 * d : 3 * d])
+    torch.cuda.synchronize()
+    assert torch.equal(ext[:, : 3 * d], ref)
+    assert bool((ext[:, 3 * d :] == 7.0).all())
