@@ -36,6 +36,9 @@ sys.path.insert(0, str(ROOT))
 CONFIGS = {
     # BASELINE.json configs[2]: OPT-1.3B (public OPT dims), LoRA r=8 on wq/wv/w1/w2, batch 8, seq 512
     "cfg3": dict(d=2048, H=32, d_ff=8192, L=24, V=50272, B=8, s=512, blk=16, attn_blk=64, r=8, desc="OPT-1.3B"),
+    # BASELINE.json configs[3]: OPT-6.7B (d 4096, hd 128), LoRA seq 1024; global batch 16 split over the GPUs
+    # (B below is per rank at 8 GPUs; `--batch` overrides)
+    "cfg4": dict(d=4096, H=32, d_ff=16384, L=32, V=50272, B=2, s=1024, blk=16, attn_blk=64, r=8, desc="OPT-6.7B"),
     # configs[0] shape (OPT-125M), batch 1 seq 256 — quick checks
     "cfg1": dict(d=768, H=12, d_ff=3072, L=12, V=50272, B=1, s=256, blk=16, attn_blk=64, r=8, desc="OPT-125M"),
 }
@@ -197,7 +200,7 @@ def time_graph(engine, K: int, dist) -> float:
     return ms
 
 
-def fc1_roofline(model, engine, tok_dev, peaks: dict) -> dict:
+def fc1_roofline(model, engine, tok_dev, peaks: dict, config: str = "cfg3") -> dict:
     """Dominant sparse kernel: the fc1 packed-row GEMM (bias + LoRA + ReLU fused), timed live inside one
     eager training step with CUDA events around each of its L launches on the launching stream (so the
     L2 state is the step's own); algorithmic FLOPs per launch = 2 * s * d * sum_b(counts_b * blk)."""
@@ -223,8 +226,10 @@ def fc1_roofline(model, engine, tok_dev, peaks: dict) -> dict:
     ach = fl_avg / (ms_avg * 1e-3) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "r01_fc1_ncu.json"
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    if prof.exists():  # ncu DRAM bytes of one fc1 launch, valid for the config it was captured on
+        pj = json.loads(prof.read_text())
+        if pj.get("config", "cfg3") == config:
+            traffic = pj.get("dram_bytes_per_launch")
     return {"kernel": "gemm_sm100_kernel<kPackedN,kEpiFc1> (neuron_matmul_fwd1+b1+LoRA+ReLU over packed active W1 rows)",
             "bound": "tensor", "achieved": round(ach, 1), "peak": peaks["bf16_sust"], "unit": "TFLOP/s",
             "frac": round(ach / peaks["bf16_sust"], 4), "traffic": traffic,
@@ -284,7 +289,9 @@ def run_ours(args, cfg, rank, world, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     final_loss = float(loss_host)
-    roof = fc1_roofline(model, eng, tok_dev, peaks) if rank == 0 else None
+    roof = fc1_roofline(model, eng, tok_dev, peaks, args.config) if rank == 0 else None
+    frozen_gb = sum(t.numel() * t.element_size() for lw in model.weights.layers
+                    for t in (lw.wqkv, lw.wo, lw.mlp.w1_t, lw.mlp.w2)) / 1e9
     extra = {}
     if not args.skip_dense and rank == 0:
         # dense reference points on the same box: (a) same engine, every head/block dense; (b) torch cuBLAS/SDPA
@@ -317,15 +324,15 @@ def run_ours(args, cfg, rank, world, dist):
         cpu = cpu_baseline(cfg, args)
     tokens_per_step = B * s * world
     line = {
-        "metric": "OPT-1.3B LoRA fwd+bwd ms/batch", "value": round(ms, 3), "unit": "ms/batch", "n_gpus": world,
+        "metric": f"{cfg['desc']} LoRA fwd+bwd ms/batch", "value": round(ms, 3), "unit": "ms/batch", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, random-init weights)",
-        "config": {"workload": f"cfg3: {cfg['desc']} LoRA r={cfg['r']} (wq,wv,w1,w2) fine-tune step (predict+fwd+bwd+Adam), predicted mode",
+        "config": {"workload": f"{args.config}: {cfg['desc']} LoRA r={cfg['r']} (wq,wv,w1,w2) fine-tune step (predict+fwd+bwd+Adam), predicted mode",
                    "model": cfg["desc"], "global_batch": B * world, "seq_len": s, "parallelism": f"dp{world}",
                    "d_model": cfg["d"], "n_layers": cfg["L"], "d_ff": cfg["d_ff"], "vocab": V, "blk_size": cfg["blk"],
                    "attn_blk": cfg["attn_blk"], "mask_scope": "per sequence", **sparsity,
                    "injected": {"mlp_zeroed_predictor_blocks": args.mlp_sparsity, "local_attention_heads": args.local_frac},
-                   "l2": "inputs larger than L2: 2.6 GB of frozen weights stream from HBM every step (no flush needed)",
+                   "l2": f"inputs larger than L2: {frozen_gb:.1f} GB of frozen weights stream from HBM every step (no flush needed)",
                    "timing": "CUDA events around K CUDA-graph replays; Adam (fp64 moments) outside the graph, inside the timed region"},
         "tokens_per_s": round(tokens_per_step / (ms * 1e-3), 1),
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms/batch", "h2d_bytes_per_step": int(B * (s + 1) * 8),
@@ -439,11 +446,14 @@ def main():
     ap.add_argument("--mlp-sparsity", type=float, default=0.85)
     ap.add_argument("--local-frac", type=float, default=0.5)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=0, help="sequences per rank (default: the config's B)")
     ap.add_argument("--skip-dense", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.batch:
+        cfg["B"] = args.batch
     world = int(os.environ.get("WORLD_SIZE", 1))
     rank = int(os.environ.get("RANK", 0))
     if args.impl == "reference":

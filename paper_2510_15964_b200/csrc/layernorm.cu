@@ -22,7 +22,7 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 
 __global__ void __launch_bounds__(kLnThreads) ln_fwd_kernel(const float* __restrict__ x, int d, const float* __restrict__ g,
                                                              const float* __restrict__ b, float eps,
-                                                             __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+                                                             __nv_bfloat16* __restrict__ y, int ldy, float* __restrict__ mean_out,
                                                              float* __restrict__ istd_out, int s, int m_small,
                                                              __nv_bfloat16* __restrict__ x_small,
                                                              const __nv_bfloat16* __restrict__ delta,
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kLnThreads) ln_fwd_kernel(const float* __restr
       float o2 = (v[i].z - mu) * istd * gg.z + bb.z;
       float o3 = (v[i].w - mu) * istd * gg.w + bb.w;
       uint2 pk = make_uint2(pack_bf16x2(o0, o1), pack_bf16x2(o2, o3));
-      *reinterpret_cast<uint2*>(y + row * d + 4 * c) = pk;
+      *reinterpret_cast<uint2*>(y + row * ldy + 4 * c) = pk;
       if (xs_row) *reinterpret_cast<uint2*>(xs_row + 4 * c) = pk;
     }
   }
@@ -333,8 +333,8 @@ int lx_layernorm_fwd(const float* x, const uint16_t* delta, float* resid_out, in
     else ln_fwd_warp<16>(x, delta, resid_out, M, d, gamma, beta, eps, y, ldy, mean, inv_std, s, m_small, x_small, stream);
     return launch_check("layernorm_fwd");
   }
-  LX_REQUIRE(ldy == d, LX_ERR_UNSUPPORTED, "layernorm: strided output needs d <= 2048");
-  launch_k(ln_fwd_kernel, M, kLnThreads, 0, stream, x, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), mean, inv_std,
+  launch_k(ln_fwd_kernel, M, kLnThreads, 0, stream, x, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), ldy, mean,
+           inv_std,
                                               s > 0 ? s : 1, m_small, reinterpret_cast<__nv_bfloat16*>(x_small),
                                               reinterpret_cast<const __nv_bfloat16*>(delta), resid_out);
   return launch_check("layernorm_fwd");
