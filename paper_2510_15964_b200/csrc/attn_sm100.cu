@@ -10,6 +10,9 @@
 // P and dS never touch shared memory: they are written as bf16 into TMEM and consumed as the
 // A operand of the next MMA (TS form). Q/K are K-major operands (rows of hd); V, dO, Q, K also
 // serve as MN-major B operands (K = rows) of P.V, P^T.dO, dS^T.Q and dS.K from the same tiles.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -890,6 +893,368 @@ __global__ void __launch_bounds__(256) bsattn_delta_tc_kernel(const __nv_bfloat1
   }
 }
 
+// ============================================================================ backward dK/dV, ping-pong
+// Persistent: grid = #SMs, one CTA per SM (512 TMEM columns); CTA c walks units u = c, c + G, ... with
+// u = (item * H + h) * nkt + kt (a key tile of one head). Two epilogue warpgroups alternate over the
+// unit's CSC list of query tiles (WG w takes entries e = w, w + 2, ...) with one S/dP TMEM buffer each,
+// so the tensor core computes S(e+1) / dV(e) / dP(e) for one warpgroup while the other runs its exp or
+// dS math — the two dependency chains interleave inside the CTA instead of stalling it:
+//   MMA:  S(0) S(1) | per e: [p_ready] dV += P^T dO, dP^T = V dO^T -> dp_full | [ds_ready] dK += dS^T Q,
+//         release the Q/dO stage, S(e+2) into the freed buffer
+//   WG w: [s_full] P = exp2(S c - lse) as bf16 into its buffer -> p_ready | [dp_full] dS = P (dP - delta)
+//         -> ds_ready
+// K/V are double-buffered across units (HD 64) and Q/dO stream through a kSt-stage ring, so the next
+// unit's loads overlap this unit's tail; the unit epilogue (dK by WG0, dV by WG1, key column sums for
+// the dQ kernel's common-mode correction) overlaps the next unit's first S MMAs.
+constexpr int kBwdThreads = 64 + 32 * 8;  // producer, MMA issuer, two 4-warp epilogue groups
+
+template <int HD>
+struct AttnDkdvPP {
+  static constexpr int kT = (HD / 64) * kAT * 128;  // one 128 x HD bf16 tile
+  static constexpr int kKV = HD == 64 ? 2 : 1;      // K/V buffers
+  static constexpr int kSt = HD == 64 ? 3 : 2;      // Q/dO ring stages
+  static constexpr int kOffRing = kKV * 2 * kT;
+  static constexpr int kOffL = kOffRing + kSt * 2 * kT;          // lse*log2e [kSt][128], delta [kSt][128]
+  static constexpr int kStgPitch = 144;                          // staging row: 128 B of bf16 + 16 B pad
+  static constexpr int kOffStg = kOffL + 2 * kSt * kAT * 4;      // [8 warps][32 rows][kStgPitch]
+  static constexpr int kOffBar = kOffStg + 8 * 32 * kStgPitch;
+  static constexpr int kTotal = kOffBar + 512 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, int s, int H,
+                      int n_units, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
+                      float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
+                      __nv_bfloat16* __restrict__ dkv, int ld_dkv, float* __restrict__ ksum) {
+  using L = AttnDkdvPP<HD>;
+  constexpr int A = HD / 64;
+  const int d_model = H * HD;
+  const int nkt = (s + kAT - 1) / kAT;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = align_smem_1024(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
+  uint64_t* kv_full = bars;                // [kKV]
+  uint64_t* kv_empty = bars + 2;           // [kKV]
+  uint64_t* qd_full = bars + 4;            // [kSt] TMA (1 arrive + tx) + 32 producer lanes (lse / delta)
+  uint64_t* qd_empty = bars + 8;           // [kSt]
+  uint64_t* s_full = bars + 12;            // [2]
+  uint64_t* p_ready = bars + 14;           // [2] 4 warps
+  uint64_t* dp_full = bars + 16;           // [2]
+  uint64_t* ds_ready = bars + 18;          // [2] 4 warps
+  uint64_t* acc_full = bars + 20;
+  uint64_t* acc_empty = bars + 21;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  float* sL = reinterpret_cast<float*>(sm + L::kOffL);  // [kSt][128]
+  float* sD = sL + L::kSt * kAT;                        // [kSt][128]
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+    for (int i = 0; i < L::kKV; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 2);
+    }
+    for (int i = 0; i < L::kSt; ++i) {
+      mbar_init(qd_full + i, 33);
+      mbar_init(qd_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(p_ready + i, 4);
+      mbar_init(dp_full + i, 1);
+      mbar_init(ds_ready + i, 4);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait_trigger();
+  if (threadIdx.x == 0) trace_stamp(0);
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_dv = tmem + 2 * kAT, t_dk = tmem + 2 * kAT + HD;
+
+  // unit -> (item, h, kt) and its CSC range
+  auto unit_of = [&](int u, int& item, int& h, int& kt, Tab128& tv, int& e0, int& n) {
+    kt = u % nkt;
+    h = (u / nkt) % H;
+    item = u / (nkt * H);
+    tv = tab128(tables, __ldg(pidx + item * item_stride + h));
+    e0 = __ldg(tv.col_ptr + kt);
+    n = __ldg(tv.col_ptr + kt + 1) - e0;
+  };
+
+  if (warp == 0) {
+    // ================= producer: K/V per unit, then the unit's Q/dO tiles (+ lse / delta rows)
+    int kvi = 0, g = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++kvi) {
+      int item, h, kt, e0, n;
+      Tab128 tv;
+      unit_of(u, item, h, kt, tv, e0, n);
+      const int row_base = item * s;
+      const int kvb = kvi % L::kKV;
+      mbar_wait(kv_empty + kvb, ((kvi / L::kKV) & 1) ^ 1);
+      if (lane == 0) {
+        uint8_t* skv = sm + kvb * 2 * L::kT;
+        mbar_arrive_expect_tx(kv_full + kvb, 2 * L::kT);
+        for (int a = 0; a < A; ++a) {
+          tma_load_2d(skv + a * kAT * 128, &tm_qkv, kv_full + kvb, d_model + h * HD + a * 64, row_base + kt * kAT);
+          tma_load_2d(skv + L::kT + a * kAT * 128, &tm_qkv, kv_full + kvb, 2 * d_model + h * HD + a * 64,
+                      row_base + kt * kAT);
+        }
+      }
+      const float* lse_b = lse + ((size_t)item * H + h) * s;
+      const float* del_b = delta + ((size_t)item * H + h) * s;
+      for (int e = 0; e < n; ++e, ++g) {
+        const int st = g % L::kSt;
+        mbar_wait(qd_empty + st, ((g / L::kSt) & 1) ^ 1);
+        const int i = __ldg(tv.csc_row + e0 + e);
+        if (lane == 0) {
+          uint8_t* sq = sm + L::kOffRing + st * 2 * L::kT;
+          mbar_arrive_expect_tx(qd_full + st, 2 * L::kT);
+          for (int a = 0; a < A; ++a) {
+            tma_load_2d(sq + a * kAT * 128, &tm_qkv, qd_full + st, h * HD + a * 64, row_base + i * kAT);
+            tma_load_2d(sq + L::kT + a * kAT * 128, &tm_do, qd_full + st, h * HD + a * 64, row_base + i * kAT);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int qi = lane * 4 + k, q = i * kAT + qi;
+          sL[st * kAT + qi] = q < s ? __ldg(lse_b + q) * 1.4426950408889634f : INFINITY;
+          sD[st * kAT + qi] = q < s ? __ldg(del_b + q) : 0.f;
+        }
+        mbar_arrive(qd_full + st);
+      }
+      // key column sums of this tile (keys < s) -> ksum[item, h, kt, :] for the dQ kernel's common-mode
+      // correction: lane l sums columns l, l + 32 (.. HD) over the tile's rows, off the critical path
+      mbar_wait(kv_full + kvb, (kvi / L::kKV) & 1);
+      const uint8_t* sk = sm + kvb * 2 * L::kT;
+      const int nrow = min(kAT, s - kt * kAT);
+#pragma unroll
+      for (int c0 = 0; c0 < HD; c0 += 32) {
+        const int col = c0 + lane;
+        const uint8_t* katom = sk + (col >> 6) * (kAT * 128);
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
+        for (int r = 0; r < kAT; ++r) {
+          const float v = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+              katom + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4) + (col & 7) * 2));
+          acc[r & 3] += r < nrow ? v : 0.f;
+        }
+        ksum[(((size_t)item * H + h) * nkt + kt) * HD + col] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(kv_empty + kvb);
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer
+    if (lane == 0) {
+      const uint32_t id_s = make_idesc_bf16(kAT, kAT, false, false);  // S^T, dP^T: B K-major
+      const uint32_t id_g = make_idesc_bf16(kAT, HD, false, true);    // dV, dK: B MN-major
+      int kvi = 0, g = 0, acc_i = 0;
+      int use[2] = {0, 0};
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++kvi, ++acc_i) {
+        int item, h, kt, e0, n;
+        Tab128 tv;
+        unit_of(u, item, h, kt, tv, e0, n);
+        const int kvb = kvi % L::kKV;
+        mbar_wait(kv_full + kvb, (kvi / L::kKV) & 1);
+        if (kvi == 0) trace_stamp(1);
+        const uint32_t sk = smem_u32(sm + kvb * 2 * L::kT), sv = sk + L::kT;
+        auto issue_s = [&](int e) {  // S^T(e) = K Q(e)^T into buffer e & 1
+          const int gg = g + e, st = gg % L::kSt;
+          mbar_wait(qd_full + st, (gg / L::kSt) & 1);
+          tc_fence_after();
+          const uint32_t sq = smem_u32(sm + L::kOffRing + st * 2 * L::kT);
+          const uint32_t tb = tmem + (e & 1) * kAT;
+          for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(tb, desc_kmajor(sk, kk), desc_kmajor(sq, kk), id_s, kk != 0);
+          mma_commit(s_full + (e & 1));
+        };
+        if (n > 0) issue_s(0);
+        if (n > 1) issue_s(1);
+        mbar_wait(acc_empty, (acc_i & 1) ^ 1);  // the previous unit's dK / dV have been drained
+        tc_fence_after();
+        // fixed two-deep schedule (deterministic accumulation order dV(0), dV(1), ..., dK(0), dK(1), ...):
+        // per pair (e, e+1): dV/dP of both, then dK of both, each dK followed by the S two entries ahead
+        auto issue_vp = [&](int e) {
+          const int b = e & 1, gg = g + e, st = gg % L::kSt;
+          const uint32_t sq = smem_u32(sm + L::kOffRing + st * 2 * L::kT), sdo = sq + L::kT;
+          const uint32_t tb = tmem + b * kAT;
+          mbar_wait(p_ready + b, use[b] & 1);
+          tc_fence_after();
+          for (int kk = 0; kk < kAT / 16; ++kk) mma_bf16_ts(t_dv, tb + kk * 8, desc_mnmajor(sdo, kk), id_g, (e | kk) != 0);
+          for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(tb, desc_kmajor(sv, kk), desc_kmajor(sdo, kk), id_s, kk != 0);
+          mma_commit(dp_full + b);
+        };
+        auto issue_k = [&](int e) {
+          const int b = e & 1, gg = g + e, st = gg % L::kSt;
+          const uint32_t sq = smem_u32(sm + L::kOffRing + st * 2 * L::kT);
+          const uint32_t tb = tmem + b * kAT;
+          mbar_wait(ds_ready + b, use[b] & 1);
+          tc_fence_after();
+          for (int kk = 0; kk < kAT / 16; ++kk) mma_bf16_ts(t_dk, tb + kk * 8, desc_mnmajor(sq, kk), id_g, (e | kk) != 0);
+          mma_commit(qd_empty + st);
+          ++use[b];
+          if (e + 2 < n) issue_s(e + 2);
+        };
+        for (int e = 0; e < n; e += 2) {
+          issue_vp(e);
+          if (e + 1 < n) issue_vp(e + 1);
+          issue_k(e);
+          if (e + 1 < n) issue_k(e + 1);
+        }
+        if (n > 0) {
+          mma_commit(acc_full);
+          mma_commit(kv_empty + kvb);
+        } else {
+          mbar_arrive(acc_full);
+          mbar_arrive(kv_empty + kvb);
+        }
+        g += n;
+      }
+    }
+  } else {
+    // ================= epilogue warpgroups: wg = (warp - 2) / 4 owns TMEM buffer wg; thread = key row
+    const int wg = (warp - 2) >> 2, quad = warp & 3;
+    const int kr = quad * 32 + lane;
+    const int ep_tid = threadIdx.x - 64;  // 0..255
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const uint32_t tb = tmem + wg * kAT + lane_base;
+    const int cj = kr >> 4;
+    int kvi = 0, g = 0, acc_i = 0, use = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++kvi, ++acc_i) {
+      int item, h, kt, e0, n;
+      Tab128 tv;
+      unit_of(u, item, h, kt, tv, e0, n);
+      const int row_base = item * s;
+      for (int e = wg; e < n; e += 2, ++use) {
+        const int gg = g + e, st = gg % L::kSt;
+        const uint32_t lo = (uint32_t)__ldg(tv.csc_lo + e0 + e), hi = (uint32_t)__ldg(tv.csc_hi + e0 + e);
+        const uint64_t mask = ((uint64_t)hi << 32) | lo;
+        const bool full = mask == ~0ull;
+        const float* l2 = sL + st * kAT;
+        const float* dl = sD + st * kAT;
+        mbar_wait(qd_full + st, (gg / L::kSt) & 1);  // lse / delta staged with the tiles
+        mbar_wait(s_full + wg, use & 1);
+        const bool tr = kvi == 0 && e < 4 && (ep_tid & 127) == 0;
+        if (tr) trace_stamp(2 + 4 * e);
+        tc_fence_after();
+        uint32_t pp[4][16];  // P^T (bf16 pairs) for the whole row, reused by dS^T
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t sv_[2][32];
+          tmem_ld_32x32b_x32(tb + h2 * 64, sv_[0]);
+          tmem_ld_32x32b_x32(tb + h2 * 64 + 32, sv_[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const int c = h2 * 2 + c2;
+#pragma unroll
+            for (int u2 = 0; u2 < 16; ++u2) {
+              const int qi = c * 32 + 2 * u2;
+              const float p0 = ex2(fmaf(__uint_as_float(sv_[c2][2 * u2]), scale_log2, -l2[qi]));
+              const float p1 = ex2(fmaf(__uint_as_float(sv_[c2][2 * u2 + 1]), scale_log2, -l2[qi + 1]));
+              const bool on = full || ((mask >> ((qi >> 4) * 8 + cj)) & 1ull);
+              pp[c][u2] = on ? pack_bf16x2(p0, p1) : 0u;
+            }
+            tmem_st_32x32b_x16(tb + c * 16, pp[c]);  // S^T chunk c/2 already consumed
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_ready + wg);
+        if (tr) trace_stamp(3 + 4 * e);
+        mbar_wait(dp_full + wg, use & 1);
+        if (tr) trace_stamp(4 + 4 * e);
+        tc_fence_after();
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t dv_[2][32];
+          tmem_ld_32x32b_x32(tb + h2 * 64, dv_[0]);
+          tmem_ld_32x32b_x32(tb + h2 * 64 + 32, dv_[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const int c = h2 * 2 + c2;
+            uint32_t dd[16];
+#pragma unroll
+            for (int u2 = 0; u2 < 16; ++u2) {
+              const int qi = c * 32 + 2 * u2;
+              const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pp[c][u2]);
+              dd[u2] = pack_bf16x2(__low2float(pb) * (__uint_as_float(dv_[c2][2 * u2]) - dl[qi]),
+                                   __high2float(pb) * (__uint_as_float(dv_[c2][2 * u2 + 1]) - dl[qi + 1]));
+            }
+            tmem_st_32x32b_x16(tb + c * 16, dd);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ds_ready + wg);
+        if (tr) trace_stamp(5 + 4 * e);
+      }
+      // ---- unit epilogue: WG0 stores dK (scaled), WG1 dV; then the key tile's column sums
+      mbar_wait(acc_full, acc_i & 1);
+      if (kvi == 0 && ep_tid == 0) trace_stamp(18);
+      tc_fence_after();
+      // dK / dV rows -> bf16 through a per-warp staging tile, stored as full 128-byte row segments
+      const uint32_t tcol = (wg == 0 ? t_dk : t_dv) + lane_base;
+      const float mul = wg == 0 ? scale : 1.f;
+      uint8_t* stg = sm + L::kOffStg + (warp - 2) * 32 * L::kStgPitch;
+#pragma unroll
+      for (int cp = 0; cp < HD / 64; ++cp) {
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) {
+          uint32_t ov[32];
+          tmem_ld_32x32b_x32(tcol + cp * 64 + c2 * 32, ov);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float f[8];
+#pragma unroll
+            for (int k2 = 0; k2 < 8; ++k2) f[k2] = n > 0 ? __uint_as_float(ov[8 * i + k2]) * mul : 0.f;
+            *reinterpret_cast<uint4*>(stg + lane * L::kStgPitch + c2 * 64 + 16 * i) =
+                make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                           pack_bf16x2(f[6], f[7]));
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int pass = 0; pass < 8; ++pass) {  // lane -> row pass*4 + lane/8, 16-byte piece lane%8
+          const int rr = pass * 4 + (lane >> 3), piece = lane & 7;
+          const int key = kt * kAT + quad * 32 + rr;
+          if (key < s) {
+            const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * L::kStgPitch + piece * 16);
+            *reinterpret_cast<uint4*>(dkv + ((size_t)row_base + key) * ld_dkv + (wg + 1) * d_model + h * HD + cp * 64 +
+                                      piece * 8) = v;
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // every epilogue thread has drained TMEM
+      if (ep_tid == 0) {
+        if (kvi == 0) trace_stamp(19);
+        if (kvi == 1) trace_stamp(20);
+        mbar_arrive(acc_empty);
+      }
+      g += n;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 template <int HD>
 static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                          int H, const int32_t* pidx, int item_stride, const int32_t* tables128, float scale,
@@ -911,8 +1276,20 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
   LX_CHECK_CUDA(a2);
   dim3 grid((s + kAT - 1) / kAT, H, n_items);
   const float sl2 = scale * 1.4426950408889634f;
+  // the ping-pong kernel's ring + staging fit in shared memory for HD 64; HD 128 keeps the 2-CTA kernel
+  static const bool old_bwd = getenv("LX_ATTN_BWD_OLD") != nullptr || AttnDkdvPP<HD>::kTotal > 227 * 1024;
+  if (old_bwd) {
   launch_k(bsattn_dkdv_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
                                                      lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);
+  } else {
+    constexpr int smem_pp = AttnDkdvPP<HD>::kTotal;
+    static cudaError_t a3 = cudaFuncSetAttribute(bsattn_dkdv_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pp);
+    LX_CHECK_CUDA(a3);
+    const int n_units = (int)grid.x * H * n_items;
+    launch_k(bsattn_dkdv_pp_kernel<HD>, std::min(n_units, num_sms()), kBwdThreads, smem_pp, st, tm_qkv, tm_do, s, H,
+             n_units, pidx, item_stride, tables128, scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d,
+             ksum);
+  }
   if ((rc = launch_check("bsattn_dkdv_tc"))) return rc;
   launch_k(bsattn_dq_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
                                                    lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);

@@ -1,6 +1,6 @@
-"""Phase timeline of the tcgen05 attention dK/dV kernel at cfg3 layer shapes (debug stamps, clock64).
-Per CTA: 0 start, 1 K/V landed, per q-tile e<4: 2+6e q/dO landed (S MMA issue), 3+6e S in TMEM,
-4+6e P stored, 5+6e dP in TMEM, 6+6e dS stored; 26 last dK MMA done; 27 epilogue end."""
+"""Phase timeline of the persistent ping-pong dK/dV kernel at cfg3 layer shapes (debug stamps, clock64).
+Per CTA (its first unit): 0 start, 1 K/V landed; per q-tile e<4 (WG e%2): 2+4e S ready, 3+4e P stored,
+4+4e dP ready, 5+4e dS stored; 18 dK/dV done, 19 unit epilogue done; 20 second unit done."""
 import sys
 from pathlib import Path
 
@@ -31,22 +31,16 @@ def run():
 for _ in range(3):
     run()
 torch.cuda.synchronize()
-n_cta = (s // 128) * H * B
-buf = torch.zeros(n_cta, 32, dtype=torch.int64, device=dev)
+buf = torch.zeros(4096, 32, dtype=torch.int64, device=dev)
 _abi.call("lx_debug_set_attn_trace", buf.data_ptr())
 run()
 torch.cuda.synchronize()
 _abi.call("lx_debug_set_attn_trace", None)
-t = buf.cpu().numpy().astype(np.int64)  # the dq kernel runs last and overwrites slots it stamps; dkdv slots are its own
-t0 = t[:, 0:1]
-rel = t - t0
-print(f"CTA lifetime (0 -> 27) mean {np.mean(t[:, 27] - t[:, 0]):.0f} cycles")
+t = buf.cpu().numpy().astype(np.int64)[:148]
+rel = t - t[:, 0:1]
 print(f"start -> K/V landed {np.mean(rel[:, 1]):.0f}")
 for e in range(4):
-    b = 2 + 6 * e
-    print(f"e={e}: qdO {np.mean(rel[:, b]):7.0f}  S {np.mean(rel[:, b+1]):7.0f}  P {np.mean(rel[:, b+2]):7.0f}  "
-          f"dP {np.mean(rel[:, b+3]):7.0f}  dS {np.mean(rel[:, b+4]):7.0f}")
-print(f"dK done {np.mean(rel[:, 26]):.0f}  epi end {np.mean(rel[:, 27]):.0f}")
-sm = t[:, 31]
-span = [t[sm == i, 27].max() - t[sm == i, 0].min() for i in np.unique(sm)]
-print(f"per-SM busy span mean {np.mean(span):.0f} cycles over {len(span)} SMs; CTAs per SM {n_cta / len(span):.1f}")
+    b = 2 + 4 * e
+    print(f"e={e} (WG{e % 2}): S {np.mean(rel[:, b]):7.0f}  P {np.mean(rel[:, b + 1]):7.0f}  dP {np.mean(rel[:, b + 2]):7.0f}  "
+          f"dS {np.mean(rel[:, b + 3]):7.0f}")
+print(f"unit0 dK/dV done {np.mean(rel[:, 18]):.0f}  epilogue done {np.mean(rel[:, 19]):.0f}  unit1 done {np.mean(rel[:, 20]):.0f}")
