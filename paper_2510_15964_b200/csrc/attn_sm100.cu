@@ -1255,6 +1255,312 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
   }
 }
 
+// ============================================================================ backward dQ, ping-pong
+// Same structure as the dK/dV kernel over query-tile units (CSR walk over key tiles): WG w takes the
+// unit's entries e = w, w + 2, ... with its own S/dP TMEM buffer; per entry the MMA issuer computes
+// S = Q K^T, dP = dO V^T (after the WG pulled P into registers) and dQ += dS K (after the WG wrote the
+// bf16 dS back over its dP), in the fixed order dP(e) dP(e+1) dQ(e) dQ(e+1) (deterministic sums).
+// The bf16 row-sum residual eps of dS (see bsattn_dq_tc_kernel) is summed per WG and combined in a
+// fixed order at the unit end before the common-mode correction.
+template <int HD>
+struct AttnDqPP {
+  static constexpr int kT = (HD / 64) * kAT * 128;
+  static constexpr int kQB = HD == 64 ? 2 : 1;  // Q/dO buffers (next unit prefetched)
+  static constexpr int kSt = HD == 64 ? 3 : 2;  // K/V ring stages
+  static constexpr int kOffRing = kQB * 2 * kT;
+  static constexpr int kOffMisc = kOffRing + kSt * 2 * kT;  // kbar [128] + eps [2][128]
+  static constexpr int kStgPitch = 80;                      // staging row: 64 B of bf16 + 16 B pad
+  static constexpr int kOffStg = kOffMisc + 384 * 4;        // [8 warps][32 rows][kStgPitch]
+  static constexpr int kOffBar = kOffStg + 8 * 32 * kStgPitch;
+  static constexpr int kTotal = kOffBar + 512 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, int s, int H,
+                    int n_units, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
+                    float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
+                    __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ ksum) {
+  using L = AttnDqPP<HD>;
+  constexpr int A = HD / 64;
+  const int d_model = H * HD;
+  const int nqt = (s + kAT - 1) / kAT;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = align_smem_1024(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
+  uint64_t* q_full = bars;        // [kQB]
+  uint64_t* q_empty = bars + 2;   // [kQB]
+  uint64_t* kv_full = bars + 4;   // [kSt]
+  uint64_t* kv_empty = bars + 8;  // [kSt]
+  uint64_t* s_full = bars + 12;   // [2]
+  uint64_t* p_done = bars + 14;   // [2] 4 warps
+  uint64_t* dp_full = bars + 16;  // [2]
+  uint64_t* ds_ready = bars + 18; // [2] 4 warps
+  uint64_t* acc_full = bars + 20;
+  uint64_t* acc_empty = bars + 21;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  float* kbar = reinterpret_cast<float*>(sm + L::kOffMisc);
+  float* eps_x = kbar + 128;  // [2][128]
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+    for (int i = 0; i < L::kQB; ++i) {
+      mbar_init(q_full + i, 1);
+      mbar_init(q_empty + i, 1);
+    }
+    for (int i = 0; i < L::kSt; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(p_done + i, 4);
+      mbar_init(dp_full + i, 1);
+      mbar_init(ds_ready + i, 4);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait_trigger();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_dq = tmem + 2 * kAT;
+
+  auto unit_of = [&](int u, int& item, int& h, int& qt, Tab128& tv, int& e0, int& n) {
+    qt = u % nqt;
+    h = (u / nqt) % H;
+    item = u / (nqt * H);
+    tv = tab128(tables, __ldg(pidx + item * item_stride + h));
+    e0 = __ldg(tv.row_ptr + qt);
+    n = __ldg(tv.row_ptr + qt + 1) - e0;
+  };
+
+  if (warp == 0) {
+    // ================= producer: Q/dO per unit, then the unit's K/V tiles
+    if (lane == 0) {
+      int qi_ = 0, g = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++qi_) {
+        int item, h, qt, e0, n;
+        Tab128 tv;
+        unit_of(u, item, h, qt, tv, e0, n);
+        const int row_base = item * s;
+        const int qb = qi_ % L::kQB;
+        mbar_wait(q_empty + qb, ((qi_ / L::kQB) & 1) ^ 1);
+        uint8_t* sq = sm + qb * 2 * L::kT;
+        mbar_arrive_expect_tx(q_full + qb, 2 * L::kT);
+        for (int a = 0; a < A; ++a) {
+          tma_load_2d(sq + a * kAT * 128, &tm_qkv, q_full + qb, h * HD + a * 64, row_base + qt * kAT);
+          tma_load_2d(sq + L::kT + a * kAT * 128, &tm_do, q_full + qb, h * HD + a * 64, row_base + qt * kAT);
+        }
+        for (int e = 0; e < n; ++e, ++g) {
+          const int st = g % L::kSt;
+          mbar_wait(kv_empty + st, ((g / L::kSt) & 1) ^ 1);
+          const int j = __ldg(tv.csr_col + e0 + e);
+          uint8_t* skv = sm + L::kOffRing + st * 2 * L::kT;
+          mbar_arrive_expect_tx(kv_full + st, 2 * L::kT);
+          for (int a = 0; a < A; ++a) {
+            tma_load_2d(skv + a * kAT * 128, &tm_qkv, kv_full + st, d_model + h * HD + a * 64, row_base + j * kAT);
+            tma_load_2d(skv + L::kT + a * kAT * 128, &tm_qkv, kv_full + st, 2 * d_model + h * HD + a * 64,
+                        row_base + j * kAT);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer
+    if (lane == 0) {
+      const uint32_t id_s = make_idesc_bf16(kAT, kAT, false, false);
+      const uint32_t id_g = make_idesc_bf16(kAT, HD, false, true);
+      int qi_ = 0, g = 0, acc_i = 0;
+      int use[2] = {0, 0};
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++qi_, ++acc_i) {
+        int item, h, qt, e0, n;
+        Tab128 tv;
+        unit_of(u, item, h, qt, tv, e0, n);
+        const int qb = qi_ % L::kQB;
+        mbar_wait(q_full + qb, (qi_ / L::kQB) & 1);
+        const uint32_t sq = smem_u32(sm + qb * 2 * L::kT), sdo = sq + L::kT;
+        auto issue_s = [&](int e) {  // S(e) = Q K(e)^T into buffer e & 1
+          const int gg = g + e, st = gg % L::kSt;
+          mbar_wait(kv_full + st, (gg / L::kSt) & 1);
+          tc_fence_after();
+          const uint32_t sk = smem_u32(sm + L::kOffRing + st * 2 * L::kT);
+          const uint32_t tb = tmem + (e & 1) * kAT;
+          for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(tb, desc_kmajor(sq, kk), desc_kmajor(sk, kk), id_s, kk != 0);
+          mma_commit(s_full + (e & 1));
+        };
+        auto issue_p = [&](int e) {  // dP(e) = dO V(e)^T once the WG pulled P(e) into registers
+          const int b = e & 1, gg = g + e, st = gg % L::kSt;
+          const uint32_t sv = smem_u32(sm + L::kOffRing + st * 2 * L::kT) + L::kT;
+          const uint32_t tb = tmem + b * kAT;
+          mbar_wait(p_done + b, use[b] & 1);
+          tc_fence_after();
+          for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(tb, desc_kmajor(sdo, kk), desc_kmajor(sv, kk), id_s, kk != 0);
+          mma_commit(dp_full + b);
+        };
+        auto issue_q = [&](int e) {  // dQ += dS(e) K(e)
+          const int b = e & 1, gg = g + e, st = gg % L::kSt;
+          const uint32_t sk = smem_u32(sm + L::kOffRing + st * 2 * L::kT);
+          const uint32_t tb = tmem + b * kAT;
+          mbar_wait(ds_ready + b, use[b] & 1);
+          tc_fence_after();
+          for (int kk = 0; kk < kAT / 16; ++kk) mma_bf16_ts(t_dq, tb + kk * 8, desc_mnmajor(sk, kk), id_g, (e | kk) != 0);
+          mma_commit(kv_empty + st);
+          ++use[b];
+          if (e + 2 < n) issue_s(e + 2);
+        };
+        if (n > 0) issue_s(0);
+        if (n > 1) issue_s(1);
+        mbar_wait(acc_empty, (acc_i & 1) ^ 1);  // the previous unit's dQ has been drained
+        tc_fence_after();
+        for (int e = 0; e < n; e += 2) {
+          issue_p(e);
+          if (e + 1 < n) issue_p(e + 1);
+          issue_q(e);
+          if (e + 1 < n) issue_q(e + 1);
+        }
+        if (n > 0) {
+          mma_commit(acc_full);
+          mma_commit(q_empty + qb);
+        } else {
+          mbar_arrive(acc_full);
+          mbar_arrive(q_empty + qb);
+        }
+        g += n;
+      }
+    }
+  } else {
+    // ================= epilogue warpgroups: wg owns TMEM buffer wg; thread = query row
+    const int wg = (warp - 2) >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int ep_tid = threadIdx.x - 64;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const uint32_t tb = tmem + wg * kAT + lane_base;
+    const int ci = r >> 4;
+    uint8_t* stg = sm + L::kOffStg + (warp - 2) * 32 * L::kStgPitch;
+    int acc_i = 0, use = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++acc_i) {
+      int item, h, qt, e0, n;
+      Tab128 tv;
+      unit_of(u, item, h, qt, tv, e0, n);
+      const int row_base = item * s;
+      const int row = qt * kAT + r;
+      const size_t lrow = ((size_t)item * H + h) * s + (row < s ? row : 0);
+      const float l2 = __ldg(lse + lrow) * 1.4426950408889634f, dl = __ldg(delta + lrow);
+      float eps = 0.f;
+      for (int e = wg; e < n; e += 2, ++use) {
+        const uint32_t lo = (uint32_t)__ldg(tv.csr_lo + e0 + e), hi = (uint32_t)__ldg(tv.csr_hi + e0 + e);
+        const uint32_t mrow = (uint32_t)((((uint64_t)hi << 32) | lo) >> (ci * 8)) & 0xffu;
+        mbar_wait(s_full + wg, use & 1);
+        tc_fence_after();
+        uint32_t pp[4][16];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t sv_[2][32];
+          tmem_ld_32x32b_x32(tb + h2 * 64, sv_[0]);
+          tmem_ld_32x32b_x32(tb + h2 * 64 + 32, sv_[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const int c = h2 * 2 + c2;
+#pragma unroll
+            for (int u2 = 0; u2 < 16; ++u2) {
+              const bool on = (mrow >> (c * 2 + (u2 >> 3))) & 1u;
+              const float p0 = ex2(fmaf(__uint_as_float(sv_[c2][2 * u2]), scale_log2, -l2));
+              const float p1 = ex2(fmaf(__uint_as_float(sv_[c2][2 * u2 + 1]), scale_log2, -l2));
+              pp[c][u2] = on ? pack_bf16x2(p0, p1) : 0u;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_done + wg);
+        mbar_wait(dp_full + wg, use & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t dv_[2][32];
+          tmem_ld_32x32b_x32(tb + h2 * 64, dv_[0]);
+          tmem_ld_32x32b_x32(tb + h2 * 64 + 32, dv_[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const int c = h2 * 2 + c2;
+            uint32_t dd[16];
+#pragma unroll
+            for (int u2 = 0; u2 < 16; ++u2) {
+              const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pp[c][u2]);
+              dd[u2] = pack_bf16x2(__low2float(pb) * (__uint_as_float(dv_[c2][2 * u2]) - dl),
+                                   __high2float(pb) * (__uint_as_float(dv_[c2][2 * u2 + 1]) - dl));
+              const __nv_bfloat162 rb = *reinterpret_cast<const __nv_bfloat162*>(&dd[u2]);
+              eps += __low2float(rb) + __high2float(rb);
+            }
+            tmem_st_32x32b_x16(tb + c * 16, dd);  // dP chunk c/2 already consumed
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ds_ready + wg);
+      }
+      // ---- unit epilogue: eps of both warpgroups (fixed order), key mean kbar, dQ rows (WG w: columns
+      // [w HD/2, (w+1) HD/2)) through the staging tile as 64-byte row segments
+      eps_x[wg * 128 + r] = eps;
+      if (wg == 0 && r < HD) {
+        const float* ks = ksum + ((size_t)item * H + h) * ((s + kAT - 1) / kAT) * HD + r;
+        float acc = 0.f;
+        for (int t = 0; t < (s + kAT - 1) / kAT; ++t) acc += __ldg(ks + t * HD);
+        kbar[r] = acc / (float)s;
+      }
+      mbar_wait(acc_full, acc_i & 1);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      tc_fence_after();
+      const float eps_row = eps_x[r] + eps_x[128 + r];
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        const int col0 = wg * (HD / 2) + c * 32;
+        uint32_t ov[32];
+        tmem_ld_32x32b_x32(t_dq + lane_base + col0, ov);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float f[8];
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2)
+            f[k2] = n > 0 ? (__uint_as_float(ov[8 * i + k2]) - eps_row * kbar[col0 + 8 * i + k2]) * scale : 0.f;
+          *reinterpret_cast<uint4*>(stg + lane * L::kStgPitch + 16 * i) =
+              make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int pass = 0; pass < 4; ++pass) {  // lane -> row pass*8 + lane/4, 16-byte piece lane%4
+          const int rr = pass * 8 + (lane >> 2), piece = lane & 3;
+          const int qrow = qt * kAT + quad * 32 + rr;
+          if (qrow < s)
+            *reinterpret_cast<uint4*>(dq + ((size_t)row_base + qrow) * ld_dq + h * HD + col0 + piece * 8) =
+                *reinterpret_cast<const uint4*>(stg + rr * L::kStgPitch + piece * 16);
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // TMEM drained, eps_x / kbar reusable
+      if (ep_tid == 0) mbar_arrive(acc_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 template <int HD>
 static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                          int H, const int32_t* pidx, int item_stride, const int32_t* tables128, float scale,
@@ -1291,8 +1597,18 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
              ksum);
   }
   if ((rc = launch_check("bsattn_dkdv_tc"))) return rc;
-  launch_k(bsattn_dq_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
+  if (old_bwd || AttnDqPP<HD>::kTotal > 227 * 1024) {
+    launch_k(bsattn_dq_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
                                                    lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);
+  } else {
+    constexpr int smem_dq = AttnDqPP<HD>::kTotal;
+    static cudaError_t a4 = cudaFuncSetAttribute(bsattn_dq_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_dq);
+    LX_CHECK_CUDA(a4);
+    const int n_units = (int)grid.x * H * n_items;
+    launch_k(bsattn_dq_pp_kernel<HD>, std::min(n_units, num_sms()), kBwdThreads, smem_dq, st, tm_qkv, tm_do, s, H,
+             n_units, pidx, item_stride, tables128, scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d,
+             ksum);
+  }
   return launch_check("bsattn_dq_tc");
 }
 
