@@ -16,4 +16,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-
   --log-file gpurun_out/${tag}_launches.csv python tools/profile_step.py > gpurun_out/${tag}_launches.log 2>&1; echo launches rc=$?
 python tools/summarize_launches.py gpurun_out/${tag}_launches.csv 30 > gpurun_out/${tag}_launches.txt 2>&1
 head -32 gpurun_out/${tag}_launches.txt
-bash tools/ncu_full.sh ${tag} fc1:'gemm_sm100_kernel<(\(int\))?3, (\(int\))?2,' attnfwd:bsattn_fwd_tc_kernel dkdv:bsattn_dkdv_tc_kernel dq:bsattn_dq_tc_kernel mask:'gemm_sm100_kernel<(\(int\))?0, (\(int\))?6,'
+bash tools/ncu_full.sh ${tag} fc1:'gemm_sm100_kernel<(\(int\))?3, (\(int\))?2,' attnfwd:bsattn_fwd_tc_kernel dkdv:bsattn_dkdv_pp_kernel dq:bsattn_dq_pp_kernel colgrad:colgrad_group_kernel lnf:ln_fwd_warp mask:'gemm_sm100_kernel<(\(int\))?0, (\(int\))?6,'
