@@ -154,13 +154,13 @@ __global__ void rowproj_wpack_kernel(const float* __restrict__ w, long long w_sk
 // One 16B load per row (g, g+8) then serves two MMA steps, and the packed W ([q][k], hi/lo bf16)
 // is read the same way. A CTA owns 16 rows; kRpWarps warps take interleaved 32-k blocks (kRpU in
 // flight each) and reduce through shared memory.
-constexpr int kRpWarps = 8, kRpU = 8;
+constexpr int kRpWarps = 8, kRpU = 4;  // 2 CTAs per SM: the 16-row CTAs of M = 4096 fit in one wave
 
 // W pack: wp + item * w_item_stride holds [2][RP][Kp] (hi, lo); with `ids` the pack is the FULL W
 // (shared by the items, w_item_stride 0) and packed k maps to ids[item][k / blk] * blk + k % blk.
 // yb (optional): bf16 copy of Y (the LoRA rows of a K-extended projection GEMM operand).
 template <int NT>
-__global__ void __launch_bounds__(32 * kRpWarps) rowproj_mma2_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int s, int K,
+__global__ void __launch_bounds__(32 * kRpWarps, 2) rowproj_mma2_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int s, int K,
                                                            int Kp, int r, float scale, const int32_t* __restrict__ counts,
                                                            int blk, const __nv_bfloat16* __restrict__ wp,
                                                            long long w_item_stride, const int32_t* __restrict__ ids,
