@@ -1585,7 +1585,7 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
   // the ping-pong kernel's ring + staging fit in shared memory for HD 64; HD 128 keeps the 2-CTA kernel
   static const bool old_bwd = getenv("LX_ATTN_BWD_OLD") != nullptr || AttnDkdvPP<HD>::kTotal > 227 * 1024;
   if (old_bwd) {
-  launch_k(bsattn_dkdv_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
+    launch_k(bsattn_dkdv_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
                                                      lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);
   } else {
     constexpr int smem_pp = AttnDkdvPP<HD>::kTotal;
