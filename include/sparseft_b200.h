@@ -237,6 +237,10 @@ int lx_layernorm_fwd(const float* x, const uint16_t* delta, float* resid_out, in
                      const float* beta, float eps, uint16_t* y, int ldy, float* mean, float* inv_std, int s, int m_small,
                      uint16_t* x_small, lx_stream_t stream);
 /* (delta != NULL: fused residual add — resid_out = x + delta (fp32) is normalised and returned.) */
+/* optimizer_step (sf/autograd.py:203-225) over the flat trainable buffer: float64 moments m, v, fp32 params,
+ * fp32 mean gradients; step t (>= 1) gives the bias corrections 1 - b1^t, 1 - b2^t. One pass. */
+int lx_adam_step(float* params, const float* grads, double* m, double* v, long long n, double lr, double b1, double b2,
+                 double eps, int t, lx_stream_t stream);
 /* loss_forward + loss_backward over rows of fp32 logits (sf/model.py:454-472): row_loss[r] =
  * logsumexp(l_r) - l_r[t_r]; grad_bf16[r] = (softmax(l_r) - onehot(t_r)) * inv_s (inv_s = 1/seq_len). */
 int lx_cross_entropy(const float* logits, int rows, int V, const int64_t* targets, float inv_s, float* row_loss,

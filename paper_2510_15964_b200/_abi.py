@@ -54,6 +54,7 @@ SIGNATURES: dict[str, list] = {
     "lx_bsattn_bwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P, _P],
     "lx_layernorm_fwd": [_P, _P, _P, _I, _I, _P, _P, _F, _P, _I, _P, _P, _I, _I, _P, _P],
     "lx_cross_entropy": [_P, _I, _I, _P, _F, _P, _P, _P],
+    "lx_adam_step": [_P, _P, _P, _P, _LL, _D, _D, _D, _D, _I, _P],
     "lx_layernorm_bwd": [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P],
 }
 RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_group_ws_floats": _LL, "lx_rowproj_ws_bytes": _LL}

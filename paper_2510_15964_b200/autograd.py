@@ -299,16 +299,19 @@ def optimizer_step(state: M.PeftState, grads: dict, lr: float, betas=(0.9, 0.999
         raise GradientError(f"optimizer grads mismatch: missing={sorted(missing)}, extra={sorted(extra)}")
     b1, b2 = betas
     state.step += 1
-    g = torch.empty_like(state.m)
+    g = torch.empty_like(state.flat)
     for name, p in state.params.items():
         off = (p.data_ptr() - state.flat.data_ptr()) // 4
-        g[off : off + p.numel()] = grads[name].reshape(-1).double()
-    adam_flat(state.flat, g, state.m, state.v, lr, b1, b2, eps, state.step)
+        g[off : off + p.numel()] = grads[name].reshape(-1)
+    _abi.call("lx_adam_step", state.flat.data_ptr(), g.data_ptr(), state.m.data_ptr(), state.v.data_ptr(),
+              state.flat.numel(), float(lr), float(b1), float(b2), float(eps), state.step,
+              _abi.stream_handle(state.flat.device))
     return state
 
 
 def adam_flat(p: torch.Tensor, g64: torch.Tensor, m: torch.Tensor, v: torch.Tensor, lr, b1, b2, eps, t) -> None:
-    """Adam on the flat buffer (float64 moments), same update order as sf/autograd.py:218-224."""
+    """Adam on the flat buffer with torch ops (float64 moments, sf/autograd.py:218-224): the test
+    reference of lx_adam_step."""
     m.mul_(b1).add_(g64, alpha=1 - b1)
     v.mul_(b2).addcmul_(g64, g64, value=1 - b2)
     upd = (m / (1 - b1**t)) / ((v / (1 - b2**t)).sqrt_() + eps) * lr

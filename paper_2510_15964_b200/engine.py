@@ -43,7 +43,6 @@ class FinetuneEngine:
         self.loss_chunk = loss_chunk
         self.grad_hook = grad_hook  # called with the flat mean-gradient buffer (e.g. NCCL all-reduce)
         self.flat_grad = torch.zeros_like(state.flat)
-        self.flat_grad64 = torch.zeros_like(state.m)
         self.graph = None
         self.static_tokens = None
         self.static_loss = None
@@ -88,9 +87,11 @@ class FinetuneEngine:
         if self.grad_hook is not None:
             self.grad_hook(self.flat_grad)
         self.state.step += 1
-        self.flat_grad64.copy_(self.flat_grad)
-        AG.adam_flat(self.state.flat, self.flat_grad64, self.state.m, self.state.v, self.lr, 0.9, 0.999, 1e-8,
-                     self.state.step)
+        from . import _abi
+
+        st = self.state
+        _abi.call("lx_adam_step", st.flat.data_ptr(), self.flat_grad.data_ptr(), st.m.data_ptr(), st.v.data_ptr(),
+                  st.flat.numel(), float(self.lr), 0.9, 0.999, 1e-8, st.step, _abi.stream_handle(st.flat.device))
 
     def step(self, tokens) -> torch.Tensor:
         """Eager step (tokens host or device). Returns the loss as a device scalar."""

@@ -309,3 +309,31 @@ def test_colgrad_group_mixed_problems():
     N.colgrad_group(probs, n_items, s)
     torch.cuda.synchronize()
     assert torch.equal(g1, g1b)
+
+
+def test_adam_step_kernel():
+    """lx_adam_step (one pass, float64 moments) vs the reference update order of sf/autograd.py:218-224
+    evaluated in float64 with NumPy, over three steps."""
+    from paper_2510_15964_b200 import _abi
+
+    dev = _dev()
+    rng = np.random.default_rng(4)
+    n = 100003
+    p0 = rng.standard_normal(n).astype(np.float32) * 0.02
+    p = torch.from_numpy(p0.copy()).to(dev)
+    m = torch.zeros(n, dtype=torch.float64, device=dev)
+    v = torch.zeros(n, dtype=torch.float64, device=dev)
+    pr, mr, vr = p0.copy(), np.zeros(n), np.zeros(n)
+    lr, b1, b2, eps = 1e-3, 0.9, 0.999, 1e-8
+    for t in range(1, 4):
+        g = rng.standard_normal(n).astype(np.float32) * 1e-3
+        _abi.call("lx_adam_step", p.data_ptr(), torch.from_numpy(g).to(dev).data_ptr(), m.data_ptr(), v.data_ptr(), n, lr,
+                  b1, b2, eps, t, _abi.stream_handle())
+        torch.cuda.synchronize()
+        gd = g.astype(np.float64)
+        mr = b1 * mr + (1 - b1) * gd
+        vr = b2 * vr + (1 - b2) * gd * gd
+        pr -= (lr * (mr / (1 - b1**t)) / (np.sqrt(vr / (1 - b2**t)) + eps)).astype(np.float32)
+    assert np.abs(m.cpu().numpy() - mr).max() <= 1e-15
+    assert np.abs(v.cpu().numpy() - vr).max() <= 1e-15
+    assert np.abs(p.cpu().numpy() - pr).max() <= 1e-7
