@@ -72,7 +72,7 @@ __global__ void mask_compact_kernel(const uint32_t* __restrict__ bits, int n_ite
   }
   __syncthreads();
   if (threadIdx.x == 0) counts[item] = s_total;
-  // tail of ids beyond the count is left untouched (never read)
+  for (int j = s_total + threadIdx.x; j < n_blk; j += blockDim.x) my_ids[j] = 0;  // defined tail (no fill launch)
 }
 
 // membership of block (i, j) in pool pattern (kind, p) — sf/patterns.py:63-85

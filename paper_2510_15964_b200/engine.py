@@ -38,9 +38,13 @@ def lm_head_loss_and_grad(hf: torch.Tensor, emb: torch.Tensor, targets: torch.Te
 class FinetuneEngine:
     """Fused fine-tune step over a batch of B sequences of length s (tokens [B, s+1])."""
 
-    def __init__(self, model: M.Model, state: M.PeftState, provider, lr: float, loss_chunk: int = 1024, grad_hook=None):
+    def __init__(self, model: M.Model, state: M.PeftState, provider, lr: float, loss_chunk: int = 0, grad_hook=None):
         self.model, self.state, self.provider, self.lr = model, state, provider, lr
-        self.loss_chunk = loss_chunk
+        import os
+
+        # LM-head row chunk: the fp32 logits of a chunk ([chunk, V]) should stay L2-resident between the
+        # cuBLAS GEMM that writes them and the CE kernel's two sweeps
+        self.loss_chunk = loss_chunk or int(os.environ.get("LX_LOSS_CHUNK", "1024"))
         self.grad_hook = grad_hook  # called with the flat mean-gradient buffer (e.g. NCCL all-reduce)
         self.flat_grad = torch.zeros_like(state.flat)
         self.graph = None

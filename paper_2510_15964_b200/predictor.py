@@ -163,7 +163,7 @@ def mlp_masks(h: torch.Tensor, n_items: int, s: int, params: MlpPredictorParams,
     words = (n_blk + 31) // 32
     bits = torch.empty(n_items, words, dtype=torch.int32, device=dev)
     counts = torch.empty(n_items, dtype=torch.int32, device=dev)
-    ids = torch.zeros(n_items, n_blk, dtype=torch.int32, device=dev)
+    ids = torch.empty(n_items, n_blk, dtype=torch.int32, device=dev)  # tail zeroed by the compaction kernel
     pos = torch.empty(n_items, n_blk, dtype=torch.int32, device=dev)
     sc = torch.empty(n_items * s, n_blk, dtype=torch.float32, device=dev) if dump else None
     _abi.call("lx_predict_mlp_mask", h.data_ptr(), n_items, s, d, wa.data_ptr(), n_blk, float(threshold), int(scope_batch),
