@@ -117,6 +117,7 @@ static int launch_gemm_auto(const CUtensorMap& ta, const CUtensorMap& tb1, const
                             const GemmArgs& args, cudaStream_t st) {
   if (g_cta_pair == 2) return launch_gemm<BMODE, EPI, 128, 2>(ta, tb4, args, st);
   if (g_cta_pair == 1) return launch_gemm<BMODE, EPI, 256, 2>(ta, tb2, args, st);
+  if (g_cta_pair == 3) return launch_gemm<BMODE, EPI, 128, 1>(ta, tb2, args, st);  // single CTA, 128 x 128 tiles
   return launch_gemm<BMODE, EPI, 256, 1>(ta, tb1, args, st);
 }
 
@@ -169,7 +170,7 @@ int lx_debug_set_gemm_trace(unsigned long long* buf) {
 
 int lx_gemm_set_cta_pair(int mode) {
   const int prev = g_cta_pair;
-  g_cta_pair = (mode == 1 || mode == 2) ? mode : 0;
+  g_cta_pair = (mode >= 1 && mode <= 3) ? mode : 0;
   return prev;
 }
 

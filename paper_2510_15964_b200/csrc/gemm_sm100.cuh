@@ -114,6 +114,7 @@ struct GemmSmem {
 
 struct TileInfo {
   int item, mt, nt;
+  int n0;        // first packed/dense column of this tile
   int n_cols;    // valid packed/dense columns in this tile
   int k_stages;  // K pipeline stages
   int k_total;   // K extent (elements)
@@ -140,7 +141,16 @@ LX_DEV TileInfo decode_tile(const GemmArgs& a, const int* prefix, const int* cnt
   ti.nt = local / m_tiles;
   int cnt = BMODE == kDense ? 0 : __ldg(cnts + lo);
   int n_total = is_ng<BMODE>() ? cnt * a.blk : a.n_dense;
-  ti.n_cols = min(BN, n_total - ti.nt * BN);
+  // an item's active columns are split into equal-width tiles (multiples of 16, <= BN): no short last
+  // tile whose CTA idles while the full ones finish
+  int w = BN;
+  if (is_ng<BMODE>()) {
+    const int nt_item = (n_total + BN - 1) / BN;
+    const int q = a.blk > 16 ? a.blk : 16;  // whole neuron blocks (gather boxes are per block)
+    if (nt_item > 0) w = min(BN, ((n_total + nt_item - 1) / nt_item + q - 1) / q * q);
+  }
+  ti.n0 = ti.nt * w;
+  ti.n_cols = min(w, n_total - ti.n0);
   ti.k_total = is_kg<BMODE>() ? cnt * a.blk : a.k_dense;
   ti.k_stages = (ti.k_total + kBK - 1) / kBK;
   return ti;
@@ -220,7 +230,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       int nb_n = 0;
       if (BMODE == kNGather) {
         nb_n = (ti.n_cols + args.blk - 1) / args.blk;
-        if ((int)lane < nb_n) my_row = __ldg(ids + ti.nt * BN / args.blk + lane) * args.blk;
+        if ((int)lane < nb_n) my_row = __ldg(ids + ti.n0 / args.blk + lane) * args.blk;
       }
       for (int ks = 0; ks < ti.k_stages; ++ks) {
         uint8_t* sa = smem + stage * L::kStageBytes;
@@ -238,12 +248,12 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           if (lane == 0) {
             if (leader) mbar_arrive_expect_tx(full + stage, 2 * (L::kABytes + L::kBBytes));
             tma_load_2d_cg2(sa, &tmap_a, full + stage, ks * kBK, row0, pol_w);
-            if (BMODE == kDense) tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.nt * BN + rank * BNC, pol_w);
+            if (BMODE == kDense) tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.n0 + rank * BNC, pol_w);
             if (BMODE == kPackedN)
-              tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.item * args.packed_stride + ti.nt * BN + rank * BNC, pol_w);
+              tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.item * args.packed_stride + ti.n0 + rank * BNC, pol_w);
             if (BMODE == kPackedK)
               for (int a = 0; a < BNC / 64; ++a)
-                tma_load_2d_cg2(sb + a * (kBK * 128), &tmap_b, full + stage, ti.nt * BN + rank * BNC + a * 64,
+                tma_load_2d_cg2(sb + a * (kBK * 128), &tmap_b, full + stage, ti.n0 + rank * BNC + a * 64,
                                 ti.item * args.packed_stride + ks * kBK, pol_w);
           }
           __syncwarp();
@@ -257,12 +267,12 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           else bytes += nb_k * (BN / 64) * args.blk * 128;
           mbar_arrive_expect_tx(full + stage, bytes);
           tma_load_2d(sa, &tmap_a, full + stage, ks * kBK, row0);
-          if (BMODE == kDense) tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.nt * BN, pol_w);
+          if (BMODE == kDense) tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.n0, pol_w);
           if (BMODE == kPackedN)  // rows [nt*BN, nt*BN+BN) of this item's packed copy, one box
-            tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.item * args.packed_stride + ti.nt * BN, pol_w);
+            tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.item * args.packed_stride + ti.n0, pol_w);
           if (BMODE == kPackedK)  // 64 packed K-rows x BN columns: one box per 64-column atom
             for (int a = 0; a < BN / 64; ++a)
-              tma_load_2d_hint(sb + a * (kBK * 128), &tmap_b, full + stage, ti.nt * BN + a * 64,
+              tma_load_2d_hint(sb + a * (kBK * 128), &tmap_b, full + stage, ti.n0 + a * 64,
                                ti.item * args.packed_stride + ks * kBK, pol_w);
         }
         if (BMODE == kNGather) {
@@ -271,7 +281,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         } else if (BMODE == kKGather) {
           const int j = lane / (BN / 64), a = lane % (BN / 64);
           if (j < nb_k)
-            tma_load_2d_hint(sb + a * (kBK * 128) + j * args.blk * 128, &tmap_b, full + stage, ti.nt * BN + a * 64,
+            tma_load_2d_hint(sb + a * (kBK * 128) + j * args.blk * 128, &tmap_b, full + stage, ti.n0 + a * 64,
                              my_k_row, pol_w);
         }
         __syncwarp();
@@ -340,7 +350,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       if (kLora) {
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
         for (int c = ep_tid; c < BN; c += 32 * kEpiWarps) {
-          int j = ti.nt * BN + c;
+          int j = ti.n0 + c;
           int oc = j;
           if (is_ng<BMODE>()) oc = (c < ti.n_cols) ? __ldg(ids + j / args.blk) * args.blk + j % args.blk : 0;
           bool ok = c < ti.n_cols;
@@ -380,7 +390,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
         const int c0 = ch * 32;
         const int nv = min(32, ti.n_cols - c0);
-        const int j0 = ti.nt * BN + c0;  // packed / dense column of v[0]
+        const int j0 = ti.n0 + c0;  // packed / dense column of v[0]
 
         if (EPI == kEpiMask) {
           uint32_t word = 0;

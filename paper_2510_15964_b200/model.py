@@ -541,6 +541,9 @@ def linear(a: torch.Tensor, b_t: torch.Tensor, out_f32: bool = False, resid: tor
 
 
 QKV_SLOT = {"wq": 0, "wk": 1, "wv": 2}
+# LX_NO_PACK=1: MLP GEMMs gather the active neuron blocks straight from W (one TMA box per block)
+# instead of streaming item-packed copies (experiments)
+_NO_PACK = __import__("os").environ.get("LX_NO_PACK", "0") == "1"
 
 
 def _qkv_lora(lora: dict, d: int):
@@ -613,8 +616,9 @@ def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, c
     nm = lower_mask(neuron_mask, dims.n_blk, blk, B, x2.device)
     ad1, ad2 = lora.get("w1"), lora.get("w2")
     # active rows of W1^T and W2 packed per item once per layer; reused by the backward's input-grads
-    w1p = neuron_ops.pack_active_rows(lw.mlp.w1_t, nm)
-    w2p = neuron_ops.pack_active_rows(lw.mlp.w2, nm)
+    pack = not _NO_PACK
+    w1p = neuron_ops.pack_active_rows(lw.mlp.w1_t, nm) if pack else None
+    w2p = neuron_ops.pack_active_rows(lw.mlp.w2, nm) if pack else None
     lp = lw.lora_pack
     if ad1 is None:
         ax1 = None
