@@ -427,7 +427,7 @@ def run_reference(args, cfg, rank) -> dict | None:
     if rank != 0:
         return None
     cpu = cpu_baseline(cfg, args)
-    return {"impl": "reference", "metric": "OPT-1.3B LoRA fwd+bwd ms/batch", "value": cpu["value"], "unit": "ms/batch",
+    return {"impl": "reference", "metric": f"{cfg['desc']} LoRA fwd+bwd ms/batch", "value": cpu["value"], "unit": "ms/batch",
             "n_gpus": int(os.environ.get("WORLD_SIZE", 1)), "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": cpu["value"], "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": "cfg3 (as ours), reference algorithm on host cores", "model": cfg["desc"],
