@@ -245,7 +245,7 @@ def run_ours(args, cfg, rank, world, dist):
     from paper_2510_15964_b200.dense_baseline import DenseLoraStep
     from paper_2510_15964_b200.engine import FinetuneEngine
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1))
     torch.cuda.set_device(dev)
     peaks = load_peaks()
     model, state, provider = build_workload(cfg, dev, seed=args.seed, mlp_sparsity=args.mlp_sparsity,
@@ -466,8 +466,9 @@ def main():
         import torch
         import torch.distributed as tdist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        tdist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1))
+        # NCCL over NVLink in production; LX_DIST_BACKEND=gloo lets several ranks share one GPU (plumbing checks)
+        tdist.init_process_group(os.environ.get("LX_DIST_BACKEND", "nccl"))
         dist = tdist
     line = run_ours(args, cfg, rank, world, dist)
     if rank == 0:
