@@ -100,26 +100,34 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
   const int item0 = scope_batch ? 0 : blockIdx.y;
   const int item1 = scope_batch ? n_items : blockIdx.y + 1;
   const int ldp = 2 * H * r;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, n_warps = blockDim.x >> 5;
   __shared__ float s_hat[kMaxM * kMaxM];
   __shared__ unsigned char cell[kMaxM * kMaxM];
   __shared__ float s_red[32];
-  __shared__ unsigned long long s_cnt[kMaxPool + 1][2];  // [pattern][0]=mass, [1]=active blocks
-  extern __shared__ float s_qk[];  // [2][m][r+1]: this (item, head)'s Q_hat and K_hat rows
+  __shared__ int s_cnt[kMaxPool + 1][2];  // [pattern][0] = mass, [1] = active blocks; [kMaxPool][0] = total
+  __shared__ int s_pool[2][kMaxPool];     // pool kinds / parameters (loaded once, off the coverage loop)
+  extern __shared__ float s_qk[];          // [2][m][rs]: this (item, head)'s Q_hat and K_hat rows
   const int mm = m * m;
-  const int rs = r + 1;            // padded row stride: conflict-free column walks
+  const bool vec = (r & 3) == 0;
+  const int rs = vec ? r + 4 : r + 1;      // 16B-aligned rows (float4 path) / odd stride (scalar path)
   for (int e = threadIdx.x; e < mm; e += blockDim.x) cell[e] = 0;
+  if (threadIdx.x < (kMaxPool + 1) * 2) (&s_cnt[0][0])[threadIdx.x] = 0;
+  if (threadIdx.x < n_pool) {
+    s_pool[0][threadIdx.x] = __ldg(pool_kind + threadIdx.x);
+    s_pool[1][threadIdx.x] = __ldg(pool_param + threadIdx.x);
+  }
   for (int item = item0; item < item1; ++item) {
     __syncthreads();
-    if ((r & 3) == 0) {
+    if (vec) {
       // float4 loads, issued in batches of 8 before any store (one round trip per batch)
-      const int nq = 2 * m * (r / 4);
+      const int r4 = r / 4, nq = 2 * m * r4;
       for (int e0 = threadIdx.x; e0 < nq; e0 += 8 * blockDim.x) {
         float4 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int e = e0 + u * blockDim.x;
           if (e < nq) {
-            const int which = e / (m * (r / 4)), rem = e % (m * (r / 4)), i = rem / (r / 4), t4 = rem % (r / 4);
+            const int which = e / (m * r4), rem = e % (m * r4), i = rem / r4, t4 = rem % r4;
             v[u] = __ldg(reinterpret_cast<const float4*>(proj + (size_t)(item * m + i) * ldp + (which ? H + h : h) * r) + t4);
           }
         }
@@ -127,9 +135,8 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
         for (int u = 0; u < 8; ++u) {
           const int e = e0 + u * blockDim.x;
           if (e < nq) {
-            const int which = e / (m * (r / 4)), rem = e % (m * (r / 4)), i = rem / (r / 4), t = 4 * (rem % (r / 4));
-            float* dst = s_qk + (which * m + i) * rs + t;
-            dst[0] = v[u].x; dst[1] = v[u].y; dst[2] = v[u].z; dst[3] = v[u].w;
+            const int which = e / (m * r4), rem = e % (m * r4), i = rem / r4, t4 = rem % r4;
+            reinterpret_cast<float4*>(s_qk + (which * m + i) * rs)[t4] = v[u];
           }
         }
       }
@@ -140,34 +147,47 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
       }
     }
     __syncthreads();
-    // S_hat = (X Wq)(X Wk)^T  (sf/predictor.py:74-76)
-    for (int e = threadIdx.x; e < mm; e += blockDim.x) {
-      const int i = e / m, j = e % m;
+    // S_hat = (X Wq)(X Wk)^T  (sf/predictor.py:74-76): warp w takes rows i = w, w + n_warps, ..., lane j a
+    // column; q_i is a warp broadcast, k_j rows are conflict-free (row stride rs = r + 4 / r + 1). Four
+    // partial sums over t mod 4 combined in a fixed order: deterministic.
+    for (int i = warp; i < m; i += n_warps) {
       const float* qr = s_qk + i * rs;
-      const float* kr = s_qk + (m + j) * rs;
-      // four independent partial sums (ILP); fixed combination order -> deterministic
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-      int t = 0;
-      for (; t + 4 <= r; t += 4) {
-        a0 = fmaf(qr[t], kr[t], a0);
-        a1 = fmaf(qr[t + 1], kr[t + 1], a1);
-        a2 = fmaf(qr[t + 2], kr[t + 2], a2);
-        a3 = fmaf(qr[t + 3], kr[t + 3], a3);
+      for (int j = lane; j < m; j += 32) {
+        const float* kr = s_qk + (m + j) * rs;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        if (vec) {
+#pragma unroll 8
+          for (int t = 0; t < r; t += 4) {
+            const float4 q4 = *reinterpret_cast<const float4*>(qr + t), k4 = *reinterpret_cast<const float4*>(kr + t);
+            a0 = fmaf(q4.x, k4.x, a0);
+            a1 = fmaf(q4.y, k4.y, a1);
+            a2 = fmaf(q4.z, k4.z, a2);
+            a3 = fmaf(q4.w, k4.w, a3);
+          }
+        } else {
+          int t = 0;
+          for (; t + 4 <= r; t += 4) {
+            a0 = fmaf(qr[t], kr[t], a0);
+            a1 = fmaf(qr[t + 1], kr[t + 1], a1);
+            a2 = fmaf(qr[t + 2], kr[t + 2], a2);
+            a3 = fmaf(qr[t + 3], kr[t + 3], a3);
+          }
+          for (; t < r; ++t) a0 = fmaf(qr[t], kr[t], a0);
+        }
+        const float acc = (a0 + a1) + (a2 + a3);
+        s_hat[i * m + j] = acc;
+        if (dump) dump[((size_t)item * H + h) * mm + i * m + j] = acc;
       }
-      for (; t < r; ++t) a0 = fmaf(qr[t], kr[t], a0);
-      const float acc = (a0 + a1) + (a2 + a3);
-      s_hat[e] = acc;
-      if (dump) dump[((size_t)item * H + h) * mm + e] = acc;
     }
     __syncthreads();
     // per-matrix max (sf/predictor.py:89)
     float mx = -INFINITY;
     for (int e = threadIdx.x; e < mm; e += blockDim.x) mx = fmaxf(mx, s_hat[e]);
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mx;
+    if (lane == 0) s_red[warp] = mx;
     __syncthreads();
     if (threadIdx.x < 32) {
-      float v = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : -INFINITY;
+      float v = threadIdx.x < n_warps ? s_red[threadIdx.x] : -INFINITY;
       for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
       if (threadIdx.x == 0) s_red[0] = v;
     }
@@ -175,44 +195,49 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
     // threshold = fp32(frac) * peak rounded to fp32; strict '>' (sf/predictor.py:90, NEP 50)
     const float thr = __fmul_rn(frac, s_red[0]);
     for (int e = threadIdx.x; e < mm; e += blockDim.x) cell[e] |= (s_hat[e] > thr) ? 1 : 0;  // OR over batch
-    __syncthreads();
   }
-  // upsample (sf/predictor.py:79-84) + integer coverage counts per pattern (sf/exposer.py:71-85):
-  // block-wide predicate counts (__syncthreads_count), cells in chunks of blockDim
-  if (threadIdx.x < (kMaxPool + 1) * 2) (&s_cnt[0][0])[threadIdx.x] = 0ull;
   __syncthreads();
+  // upsample (sf/predictor.py:79-84) + integer coverage counts per pattern (sf/exposer.py:71-85): per-thread
+  // counts, warp sums, one shared atomic per warp and counter (integers: order-independent)
   const int cells = n_b * n_b;
-  for (int e0 = 0; e0 < cells; e0 += blockDim.x) {
-    const int e = e0 + threadIdx.x;
-    bool on = false;
-    int i = 0, j = 0;
-    if (e < cells) {
-      i = e / n_b;
-      j = e % n_b;
-      const int si = min((int)(((long long)i * m) / n_b), m - 1);
-      const int sj = min((int)(((long long)j * m) / n_b), m - 1);
-      on = cell[si * m + sj] != 0;
+  int tot = 0, mass[kMaxPool], nnz[kMaxPool];
+#pragma unroll
+  for (int p = 0; p < kMaxPool; ++p) mass[p] = nnz[p] = 0;
+  for (int e = threadIdx.x; e < cells; e += blockDim.x) {
+    const int i = e / n_b, j = e % n_b;
+    const int si = min((int)(((long long)i * m) / n_b), m - 1);
+    const int sj = min((int)(((long long)j * m) / n_b), m - 1);
+    const bool on = cell[si * m + sj] != 0;
+    tot += on;
+#pragma unroll
+    for (int p = 0; p < kMaxPool; ++p) {
+      if (p < n_pool) {
+        const bool in = pool_member(s_pool[0][p], s_pool[1][p], i, j);
+        nnz[p] += in;
+        mass[p] += in && on;
+      }
     }
-    const int tot_c = __syncthreads_count(on);
-    if (threadIdx.x == 0) s_cnt[kMaxPool][0] += (unsigned long long)tot_c;
-    for (int p = 0; p < n_pool; ++p) {
-      const bool in = e < cells && pool_member(__ldg(pool_kind + p), __ldg(pool_param + p), i, j);
-      const int n_in = __syncthreads_count(in);
-      const int n_mass = __syncthreads_count(in && on);
-      if (threadIdx.x == 0) {
-        s_cnt[p][0] += (unsigned long long)n_mass;
-        s_cnt[p][1] += (unsigned long long)n_in;
+  }
+  tot = __reduce_add_sync(0xffffffffu, tot);
+  if (lane == 0 && tot) atomicAdd(&s_cnt[kMaxPool][0], tot);
+#pragma unroll
+  for (int p = 0; p < kMaxPool; ++p) {
+    if (p < n_pool) {
+      const int m32 = __reduce_add_sync(0xffffffffu, mass[p]), n32 = __reduce_add_sync(0xffffffffu, nnz[p]);
+      if (lane == 0) {
+        if (m32) atomicAdd(&s_cnt[p][0], m32);
+        if (n32) atomicAdd(&s_cnt[p][1], n32);
       }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned long long tot = s_cnt[kMaxPool][0];
+    const int total = s_cnt[kMaxPool][0];
     int dense = n_pool - 1;  // dense is always last in the pool
     int best = -1;
-    if (tot > 0) {
+    if (total > 0) {
       for (int p = 0; p < n_pool; ++p) {
-        double frac_cov = (double)s_cnt[p][0] / (double)tot;
+        double frac_cov = (double)s_cnt[p][0] / (double)total;
         if (frac_cov >= tau - 1e-9 && (best < 0 || s_cnt[p][1] < s_cnt[best][1])) best = p;
       }
     }
@@ -287,7 +312,7 @@ int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, i
   int rc = lx_gemm_bf16_tn(x_small, d, wqk_t, d, proj_ws, 2 * H * r, 1, n_items * m, 2 * H * r, d, stream);
   if (rc) return rc;
   dim3 grid(H, scope_batch ? 1 : n_items);
-  const size_t smem = sizeof(float) * 2 * m * (r + 1);
+  const size_t smem = sizeof(float) * 2 * m * (r + 4);
   LX_REQUIRE(smem <= 200 * 1024, LX_ERR_UNSUPPORTED, "predictor rank %d x m %d exceeds shared memory", r, m);
   static cudaError_t attr = cudaFuncSetAttribute(attn_pattern_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   LX_CHECK_CUDA(attr);
