@@ -244,6 +244,44 @@ def sweep_attn(args, timer, peak):
     return rows
 
 
+def sweep_exposer(args, timer, peaks):
+    """Exposer oracle mode (csrc/exposer.cu) at the cfg2 layer shape: exact block masses (fp32 dot
+    products + float64 softmax: bound by the FP32/FP64 pipes, reported against the FP32 FFMA peak at
+    the measured max clock), coverage selection, MLP block importance (HBM-bound: one read of z) and
+    the whole OracleProvider per layer (cuBLAS projections included) next to PredictedProvider."""
+    import torch
+
+    from paper_2510_15964_b200 import exposer as EX, patterns as PT, predictor as P
+
+    c = CFG2
+    d, H, hd, f, s, B, blk = c["d"], c["H"], c["hd"], c["d_ff"], c["s"], c["B"], c["blk"]
+    M = B * s
+    fp32_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    g = torch.Generator(device="cuda").manual_seed(0)
+    qk = torch.randn(M, 2 * d, device="cuda", generator=g)
+    z = torch.randn(M, f, device="cuda", generator=g)
+    rows = []
+    for ab in args.attn_blk:
+        n_b = s // ab
+        dp = P._pool_dev(PT.build_pool(n_b), torch.device("cuda"))
+        ms = timer(lambda: EX.exact_block_mass(qk, B, s, H, n_b), args.reps)
+        rows.append(line("exposer_exact_block_mass", "fwd", 0.0, ms, 2 * B * H * s * s * hd, fp32_peak,
+                         {"n_b": n_b, "peak_kind": "fp32 FFMA", "exps_f64": 2 * B * H * s * s}))
+        mass = EX.exact_block_mass(qk, B, s, H, n_b)
+        for hs in (False, True):
+            ms = timer(lambda: EX.select_by_coverage(mass, dp, 0.95, head_sum=hs), args.reps)
+            print(json.dumps({"op": "exposer_select_by_coverage", "head_sum": hs, "n_b": n_b, "ms": round(ms, 4)}),
+                  flush=True)
+    ms = timer(lambda: EX.block_importance(z, B, s, blk), args.reps)
+    gbs = M * f * 4 / (ms * 1e-3) / 1e9
+    print(json.dumps({"op": "exposer_block_importance", "ms": round(ms, 4), "bytes": M * f * 4, "gbs": round(gbs, 1),
+                      "frac_of_hbm": round(gbs / peaks["hbm"], 3)}), flush=True)
+    imp = EX.block_importance(z, B, s, blk)
+    ms = timer(lambda: EX.filter_neuron_blocks(imp, 0.1, blk), args.reps)
+    print(json.dumps({"op": "exposer_filter_neuron_blocks", "ms": round(ms, 4)}), flush=True)
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
@@ -270,6 +308,8 @@ def main():
         sweep_mlp(args, timer, peak)
     if "attn" in ops:
         sweep_attn(args, timer, peak)
+    if "exposer" in ops:
+        sweep_exposer(args, timer, peaks)
 
 
 if __name__ == "__main__":

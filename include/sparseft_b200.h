@@ -19,6 +19,7 @@
 #ifndef SPARSEFT_B200_H
 #define SPARSEFT_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -250,6 +251,29 @@ int lx_cross_entropy(const float* logits, int rows, int V, const int64_t* target
  * optionally also writes bf16(dx_accum) to dx_bf16 (the next GEMM's operand). */
 int lx_layernorm_bwd(const void* dy, int dy_is_f32, const float* x, const float* gamma, const float* mean,
                      const float* inv_std, int M, int d, float* dx_accum, uint16_t* dx_bf16, lx_stream_t stream);
+
+
+/* ------------------------------------------------------------------ exposer oracle mode (verification)
+ * exact_attention + block_mass (sf/exposer.py:47-68): q, k fp32 rows [n_items*s, ld] (head h at columns
+ * h*hd; the frozen projections x W_Q + b_Q, x W_K + b_K, no LoRA). mass: float64 [n_items, H, n_b, n_b],
+ * the per-head softmax probabilities (float64, like the reference) summed over each block. */
+size_t lx_exact_mass_smem(int s, int hd);
+int lx_exact_block_mass(const float* q, const float* k, int ld, int n_items, int s, int H, int hd, int n_b,
+                        double* mass, lx_stream_t stream);
+/* select_pattern_by_coverage per grid (sf/exposer.py:71-91, OracleProvider._attn sf/harness.py:165-167);
+ * head_sum = 1 sums the heads' grids first (ShadowyProvider._attn sf/harness.py:183-187) and writes the
+ * one choice to every head. pattern_idx int32 [n_items, H]. */
+int lx_select_by_coverage(const double* mass, int n_items, int H, int n_b, const int32_t* pool_kind,
+                          const int32_t* pool_param, int n_pool, double tau, int head_sum, int32_t* pattern_idx,
+                          lx_stream_t stream);
+/* block_importance (sf/exposer.py:94-98): imp fp32 [n_items, ceil(n_cols/blk)] = max over the item's s
+ * rows and the block's columns of |relu(z)|; z fp32 rows [n_items*s, ldz]. */
+int lx_block_importance(const float* z, int ldz, int n_items, int s, int n_cols, int blk, float* imp,
+                        lx_stream_t stream);
+/* filter_neuron_blocks (sf/exposer.py:101-111) per item: bit b of bits [n_items, ceil(n_blk/32)] set iff
+ * (double)imp[b] > theta * peak; all-zero importance -> no bits. Lower with lx_mask_compact. */
+int lx_filter_neuron_blocks(const float* imp, int n_items, int n_blk, double theta, uint32_t* bits,
+                            lx_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -288,6 +288,55 @@ def block_mass(weight: np.ndarray, n_b: int) -> np.ndarray:
     return weight.reshape(n_b, blk, n_b, blk).sum(axis=(1, 3))
 
 
+def exact_attention(x, wq, bq, wk, bk, n_heads: int):
+    """sf/exposer.py:47-59: per-head (probabilities, raw scores). q, k in the input dtype; the
+    np.float64 scale 1/sqrt(head_dim) promotes raw scores (and so the softmax) to float64."""
+    q = x @ wq + bq
+    k = x @ wk + bk
+    return exact_attention_qk(q, k, n_heads)
+
+
+def exact_attention_qk(q, k, n_heads: int):
+    """exact_attention from given projections (sf/exposer.py:51-59; softmax sf/tensor_core.py:85-91)."""
+    hd = q.shape[1] // n_heads
+    scale = 1.0 / np.sqrt(hd)
+    probs, raws = [], []
+    for h in range(n_heads):
+        sl = slice(h * hd, (h + 1) * hd)
+        raw = (q[:, sl] @ k[:, sl].T) * scale
+        sh = raw - raw.max(axis=1, keepdims=True)
+        e = np.exp(sh)
+        raws.append(raw)
+        probs.append(e / e.sum(axis=1, keepdims=True))
+    return probs, raws
+
+
+def select_head_pattern(probs_h, pool: dict, tau: float = 0.95) -> str:
+    """sf/exposer.py:88-91."""
+    n_b = _pool_nb(pool)
+    return select_pattern_by_coverage(block_mass(probs_h, n_b), pool, tau)
+
+
+def _pool_nb(pool: dict) -> int:
+    """Grid side of a pool (its dense pattern holds every cell)."""
+    return int(round(math.sqrt(len(pool["dense"]))))
+
+
+def shadowy_pattern(probs, pool: dict, tau: float) -> str:
+    """ShadowyProvider._attn (sf/harness.py:183-187): one pattern for all heads from the summed masses."""
+    n_b = _pool_nb(pool)
+    mass = sum(block_mass(p, n_b) for p in probs)
+    return select_pattern_by_coverage(mass, pool, tau)
+
+
+def oracle_mlp_mask(h, w1, b1, lora_a, lora_b, scaling, blk: int, theta: float):
+    """OracleProvider._mlp (sf/harness.py:169-176): z = h W1 + b1 (+ s (h A) B), importance, filter."""
+    z = h @ w1 + b1
+    if lora_a is not None:
+        z = z + scaling * ((h @ lora_a) @ lora_b)
+    return filter_neuron_blocks(block_importance(z, blk), theta), z
+
+
 # ---------------------------------------------------------------------------
 # block-sparse attention operators (sf/block_sparse.py:47-150), vectorised
 

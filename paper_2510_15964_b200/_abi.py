@@ -56,8 +56,13 @@ SIGNATURES: dict[str, list] = {
     "lx_cross_entropy": [_P, _I, _I, _P, _F, _P, _P, _P],
     "lx_adam_step": [_P, _P, _P, _P, _LL, _D, _D, _D, _D, _I, _P],
     "lx_layernorm_bwd": [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P],
+    "lx_exact_mass_smem": [_I, _I],
+    "lx_exact_block_mass": [_P, _P, _I, _I, _I, _I, _I, _I, _P, _P],
+    "lx_select_by_coverage": [_P, _I, _I, _I, _P, _P, _I, _D, _I, _P, _P],
+    "lx_block_importance": [_P, _I, _I, _I, _I, _I, _P, _P],
+    "lx_filter_neuron_blocks": [_P, _I, _I, _D, _P, _P],
 }
-RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_group_ws_floats": _LL, "lx_rowproj_ws_bytes": _LL}
+RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_group_ws_floats": _LL, "lx_rowproj_ws_bytes": _LL, "lx_exact_mass_smem": C.c_size_t}
 
 
 
@@ -99,10 +104,13 @@ def lib() -> C.CDLL:
     return _lib
 
 
+_NON_STATUS = ("lx_abi_version", "lx_device_sm_count", "lx_attn_tables_size", "lx_gemm_set_cta_pair", "lx_exact_mass_smem")
+
+
 def call(name: str, *args) -> int:
     """Invoke an entry point; map a nonzero return code to the reference's exception type."""
     rc = getattr(lib(), name)(*args)
-    if isinstance(rc, int) and rc != 0 and name not in ("lx_abi_version", "lx_device_sm_count", "lx_attn_tables_size", "lx_gemm_set_cta_pair"):
+    if isinstance(rc, int) and rc != 0 and name not in _NON_STATUS:
         msg = lib().lx_last_error().decode(errors="replace")
         raise _ERRORS.get(rc, E.CudaError)(f"{name}: {msg}")
     return rc

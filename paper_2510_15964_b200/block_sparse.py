@@ -73,7 +73,14 @@ def attention_backward(q, k, v, o, d_o, ld: int, n_items: int, s: int, H: int, h
                   delta.data_ptr(), ksum.data_ptr(), dq.data_ptr(), _abi.stream_handle(dev))
         return
     if dq.stride(0) != ld or dk.stride(0) != ld or dv.stride(0) != ld:
-        raise LayoutError("attention_backward (warp-MMA path) expects dq/dk/dv with the row stride of q")
+        # the warp-MMA kernels write dq/dk/dv with q's row stride: stage them (e.g. head_dim 32 under the
+        # K-extended projection operand, whose row stride is 3d + kx)
+        st = [torch.empty(dq.shape[0], ld, dtype=dq.dtype, device=dev) for _ in range(3)]
+        attention_backward(q, k, v, o, d_o, ld, n_items, s, H, hd, pidx, item_stride, dpool, scale, lse,
+                           st[0][:, :d], st[1][:, :d], st[2][:, :d])
+        for dst, src in zip((dq, dk, dv), st):
+            dst.copy_(src[:, :d])
+        return
     _abi.call("lx_bsattn_bwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), d_o.data_ptr(), ld, o.stride(0),
               n_items, s, H, hd,
               pidx.data_ptr(), item_stride, dpool.tables.data_ptr(), len(dpool.ids), float(scale), lse.data_ptr(),

@@ -15,10 +15,10 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import autograd, model as M, predictor as P
+from . import autograd, exposer as EX, model as M, predictor as P
 from .errors import ConfigError
 
-MODES = ("dense", "predicted", "random", "static")
+MODES = ("dense", "shadowy", "exposer-oracle", "predicted", "random", "static")
 
 
 class _TimedProvider:
@@ -103,6 +103,64 @@ class PredictedProvider(_TimedProvider):
         if self.counter is not None:
             self.counter.add(B * (s * d * self.model.dims.n_blk + s))
         return nm
+
+
+class OracleProvider(_TimedProvider):
+    """Ground-truth masks from the exact dense computation (sf/harness.py:157-176); verification
+    mode. Per item: exact block masses of every head -> coverage-selected pool pattern; exact
+    MLP pre-activation -> block importance -> theta filter. Device-resident like PredictedProvider."""
+
+    def __init__(self, model: M.Model, theta: float, tau: float):
+        super().__init__()
+        if not (0 <= theta <= 1):
+            raise ConfigError(f"theta must be in [0, 1], got {theta}")
+        if not (0 < tau <= 1):
+            raise ConfigError(f"coverage tau must be in (0, 1], got {tau}")
+        self.model, self.theta, self.tau = model, theta, tau
+
+    _head_sum = False
+
+    def _attn(self, layer, h, x_small=None):
+        B, s, _ = h.shape
+        dims = self.model.dims
+        mass = EX.exact_block_mass(EX.exact_qk(h, self.model.weights.layers[layer]), B, s, dims.n_heads, dims.n_b)
+        return EX.select_by_coverage(mass, self.model.dpool, self.tau, head_sum=self._head_sum)
+
+    def _mlp(self, layer, h):
+        B, s, _ = h.shape
+        m = self.model
+        ad = m.lora.get((layer, "w1")) if m.peft_method == "lora" else None
+        z = EX.mlp_preactivation(h, m.weights.layers[layer], ad)
+        imp = EX.block_importance(z, B, s, m.dims.blk_size)
+        return EX.filter_neuron_blocks(imp, self.theta, m.dims.blk_size)
+
+
+class ShadowyProvider(OracleProvider):
+    """One attention pattern for all heads from the head-summed block masses; MLP keeps every
+    block any token activates (theta = 0) — sf/harness.py:179-190."""
+
+    _head_sum = True
+
+    def __init__(self, model: M.Model, tau: float):
+        super().__init__(model, theta=0.0, tau=tau)
+
+
+def make_provider(mode: str, model: M.Model, *, predictors=None, theta: float = 0.0, tau: float = 0.95,
+                  seed: int = 0, pcfg=None, counter=None, scope: str = "item") -> _TimedProvider:
+    """sf/harness.py:232-244 (mode names as the reference's RunConfig)."""
+    if mode == "dense":
+        return DenseProvider(model)
+    if mode == "shadowy":
+        return ShadowyProvider(model, tau)
+    if mode == "exposer-oracle":
+        return OracleProvider(model, theta, tau)
+    if mode == "predicted":
+        if predictors is None:
+            raise ConfigError("mode=predicted requires trained predictors")
+        return PredictedProvider(model, predictors, pcfg, counter=counter, scope=scope)
+    if mode == "random":
+        return RandomProvider(model, seed=seed + 10_000)
+    raise ConfigError(f"unknown mode {mode!r}; expected one of {MODES}")
 
 
 class RandomProvider(_TimedProvider):

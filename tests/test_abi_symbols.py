@@ -12,7 +12,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def header_symbols():
     text = (ROOT / "include" / "sparseft_b200.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|long long|const char\*)\s+(lx_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|long long|size_t|const char\*)\s+(lx_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_entry_points():

@@ -220,3 +220,32 @@ def test_finetune_step_predicted_mode(golden):
         assert (rel(v, ref) < 1e-4) if np.abs(ref).max() > 0 else np.abs(v).max() == 0, n
     for n, p in params.items():
         assert np.abs(p - g[f"after/{n}"]).max() <= 1e-3 + 1e-7, n  # |update| <= lr; sign of tiny grads may flip
+
+
+# ---------------------------------------------------------------- exposer oracle mode
+def test_exposer_attention(golden):
+    """exact_attention -> block_mass -> select_head_pattern / shadowy (sf/exposer.py:47-91,
+    sf/harness.py:165-187) against the reference providers' own outputs."""
+    g = golden("exposer")
+    for c in range(int(g["n_att"])):
+        s, n_b, d, H, tau = g[f"att{c}/meta"]
+        n_b, H = int(n_b), int(H)
+        probs, _ = O.exact_attention(g[f"att{c}/x"], g[f"att{c}/wq"], g[f"att{c}/bq"], g[f"att{c}/wk"],
+                                     g[f"att{c}/bk"], H)
+        mass = np.stack([O.block_mass(p, n_b) for p in probs])
+        np.testing.assert_allclose(mass, g[f"att{c}/mass"], rtol=1e-12, atol=1e-15)
+        pool = O.build_pool(n_b)
+        assert [O.select_head_pattern(p, pool, float(tau)) for p in probs] == list(g[f"att{c}/pids"])
+        assert O.shadowy_pattern(probs, pool, float(tau)) == str(g[f"att{c}/shadowy"][0])
+
+
+def test_exposer_mlp(golden):
+    """OracleProvider._mlp (sf/harness.py:169-176) against the reference."""
+    g = golden("exposer")
+    for c in range(int(g["n_mlp"])):
+        s, d, d_ff, blk, theta, r, scaling = g[f"mlp{c}/meta"]
+        a = g.get(f"mlp{c}/a") if int(r) else None
+        b = g.get(f"mlp{c}/b") if int(r) else None
+        mask, _ = O.oracle_mlp_mask(g[f"mlp{c}/h"], g[f"mlp{c}/w1"], g[f"mlp{c}/b1"], a, b, float(scaling), int(blk),
+                                    float(theta))
+        np.testing.assert_array_equal(mask, g[f"mlp{c}/mask"])
