@@ -275,6 +275,17 @@ int lx_block_importance(const float* z, int ldz, int n_items, int s, int n_cols,
 int lx_filter_neuron_blocks(const float* imp, int n_items, int n_blk, double theta, uint32_t* bits,
                             lx_stream_t stream);
 
+
+/* ------------------------------------------------------------------ offline predictor pipeline
+ * mlp_truth_labels (sf/predictor.py:251-259): bits [rows, ceil(ceil(n_cols/blk)/32)], bit b of row t set
+ * iff some z[t, c] > 0 with c in block b; z fp32 rows [rows, ldz]. */
+int lx_block_activity(const float* z, int ldz, int rows, int n_cols, int blk, uint32_t* bits, lx_stream_t stream);
+/* the weighted logistic loss of train_mlp_predictor (sf/predictor.py:281-289) on fp32 logits [rows, ld]
+ * against label bits (lx_block_activity layout): d_logits fp32 [rows, ldd] = dL/dlogits / (rows*n_blk),
+ * row_loss float64 [rows] = the row's summed loss (mean = sum(row_loss) / (rows*n_blk)). */
+int lx_weighted_bce(const float* logits, int ld, int rows, int n_blk, const uint32_t* labels, float pos_w,
+                    float* d_logits, int ldd, double* row_loss, lx_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

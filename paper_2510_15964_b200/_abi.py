@@ -61,6 +61,8 @@ SIGNATURES: dict[str, list] = {
     "lx_select_by_coverage": [_P, _I, _I, _I, _P, _P, _I, _D, _I, _P, _P],
     "lx_block_importance": [_P, _I, _I, _I, _I, _I, _P, _P],
     "lx_filter_neuron_blocks": [_P, _I, _I, _D, _P, _P],
+    "lx_block_activity": [_P, _I, _I, _I, _I, _P, _P],
+    "lx_weighted_bce": [_P, _I, _I, _I, _P, _F, _P, _I, _P, _P],
 }
 RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_group_ws_floats": _LL, "lx_rowproj_ws_bytes": _LL, "lx_exact_mass_smem": C.c_size_t}
 
