@@ -38,7 +38,7 @@ class DenseLoraStep:
         d, H, hd = dims.d_model, dims.n_heads, dims.head_dim
         inp, tgt = tokens[:, :-1], tokens[:, 1:]
         B, s = inp.shape
-        h = m.weights.emb[inp]
+        h = torch.nn.functional.embedding(inp, m.weights.emb)
         for i, lw in enumerate(m.weights.layers):
             x = F.layer_norm(h.float(), (d,), lw.ln1_g, lw.ln1_b, 1e-5).to(torch.bfloat16)
             q = self._lin(x, lw.wq, lw.bq, (i, "wq"))

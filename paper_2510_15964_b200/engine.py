@@ -65,7 +65,7 @@ class FinetuneEngine:
         s = s1 - 1
         inp, tgt = tokens[:, :-1], tokens[:, 1:].reshape(-1)
         M.refresh_lora_packs(m)  # one launch: LoRA factors (updated by Adam) -> bf16 packs / K-extended rows
-        h = m.weights.emb[inp].float()
+        h = torch.nn.functional.embedding(inp, m.weights.emb).float()  # index_select gather, not advanced indexing
         caches = []
         for layer in range(m.dims.n_layers):
             h, c = M.block_forward(h, m, layer, self.provider)

@@ -557,8 +557,21 @@ def _qkv_lora(lora: dict, d: int):
     return tq, a_cat, r
 
 
+def _bias_bf16(lw: LayerWeights, name: str, frozen: bool) -> torch.Tensor:
+    """bf16 copy of a projection bias for the cuBLAS addmm; frozen biases (every PEFT method but BitFit)
+    are converted once per storage instead of once per step."""
+    src = getattr(lw, name)
+    if not frozen:
+        return src.to(torch.bfloat16)
+    cache = lw.__dict__.setdefault("_bias_bf16", {})
+    key = (name, src.data_ptr())
+    if key not in cache:
+        cache[key] = src.to(torch.bfloat16)
+    return cache[key]
+
+
 def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: ModelDims, counter=None, *, dpool=None,
-                x_ext=None):
+                x_ext=None, frozen_bias: bool = False):
     """Block-sparse multi-head attention (sf/model.py:322-360). x: LN1 output bf16 [B, s, d] (or [s, d]).
     The dense projections are plain library GEMMs (cuBLAS, bias in the addmm); each LoRA delta
     s*(xA)B is a rank-r cuBLAS update of its column slice with xA from the skinny rowproj kernel.
@@ -568,17 +581,20 @@ def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: Mode
     d, H, hd = dims.d_model, dims.n_heads, dims.head_dim
     dp = dpool if dpool is not None else device_pool(pool, x2.device, dims.seq_len, dims.attn_blk)
     pidx, stride = resolve_head_patterns(head_patterns, dp, B, H, x2.device)
-    tq, a_cat, r = _qkv_lora(lora, d)
+    tq = [t for t in ("wq", "wk", "wv") if t in lora]
     lp = lw.lora_pack
     ext = bool(tq) and x_ext is not None and lp is not None and lp["kx"] > 0 and lp["tq"] == tuple(tq)
+    # the concatenated A is only an operand of the unfused path (the fused one reads the packs)
+    tq, a_cat, r = _qkv_lora(lora, d) if not ext else (tq, None, lora[tq[0]].rank)
+    bqkv16 = _bias_bf16(lw, "bqkv", frozen_bias)
     ax = None
     if ext:
         # K-extended projection: x_ext = [x | xA_cat] (bf16 LoRA columns written by the rowproj), W_ext rows d.. = s*B
         kx = lp["kx"]
         ax = rowproj_packed(x_ext, B, s, d, lp["a_qkv"], kx, out_bf16=x_ext[:, d:])  # fp32 [M, n*r] for the LoRA grads
-        qkv = torch.addmm(lw.bqkv.to(torch.bfloat16), x_ext, lw.wqkv_ext[: d + kx, : 3 * d])
+        qkv = torch.addmm(bqkv16, x_ext, lw.wqkv_ext[: d + kx, : 3 * d])
     else:
-        qkv = torch.addmm(lw.bqkv.to(torch.bfloat16), x2, lw.wqkv)  # bf16 [M, 3d]
+        qkv = torch.addmm(bqkv16, x2, lw.wqkv)  # bf16 [M, 3d]
     if tq and not ext:
         ax = rowproj(x2, B, s, d, a_cat, a_cat.shape[1], 1, a_cat.shape[1])  # fp32 [M, n*r] (kept for the LoRA grads)
         axb = ax.to(torch.bfloat16)
@@ -590,7 +606,7 @@ def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: Mode
     if counter is not None:
         nnz = sum(dp_nnz(dp, int(i)) for i in pidx.flatten().tolist()) * (B if stride == 0 else 1)
         counter.add(2 * nnz * dims.attn_blk * dims.attn_blk * hd)
-    out = torch.addmm(lw.bo.to(torch.bfloat16), o, lw.wo)  # bf16 [M, d]
+    out = torch.addmm(_bias_bf16(lw, "bo", frozen_bias), o, lw.wo)  # bf16 [M, d]
     ad_o = lora.get("wo")
     ax_o = None
     if ad_o is not None:
@@ -671,7 +687,8 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
         hp = masks.attn_patterns(layer, h1v)
     adapter = model.peft_method == "adapter"
     x2 = c1["x"]  # the block input (materialised by LN1 when x was a pending residual)
-    att, ca = mha_forward(h1v, lw, lora, hp, model.pool, model.dims, counter, dpool=model.dpool, x_ext=c1["y_ext"])
+    att, ca = mha_forward(h1v, lw, lora, hp, model.pool, model.dims, counter, dpool=model.dpool, x_ext=c1["y_ext"],
+                          frozen_bias=model.peft_method != "bitfit")
     caa = None
     if adapter:
         att, caa = adapter_forward(att.float(), model.adapters[(layer, "attn")])
@@ -707,7 +724,7 @@ def model_forward(model: Model, tokens, masks, counter=None):
     B, s = tok.shape
     if ensure_lora_packs(model):
         refresh_lora_packs(model)
-    h = model.weights.emb[tok].float()
+    h = torch.nn.functional.embedding(tok, model.weights.emb).float()
     caches = []
     for layer in range(model.dims.n_layers):
         lm = masks[layer] if isinstance(masks, list) else masks
