@@ -132,7 +132,7 @@ def adapter_backward(dy, ad: M.AdapterLayer, cache, grads: dict, prefix: str):
 
 
 def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims: M.ModelDims, grads: dict,
-                 prefix: str = "", bitfit: bool = False):
+                 prefix: str = "", bitfit: bool = False, cg: "_CgBatch | None" = None):
     """Backward of mlp_forward (sf/autograd.py:78-124). d_out [M, d] (bf16 preferred) -> dx bf16 [M, d]."""
     nm = cache["mask"]
     if neuron_mask is not None and neuron_mask is not nm:
@@ -146,7 +146,8 @@ def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims
     dev = a.device
     dO = _bf16(d_out.reshape(-1, d)).contiguous()
     st = _abi.stream_handle(dev)
-    cg = _CgBatch(grads, B, s)
+    own = cg is None  # a caller-provided batch (block_backward) is flushed by the caller
+    cg = _CgBatch(grads, B, s) if own else cg
     if bitfit:
         cg.add(f"{prefix}b2", (d,), None, dO, d, 1, 1.0, 0, 1)
     ad1, ad2 = lora.get("w1"), lora.get("w2")
@@ -180,12 +181,13 @@ def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims
     _abi.call("lx_neuron_fc1_dgrad", dz.data_ptr(), dz.stride(0), B, s, d, f, blk, lw.mlp.w1_t.data_ptr(),
               nm.counts.data_ptr(), nm.ids.data_ptr(), _abi.ptr(dax1), _abi.ptr(ad1.a if ad1 else None),
               ad1.rank if ad1 else 0, dx.data_ptr(), 0, _abi.ptr(cache.get("w1p")), st)
-    cg.flush()
+    if own:
+        cg.flush()
     return dx
 
 
 def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims, grads: dict, prefix: str = "",
-                 bitfit: bool = False):
+                 bitfit: bool = False, cg: "_CgBatch | None" = None):
     """Backward of mha_forward (sf/autograd.py:127-162); score gradients only on active blocks.
     d_out [M, d] (bf16 preferred) -> dx bf16 [M, d]."""
     B, s = cache["n_items"], cache["s"]
@@ -202,7 +204,8 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
     if ad_o is not None:
         dax_o = rowproj(g, B, s, d, ad_o.b, 1, d, ad_o.rank, scale=ad_o.scaling)
         d_heads.addmm_(dax_o.to(torch.bfloat16), ad_o.a.t().to(torch.bfloat16))
-    cg = _CgBatch(grads, B, s)
+    own = cg is None  # a caller-provided batch (block_backward) is flushed by the caller
+    cg = _CgBatch(grads, B, s) if own else cg
     if ad_o is not None:
         r = ad_o.rank
         cg.add(f"{prefix}wo.lora_a", (d, r), dax_o, cache["o"], d, r, 1.0, 1, r)
@@ -248,7 +251,8 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
         for t in ("wq", "wk", "wv"):
             sl = M.QKV_SLOT[t]
             cg.add(f"{prefix}b{t[1]}", (d,), None, dqkv[:, sl * d : (sl + 1) * d], d, 1, 1.0, 0, 1)
-    cg.flush()
+    if own:
+        cg.flush()
     return dx
 
 
@@ -265,12 +269,17 @@ def block_backward(d_out, model: M.Model, layer: int, cache, masks, grads: dict,
     if adapter:
         d_mlp = adapter_backward(d_out, model.adapters[(layer, "mlp")], cache["mlp_adapter"], grads, f"{prefix}mlp_adapter")
     nm = masks.neuron_mask if masks is not None else None
-    dh2 = mlp_backward(d_mlp, cache["mlp"], lw, lora, nm, model.dims, grads, prefix, bitfit)
+    # the layer's LoRA / BitFit column reductions (MLP then attention) run as one deterministic group
+    # launch after both sublayers (their operands stay referenced by the batch until then)
+    B, s = cache["mlp"]["n_items"], cache["mlp"]["s"]
+    cg = _CgBatch(grads, B, s)
+    dh2 = mlp_backward(d_mlp, cache["mlp"], lw, lora, nm, model.dims, grads, prefix, bitfit, cg=cg)
     dy, dy_bf = layernorm_backward(dh2, cache["ln2"], accumulate_into=d_out if inplace else d_out.clone(), want_bf16=True)
     d_attn = dy_bf
     if adapter:
         d_attn = adapter_backward(dy, model.adapters[(layer, "attn")], cache["attn_adapter"], grads, f"{prefix}attn_adapter")
-    dh1 = mha_backward(d_attn, cache["attn"], lw, lora, model.dims, grads, prefix, bitfit)
+    dh1 = mha_backward(d_attn, cache["attn"], lw, lora, model.dims, grads, prefix, bitfit, cg=cg)
+    cg.flush()
     return layernorm_backward(dh1, cache["ln1"], accumulate_into=dy, want_bf16=True)
 
 
