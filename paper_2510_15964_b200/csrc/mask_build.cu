@@ -18,18 +18,20 @@
 
 namespace lx {
 
+constexpr int kCompactMaxWords = 512;  // n_blk <= 16384 neuron blocks
+
+// bits -> ascending active ids, counts and the inverse map, one CTA per item, fully parallel:
+// per-word popcounts, one warp's exclusive scan over the words, then one thread per block writes
+// its id at (word prefix + popc of the lower bits of its word). No serial per-bit loop.
 __global__ void mask_compact_kernel(const uint32_t* __restrict__ bits, int n_items, int n_blk, int scope_batch,
                                     int32_t* __restrict__ counts, int32_t* __restrict__ ids, int32_t* __restrict__ pos) {
   pdl_wait_trigger();
   const int item = blockIdx.x;
   const int words = (n_blk + 31) / 32;
-  __shared__ int s_scan[1024];
+  __shared__ uint32_t s_v[kCompactMaxWords];
+  __shared__ int s_pre[kCompactMaxWords];
   __shared__ int s_total;
-  // each thread owns a contiguous range of words
-  const int per = (words + blockDim.x - 1) / blockDim.x;
-  const int w0 = threadIdx.x * per;
-  int local = 0;
-  for (int w = w0; w < min(words, w0 + per); ++w) {
+  for (int w = threadIdx.x; w < words; w += blockDim.x) {
     uint32_t v = 0;
     if (scope_batch) {
       for (int b = 0; b < n_items; ++b) v |= bits[(size_t)b * words + w];
@@ -37,42 +39,39 @@ __global__ void mask_compact_kernel(const uint32_t* __restrict__ bits, int n_ite
       v = bits[(size_t)item * words + w];
     }
     if (w == words - 1 && (n_blk & 31)) v &= (1u << (n_blk & 31)) - 1u;
-    local += __popc(v);
+    s_v[w] = v;
   }
-  s_scan[threadIdx.x] = local;
   __syncthreads();
-  // inclusive Hillis-Steele scan over blockDim.x entries
-  for (int off = 1; off < blockDim.x; off <<= 1) {
-    int v = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0;
-    __syncthreads();
-    s_scan[threadIdx.x] += v;
-    __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of the word popcounts: lane owns a contiguous run of words
+    const int lane = threadIdx.x, per = (words + 31) / 32, w0 = lane * per, w1 = min(words, w0 + per);
+    int local = 0;
+    for (int w = w0; w < w1; ++w) local += __popc(s_v[w]);
+    int inc = local;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    int run = inc - local;
+    for (int w = w0; w < w1; ++w) {
+      s_pre[w] = run;
+      run += __popc(s_v[w]);
+    }
+    if (lane == 31) s_total = inc;
   }
-  int base = s_scan[threadIdx.x] - local;
-  if (threadIdx.x == blockDim.x - 1) s_total = s_scan[threadIdx.x];
+  __syncthreads();
   int32_t* my_ids = ids + (size_t)item * n_blk;
   int32_t* my_pos = pos ? pos + (size_t)item * n_blk : nullptr;
-  for (int w = w0; w < min(words, w0 + per); ++w) {
-    uint32_t v = 0;
-    if (scope_batch) {
-      for (int b = 0; b < n_items; ++b) v |= bits[(size_t)b * words + w];
-    } else {
-      v = bits[(size_t)item * words + w];
-    }
-    for (int i = 0; i < 32 && w * 32 + i < n_blk; ++i) {
-      int blk = w * 32 + i;
-      if ((v >> i) & 1u) {
-        my_ids[base] = blk;
-        if (my_pos) my_pos[blk] = base;
-        ++base;
-      } else if (my_pos) {
-        my_pos[blk] = -1;
-      }
-    }
+  for (int b = threadIdx.x; b < n_blk; b += blockDim.x) {
+    const uint32_t v = s_v[b >> 5];
+    const int l = b & 31;
+    const bool on = (v >> l) & 1u;
+    const int r = s_pre[b >> 5] + __popc(v & ((1u << l) - 1u));
+    if (on) my_ids[r] = b;
+    if (my_pos) my_pos[b] = on ? r : -1;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) counts[item] = s_total;
-  for (int j = s_total + threadIdx.x; j < n_blk; j += blockDim.x) my_ids[j] = 0;  // defined tail (no fill launch)
+  const int total = s_total;
+  if (threadIdx.x == 0) counts[item] = total;
+  for (int j = total + threadIdx.x; j < n_blk; j += blockDim.x) my_ids[j] = 0;  // defined tail (no fill launch)
 }
 
 // membership of block (i, j) in pool pattern (kind, p) — sf/patterns.py:63-85
@@ -254,7 +253,8 @@ extern "C" {
 int lx_mask_compact(const uint32_t* bits, int n_items, int n_blk, int scope_batch, int32_t* counts, int32_t* ids,
                     int32_t* pos, lx_stream_t stream) {
   LX_REQUIRE(n_items >= 1 && n_blk >= 1, LX_ERR_SHAPE, "mask_compact: empty shape");
-  launch_k(mask_compact_kernel, n_items, 256, 0, stream, bits, n_items, n_blk, scope_batch, counts, ids, pos);
+  LX_REQUIRE(n_blk <= 32 * kCompactMaxWords, LX_ERR_UNSUPPORTED, "mask_compact: n_blk %d > %d", n_blk, 32 * kCompactMaxWords);
+  launch_k(mask_compact_kernel, n_items, 512, 0, stream, bits, n_items, n_blk, scope_batch, counts, ids, pos);
   return launch_check("mask_compact");
 }
 
