@@ -196,51 +196,44 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
     for (int e = threadIdx.x; e < mm; e += blockDim.x) cell[e] |= (s_hat[e] > thr) ? 1 : 0;  // OR over batch
   }
   __syncthreads();
-  // upsample (sf/predictor.py:79-84) + integer coverage counts per pattern (sf/exposer.py:71-85): per-thread
-  // counts, warp sums, one shared atomic per warp and counter (integers: order-independent)
+  // upsample (sf/predictor.py:79-84) + integer coverage counts per pattern (sf/exposer.py:71-85): warp w
+  // owns patterns w, w + 8 (no per-thread loop over the pool), lanes sweep the grid cells, integer warp
+  // sums (order-free); warp 0 also counts the active cells
   const int cells = n_b * n_b;
-  int tot = 0, mass[kMaxPool], nnz[kMaxPool];
-#pragma unroll
-  for (int p = 0; p < kMaxPool; ++p) mass[p] = nnz[p] = 0;
-  for (int e = threadIdx.x; e < cells; e += blockDim.x) {
-    const int i = e / n_b, j = e % n_b;
-    const int si = min((int)(((long long)i * m) / n_b), m - 1);
-    const int sj = min((int)(((long long)j * m) / n_b), m - 1);
-    const bool on = cell[si * m + sj] != 0;
-    tot += on;
-#pragma unroll
-    for (int p = 0; p < kMaxPool; ++p) {
-      if (p < n_pool) {
-        const bool in = pool_member(s_pool[0][p], s_pool[1][p], i, j);
-        nnz[p] += in;
-        mass[p] += in && on;
-      }
+  for (int p = warp; p < n_pool; p += n_warps) {
+    const int kind = s_pool[0][p], prm = s_pool[1][p];
+    int mass = 0, nnz = 0, tot = 0;
+    for (int e = lane; e < cells; e += 32) {
+      const int i = e / n_b, j = e - (e / n_b) * n_b;
+      const int si = min((i * m) / n_b, m - 1), sj = min((j * m) / n_b, m - 1);
+      const bool on = cell[si * m + sj] != 0;
+      const bool in = pool_member(kind, prm, i, j);
+      nnz += in;
+      mass += in && on;
+      tot += on;
     }
-  }
-  tot = __reduce_add_sync(0xffffffffu, tot);
-  if (lane == 0 && tot) atomicAdd(&s_cnt[kMaxPool][0], tot);
-#pragma unroll
-  for (int p = 0; p < kMaxPool; ++p) {
-    if (p < n_pool) {
-      const int m32 = __reduce_add_sync(0xffffffffu, mass[p]), n32 = __reduce_add_sync(0xffffffffu, nnz[p]);
-      if (lane == 0) {
-        if (m32) atomicAdd(&s_cnt[p][0], m32);
-        if (n32) atomicAdd(&s_cnt[p][1], n32);
-      }
+    mass = __reduce_add_sync(0xffffffffu, mass);
+    nnz = __reduce_add_sync(0xffffffffu, nnz);
+    tot = __reduce_add_sync(0xffffffffu, tot);
+    if (lane == 0) {
+      s_cnt[p][0] = mass;
+      s_cnt[p][1] = nnz;
+      if (p == 0) s_cnt[kMaxPool][0] = tot;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
+    // lane p: fp64 coverage mass/total >= tau - 1e-9 (the reference's float64 division, one per lane);
+    // the winner is the fewest active blocks, then the lowest pool index: min over (nnz, p)
     const int total = s_cnt[kMaxPool][0];
-    int dense = n_pool - 1;  // dense is always last in the pool
-    int best = -1;
-    if (total > 0) {
-      for (int p = 0; p < n_pool; ++p) {
-        double frac_cov = (double)s_cnt[p][0] / (double)total;
-        if (frac_cov >= tau - 1e-9 && (best < 0 || s_cnt[p][1] < s_cnt[best][1])) best = p;
-      }
+    int key = 0x7fffffff;
+    if (total > 0 && lane < n_pool) {
+      const double frac_cov = (double)s_cnt[lane][0] / (double)total;
+      if (frac_cov >= tau - 1e-9) key = (s_cnt[lane][1] << 5) | lane;
     }
-    pattern_idx[(size_t)(scope_batch ? 0 : blockIdx.y) * H + h] = best < 0 ? dense : best;
+    key = __reduce_min_sync(0xffffffffu, key);
+    if (lane == 0)
+      pattern_idx[(size_t)(scope_batch ? 0 : blockIdx.y) * H + h] = key == 0x7fffffff ? n_pool - 1 : (key & 31);
   }
 }
 
