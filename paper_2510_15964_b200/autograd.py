@@ -59,6 +59,9 @@ class FlatGrads(dict):
         self.views, self.scale = views, scale
 
 
+CG_LAYERS = 2  # layers whose LoRA / BitFit column reductions share one lx_colgrad_group launch
+
+
 class _CgBatch:
     """The LoRA / BitFit column reductions of one sublayer's backward, collected and run as one
     deterministic lx_colgrad_group launch. A gradient with a view in a FlatGrads buffer is written
@@ -256,8 +259,11 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
     return dx
 
 
-def block_backward(d_out, model: M.Model, layer: int, cache, masks, grads: dict, d_out_bf16=None, inplace: bool = False):
-    """sf/autograd.py:165-181; d_out fp32 [B*s, d] (+ its bf16 copy). Returns (dx fp32, dx bf16)."""
+def block_backward(d_out, model: M.Model, layer: int, cache, masks, grads: dict, d_out_bf16=None, inplace: bool = False,
+                   cg: "_CgBatch | None" = None):
+    """sf/autograd.py:165-181; d_out fp32 [B*s, d] (+ its bf16 copy). Returns (dx fp32, dx bf16).
+    `cg`: a column-reduction batch shared with other layers (the caller flushes it); by default the
+    layer's own batch is flushed here."""
     lw = model.weights.layers[layer]
     bitfit = model.peft_method == "bitfit"
     lora = {t: model.lora[(layer, t)] for t in model.lora_targets} if model.peft_method == "lora" else {}
@@ -271,15 +277,17 @@ def block_backward(d_out, model: M.Model, layer: int, cache, masks, grads: dict,
     nm = masks.neuron_mask if masks is not None else None
     # the layer's LoRA / BitFit column reductions (MLP then attention) run as one deterministic group
     # launch after both sublayers (their operands stay referenced by the batch until then)
-    B, s = cache["mlp"]["n_items"], cache["mlp"]["s"]
-    cg = _CgBatch(grads, B, s)
+    own = cg is None
+    if own:
+        cg = _CgBatch(grads, cache["mlp"]["n_items"], cache["mlp"]["s"])
     dh2 = mlp_backward(d_mlp, cache["mlp"], lw, lora, nm, model.dims, grads, prefix, bitfit, cg=cg)
     dy, dy_bf = layernorm_backward(dh2, cache["ln2"], accumulate_into=d_out if inplace else d_out.clone(), want_bf16=True)
     d_attn = dy_bf
     if adapter:
         d_attn = adapter_backward(dy, model.adapters[(layer, "attn")], cache["attn_adapter"], grads, f"{prefix}attn_adapter")
     dh1 = mha_backward(d_attn, cache["attn"], lw, lora, model.dims, grads, prefix, bitfit, cg=cg)
-    cg.flush()
+    if own:
+        cg.flush()
     return layernorm_backward(dh1, cache["ln1"], accumulate_into=dy, want_bf16=True)
 
 
@@ -290,9 +298,17 @@ def model_backward(model: M.Model, cache, d_logits, masks=None) -> dict:
     V = model.dims.vocab
     d_hf = M._mm_f32(d_logits.reshape(-1, V).to(torch.bfloat16), model.weights.emb)
     dh, dh_bf = layernorm_backward(d_hf, cache["lnf"], want_bf16=True)
-    for layer in reversed(range(model.dims.n_layers)):
+    cg = None
+    for k, layer in enumerate(reversed(range(model.dims.n_layers))):
         lm = None if masks is None else masks[layer]
-        dh, dh_bf = block_backward(dh, model, layer, cache["blocks"][layer], lm, grads, dh_bf, inplace=True)
+        bc = cache["blocks"][layer]
+        cg = cg or _CgBatch(grads, bc["mlp"]["n_items"], bc["mlp"]["s"])
+        dh, dh_bf = block_backward(dh, model, layer, bc, lm, grads, dh_bf, inplace=True, cg=cg)
+        if k % CG_LAYERS == CG_LAYERS - 1:  # two layers' column reductions per group launch
+            cg.flush()
+            cg = None
+    if cg is not None:
+        cg.flush()
     for name, p in M.trainable_params(model).items():
         if name not in grads:
             grads[name] = torch.zeros_like(p)

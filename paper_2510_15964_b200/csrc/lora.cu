@@ -287,7 +287,7 @@ __global__ void pack_params_kernel(const lx_pack_segment* __restrict__ segs) {
 // active 16-column sub-block, addressed through pos), so the partials of every item line up and inactive
 // columns come out exactly 0. A unit writes its partial [r][64] (or G itself when it is the only split);
 // a final launch sums the splits in order: deterministic, no float atomics.
-constexpr int kCgMaxProbs = 8;
+constexpr int kCgMaxProbs = 16;  // two layers of LoRA factors (q/v/fc1/fc2 A and B) per launch
 constexpr int kCgChunk = 64;
 constexpr int kCgConsumers = 8;
 constexpr int kCgThreads = 32 * (kCgConsumers + 1);

@@ -75,8 +75,15 @@ class FinetuneEngine:
         # gradient reductions write straight into the flat buffer, pre-scaled by 1/B (sf/harness.py:415)
         grads = AG.FlatGrads(self._grad_views, 1.0 / B)
         dh, dh_bf = AG.layernorm_backward(d_hf, cf, want_bf16=True)
-        for layer in reversed(range(m.dims.n_layers)):
-            dh, dh_bf = AG.block_backward(dh, m, layer, caches[layer], None, grads, dh_bf, inplace=True)
+        cg = None
+        for k, layer in enumerate(reversed(range(m.dims.n_layers))):
+            cg = cg or AG._CgBatch(grads, B, s)
+            dh, dh_bf = AG.block_backward(dh, m, layer, caches[layer], None, grads, dh_bf, inplace=True, cg=cg)
+            if k % AG.CG_LAYERS == AG.CG_LAYERS - 1:  # two layers' column reductions per group launch
+                cg.flush()
+                cg = None
+        if cg is not None:
+            cg.flush()
         self.last_masks = [c["masks"] for c in caches]
         for name, view in self._grad_views.items():
             t = grads.get(name)

@@ -284,7 +284,7 @@ def colgrad_problem(p: torch.Tensor | None, x2: torch.Tensor, ncols: int, r: int
 
 
 def colgrad_group(problems: list, n_items: int, s: int) -> None:
-    """All problems in one deterministic launch (lx_colgrad_group, up to 8; ranks above 16 split)."""
+    """All problems in one deterministic launch (lx_colgrad_group, up to 16; ranks above 16 split)."""
     flat = []
     for pr in problems:
         r = pr["r"]
@@ -295,8 +295,8 @@ def colgrad_group(problems: list, n_items: int, s: int) -> None:
                 flat.append(sub)
         else:
             flat.append(pr)
-    for i in range(0, len(flat), 8):
-        chunk = flat[i : i + 8]
+    for i in range(0, len(flat), 16):
+        chunk = flat[i : i + 16]
         arr = (_abi.ColgradProblem * len(chunk))()
         keep = []
         for j, pr in enumerate(chunk):
