@@ -59,7 +59,7 @@ class FlatGrads(dict):
         self.views, self.scale = views, scale
 
 
-CG_LAYERS = 2  # layers whose LoRA / BitFit column reductions share one lx_colgrad_group launch
+CG_LAYERS = 2  # layers whose LoRA / BitFit column reductions share one lx_colgrad_group launch (4: no gain)
 
 
 class _CgBatch:
@@ -304,7 +304,7 @@ def model_backward(model: M.Model, cache, d_logits, masks=None) -> dict:
         bc = cache["blocks"][layer]
         cg = cg or _CgBatch(grads, bc["mlp"]["n_items"], bc["mlp"]["s"])
         dh, dh_bf = block_backward(dh, model, layer, bc, lm, grads, dh_bf, inplace=True, cg=cg)
-        if k % CG_LAYERS == CG_LAYERS - 1:  # two layers' column reductions per group launch
+        if k % CG_LAYERS == CG_LAYERS - 1:  # CG_LAYERS layers' column reductions per group launch
             cg.flush()
             cg = None
     if cg is not None:

@@ -79,7 +79,7 @@ class FinetuneEngine:
         for k, layer in enumerate(reversed(range(m.dims.n_layers))):
             cg = cg or AG._CgBatch(grads, B, s)
             dh, dh_bf = AG.block_backward(dh, m, layer, caches[layer], None, grads, dh_bf, inplace=True, cg=cg)
-            if k % AG.CG_LAYERS == AG.CG_LAYERS - 1:  # two layers' column reductions per group launch
+            if k % AG.CG_LAYERS == AG.CG_LAYERS - 1:  # CG_LAYERS layers' column reductions per group launch
                 cg.flush()
                 cg = None
         if cg is not None:
