@@ -67,9 +67,10 @@ class _CgBatch:
     deterministic lx_colgrad_group launch. A gradient with a view in a FlatGrads buffer is written
     there directly (pre-scaled by the batch mean); others are accumulated after the launch."""
 
-    def __init__(self, grads: dict, n_items: int, s: int):
+    def __init__(self, grads: dict, n_items: int, s: int, stream=None):
         self.grads, self.n_items, self.s = grads, n_items, s
         self.probs, self.post = [], []
+        self.stream = stream  # side stream: the launch overlaps the following layers' backward
 
     def add(self, name, shape, p, x2, ncols, r, scale, g_sq, g_sc, masks=None, blk=1) -> None:
         g = self.grads
@@ -83,7 +84,20 @@ class _CgBatch:
         self.probs.append(colgrad_problem(p, x2, ncols, r, scale, out, g_sq, g_sc, masks=masks, blk=blk))
 
     def flush(self) -> None:
-        if self.probs:
+        if self.probs and self.stream is not None and not self.post:
+            # nothing downstream of the backward reads these gradients before the optimizer step, so the
+            # group runs on a side stream (joined by the caller) and fills SMs the next layers leave idle
+            main = torch.cuda.current_stream()
+            self.stream.wait_stream(main)
+            for pr in self.probs:
+                for t in (pr["p"], pr["x"], pr["out"]):
+                    if t is not None:
+                        t.record_stream(self.stream)
+                if pr["masks"] is not None:
+                    pr["masks"].pos.record_stream(self.stream)
+            with torch.cuda.stream(self.stream):
+                colgrad_group(self.probs, self.n_items, self.s)
+        elif self.probs:
             colgrad_group(self.probs, self.n_items, self.s)
         for name, out in self.post:
             _acc(self.grads, name, out)

@@ -58,6 +58,16 @@ class FinetuneEngine:
         self.last_masks = None
         M.ensure_lora_packs(model)  # packed LoRA operands, refreshed at the start of every step
 
+    def _cg_stream(self):
+        """Side stream for the LoRA / BitFit column reductions (LX_CG_SIDE_STREAM=0 keeps them inline)."""
+        import os
+
+        if os.environ.get("LX_CG_SIDE_STREAM", "1") == "0":
+            return None
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.model.device)
+        return self._side
+
     # -------------------------------------------------------------- one step (capturable)
     def _step(self, tokens: torch.Tensor) -> torch.Tensor:
         m = self.model
@@ -76,14 +86,17 @@ class FinetuneEngine:
         grads = AG.FlatGrads(self._grad_views, 1.0 / B)
         dh, dh_bf = AG.layernorm_backward(d_hf, cf, want_bf16=True)
         cg = None
+        side = self._cg_stream()
         for k, layer in enumerate(reversed(range(m.dims.n_layers))):
-            cg = cg or AG._CgBatch(grads, B, s)
+            cg = cg or AG._CgBatch(grads, B, s, stream=side)
             dh, dh_bf = AG.block_backward(dh, m, layer, caches[layer], None, grads, dh_bf, inplace=True, cg=cg)
             if k % AG.CG_LAYERS == AG.CG_LAYERS - 1:  # CG_LAYERS layers' column reductions per group launch
                 cg.flush()
                 cg = None
         if cg is not None:
             cg.flush()
+        if side is not None:
+            torch.cuda.current_stream().wait_stream(side)  # join: Adam reads every gradient
         self.last_masks = [c["masks"] for c in caches]
         for name, view in self._grad_views.items():
             t = grads.get(name)
