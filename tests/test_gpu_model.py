@@ -223,3 +223,24 @@ def test_engine_graph_replay_matches_eager_steps(dev):
     diff = (s2.flat - s1.flat).abs()
     assert float(diff.max()) <= 2 * 3 * 1e-3 + 1e-5
     assert float(diff.median()) < 1e-4
+
+
+def test_engine_side_stream_reductions_are_bit_identical(dev, monkeypatch):
+    """The LoRA column reductions on the side stream (default) give exactly the gradients of the inline
+    path: same kernels, same fixed reduction order, only the stream differs."""
+    import bench
+    from paper_2510_15964_b200.engine import FinetuneEngine
+
+    cfg = dict(d=256, H=4, d_ff=1024, L=3, V=128, B=2, s=128, blk=16, attn_blk=32, r=8)
+    tok = torch.randint(0, cfg["V"], (cfg["B"], cfg["s"] + 1), generator=torch.Generator().manual_seed(3)).to(dev)
+    grads = []
+    for side in ("1", "0"):
+        monkeypatch.setenv("LX_CG_SIDE_STREAM", side)
+        m, st, prov = bench.build_workload(cfg, dev, 7, 0.5, 0.5)
+        eng = FinetuneEngine(m, st, prov, lr=1e-3)
+        eng.flat_grad.fill_(float("nan"))  # every trainable gradient must be written by the step
+        eng._step(tok)
+        torch.cuda.synchronize()
+        grads.append(eng.flat_grad.clone())
+    assert torch.isfinite(grads[0]).all()
+    assert torch.equal(grads[0], grads[1])
