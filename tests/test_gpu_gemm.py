@@ -228,6 +228,31 @@ def test_cross_entropy_kernel():
     assert rel(d_hf, ref_dhf) < 1e-2
 
 
+def test_cross_entropy_kernel_persistent_rows():
+    """More rows than the persistent CE grid (2 CTAs per SM) at the OPT vocabulary (V % 1024 != 0):
+    every row's loss and gradient vs torch fp32, so rows handled on a CTA's second and later passes
+    are covered (sf/model.py:454-472)."""
+    from paper_2510_15964_b200 import _abi
+
+    dev = _dev()
+    g = torch.Generator(device="cpu").manual_seed(5)
+    rows, V = 2 * torch.cuda.get_device_properties(0).multi_processor_count + 77, 50272
+    logits = (torch.randn(rows, V, generator=g) * 3).to(dev)
+    tgt = torch.randint(0, V, (rows,), generator=g).to(dev)
+    tgt[0], tgt[1] = 0, V - 1  # first and last column as targets
+    row_loss = torch.empty(rows, dtype=torch.float32, device=dev)
+    gb = torch.empty(rows, V, dtype=torch.bfloat16, device=dev)
+    inv_s = 1.0 / 37
+    _abi.call("lx_cross_entropy", logits.data_ptr(), rows, V, tgt.data_ptr(), inv_s, row_loss.data_ptr(), gb.data_ptr(),
+              _abi.stream_handle(logits.device))
+    torch.cuda.synchronize()
+    ref_loss = torch.nn.functional.cross_entropy(logits, tgt, reduction="none")
+    ref_g = (torch.softmax(logits, dim=1) - torch.nn.functional.one_hot(tgt, V).float()) * inv_s
+    assert (row_loss - ref_loss).abs().max().item() < 1e-4 * ref_loss.abs().max().item()
+    assert rel(gb.float(), ref_g) < 1e-2
+    assert torch.equal(gb[:, 0].float() < 0, tgt == 0)  # the one-hot lands on the target column only
+
+
 @pytest.mark.parametrize("gather", [False, True])
 @pytest.mark.parametrize("r,rp", [(8, 8), (16, 16), (4, 8), (12, 16)])
 def test_rowproj_packed_and_pack_params(gather, r, rp):
