@@ -362,3 +362,39 @@ def test_adam_step_kernel():
     assert np.abs(m.cpu().numpy() - mr).max() <= 1e-15
     assert np.abs(v.cpu().numpy() - vr).max() <= 1e-15
     assert np.abs(p.cpu().numpy() - pr).max() <= 1e-7
+
+
+@pytest.mark.parametrize("d", [768, 1024, 2048])
+@pytest.mark.parametrize("with_delta", [False, True])
+def test_layernorm_fwd_kernel(d, with_delta):
+    """lx_layernorm_fwd (csrc/layernorm.cu) vs torch fp32 (sf/model.py:307-312): fused residual add
+    (bit-exact fp32 sum), mean / inv-std, bf16 output and the fused downsampled rows
+    (sf/predictor.py:62-71). M spans several row passes of the persistent grid with a ragged last pass."""
+    from paper_2510_15964_b200 import _abi
+
+    dev = _dev()
+    g = torch.Generator(device="cpu").manual_seed(11)
+    n_items, s, m_small = 7, 700, 26  # M = 4900 rows
+    M = n_items * s
+    x = torch.randn(M, d, generator=g).to(dev)
+    delta = torch.randn(M, d, generator=g).to(dev, torch.bfloat16) if with_delta else None
+    gamma = (1 + 0.1 * torch.randn(d, generator=g)).to(dev)
+    beta = (0.1 * torch.randn(d, generator=g)).to(dev)
+    resid = torch.empty(M, d, device=dev) if with_delta else None
+    y = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
+    mean = torch.empty(M, device=dev)
+    istd = torch.empty(M, device=dev)
+    xs = torch.zeros(n_items * m_small, d, dtype=torch.bfloat16, device=dev)
+    _abi.call("lx_layernorm_fwd", x.data_ptr(), _abi.ptr(delta), _abi.ptr(resid), M, d, gamma.data_ptr(), beta.data_ptr(),
+              1e-5, y.data_ptr(), d, mean.data_ptr(), istd.data_ptr(), s, m_small, xs.data_ptr(), _abi.stream_handle(dev))
+    torch.cuda.synchronize()
+    h = x + delta.float() if with_delta else x
+    if with_delta:
+        assert torch.equal(resid, h)
+    ref = torch.nn.functional.layer_norm(h, (d,), gamma, beta, 1e-5)
+    assert rel(y.float(), ref) < 1e-2
+    assert torch.allclose(mean, h.mean(1), atol=1e-5)
+    assert torch.allclose(istd, 1 / torch.sqrt(h.var(1, unbiased=False) + 1e-5), rtol=1e-4)
+    idx = torch.tensor([(i * s) // m_small for i in range(m_small)], device=dev)
+    want = y.view(n_items, s, d)[:, idx].reshape(-1, d)
+    assert torch.equal(xs, want)
