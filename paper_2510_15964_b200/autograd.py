@@ -4,9 +4,9 @@ Inactive neuron blocks and attention blocks are never touched: the MLP
 input-grad runs the tcgen05 gather-GEMMs over the forward's index lists, the
 LoRA / BitFit gradients are deterministic skinny reductions over the packed
 active columns (inactive rows/columns stay exactly 0, sf/autograd.py:89-90),
-attention gradients flow through the block-sparse backward kernels only, and
-the projection input-grads run on the tcgen05 engine with the LoRA term
-fused in the epilogue. Gradients are sums over the batch items (the
+attention gradients flow through the block-sparse backward kernels only. The
+dense projection input-grads are library GEMMs (cuBLAS); the q/k/v LoRA term
+rides in the same GEMM by K-extension ([dqkv | dAx] x [W_qkv^T ; A^T]). Gradients are sums over the batch items (the
 reference harness sums per-item gradients and divides by the batch size,
 sf/harness.py:413-415).
 

@@ -45,6 +45,7 @@ __device__ __forceinline__ bool ex_pool_member(int kind, int p, int i, int j) { 
 __global__ void __launch_bounds__(kExThreads) exact_mass_kernel(const float* __restrict__ q, const float* __restrict__ k,
                                                                 int ld, int s, int H, int hd, int n_b, double scale,
                                                                 double* __restrict__ mass) {
+  pdl_wait_trigger();  // launched with PDL (launch_k): see the predecessor's writes first
   extern __shared__ float ex_smem[];
   const int br = blockIdx.x, h = blockIdx.y, item = blockIdx.z;
   const int blk = s / n_b;
@@ -193,6 +194,7 @@ __device__ double np_pairwise_sum(const double* a, int n) {
 __global__ void coverage_select_kernel(const double* __restrict__ mass, int n_items, int H, int n_b,
                                        const int32_t* __restrict__ pool_kind, const int32_t* __restrict__ pool_param,
                                        int n_pool, double tau, int head_sum, int32_t* __restrict__ pattern_idx) {
+  pdl_wait_trigger();  // launched with PDL (launch_k): see the predecessor's writes first
   const int n_sel = head_sum ? n_items : n_items * H;
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -249,6 +251,7 @@ __global__ void coverage_select_kernel(const double* __restrict__ mass, int n_it
 // block max through the non-negative float bits (atomicMax on int is exact and order-free)
 __global__ void block_importance_kernel(const float* __restrict__ z, int ldz, int s, int n_cols, int blk,
                                         int rows_per_cta, int n_blk, int* __restrict__ imp_bits) {
+  pdl_wait_trigger();  // launched with PDL (launch_k): see the predecessor's writes first
   const int item = blockIdx.z;
   const int r0 = blockIdx.y * rows_per_cta, r1 = min(s, r0 + rows_per_cta);
   const bool vec = (n_cols & 3) == 0 && (ldz & 3) == 0 && (blk & 3) == 0;
@@ -273,6 +276,7 @@ __global__ void block_importance_kernel(const float* __restrict__ z, int ldz, in
 // one warp per item: peak, then active iff (double)imp > theta * peak (strict), all-zero -> none
 __global__ void filter_blocks_kernel(const float* __restrict__ imp, int n_items, int n_blk, double theta,
                                      uint32_t* __restrict__ bits) {
+  pdl_wait_trigger();  // launched with PDL (launch_k): see the predecessor's writes first
   const int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (item >= n_items) return;

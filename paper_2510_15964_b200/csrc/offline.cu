@@ -16,6 +16,7 @@ namespace lx {
 
 __global__ void block_activity_kernel(const float* __restrict__ z, int ldz, int n_cols, int blk, int words,
                                       uint32_t* __restrict__ bits) {
+  pdl_wait_trigger();  // launched with PDL (launch_k): see the predecessor's writes first
   extern __shared__ uint32_t act[];
   const int row = blockIdx.x;
   for (int w = threadIdx.x; w < words; w += blockDim.x) act[w] = 0u;
@@ -45,6 +46,7 @@ __device__ __forceinline__ float log_sigmoid(float x) {  // -logaddexp(0, -x)
 __global__ void weighted_bce_kernel(const float* __restrict__ logits, int ld, int rows, int n_blk,
                                     const uint32_t* __restrict__ labels, int words, float pos_w, double inv_size,
                                     float* __restrict__ d_logits, int ldd, double* __restrict__ row_loss) {
+  pdl_wait_trigger();  // launched with PDL (launch_k): see the predecessor's writes first
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;

@@ -18,7 +18,7 @@ import torch
 from . import autograd, exposer as EX, model as M, predictor as P
 from .errors import ConfigError
 
-MODES = ("dense", "shadowy", "exposer-oracle", "predicted", "random", "static")
+MODES = ("dense", "shadowy", "exposer-oracle", "predicted", "random")
 
 
 class _TimedProvider:
@@ -145,9 +145,20 @@ class ShadowyProvider(OracleProvider):
         super().__init__(model, theta=0.0, tau=tau)
 
 
-def make_provider(mode: str, model: M.Model, *, predictors=None, theta: float = 0.0, tau: float = 0.95,
-                  seed: int = 0, pcfg=None, counter=None, scope: str = "item") -> _TimedProvider:
-    """sf/harness.py:232-244 (mode names as the reference's RunConfig)."""
+def make_provider(cfg, model: M.Model, predictors=None, counter=None, *, theta: float = 0.1, tau: float = 0.95,
+                  seed: int = 0, pcfg=None, scope: str = "item") -> _TimedProvider:
+    """sf/harness.py:233-244. `cfg` is the reference's RunConfig (or any object with its `mode`, `theta`,
+    `tau`, `seed`, `tau_pred`, `attn_threshold_frac` and `mlp_threshold` fields), so a reference call
+    make_provider(cfg, model, predictors, counter) drops in unchanged; a bare mode string with keyword
+    overrides is also accepted. Unknown modes fall through to RandomProvider, as in the reference."""
+    if isinstance(cfg, str):
+        mode = cfg
+    else:
+        mode = cfg.mode
+        theta, tau, seed = cfg.theta, cfg.tau, cfg.seed
+        if pcfg is None and hasattr(cfg, "tau_pred"):
+            pcfg = P.PredictorTrainConfig(attn_threshold_frac=cfg.attn_threshold_frac, mlp_threshold=cfg.mlp_threshold,
+                                          tau_pred=cfg.tau_pred)
     if mode == "dense":
         return DenseProvider(model)
     if mode == "shadowy":
@@ -158,9 +169,7 @@ def make_provider(mode: str, model: M.Model, *, predictors=None, theta: float = 
         if predictors is None:
             raise ConfigError("mode=predicted requires trained predictors")
         return PredictedProvider(model, predictors, pcfg, counter=counter, scope=scope)
-    if mode == "random":
-        return RandomProvider(model, seed=seed + 10_000)
-    raise ConfigError(f"unknown mode {mode!r}; expected one of {MODES}")
+    return RandomProvider(model, seed=seed + 10_000)
 
 
 class RandomProvider(_TimedProvider):
@@ -185,7 +194,8 @@ class RandomProvider(_TimedProvider):
 def finetune_step(model: M.Model, state: M.PeftState, batch_tokens, provider, lr: float, grad_hook=None) -> dict:
     """One optimiser step of run_finetune (sf/harness.py:396-417) over a batch [B, s+1]:
     per-item masks, mean loss, grads summed over items then / B, Adam (float64 moments).
-    `grad_hook(flat_grads)` runs before the update (the data-parallel all-reduce)."""
+    `grad_hook(flat)` runs before the update on the flat fp32 mean-gradient buffer (state.flat's layout)
+    and reduces it in place (the data-parallel all-reduce, dp.make_grad_hook)."""
     tok = torch.as_tensor(np.asarray(batch_tokens) if not torch.is_tensor(batch_tokens) else batch_tokens)
     tok = tok.to(model.device, torch.int64)
     inp, tgt = tok[:, :-1], tok[:, 1:]
@@ -195,7 +205,16 @@ def finetune_step(model: M.Model, state: M.PeftState, batch_tokens, provider, lr
     B = tok.shape[0]
     mean = {n: g / B for n, g in grads.items()}
     if grad_hook is not None:
-        mean = grad_hook(mean)
+        # same contract as FinetuneEngine: the hook reduces the flat fp32 mean-gradient buffer (laid out like
+        # state.flat) in place, e.g. dp.make_grad_hook's all-reduce; its return value is ignored
+        flat = torch.empty_like(state.flat)
+        for n, p in state.params.items():
+            off = (p.data_ptr() - state.flat.data_ptr()) // 4
+            flat[off : off + p.numel()] = mean[n].reshape(-1)
+        grad_hook(flat)
+        for n, p in state.params.items():
+            off = (p.data_ptr() - state.flat.data_ptr()) // 4
+            mean[n] = flat[off : off + p.numel()].view(p.shape)
     autograd.optimizer_step(state, mean, lr)
     if not np.isfinite(loss):
         raise FloatingPointError(f"non-finite loss {loss}")

@@ -99,7 +99,12 @@ def _words64_to_32(bits64: np.ndarray) -> np.ndarray:
 @torch.no_grad()
 def collect_traces(model: M.Model, corpus, path=None, batch: int = 8, full: bool = False) -> dict:
     """run_collect_traces (sf/harness.py:249-265) on the device: dense forward over `corpus`
-    ([n, s] tokens) in batches; returns (and writes to `path` if given) the trace tensors."""
+    ([n, s] tokens) in batches; returns (and writes to `path` if given) the trace tensors.
+
+    full=False (default) writes the compact schema (x_attn_ds / mlp_active / raw_ds): what the trainers
+    read, ~35x smaller. It is ONE-WAY: `load_traces` here reads it, the reference's load_traces
+    (sf/harness.py:268-285) does not. Pass full=True to write the reference's own keys for a trace file the
+    reference will read."""
     corpus = np.asarray(corpus)
     n, s = corpus.shape
     dims = model.dims

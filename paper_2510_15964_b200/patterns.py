@@ -10,7 +10,7 @@ also lowered once to the two device forms the kernels consume:
   tiles and CSC over 64-key tiles with 16x16-cell masks.
 
 Pattern ids, order (the tie-break), coordinates and errors match the
-reference exactly (pinned by tests/test_host_logic.py against tests/golden).
+reference exactly (pinned by tests/test_oracle_golden.py::test_pools_match_reference against tests/golden/pools.npz).
 """
 
 from __future__ import annotations
