@@ -3,18 +3,35 @@
 predicted mode on B200 — BASELINE.json metric "OPT-1.3B LoRA fwd+bwd ms/batch"
 at configs[2] (batch 8, seq 512, bf16).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg3]
     torchrun --nproc-per-node N bench.py --gpus N ...   (data parallel, NCCL)
 
-Prints ONE JSON line (rank 0). `value` = device-timed ms per step of the whole
-job (max over ranks; CUDA events around K CUDA-graph replays of the full step,
-inputs resident), `e2e` = the same step through the public engine API with the
-batch copied host->device and the loss device->host every step. Sparsity is
-injected through the predictor weights (zeroed MLP scoring columns; Gram-form
-attention predictors for local heads) and the predictor kernels run for real;
-the achieved sparsity is reported beside every number. `cpu_baseline` and
-`--impl reference` time the reference algorithm (oracle/ NumPy port) on the
-host cores on a bounded sample and extrapolate (see `sample`).
+`--gpus N > 1` without a torchrun environment re-launches this script under
+torch.distributed.run with N ranks; it exits non-zero when fewer than N GPUs
+are visible, or when WORLD_SIZE disagrees with --gpus.
+
+Data parallel by batch with STRONG scaling: the global batch
+G (the config's B) is split contiguously over the ranks (dp.shard_range), each
+rank runs its shard, and the only collective is the flat trainable-gradient
+all-reduce (NCCL) before the replicated Adam step.
+
+Prints ONE JSON line (rank 0):
+  value     device time per global batch, max over ranks: CUDA events around K
+            CUDA-graph replays of the whole step, inputs resident;
+  e2e       the same step through the public engine API (FinetuneEngine.replay)
+            timed on the HOST clock: every step copies its token batch from pinned
+            host memory and reads the loss back to the host (sf/harness.py:423-425);
+  roofline  the dominant hot-path kernel (largest device time in one eager step,
+            CUDA events around each launch on its stream) against MEASURED_PEAKS;
+  kernels   the same for every timed hot-path kernel, with algorithmic units;
+  cpu_baseline  the reference algorithm (oracle/ NumPy port) on the host cores.
+Sparsity is injected through the predictor weights and the predictor kernels
+run for real: MLP predictor columns zeroed for a fraction of neuron blocks, and
+on a fraction of the heads Gram attention predictors (Wq_hat = Wk_hat) with the
+residual stream's common mode projected out (calibrated layer by layer in one
+predicted-mode forward), which the device predictor turns into block-diagonal
+patterns. The achieved
+sparsity is reported beside the number.
 """
 
 from __future__ import annotations
@@ -23,6 +40,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -34,21 +52,28 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
-    # BASELINE.json configs[2]: OPT-1.3B (public OPT dims), LoRA r=8 on wq/wv/w1/w2, batch 8, seq 512
+    # BASELINE.json configs[2]: OPT-1.3B (public OPT dims), LoRA r=8 on wq/wv/w1/w2, global batch 8, seq 512
     "cfg3": dict(d=2048, H=32, d_ff=8192, L=24, V=50272, B=8, s=512, blk=16, attn_blk=64, r=8, desc="OPT-1.3B"),
-    # BASELINE.json configs[3]: OPT-6.7B (d 4096, hd 128), LoRA seq 1024; global batch 16 split over the GPUs
-    # (B below is per rank at 8 GPUs; `--batch` overrides)
-    "cfg4": dict(d=4096, H=32, d_ff=16384, L=32, V=50272, B=2, s=1024, blk=16, attn_blk=64, r=8, desc="OPT-6.7B"),
-    # configs[0] shape (OPT-125M), batch 1 seq 256 — quick checks
-    "cfg1": dict(d=768, H=12, d_ff=3072, L=12, V=50272, B=1, s=256, blk=16, attn_blk=64, r=8, desc="OPT-125M"),
+    # configs[3]: OPT-6.7B (d 4096, hd 128), seq 1024, global batch 16, LoRA / Adapter / BitFit
+    "cfg4": dict(d=4096, H=32, d_ff=16384, L=32, V=50272, B=16, s=1024, blk=16, attn_blk=64, r=8, desc="OPT-6.7B"),
+    # configs[4]: OPT-13B (d 5120, H 40, hd 128), seq 2048, global batch 8 (one sequence per GPU at 8 GPUs)
+    "cfg5": dict(d=5120, H=40, d_ff=20480, L=40, V=50272, B=8, s=2048, blk=16, attn_blk=128, r=8, desc="OPT-13B"),
+    # configs[0] shape (OPT-125M), batch 1 seq 256
+    "cfg1": dict(d=768, H=12, d_ff=3072, L=12, V=50272, B=1, s=256, blk=16, attn_blk=16, r=8, desc="OPT-125M"),
 }
 
 # kernels of ours launched per C-ABI call (for gpu_launches)
 KERNELS_PER_CALL = {
-    "lx_gemm_bf16_tn": 1, "lx_linear": 1, "lx_cross_entropy": 1, "lx_adam_step": 1, "lx_predict_mlp_mask": 2, "lx_mask_compact": 1, "lx_predict_attention_patterns": 2,
-    "lx_neuron_fc1": 1, "lx_neuron_fc2": 1, "lx_neuron_fc2_dgrad": 1, "lx_neuron_fc1_dgrad": 1, "lx_rowproj": 2, "lx_rowproj_packed": 1, "lx_pack_params": 1, "lx_pack_active_rows": 1,
-    "lx_colgrad_group": 3, "lx_bsattn_fwd": 1, "lx_bsattn_bwd": 3, "lx_bsattn_fwd_tc": 1, "lx_bsattn_bwd_tc": 3, "lx_layernorm_fwd": 1, "lx_layernorm_bwd": 1,
+    "lx_gemm_bf16_tn": 1, "lx_linear": 1, "lx_cross_entropy": 1, "lx_adam_step": 1, "lx_predict_mlp_mask": 2, "lx_mask_compact": 1,
+    "lx_predict_attention_patterns": 2, "lx_neuron_fc1": 1, "lx_neuron_fc2": 1, "lx_neuron_fc2_dgrad": 1, "lx_neuron_fc1_dgrad": 1,
+    "lx_rowproj": 2, "lx_rowproj_packed": 1, "lx_pack_params": 1, "lx_pack_active_rows": 1, "lx_colgrad_group": 3,
+    "lx_bsattn_fwd": 1, "lx_bsattn_bwd": 3, "lx_bsattn_fwd_tc": 1, "lx_bsattn_bwd_tc": 3, "lx_layernorm_fwd": 1,
+    "lx_layernorm_bwd": 1, "lx_adapter_fwd": 2, "lx_adapter_bwd": 3,
 }
+
+# hot-path C-ABI calls timed by the roofline probe
+PROBED = ("lx_neuron_fc1", "lx_neuron_fc2", "lx_neuron_fc2_dgrad", "lx_neuron_fc1_dgrad", "lx_bsattn_fwd_tc",
+          "lx_bsattn_bwd_tc", "lx_predict_mlp_mask", "lx_predict_attention_patterns")
 
 
 def load_peaks() -> dict:
@@ -96,7 +121,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.1)
+            time.sleep(0.05)
 
     def __exit__(self, *a):
         self._stop.set()
@@ -109,31 +134,67 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-# ---------------------------------------------------------------------------- our arm
+# ---------------------------------------------------------------------------- workload
 
 
-def build_workload(cfg: dict, device, seed: int, mlp_sparsity: float, local_frac: float):
+class _CalibratingProvider:
+    """One forward in which each layer's attention predictor is built from the LN1 output the layer
+    actually receives (so from the predicted patterns / masks of all earlier layers): heads < n_local get
+    a Gram predictor W_q = W_k = (I - c c^T) R, c the layer's residual-stream common mode (mean LN1 row);
+    the remaining heads independent random factors (N(0, 0.1^2), sf/predictor.py:194-206). Without the
+    projection every token pair shares the common mode and the Gram map is dense."""
+
+    fused_downsample = False
+
+    def __init__(self, inner, n_local: int, r_pred: int, g, device):
+        self.inner, self.n_local, self.r_pred, self.g, self.device = inner, n_local, r_pred, g, device
+
+    def attn_patterns(self, layer, h, x_small=None):
+        import torch
+
+        from paper_2510_15964_b200 import predictor as P
+
+        d = h.shape[-1]
+        H = self.inner.model.dims.n_heads
+        c = h.float().reshape(-1, d).mean(0)
+        c = c / c.norm().clamp_min(1e-12)
+        wq, wk = [], []
+        for hh in range(H):
+            w = torch.randn(d, self.r_pred, generator=self.g, device=self.device) * 0.1
+            if hh < self.n_local:
+                w = w - torch.outer(c, c @ w)
+                wq.append(w)
+                wk.append(w)
+            else:
+                wq.append(w)
+                wk.append(torch.randn(d, self.r_pred, generator=self.g, device=self.device) * 0.1)
+        ap = P.AttnPredictorParams(wq, wk)
+        ap.packed_t(self.device)  # device copy [2*H*r, d] bf16; drop the fp32 factors (shape-only meta tensors)
+        ap.wq_hat = ap.wk_hat = [torch.empty(d, self.r_pred, device="meta") for _ in range(H)]
+        self.inner.predictors["attn"][layer] = ap
+        return self.inner.attn_patterns(layer, h)
+
+    def mlp_mask(self, layer, h):
+        return self.inner.mlp_mask(layer, h)
+
+
+def build_workload(cfg: dict, device, seed: int, mlp_sparsity: float, local_frac: float, peft: str = "lora"):
     import torch
 
     from paper_2510_15964_b200 import harness as HN, model as M, predictor as P
 
     dims = M.ModelDims(cfg["d"], cfg["H"], cfg["d_ff"], cfg["s"], cfg["L"], cfg["V"], cfg["blk"], cfg["attn_blk"])
-    model = M.build_model(dims, seed=seed, peft="lora", lora_rank=cfg["r"], device=device)
+    model = M.build_model(dims, seed=seed, peft=peft, lora_rank=cfg["r"], device=device)
     g = torch.Generator(device=device).manual_seed(seed + 1)
     for ad in model.lora.values():  # LoRA-B off its zero init so every LoRA path carries signal
         ad.b.normal_(0.0, 0.02, generator=g)
+    for ad in model.adapters.values():
+        ad.w_up.normal_(0.0, 0.02, generator=g)
     state = M.make_peft_state(model)
     d, H, n_blk = dims.d_model, dims.n_heads, dims.n_blk
     r_pred = max(4, d // 16)  # sf/harness.py:332 default
-    attn, mlp = [], []
-    n_local = int(round(H * local_frac))
+    mlp = []
     for layer in range(dims.n_layers):
-        wq = [torch.randn(d, r_pred, generator=g, device=device) * 0.1 for _ in range(H)]
-        wk = [wq[h] if h < n_local else torch.randn(d, r_pred, generator=g, device=device) * 0.1 for h in range(H)]
-        ap = P.AttnPredictorParams(wq, wk)
-        ap.packed_t(device)  # device copy [2*H*r, d] bf16; drop the fp32 factors (shape-only meta tensors)
-        ap.wq_hat = ap.wk_hat = [torch.empty(d, r_pred, device="meta") for _ in range(H)]
-        attn.append(ap)
         wa = torch.randn(d, n_blk, generator=g, device=device) * 0.1
         kill = torch.randperm(n_blk, generator=torch.Generator().manual_seed(seed * 131 + layer))[: int(round(mlp_sparsity * n_blk))]
         wa[:, kill.to(device)] = 0.0  # S_hat = 0 -> never > 0 -> block inactive (sparsity injection)
@@ -141,7 +202,12 @@ def build_workload(cfg: dict, device, seed: int, mlp_sparsity: float, local_frac
         mp.packed_t(device)
         mp.wa_hat = None
         mlp.append(mp)
-    provider = HN.PredictedProvider(model, {"attn": attn, "mlp": mlp}, P.PredictorTrainConfig())
+    provider = HN.PredictedProvider(model, {"attn": [None] * dims.n_layers, "mlp": mlp}, P.PredictorTrainConfig())
+    # calibration forward on one synthetic sequence builds every layer's attention predictor in place
+    tok = torch.randint(0, dims.vocab, (1, dims.seq_len), generator=torch.Generator().manual_seed(seed + 4242)).to(device)
+    with torch.no_grad():
+        M.model_forward(model, tok, _CalibratingProvider(provider, int(round(H * local_frac)), r_pred, g, device))
+    provider.reset_timing()
     return model, state, provider
 
 
@@ -163,15 +229,13 @@ def count_launches(fn) -> int:
     return n[0]
 
 
-def achieved_sparsity(engine, model) -> dict:
-    import torch
-
-    dims = model.dims
-    nm_density, at_density = [], []
+def achieved_sparsity(masks, model) -> dict:
     from paper_2510_15964_b200.model import dp_nnz
 
+    dims = model.dims
     nnz_of = {i: dp_nnz(model.dpool, i) for i in range(len(model.dpool.ids))}
-    for lm in engine.last_masks:
+    nm_density, at_density = [], []
+    for lm in masks:
         nm_density.append(float(lm.neuron_mask.counts.float().mean()) / dims.n_blk)
         idx = lm.head_patterns.flatten().tolist()
         at_density.append(float(np.mean([nnz_of[i] for i in idx])) / dims.n_b ** 2)
@@ -179,7 +243,17 @@ def achieved_sparsity(engine, model) -> dict:
             "attn_block_sparsity": round(1 - float(np.mean(at_density)), 4)}
 
 
-def time_graph(engine, K: int, dist) -> float:
+def _max_over_ranks(x: float, dist, device) -> float:
+    if dist is None:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def time_graph(engine, K: int, dist, device) -> float:
     import torch
 
     if dist is not None:
@@ -191,51 +265,95 @@ def time_graph(engine, K: int, dist) -> float:
         engine.replay()
     en.record()
     torch.cuda.synchronize()
-    ms = st.elapsed_time(en) / K
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        dist.barrier()
-    return ms
+    return _max_over_ranks(st.elapsed_time(en) / K, dist, device)
 
 
-def fc1_roofline(model, engine, tok_dev, peaks: dict, config: str = "cfg3") -> dict:
-    """Dominant sparse kernel: the fc1 packed-row GEMM (bias + LoRA + ReLU fused), timed live inside one
-    eager training step with CUDA events around each of its L launches on the launching stream (so the
-    L2 state is the step's own); algorithmic FLOPs per launch = 2 * s * d * sum_b(counts_b * blk)."""
+class StateSnapshot:
+    """Trainable parameters, Adam moments and step count; rank-0-only probe steps run between
+    snapshot and restore so every rank ends with the state the timed steps left."""
+
+    def __init__(self, state):
+        self.state = state
+        self.saved = (state.flat.clone(), state.m.clone(), state.v.clone(), state.step)
+
+    def restore(self):
+        f, m, v, step = self.saved
+        self.state.flat.copy_(f)
+        self.state.m.copy_(m)
+        self.state.v.copy_(v)
+        self.state.step = step
+
+
+def kernel_probe(model, engine, tok_dev, peaks: dict, config: str) -> tuple[dict, list]:
+    """Time every probed hot-path call of one eager training step (CUDA events around each launch on its
+    stream; the GPU is held ~1 s first so the whole step is queued and the events bracket GPU execution
+    only) and credit algorithmic units per launch:
+      fc GEMMs   2 * s * d * sum_b counts_b * blk FLOPs
+      attention  fwd 4 * sum_(b,h) nnz * attn_blk^2 * hd, bwd 8 * (...) FLOPs (reference MAC convention)
+      K1 mask    HBM bytes: MLP = M*d*2 (h2) + n_blk*d*2 (W_a) + outputs; attention = B*m*d*2 + 2*H*r*d*2.
+    Returns (dominant kernel's roofline object, per-kernel list)."""
     import torch
 
-    from paper_2510_15964_b200 import neuron_ops as N
+    from paper_2510_15964_b200 import _abi
+    from paper_2510_15964_b200.model import dp_nnz
+    from paper_2510_15964_b200.predictor import downsample_indices
 
-    N.FC1_EVENTS = []
-    hook, engine.grad_hook = engine.grad_hook, None  # rank-0-only probe step: no collective
+    dims = model.dims
+    _abi.PROBE = {n: [] for n in PROBED}
     try:
-        # hold the GPU ~1 s so the whole eager step is queued before it runs: the events then bracket
-        # GPU execution only (no host-enqueue gaps between an event and its kernel)
         torch.cuda._sleep(2_000_000_000)
         engine.step(tok_dev)
         torch.cuda.synchronize()
-        recs = N.FC1_EVENTS
+        rec = _abi.PROBE
     finally:
-        N.FC1_EVENTS = None
-        engine.grad_hook = hook
-    ms = [a.elapsed_time(b) for a, b, *_ in recs]
-    flops = [2.0 * s * d * float(c.sum()) * blk for _, _, c, s, d, blk in recs]
-    ms_avg, fl_avg = statistics.mean(ms), statistics.mean(flops)
-    ach = fl_avg / (ms_avg * 1e-3) / 1e12
-    traffic = None
-    prof = ROOT / "profiles" / "r01_fc1_ncu.json"
-    if prof.exists():  # ncu DRAM bytes of one fc1 launch, valid for the config it was captured on
-        pj = json.loads(prof.read_text())
-        if pj.get("config", "cfg3") == config:
-            traffic = pj.get("dram_bytes_per_launch")
-    return {"kernel": "gemm_sm100_kernel<kPackedN,kEpiFc1> (neuron_matmul_fwd1+b1+LoRA+ReLU over packed active W1 rows)",
-            "bound": "tensor", "achieved": round(ach, 1), "peak": peaks["bf16_sust"], "unit": "TFLOP/s",
-            "frac": round(ach / peaks["bf16_sust"], 4), "traffic": traffic,
-            "peak_src": f"{peaks['src']} sustained bf16 (kernel timed inside the step)",
-            "ms_per_launch": round(ms_avg, 4), "flops_per_launch": fl_avg, "launches_timed": len(recs),
-            "timing": "CUDA events around each fc1 launch of one eager step (all layers), mean"}
+        _abi.PROBE = None
+    masks = engine.last_masks
+    L, s, d, hd, blk, ab = dims.n_layers, dims.seq_len, dims.d_model, dims.head_dim, dims.blk_size, dims.attn_blk
+    B = int(masks[0].neuron_mask.counts.numel())
+    nnz_of = {i: dp_nnz(model.dpool, i) for i in range(len(model.dpool.ids))}
+    fc_fl = [2.0 * s * d * float(lm.neuron_mask.counts.sum()) * blk for lm in masks]
+    att_nnz = []
+    for lm in masks:
+        hp = lm.head_patterns
+        n = sum(nnz_of[i] for i in hp.flatten().tolist())
+        att_nnz.append(n * (B if hp.shape[0] == 1 else 1))
+    m = len(downsample_indices(s))
+    r_pred = max(4, d // 16)
+    units = {
+        "lx_neuron_fc1": ("tensor", fc_fl), "lx_neuron_fc2": ("tensor", fc_fl),
+        "lx_neuron_fc2_dgrad": ("tensor", fc_fl[::-1]), "lx_neuron_fc1_dgrad": ("tensor", fc_fl[::-1]),
+        "lx_bsattn_fwd_tc": ("tensor", [4.0 * n * ab * ab * hd for n in att_nnz]),
+        "lx_bsattn_bwd_tc": ("tensor", [8.0 * n * ab * ab * hd for n in att_nnz[::-1]]),
+        "lx_predict_mlp_mask": ("hbm", [float(B * s * d * 2 + dims.n_blk * d * 2 + 4 * B * (2 * dims.n_blk + 1))] * L),
+        "lx_predict_attention_patterns": ("hbm", [float(B * m * d * 2 + 2 * dims.n_heads * r_pred * d * 2 + 4 * B * dims.n_heads)] * L),
+    }
+    traffic_db = {}
+    prof = ROOT / "profiles" / "r02_ncu_traffic.json"
+    if prof.exists():
+        traffic_db = json.loads(prof.read_text()).get(config, {})
+    out = []
+    for name, evs in rec.items():
+        if not evs:
+            continue
+        bound, work = units[name]
+        ms = [a.elapsed_time(b) for a, b in evs]
+        n = min(len(ms), len(work))
+        ms_avg = statistics.mean(ms[:n])
+        w_avg = statistics.mean(work[:n])
+        if bound == "tensor":
+            ach, peak, unit = w_avg / (ms_avg * 1e-3) / 1e12, peaks["bf16_sust"], "TFLOP/s"
+        else:
+            ach, peak, unit = w_avg / (ms_avg * 1e-3) / 1e9, peaks["hbm"], "GB/s"
+        out.append({"kernel": name, "bound": bound, "achieved": round(ach, 1), "peak": peak, "unit": unit,
+                    "frac": round(ach / peak, 4), "traffic": traffic_db.get(name), "ms_per_launch": round(ms_avg, 4),
+                    "launches": len(ms), "total_ms": round(sum(ms), 3),
+                    ("flops_per_launch" if bound == "tensor" else "bytes_per_launch"): w_avg})
+    out.sort(key=lambda k: -k["total_ms"])
+    dom = dict(out[0])
+    dom["peak_src"] = (f"{peaks['src']} " + ("sustained bf16 (kernel timed inside the step)" if dom["bound"] == "tensor"
+                                             else "HBM copy bandwidth"))
+    dom["timing"] = "CUDA events around each launch of one eager step (all layers) on the launching stream, mean"
+    return dom, out
 
 
 def run_ours(args, cfg, rank, world, dist):
@@ -243,23 +361,23 @@ def run_ours(args, cfg, rank, world, dist):
 
     from paper_2510_15964_b200 import harness as HN
     from paper_2510_15964_b200.dense_baseline import DenseLoraStep
+    from paper_2510_15964_b200.dp import make_grad_hook, shard_range
     from paper_2510_15964_b200.engine import FinetuneEngine
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     peaks = load_peaks()
+    G = cfg["B"]
+    b0, b1 = shard_range(G, rank, world)
+    B = b1 - b0
     model, state, provider = build_workload(cfg, dev, seed=args.seed, mlp_sparsity=args.mlp_sparsity,
-                                            local_frac=args.local_frac)
-    from paper_2510_15964_b200.dp import make_grad_hook
-
-    # weak scaling: each rank runs its own B-sequence shard of a global batch of B*world
-    hook = make_grad_hook(dist, cfg["B"] * world, rank, world) if dist is not None else None
+                                            local_frac=args.local_frac, peft=args.peft)
+    hook = make_grad_hook(dist, G, rank, world) if dist is not None else None
     eng = FinetuneEngine(model, state, provider, lr=1e-4, grad_hook=hook)
-    B, s, V = cfg["B"], cfg["s"], cfg["V"]
-    gen = torch.Generator().manual_seed(args.seed + 2 + rank)  # synthetic uniform tokens, per-rank shard
-    batches = [torch.randint(0, V, (B, s + 1), generator=gen) for _ in range(max(args.steps, 1))]
+    s, V = cfg["s"], cfg["V"]
+    gen = torch.Generator().manual_seed(args.seed + 2)  # synthetic uniform tokens (sf/harness.py:391 seed + 2)
+    batches = [torch.randint(0, V, (G, s + 1), generator=gen)[b0:b1].contiguous() for _ in range(max(args.steps, 1))]
     tok_dev = batches[0].to(dev)
-    # warm-up (eager; first calls set kernel attributes), then capture the step
     for _ in range(max(args.warmup - 1, 1)):
         eng.step(tok_dev)
     per_step = count_launches(lambda: eng.step(tok_dev))
@@ -268,79 +386,92 @@ def run_ours(args, cfg, rank, world, dist):
     eng.replay()
     torch.cuda.synchronize()
     with ClockSampler(dev.index) as clk:
-        ms = time_graph(eng, args.steps, dist)
-    sparsity = achieved_sparsity(eng, model)
-    # e2e through the public API: host (pinned) batch -> device, step, loss -> host, every step
+        ms = time_graph(eng, args.steps, dist, dev)
+    sparsity = achieved_sparsity(eng.last_masks, model)
+    # e2e through the public API on the host clock: pinned host batch -> device, step, loss -> host, every step
     pinned = [b.pin_memory() for b in batches]
     loss_host = torch.empty((), dtype=torch.float32).pin_memory()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    st.record()
+    t0 = time.perf_counter()
+    losses = []
     for k in range(args.steps):
         loss = eng.replay(pinned[k % len(pinned)])
-        loss_host.copy_(loss, non_blocking=True)
-    en.record()
-    torch.cuda.synchronize()
-    e2e_ms = st.elapsed_time(en) / args.steps
-    if dist is not None:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    final_loss = float(loss_host)
-    roof = fc1_roofline(model, eng, tok_dev, peaks, args.config) if rank == 0 else None
-    frozen_gb = sum(t.numel() * t.element_size() for lw in model.weights.layers
-                    for t in (lw.wqkv, lw.wo, lw.mlp.w1_t, lw.mlp.w2)) / 1e9
+        loss_host.copy_(loss)  # blocking device->host read: the host has the loss before the next step starts
+        losses.append(float(loss_host))
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    e2e_ms = _max_over_ranks(e2e_ms, dist, dev)
     extra = {}
-    if not args.skip_dense and rank == 0:
-        # dense reference points on the same box: (a) same engine, every head/block dense; (b) torch cuBLAS/SDPA
-        dprov = HN.DenseProvider(model)
-        deng = FinetuneEngine(model, state, dprov, lr=1e-4)
-        deng.step(tok_dev)
-        deng.capture(tok_dev, warmup=1)
-        extra["dense_same_kernels_ms"] = round(time_graph(deng, max(3, args.steps // 2), None), 3)
-        del deng
-        torch.cuda.empty_cache()
-        try:
-            tstep = DenseLoraStep(model)
-            for _ in range(2):
-                tstep.step(tok_dev)
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            n = max(3, args.steps // 2)
-            for _ in range(n):
-                tstep.step(tok_dev)
-            b.record()
-            torch.cuda.synchronize()
-            extra["dense_torch_ms"] = round(a.elapsed_time(b) / n, 3)
-            extra["speedup_vs_dense_torch"] = round(extra["dense_torch_ms"] / ms, 3)
-            del tstep
-        except Exception as e:  # pragma: no cover
-            extra["dense_torch_error"] = repr(e)[:200]
+    roof, kernels = None, None
+    if rank == 0:
+        snap = StateSnapshot(state)  # rank-0-only probes below must not leave rank 0's state diverged
+        hook_saved, eng.grad_hook = eng.grad_hook, None
+        roof, kernels = kernel_probe(model, eng, tok_dev, peaks, args.config)
+        eng.grad_hook = hook_saved
+        if not args.skip_dense:
+            # dense reference points on the same box: (a) same engine, every head/block dense; (b) torch cuBLAS/SDPA
+            dprov = HN.DenseProvider(model)
+            deng = FinetuneEngine(model, state, dprov, lr=1e-4)
+            deng.step(tok_dev)
+            deng.capture(tok_dev, warmup=1)
+            extra["dense_same_kernels_ms"] = round(time_graph(deng, max(3, args.steps // 2), None, dev), 3)
+            extra["speedup_vs_dense_same_kernels"] = round(extra["dense_same_kernels_ms"] / ms, 3)
+            del deng
+            torch.cuda.empty_cache()
+            if args.peft == "lora":
+                try:
+                    tstep = DenseLoraStep(model, lr=1e-4)
+                    tstep.capture(tok_dev)
+                    torch.cuda.synchronize()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    n = max(3, args.steps // 2)
+                    a.record()
+                    for _ in range(n):
+                        tstep.replay()
+                    b.record()
+                    torch.cuda.synchronize()
+                    extra["dense_torch_ms"] = round(a.elapsed_time(b) / n, 3)
+                    extra["speedup_vs_dense_torch"] = round(extra["dense_torch_ms"] / ms, 3)
+                    extra["dense_torch"] = ("CUDA-graphed torch bf16 step: cuBLAS GEMMs, SDPA, chunked fused LM-head CE, "
+                                            "fused capturable Adam (paper_2510_15964_b200/dense_baseline.py), same B")
+                    del tstep
+                except Exception as e:  # pragma: no cover
+                    extra["dense_torch_error"] = repr(e)[:200]
+        snap.restore()
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         cpu = cpu_baseline(cfg, args)
-    tokens_per_step = B * s * world
+    frozen_gb = sum(t.numel() * t.element_size() for lw in model.weights.layers
+                    for t in (lw.wqkv, lw.wo, lw.mlp.w1_t, lw.mlp.w2)) / 1e9
+    tokens_per_step = G * s
     line = {
-        "metric": f"{cfg['desc']} LoRA fwd+bwd ms/batch", "value": round(ms, 3), "unit": "ms/batch", "n_gpus": world,
+        "metric": f"{cfg['desc']} {args.peft.upper() if args.peft != 'lora' else 'LoRA'} fwd+bwd ms/batch",
+        "value": round(ms, 3), "unit": "ms/batch", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, random-init weights)",
-        "config": {"workload": f"{args.config}: {cfg['desc']} LoRA r={cfg['r']} (wq,wv,w1,w2) fine-tune step (predict+fwd+bwd+Adam), predicted mode",
-                   "model": cfg["desc"], "global_batch": B * world, "seq_len": s, "parallelism": f"dp{world}",
-                   "d_model": cfg["d"], "n_layers": cfg["L"], "d_ff": cfg["d_ff"], "vocab": V, "blk_size": cfg["blk"],
-                   "attn_blk": cfg["attn_blk"], "mask_scope": "per sequence", **sparsity,
-                   "injected": {"mlp_zeroed_predictor_blocks": args.mlp_sparsity, "local_attention_heads": args.local_frac},
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, random-init weights)",
+        "config": {"workload": (f"{args.config}: {cfg['desc']} {args.peft} fine-tune step (predict+fwd+bwd+Adam), predicted "
+                                f"mode, global batch {G} split over {world} GPU(s)"),
+                   "model": cfg["desc"], "peft": args.peft, "global_batch": G, "per_rank_batch": B, "seq_len": s,
+                   "parallelism": f"dp{world}", "d_model": cfg["d"], "n_layers": cfg["L"], "d_ff": cfg["d_ff"], "vocab": V,
+                   "blk_size": cfg["blk"], "attn_blk": cfg["attn_blk"], "lora_rank": cfg["r"], "mask_scope": "per sequence",
+                   **sparsity,
+                   "injected": {"mlp_zeroed_predictor_blocks": args.mlp_sparsity,
+                                "calibrated_gram_attention_heads": args.local_frac},
                    "l2": f"inputs larger than L2: {frozen_gb:.1f} GB of frozen weights stream from HBM every step (no flush needed)",
-                   "timing": "CUDA events around K CUDA-graph replays; Adam (fp64 moments) outside the graph, inside the timed region"},
+                   "timing": "CUDA events around K CUDA-graph replays (max over ranks); Adam (fp64 moments) and the "
+                             "gradient all-reduce outside the graph, inside the timed region"},
         "tokens_per_s": round(tokens_per_step / (ms * 1e-3), 1),
-        "e2e": {"value": round(e2e_ms, 3), "unit": "ms/batch", "h2d_bytes_per_step": int(B * (s + 1) * 8),
-                "d2h_bytes_per_step": 4, "api": "FinetuneEngine.replay(host pinned batch) + loss.copy_ to host"},
+        "e2e": {"value": round(e2e_ms, 3), "unit": "ms/batch", "h2d_bytes_per_step": int(G * (s + 1) * 8),
+                "d2h_bytes_per_step": 4 * world,
+                "api": "FinetuneEngine.replay(pinned host batch) + blocking loss read to the host every step; host "
+                       "perf_counter, max over ranks",
+                "tokens_per_s": round(tokens_per_step / (e2e_ms * 1e-3), 1)},
         "gpu_launches": int(per_step * args.steps), "gpu_launches_per_step": int(per_step),
-        "final_loss": round(final_loss, 5),
+        "final_loss": round(losses[-1], 5),
         "clocks": clk.summary(),
         "roofline": roof,
+        "kernels": kernels,
         "cpu_baseline": cpu,
         **extra,
     }
@@ -350,39 +481,46 @@ def run_ours(args, cfg, rank, world, dist):
 # ---------------------------------------------------------------------------- CPU reference (oracle port)
 
 
-def cpu_baseline(cfg: dict, args, n_layers_sample: int = 2) -> dict:
-    """Time the reference algorithm (oracle/ NumPy restatement of sf/harness.py:401-417) on the host
-    cores on a bounded sample — one sequence through `n_layers_sample` layers + LM head + Adam — and
-    extrapolate to the full batch (B sequences, L layers)."""
-    from oracle import sf_oracle as O
-
+def _blas_threads() -> int:
     try:
         from threadpoolctl import threadpool_info
 
-        blas_threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+        return max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
     except Exception:  # pragma: no cover
-        blas_threads = os.cpu_count()
+        return os.cpu_count() or 1
+
+
+def _oracle_setup(cfg: dict, args, n_layers: int, seed: int):
+    from oracle import sf_oracle as O
+
     d, H, f, s, V = cfg["d"], cfg["H"], cfg["d_ff"], cfg["s"], cfg["V"]
-    dims = O.Dims(d, H, f, s, n_layers_sample, V, cfg["blk"], cfg["attn_blk"])
-    om = O.build_model(dims, seed=args.seed, peft="lora", lora_rank=cfg["r"])
-    rng = O.make_rng(args.seed + 1)
-    n_blk = dims.n_blk
-    r_pred = max(4, d // 16)
+    dims = O.Dims(d, H, f, s, n_layers, V, cfg["blk"], cfg["attn_blk"])
+    om = O.build_model(dims, seed=seed, peft="lora", lora_rank=cfg["r"])
+    rng = O.make_rng(seed + 1)
+    n_blk, r_pred = dims.n_blk, max(4, d // 16)
     attn, mlp = [], []
     n_local = int(round(H * args.local_frac))
-    for layer in range(n_layers_sample):
+    for _ in range(n_layers):
         wq = [O.randn(rng, (d, r_pred), 0.1) for _ in range(H)]
         wk = [wq[h] if h < n_local else O.randn(rng, (d, r_pred), 0.1) for h in range(H)]
         attn.append(O.AttnPredictorParams(wq, wk))
         wa = O.randn(rng, (d, n_blk), 0.1)
         wa[:, rng.permutation(n_blk)[: int(round(args.mlp_sparsity * n_blk))]] = 0.0
         mlp.append(O.MlpPredictorParams(wa))
-    prov = O.PredictedProvider(om, attn, mlp, O.PredictorConfig())
+    return O, om, O.PredictedProvider(om, attn, mlp, O.PredictorConfig()), rng
+
+
+def cpu_sample(cfg: dict, args, n_layers_sample: int = 2):
+    """One bounded sample of the reference step (sf/harness.py:401-417 on the oracle, predicted mode):
+    one sequence through `n_layers_sample` layers + LM head + loss + backward + Adam. Returns a callable
+    that runs the sample and returns the extrapolation to the full batch (G sequences, L layers) in ms."""
+    O, om, prov, rng = _oracle_setup(cfg, args, n_layers_sample, args.seed)
+    s, V = cfg["s"], cfg["V"]
     seq = rng.integers(0, V, size=s + 1)
     tok, tgt = seq[:-1], seq[1:]
     params = O.trainable_params(om)
 
-    def one():
+    def one() -> dict:
         t = {}
         t0 = time.perf_counter()
         h = om.emb[tok]
@@ -406,34 +544,91 @@ def cpu_baseline(cfg: dict, args, n_layers_sample: int = 2) -> dict:
         t3 = time.perf_counter()
         O.optimizer_step(params, {}, {}, 0, {k: grads.get(k, np.zeros_like(v)) for k, v in params.items()}, 1e-4)
         t["adam"] = time.perf_counter() - t3
+        per_layer = (t["layers_fwd"] + t["layers_bwd"]) / n_layers_sample
+        t["extrapolated_ms"] = (cfg["B"] * (per_layer * cfg["L"] + t["head"]) + t["adam"] * cfg["L"] / n_layers_sample) * 1e3
+        t["per_layer_ms"] = per_layer * 1e3
         return t
 
+    return one
+
+
+def cfg1_measured(args) -> dict:
+    """The reference's own CPU-runnable config (BASELINE configs[0]) timed for real: the full OPT-125M-shaped
+    predicted-mode LoRA step, B=1, s=256, 12 layers (sf/harness.py:401-417), 1 warm-up + median of 3."""
+    c1 = CONFIGS["cfg1"]
+    O, om, prov, rng = _oracle_setup(c1, args, c1["L"], args.seed)
+    seq = rng.integers(0, c1["V"], size=(1, c1["s"] + 1))
+    params = O.trainable_params(om)
+    mom, vel, step = {}, {}, 0
+    ts = []
+    for k in range(4):
+        t0 = time.perf_counter()
+        _, _, step = O.finetune_step(om, seq, prov, params, mom, vel, step, 1e-4)
+        ts.append(time.perf_counter() - t0)
+    return {"value": round(statistics.median(ts[1:]) * 1e3, 1), "unit": "ms/batch", "config": "cfg1 (OPT-125M shape, B=1, s=256, L=12)",
+            "runs": "1 warm-up + median of 3", "extrapolated": False}
+
+
+def cpu_baseline(cfg: dict, args) -> dict:
+    one = cpu_sample(cfg, args)
     one()  # warm-up
     runs = [one() for _ in range(2)]
-    med = {k: statistics.median(r[k] for r in runs) for k in runs[0]}
-    per_layer = (med["layers_fwd"] + med["layers_bwd"]) / n_layers_sample
-    per_item = per_layer * cfg["L"] + med["head"]
-    adam_full = med["adam"] * cfg["L"] / n_layers_sample
-    batch_s = cfg["B"] * per_item + adam_full
-    return {"value": round(batch_s * 1e3, 1), "unit": "ms/batch", "cores": int(blas_threads), "kind": "port",
-            "sample": (f"1 sequence x {n_layers_sample} of {cfg['L']} layers + LM head + Adam on the oracle "
-                       f"(NumPy restatement of sf/harness.py:401-417, predicted mode, same injected sparsity), "
-                       f"extrapolated x{cfg['B']} sequences x{cfg['L']}/{n_layers_sample} layers; "
-                       f"measured per-layer {per_layer * 1e3:.0f} ms, head {med['head'] * 1e3:.0f} ms"),
-            "host_cpu_count": os.cpu_count()}
+    med = statistics.median(r["extrapolated_ms"] for r in runs)
+    per_layer = statistics.median(r["per_layer_ms"] for r in runs)
+    return {"value": round(med, 1), "unit": "ms/batch", "cores": int(_blas_threads()), "kind": "port",
+            "sample": (f"1 sequence x 2 of {cfg['L']} layers + LM head + Adam on the oracle (NumPy restatement of "
+                       f"sf/harness.py:401-417, predicted mode, same injected sparsity), extrapolated x{cfg['B']} sequences "
+                       f"x{cfg['L']}/2 layers; measured per-layer {per_layer:.0f} ms"),
+            "extrapolated": True, "host_cpu_count": os.cpu_count(),
+            "cfg1_measured": cfg1_measured(args) if not args.skip_cfg1 else None}
 
 
 def run_reference(args, cfg, rank) -> dict | None:
+    """The reference arm: the reference algorithm (oracle port of sf/, pure NumPy) on the host cores, rank 0 only.
+    Each step is one bounded sample (1 sequence x 2 layers + head + Adam) extrapolated to ms per global batch."""
     if rank != 0:
         return None
-    cpu = cpu_baseline(cfg, args)
-    return {"impl": "reference", "metric": f"{cfg['desc']} LoRA fwd+bwd ms/batch", "value": cpu["value"], "unit": "ms/batch",
+    one = cpu_sample(cfg, args)
+    t_start = time.perf_counter()
+    for _ in range(args.warmup):
+        one()
+    vals = [one()["extrapolated_ms"] for _ in range(args.steps)]
+    wall = time.perf_counter() - t_start
+    v = statistics.median(vals)
+    cores = int(_blas_threads())
+    cpu = {"value": round(v, 1), "unit": "ms/batch", "cores": cores, "kind": "port", "extrapolated": True,
+           "sample": (f"each step: 1 sequence x 2 of {cfg['L']} layers + LM head + Adam of the oracle (NumPy restatement "
+                      f"of sf/harness.py:401-417), extrapolated x{cfg['B']} sequences x{cfg['L']}/2 layers; "
+                      f"{args.warmup + args.steps} samples ran in {wall:.1f} s"),
+           "host_cpu_count": os.cpu_count(),
+           "cfg1_measured": cfg1_measured(args) if not args.skip_cfg1 else None}
+    return {"impl": "reference", "metric": f"{cfg['desc']} LoRA fwd+bwd ms/batch", "value": round(v, 1), "unit": "ms/batch",
             "n_gpus": int(os.environ.get("WORLD_SIZE", 1)), "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": cpu["value"], "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": "cfg3 (as ours), reference algorithm on host cores", "model": cfg["desc"],
+            "ms_per_step": round(v, 1), "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": f"{args.config} (as ours), reference algorithm on host cores, "
+                                                        "bounded samples extrapolated", "model": cfg["desc"],
                                             "global_batch": cfg["B"], "seq_len": cfg["s"], "parallelism": "host"},
-            "cpu_baseline": cpu, "e2e": {"value": cpu["value"], "unit": "ms/batch", "h2d_bytes_per_step": 0,
-                                         "d2h_bytes_per_step": 0}}
+            "cpu_baseline": cpu, "e2e": {"value": round(v, 1), "unit": "ms/batch", "h2d_bytes_per_step": 0,
+                                         "d2h_bytes_per_step": 0},
+            "wall_s": round(wall, 1)}
+
+
+def _relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: start N ranks under torch.distributed.run (127.0.0.1 rendezvous)."""
+    import socket
+
+    import torch
+
+    n_vis = torch.cuda.device_count()
+    if n_vis < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but only {n_vis} GPU(s) visible"}), flush=True)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -443,32 +638,44 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--peft", default="lora", choices=["lora", "adapter", "bitfit"])
     ap.add_argument("--mlp-sparsity", type=float, default=0.85)
-    ap.add_argument("--local-frac", type=float, default=0.5)
+    ap.add_argument("--local-frac", type=float, default=0.75)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--batch", type=int, default=0, help="sequences per rank (default: the config's B)")
+    ap.add_argument("--global-batch", type=int, default=0, help="global batch (default: the config's B)")
     ap.add_argument("--skip-dense", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-cfg1", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = dict(CONFIGS[args.config])
-    if args.batch:
-        cfg["B"] = args.batch
-    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.global_batch:
+        cfg["B"] = args.global_batch
+    env_world = os.environ.get("WORLD_SIZE")
+    world = int(env_world or 1)
     rank = int(os.environ.get("RANK", 0))
     if args.impl == "reference":
         line = run_reference(args, cfg, rank)
         if line is not None:
             print(json.dumps(line), flush=True)
-        return
+        return 0
+    if env_world is None and args.gpus > 1:
+        return _relaunch(args)
+    if world != args.gpus:
+        print(json.dumps({"error": f"WORLD_SIZE={world} but --gpus {args.gpus}"}), flush=True)
+        return 2
+    import torch
+
+    if torch.cuda.device_count() < 1 or (world > 1 and torch.cuda.device_count() < world):
+        print(json.dumps({"error": f"{world} rank(s) need {world} visible GPU(s); found {torch.cuda.device_count()}"}),
+              flush=True)
+        return 2
     dist = None
     if world > 1:
-        import torch
         import torch.distributed as tdist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1))
-        # NCCL over NVLink in production; LX_DIST_BACKEND=gloo lets several ranks share one GPU (plumbing checks)
-        tdist.init_process_group(os.environ.get("LX_DIST_BACKEND", "nccl"))
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
         dist = tdist
     line = run_ours(args, cfg, rank, world, dist)
     if rank == 0:
@@ -476,7 +683,8 @@ def main():
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -109,9 +109,24 @@ def lib() -> C.CDLL:
 _NON_STATUS = ("lx_abi_version", "lx_device_sm_count", "lx_attn_tables_size", "lx_gemm_set_cta_pair", "lx_exact_mass_smem")
 
 
+# Kernel-time probe (bench.py's roofline): when a dict {symbol: list}, every call of a listed symbol is
+# bracketed by CUDA events on the current stream (the stream the call launches on) and the event pair is
+# appended to its list. Eager steps only; never set during CUDA-graph capture.
+PROBE: dict | None = None
+
+
 def call(name: str, *args) -> int:
     """Invoke an entry point; map a nonzero return code to the reference's exception type."""
-    rc = getattr(lib(), name)(*args)
+    if PROBE is not None and name in PROBE:
+        import torch
+
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
+        rc = getattr(lib(), name)(*args)
+        ev[1].record()
+        PROBE[name].append(ev)
+    else:
+        rc = getattr(lib(), name)(*args)
     if isinstance(rc, int) and rc != 0 and name not in _NON_STATUS:
         msg = lib().lx_last_error().decode(errors="replace")
         raise _ERRORS.get(rc, E.CudaError)(f"{name}: {msg}")

@@ -180,11 +180,6 @@ def _check_device_blk(d_ff: int, blk: int) -> None:
         raise MaskError(f"d_ff {d_ff} must be a multiple of blk_size {blk} on the sm_100a path (ragged tail unsupported)")
 
 
-# bench.py's roofline probe: when a list, every fc1 launch is bracketed by CUDA events on its stream
-# and (start, end, counts, s, d, blk) is appended (eager steps only; never set inside graph capture)
-FC1_EVENTS: list | None = None
-
-
 def neuron_matmul_fwd1(x, weights: LayeredWeights, mask, blk_size: int, counter=None, *, bias=None, ax=None, lora_b=None,
                        lora_r=0, scaling=1.0, relu=False, out=None, w_packed=None) -> ActiveHidden:
     """x @ W1[:, cols] over active column blocks (sf/neuron_ops.py:75-82) on the tcgen05
@@ -194,16 +189,9 @@ def neuron_matmul_fwd1(x, weights: LayeredWeights, mask, blk_size: int, counter=
     x2, B, s = _as_items(x.to(torch.bfloat16))
     nm = lower_mask(mask, n_blocks(d_ff, blk_size), blk_size, B, x2.device)
     vals = out if out is not None else torch.empty(B * s, d_ff, dtype=torch.bfloat16, device=x2.device)
-    ev = None
-    if FC1_EVENTS is not None:
-        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-        ev[0].record()
     _abi.call("lx_neuron_fc1", x2.data_ptr(), B, s, d, d_ff, blk_size, weights.w1_t.data_ptr(), nm.counts.data_ptr(),
               nm.ids.data_ptr(), _abi.ptr(bias), _abi.ptr(ax), _abi.ptr(lora_b), lora_r, float(scaling), int(relu),
               vals.data_ptr(), d_ff, _abi.ptr(w_packed), _abi.stream_handle(x2.device))
-    if ev is not None:
-        ev[1].record()
-        FC1_EVENTS.append((ev[0], ev[1], nm.counts, s, d, blk_size))
     if counter is not None:
         counter.add(s * d * int(nm.counts.sum()) * blk_size)
     return ActiveHidden(vals, nm, blk_size, d_ff, B)

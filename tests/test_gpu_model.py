@@ -3,8 +3,11 @@ sf/harness.py) against the reference's golden outputs and the oracle.
 
 Tolerance (stated per north_star): bf16 operands with fp32 accumulation ->
 tensor-level max|gpu - ref| / max|ref| <= 1e-2 for logits, activations and
-LoRA / Adapter / BitFit gradients; loss within 1e-2 relative. Gradients of
-inactive neuron blocks must be exactly zero (sf/autograd.py:89-90)."""
+every LoRA / Adapter / BitFit gradient tensor; loss within 1e-2 relative.
+Logits and loss are compared with the reference's float32 outputs; gradients
+with the bf16 rounding-point oracle (oracle/bf16_emul.py, pinned to the
+reference in tests/test_bf16_emul.py). Gradients of inactive neuron blocks
+must be exactly zero (sf/autograd.py:89-90)."""
 
 import numpy as np
 import pytest
@@ -52,14 +55,45 @@ def _golden_model(g, peft):
     return om, masks
 
 
+def emulated(om, toks, masks):
+    """The bf16 rounding-point oracle (oracle/bf16_emul.py) on one sequence: (logits, grads)."""
+    from oracle import bf16_emul as E
+
+    e = E.Emul()
+    lg, c = E.model_forward(e, om, toks[:-1], masks)
+    return lg, E.model_backward(e, om, c, O.loss_backward(lg, toks[1:]))
+
+
+def check_grads(grads, ref: dict, tol: float = 1e-2):
+    """Every gradient tensor within max|dev - ref| / max|ref| <= tol; all-zero references (inactive
+    neuron blocks, unreached parameters) exactly zero on the device; inactive columns of w1.lora_b /
+    w2.lora_a / b1 exactly zero; bk (exactly 0 by softmax shift invariance) bounded absolutely by tol *
+    max|g_bv|. Returns the worst relative error."""
+    worst = 0.0
+    for n, v in ref.items():
+        gr = grads[n].detach().float().cpu().numpy()
+        if np.abs(v).max() == 0:
+            assert float(np.abs(gr).max()) == 0, n
+            continue
+        if n.endswith(".bk"):
+            assert np.abs(gr - v).max() <= tol * np.abs(ref[n[:-2] + "bv"]).max(), n
+            continue
+        if n.endswith("w1.lora_b") or n.endswith("w2.lora_a") or n.endswith(".b1"):
+            assert np.all(gr[v == 0] == 0), n  # inactive neuron blocks untouched (sf/autograd.py:89-90)
+        e = rel(gr, v)
+        worst = max(worst, e)
+        assert e <= tol, (n, e)
+    return worst
+
+
 @pytest.mark.parametrize("peft", ["lora", "adapter", "bitfit"])
 def test_model_fwd_bwd_matches_reference(dev, golden, peft):
-    """The reference's own fixture (s=64, init 0.02). Logits / loss at 1e-2 against the
-    reference outputs. Its gradients are ill-conditioned for bf16 activations (ReLU
-    pre-activations within bf16 resolution of 0 flip sign; near-uniform attention gives
-    q/k a common mode ~3.6x their spread, so dq cancels) -- measured in
-    tests/test_gpu_model.py::test_model_grads_well_conditioned and DESIGN.md. Here the
-    gradient bar is direction (cosine >= 0.97) plus exact structural zeros."""
+    """The reference's own fixture (tests/golden/model.npz: s=64, init 0.02, unmodified). Logits and loss
+    within 1e-2 of the reference's float32 outputs. Every LoRA / Adapter / BitFit gradient tensor within
+    1e-2 (max|dev - ref| / max|ref|) of the bf16 rounding-point oracle (oracle/bf16_emul.py, pinned to the
+    reference by tests/test_bf16_emul.py): the fixture amplifies bf16 rounding (ReLU pre-activations within
+    bf16 resolution of 0, near-uniform attention), so float32 itself sits up to 0.23 away from any bf16
+    implementation (measured in tests/test_bf16_emul.py::test_bf16_rounding_points_move_gradients)."""
     from paper_2510_15964_b200 import autograd as AG, model as M
 
     g = golden("model")
@@ -72,28 +106,17 @@ def test_model_fwd_bwd_matches_reference(dev, golden, peft):
     loss = M.loss_forward(logits, toks[1:])
     assert abs(loss - float(g[f"{peft}/loss"])) < 1e-2 * abs(float(g[f"{peft}/loss"]))
     grads = AG.model_backward(m, cache, M.loss_backward(logits, toks[1:]), masks)
-    for n, gr in grads.items():
-        ref = g[f"{peft}/grad/{n}"]
-        if np.abs(ref).max() == 0:
-            assert float(gr.abs().max()) == 0, n
-        elif n.endswith(".bk"):  # true gradient is 0 (softmax shift invariance)
-            assert float((gr.cpu() - torch.from_numpy(ref)).abs().max()) < 1e-4, n
-        else:
-            assert cos(gr, ref) > 0.97, (n, cos(gr, ref))
-        if n.endswith("w1.lora_b") or n.endswith("w2.lora_a") or n.endswith(".b1"):
-            assert np.all(gr.detach().cpu().numpy()[ref == 0] == 0), n  # inactive neuron blocks untouched
+    lg_e, ref = emulated(om, toks, masks_o)
+    assert rel(logits, lg_e) < 1e-3
+    check_grads(grads, ref)
 
 
 @pytest.mark.parametrize("peft", ["lora", "adapter", "bitfit"])
 def test_model_grads_well_conditioned(dev, golden, peft):
-    """Same fixture with margin-separated ReLU pre-activations (b1 = +-1) and moderately sharper
-    attention (W_q, W_k x 3, so q/k lose the common mode that near-uniform attention builds up, without
-    going one-hot): MLP-side gradients (w1/w2 LoRA, b1/b2, MLP adapter) within max|d| / max|ref| <= 1e-2
-    of the fp32 oracle; attention-side gradients (q/k/v/o LoRA and biases, attention adapter) within 5e-2
-    -- their bf16 operands (q, k, v, O, dO) feed dq = sum_j dS_ij k_j and dS = P (dP - rowsum), both
-    cancelling sums; the tcgen05 dQ kernel removes the bf16 row-sum residual of dS against the keys'
-    common mode, csrc/attn_sm100.cu) -- and bq (a sum of dq over tokens, ~0 by shift invariance) within
-    1e-2 of max|g_bv|."""
+    """Same fixture with margin-separated ReLU pre-activations (b1 = +-1) and sharper attention
+    (W_q, W_k x 3): every gradient within 1e-2 of the bf16 rounding-point oracle, and within 5e-2 of
+    the float32 oracle (on this fixture bf16 rounding alone is worth a few 1e-2 on attention-side
+    gradients, which feed cancelling sums)."""
     from paper_2510_15964_b200 import autograd as AG, model as M
 
     g = golden("model")
@@ -111,25 +134,14 @@ def test_model_grads_well_conditioned(dev, golden, peft):
     logits, cache = M.model_forward(m, toks[:-1], masks)
     assert rel(logits, lg) < 1e-2
     grads = AG.model_backward(m, cache, M.loss_backward(logits, toks[1:]), masks)
-    for n, v in og.items():
-        if np.abs(v).max() == 0:
-            assert float(grads[n].abs().max()) == 0, n
-        elif n.endswith(".bq"):  # sum over tokens of dq: near-zero by shift invariance -> absolute bound
-            bv = og[n[:-2] + "bv"]
-            err = float(np.abs(grads[n].cpu().numpy() - v).max())
-            assert err <= 1e-2 * np.abs(bv).max(), (n, err)
-        elif not n.endswith(".bk"):
-            attn_path = any(k in n for k in (".wq.", ".wk.", ".wv.", ".wo.", ".bo", ".bv", "attn_adapter"))
-            tol = 5e-2 if attn_path else 1e-2
-            if n.endswith("attn_adapter.b_down"):
-                # sum over tokens of an 8-dim projection of dx through W_up: norm 0.0072 vs b_up's 0.166
-                # in the fp32 oracle (a cancelling sum like bq); measured 5.3e-2 on B200
-                tol = 1e-1
-            assert rel(grads[n], v) < tol, (n, rel(grads[n], v))
+    check_grads(grads, emulated(om, toks, masks_o)[1])
+    check_grads(grads, og, tol=5e-2)
 
 
 def test_batched_items_equal_per_item_loop(dev):
-    """B items with different per-item masks in one batched call == the reference's per-item loop."""
+    """B items with different per-item masks in one batched call == the reference's per-item loop: logits
+    and loss per item against the float32 oracle at 1e-2, the batch-summed gradients against the summed
+    per-item bf16 rounding-point oracle at 1e-2."""
     from paper_2510_15964_b200 import autograd as AG, model as M
 
     dims = O.Dims(128, 2, 256, 128, 2, 80, 16, 32)
@@ -153,11 +165,10 @@ def test_batched_items_equal_per_item_loop(dev):
         lg, c = O.model_forward(om, toks[b, :-1], om_masks)
         assert rel(logits[b], lg) < 1e-2
         ref_loss.append(O.loss_forward(lg, toks[b, 1:]))
-        for n, v in O.model_backward(om, c, O.loss_backward(lg, toks[b, 1:])).items():
+        for n, v in emulated(om, toks[b], om_masks)[1].items():
             gsum[n] = gsum.get(n, 0) + v
     assert abs(loss - np.mean(ref_loss)) < 1e-2 * abs(np.mean(ref_loss))
-    for n, v in gsum.items():
-        assert cos(grads[n], v) > 0.97 if np.abs(v).max() > 0 else float(grads[n].abs().max()) == 0, n
+    check_grads(grads, gsum)
 
 
 def test_finetune_step_predicted_mode(dev, golden):
@@ -203,7 +214,6 @@ def test_engine_graph_replay_matches_eager_steps(dev):
     cfg = dict(d=256, H=4, d_ff=1024, L=2, V=128, B=2, s=128, blk=16, attn_blk=32, r=8)
     m1, s1, p1 = bench.build_workload(cfg, dev, 5, 0.5, 0.5)
     m2, s2, p2 = bench.build_workload(cfg, dev, 5, 0.5, 0.5)
-    assert m2.weights.layers[0].lora_pack is None
     eng = FinetuneEngine(m2, s2, p2, lr=1e-3)
     assert m2.weights.layers[0].lora_pack["kx"] == 16  # wq + wv at r = 8: the K-extended path is live
     g = torch.Generator(device="cpu").manual_seed(9)
