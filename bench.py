@@ -140,14 +140,16 @@ class ClockSampler:
 class _CalibratingProvider:
     """One forward in which each layer's attention predictor is built from the LN1 output the layer
     actually receives (so from the predicted patterns / masks of all earlier layers): heads < n_local get
-    a Gram predictor W_q = W_k = (I - c c^T) R, c the layer's residual-stream common mode (mean LN1 row);
-    the remaining heads independent random factors (N(0, 0.1^2), sf/predictor.py:194-206). Without the
-    projection every token pair shares the common mode and the Gram map is dense."""
+    a Gram predictor W_q = W_k = (I - U U^T) R, U the layer's k_shared dominant row directions (top right
+    singular vectors of the LN1 output: the residual stream's common mode and the components that blocks of
+    tokens share); the remaining heads independent random factors (N(0, 0.1^2), sf/predictor.py:194-206).
+    Without the projection every token pair shares those directions and the Gram map is dense."""
 
     fused_downsample = False
 
-    def __init__(self, inner, n_local: int, r_pred: int, g, device):
+    def __init__(self, inner, n_local: int, r_pred: int, g, device, k_shared: int = 32):
         self.inner, self.n_local, self.r_pred, self.g, self.device = inner, n_local, r_pred, g, device
+        self.k_shared = k_shared
 
     def attn_patterns(self, layer, h, x_small=None):
         import torch
@@ -156,13 +158,15 @@ class _CalibratingProvider:
 
         d = h.shape[-1]
         H = self.inner.model.dims.n_heads
-        c = h.float().reshape(-1, d).mean(0)
-        c = c / c.norm().clamp_min(1e-12)
+        # the shared directions of the layer's rows: the top singular vectors of the LN1 output (the mean
+        # direction first); projecting them out of R leaves token-specific directions only
+        _, _, vh = torch.linalg.svd(h.float().reshape(-1, d), full_matrices=False)
+        U = vh[: self.k_shared].t().contiguous()  # [d, k]
         wq, wk = [], []
         for hh in range(H):
             w = torch.randn(d, self.r_pred, generator=self.g, device=self.device) * 0.1
             if hh < self.n_local:
-                w = w - torch.outer(c, c @ w)
+                w = w - U @ (U.t() @ w)
                 wq.append(w)
                 wk.append(w)
             else:

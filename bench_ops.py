@@ -192,8 +192,8 @@ def sweep_attn(args, timer, peak):
                 grids[h, cs[:, 0], cs[:, 1]] = True
                 nnz += len(cs)
             dp = PT.DevicePool([f"h{h}" for h in range(H)], None, None, None, s, ab)
-            dp.tables = torch.from_numpy(PT.tables_from_grids(grids, s, ab)).cuda()
-            dp.tables128 = torch.from_numpy(PT.tables128_from_grids(grids, s, ab)).cuda()
+            tab = PT.tables128_from_grids(grids, s, ab)
+            dp.tables = torch.from_numpy(tab).cuda()
             pidx = torch.arange(H, dtype=torch.int32, device="cuda")[None]
             Q, K, V = qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :]
             o = torch.empty(M, d, dtype=torch.bfloat16, device="cuda")
@@ -209,8 +209,9 @@ def sweep_attn(args, timer, peak):
                 BS.attention_backward(Q, K, V, st["o"], dO, 3 * d, B, s, H, hd, pidx, 0, dp, scale, st["lse"],
                                       dqkv[:, :d], dqkv[:, d : 2 * d], dqkv[:, 2 * d :])
 
-            # active block density in 128x128-tile terms (what the kernel walks) for the record
-            tiles = int(np.asarray(dp.tables128.cpu().numpy().view(np.uint32)[:4])[0])
+            # gathered 128x128 MMA tiles the kernels walk (forward / dQ and dK/dV), summed over heads
+            work = [PT.tables128_work(tab, h) for h in range(H)]
+            tiles_f, tiles_b = sum(w[0] for w in work), sum(w[1] for w in work)
             for phase, fn, mult in (("fwd", fwd, 4), ("bwd", bwd, 8)):
                 ms = timer(fn, args.reps)
                 if sp == 0.0:
@@ -218,7 +219,8 @@ def sweep_attn(args, timer, peak):
                 fl = mult * B * nnz * ab * ab * hd  # nnz summed over heads
                 rows.append(line("block_sparse_attn", phase, sp, ms, fl, peak, {
                     "attn_blk": ab, "n_b": n_b, "nnz_per_head": round(nnz / H, 1),
-                    "density": round(nnz / (H * n_b * n_b), 4), "B": B, "s": s, "H": H, "hd": hd, "q_tiles": tiles,
+                    "density": round(nnz / (H * n_b * n_b), 4), "B": B, "s": s, "H": H, "hd": hd,
+                    "mma_tiles_fwd_dq": tiles_f, "mma_tiles_dkdv": tiles_b, "dense_tiles": H * (-(-s // 128)) ** 2,
                     "speedup_vs_same_kernel_dense": round(dense_ms[phase] / ms, 3),
                     "kernels": "bsattn_fwd_tc" if phase == "fwd" else "bsattn_delta_tc + bsattn_dkdv_tc + bsattn_dq_tc"}))
     # dense SDPA (flash) of the same shape, non-causal
@@ -287,7 +289,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--ops", default="mlp,attn")
     ap.add_argument("--sparsity", default="0.5,0.75,0.9")
-    ap.add_argument("--attn-blk", default="64,128")
+    ap.add_argument("--attn-blk", default="16,64,128")
     args = ap.parse_args()
     args.sparsity = [float(x) for x in args.sparsity.split(",")]
     args.attn_blk = [int(x) for x in args.attn_blk.split(",")]

@@ -196,40 +196,33 @@ long long lx_colgrad_group_ws_floats(const lx_colgrad_problem* probs, int n_prob
 int lx_colgrad_group(const lx_colgrad_problem* probs, int n_probs, int n_items, int s, float* ws, lx_stream_t stream);
 
 /* ------------------------------------------------------------------ K3 block-sparse attention
- * q,k,v,o: bf16 [n_items*s, ld] with head h at columns [h*hd, (h+1)*hd); non-causal; scale = 1/sqrt(hd).
- * pattern_idx: int32 [n_items, H] pool index per (item, head) (or [1,H] with item_stride 0).
- * Tile tables (from lx_attn_tables): per pool pattern, CSR over q-tiles and CSC over k-tiles of
- * 64x64 tiles with a 16-bit mask of active 16x16 cells.
- * fwd = sdd -> sparse_softmax -> dsd (sf/block_sparse.py:47-126); lse fp32 [n_items, H, s]. */
-int lx_attn_tables_size(int n_pool, int s, int attn_blk, int* n_row_entries);
-int lx_attn_tables(const int32_t* pool_kind_host, const int32_t* pool_param_host, int n_pool, int s, int attn_blk,
-                   int32_t* host_out, int host_out_ints);
-int lx_bsattn_fwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, int ld, int n_items, int s, int H, int hd,
-                  const int32_t* pattern_idx, int item_stride, const int32_t* tables, int n_pool, float scale,
-                  uint16_t* o, int ldo, float* lse, lx_stream_t stream);
-/* Same forward on tcgen05 (hd 64 or 128) over the fused projection output qkv [n_items*s, 3*H*hd]
- * (q | k | v column blocks) and 128x128-tile tables (64-bit cell masks, patterns.tables128_from_grids). */
+ * One implementation: tcgen05 flash kernels (csrc/attn_sm100.cu), hd 64 or 128 (other head dims are
+ * zero-padded to 64 / 128 by the Python shim, block_sparse.py), non-causal, explicit scale.
+ * qkv: the fused projection output bf16 [n_items*s, ld] with q | k | v column blocks of H*hd each
+ * (head h at columns h*hd of each block). pattern_idx: int32 [n_items, H] pool index per (item, head)
+ * (or [1, H] with item_stride 0).
+ * tables128: gathered 128-tile tables (patterns.tables128_from_grids): per pattern, CSR over 128-query
+ * tiles and CSC over 128-key tiles whose entries each stack 128 / gather_rows units of gather_rows
+ * consecutive tokens (gather_rows = gcd(attn_blk, 128)) with a 64-bit mask of active 16x16 cells, so
+ * the MMA work is proportional to the active blocks (sf/block_sparse.py:47-137 computes exactly the
+ * layout's blocks).
+ * fwd = sdd -> sparse_softmax -> dsd (sf/block_sparse.py:47-126, sf/model.py:343-353); o bf16 with row
+ * stride ldo, lse fp32 [n_items, H, s]. */
 int lx_bsattn_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H, int hd, const int32_t* pattern_idx,
-                     int item_stride, const int32_t* tables128, float scale, uint16_t* o, int ldo, float* lse,
-                     lx_stream_t stream);
-/* Backward on tcgen05 (hd 64 or 128): dqkv [n_items*s, 3*H*hd] (same fused layout as qkv) from
- * d_o [n_items*s, ld_o] and the forward's o / lse; delta_ws fp32 [n_items, H, s]; ksum_ws fp32
- * [n_items, H, ceil(s/128), hd] (per-key-tile column sums of K, used by dQ to cancel the bf16
- * row-sum residual of dS against the keys' common mode). dK/dV walk the CSC of each 128-key tile,
- * dQ the CSR of each 128-query tile (sf/block_sparse.py:63-137). */
-/* (ld: row stride of the fused qkv input; ld_d: row stride of the fused dqkv output.) */
+                     int item_stride, const int32_t* tables128, int gather_rows, float scale, uint16_t* o, int ldo,
+                     float* lse, lx_stream_t stream);
+/* Backward (dsd_backward -> sparse_softmax_backward -> sdd_backward, sf/block_sparse.py:63-137;
+ * replaces mha_backward's per-head loop, sf/autograd.py:149-156): dqkv [n_items*s, ld_d] (same fused
+ * layout as qkv) from d_o [n_items*s, ld_o] and the forward's o / lse; delta_ws fp32 [n_items, H, s];
+ * ksum_ws fp32 [n_items, H, ceil(s/128), hd] (per-key-tile column sums of K, used by dQ to cancel the
+ * bf16 row-sum residual of dS against the keys' common mode). dK/dV walk the CSC of each 128-key tile,
+ * dQ the CSR of each 128-query tile. */
 int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
-                     int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128, float scale,
-                     const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv, lx_stream_t stream);
+                     int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128, int gather_rows,
+                     float scale, const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv, lx_stream_t stream);
 /* Debug only: per-CTA clock64 phase stamps of the tcgen05 attention kernels into buf
  * [n_ctas][32] (slot 31 = SM id); NULL disables. Used by tools/attn_trace.py. */
 int lx_debug_set_attn_trace(unsigned long long* buf);
-/* dsd_backward -> sparse_softmax_backward -> sdd_backward (sf/block_sparse.py:63-137).
- * o/d_o row stride ld_o; delta_ws fp32 [n_items, H, s]; dq/dk/dv bf16 with stride ld like q. */
-int lx_bsattn_bwd(const uint16_t* q, const uint16_t* k, const uint16_t* v, const uint16_t* o, const uint16_t* d_o, int ld,
-                  int ld_o, int n_items, int s, int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables,
-                  int n_pool, float scale, const float* lse, float* delta_ws, uint16_t* dq, uint16_t* dk, uint16_t* dv,
-                  lx_stream_t stream);
 
 /* ------------------------------------------------------------------ glue (fused neighbours)
  * layernorm_forward (sf/model.py:307-312), fp32 residual in, bf16 out; saves mean/inv_std.

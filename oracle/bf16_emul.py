@@ -51,10 +51,18 @@ def bf16(x) -> np.ndarray:
 
 
 class Emul:
-    """Rounding policy: `rd` is bf16 rounding (device) or the identity (exact=True)."""
+    """Rounding policy: `rd` is bf16 rounding (device) or the identity (exact=True).
 
-    def __init__(self, exact: bool = False):
+    `relu` (optional) teacher-forces the discrete ReLU decisions: {(layer, "mlp"): bool [s, F_act],
+    (layer, "attn_ad") / (layer, "mlp_ad"): bool [s, r]} taken from the implementation under test. A
+    pre-activation within accumulation-order noise of 0 can land on either side in two correct bf16
+    implementations, and on ill-conditioned fixtures one such flip moves a gradient tensor by >1e-2; with
+    the decisions shared, the comparison measures the continuous arithmetic only (like giving both sides
+    the same neuron / attention masks)."""
+
+    def __init__(self, exact: bool = False, relu: dict | None = None):
         self.exact = exact
+        self.relu = relu or {}
 
     def rd(self, x):
         return np.asarray(x, np.float32) if self.exact else bf16(x)
@@ -208,7 +216,7 @@ def mha_backward(e: Emul, g, c, lw, lora, dims, grads, prefix, bitfit):
     return e.rd(dx)
 
 
-def mlp_forward(e: Emul, x, lw, lora, neuron_mask, dims, out_f32=False):
+def mlp_forward(e: Emul, x, lw, lora, neuron_mask, dims, out_f32=False, layer=None):
     """sf/model.py:363-400 at the device's rounding points; x = bf16 LN2 output."""
     _, cols = O.active_columns(neuron_mask, dims.d_ff, dims.blk_size)
     z = e.mm(x, e.rd(lw["w1"])[:, cols]) + lw["b1"][cols]
@@ -217,13 +225,17 @@ def mlp_forward(e: Emul, x, lw, lora, neuron_mask, dims, out_f32=False):
     if ad1 is not None and cols.size:
         ax1 = e.mm(x, ad1["a"])
         z = z + np.float32(ad1["scaling"]) * e.mm(ax1, ad1["b"][:, cols])
-    a = e.rd(np.maximum(z, 0))
+    act = z > 0
+    forced = e.relu.get((layer, "mlp"))
+    if forced is not None:
+        act = np.asarray(forced, bool)[:, : z.shape[1]]
+    a = e.rd(np.where(act, z, 0))
     out = e.mm(a, e.rd(lw["w2"])[cols, :]) + lw["b2"]
     if ad2 is not None and cols.size:
         ax2 = e.mm(a, ad2["a"][cols, :])
         out = out + np.float32(ad2["scaling"]) * e.mm(ax2, ad2["b"])
     out = out.astype(np.float32) if out_f32 else e.rd(out)
-    return out, {"x": x, "z": z, "a": a, "cols": cols, "ax1": ax1, "ax2": ax2}
+    return out, {"x": x, "z": z, "a": a, "act": act, "cols": cols, "ax1": ax1, "ax2": ax2}
 
 
 def mlp_backward(e: Emul, dO, c, lw, lora, dims, grads, prefix, bitfit):
@@ -243,7 +255,8 @@ def mlp_backward(e: Emul, dO, c, lw, lora, dims, grads, prefix, bitfit):
     elif ad2 is not None:
         O._acc(grads, f"{prefix}w2.lora_b", np.zeros_like(ad2["b"]))
         O._acc(grads, f"{prefix}w2.lora_a", np.zeros_like(ad2["a"]))
-    dz = e.rd(da * (a > 0))
+    dz = e.rd(da * c["act"])
+    c["dO"], c["dz"] = dO, dz  # diagnostics (tools/debug_bitfit.py)
     if bitfit:
         gb = np.zeros_like(lw["b1"])
         if cols.size:
@@ -263,9 +276,26 @@ def mlp_backward(e: Emul, dO, c, lw, lora, dims, grads, prefix, bitfit):
     return e.rd(dx)
 
 
-def adapter_forward(x, ad):
-    """sf/model.py:315-319 (fp32 on the device too)."""
-    return O.adapter_forward(x.astype(np.float32), ad)
+def adapter_forward(e: Emul, x, ad, key=None):
+    """sf/model.py:315-319 (fp32 on the device too), ReLU decisions optionally teacher-forced."""
+    x = x.astype(np.float32)
+    z = e.mm(x, ad["w_down"]) + ad["b_down"]
+    act = z > 0
+    forced = e.relu.get(key)
+    if forced is not None:
+        act = np.asarray(forced, bool)
+    h = np.where(act, z, 0).astype(np.float32)
+    return x + e.mm(h, ad["w_up"]) + ad["b_up"], {"x": x, "z": z, "h": h, "act": act}
+
+
+def adapter_backward(e: Emul, dy, ad, c, grads, prefix):
+    """sf/autograd.py:69-75 (fp32)."""
+    O._acc(grads, f"{prefix}.w_up", e.mm(c["h"].T, dy))
+    O._acc(grads, f"{prefix}.b_up", dy.astype(np.float64).sum(0).astype(np.float32))
+    dh = e.mm(dy, ad["w_up"].T) * c["act"]
+    O._acc(grads, f"{prefix}.w_down", e.mm(c["x"].T, dh))
+    O._acc(grads, f"{prefix}.b_down", dh.astype(np.float64).sum(0).astype(np.float32))
+    return dy + e.mm(dh, ad["w_down"].T)
 
 
 def model_forward(e: Emul, m: O.OModel, tokens, masks):
@@ -281,13 +311,13 @@ def model_forward(e: Emul, m: O.OModel, tokens, masks):
         att, ca = mha_forward(e, h1, lw, lora, pats, m.pool, m.dims)
         caa = None
         if adapter:
-            att, caa = adapter_forward(att, m.adapters[(i, "attn")])
+            att, caa = adapter_forward(e, att, m.adapters[(i, "attn")], (i, "attn_ad"))
         y = h + att
         h2, c2 = _ln_fwd(e, y, lw["ln2_g"], lw["ln2_b"])
-        mo, cm = mlp_forward(e, h2, lw, lora, nm, m.dims, out_f32=adapter)
+        mo, cm = mlp_forward(e, h2, lw, lora, nm, m.dims, out_f32=adapter, layer=i)
         cma = None
         if adapter:
-            mo, cma = adapter_forward(mo, m.adapters[(i, "mlp")])
+            mo, cma = adapter_forward(e, mo, m.adapters[(i, "mlp")], (i, "mlp_ad"))
         h = y + mo
         caches.append({"ln1": c1, "attn": ca, "attn_ad": caa, "ln2": c2, "mlp": cm, "mlp_ad": cma})
     hf, cf = _ln_fwd(e, h, m.lnf_g, m.lnf_b)
@@ -304,12 +334,12 @@ def model_backward(e: Emul, m: O.OModel, cache, d_logits):
         c, lw, lora, prefix = cache["blocks"][i], m.layers[i], O._layer_lora(m, i), f"layers.{i}."
         dm = dh
         if adapter:
-            dm = O.adapter_backward(dh, m.adapters[(i, "mlp")], c["mlp_ad"], grads, f"{prefix}mlp_adapter")
+            dm = adapter_backward(e, dh, m.adapters[(i, "mlp")], c["mlp_ad"], grads, f"{prefix}mlp_adapter")
         dh2 = mlp_backward(e, e.rd(dm), c["mlp"], lw, lora, m.dims, grads, prefix, bitfit)
         dy = dh + O.layernorm_backward(dh2, c["ln2"])
         da = dy
         if adapter:
-            da = O.adapter_backward(dy, m.adapters[(i, "attn")], c["attn_ad"], grads, f"{prefix}attn_adapter")
+            da = adapter_backward(e, dy, m.adapters[(i, "attn")], c["attn_ad"], grads, f"{prefix}attn_adapter")
         dh1 = mha_backward(e, e.rd(da), c["attn"], lw, lora, m.dims, grads, prefix, bitfit)
         dh = dy + O.layernorm_backward(dh1, c["ln1"])
     for name, p in O.trainable_params(m).items():

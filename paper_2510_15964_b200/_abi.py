@@ -45,13 +45,9 @@ SIGNATURES: dict[str, list] = {
     "lx_pack_params": [_P, _I, _P],
     "lx_colgrad_group_ws_floats": [_P, _I, _I, _I],
     "lx_colgrad_group": [_P, _I, _I, _I, _P, _P],
-    "lx_attn_tables_size": [_I, _I, _I, _P],
-    "lx_attn_tables": [_P, _P, _I, _I, _I, _P, _I],
-    "lx_bsattn_fwd": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _I, _P, _P],
-    "lx_bsattn_fwd_tc": [_P, _I, _I, _I, _I, _I, _P, _I, _P, _F, _P, _I, _P, _P],
+    "lx_bsattn_fwd_tc": [_P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _I, _P, _P],
+    "lx_bsattn_bwd_tc": [_P, _I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P],
     "lx_debug_set_attn_trace": [_P],
-    "lx_bsattn_bwd_tc": [_P, _I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _F, _P, _P, _P, _P, _P],
-    "lx_bsattn_bwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P, _P],
     "lx_layernorm_fwd": [_P, _P, _P, _I, _I, _P, _P, _F, _P, _I, _P, _P, _I, _I, _P, _P],
     "lx_cross_entropy": [_P, _I, _I, _P, _F, _P, _P, _P],
     "lx_adam_step": [_P, _P, _P, _P, _LL, _D, _D, _D, _D, _I, _P],
@@ -106,7 +102,7 @@ def lib() -> C.CDLL:
     return _lib
 
 
-_NON_STATUS = ("lx_abi_version", "lx_device_sm_count", "lx_attn_tables_size", "lx_gemm_set_cta_pair", "lx_exact_mass_smem")
+_NON_STATUS = ("lx_abi_version", "lx_device_sm_count", "lx_gemm_set_cta_pair", "lx_exact_mass_smem")
 
 
 # Kernel-time probe (bench.py's roofline): when a dict {symbol: list}, every call of a listed symbol is

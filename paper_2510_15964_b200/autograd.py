@@ -59,6 +59,9 @@ class FlatGrads(dict):
         self.views, self.scale = views, scale
 
 
+# diagnostics (tools/): when a dict, mlp_backward records its bf16 dO and dz under "<prefix>dO" / "<prefix>dz"
+DEBUG_TAPS: dict | None = None
+
 CG_LAYERS = 2  # layers whose LoRA / BitFit column reductions share one lx_colgrad_group launch (4: no gain)
 
 
@@ -181,6 +184,8 @@ def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims
     _abi.call("lx_neuron_fc2_dgrad", dO.data_ptr(), B, s, d, f, blk, lw.mlp.w2.data_ptr(), nm.counts.data_ptr(),
               nm.ids.data_ptr(), _abi.ptr(dax2), _abi.ptr(ad2.a if ad2 else None), ad2.rank if ad2 else 0, a.data_ptr(),
               dz.data_ptr(), a.stride(0), _abi.ptr(cache.get("w2p")), st)
+    if DEBUG_TAPS is not None:
+        DEBUG_TAPS[f"{prefix}dO"], DEBUG_TAPS[f"{prefix}dz"] = dO, dz
     if ad2 is not None:
         cg.add(f"{prefix}w2.lora_a", (f, ad2.rank), dax2, a, f, ad2.rank, 1.0, 1, ad2.rank, masks=nm, blk=blk)
     if bitfit:

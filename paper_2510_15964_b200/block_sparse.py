@@ -1,9 +1,17 @@
 """Block-sparse attention on the B200 (drop-in for sf/block_sparse.py).
 
 Hot path: `attention_forward` / `attention_backward` run the fused
-SDD -> sparse softmax -> DSD chain (and its backward) in csrc/attn.cu, walking
-each (item, head)'s pool pattern through the precomputed tile tables; the
-probabilities are never materialised (the cache holds O and the row LSE).
+SDD -> sparse softmax -> DSD chain (and its backward) in the tcgen05 kernels of
+csrc/attn_sm100.cu, walking each (item, head)'s pool pattern through the gathered
+128-tile tables (patterns.tables128_from_grids): only the active blocks' keys
+(forward, dQ) or queries (dK/dV) are loaded and multiplied. The probabilities
+are never materialised (the cache holds O and the row LSE).
+
+There is one implementation. The kernels take the fused projection output
+([M, 3d], q | k | v column blocks) at head_dim 64 or 128; other operands (separate
+q/k/v, other head dims) are staged into that layout with the head dimension
+zero-padded to 64 / 128 -- zero columns change neither QK^T nor the used part of
+P.V -- and the explicit `scale` keeps 1/sqrt(hd) of the true head dim.
 
 The reference's materialising operators (`sdd`, `sparse_softmax`, `dsd` and
 their backward, over `BlockSparseMatrix`) are kept with the same signatures
@@ -19,72 +27,92 @@ import numpy as np
 import torch
 
 from . import _abi
-from .errors import LayoutError
+from .errors import LayoutError, UnsupportedError
 from .patterns import DevicePool
 
 Coord = tuple[int, int]
-
-# tcgen05 kernels for hd in {64, 128} on the fused QKV layout; the warp-MMA kernels cover the rest
-USE_TCGEN05 = True
 
 
 # ---------------------------------------------------------------- fused hot path
 
 
+def _padded_hd(hd: int) -> int:
+    if hd <= 64:
+        return 64
+    if hd <= 128:
+        return 128
+    raise UnsupportedError(f"head_dim {hd} > 128 unsupported by the tcgen05 attention kernels")
+
+
+def _is_fused(q, k, v, ld: int, d: int) -> bool:
+    return ld == 3 * d and k.data_ptr() == q.data_ptr() + 2 * d and v.data_ptr() == q.data_ptr() + 4 * d
+
+
+def _stage(ts, M: int, H: int, hd: int, hdp: int) -> torch.Tensor:
+    """[M, len(ts) * H * hdp] bf16 with tensor t's head h at block t, columns h*hdp .. h*hdp + hd (rest 0)."""
+    out = torch.zeros(M, len(ts), H, hdp, dtype=torch.bfloat16, device=ts[0].device)
+    for i, t in enumerate(ts):
+        out[:, i, :, :hd] = t[:M, : H * hd].reshape(M, H, hd)
+    return out.view(M, len(ts) * H * hdp)
+
+
+def _check_tables(dpool: DevicePool, s: int):
+    if dpool.tables is None or dpool.seq_len != s:
+        raise LayoutError(f"device pool tables were built for seq_len {dpool.seq_len}, not {s}")
+
+
 def attention_forward(q, k, v, ld: int, n_items: int, s: int, H: int, hd: int, pidx: torch.Tensor, item_stride: int,
                       dpool: DevicePool, scale: float, out: torch.Tensor | None = None):
     """Non-causal block-sparse attention for all (item, head): returns (O bf16 [n_items*s, H*hd], lse fp32 [n_items, H, s])."""
-    if dpool.tables is None or dpool.seq_len != s:
-        raise LayoutError(f"device pool tables were built for seq_len {dpool.seq_len}, not {s}")
+    _check_tables(dpool, s)
     dev = q.device
-    o = out if out is not None else torch.empty(n_items * s, H * hd, dtype=torch.bfloat16, device=dev)
+    M, d = n_items * s, H * hd
+    o = out if out is not None else torch.empty(M, d, dtype=torch.bfloat16, device=dev)
     lse = torch.empty(n_items, H, s, dtype=torch.float32, device=dev)
-    d = H * hd
-    fused = (ld == 3 * d and k.data_ptr() == q.data_ptr() + 2 * d and v.data_ptr() == q.data_ptr() + 4 * d)
-    if fused and hd in (64, 128) and dpool.tables128 is not None and USE_TCGEN05:
-        # tcgen05 flash kernel over 128x128 tiles (csrc/attn_sm100.cu)
+    if _is_fused(q, k, v, ld, d) and hd in (64, 128):
         _abi.call("lx_bsattn_fwd_tc", q.data_ptr(), ld, n_items, s, H, hd, pidx.data_ptr(), item_stride,
-                  dpool.tables128.data_ptr(), float(scale), o.data_ptr(), o.stride(0), lse.data_ptr(),
+                  dpool.tables.data_ptr(), dpool.gather_rows, float(scale), o.data_ptr(), o.stride(0), lse.data_ptr(),
                   _abi.stream_handle(dev))
         return o, lse
-    _abi.call("lx_bsattn_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), ld, n_items, s, H, hd, pidx.data_ptr(), item_stride,
-              dpool.tables.data_ptr(), len(dpool.ids), float(scale), o.data_ptr(), o.stride(0), lse.data_ptr(),
+    hdp = _padded_hd(hd)
+    qkv = _stage([q, k, v], M, H, hd, hdp)
+    op = torch.empty(M, H * hdp, dtype=torch.bfloat16, device=dev)
+    _abi.call("lx_bsattn_fwd_tc", qkv.data_ptr(), qkv.stride(0), n_items, s, H, hdp, pidx.data_ptr(), item_stride,
+              dpool.tables.data_ptr(), dpool.gather_rows, float(scale), op.data_ptr(), op.stride(0), lse.data_ptr(),
               _abi.stream_handle(dev))
+    o.view(M, H, hd).copy_(op.view(M, H, hdp)[:, :, :hd])
     return o, lse
 
 
 def attention_backward(q, k, v, o, d_o, ld: int, n_items: int, s: int, H: int, hd: int, pidx, item_stride: int,
                        dpool: DevicePool, scale: float, lse, dq, dk, dv):
-    """dq/dk/dv (bf16, same layout/stride `ld` as q) of the fused forward; deterministic."""
+    """dq/dk/dv (bf16) of the fused forward; deterministic (fixed accumulation order)."""
+    _check_tables(dpool, s)
     dev = q.device
+    M, d = n_items * s, H * hd
     delta = torch.empty(n_items, H, s, dtype=torch.float32, device=dev)
     if d_o.stride(0) != o.stride(0):
         raise LayoutError("attention_backward expects o and d_o with the same row stride")
-    d = H * hd
-    fused = (ld == 3 * d and k.data_ptr() == q.data_ptr() + 2 * d and v.data_ptr() == q.data_ptr() + 4 * d
-             and dk.data_ptr() == dq.data_ptr() + 2 * d and dv.data_ptr() == dq.data_ptr() + 4 * d
-             and dk.stride(0) == dq.stride(0) == dv.stride(0) >= 3 * d)
-    if fused and hd in (64, 128) and dpool.tables128 is not None and USE_TCGEN05:
-        # tcgen05 dK/dV (CSC walk) + dQ (CSR walk) over 128x128 tiles (csrc/attn_sm100.cu); dqkv may be the
-        # K-extended [M, 3d + kx] operand of the projection input-grad GEMM (row stride dq.stride(0))
+    fused = (_is_fused(q, k, v, ld, d) and hd in (64, 128) and dk.data_ptr() == dq.data_ptr() + 2 * d
+             and dv.data_ptr() == dq.data_ptr() + 4 * d and dk.stride(0) == dq.stride(0) == dv.stride(0) >= 3 * d)
+    if fused:
+        # dqkv may be the K-extended [M, 3d + kx] operand of the projection input-grad GEMM (row stride dq.stride(0))
         ksum = torch.empty(n_items, H, (s + 127) // 128, hd, dtype=torch.float32, device=dev)
-        _abi.call("lx_bsattn_bwd_tc", q.data_ptr(), ld, dq.stride(0), o.data_ptr(), d_o.data_ptr(), o.stride(0), n_items, s, H, hd,
-                  pidx.data_ptr(), item_stride, dpool.tables128.data_ptr(), float(scale), lse.data_ptr(),
+        _abi.call("lx_bsattn_bwd_tc", q.data_ptr(), ld, dq.stride(0), o.data_ptr(), d_o.data_ptr(), o.stride(0), n_items, s, H,
+                  hd, pidx.data_ptr(), item_stride, dpool.tables.data_ptr(), dpool.gather_rows, float(scale), lse.data_ptr(),
                   delta.data_ptr(), ksum.data_ptr(), dq.data_ptr(), _abi.stream_handle(dev))
         return
-    if dq.stride(0) != ld or dk.stride(0) != ld or dv.stride(0) != ld:
-        # the warp-MMA kernels write dq/dk/dv with q's row stride: stage them (e.g. head_dim 32 under the
-        # K-extended projection operand, whose row stride is 3d + kx)
-        st = [torch.empty(dq.shape[0], ld, dtype=dq.dtype, device=dev) for _ in range(3)]
-        attention_backward(q, k, v, o, d_o, ld, n_items, s, H, hd, pidx, item_stride, dpool, scale, lse,
-                           st[0][:, :d], st[1][:, :d], st[2][:, :d])
-        for dst, src in zip((dq, dk, dv), st):
-            dst.copy_(src[:, :d])
-        return
-    _abi.call("lx_bsattn_bwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), d_o.data_ptr(), ld, o.stride(0),
-              n_items, s, H, hd,
-              pidx.data_ptr(), item_stride, dpool.tables.data_ptr(), len(dpool.ids), float(scale), lse.data_ptr(),
-              delta.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), _abi.stream_handle(dev))
+    hdp = _padded_hd(hd)
+    qkv = _stage([q, k, v], M, H, hd, hdp)
+    od = _stage([o, d_o], M, H, hd, hdp)
+    dqkv = torch.empty(M, 3 * H * hdp, dtype=torch.bfloat16, device=dev)
+    ksum = torch.empty(n_items, H, (s + 127) // 128, hdp, dtype=torch.float32, device=dev)
+    _abi.call("lx_bsattn_bwd_tc", qkv.data_ptr(), qkv.stride(0), dqkv.stride(0), od.data_ptr(), od[:, H * hdp :].data_ptr(),
+              od.stride(0), n_items, s, H, hdp, pidx.data_ptr(), item_stride, dpool.tables.data_ptr(), dpool.gather_rows,
+              float(scale), lse.data_ptr(), delta.data_ptr(), ksum.data_ptr(), dqkv.data_ptr(), _abi.stream_handle(dev))
+    g = dqkv.view(M, 3, H, hdp)
+    for i, dst in enumerate((dq, dk, dv)):
+        dst[:M, :d].view(M, H, hd).copy_(g[:, i, :, :hd])
 
 
 # ---------------------------------------------------------------- reference-API operators

@@ -37,26 +37,36 @@ LX_DEV void trace_stamp(int slot) {
   }
 }
 
-// 128x128 tile tables (built by patterns.tables_from_grids(tile=128)): per pattern
-// row_ptr[nt+1] csr_col[nt2] csr_lo[nt2] csr_hi[nt2] col_ptr[nt+1] csc_row[nt2] csc_lo[nt2] csc_hi[nt2]
+// Gathered 128-tile tables (patterns.tables128_from_grids): header [nt, P, s, attn_blk, gu, nsub, per, 0];
+// per pattern row_ptr[nt+1] col_ptr[nt+1] csr[nt*nt][10] csc[nt*nt][10]. A CSR entry of query tile i is one
+// gathered key tile: nsub = 128 / gu units of gu consecutive keys (entry[2 + k] = unit id of slot k, padding
+// repeats the first unit), entry[0..1] the 64-bit mask of active 16x16 cells (bit a*8 + b, a = query cell
+// of the tile, b = key cell of the gathered tile). CSC entries gather query units for a key tile the same
+// way (a = gathered query cell, b = key cell). Work per tile list is ceil(active units / nsub) MMA tiles.
+constexpr int kEntryInts = 10;
 struct Tab128 {
-  const int32_t *row_ptr, *csr_col, *csr_lo, *csr_hi, *col_ptr, *csc_row, *csc_lo, *csc_hi;
+  const int32_t *row_ptr, *col_ptr, *csr, *csc;
 };
 LX_DEV Tab128 tab128(const int32_t* t, int p) {
-  const int nt = t[0];
-  const int per = 2 * (nt + 1) + 6 * nt * nt;
-  const int32_t* b = t + 4 + (size_t)p * per;
+  const int nt = t[0], per = t[6];
+  const int32_t* b = t + 8 + (size_t)p * per;
   Tab128 v;
   v.row_ptr = b;
-  v.csr_col = b + nt + 1;
-  v.csr_lo = v.csr_col + nt * nt;
-  v.csr_hi = v.csr_lo + nt * nt;
-  v.col_ptr = v.csr_hi + nt * nt;
-  v.csc_row = v.col_ptr + nt + 1;
-  v.csc_lo = v.csc_row + nt * nt;
-  v.csc_hi = v.csc_lo + nt * nt;
+  v.col_ptr = b + nt + 1;
+  v.csr = v.col_ptr + nt + 1;
+  v.csc = v.csr + kEntryInts * nt * nt;
   return v;
 }
+LX_DEV uint64_t ent_mask(const int32_t* e) {
+  return ((uint64_t)(uint32_t)__ldg(e + 1) << 32) | (uint32_t)__ldg(e);
+}
+// one gathered 128-row tile of one 64-column atom: nsub TMA boxes of gu rows (tm's box height is gu)
+LX_DEV void tma_load_gather(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, int col, int row_base, const int32_t* ent,
+                            int gu, int nsub) {
+  for (int k = 0; k < nsub; ++k) tma_load_2d(dst + k * gu * 128, tm, bar, col, row_base + __ldg(ent + 2 + k) * gu);
+}
+// token row of row r of a gathered tile
+LX_DEV int gathered_row(const int32_t* ent, int r, int gu) { return __ldg(ent + 2 + r / gu) * gu + r % gu; }
 
 LX_DEV void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
@@ -125,7 +135,8 @@ LX_DEV void decode_unit(int u, int nqt, int H, int& qt, int& h, int& item) {
 
 template <int HD>
 __global__ void __launch_bounds__(AttnFwdSmem<HD>::kThreads, AttnFwdSmem<HD>::kCtas)
-bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, int d_model,
+bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_g, int gu, int s,
+                     int H, int d_model,
                      const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                      float scale_log2, __nv_bfloat16* __restrict__ o, int ldo, float* __restrict__ lse, int n_units) {
   pdl_wait_trigger();
@@ -153,6 +164,7 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
   if (warp == 0 && lane == 0) {
     trace_stamp(0);
     tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_g);
     for (int i = 0; i < 2; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
@@ -177,6 +189,7 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
 
   if (warp == 0) {
     if (lane == 0) {
+      const int nsub = kAT / gu;
       int g = 0, ul = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         int qt, h, item;
@@ -193,15 +206,15 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
           tma_load_2d(sm + L::kOffQ + qb * L::kT + a * kAT * 128, &tm_qkv, q_full + qb, qcol + a * 64, row_base + qt * kAT);
         for (int e = 0; e < n; ++e, ++g) {
           const int st = g & 1;
-          const int j = __ldg(tv.csr_col + e0 + e);
+          const int32_t* ent = tv.csr + (size_t)(e0 + e) * kEntryInts;
           uint8_t* sk = sm + L::kOffK + st * L::kT;
           uint8_t* sv = sm + L::kOffV + st * L::kT;
           mbar_wait(k_empty + st, ((g >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(k_full + st, L::kT);
-          for (int a = 0; a < A; ++a) tma_load_2d(sk + a * kAT * 128, &tm_qkv, k_full + st, kcol + a * 64, row_base + j * kAT);
+          for (int a = 0; a < A; ++a) tma_load_gather(sk + a * kAT * 128, &tm_g, k_full + st, kcol + a * 64, row_base, ent, gu, nsub);
           mbar_wait(v_empty + st, ((g >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(v_full + st, L::kT);
-          for (int a = 0; a < A; ++a) tma_load_2d(sv + a * kAT * 128, &tm_qkv, v_full + st, vcol + a * 64, row_base + j * kAT);
+          for (int a = 0; a < A; ++a) tma_load_gather(sv + a * kAT * 128, &tm_g, v_full + st, vcol + a * 64, row_base, ent, gu, nsub);
         }
         ++ul;
       }
@@ -272,7 +285,8 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
       const int row_base = item * s;
       float m = -INFINITY, l = 0.f;  // running max (log2 domain, scaled) and this half's row sum
       for (int e = 0; e < n; ++e, ++g) {
-        const uint32_t lo = (uint32_t)__ldg(tv.csr_lo + e0 + e), hi = (uint32_t)__ldg(tv.csr_hi + e0 + e);
+        const int32_t* ent = tv.csr + (size_t)(e0 + e) * kEntryInts;
+        const uint32_t lo = (uint32_t)__ldg(ent), hi = (uint32_t)__ldg(ent + 1);
         // 16-key groups 4*half .. 4*half+3 of this row's 16-row group
         const uint32_t mrow = (uint32_t)((((uint64_t)hi << 32) | lo) >> ((r >> 4) * 8 + 4 * half)) & 0xfu;
         const bool full = __all_sync(0xffffffffu, mrow == 0xfu);
@@ -394,16 +408,17 @@ bsattn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int s, int H, i
 
 template <int HD>
 static int launch_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H, const int32_t* pidx, int item_stride,
-                         const int32_t* tables128, float scale, uint16_t* o, int ldo, float* lse, cudaStream_t st) {
-  CUtensorMap tm;
+                         const int32_t* tables128, int gu, float scale, uint16_t* o, int ldo, float* lse, cudaStream_t st) {
+  CUtensorMap tm, tm_g;
   int rc = make_tmap_bf16_2d(&tm, qkv, ld, (uint64_t)n_items * s, ld, 64, kAT);
   if (rc) return rc;
+  if ((rc = make_tmap_bf16_2d(&tm_g, qkv, ld, (uint64_t)n_items * s, ld, 64, gu))) return rc;
   constexpr int smem = AttnFwdSmem<HD>::kTotal;
   static cudaError_t attr = cudaFuncSetAttribute(bsattn_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   LX_CHECK_CUDA(attr);
   const int n_units = ((s + kAT - 1) / kAT) * H * n_items;
   const int grid = n_units < AttnFwdSmem<HD>::kCtas * num_sms() ? n_units : AttnFwdSmem<HD>::kCtas * num_sms();
-  launch_k(bsattn_fwd_tc_kernel<HD>, grid, AttnFwdSmem<HD>::kThreads, smem, st, tm, s, H, H * HD, pidx, item_stride, tables128,
+  launch_k(bsattn_fwd_tc_kernel<HD>, grid, AttnFwdSmem<HD>::kThreads, smem, st, tm, tm_g, gu, s, H, H * HD, pidx, item_stride, tables128,
                                                     scale * 1.4426950408889634f, reinterpret_cast<__nv_bfloat16*>(o), ldo,
                                                     lse, n_units);
   return launch_check("bsattn_fwd_tc");
@@ -427,7 +442,8 @@ struct AttnBwdSmem {
 
 template <int HD>
 __global__ void __launch_bounds__(192, AttnBwdSmem<HD>::kCtas)
-bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, int s, int H,
+bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                      const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_do_g, int gu, int s, int H,
                       int d_model, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                       float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
                       __nv_bfloat16* __restrict__ dkv, int ld_dkv, float* __restrict__ ksum) {
@@ -460,6 +476,8 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
     tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_g);
+    tma_prefetch_desc(&tm_do_g);
     mbar_init(kv_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(qd_full + i, 33);
@@ -490,23 +508,24 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
         tma_load_2d(sm + L::kT + a * kAT * 128, &tm_qkv, kv_full, vcol + a * 64, row_base + kt * kAT);
       }
     }
+    const int nsub = kAT / gu;
     for (int e = 0; e < n; ++e) {
       const int st = e % L::kSt;
       mbar_wait(qd_empty + st, ((e / L::kSt) & 1) ^ 1);
-      const int i = __ldg(tv.csc_row + e0 + e);
+      const int32_t* ent = tv.csc + (size_t)(e0 + e) * kEntryInts;
       if (lane == 0) {
         uint8_t* sq = sm + L::kOffRing + st * 2 * L::kT;
         mbar_arrive_expect_tx(qd_full + st, 2 * L::kT);
         for (int a = 0; a < A; ++a) {
-          tma_load_2d(sq + a * kAT * 128, &tm_qkv, qd_full + st, qcol + a * 64, row_base + i * kAT);
-          tma_load_2d(sq + L::kT + a * kAT * 128, &tm_do, qd_full + st, h * HD + a * 64, row_base + i * kAT);
+          tma_load_gather(sq + a * kAT * 128, &tm_g, qd_full + st, qcol + a * 64, row_base, ent, gu, nsub);
+          tma_load_gather(sq + L::kT + a * kAT * 128, &tm_do_g, qd_full + st, h * HD + a * 64, row_base, ent, gu, nsub);
         }
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int qi = lane * 4 + k, q = i * kAT + qi;
-        sL[st * kAT + qi] = q < s ? __ldg(lse_b + q) * 1.4426950408889634f : INFINITY;
-        sD[st * kAT + qi] = q < s ? __ldg(del_b + q) : 0.f;
+        const int qi = lane * 4 + k, q = gathered_row(ent, qi, gu);  // gathered query units lie inside the item
+        sL[st * kAT + qi] = __ldg(lse_b + q) * 1.4426950408889634f;
+        sD[st * kAT + qi] = __ldg(del_b + q);
       }
       mbar_arrive(qd_full + st);
     }
@@ -545,7 +564,8 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
     const int cj = kr >> 4;
     for (int e = 0; e < n; ++e) {
       const int st = e % L::kSt;
-      const uint32_t lo = (uint32_t)__ldg(tv.csc_lo + e0 + e), hi = (uint32_t)__ldg(tv.csc_hi + e0 + e);
+      const int32_t* ent = tv.csc + (size_t)(e0 + e) * kEntryInts;
+        const uint32_t lo = (uint32_t)__ldg(ent), hi = (uint32_t)__ldg(ent + 1);
       const uint64_t mask = ((uint64_t)hi << 32) | lo;
       const float* l2 = sL + st * kAT;
       const float* dl = sD + st * kAT;
@@ -660,7 +680,8 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
 
 template <int HD>
 __global__ void __launch_bounds__(192, AttnBwdSmem<HD>::kCtas)
-bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, int s, int H,
+bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                    const __grid_constant__ CUtensorMap tm_g, int gu, int s, int H,
                     int d_model, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                     float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
                     __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ ksum) {
@@ -691,6 +712,7 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
     tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_g);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(kv_full + i, 1);
@@ -718,15 +740,16 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
         tma_load_2d(sm + a * kAT * 128, &tm_qkv, q_full, qcol + a * 64, row_base + qt * kAT);
         tma_load_2d(sm + L::kT + a * kAT * 128, &tm_do, q_full, h * HD + a * 64, row_base + qt * kAT);
       }
+      const int nsub = kAT / gu;
       for (int e = 0; e < n; ++e) {
         const int st = e % L::kSt;
         mbar_wait(kv_empty + st, ((e / L::kSt) & 1) ^ 1);
-        const int j = __ldg(tv.csr_col + e0 + e);
+        const int32_t* ent = tv.csr + (size_t)(e0 + e) * kEntryInts;
         uint8_t* skv = sm + L::kOffRing + st * 2 * L::kT;
         mbar_arrive_expect_tx(kv_full + st, 2 * L::kT);
         for (int a = 0; a < A; ++a) {
-          tma_load_2d(skv + a * kAT * 128, &tm_qkv, kv_full + st, kcol + a * 64, row_base + j * kAT);
-          tma_load_2d(skv + L::kT + a * kAT * 128, &tm_qkv, kv_full + st, vcol + a * 64, row_base + j * kAT);
+          tma_load_gather(skv + a * kAT * 128, &tm_g, kv_full + st, kcol + a * 64, row_base, ent, gu, nsub);
+          tma_load_gather(skv + L::kT + a * kAT * 128, &tm_g, kv_full + st, vcol + a * 64, row_base, ent, gu, nsub);
         }
       }
     }
@@ -767,7 +790,8 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
     // the keys' common mode kbar is removed in the epilogue.
     float eps = 0.f;
     for (int e = 0; e < n; ++e) {
-      const uint32_t lo = (uint32_t)__ldg(tv.csr_lo + e0 + e), hi = (uint32_t)__ldg(tv.csr_hi + e0 + e);
+      const int32_t* ent = tv.csr + (size_t)(e0 + e) * kEntryInts;
+        const uint32_t lo = (uint32_t)__ldg(ent), hi = (uint32_t)__ldg(ent + 1);
       const uint32_t mrow = (uint32_t)((((uint64_t)hi << 32) | lo) >> (ci * 8)) & 0xffu;
       mbar_wait(s_full, e & 1);
       tc_fence_after();
@@ -923,7 +947,8 @@ struct AttnDkdvPP {
 
 template <int HD>
 __global__ void __launch_bounds__(kBwdThreads, 1)
-bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, int s, int H,
+bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                      const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_do_g, int gu, int s, int H,
                       int n_units, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                       float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
                       __nv_bfloat16* __restrict__ dkv, int ld_dkv, float* __restrict__ ksum) {
@@ -952,6 +977,8 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
     tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_g);
+    tma_prefetch_desc(&tm_do_g);
     for (int i = 0; i < L::kKV; ++i) {
       mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 2);
@@ -1010,23 +1037,24 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       }
       const float* lse_b = lse + ((size_t)item * H + h) * s;
       const float* del_b = delta + ((size_t)item * H + h) * s;
+      const int nsub = kAT / gu;
       for (int e = 0; e < n; ++e, ++g) {
         const int st = g % L::kSt;
         mbar_wait(qd_empty + st, ((g / L::kSt) & 1) ^ 1);
-        const int i = __ldg(tv.csc_row + e0 + e);
+        const int32_t* ent = tv.csc + (size_t)(e0 + e) * kEntryInts;
         if (lane == 0) {
           uint8_t* sq = sm + L::kOffRing + st * 2 * L::kT;
           mbar_arrive_expect_tx(qd_full + st, 2 * L::kT);
           for (int a = 0; a < A; ++a) {
-            tma_load_2d(sq + a * kAT * 128, &tm_qkv, qd_full + st, h * HD + a * 64, row_base + i * kAT);
-            tma_load_2d(sq + L::kT + a * kAT * 128, &tm_do, qd_full + st, h * HD + a * 64, row_base + i * kAT);
+            tma_load_gather(sq + a * kAT * 128, &tm_g, qd_full + st, h * HD + a * 64, row_base, ent, gu, nsub);
+            tma_load_gather(sq + L::kT + a * kAT * 128, &tm_do_g, qd_full + st, h * HD + a * 64, row_base, ent, gu, nsub);
           }
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const int qi = lane * 4 + k, q = i * kAT + qi;
-          sL[st * kAT + qi] = q < s ? __ldg(lse_b + q) * 1.4426950408889634f : INFINITY;
-          sD[st * kAT + qi] = q < s ? __ldg(del_b + q) : 0.f;
+          const int qi = lane * 4 + k, q = gathered_row(ent, qi, gu);  // gathered query units lie inside the item
+          sL[st * kAT + qi] = __ldg(lse_b + q) * 1.4426950408889634f;
+          sD[st * kAT + qi] = __ldg(del_b + q);
         }
         mbar_arrive(qd_full + st);
       }
@@ -1134,7 +1162,8 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       const int row_base = item * s;
       for (int e = wg; e < n; e += 2, ++use) {
         const int gg = g + e, st = gg % L::kSt;
-        const uint32_t lo = (uint32_t)__ldg(tv.csc_lo + e0 + e), hi = (uint32_t)__ldg(tv.csc_hi + e0 + e);
+        const int32_t* ent = tv.csc + (size_t)(e0 + e) * kEntryInts;
+        const uint32_t lo = (uint32_t)__ldg(ent), hi = (uint32_t)__ldg(ent + 1);
         const uint64_t mask = ((uint64_t)hi << 32) | lo;
         const bool full = mask == ~0ull;
         const float* l2 = sL + st * kAT;
@@ -1277,7 +1306,8 @@ struct AttnDqPP {
 
 template <int HD>
 __global__ void __launch_bounds__(kBwdThreads, 1)
-bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, int s, int H,
+bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                    const __grid_constant__ CUtensorMap tm_g, int gu, int s, int H,
                     int n_units, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                     float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
                     __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ ksum) {
@@ -1306,6 +1336,7 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
     tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_g);
     for (int i = 0; i < L::kQB; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
@@ -1361,13 +1392,13 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
         for (int e = 0; e < n; ++e, ++g) {
           const int st = g % L::kSt;
           mbar_wait(kv_empty + st, ((g / L::kSt) & 1) ^ 1);
-          const int j = __ldg(tv.csr_col + e0 + e);
+          const int32_t* ent = tv.csr + (size_t)(e0 + e) * kEntryInts;
           uint8_t* skv = sm + L::kOffRing + st * 2 * L::kT;
           mbar_arrive_expect_tx(kv_full + st, 2 * L::kT);
           for (int a = 0; a < A; ++a) {
-            tma_load_2d(skv + a * kAT * 128, &tm_qkv, kv_full + st, d_model + h * HD + a * 64, row_base + j * kAT);
-            tma_load_2d(skv + L::kT + a * kAT * 128, &tm_qkv, kv_full + st, 2 * d_model + h * HD + a * 64,
-                        row_base + j * kAT);
+            tma_load_gather(skv + a * kAT * 128, &tm_g, kv_full + st, d_model + h * HD + a * 64, row_base, ent, gu, kAT / gu);
+            tma_load_gather(skv + L::kT + a * kAT * 128, &tm_g, kv_full + st, 2 * d_model + h * HD + a * 64, row_base, ent,
+                            gu, kAT / gu);
           }
         }
       }
@@ -1455,7 +1486,8 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
       const float l2 = __ldg(lse + lrow) * 1.4426950408889634f, dl = __ldg(delta + lrow);
       float eps = 0.f;
       for (int e = wg; e < n; e += 2, ++use) {
-        const uint32_t lo = (uint32_t)__ldg(tv.csr_lo + e0 + e), hi = (uint32_t)__ldg(tv.csr_hi + e0 + e);
+        const int32_t* ent = tv.csr + (size_t)(e0 + e) * kEntryInts;
+        const uint32_t lo = (uint32_t)__ldg(ent), hi = (uint32_t)__ldg(ent + 1);
         const uint32_t mrow = (uint32_t)((((uint64_t)hi << 32) | lo) >> (ci * 8)) & 0xffu;
         mbar_wait(s_full + wg, use & 1);
         tc_fence_after();
@@ -1563,7 +1595,7 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
 
 template <int HD>
 static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
-                         int H, const int32_t* pidx, int item_stride, const int32_t* tables128, float scale,
+                         int H, const int32_t* pidx, int item_stride, const int32_t* tables128, int gu, float scale,
                          const float* lse, float* delta, float* ksum, uint16_t* dqkv, cudaStream_t st) {
   const int rows = n_items * s;
   LX_REQUIRE(ld_o % 8 == 0, LX_ERR_SHAPE, "attention bwd: O / dO row stride must be a multiple of 8");
@@ -1572,9 +1604,11 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
                                                                       rows, s, H, delta);
   int rc = launch_check("bsattn_delta_tc");
   if (rc) return rc;
-  CUtensorMap tm_qkv, tm_do;
+  CUtensorMap tm_qkv, tm_do, tm_g, tm_do_g;
   if ((rc = make_tmap_bf16_2d(&tm_qkv, qkv, ld, (uint64_t)rows, ld, 64, kAT))) return rc;
   if ((rc = make_tmap_bf16_2d(&tm_do, d_o, ld_o, (uint64_t)rows, ld_o, 64, kAT))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tm_g, qkv, ld, (uint64_t)rows, ld, 64, gu))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tm_do_g, d_o, ld_o, (uint64_t)rows, ld_o, 64, gu))) return rc;
   constexpr int smem = AttnBwdSmem<HD>::kTotal;
   static cudaError_t a1 = cudaFuncSetAttribute(bsattn_dkdv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   static cudaError_t a2 = cudaFuncSetAttribute(bsattn_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1585,27 +1619,28 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
   // the ping-pong kernel's ring + staging fit in shared memory for HD 64; HD 128 keeps the 2-CTA kernel
   static const bool old_bwd = getenv("LX_ATTN_BWD_OLD") != nullptr || AttnDkdvPP<HD>::kTotal > 227 * 1024;
   if (old_bwd) {
-    launch_k(bsattn_dkdv_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
+    launch_k(bsattn_dkdv_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, tm_g, tm_do_g, gu, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
                                                      lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);
   } else {
     constexpr int smem_pp = AttnDkdvPP<HD>::kTotal;
     static cudaError_t a3 = cudaFuncSetAttribute(bsattn_dkdv_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pp);
     LX_CHECK_CUDA(a3);
     const int n_units = (int)grid.x * H * n_items;
-    launch_k(bsattn_dkdv_pp_kernel<HD>, std::min(n_units, num_sms()), kBwdThreads, smem_pp, st, tm_qkv, tm_do, s, H,
+    launch_k(bsattn_dkdv_pp_kernel<HD>, std::min(n_units, num_sms()), kBwdThreads, smem_pp, st, tm_qkv, tm_do, tm_g, tm_do_g,
+             gu, s, H,
              n_units, pidx, item_stride, tables128, scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d,
              ksum);
   }
   if ((rc = launch_check("bsattn_dkdv_tc"))) return rc;
   if (old_bwd || AttnDqPP<HD>::kTotal > 227 * 1024) {
-    launch_k(bsattn_dq_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
+    launch_k(bsattn_dq_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, tm_g, gu, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
                                                    lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);
   } else {
     constexpr int smem_dq = AttnDqPP<HD>::kTotal;
     static cudaError_t a4 = cudaFuncSetAttribute(bsattn_dq_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_dq);
     LX_CHECK_CUDA(a4);
     const int n_units = (int)grid.x * H * n_items;
-    launch_k(bsattn_dq_pp_kernel<HD>, std::min(n_units, num_sms()), kBwdThreads, smem_dq, st, tm_qkv, tm_do, s, H,
+    launch_k(bsattn_dq_pp_kernel<HD>, std::min(n_units, num_sms()), kBwdThreads, smem_dq, st, tm_qkv, tm_do, tm_g, gu, s, H,
              n_units, pidx, item_stride, tables128, scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d,
              ksum);
   }
@@ -1627,25 +1662,30 @@ int lx_debug_set_attn_trace(unsigned long long* buf) {
 
 int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items,
                      int s, int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128,
-                     float scale, const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv, lx_stream_t stream) {
+                     int gather_rows, float scale, const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv,
+                     lx_stream_t stream) {
+  LX_REQUIRE(gather_rows >= 16 && gather_rows <= 128 && (gather_rows & (gather_rows - 1)) == 0, LX_ERR_LAYOUT,
+             "attention bwd: gather_rows %d must be a power of two in [16, 128]", gather_rows);
   LX_REQUIRE(ld >= 3 * H * hd && ld_d >= 3 * H * hd && ld % 8 == 0 && ld_d % 8 == 0 && ld_o % 8 == 0, LX_ERR_SHAPE,
              "attention bwd (tcgen05): qkv / dqkv must be fused [M, >= 3*H*hd] with 16B-aligned rows");
   switch (hd) {
-    case 64: return launch_bwd_tc<64>(qkv, ld, ld_d, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, ksum_ws, dqkv, stream);
-    case 128: return launch_bwd_tc<128>(qkv, ld, ld_d, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, scale, lse, delta_ws, ksum_ws, dqkv, stream);
+    case 64: return launch_bwd_tc<64>(qkv, ld, ld_d, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, gather_rows, scale, lse, delta_ws, ksum_ws, dqkv, stream);
+    case 128: return launch_bwd_tc<128>(qkv, ld, ld_d, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, gather_rows, scale, lse, delta_ws, ksum_ws, dqkv, stream);
     default: LX_REQUIRE(false, LX_ERR_UNSUPPORTED, "tcgen05 attention: head_dim %d unsupported (64, 128)", hd);
   }
 }
 
 int lx_bsattn_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H, int hd, const int32_t* pattern_idx,
-                     int item_stride, const int32_t* tables128, float scale, uint16_t* o, int ldo, float* lse,
-                     lx_stream_t stream) {
+                     int item_stride, const int32_t* tables128, int gather_rows, float scale, uint16_t* o, int ldo,
+                     float* lse, lx_stream_t stream) {
+  LX_REQUIRE(gather_rows >= 16 && gather_rows <= 128 && (gather_rows & (gather_rows - 1)) == 0, LX_ERR_LAYOUT,
+             "attention: gather_rows %d must be a power of two in [16, 128]", gather_rows);
   LX_REQUIRE(ld % 8 == 0 && ldo % 8 == 0 && ld >= 3 * H * hd, LX_ERR_SHAPE,
              "attention (tcgen05): qkv must be the fused [M, >= 3*H*hd] projection output (16B-aligned rows)");
   LX_REQUIRE(n_items >= 1 && n_items < 65536 && H >= 1 && H < 65536, LX_ERR_SHAPE, "attention: bad grid");
   switch (hd) {
-    case 64: return launch_fwd_tc<64>(qkv, ld, n_items, s, H, pattern_idx, item_stride, tables128, scale, o, ldo, lse, stream);
-    case 128: return launch_fwd_tc<128>(qkv, ld, n_items, s, H, pattern_idx, item_stride, tables128, scale, o, ldo, lse, stream);
+    case 64: return launch_fwd_tc<64>(qkv, ld, n_items, s, H, pattern_idx, item_stride, tables128, gather_rows, scale, o, ldo, lse, stream);
+    case 128: return launch_fwd_tc<128>(qkv, ld, n_items, s, H, pattern_idx, item_stride, tables128, gather_rows, scale, o, ldo, lse, stream);
     default: LX_REQUIRE(false, LX_ERR_UNSUPPORTED, "tcgen05 attention: head_dim %d unsupported (64, 128)", hd);
   }
 }

@@ -11,6 +11,7 @@
 //     dL/dl = (w y (sigmoid(l) - 1) + (1 - y) sigmoid(l)) / (rows * n_blk)
 //   row_loss[t] = sum over the row in float64, fixed order (the caller sums rows in order).
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace lx {
 

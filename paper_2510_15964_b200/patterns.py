@@ -6,8 +6,10 @@ also lowered once to the two device forms the kernels consume:
 
 * ``kinds/params`` (int32) — analytic membership used by the predictor's
   coverage selection kernel (csrc/mask_build.cu);
-* attention tile tables (csrc/attn.cu) — per pattern, CSR over 64-row query
-  tiles and CSC over 64-key tiles with 16x16-cell masks.
+* gathered 128-tile attention tables (csrc/attn_sm100.cu, tables128_from_grids)
+  — per pattern, CSR over 128-query tiles and CSC over 128-key tiles whose
+  entries stack the active gather units (gcd(attn_blk, 128) tokens) with
+  64-bit masks of active 16x16 cells.
 
 Pattern ids, order (the tie-break), coordinates and errors match the
 reference exactly (pinned by tests/test_oracle_golden.py::test_pools_match_reference against tests/golden/pools.npz).
@@ -15,7 +17,7 @@ reference exactly (pinned by tests/test_oracle_golden.py::test_pools_match_refer
 
 from __future__ import annotations
 
-import ctypes
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -143,11 +145,19 @@ class DevicePool:
     ids: list[str]
     kinds: object  # torch int32 [P]
     params: object  # torch int32 [P]
-    tables: object | None  # torch int32 attention tile tables, 64x64 tiles (None until built for a seq_len)
+    tables: object | None  # torch int32 gathered 128-tile attention tables (tables128_from_grids), None until built
     seq_len: int = 0
     attn_blk: int = 0
     index: dict = field(default_factory=dict)
-    tables128: object | None = None  # 128x128-tile tables for the tcgen05 attention kernels
+
+    @property
+    def tables128(self):
+        return self.tables
+
+    @property
+    def gather_rows(self) -> int:
+        """Rows per gather unit of the attention tables: gcd(attn_blk, 128)."""
+        return math.gcd(self.attn_blk, 128)
 
     def idx(self, pid: str) -> int:
         if pid not in self.index:
@@ -155,58 +165,26 @@ class DevicePool:
         return self.index[pid]
 
 
-TILE = 64  # attention kernel tile edge (csrc/attn.cu kT)
-
-
-def tables_from_grids(grids: np.ndarray, seq_len: int, attn_blk: int) -> np.ndarray:
-    """Attention tile tables (csrc/attn.cu layout) for arbitrary block layouts: grids bool
-    [P, n_b, n_b] -> int32 array. Same format the C-ABI builds for pool kinds."""
-    from .errors import LayoutError, UnsupportedError
-
-    if attn_blk % 16 or attn_blk < 16:
-        raise UnsupportedError(f"attn_blk {attn_blk} unsupported on the sm_100a path (multiple of 16)")
-    if seq_len % attn_blk:
-        raise LayoutError(f"sequence length {seq_len} != n_b*blk")
-    P = grids.shape[0]
-    nt = -(-seq_len // TILE)
-    per = 2 * (nt + 1) + 4 * nt * nt
-    out = np.zeros(4 + P * per, np.int32)
-    out[:4] = (nt, P, seq_len, attn_blk)
-    nc = seq_len // 16
-    ci = np.arange(nc)
-    for p in range(P):
-        cells = grids[p][np.ix_(ci * 16 // attn_blk, ci * 16 // attn_blk)]  # [nc, nc] active 16x16 cells
-        tm = np.zeros((nt, nt), np.int64)
-        for a in range(nc):
-            for b in np.flatnonzero(cells[a]):
-                tm[a // 4, b // 4] |= 1 << ((a % 4) * 4 + b % 4)
-        base = 4 + p * per
-        row_ptr, csr_col, csr_mask = base, base + nt + 1, base + nt + 1 + nt * nt
-        col_ptr = csr_mask + nt * nt
-        csc_row, csc_mask = col_ptr + nt + 1, col_ptr + nt + 1 + nt * nt
-        n = 0
-        for i in range(nt):
-            out[row_ptr + i] = n
-            for j in np.flatnonzero(tm[i]):
-                out[csr_col + n], out[csr_mask + n] = j, tm[i, j]
-                n += 1
-        out[row_ptr + nt] = n
-        n = 0
-        for j in range(nt):
-            out[col_ptr + j] = n
-            for i in np.flatnonzero(tm[:, j]):
-                out[csc_row + n], out[csc_mask + n] = i, tm[i, j]
-                n += 1
-        out[col_ptr + nt] = n
-        if np.any(out[row_ptr + 1 : row_ptr + nt + 1] == out[row_ptr : row_ptr + nt]):
-            raise LayoutError("a block-row has no active blocks (pattern pool violation)")
-    return out
+GATHER_SLOTS = 8  # unit slots per gathered 128-row tile (128 / 16)
+ENTRY_INTS = 2 + GATHER_SLOTS  # lo, hi, unit ids
 
 
 def tables128_from_grids(grids: np.ndarray, seq_len: int, attn_blk: int) -> np.ndarray:
-    """128x128-tile tables for the tcgen05 attention kernels (csrc/attn_sm100.cu): per pattern
-    row_ptr, csr_col, csr_lo, csr_hi, col_ptr, csc_row, csc_lo, csc_hi; a tile's 64-bit mask has
-    bit (ci*8 + cj) set when its 16x16 cell (ci, cj) is active."""
+    """Gathered 128x128-tile tables for the tcgen05 attention kernels (csrc/attn_sm100.cu), so the work of a
+    tile list is proportional to the active blocks, not to the 128-tiles they touch.
+
+    A gather unit is gu = min(attn_blk, 128) consecutive tokens (one block, or a 128-token tile of a larger
+    block); a gathered tile is nsub = 128 / gu units stacked, loaded as nsub TMA boxes of gu rows.
+      CSR (forward, dQ): for query tile i (128 contiguous queries) the ascending union of the key units any
+        of its rows attends to, packed nsub per entry;
+      CSC (dK/dV): for key tile j (128 contiguous keys) the ascending union of the query units attending
+        to it, packed nsub per entry.
+    An entry is [lo, hi, u_0 .. u_7]: the 64-bit mask (bit a*8 + b) of active 16x16 cells, a the query cell
+    and b the key cell inside the (gathered) tile, and the unit ids of its slots. Unused slots repeat the
+    entry's first unit with no mask bit set (real, finite data; contributes nothing).
+
+    int32 layout: header [nt, P, seq_len, attn_blk, gu, nsub, per, 0]; per pattern p at 8 + p * per:
+    row_ptr[nt + 1], col_ptr[nt + 1], csr[nt * nt][10], csc[nt * nt][10]."""
     from .errors import LayoutError, UnsupportedError
 
     if attn_blk % 16 or attn_blk < 16:
@@ -214,40 +192,56 @@ def tables128_from_grids(grids: np.ndarray, seq_len: int, attn_blk: int) -> np.n
     if seq_len % attn_blk:
         raise LayoutError(f"sequence length {seq_len} != n_b*blk")
     T = 128
+    gu = math.gcd(attn_blk, T)  # largest power of two <= 128 dividing the block
+    nsub = T // gu
+    cpu = gu // 16  # 16-cells per unit
     P = grids.shape[0]
     nt = -(-seq_len // T)
-    per = 2 * (nt + 1) + 6 * nt * nt
-    out = np.zeros(4 + P * per, np.int64)
-    out[:4] = (nt, P, seq_len, attn_blk)
+    n_units = seq_len // gu
+    per = 2 * (nt + 1) + 2 * ENTRY_INTS * nt * nt
+    out = np.zeros(8 + P * per, np.int64)
+    out[:8] = (nt, P, seq_len, attn_blk, gu, nsub, per, 0)
     nc = seq_len // 16
     ci = np.arange(nc)
     for p in range(P):
-        cells = grids[p][np.ix_(ci * 16 // attn_blk, ci * 16 // attn_blk)]
-        tm = np.zeros((nt, nt), np.uint64)
-        a_idx, b_idx = np.nonzero(cells)
-        for a, b in zip(a_idx, b_idx):
-            tm[a // 8, b // 8] |= np.uint64(1) << np.uint64((a % 8) * 8 + b % 8)
-        base = 4 + p * per
-        rp, cc, clo, chi = base, base + nt + 1, base + nt + 1 + nt * nt, base + nt + 1 + 2 * nt * nt
-        cp = base + nt + 1 + 3 * nt * nt
-        cr, rlo, rhi = cp + nt + 1, cp + nt + 1 + nt * nt, cp + nt + 1 + 2 * nt * nt
-        n = 0
-        for i in range(nt):
-            out[rp + i] = n
-            for j in np.flatnonzero(tm[i]):
-                out[cc + n], out[clo + n], out[chi + n] = j, int(tm[i, j]) & 0xFFFFFFFF, int(tm[i, j]) >> 32
-                n += 1
-        out[rp + nt] = n
-        n = 0
-        for j in range(nt):
-            out[cp + j] = n
-            for i in np.flatnonzero(tm[:, j]):
-                out[cr + n], out[rlo + n], out[rhi + n] = i, int(tm[i, j]) & 0xFFFFFFFF, int(tm[i, j]) >> 32
-                n += 1
-        out[cp + nt] = n
-        if np.any(out[rp + 1 : rp + nt + 1] == out[rp : rp + nt]):
+        cells = grids[p][np.ix_(ci * 16 // attn_blk, ci * 16 // attn_blk)]  # [nc, nc] active 16x16 cells
+        cells_pad = np.zeros((nt * 8, nt * 8), bool)
+        cells_pad[:nc, :nc] = cells
+        base = 8 + p * per
+        rp, cp = base, base + nt + 1
+        csr0, csc0 = cp + nt + 1, cp + nt + 1 + ENTRY_INTS * nt * nt
+        if np.any(~cells.any(1)):
             raise LayoutError("a block-row has no active blocks (pattern pool violation)")
+        for transpose, ptr, ent0 in ((False, rp, csr0), (True, cp, csc0)):
+            cm = cells_pad.T if transpose else cells_pad  # rows: the tile side, cols: the gathered side
+            n = 0
+            for t in range(nt):
+                out[ptr + t] = n
+                rows = cm[t * 8 : (t + 1) * 8]  # [8 cells of the tile, nt*8 cells]
+                unit_act = rows[:, : n_units * cpu].reshape(8, n_units, cpu).any(axis=(0, 2))
+                units = np.flatnonzero(unit_act)
+                for c0 in range(0, len(units), nsub):
+                    grp = units[c0 : c0 + nsub]
+                    mask = 0
+                    for slot, u in enumerate(grp):
+                        sub = rows[:, u * cpu : (u + 1) * cpu]  # [8, cpu]
+                        for a, b in zip(*np.nonzero(sub)):
+                            qa, kb = (slot * cpu + b, a) if transpose else (a, slot * cpu + b)
+                            mask |= 1 << (qa * 8 + kb)
+                    e = ent0 + n * ENTRY_INTS
+                    out[e], out[e + 1] = mask & 0xFFFFFFFF, mask >> 32
+                    out[e + 2 : e + 2 + nsub] = np.concatenate([grp, np.full(nsub - len(grp), grp[0])])
+                    n += 1
+            out[ptr + nt] = n
     return out.astype(np.uint32).view(np.int32)
+
+
+def tables128_work(tables: np.ndarray, p: int = 0) -> tuple[int, int]:
+    """(forward / dQ gathered tiles, dK/dV gathered tiles) of pattern p: the kernels' work units."""
+    t = np.asarray(tables).view(np.int32)
+    nt, per = int(t[0]), int(t[6])
+    base = 8 + p * per
+    return int(t[base + nt]), int(t[base + nt + 1 + nt])
 
 
 def pool_grids(pool: dict[str, LayoutTable]) -> np.ndarray:
@@ -262,8 +256,6 @@ def pool_grids(pool: dict[str, LayoutTable]) -> np.ndarray:
 def device_pool(pool: dict[str, LayoutTable], device, seq_len: int | None = None, attn_blk: int | None = None) -> DevicePool:
     import torch
 
-    from . import _abi
-
     ids = list(pool)
     if ids[-1] != "dense":
         raise PatternError("pool must end with 'dense'")
@@ -272,11 +264,6 @@ def device_pool(pool: dict[str, LayoutTable], device, seq_len: int | None = None
     dp = DevicePool(ids, torch.from_numpy(kinds).to(device), torch.from_numpy(params).to(device), None,
                     index={p: i for i, p in enumerate(ids)})
     if seq_len is not None:
-        n = ctypes.c_int(0)
-        _abi.lib().lx_attn_tables_size(len(ids), seq_len, attn_blk, ctypes.byref(n))
-        host = np.zeros(n.value, np.int32)
-        _abi.call("lx_attn_tables", kinds.ctypes.data, params.ctypes.data, len(ids), seq_len, attn_blk, host.ctypes.data, n.value)
-        dp.tables = torch.from_numpy(host).to(device)
-        dp.tables128 = torch.from_numpy(tables128_from_grids(pool_grids(pool), seq_len, attn_blk)).to(device)
+        dp.tables = torch.from_numpy(tables128_from_grids(pool_grids(pool), seq_len, attn_blk)).to(device)
         dp.seq_len, dp.attn_blk = seq_len, attn_blk
     return dp

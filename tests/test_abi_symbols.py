@@ -17,7 +17,7 @@ def header_symbols():
 
 def test_header_declares_entry_points():
     syms = header_symbols()
-    assert "lx_neuron_fc1" in syms and "lx_bsattn_bwd" in syms and "lx_predict_mlp_mask" in syms
+    assert "lx_neuron_fc1" in syms and "lx_bsattn_bwd_tc" in syms and "lx_predict_mlp_mask" in syms
     assert len(syms) >= 20
 
 
@@ -42,12 +42,6 @@ def test_error_mapping_without_gpu():
     with pytest.raises(E.UnsupportedError):
         _abi.call("lx_neuron_fc1", None, 1, 16, 64, 64, 24, None, None, None, None, None, None, 0, 1.0, 1, None, 64, None,
                   None)
-    with pytest.raises(E.LayoutError):
-        import ctypes
-
-        import numpy as np
-
-        kinds = np.zeros(1, np.int32)
-        out = np.zeros(64, np.int32)
-        _abi.call("lx_attn_tables", kinds.ctypes.data, kinds.ctypes.data, 1, 100, 16, out.ctypes.data, 64)
+    with pytest.raises(E.LayoutError):  # gather_rows must be a power of two in [16, 128]
+        _abi.call("lx_bsattn_fwd_tc", None, 192, 1, 128, 1, 64, None, 0, None, 48, 0.125, None, 64, None, None)
     assert issubclass(E.LayoutError, ValueError) and issubclass(E.MaskError, ValueError)

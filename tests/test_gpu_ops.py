@@ -137,7 +137,7 @@ def _attn_case(dev, n_items, s, H, hd, attn_blk, seed, layouts=None):
             np.fill_diagonal(grid, True)
             layouts.append(grid)
     grids = np.stack(layouts)
-    tables = torch.from_numpy(PT.tables_from_grids(grids, s, attn_blk)).to(dev)
+    tables = torch.from_numpy(PT.tables128_from_grids(grids, s, attn_blk)).to(dev)
     pidx = torch.arange(len(layouts), dtype=torch.int32, device=dev).view(n_items, H)
     dp = PT.DevicePool([str(i) for i in range(len(layouts))], None, None, tables, s, attn_blk)
     return q, k, v, do, grids, pidx, dp
@@ -187,7 +187,7 @@ def test_bsattn_golden(dev, golden, c):
     grid = np.zeros((1, n_b, n_b), bool)
     cs = g[f"c{c}/coords"]
     grid[0, cs[:, 0], cs[:, 1]] = True
-    tables = torch.from_numpy(PT.tables_from_grids(grid, s, blk)).to(dev)
+    tables = torch.from_numpy(PT.tables128_from_grids(grid, s, blk)).to(dev)
     dp = PT.DevicePool(["custom"], None, None, tables, s, blk)
     pidx = torch.zeros(1, 1, dtype=torch.int32, device=dev)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev, torch.bfloat16)  # noqa: E731
@@ -203,42 +203,21 @@ def test_bsattn_golden(dev, golden, c):
     assert rel(dk.float().cpu(), g[f"c{c}/dk"]) < 2e-2
 
 
-def test_pool_tables_match_python(dev):
-    """C-ABI pool-kind tables == generic grid tables for every pool pattern."""
-    from paper_2510_15964_b200 import patterns as PT
-
-    for s, ab in ((256, 16), (512, 64), (1024, 128), (192, 32)):
-        pool = PT.build_pool(s // ab)
-        dp = PT.device_pool(pool, dev, s, ab)
-        grids = np.zeros((len(pool), s // ab, s // ab), bool)
-        for i, t in enumerate(pool.values()):
-            c = np.array(t.coords)
-            grids[i, c[:, 0], c[:, 1]] = True
-        np.testing.assert_array_equal(dp.tables.cpu().numpy(), PT.tables_from_grids(grids, s, ab))
-
-
 @pytest.mark.parametrize("n_items,s,H,hd,attn_blk", [(2, 256, 2, 64, 16), (1, 384, 3, 64, 32), (2, 512, 4, 64, 64),
-                                                      (1, 256, 2, 128, 64), (2, 240, 2, 64, 48), (3, 1024, 2, 64, 128)])
+                                                      (1, 256, 2, 128, 64), (2, 240, 2, 64, 48), (3, 1024, 2, 64, 128),
+                                                      (1, 1024, 2, 128, 16), (2, 2048, 1, 64, 256), (1, 640, 2, 128, 32)])
 def test_bsattn_tcgen05_fwd(dev, n_items, s, H, hd, attn_blk):
-    """tcgen05 forward (csrc/attn_sm100.cu, 128x128 tiles) on the fused QKV layout vs the oracle
-    (sdd -> sparse_softmax -> dsd) and vs the warp-MMA kernel; LSE vs the fp64 reference."""
+    """tcgen05 forward (csrc/attn_sm100.cu, gathered 128-tiles) on the fused QKV layout vs the oracle
+    (sdd -> sparse_softmax -> dsd); LSE vs the fp64 reference."""
     from paper_2510_15964_b200 import block_sparse as BS, patterns as PT
 
     q, k, v, do, grids, pidx, dp = _attn_case(dev, n_items, s, H, hd, attn_blk, seed=s + hd + attn_blk)
-    dp.tables128 = torch.from_numpy(PT.tables128_from_grids(grids, s, attn_blk)).to(dev)
     d = H * hd
     qkv = torch.from_numpy(np.concatenate([q, k, v], 1)).to(dev, torch.bfloat16)
     scale = 1.0 / np.sqrt(hd)
     o, lse = BS.attention_forward(qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :], 3 * d, n_items, s, H, hd, pidx, H, dp, scale)
-    BS.USE_TCGEN05 = False
-    try:
-        o2, lse2 = BS.attention_forward(qkv[:, :d], qkv[:, d : 2 * d], qkv[:, 2 * d :], 3 * d, n_items, s, H, hd, pidx, H, dp,
-                                        scale)
-    finally:
-        BS.USE_TCGEN05 = True
     torch.cuda.synchronize()
-    o, o2, lse, lse2 = o.float().cpu().numpy(), o2.float().cpu().numpy(), lse.cpu().numpy(), lse2.cpu().numpy()
-    assert rel(o, o2) < 1e-2
+    o, lse = o.float().cpu().numpy(), lse.cpu().numpy()
     n_b = s // attn_blk
     for b in range(n_items):
         rows = slice(b * s, (b + 1) * s)
@@ -248,18 +227,21 @@ def test_bsattn_tcgen05_fwd(dev, n_items, s, H, hd, attn_blk):
             qq, kk, vv = (bf(a[rows, cols]) for a in (q, k, v))
             p = O.sparse_softmax(O.sdd(qq, kk, coords, attn_blk, scale), coords, n_b)
             assert rel(o[rows, cols], O.dsd(p, vv, coords, n_b)) < 1e-2, (b, h)
-    assert np.abs(lse - lse2).max() < 2e-2
+            sc = (qq.astype(np.float64) @ kk.astype(np.float64).T) * scale
+            mk = np.kron(grids[b * H + h], np.ones((attn_blk, attn_blk), bool))
+            ref_lse = np.log(np.where(mk, np.exp(sc - sc.max()), 0).sum(1)) + sc.max()
+            assert np.abs(lse[b, h] - ref_lse).max() < 2e-2, (b, h)
 
 
 @pytest.mark.parametrize("n_items,s,H,hd,attn_blk", [(2, 256, 2, 64, 16), (1, 384, 3, 64, 32), (2, 512, 4, 64, 64),
-                                                      (1, 256, 2, 128, 64), (2, 240, 2, 64, 48), (3, 1024, 2, 64, 128)])
+                                                      (1, 256, 2, 128, 64), (2, 240, 2, 64, 48), (3, 1024, 2, 64, 128),
+                                                      (1, 1024, 2, 128, 16), (2, 2048, 1, 64, 256), (1, 640, 2, 128, 32)])
 def test_bsattn_tcgen05_bwd(dev, n_items, s, H, hd, attn_blk):
     """tcgen05 backward (dK/dV over the CSC walk, dQ over the CSR walk) on the fused dQKV layout vs
-    the oracle chain dsd_backward -> sparse_softmax_backward -> sdd_backward and the warp-MMA kernel."""
+    the oracle chain dsd_backward -> sparse_softmax_backward -> sdd_backward."""
     from paper_2510_15964_b200 import block_sparse as BS, patterns as PT
 
     q, k, v, do, grids, pidx, dp = _attn_case(dev, n_items, s, H, hd, attn_blk, seed=3 * s + hd + attn_blk)
-    dp.tables128 = torch.from_numpy(PT.tables128_from_grids(grids, s, attn_blk)).to(dev)
     d = H * hd
     qkv = torch.from_numpy(np.concatenate([q, k, v], 1)).to(dev, torch.bfloat16)
     dod = torch.from_numpy(do).to(dev, torch.bfloat16)
@@ -269,17 +251,9 @@ def test_bsattn_tcgen05_bwd(dev, n_items, s, H, hd, attn_blk):
     dqkv = torch.full_like(qkv, float("nan"))
     BS.attention_backward(Q, K, V, o, dod, 3 * d, n_items, s, H, hd, pidx, H, dp, scale, lse,
                           dqkv[:, :d], dqkv[:, d : 2 * d], dqkv[:, 2 * d :])
-    BS.USE_TCGEN05 = False
-    try:
-        dqkv2 = torch.zeros_like(qkv)
-        BS.attention_backward(Q, K, V, o, dod, 3 * d, n_items, s, H, hd, pidx, H, dp, scale, lse,
-                              dqkv2[:, :d], dqkv2[:, d : 2 * d], dqkv2[:, 2 * d :])
-    finally:
-        BS.USE_TCGEN05 = True
     torch.cuda.synchronize()
-    g, g2 = dqkv.float().cpu().numpy(), dqkv2.float().cpu().numpy()
+    g = dqkv.float().cpu().numpy()
     assert np.isfinite(g).all()
-    assert rel(g, g2) < 2e-2
     n_b = s // attn_blk
     for b in range(n_items):
         rows = slice(b * s, (b + 1) * s)
@@ -304,7 +278,6 @@ def test_bsattn_tcgen05_bwd_extended_dqkv(dev):
 
     n_items, s, H, hd, attn_blk = 2, 512, 4, 64, 64
     q, k, v, do, grids, pidx, dp = _attn_case(dev, n_items, s, H, hd, attn_blk, seed=77)
-    dp.tables128 = torch.from_numpy(PT.tables128_from_grids(grids, s, attn_blk)).to(dev)
     d = H * hd
     qkv = torch.from_numpy(np.concatenate([q, k, v], 1)).to(dev, torch.bfloat16)
     dod = torch.from_numpy(do).to(dev, torch.bfloat16)

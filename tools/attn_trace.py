@@ -24,8 +24,8 @@ buf = torch.zeros(n_cta, 32, dtype=torch.int64, device=dev)
 
 
 def run():
-    _abi.call("lx_bsattn_fwd_tc", qkv.data_ptr(), 3 * d, B, s, H, hd, pidx.data_ptr(), H, dp.tables128.data_ptr(),
-              1.0 / 8, o.data_ptr(), d, lse.data_ptr(), _abi.stream_handle())
+    _abi.call("lx_bsattn_fwd_tc", qkv.data_ptr(), 3 * d, B, s, H, hd, pidx.data_ptr(), H, dp.tables.data_ptr(),
+              dp.gather_rows, 1.0 / 8, o.data_ptr(), d, lse.data_ptr(), _abi.stream_handle())
 
 
 for _ in range(3):
