@@ -147,7 +147,7 @@ class _CalibratingProvider:
 
     fused_downsample = False
 
-    def __init__(self, inner, n_local: int, r_pred: int, g, device, k_shared: int = 32):
+    def __init__(self, inner, n_local: int, r_pred: int, g, device, k_shared: int = int(os.environ.get("LX_BENCH_KSHARED", "32"))):
         self.inner, self.n_local, self.r_pred, self.g, self.device = inner, n_local, r_pred, g, device
         self.k_shared = k_shared
 
@@ -194,8 +194,20 @@ def build_workload(cfg: dict, device, seed: int, mlp_sparsity: float, local_frac
         ad.b.normal_(0.0, 0.02, generator=g)
     for ad in model.adapters.values():
         ad.w_up.normal_(0.0, 0.02, generator=g)
-    state = M.make_peft_state(model)
     d, H, n_blk = dims.d_model, dims.n_heads, dims.n_blk
+    n_local = int(round(H * local_frac))
+    if os.environ.get("LX_BENCH_IDENTITY_QK", "1") == "1":
+        # pkg/demos/01_expose_sparsity.py:20-42: the local heads' q/k projections become scaled identities on the
+        # head slice (3 I), so each token's score concentrates on itself and similar tokens
+        hd = dims.head_dim
+        eye = 3.0 * torch.eye(hd, device=device, dtype=torch.bfloat16)
+        for lw in model.weights.layers:
+            for off in (0, d):  # W_q | W_k column blocks of the fused [d, 3d] projection
+                for h in range(n_local):
+                    c0 = off + h * hd
+                    lw.wqkv[:, c0 : c0 + hd] = 0
+                    lw.wqkv[h * hd : (h + 1) * hd, c0 : c0 + hd] = eye
+    state = M.make_peft_state(model)
     r_pred = max(4, d // 16)  # sf/harness.py:332 default
     mlp = []
     for layer in range(dims.n_layers):
@@ -210,7 +222,7 @@ def build_workload(cfg: dict, device, seed: int, mlp_sparsity: float, local_frac
     # calibration forward on one synthetic sequence builds every layer's attention predictor in place
     tok = torch.randint(0, dims.vocab, (1, dims.seq_len), generator=torch.Generator().manual_seed(seed + 4242)).to(device)
     with torch.no_grad():
-        M.model_forward(model, tok, _CalibratingProvider(provider, int(round(H * local_frac)), r_pred, g, device))
+        M.model_forward(model, tok, _CalibratingProvider(provider, n_local, r_pred, g, device))
     provider.reset_timing()
     return model, state, provider
 

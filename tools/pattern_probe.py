@@ -24,11 +24,14 @@ torch.cuda.synchronize()
 ids = list(model.pool)
 H = cfg["H"]
 nl = int(round(H * lf))
-for layer, lm in enumerate(eng.last_masks):
-    hp = lm.head_patterns.cpu().numpy()
-    loc = Counter(ids[i] for i in hp[:, :nl].ravel())
-    oth = Counter(ids[i] for i in hp[:, nl:].ravel())
-    print(f"layer {layer:2d} local {dict(loc)} other {dict(oth)}")
+print("achieved", bench.achieved_sparsity(eng.last_masks, model))
+if "-v" in sys.argv:
+    for layer, lm in enumerate(eng.last_masks):
+        hp = lm.head_patterns.cpu().numpy()
+        loc = Counter(ids[i] for i in hp[:, :nl].ravel())
+        oth = Counter(ids[i] for i in hp[:, nl:].ravel())
+        print(f"layer {layer:2d} local {dict(loc)} other {dict(oth)}")
+sys.exit(0)
 # score maps of layer L/2 local head 0 on the recorded LN1 rows
 rec = EX._Recorder(model)
 with torch.no_grad():
