@@ -214,12 +214,13 @@ int lx_bsattn_fwd_tc(const uint16_t* qkv, int ld, int n_items, int s, int H, int
 /* Backward (dsd_backward -> sparse_softmax_backward -> sdd_backward, sf/block_sparse.py:63-137;
  * replaces mha_backward's per-head loop, sf/autograd.py:149-156): dqkv [n_items*s, ld_d] (same fused
  * layout as qkv) from d_o [n_items*s, ld_o] and the forward's o / lse; delta_ws fp32 [n_items, H, s];
- * ksum_ws fp32 [n_items, H, ceil(s/128), hd] (per-key-tile column sums of K, used by dQ to cancel the
- * bf16 row-sum residual of dS against the keys' common mode). dK/dV walk the CSC of each 128-key tile,
- * dQ the CSR of each 128-query tile. */
+ * ws fp32 [n_items * H * (hd + 8 * ceil(s/128))]: the per-(item, head) mean key (used by dQ to cancel the
+ * bf16 row-sum residual of dS against the keys' common mode) and the per-unit work descriptors, all
+ * written by the backward's prologue kernel. dK/dV walk the CSC of each 128-key tile, dQ the CSR of each
+ * 128-query tile. */
 int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                      int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128, int gather_rows,
-                     float scale, const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv, lx_stream_t stream);
+                     float scale, const float* lse, float* delta_ws, float* ws, uint16_t* dqkv, lx_stream_t stream);
 /* Debug only: per-CTA clock64 phase stamps of the tcgen05 attention kernels into buf
  * [n_ctas][32] (slot 31 = SM id); NULL disables. Used by tools/attn_trace.py. */
 int lx_debug_set_attn_trace(unsigned long long* buf);

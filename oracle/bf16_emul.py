@@ -29,7 +29,7 @@ Device rounding points (file:line of this repo's product path):
     * (a > 0)); dx_mlp = bf16(dz W1^T + dax1 A1^T); d_heads = bf16(g W_o^T); attention backward
     recomputes P = 2^(S c - lse log2 e), dS = bf16(bf16(P) (dP - D)), D = rowsum(dO O),
     dV = bf16(bf16(P)^T dO), dK = bf16(c dS^T Q), dQ = bf16(c (dS K - eps kbar)) with eps the row
-    sum of the bf16 dS and kbar the mean key (the dQ kernel's common-mode correction); the q/k/v
+    sum of the bf16 dS and kbar the mean of the first 128 keys (the dQ kernel's common-mode correction); the q/k/v
     input-grad is one K-extended GEMM bf16(dq W_q^T + dk W_k^T + dv W_v^T + bf16(dax) bf16(A)^T);
   * LoRA / BitFit gradients are fp32 reductions of the bf16 activations and fp32 dax/ax;
   * Adapter: fp32 torch ops on the fp32 (or bf16-valued) inputs (model.py:adapter_forward).
@@ -136,7 +136,7 @@ def attention_backward_dev(e: Emul, q, k, v, o, do, lse, mask, scale):
     dv = e.rd(e.mm(Pb.T, do))
     dk = e.rd(e.mm(dS.T, q) * np.float32(scale))
     eps = dS.astype(np.float64).sum(1)
-    kbar = k.astype(np.float64).mean(0)
+    kbar = k[: min(len(k), 128)].astype(np.float64).mean(0)  # the prep kernel's first-tile key mean
     dq_raw = dS.astype(np.float64) @ k.astype(np.float64)
     if not e.exact:
         dq_raw = dq_raw - eps[:, None] * kbar[None, :]  # the dQ kernel's row-sum (common-mode) correction

@@ -97,19 +97,19 @@ def attention_backward(q, k, v, o, d_o, ld: int, n_items: int, s: int, H: int, h
              and dv.data_ptr() == dq.data_ptr() + 4 * d and dk.stride(0) == dq.stride(0) == dv.stride(0) >= 3 * d)
     if fused:
         # dqkv may be the K-extended [M, 3d + kx] operand of the projection input-grad GEMM (row stride dq.stride(0))
-        ksum = torch.empty(n_items, H, (s + 127) // 128, hd, dtype=torch.float32, device=dev)
+        ws = torch.empty(n_items * H * (hd + 8 * ((s + 127) // 128)), dtype=torch.float32, device=dev)
         _abi.call("lx_bsattn_bwd_tc", q.data_ptr(), ld, dq.stride(0), o.data_ptr(), d_o.data_ptr(), o.stride(0), n_items, s, H,
                   hd, pidx.data_ptr(), item_stride, dpool.tables.data_ptr(), dpool.gather_rows, float(scale), lse.data_ptr(),
-                  delta.data_ptr(), ksum.data_ptr(), dq.data_ptr(), _abi.stream_handle(dev))
+                  delta.data_ptr(), ws.data_ptr(), dq.data_ptr(), _abi.stream_handle(dev))
         return
     hdp = _padded_hd(hd)
     qkv = _stage([q, k, v], M, H, hd, hdp)
     od = _stage([o, d_o], M, H, hd, hdp)
     dqkv = torch.empty(M, 3 * H * hdp, dtype=torch.bfloat16, device=dev)
-    ksum = torch.empty(n_items, H, (s + 127) // 128, hdp, dtype=torch.float32, device=dev)
+    ws = torch.empty(n_items * H * (hdp + 8 * ((s + 127) // 128)), dtype=torch.float32, device=dev)
     _abi.call("lx_bsattn_bwd_tc", qkv.data_ptr(), qkv.stride(0), dqkv.stride(0), od.data_ptr(), od[:, H * hdp :].data_ptr(),
               od.stride(0), n_items, s, H, hdp, pidx.data_ptr(), item_stride, dpool.tables.data_ptr(), dpool.gather_rows,
-              float(scale), lse.data_ptr(), delta.data_ptr(), ksum.data_ptr(), dqkv.data_ptr(), _abi.stream_handle(dev))
+              float(scale), lse.data_ptr(), delta.data_ptr(), ws.data_ptr(), dqkv.data_ptr(), _abi.stream_handle(dev))
     g = dqkv.view(M, 3, H, hdp)
     for i, dst in enumerate((dq, dk, dv)):
         dst[:M, :d].view(M, H, hd).copy_(g[:, i, :, :hd])

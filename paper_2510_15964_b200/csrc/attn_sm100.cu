@@ -446,7 +446,7 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
                       const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_do_g, int gu, int s, int H,
                       int d_model, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                       float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
-                      __nv_bfloat16* __restrict__ dkv, int ld_dkv, float* __restrict__ ksum) {
+                      __nv_bfloat16* __restrict__ dkv, int ld_dkv) {
   pdl_wait_trigger();
   if (threadIdx.x == 0) trace_stamp(0);
   using L = AttnBwdSmem<HD>;
@@ -648,26 +648,6 @@ bsattn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
         }
       }
     }
-    // column sums of this key tile (keys < s) -> ksum[item, h, kt, :]: the common mode the dQ
-    // kernel removes (see bsattn_dq_tc_kernel). K is still resident; sL is free now.
-    {
-      constexpr int G = 128 / HD;  // row groups
-      const int col = ep_tid % HD, grp = ep_tid / HD, rows = kAT / G;
-      const uint8_t* katom = sm + (col >> 6) * (kAT * 128);
-      float acc = 0.f;
-      for (int rr = 0; rr < rows; ++rr) {
-        const int r = grp * rows + rr;
-        if (kt * kAT + r < s)
-          acc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
-              katom + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4) + (col & 7) * 2));
-      }
-      sL[ep_tid] = acc;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (grp == 0) {
-        for (int g2 = 1; g2 < G; ++g2) acc += sL[g2 * HD + col];
-        ksum[(((size_t)item * H + h) * gridDim.x + kt) * HD + col] = acc;
-      }
-    }
   }
   if (threadIdx.x == 64) trace_stamp(27);
   tc_fence_before();
@@ -684,7 +664,7 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
                     const __grid_constant__ CUtensorMap tm_g, int gu, int s, int H,
                     int d_model, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                     float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
-                    __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ ksum) {
+                    __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ kbar_g) {
   pdl_wait_trigger();
   using L = AttnBwdSmem<HD>;  // [Q | dO] [kSt x (K | V)] [kbar]
   constexpr int A = HD / 64;
@@ -834,13 +814,8 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_ready);
     }
-    // kbar = mean over the item's keys (column sums from the dK/dV kernel)
-    if (r < HD) {
-      const float* ks = ksum + ((size_t)item * H + h) * gridDim.x * HD + r;
-      float acc = 0.f;
-      for (int t = 0; t < (int)gridDim.x; ++t) acc += __ldg(ks + t * HD);
-      kbar[r] = acc / (float)s;
-    }
+    // kbar = mean over the item's keys (bsattn_prep_kernel)
+    if (r < HD) kbar[r] = __ldg(kbar_g + ((size_t)item * H + h) * HD + r);
     asm volatile("bar.sync 1, 128;" ::: "memory");
     mbar_wait(done, 0);
     tc_fence_after();
@@ -870,51 +845,112 @@ bsattn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
   }
 }
 
-// delta[item, h, row] = sum_c dO[row, c] * O[row, c]  (== rowsum(dP * P), sf/block_sparse.py:102-113).
-// One warp per token row: lane l reads 16 B chunks l, l+32, ... of O and dO (all in flight), a group of
-// HD/8 lanes holds one head per pass and reduces it with shuffles.
+// Backward prologue, one launch (three block ranges):
+//  [0, nb_delta)            delta[item, h, row] = sum_c dO[row, c] * O[row, c] (== rowsum(dP * P),
+//                           sf/block_sparse.py:102-113): one warp per token row, lane l reads 16 B chunks
+//                           l, l+32, ... of O and dO (all in flight), a group of HD/8 lanes holds one head;
+//  [nb_delta, +n_items*H)   kbar[item, h, :] = mean of K over the item's first min(s, 128) keys (the dQ
+//                           kernels' common-mode vector, fixed-order tree);
+//  [.., +nb_desc)           per-unit work descriptors {e0, n, pattern} of the dK/dV walk (CSC of each key
+//                           tile) and the dQ walk (CSR of each query tile), so the persistent kernels read one
+//                           int4 per unit (prefetched a unit ahead) instead of a pidx -> table -> pointer chain.
 template <int HD>
-__global__ void __launch_bounds__(256) bsattn_delta_tc_kernel(const __nv_bfloat16* __restrict__ o,
-                                                              const __nv_bfloat16* __restrict__ d_o, int ld,
-                                                              int n_rows_total, int s, int H, float* __restrict__ delta) {
+__global__ void __launch_bounds__(256) bsattn_prep_kernel(const __nv_bfloat16* __restrict__ o,
+                                                          const __nv_bfloat16* __restrict__ d_o, int ld, int n_rows_total,
+                                                          int s, int H, float* __restrict__ delta,
+                                                          const __nv_bfloat16* __restrict__ qkv, int ldq,
+                                                          float* __restrict__ kbar, const int32_t* __restrict__ pidx,
+                                                          int item_stride, const int32_t* __restrict__ tables,
+                                                          int4* __restrict__ desc_kv, int4* __restrict__ desc_q, int n_units,
+                                                          int nb_delta, int nb_kbar) {
   pdl_wait_trigger();
-  constexpr int G = HD / 8;  // lanes per head
-  constexpr int kIt = 8;     // 16 B chunks per lane per pass (2048 columns)
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= n_rows_total) return;
-  const int d = H * HD, n_it = (d + 255) / 256;
-  const uint4* a = reinterpret_cast<const uint4*>(o + (size_t)row * ld);
-  const uint4* b = reinterpret_cast<const uint4*>(d_o + (size_t)row * ld);
-  const size_t out_row = (size_t)(row / s) * H * s + row % s;
-  for (int base = 0; base < n_it; base += kIt) {
-  uint4 va[kIt], vb[kIt];
+  const int d = H * HD;
+  if ((int)blockIdx.x < nb_delta) {
+    constexpr int G = HD / 8;  // lanes per head
+    constexpr int kIt = 8;     // 16 B chunks per lane per pass (2048 columns)
+    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= n_rows_total) return;
+    const int n_it = (d + 255) / 256;
+    const uint4* a = reinterpret_cast<const uint4*>(o + (size_t)row * ld);
+    const uint4* b = reinterpret_cast<const uint4*>(d_o + (size_t)row * ld);
+    const size_t out_row = (size_t)(row / s) * H * s + row % s;
+    for (int base = 0; base < n_it; base += kIt) {
+      uint4 va[kIt], vb[kIt];
 #pragma unroll
-  for (int i = 0; i < kIt; ++i) {
-    const int c = (base + i) * 32 + lane;
-    const bool ok = base + i < n_it && c * 8 < d;
-    va[i] = ok ? __ldg(a + c) : make_uint4(0u, 0u, 0u, 0u);
-    vb[i] = ok ? __ldg(b + c) : make_uint4(0u, 0u, 0u, 0u);
+      for (int i = 0; i < kIt; ++i) {
+        const int c = (base + i) * 32 + lane;
+        const bool ok = base + i < n_it && c * 8 < d;
+        va[i] = ok ? __ldg(a + c) : make_uint4(0u, 0u, 0u, 0u);
+        vb[i] = ok ? __ldg(b + c) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int i = 0; i < kIt; ++i) {
+        const int it = base + i;
+        if (it >= n_it) break;
+        const uint32_t xa[4] = {va[i].x, va[i].y, va[i].z, va[i].w}, xb[4] = {vb[i].x, vb[i].y, vb[i].z, vb[i].w};
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const __nv_bfloat162 p = *reinterpret_cast<const __nv_bfloat162*>(&xa[k]);
+          const __nv_bfloat162 q = *reinterpret_cast<const __nv_bfloat162*>(&xb[k]);
+          acc = fmaf(__low2float(p), __low2float(q), acc);
+          acc = fmaf(__high2float(p), __high2float(q), acc);
+        }
+#pragma unroll
+        for (int off = 1; off < G; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        const int h = (it * 32 + lane) * 8 / HD;
+        if ((lane % G) == 0 && h < H) delta[out_row + (size_t)h * s] = acc;
+      }
+    }
+    return;
   }
+  if ((int)blockIdx.x < nb_delta + nb_kbar) {
+    // kbar of (item, h) over the item's first min(s, 128) keys: any fixed vector is exact for the dQ
+    // identity sum_j dS_ij (k_j - kbar) = sum_j dS_ij k_j; the first tile's mean estimates the common mode.
+    // 16-byte loads: thread t reads chunk t % (HD / 8) of rows t / (HD / 8), + 256 / (HD / 8), ...
+    __shared__ float part[256 / (HD / 8)][HD];
+    constexpr int CH = HD / 8, RS = 256 / CH;
+    const int ih = blockIdx.x - nb_delta, item = ih / H, h = ih % H;
+    const int ch = threadIdx.x % CH, r0 = threadIdx.x / CH;
+    const int nr = s < kAT ? s : kAT;
+    const __nv_bfloat16* kp = qkv + (size_t)item * s * ldq + d + h * HD + ch * 8;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int r = r0; r < nr; r += RS) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(kp + (size_t)r * ldq));
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-  for (int i = 0; i < kIt; ++i) {
-    const int it = base + i;
-    if (it >= n_it) break;
-    const uint32_t xa[4] = {va[i].x, va[i].y, va[i].z, va[i].w}, xb[4] = {vb[i].x, vb[i].y, vb[i].z, vb[i].w};
-    float acc = 0.f;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const __nv_bfloat162 p = *reinterpret_cast<const __nv_bfloat162*>(&xa[k]);
-      const __nv_bfloat162 q = *reinterpret_cast<const __nv_bfloat162*>(&xb[k]);
-      acc = fmaf(__low2float(p), __low2float(q), acc);
-      acc = fmaf(__high2float(p), __high2float(q), acc);
+      for (int q = 0; q < 4; ++q) {
+        const __nv_bfloat162 p2 = *reinterpret_cast<const __nv_bfloat162*>(&w[q]);
+        acc[2 * q] += __low2float(p2);
+        acc[2 * q + 1] += __high2float(p2);
+      }
     }
 #pragma unroll
-    for (int off = 1; off < G; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    const int h = (it * 32 + lane) * 8 / HD;
-    if ((lane % G) == 0 && h < H) delta[out_row + (size_t)h * s] = acc;
+    for (int q = 0; q < 8; ++q) part[r0][ch * 8 + q] = acc[q];
+    __syncthreads();
+    if ((int)threadIdx.x < HD) {
+      float t = 0.f;
+      for (int g2 = 0; g2 < RS; ++g2) t += part[g2][threadIdx.x];
+      kbar[(size_t)ih * HD + threadIdx.x] = t / (float)nr;
+    }
+    return;
   }
-  }
+  const int u = (blockIdx.x - nb_delta - nb_kbar) * blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  const int nt = __ldg(tables), per = __ldg(tables + 6);
+  const int t = u % nt, h = (u / nt) % H, item = u / (nt * H);
+  const int p = __ldg(pidx + item * item_stride + h);
+  const int32_t* b = tables + 8 + (size_t)p * per;
+  const int r0 = __ldg(b + t), r1 = __ldg(b + t + 1);
+  const int c0 = __ldg(b + nt + 1 + t), c1 = __ldg(b + nt + 2 + t);
+  desc_q[u] = make_int4(r0, r1 - r0, p, 0);
+  desc_kv[u] = make_int4(c0, c1 - c0, p, 0);
+}
+
+// the pattern's CSR (csc = false) or CSC entry array, from a unit descriptor
+LX_DEV const int32_t* desc_entries(const int32_t* tables, int nt, int per, int p, bool csc) {
+  return tables + 8 + (size_t)p * per + 2 * (nt + 1) + (csc ? kEntryInts * nt * nt : 0);
 }
 
 // ============================================================================ backward dK/dV, ping-pong
@@ -935,10 +971,14 @@ constexpr int kBwdThreads = 64 + 32 * 8;  // producer, MMA issuer, two 4-warp ep
 template <int HD>
 struct AttnDkdvPP {
   static constexpr int kT = (HD / 64) * kAT * 128;  // one 128 x HD bf16 tile
-  static constexpr int kKV = HD == 64 ? 2 : 1;      // K/V buffers
-  static constexpr int kSt = HD == 64 ? 3 : 2;      // Q/dO ring stages
+#ifndef LX_DKDV_KV
+#define LX_DKDV_KV 2
+#define LX_DKDV_ST 3
+#endif
+  static constexpr int kKV = HD == 64 ? LX_DKDV_KV : 1;  // K/V buffers
+  static constexpr int kSt = HD == 64 ? LX_DKDV_ST : 2;  // Q/dO ring stages
   static constexpr int kOffRing = kKV * 2 * kT;
-  static constexpr int kOffL = kOffRing + kSt * 2 * kT;          // lse*log2e [kSt][128], delta [kSt][128]
+  static constexpr int kOffL = kOffRing + kSt * 2 * kT;          // lse [kSt][128], delta [kSt][128]
   static constexpr int kStgPitch = 144;                          // staging row: 128 B of bf16 + 16 B pad
   static constexpr int kOffStg = kOffL + 2 * kSt * kAT * 4;      // [8 warps][32 rows][kStgPitch]
   static constexpr int kOffBar = kOffStg + 8 * 32 * kStgPitch;
@@ -951,7 +991,7 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
                       const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_do_g, int gu, int s, int H,
                       int n_units, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                       float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
-                      __nv_bfloat16* __restrict__ dkv, int ld_dkv, float* __restrict__ ksum) {
+                      __nv_bfloat16* __restrict__ dkv, int ld_dkv, const int4* __restrict__ desc) {
   using L = AttnDkdvPP<HD>;
   constexpr int A = HD / 64;
   const int d_model = H * HD;
@@ -961,7 +1001,7 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
   uint64_t* kv_full = bars;                // [kKV]
   uint64_t* kv_empty = bars + 2;           // [kKV]
-  uint64_t* qd_full = bars + 4;            // [kSt] TMA (1 arrive + tx) + 32 producer lanes (lse / delta)
+  uint64_t* qd_full = bars + 4;            // [kSt] TMA + bulk copies (1 arrive + tx)
   uint64_t* qd_empty = bars + 8;           // [kSt]
   uint64_t* s_full = bars + 12;            // [2]
   uint64_t* p_ready = bars + 14;           // [2] 4 warps
@@ -970,8 +1010,9 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
   uint64_t* acc_full = bars + 20;
   uint64_t* acc_empty = bars + 21;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
-  float* sL = reinterpret_cast<float*>(sm + L::kOffL);  // [kSt][128]
-  float* sD = sL + L::kSt * kAT;                        // [kSt][128]
+  uint64_t* sMask = bars + 32;                          // [kSt] cell mask of the staged entry
+  float* sL = reinterpret_cast<float*>(sm + L::kOffL);  // [kSt][128] lse (natural log) of the gathered rows
+  float* sD = sL + L::kSt * kAT;                        // [kSt][128] delta
 
   const uint32_t warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
@@ -981,10 +1022,10 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
     tma_prefetch_desc(&tm_do_g);
     for (int i = 0; i < L::kKV; ++i) {
       mbar_init(kv_full + i, 1);
-      mbar_init(kv_empty + i, 2);
+      mbar_init(kv_empty + i, 1);
     }
     for (int i = 0; i < L::kSt; ++i) {
-      mbar_init(qd_full + i, 33);
+      mbar_init(qd_full + i, 1);
       mbar_init(qd_empty + i, 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -1006,23 +1047,28 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_dv = tmem + 2 * kAT, t_dk = tmem + 2 * kAT + HD;
 
-  // unit -> (item, h, kt) and its CSC range
-  auto unit_of = [&](int u, int& item, int& h, int& kt, Tab128& tv, int& e0, int& n) {
+  // unit -> (item, h, kt) and its CSC range from the prep kernel's descriptors, read one unit ahead
+  const int tab_nt = __ldg(tables), tab_per = __ldg(tables + 6);
+  auto dload = [&](int u) { return u < n_units ? __ldg(desc + u) : make_int4(0, 0, 0, 0); };
+  auto unit_of = [&](int u, int4& dnext, int& item, int& h, int& kt, const int32_t*& ents, int& e0, int& n) {
+    const int4 dd = dnext;
+    dnext = dload(u + gridDim.x);
     kt = u % nkt;
     h = (u / nkt) % H;
     item = u / (nkt * H);
-    tv = tab128(tables, __ldg(pidx + item * item_stride + h));
-    e0 = __ldg(tv.col_ptr + kt);
-    n = __ldg(tv.col_ptr + kt + 1) - e0;
+    e0 = dd.x;
+    n = dd.y;
+    ents = desc_entries(tables, tab_nt, tab_per, dd.z, true);
   };
 
   if (warp == 0) {
     // ================= producer: K/V per unit, then the unit's Q/dO tiles (+ lse / delta rows)
     int kvi = 0, g = 0;
+    int4 dnext = dload(blockIdx.x);
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++kvi) {
       int item, h, kt, e0, n;
-      Tab128 tv;
-      unit_of(u, item, h, kt, tv, e0, n);
+      const int32_t* ents;
+      unit_of(u, dnext, item, h, kt, ents, e0, n);
       const int row_base = item * s;
       const int kvb = kvi % L::kKV;
       mbar_wait(kv_empty + kvb, ((kvi / L::kKV) & 1) ^ 1);
@@ -1041,43 +1087,24 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       for (int e = 0; e < n; ++e, ++g) {
         const int st = g % L::kSt;
         mbar_wait(qd_empty + st, ((g / L::kSt) & 1) ^ 1);
-        const int32_t* ent = tv.csc + (size_t)(e0 + e) * kEntryInts;
+        const int32_t* ent = ents + (size_t)(e0 + e) * kEntryInts;
         if (lane == 0) {
+          // entry mask, Q / dO tiles and the gathered rows' lse / delta, all landing on qd_full[st]
+          sMask[st] = ent_mask(ent);
           uint8_t* sq = sm + L::kOffRing + st * 2 * L::kT;
-          mbar_arrive_expect_tx(qd_full + st, 2 * L::kT);
+          mbar_arrive_expect_tx(qd_full + st, 2 * L::kT + 2 * kAT * 4);
           for (int a = 0; a < A; ++a) {
             tma_load_gather(sq + a * kAT * 128, &tm_g, qd_full + st, h * HD + a * 64, row_base, ent, gu, nsub);
             tma_load_gather(sq + L::kT + a * kAT * 128, &tm_do_g, qd_full + st, h * HD + a * 64, row_base, ent, gu, nsub);
           }
+          for (int k = 0; k < nsub; ++k) {  // gathered query units lie inside the item
+            const int q0 = __ldg(ent + 2 + k) * gu;
+            bulk_load_1d(sL + st * kAT + k * gu, lse_b + q0, gu * 4, qd_full + st);
+            bulk_load_1d(sD + st * kAT + k * gu, del_b + q0, gu * 4, qd_full + st);
+          }
         }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int qi = lane * 4 + k, q = gathered_row(ent, qi, gu);  // gathered query units lie inside the item
-          sL[st * kAT + qi] = __ldg(lse_b + q) * 1.4426950408889634f;
-          sD[st * kAT + qi] = __ldg(del_b + q);
-        }
-        mbar_arrive(qd_full + st);
+        __syncwarp();
       }
-      // key column sums of this tile (keys < s) -> ksum[item, h, kt, :] for the dQ kernel's common-mode
-      // correction: lane l sums columns l, l + 32 (.. HD) over the tile's rows, off the critical path
-      mbar_wait(kv_full + kvb, (kvi / L::kKV) & 1);
-      const uint8_t* sk = sm + kvb * 2 * L::kT;
-      const int nrow = min(kAT, s - kt * kAT);
-#pragma unroll
-      for (int c0 = 0; c0 < HD; c0 += 32) {
-        const int col = c0 + lane;
-        const uint8_t* katom = sk + (col >> 6) * (kAT * 128);
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 8
-        for (int r = 0; r < kAT; ++r) {
-          const float v = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
-              katom + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4) + (col & 7) * 2));
-          acc[r & 3] += r < nrow ? v : 0.f;
-        }
-        ksum[(((size_t)item * H + h) * nkt + kt) * HD + col] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(kv_empty + kvb);
     }
   } else if (warp == 1) {
     // ================= MMA issuer
@@ -1086,13 +1113,14 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       const uint32_t id_g = make_idesc_bf16(kAT, HD, false, true);    // dV, dK: B MN-major
       int kvi = 0, g = 0, acc_i = 0;
       int use[2] = {0, 0};
+      int4 dnext = dload(blockIdx.x);
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++kvi, ++acc_i) {
         int item, h, kt, e0, n;
-        Tab128 tv;
-        unit_of(u, item, h, kt, tv, e0, n);
+        const int32_t* ents;
+        unit_of(u, dnext, item, h, kt, ents, e0, n);
         const int kvb = kvi % L::kKV;
         mbar_wait(kv_full + kvb, (kvi / L::kKV) & 1);
-        if (kvi == 0) trace_stamp(1);
+        if (kvi < 5) trace_stamp(2 + 5 * kvi);  // debug timeline: K/V landed (MMA view)
         const uint32_t sk = smem_u32(sm + kvb * 2 * L::kT), sv = sk + L::kT;
         auto issue_s = [&](int e) {  // S^T(e) = K Q(e)^T into buffer e & 1
           const int gg = g + e, st = gg % L::kSt;
@@ -1155,23 +1183,22 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
     const uint32_t tb = tmem + wg * kAT + lane_base;
     const int cj = kr >> 4;
     int kvi = 0, g = 0, acc_i = 0, use = 0;
+    int4 dnext = dload(blockIdx.x);
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++kvi, ++acc_i) {
       int item, h, kt, e0, n;
-      Tab128 tv;
-      unit_of(u, item, h, kt, tv, e0, n);
+      const int32_t* ents;
+      unit_of(u, dnext, item, h, kt, ents, e0, n);
       const int row_base = item * s;
       for (int e = wg; e < n; e += 2, ++use) {
         const int gg = g + e, st = gg % L::kSt;
-        const int32_t* ent = tv.csc + (size_t)(e0 + e) * kEntryInts;
-        const uint32_t lo = (uint32_t)__ldg(ent), hi = (uint32_t)__ldg(ent + 1);
-        const uint64_t mask = ((uint64_t)hi << 32) | lo;
-        const bool full = mask == ~0ull;
         const float* l2 = sL + st * kAT;
         const float* dl = sD + st * kAT;
-        mbar_wait(qd_full + st, (gg / L::kSt) & 1);  // lse / delta staged with the tiles
+        mbar_wait(qd_full + st, (gg / L::kSt) & 1);  // mask, lse / delta staged with the tiles
+        const uint64_t mask = sMask[st];
+        const bool full = mask == ~0ull;
         mbar_wait(s_full + wg, use & 1);
-        const bool tr = kvi == 0 && e < 4 && (ep_tid & 127) == 0;
-        if (tr) trace_stamp(2 + 4 * e);
+        const bool tr = kvi < 5 && e == 0 && ep_tid == 0;
+        if (tr) trace_stamp(3 + 5 * kvi);  // first entry's S ready
         tc_fence_after();
         uint32_t pp[4][16];  // P^T (bf16 pairs) for the whole row, reused by dS^T
 #pragma unroll
@@ -1186,8 +1213,8 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
 #pragma unroll
             for (int u2 = 0; u2 < 16; ++u2) {
               const int qi = c * 32 + 2 * u2;
-              const float p0 = ex2(fmaf(__uint_as_float(sv_[c2][2 * u2]), scale_log2, -l2[qi]));
-              const float p1 = ex2(fmaf(__uint_as_float(sv_[c2][2 * u2 + 1]), scale_log2, -l2[qi + 1]));
+              const float p0 = ex2(fmaf(__uint_as_float(sv_[c2][2 * u2]), scale_log2, -l2[qi] * 1.4426950408889634f));
+              const float p1 = ex2(fmaf(__uint_as_float(sv_[c2][2 * u2 + 1]), scale_log2, -l2[qi + 1] * 1.4426950408889634f));
               const bool on = full || ((mask >> ((qi >> 4) * 8 + cj)) & 1ull);
               pp[c][u2] = on ? pack_bf16x2(p0, p1) : 0u;
             }
@@ -1198,9 +1225,7 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_ready + wg);
-        if (tr) trace_stamp(3 + 4 * e);
         mbar_wait(dp_full + wg, use & 1);
-        if (tr) trace_stamp(4 + 4 * e);
         tc_fence_after();
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
@@ -1226,11 +1251,11 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(ds_ready + wg);
-        if (tr) trace_stamp(5 + 4 * e);
+        if (tr) trace_stamp(4 + 5 * kvi);  // first entry's dS stored
       }
       // ---- unit epilogue: WG0 stores dK (scaled), WG1 dV; then the key tile's column sums
       mbar_wait(acc_full, acc_i & 1);
-      if (kvi == 0 && ep_tid == 0) trace_stamp(18);
+      if (kvi < 5 && (ep_tid & 127) == 0) trace_stamp(5 + 5 * kvi);  // dK/dV accumulated (draining WG view)
       tc_fence_after();
       // dK / dV rows -> bf16 through a per-warp staging tile, stored as full 128-byte row segments
       const uint32_t tcol = (wg == 0 ? t_dk : t_dv) + lane_base;
@@ -1269,8 +1294,7 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       tc_fence_before();
       asm volatile("bar.sync 1, 256;" ::: "memory");  // every epilogue thread has drained TMEM
       if (ep_tid == 0) {
-        if (kvi == 0) trace_stamp(19);
-        if (kvi == 1) trace_stamp(20);
+        if (kvi < 5) trace_stamp(6 + 5 * kvi);  // drained
         mbar_arrive(acc_empty);
       }
       g += n;
@@ -1310,7 +1334,7 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
                     const __grid_constant__ CUtensorMap tm_g, int gu, int s, int H,
                     int n_units, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                     float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
-                    __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ ksum) {
+                    __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ kbar_g, const int4* __restrict__ desc) {
   using L = AttnDqPP<HD>;
   constexpr int A = HD / 64;
   const int d_model = H * HD;
@@ -1329,6 +1353,7 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
   uint64_t* acc_full = bars + 20;
   uint64_t* acc_empty = bars + 21;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  uint64_t* sMask = bars + 32;    // [kSt] cell mask of the staged K/V entry
   float* kbar = reinterpret_cast<float*>(sm + L::kOffMisc);
   float* eps_x = kbar + 128;  // [2][128]
 
@@ -1363,23 +1388,29 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_dq = tmem + 2 * kAT;
 
-  auto unit_of = [&](int u, int& item, int& h, int& qt, Tab128& tv, int& e0, int& n) {
+  // unit -> (item, h, qt) and its CSR range from the prep kernel's descriptors, read one unit ahead
+  const int tab_nt = __ldg(tables), tab_per = __ldg(tables + 6);
+  auto dload = [&](int u) { return u < n_units ? __ldg(desc + u) : make_int4(0, 0, 0, 0); };
+  auto unit_of = [&](int u, int4& dnext, int& item, int& h, int& qt, const int32_t*& ents, int& e0, int& n) {
+    const int4 dd = dnext;
+    dnext = dload(u + gridDim.x);
     qt = u % nqt;
     h = (u / nqt) % H;
     item = u / (nqt * H);
-    tv = tab128(tables, __ldg(pidx + item * item_stride + h));
-    e0 = __ldg(tv.row_ptr + qt);
-    n = __ldg(tv.row_ptr + qt + 1) - e0;
+    e0 = dd.x;
+    n = dd.y;
+    ents = desc_entries(tables, tab_nt, tab_per, dd.z, false);
   };
 
   if (warp == 0) {
     // ================= producer: Q/dO per unit, then the unit's K/V tiles
     if (lane == 0) {
       int qi_ = 0, g = 0;
+      int4 dnext = dload(blockIdx.x);
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++qi_) {
         int item, h, qt, e0, n;
-        Tab128 tv;
-        unit_of(u, item, h, qt, tv, e0, n);
+        const int32_t* ents;
+        unit_of(u, dnext, item, h, qt, ents, e0, n);
         const int row_base = item * s;
         const int qb = qi_ % L::kQB;
         mbar_wait(q_empty + qb, ((qi_ / L::kQB) & 1) ^ 1);
@@ -1392,8 +1423,9 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
         for (int e = 0; e < n; ++e, ++g) {
           const int st = g % L::kSt;
           mbar_wait(kv_empty + st, ((g / L::kSt) & 1) ^ 1);
-          const int32_t* ent = tv.csr + (size_t)(e0 + e) * kEntryInts;
+          const int32_t* ent = ents + (size_t)(e0 + e) * kEntryInts;
           uint8_t* skv = sm + L::kOffRing + st * 2 * L::kT;
+          sMask[st] = ent_mask(ent);  // released to the epilogue by the arrive below
           mbar_arrive_expect_tx(kv_full + st, 2 * L::kT);
           for (int a = 0; a < A; ++a) {
             tma_load_gather(skv + a * kAT * 128, &tm_g, kv_full + st, d_model + h * HD + a * 64, row_base, ent, gu, kAT / gu);
@@ -1410,10 +1442,11 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
       const uint32_t id_g = make_idesc_bf16(kAT, HD, false, true);
       int qi_ = 0, g = 0, acc_i = 0;
       int use[2] = {0, 0};
+      int4 dnext = dload(blockIdx.x);
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++qi_, ++acc_i) {
         int item, h, qt, e0, n;
-        Tab128 tv;
-        unit_of(u, item, h, qt, tv, e0, n);
+        const int32_t* ents;
+        unit_of(u, dnext, item, h, qt, ents, e0, n);
         const int qb = qi_ % L::kQB;
         mbar_wait(q_full + qb, (qi_ / L::kQB) & 1);
         const uint32_t sq = smem_u32(sm + qb * 2 * L::kT), sdo = sq + L::kT;
@@ -1475,20 +1508,31 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
     const uint32_t tb = tmem + wg * kAT + lane_base;
     const int ci = r >> 4;
     uint8_t* stg = sm + L::kOffStg + (warp - 2) * 32 * L::kStgPitch;
-    int acc_i = 0, use = 0;
+    int acc_i = 0, use = 0, g = 0;
+    int4 dnext = dload(blockIdx.x);
+    // this thread's row terms (lse, delta) and kbar component of a unit: loaded one unit ahead
+    float l2n = 0.f, dln = 0.f, kbn = 0.f;
+    auto row_terms = [&](int u) {
+      if (u >= n_units) return;
+      const int qt_ = u % nqt, h_ = (u / nqt) % H, it_ = u / (nqt * H), row_ = qt_ * kAT + r;
+      const size_t lr = ((size_t)it_ * H + h_) * s + (row_ < s ? row_ : 0);
+      l2n = __ldg(lse + lr);
+      dln = __ldg(delta + lr);
+      if (r < HD) kbn = __ldg(kbar_g + ((size_t)it_ * H + h_) * HD + r);
+    };
+    row_terms(blockIdx.x);
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++acc_i) {
       int item, h, qt, e0, n;
-      Tab128 tv;
-      unit_of(u, item, h, qt, tv, e0, n);
+      const int32_t* ents;
+      unit_of(u, dnext, item, h, qt, ents, e0, n);
       const int row_base = item * s;
-      const int row = qt * kAT + r;
-      const size_t lrow = ((size_t)item * H + h) * s + (row < s ? row : 0);
-      const float l2 = __ldg(lse + lrow) * 1.4426950408889634f, dl = __ldg(delta + lrow);
+      const float l2 = l2n * 1.4426950408889634f, dl = dln, kb = kbn;
+      row_terms(u + gridDim.x);
       float eps = 0.f;
       for (int e = wg; e < n; e += 2, ++use) {
-        const int32_t* ent = tv.csr + (size_t)(e0 + e) * kEntryInts;
-        const uint32_t lo = (uint32_t)__ldg(ent), hi = (uint32_t)__ldg(ent + 1);
-        const uint32_t mrow = (uint32_t)((((uint64_t)hi << 32) | lo) >> (ci * 8)) & 0xffu;
+        const int gg = g + e, st = gg % L::kSt;
+        mbar_wait(kv_full + st, (gg / L::kSt) & 1);  // the entry's mask was staged with its K/V tiles
+        const uint32_t mrow = (uint32_t)(sMask[st] >> (ci * 8)) & 0xffu;
         mbar_wait(s_full + wg, use & 1);
         tc_fence_after();
         uint32_t pp[4][16];
@@ -1544,12 +1588,7 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
       // ---- unit epilogue: eps of both warpgroups (fixed order), key mean kbar, dQ rows (WG w: columns
       // [w HD/2, (w+1) HD/2)) through the staging tile as 64-byte row segments
       eps_x[wg * 128 + r] = eps;
-      if (wg == 0 && r < HD) {
-        const float* ks = ksum + ((size_t)item * H + h) * ((s + kAT - 1) / kAT) * HD + r;
-        float acc = 0.f;
-        for (int t = 0; t < (s + kAT - 1) / kAT; ++t) acc += __ldg(ks + t * HD);
-        kbar[r] = acc / (float)s;
-      }
+      if (wg == 0 && r < HD) kbar[r] = kb;  // mean key of (item, h), bsattn_prep_kernel
       mbar_wait(acc_full, acc_i & 1);
       asm volatile("bar.sync 1, 256;" ::: "memory");
       tc_fence_after();
@@ -1583,6 +1622,7 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
       tc_fence_before();
       asm volatile("bar.sync 1, 256;" ::: "memory");  // TMEM drained, eps_x / kbar reusable
       if (ep_tid == 0) mbar_arrive(acc_empty);
+      g += n;
     }
   }
   tc_fence_before();
@@ -1596,13 +1636,20 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
 template <int HD>
 static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                          int H, const int32_t* pidx, int item_stride, const int32_t* tables128, int gu, float scale,
-                         const float* lse, float* delta, float* ksum, uint16_t* dqkv, cudaStream_t st) {
+                         const float* lse, float* delta, float* ws, uint16_t* dqkv, cudaStream_t st) {
   const int rows = n_items * s;
   LX_REQUIRE(ld_o % 8 == 0, LX_ERR_SHAPE, "attention bwd: O / dO row stride must be a multiple of 8");
-  launch_k(bsattn_delta_tc_kernel<HD>, (rows * 32 + 255) / 256, 256, 0, st, reinterpret_cast<const __nv_bfloat16*>(o),
-                                                                      reinterpret_cast<const __nv_bfloat16*>(d_o), ld_o,
-                                                                      rows, s, H, delta);
-  int rc = launch_check("bsattn_delta_tc");
+  const int nt = (s + kAT - 1) / kAT;
+  const int n_units = nt * H * n_items;
+  // ws: kbar [n_items * H * HD] floats, then the dK/dV and dQ unit descriptors (int4 [n_units] each)
+  float* kbar = ws;
+  int4* desc_kv = reinterpret_cast<int4*>(ws + (size_t)n_items * H * HD);
+  int4* desc_q = desc_kv + n_units;
+  const int nb_delta = (rows * 32 + 255) / 256, nb_kbar = n_items * H, nb_desc = (n_units + 255) / 256;
+  launch_k(bsattn_prep_kernel<HD>, nb_delta + nb_kbar + nb_desc, 256, 0, st, reinterpret_cast<const __nv_bfloat16*>(o),
+           reinterpret_cast<const __nv_bfloat16*>(d_o), ld_o, rows, s, H, delta, reinterpret_cast<const __nv_bfloat16*>(qkv), ld,
+           kbar, pidx, item_stride, tables128, desc_kv, desc_q, n_units, nb_delta, nb_kbar);
+  int rc = launch_check("bsattn_prep");
   if (rc) return rc;
   CUtensorMap tm_qkv, tm_do, tm_g, tm_do_g;
   if ((rc = make_tmap_bf16_2d(&tm_qkv, qkv, ld, (uint64_t)rows, ld, 64, kAT))) return rc;
@@ -1614,35 +1661,32 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
   static cudaError_t a2 = cudaFuncSetAttribute(bsattn_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   LX_CHECK_CUDA(a1);
   LX_CHECK_CUDA(a2);
-  dim3 grid((s + kAT - 1) / kAT, H, n_items);
+  dim3 grid(nt, H, n_items);
   const float sl2 = scale * 1.4426950408889634f;
-  // the ping-pong kernel's ring + staging fit in shared memory for HD 64; HD 128 keeps the 2-CTA kernel
+  // the ping-pong kernels' rings + staging fit in shared memory for HD 64; HD 128 keeps the 2-CTA kernels
   static const bool old_bwd = getenv("LX_ATTN_BWD_OLD") != nullptr || AttnDkdvPP<HD>::kTotal > 227 * 1024;
   if (old_bwd) {
-    launch_k(bsattn_dkdv_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, tm_g, tm_do_g, gu, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
-                                                     lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);
+    launch_k(bsattn_dkdv_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, tm_g, tm_do_g, gu, s, H, H * HD, pidx, item_stride,
+             tables128, scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d);
   } else {
     constexpr int smem_pp = AttnDkdvPP<HD>::kTotal;
     static cudaError_t a3 = cudaFuncSetAttribute(bsattn_dkdv_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pp);
     LX_CHECK_CUDA(a3);
-    const int n_units = (int)grid.x * H * n_items;
     launch_k(bsattn_dkdv_pp_kernel<HD>, std::min(n_units, num_sms()), kBwdThreads, smem_pp, st, tm_qkv, tm_do, tm_g, tm_do_g,
-             gu, s, H,
-             n_units, pidx, item_stride, tables128, scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d,
-             ksum);
+             gu, s, H, n_units, pidx, item_stride, tables128, scale, sl2, lse, delta,
+             reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, (const int4*)desc_kv);
   }
   if ((rc = launch_check("bsattn_dkdv_tc"))) return rc;
   if (old_bwd || AttnDqPP<HD>::kTotal > 227 * 1024) {
-    launch_k(bsattn_dq_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, tm_g, gu, s, H, H * HD, pidx, item_stride, tables128, scale, sl2,
-                                                   lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, ksum);
+    launch_k(bsattn_dq_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, tm_g, gu, s, H, H * HD, pidx, item_stride, tables128,
+             scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, (const float*)kbar);
   } else {
     constexpr int smem_dq = AttnDqPP<HD>::kTotal;
     static cudaError_t a4 = cudaFuncSetAttribute(bsattn_dq_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_dq);
     LX_CHECK_CUDA(a4);
-    const int n_units = (int)grid.x * H * n_items;
     launch_k(bsattn_dq_pp_kernel<HD>, std::min(n_units, num_sms()), kBwdThreads, smem_dq, st, tm_qkv, tm_do, tm_g, gu, s, H,
              n_units, pidx, item_stride, tables128, scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d,
-             ksum);
+             (const float*)kbar, (const int4*)desc_q);
   }
   return launch_check("bsattn_dq_tc");
 }
@@ -1662,15 +1706,15 @@ int lx_debug_set_attn_trace(unsigned long long* buf) {
 
 int lx_bsattn_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items,
                      int s, int H, int hd, const int32_t* pattern_idx, int item_stride, const int32_t* tables128,
-                     int gather_rows, float scale, const float* lse, float* delta_ws, float* ksum_ws, uint16_t* dqkv,
+                     int gather_rows, float scale, const float* lse, float* delta_ws, float* ws, uint16_t* dqkv,
                      lx_stream_t stream) {
   LX_REQUIRE(gather_rows >= 16 && gather_rows <= 128 && (gather_rows & (gather_rows - 1)) == 0, LX_ERR_LAYOUT,
              "attention bwd: gather_rows %d must be a power of two in [16, 128]", gather_rows);
   LX_REQUIRE(ld >= 3 * H * hd && ld_d >= 3 * H * hd && ld % 8 == 0 && ld_d % 8 == 0 && ld_o % 8 == 0, LX_ERR_SHAPE,
              "attention bwd (tcgen05): qkv / dqkv must be fused [M, >= 3*H*hd] with 16B-aligned rows");
   switch (hd) {
-    case 64: return launch_bwd_tc<64>(qkv, ld, ld_d, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, gather_rows, scale, lse, delta_ws, ksum_ws, dqkv, stream);
-    case 128: return launch_bwd_tc<128>(qkv, ld, ld_d, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, gather_rows, scale, lse, delta_ws, ksum_ws, dqkv, stream);
+    case 64: return launch_bwd_tc<64>(qkv, ld, ld_d, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, gather_rows, scale, lse, delta_ws, ws, dqkv, stream);
+    case 128: return launch_bwd_tc<128>(qkv, ld, ld_d, o, d_o, ld_o, n_items, s, H, pattern_idx, item_stride, tables128, gather_rows, scale, lse, delta_ws, ws, dqkv, stream);
     default: LX_REQUIRE(false, LX_ERR_UNSUPPORTED, "tcgen05 attention: head_dim %d unsupported (64, 128)", hd);
   }
 }

@@ -52,6 +52,18 @@ LX_DEV void mbar_arrive(uint64_t* bar) {
 #ifndef LX_MBAR_SUSPEND_NS
 #define LX_MBAR_SUSPEND_NS 0x989680u
 #endif
+// non-blocking: has the phase with this parity completed?
+LX_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 LX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 #if LX_MBAR_SPIN
   // pure polling: the waiter resumes the cycle the phase flips (no suspend/wake latency)
@@ -93,6 +105,13 @@ LX_DEV void tma_load_2d_hint(void* smem_dst, const void* desc, uint64_t* bar, in
           smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(hint)
       : "memory");
+}
+// 1D bulk copy global -> shared (16 B aligned, bytes % 16 == 0), completing `bytes` on the mbarrier.
+LX_DEV void bulk_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 // Dynamic shared memory rounded up to 1024 B (SWIZZLE_128B atoms) by integer offset, so the
 // result stays a shared-space pointer (a uintptr_t round-trip would turn every access generic).
