@@ -48,9 +48,12 @@ int lx_debug_set_gemm_trace(unsigned long long* buf);
 
 /* ------------------------------------------------------------------ generic
  * C[M,N] (fp32 or bf16) = A[M,K] * B[N,K]^T, bf16 inputs, tcgen05 path.
- * Used by the predictor projections and by tests of the GEMM engine. */
+ * a_k_split > 0 (a multiple of 64): A's K coordinate k maps to k - a_k_split for k >= a_k_split, so with
+ * B = [W_hi | W_lo] (bf16 hi/lo split of an fp32 W, segments a_k_split wide) one GEMM returns A (W_hi + W_lo),
+ * i.e. the product with W at ~2^-16 relative precision. Used by the predictor projections (split terms) and
+ * by tests of the GEMM engine. */
 int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void* c, int ldc, int c_is_f32, int M, int N,
-                    int K, lx_stream_t stream);
+                    int K, int a_k_split, lx_stream_t stream);
 
 /* lora_linear_forward / lora_linear_backward's dense products (sf/model.py:292-304,
  * sf/autograd.py:48-58) with the bias, LoRA and residual fused in the epilogue:
@@ -64,14 +67,20 @@ int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, i
  * approx_mlp_scores + predict_mlp_mask + active_columns
  *   (sf/predictor.py:121-139, sf/neuron_ops.py:67-72)
  * h:      bf16 [n_items*s, d] post-LN2 MLP input (one item = one sequence)
- * wa_t:   bf16 [n_blk, d]  (Wa_hat transposed: each block's scoring vector contiguous)
+ * wa_t:   bf16 [n_blk, k_terms*d]  (Wa_hat transposed: each block's scoring vector contiguous)
+ * k_terms: precision of S_hat = h Wa_hat (the reference computes it in float32, sf/predictor.py:121-125):
+ *          1: wa_t = bf16(W) (bf16 scores);
+ *          2: wa_t = [W_hi | W_lo] (bf16 hi/lo split of the fp32 weights): h W exact to ~2^-16 for a bf16 h
+ *             (the fine-tune step: h is the bf16 LN output);
+ *          3: h = [x_hi | x_lo] bf16 [n_items*s, 2d] and wa_t = [W_hi | W_lo | W_hi]: an fp32 x and fp32 W
+ *             (the reference-API call on host float32 inputs). Split terms need d % 64 == 0.
  * scope_batch: 0 = per-item masks (sf/harness.py:204-211), 1 = OR over items (sf/predictor.py:132-136)
  * bits_ws: uint32 [n_items, ceil(n_blk/32)] workspace
  * counts: int32 [n_items]; ids: int32 [n_items, n_blk] ascending active block ids;
  * pos:    int32 [n_items, n_blk] packed position of each block or -1
  * scores_dump: optional fp32 [n_items*s, n_blk] copy of S_hat (parity tests) */
-int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint16_t* wa_t, int n_blk, float threshold,
-                        int scope_batch, uint32_t* bits_ws, int32_t* counts, int32_t* ids, int32_t* pos,
+int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint16_t* wa_t, int n_blk, int k_terms,
+                        float threshold, int scope_batch, uint32_t* bits_ws, int32_t* counts, int32_t* ids, int32_t* pos,
                         float* scores_dump, lx_stream_t stream);
 
 /* Compaction only: bitmask words -> counts/ids/pos (used when masks come from a provider). */
@@ -81,12 +90,14 @@ int lx_mask_compact(const uint32_t* bits, int n_items, int n_blk, int scope_batc
 /* predict_attention_patterns + select_pattern_by_coverage
  *   (sf/predictor.py:62-118, sf/exposer.py:71-85)
  * x_small: bf16 [n_items*m, d] downsampled rows (m = ceil(sqrt(s)), rows min(i*s//m, s-1))
- * wqk_t:   bf16 [2*H*r, d]: rows [h*r,(h+1)*r) = Wq_hat[h]^T, rows [(H+h)*r, ...) = Wk_hat[h]^T
+ *          ([x_hi | x_lo] [n_items*m, 2d] for k_terms 3)
+ * wqk_t:   bf16 [2*H*r, k_terms*d]: rows [h*r,(h+1)*r) = Wq_hat[h]^T, rows [(H+h)*r, ...) = Wk_hat[h]^T,
+ *          as k_terms bf16 segments (see lx_predict_mlp_mask: 2 = [W_hi | W_lo], 3 = [W_hi | W_lo | W_hi])
  * pool_kind/pool_param: pool in reference order (kind 0 blockdiag,1 band,2 causal,3 global,4 strided,5 dense)
  * proj_ws: fp32 [n_items*m, 2*H*r] workspace; pattern_idx: int32 [n_items(or 1), H] pool index
  * scores_dump: optional fp32 [n_items, H, m, m] */
 int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, int d, const uint16_t* wqk_t, int H,
-                                  int r, float threshold_frac, double tau, int n_b, const int32_t* pool_kind,
+                                  int r, int k_terms, float threshold_frac, double tau, int n_b, const int32_t* pool_kind,
                                   const int32_t* pool_param, int n_pool, int scope_batch, float* proj_ws,
                                   int32_t* pattern_idx, float* scores_dump, lx_stream_t stream);
 

@@ -175,11 +175,14 @@ int lx_gemm_set_cta_pair(int mode) {
 }
 
 int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void* c, int ldc, int c_is_f32, int M, int N,
-                    int K, lx_stream_t stream) {
+                    int K, int a_k_split, lx_stream_t stream) {
   LX_REQUIRE(M > 0 && N > 0 && K > 0, LX_ERR_SHAPE, "gemm: empty shape");
+  LX_REQUIRE(a_k_split >= 0 && a_k_split % kBK == 0 && a_k_split < K, LX_ERR_SHAPE,
+             "gemm: a_k_split %d must be a multiple of %d below K", a_k_split, kBK);
   CUtensorMap ta, tb;
   int rc;
-  if ((rc = make_tmap_bf16_2d(&ta, a, K, M, lda, kBK, kBM))) return rc;
+  // with a K split, A spans K - a_k_split columns (its tail reads zero-filled past them)
+  if ((rc = make_tmap_bf16_2d(&ta, a, a_k_split ? K - a_k_split : K, M, lda, kBK, kBM))) return rc;
   CUtensorMap tb2, tb4;
   if ((rc = make_tmap_bf16_2d(&tb, b, K, N, ldb, kBK, 256))) return rc;
   if ((rc = make_tmap_bf16_2d(&tb2, b, K, N, ldb, kBK, 128))) return rc;
@@ -187,6 +190,7 @@ int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void
   GemmArgs args = base_args(1, M, N, K);
   args.out = c;
   args.ldo = ldc;
+  args.a_k_split = a_k_split;
   // under-filled single-CTA problems (e.g. the predictor projection, M = B*m = 184): 128-wide tiles
   const long long tiles256 = (long long)((M + kBM - 1) / kBM) * ((N + 255) / 256);
   if (g_cta_pair == 0 && tiles256 < num_sms())

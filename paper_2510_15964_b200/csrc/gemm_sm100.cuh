@@ -94,6 +94,8 @@ struct GemmArgs {
   int out_f32;          // store fp32 instead of bf16 (any epilogue except kEpiMask)
   const float* resid;   // fp32 [rows, ldo]: out = resid + value (fused residual add; requires out_f32)
   int packed_stride;    // kPacked*: rows per item in the packed weight copy
+  int a_k_split;        // kDense: A's K coordinate is k - a_k_split for k >= a_k_split (0: off). With B =
+                        // [W_hi | W_lo] (segments a_k_split wide) one GEMM computes A W_hi + A W_lo.
 };
 
 constexpr int kStgPitch = 80;  // bytes per staged row: 64 B of bf16 + 16 B pad (conflict-free 16 B writes)
@@ -266,7 +268,8 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           else if (BMODE == kNGather) bytes += nb_n * args.blk * kBK * 2;
           else bytes += nb_k * (BN / 64) * args.blk * 128;
           mbar_arrive_expect_tx(full + stage, bytes);
-          tma_load_2d(sa, &tmap_a, full + stage, ks * kBK, row0);
+          const int ak = (BMODE == kDense && args.a_k_split && ks * kBK >= args.a_k_split) ? ks * kBK - args.a_k_split : ks * kBK;
+          tma_load_2d(sa, &tmap_a, full + stage, ak, row0);
           if (BMODE == kDense) tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.n0, pol_w);
           if (BMODE == kPackedN)  // rows [nt*BN, nt*BN+BN) of this item's packed copy, one box
             tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.item * args.packed_stride + ti.n0, pol_w);

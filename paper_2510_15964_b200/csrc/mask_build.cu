@@ -251,10 +251,12 @@ int lx_mask_compact(const uint32_t* bits, int n_items, int n_blk, int scope_batc
   return launch_check("mask_compact");
 }
 
-int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint16_t* wa_t, int n_blk, float threshold,
-                        int scope_batch, uint32_t* bits_ws, int32_t* counts, int32_t* ids, int32_t* pos,
+int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint16_t* wa_t, int n_blk, int k_terms,
+                        float threshold, int scope_batch, uint32_t* bits_ws, int32_t* counts, int32_t* ids, int32_t* pos,
                         float* scores_dump, lx_stream_t stream) {
   LX_REQUIRE(n_items >= 1 && s >= 1 && d >= 1 && n_blk >= 1, LX_ERR_SHAPE, "predict_mlp_mask: empty shape");
+  LX_REQUIRE(k_terms >= 1 && k_terms <= 3 && (k_terms == 1 || d % kBK == 0), LX_ERR_SHAPE,
+             "predict_mlp_mask: k_terms %d (1..3; split terms need d %% %d == 0)", k_terms, kBK);
   LX_REQUIRE(n_items <= kMaxItems, LX_ERR_UNSUPPORTED, "too many items");
   const int words = (n_blk + 31) / 32;
   LX_CHECK_CUDA(cudaMemsetAsync(bits_ws, 0, sizeof(uint32_t) * n_items * words, stream));
@@ -263,14 +265,17 @@ int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint
   const int bn = tiles256 < num_sms() ? 128 : 256;
   CUtensorMap ta, tb;
   int rc;
-  if ((rc = make_tmap_bf16_2d(&ta, h, d, (uint64_t)n_items * s, d, kBK, kBM))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, wa_t, d, n_blk, d, kBK, bn))) return rc;
+  // k_terms 2: h [M, d] x [W_hi | W_lo]; 3: [x_hi | x_lo] [M, 2d] x [W_hi | W_lo | W_hi] (A's K wraps at d)
+  const int a_cols = k_terms == 3 ? 2 * d : d, kt = k_terms * d;
+  if ((rc = make_tmap_bf16_2d(&ta, h, a_cols, (uint64_t)n_items * s, a_cols, kBK, kBM))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, wa_t, kt, n_blk, kt, kBK, bn))) return rc;
   GemmArgs args;
   memset(&args, 0, sizeof(args));
   args.n_items = n_items;
   args.rows_per_item = s;
   args.n_dense = n_blk;
-  args.k_dense = d;
+  args.k_dense = kt;
+  args.a_k_split = k_terms > 1 ? d : 0;
   args.blk = 16;
   args.out = scores_dump;
   args.ldo = n_blk;
@@ -296,13 +301,17 @@ int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint
 }
 
 int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, int d, const uint16_t* wqk_t, int H,
-                                  int r, float threshold_frac, double tau, int n_b, const int32_t* pool_kind,
+                                  int r, int k_terms, float threshold_frac, double tau, int n_b, const int32_t* pool_kind,
                                   const int32_t* pool_param, int n_pool, int scope_batch, float* proj_ws,
                                   int32_t* pattern_idx, float* scores_dump, lx_stream_t stream) {
   LX_REQUIRE(m >= 1 && m <= kMaxM, LX_ERR_UNSUPPORTED, "downsampled length m=%d outside [1, %d] (s <= 4096)", m, kMaxM);
   LX_REQUIRE(n_pool >= 1 && n_pool <= kMaxPool, LX_ERR_PATTERN, "pool size %d outside [1, %d]", n_pool, kMaxPool);
   LX_REQUIRE(tau > 0 && tau <= 1, LX_ERR_SHAPE, "coverage tau must be in (0, 1]");
-  int rc = lx_gemm_bf16_tn(x_small, d, wqk_t, d, proj_ws, 2 * H * r, 1, n_items * m, 2 * H * r, d, stream);
+  LX_REQUIRE(k_terms >= 1 && k_terms <= 3 && (k_terms == 1 || d % 64 == 0), LX_ERR_SHAPE,
+             "predict_attention_patterns: k_terms %d (1..3; split terms need d %% 64 == 0)", k_terms);
+  // k_terms 2: x_small [M, d] x [W_hi | W_lo]; 3: [x_hi | x_lo] [M, 2d] x [W_hi | W_lo | W_hi]
+  int rc = lx_gemm_bf16_tn(x_small, k_terms == 3 ? 2 * d : d, wqk_t, k_terms * d, proj_ws, 2 * H * r, 1, n_items * m,
+                           2 * H * r, k_terms * d, k_terms > 1 ? d : 0, stream);
   if (rc) return rc;
   dim3 grid(H, scope_batch ? 1 : n_items);
   const size_t smem = sizeof(float) * 2 * m * (r + 4);

@@ -99,6 +99,7 @@ class PredictedProvider(_TimedProvider):
         B, s, d = h.shape
         params = self.predictors["mlp"][layer]
         nm, _ = P.mlp_masks(h.reshape(B * s, d), B, s, params, self.pcfg.mlp_threshold, self.model.dims.blk_size,
+                            terms=self.pcfg.score_terms,
                             scope_batch=self.scope_batch)
         if self.counter is not None:
             self.counter.add(B * (s * d * self.model.dims.n_blk + s))

@@ -41,7 +41,7 @@ def test_dense_gemm(M, N, K, f32, engine):
     a = torch.randn(M, K, generator=g).to(dev, torch.bfloat16)
     b = torch.randn(N, K, generator=g).to(dev, torch.bfloat16)
     c = torch.empty(M, N, device=dev, dtype=torch.float32 if f32 else torch.bfloat16)
-    _abi.call("lx_gemm_bf16_tn", a.data_ptr(), K, b.data_ptr(), K, c.data_ptr(), N, int(f32), M, N, K, _abi.stream_handle())
+    _abi.call("lx_gemm_bf16_tn", a.data_ptr(), K, b.data_ptr(), K, c.data_ptr(), N, int(f32), M, N, K, 0, _abi.stream_handle())
     ref = a.float() @ b.float().T
     torch.cuda.synchronize()
     assert rel(c, ref) < (2e-3 if f32 else 1e-2)

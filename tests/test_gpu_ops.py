@@ -47,8 +47,8 @@ def test_mlp_mask_bit_exact(dev, n_items, s, d, n_blk, thr, scope):
     nm, sc = P.mlp_masks(ht, n_items, s, P.MlpPredictorParams(wa), thr, 16, scope_batch=scope == "batch", dump=True)
     torch.cuda.synchronize()
     sc = sc.cpu().numpy()
-    # scores agree with fp32 math on the same bf16 operands
-    assert rel(sc, bf(h) @ bf(wa)) < 2e-3
+    # scores agree with float32 math on the bf16 input and the float32 weights (hi/lo split, k_terms 2)
+    assert rel(sc, bf(h).astype(np.float64) @ wa.astype(np.float64)) < 1e-4
     # mask logic bit-exact on identical scores (sf/predictor.py:128-139, sf/neuron_ops.py:67-72)
     per = [O.predict_mlp_mask([sc[b * s : (b + 1) * s]], thr) for b in range(n_items)]
     if scope == "batch":
@@ -87,11 +87,11 @@ def test_attention_patterns_bit_exact(dev, n_items, s, d, H, r, attn_blk, scope,
     ids = list(opool)
     ocfg = O.PredictorConfig()
     for h in range(H):
-        # scores vs fp32 math on bf16 operands
+        # scores vs float32 math on the bf16 downsampled rows and the float32 predictor weights (k_terms 2)
         for b in range(n_items):
-            x_s = bf(xb[b][O.downsample_indices(s)])
-            ref = (x_s @ bf(wq[h])) @ (x_s @ bf(wk[h])).T
-            assert rel(sc[b, h], ref) < 2e-3
+            x_s = bf(xb[b][O.downsample_indices(s)]).astype(np.float64)
+            ref = (x_s @ wq[h]) @ (x_s @ wk[h]).T
+            assert rel(sc[b, h], ref) < 1e-4
         if scope == "batch":
             active = None
             for b in range(n_items):
@@ -106,21 +106,36 @@ def test_attention_patterns_bit_exact(dev, n_items, s, d, H, r, attn_blk, scope,
 
 
 def test_predict_attention_patterns_golden(dev, golden):
-    """Reference-API call on the reference's own inputs (pap fixtures): pattern ids must match
-    the reference unless a score sits within bf16 rounding of the threshold."""
+    """Reference-API call on the reference's own float32 inputs (pap fixtures): the scores are computed at
+    float32 precision (x and the predictor weights as bf16 hi/lo pairs, k_terms 3), so every head's pattern id
+    must equal the reference's. A mismatch is allowed only for a documented tie: a score of that head within
+    1e-5 (relative to the map's peak) of the fp32 threshold frac * peak, where float32 accumulation order
+    alone decides the strict '>' (sf/predictor.py:87-90)."""
     from paper_2510_15964_b200 import patterns as PT, predictor as P
 
     g = golden("predictor")
-    agree = total = 0
+    ocfg = O.PredictorConfig()
+    total = exact = 0
     for c in range(6):
         nx, n_b = (int(v) for v in g[f"pap{c}/meta"])
-        params = P.AttnPredictorParams(list(g[f"pap{c}/wq"]), list(g[f"pap{c}/wk"]))
-        xb = torch.from_numpy(np.stack([g[f"pap{c}/x{j}"] for j in range(nx)])).to(dev)
+        wq, wk = list(g[f"pap{c}/wq"]), list(g[f"pap{c}/wk"])
+        params = P.AttnPredictorParams(wq, wk)
+        xs = [g[f"pap{c}/x{j}"] for j in range(nx)]
+        xb = torch.from_numpy(np.stack(xs)).to(dev)
         out = P.predict_attention_patterns(xb, params, PT.build_pool(n_b), P.PredictorTrainConfig())
         ref = list(g[f"pap{c}/out"])
-        agree += sum(a == b for a, b in zip(out, ref))
-        total += len(ref)
-    assert agree / total >= 0.8, (agree, total)
+        for h, (a, b) in enumerate(zip(out, ref)):
+            total += 1
+            if a == b:
+                exact += 1
+                continue
+            margins = []
+            for x in xs:
+                sc = O.approx_attention_scores(x[O.downsample_indices(x.shape[0])], wq[h], wk[h])
+                thr = np.float32(ocfg.attn_threshold_frac) * sc.max()
+                margins.append(np.abs(sc - thr).min() / np.abs(sc).max())
+            assert min(margins) < 1e-5, (c, h, a, b, min(margins))
+    assert exact >= total - 1, (exact, total)
 
 
 # ------------------------------------------------------------------ K3: block-sparse attention

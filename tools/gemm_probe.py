@@ -29,11 +29,11 @@ for _ in range(3):
               None, 0, 1.0, 1, out.data_ptr(), f, None, st)
     _abi.call("lx_neuron_fc2", a.data_ptr(), f, B, s, d, f, blk, w2.data_ptr(), counts.data_ptr(), ids.data_ptr(), None, None,
               None, 0, 1.0, o2.data_ptr(), 0, None, None, st)
-    _abi.call("lx_gemm_bf16_tn", x.data_ptr(), d, w1t.data_ptr(), d, out.data_ptr(), f, 0, B * s, f, d, st)
+    _abi.call("lx_gemm_bf16_tn", x.data_ptr(), d, w1t.data_ptr(), d, out.data_ptr(), f, 0, B * s, f, d, 0, st)
 torch.cuda.synchronize()
 for name, fn, flops in (("fc1", lambda: _abi.call("lx_neuron_fc1", x.data_ptr(), B, s, d, f, blk, w1t.data_ptr(), counts.data_ptr(), ids.data_ptr(), None, None, None, 0, 1.0, 1, out.data_ptr(), f, None, st), 2 * B * s * d * len(act) * blk),
                         ("fc2", lambda: _abi.call("lx_neuron_fc2", a.data_ptr(), f, B, s, d, f, blk, w2.data_ptr(), counts.data_ptr(), ids.data_ptr(), None, None, None, 0, 1.0, o2.data_ptr(), 0, None, None, st), 2 * B * s * d * len(act) * blk),
-                        ("dense", lambda: _abi.call("lx_gemm_bf16_tn", x.data_ptr(), d, w1t.data_ptr(), d, out.data_ptr(), f, 0, B * s, f, d, st), 2 * B * s * d * f)):
+                        ("dense", lambda: _abi.call("lx_gemm_bf16_tn", x.data_ptr(), d, w1t.data_ptr(), d, out.data_ptr(), f, 0, B * s, f, d, 0, st), 2 * B * s * d * f)):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(10):

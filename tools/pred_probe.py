@@ -27,7 +27,7 @@ def t(fn, reps=30, cold=True):
         a.record(); fn(); b.record(); b.synchronize(); ts.append(a.elapsed_time(b) * 1e3)
     return statistics.median(ts)
 st = _abi.stream_handle()
-gemm = lambda: _abi.call("lx_gemm_bf16_tn", xs.data_ptr(), d, w.data_ptr(), d, out.data_ptr(), 2 * H * r, 1, B * m, 2 * H * r, d, st)
+gemm = lambda: _abi.call("lx_gemm_bf16_tn", xs.data_ptr(), d, w.data_ptr(), d, out.data_ptr(), 2 * H * r, 1, B * m, 2 * H * r, d, 0, st)
 full = lambda: P.attn_pattern_idx(xs, B, m, params, pool, n_b, P.PredictorTrainConfig())
 ref = xs.float() @ w.float().t()
 gemm(); torch.cuda.synchronize()
