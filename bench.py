@@ -377,7 +377,7 @@ def run_ours(args, cfg, rank, world, dist):
 
     from paper_2510_15964_b200 import harness as HN
     from paper_2510_15964_b200.dense_baseline import DenseLoraStep
-    from paper_2510_15964_b200.dp import make_grad_hook, shard_range
+    from paper_2510_15964_b200.dp import BucketedGradSync, shard_range
     from paper_2510_15964_b200.engine import FinetuneEngine
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
@@ -388,8 +388,10 @@ def run_ours(args, cfg, rank, world, dist):
     B = b1 - b0
     model, state, provider = build_workload(cfg, dev, seed=args.seed, mlp_sparsity=args.mlp_sparsity,
                                             local_frac=args.local_frac, peft=args.peft)
-    hook = make_grad_hook(dist, G, rank, world) if dist is not None else None
-    eng = FinetuneEngine(model, state, provider, lr=1e-4, grad_hook=hook)
+    # the only collective: the flat trainable-gradient all-reduce, bucketed per layer group and overlapped with the
+    # backward on a communication stream (NCCL, captured in the step's CUDA graph)
+    sync = BucketedGradSync(dist, G, rank, world) if dist is not None else None
+    eng = FinetuneEngine(model, state, provider, lr=1e-4, grad_sync=sync)
     s, V = cfg["s"], cfg["V"]
     gen = torch.Generator().manual_seed(args.seed + 2)  # synthetic uniform tokens (sf/harness.py:391 seed + 2)
     batches = [torch.randint(0, V, (G, s + 1), generator=gen)[b0:b1].contiguous() for _ in range(max(args.steps, 1))]
@@ -422,9 +424,9 @@ def run_ours(args, cfg, rank, world, dist):
     roof, kernels = None, None
     if rank == 0:
         snap = StateSnapshot(state)  # rank-0-only probes below must not leave rank 0's state diverged
-        hook_saved, eng.grad_hook = eng.grad_hook, None
+        sync_saved, eng.grad_sync = eng.grad_sync, None  # rank-0-only probe step: no collective
         roof, kernels = kernel_probe(model, eng, tok_dev, peaks, args.config)
-        eng.grad_hook = hook_saved
+        eng.grad_sync = sync_saved
         if not args.skip_dense:
             # dense reference points on the same box: (a) same engine, every head/block dense; (b) torch cuBLAS/SDPA
             dprov = HN.DenseProvider(model)
@@ -475,8 +477,8 @@ def run_ours(args, cfg, rank, world, dist):
                    "injected": {"mlp_zeroed_predictor_blocks": args.mlp_sparsity,
                                 "calibrated_gram_attention_heads": args.local_frac},
                    "l2": f"inputs larger than L2: {frozen_gb:.1f} GB of frozen weights stream from HBM every step (no flush needed)",
-                   "timing": "CUDA events around K CUDA-graph replays (max over ranks); Adam (fp64 moments) and the "
-                             "gradient all-reduce outside the graph, inside the timed region"},
+                   "timing": "CUDA events around K CUDA-graph replays (max over ranks); the bucketed gradient all-reduce "
+                             "inside the graph, Adam (fp64 moments) after it, both inside the timed region"},
         "tokens_per_s": round(tokens_per_step / (ms * 1e-3), 1),
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms/batch", "h2d_bytes_per_step": int(G * (s + 1) * 8),
                 "d2h_bytes_per_step": 4 * world,

@@ -41,3 +41,58 @@ def make_grad_hook(dist, global_batch: int, rank: int, world: int, group=None):
         dist.all_reduce(flat_grad, group=group)
 
     return hook
+
+
+class BucketedGradSync:
+    """The same global-mean reduction as make_grad_hook, issued per layer group DURING the backward (§8(e)):
+    once a group's LoRA / BitFit column reductions have been written into the flat gradient buffer (the
+    engine's _CgBatch flush), that slice is scaled and all-reduced on a dedicated communication stream, so the
+    transfer overlaps the remaining layers' backward; `finish` reduces whatever the buckets did not cover and
+    makes the compute stream wait for the collectives (Adam reads every gradient). NCCL collectives on that
+    stream are captured into the engine's CUDA graph like its kernels. Deterministic: each element is reduced
+    exactly once with the same operands as the single all-reduce."""
+
+    def __init__(self, dist, global_batch: int, rank: int, world: int, group=None):
+        start, stop = shard_range(global_batch, rank, world)
+        self.w = (stop - start) / global_batch
+        self.dist, self.group = dist, group
+        self.stream = None
+        self.done: list[tuple[int, int]] = []
+
+    def begin(self) -> None:
+        self.done = []
+
+    def bucket(self, flat, lo: int, hi: int, producer_stream=None) -> None:
+        if hi <= lo:
+            return
+        if flat.is_cuda:
+            import torch
+
+            if self.stream is None:
+                self.stream = torch.cuda.Stream(device=flat.device)
+            self.stream.wait_stream(torch.cuda.current_stream(flat.device))
+            if producer_stream is not None:
+                self.stream.wait_stream(producer_stream)
+            with torch.cuda.stream(self.stream):
+                v = flat[lo:hi]
+                v.mul_(self.w)
+                self.dist.all_reduce(v, group=self.group)
+        else:
+            v = flat[lo:hi]
+            v.mul_(self.w)
+            self.dist.all_reduce(v, group=self.group)
+        self.done.append((lo, hi))
+
+    def finish(self, flat) -> None:
+        """Reduce the gaps between the issued buckets, then join the communication stream."""
+        n, pos = flat.numel(), 0
+        for lo, hi in sorted(self.done):
+            if lo > pos:
+                self.bucket(flat, pos, lo)
+            pos = max(pos, hi)
+        if pos < n:
+            self.bucket(flat, pos, n)
+        if flat.is_cuda and self.stream is not None:
+            import torch
+
+            torch.cuda.current_stream(flat.device).wait_stream(self.stream)

@@ -38,8 +38,12 @@ def lm_head_loss_and_grad(hf: torch.Tensor, emb: torch.Tensor, targets: torch.Te
 class FinetuneEngine:
     """Fused fine-tune step over a batch of B sequences of length s (tokens [B, s+1])."""
 
-    def __init__(self, model: M.Model, state: M.PeftState, provider, lr: float, loss_chunk: int = 0, grad_hook=None):
+    def __init__(self, model: M.Model, state: M.PeftState, provider, lr: float, loss_chunk: int = 0, grad_hook=None,
+                 grad_sync=None):
+        """grad_hook(flat): one in-place reduction of the flat mean-gradient buffer after the step (dp.make_grad_hook);
+        grad_sync: a dp.BucketedGradSync issuing that reduction per layer group during the backward instead."""
         self.model, self.state, self.provider, self.lr = model, state, provider, lr
+        self.grad_sync = grad_sync
         import os
 
         # LM-head row chunk: the fp32 logits of a chunk ([chunk, V]) should stay L2-resident between the
@@ -51,10 +55,14 @@ class FinetuneEngine:
         self.static_tokens = None
         self.static_loss = None
         self._grad_views = {}
+        self._layer_range = {}  # layer -> [lo, hi) of its trainables in the flat buffer (contiguous per layer)
         base = state.flat.data_ptr()
         for name, p in state.params.items():
             off = (p.data_ptr() - base) // 4
             self._grad_views[name] = self.flat_grad[off : off + p.numel()].view(p.shape)
+            layer = int(name.split(".")[1])
+            lo, hi = self._layer_range.get(layer, (off, off))
+            self._layer_range[layer] = (min(lo, off), max(hi, off + p.numel()))
         self.last_masks = None
         M.ensure_lora_packs(model)  # packed LoRA operands, refreshed at the start of every step
 
@@ -87,14 +95,27 @@ class FinetuneEngine:
         dh, dh_bf = AG.layernorm_backward(d_hf, cf, want_bf16=True)
         cg = None
         side = self._cg_stream()
+        sync = self.grad_sync
+        # buckets only where every trainable is written by the column reductions (LoRA, BitFit); the adapter's
+        # torch-op gradients are copied in at the end and reduced by finish()
+        bucketed = sync is not None and m.peft_method != "adapter"
+        if sync is not None:
+            sync.begin()
+        group = []
         for k, layer in enumerate(reversed(range(m.dims.n_layers))):
             cg = cg or AG._CgBatch(grads, B, s, stream=side)
             dh, dh_bf = AG.block_backward(dh, m, layer, caches[layer], None, grads, dh_bf, inplace=True, cg=cg)
+            group.append(layer)
             if k % AG.CG_LAYERS == AG.CG_LAYERS - 1:  # CG_LAYERS layers' column reductions per group launch
                 cg.flush()
                 cg = None
+                if bucketed:
+                    self._bucket(group, side)
+                group = []
         if cg is not None:
             cg.flush()
+            if bucketed:
+                self._bucket(group, side)
         if side is not None:
             torch.cuda.current_stream().wait_stream(side)  # join: Adam reads every gradient
         self.last_masks = [c["masks"] for c in caches]
@@ -104,11 +125,19 @@ class FinetuneEngine:
                 view.zero_()  # unreached trainables get zero gradients (sf/autograd.py:191-194)
             elif t is not view:
                 view.copy_(t).mul_(1.0 / B)  # gradients produced by torch ops (adapter path)
+        if sync is not None:
+            sync.finish(self.flat_grad)  # the rest, then the compute stream waits for the collectives
         return loss
 
+    def _bucket(self, layers, producer_stream) -> None:
+        rs = [self._layer_range[i] for i in layers if i in self._layer_range]
+        if rs:
+            self.grad_sync.bucket(self.flat_grad, min(r[0] for r in rs), max(r[1] for r in rs), producer_stream)
+
     def _finish(self) -> None:
-        """Data-parallel gradient reduction hook, then Adam (float64 moments, sf/autograd.py:203-225)."""
-        if self.grad_hook is not None:
+        """Data-parallel gradient reduction hook (unless bucketed inside the step), then Adam (float64 moments,
+        sf/autograd.py:203-225)."""
+        if self.grad_hook is not None and self.grad_sync is None:
             self.grad_hook(self.flat_grad)
         self.state.step += 1
         from . import _abi

@@ -313,3 +313,48 @@ def test_engine_side_stream_reductions_are_bit_identical(dev, monkeypatch):
         grads.append(eng.flat_grad.clone())
     assert torch.isfinite(grads[0]).all()
     assert torch.equal(grads[0], grads[1])
+
+
+def test_cfg1_end_to_end_predicted_mode(dev):
+    """BASELINE configs[0] end to end: OPT-125M shape (d 768, H 12, d_ff 3072, L 12, V 50272), B = 1, s = 256,
+    predicted mode with reference-initialised predictors (N(0, 0.1^2), sf/predictor.py:194-206) and the model
+    initialised by the reference's draw order (sf/model.py:174-231), LoRA-B perturbed as the reference's
+    autograd tests do. Device vs oracle on the device-chosen masks (sf/harness.py:401-417):
+      * logits and loss within 1e-2 of the float32 oracle;
+      * every layer's masks equal the oracle predictor's on the device's own predictor inputs (ties excepted);
+      * every LoRA gradient within 1e-2 of the bf16 rounding-point oracle given the device's masks and ReLU
+        decisions, and within 1e-1 of float32 (sanity)."""
+    from paper_2510_15964_b200 import autograd as AG, harness as HN, model as M, predictor as P
+
+    dims = O.Dims(768, 12, 3072, 256, 12, 50272, 16, 16)
+    om = O.build_model(dims, seed=0, peft="lora")
+    rng = O.make_rng(1)
+    for ad in om.lora.values():
+        ad["b"] += (rng.standard_normal(ad["b"].shape) * 0.02).astype(np.float32)
+    r_pred = max(4, dims.d_model // 16)
+    preds = {"attn": [P.AttnPredictorParams([O.randn(rng, (dims.d_model, r_pred), 0.1) for _ in range(dims.n_heads)],
+                                            [O.randn(rng, (dims.d_model, r_pred), 0.1) for _ in range(dims.n_heads)])
+                      for _ in range(dims.n_layers)],
+             "mlp": [P.MlpPredictorParams(O.randn(rng, (dims.d_model, dims.n_blk), 0.1)) for _ in range(dims.n_layers)]}
+    m = device_model(om, dev)
+    prov = HN.PredictedProvider(m, preds, P.PredictorTrainConfig())
+    toks = rng.integers(0, dims.vocab, size=dims.seq_len + 1)
+    logits, cache = M.model_forward(m, toks[None, :-1], prov)
+    grads = AG.model_backward(m, cache, M.loss_backward(logits, toks[None, 1:]))
+    ids = list(m.pool)
+    ref = predictor_masks_on_device_inputs(cache, preds, om.pool, 0)
+    masks = []
+    for i, c in enumerate(cache["blocks"]):
+        pid = [ids[k] for k in c["masks"].head_patterns[0].tolist()]
+        nm = c["masks"].neuron_mask.to_bool()[0].cpu().numpy()
+        pats, onm, margin, mlp_margin = ref[i]
+        if pid != pats:
+            assert margin < 1e-5, (i, pid, pats, margin)
+        if not np.array_equal(nm, onm):
+            assert mlp_margin < 1e-5, (i, mlp_margin)
+        masks.append((pid, nm))
+    lg, c32 = O.model_forward(om, toks[:-1], masks)
+    assert rel(logits[0], lg) < 1e-2
+    assert abs(M.loss_forward(logits, toks[None, 1:]) - O.loss_forward(lg, toks[1:])) < 1e-2 * O.loss_forward(lg, toks[1:])
+    check_grads(grads, emulated(om, toks, masks, device_relu(cache))[1])
+    check_grads(grads, O.model_backward(om, c32, O.loss_backward(lg, toks[1:])), tol=1e-1)
