@@ -108,12 +108,13 @@ def attention_forward_dev(e: Emul, q, k, v, coords, blk, scale, tile=128):
             c0, c1 = j * tile, min(s, (j + 1) * tile)
             Sb, Mb = S[r0:r1, c0:c1], mask[r0:r1, c0:c1]
             mx = np.where(Mb, Sb, -np.inf).max(1).astype(np.float32)
-            mxs = (mx * c).astype(np.float32)
-            mo = m[r0:r1]
-            m_new = np.where(mxs > mo + 8.0, mxs, mo)  # lazy max (FA4-style, > 2^8 growth only)
-            alpha = np.where(m_new == mo, 1.0, np.exp2(mo - m_new)).astype(np.float32)
-            use = np.where(m_new == -np.inf, 0.0, m_new).astype(np.float32)
-            p = np.where(Mb, np.exp2(Sb * c - use[:, None]), 0.0).astype(np.float32)
+            with np.errstate(invalid="ignore", over="ignore"):  # rows with no active key yet: -inf - -inf
+                mxs = (mx * c).astype(np.float32)
+                mo = m[r0:r1]
+                m_new = np.where(mxs > mo + 8.0, mxs, mo)  # lazy max (FA4-style, > 2^8 growth only)
+                alpha = np.where(m_new == mo, 1.0, np.exp2(mo - m_new)).astype(np.float32)
+                use = np.where(m_new == -np.inf, 0.0, m_new).astype(np.float32)
+                p = np.where(Mb, np.exp2(Sb * c - use[:, None]), 0.0).astype(np.float32)
             l[r0:r1] = l[r0:r1] * alpha + p.sum(1, dtype=np.float32)
             o[r0:r1] = o[r0:r1] * alpha[:, None] + e.rd(p).astype(np.float64) @ v[c0:c1].astype(np.float64)
             m[r0:r1] = m_new
@@ -298,50 +299,60 @@ def adapter_backward(e: Emul, dy, ad, c, grads, prefix):
     return dy + e.mm(dh, ad["w_down"].T)
 
 
+def block_forward(e: Emul, m: O.OModel, i: int, h, masks_i):
+    """sf/model.py:403-433: one pre-LN block on the fp32 residual h [s, d]; masks_i = (head_patterns, neuron_mask)."""
+    lw, lora = m.layers[i], O._layer_lora(m, i)
+    adapter = m.peft == "adapter"
+    pats, nm = masks_i
+    h1, c1 = _ln_fwd(e, h, lw["ln1_g"], lw["ln1_b"])
+    att, ca = mha_forward(e, h1, lw, lora, pats, m.pool, m.dims)
+    caa = None
+    if adapter:
+        att, caa = adapter_forward(e, att, m.adapters[(i, "attn")], (i, "attn_ad"))
+    y = h + att
+    h2, c2 = _ln_fwd(e, y, lw["ln2_g"], lw["ln2_b"])
+    mo, cm = mlp_forward(e, h2, lw, lora, nm, m.dims, out_f32=adapter, layer=i)
+    cma = None
+    if adapter:
+        mo, cma = adapter_forward(e, mo, m.adapters[(i, "mlp")], (i, "mlp_ad"))
+    return y + mo, {"ln1": c1, "attn": ca, "attn_ad": caa, "ln2": c2, "mlp": cm, "mlp_ad": cma}
+
+
+def block_backward(e: Emul, m: O.OModel, i: int, c, dh, grads: dict):
+    """sf/autograd.py:165-181: fp32 d_out of block i -> fp32 d_in; accumulates the block's trainable gradients."""
+    lw, lora, prefix = m.layers[i], O._layer_lora(m, i), f"layers.{i}."
+    adapter, bitfit = m.peft == "adapter", m.peft == "bitfit"
+    dm = dh
+    if adapter:
+        dm = adapter_backward(e, dh, m.adapters[(i, "mlp")], c["mlp_ad"], grads, f"{prefix}mlp_adapter")
+    dh2 = mlp_backward(e, e.rd(dm), c["mlp"], lw, lora, m.dims, grads, prefix, bitfit)
+    dy = dh + O.layernorm_backward(dh2, c["ln2"])
+    da = dy
+    if adapter:
+        da = adapter_backward(e, dy, m.adapters[(i, "attn")], c["attn_ad"], grads, f"{prefix}attn_adapter")
+    dh1 = mha_backward(e, e.rd(da), c["attn"], lw, lora, m.dims, grads, prefix, bitfit)
+    return dy + O.layernorm_backward(dh1, c["ln1"])
+
+
 def model_forward(e: Emul, m: O.OModel, tokens, masks):
-    """sf/model.py:403-451 for one sequence; masks = list of (head_patterns, neuron_mask)."""
+    """sf/model.py:436-451 for one sequence; masks = list of (head_patterns, neuron_mask)."""
     emb = e.rd(m.emb)
     h = emb[tokens].astype(np.float32)
     caches = []
-    adapter = m.peft == "adapter"
     for i in range(m.dims.n_layers):
-        lw, lora = m.layers[i], O._layer_lora(m, i)
-        pats, nm = masks[i]
-        h1, c1 = _ln_fwd(e, h, lw["ln1_g"], lw["ln1_b"])
-        att, ca = mha_forward(e, h1, lw, lora, pats, m.pool, m.dims)
-        caa = None
-        if adapter:
-            att, caa = adapter_forward(e, att, m.adapters[(i, "attn")], (i, "attn_ad"))
-        y = h + att
-        h2, c2 = _ln_fwd(e, y, lw["ln2_g"], lw["ln2_b"])
-        mo, cm = mlp_forward(e, h2, lw, lora, nm, m.dims, out_f32=adapter, layer=i)
-        cma = None
-        if adapter:
-            mo, cma = adapter_forward(e, mo, m.adapters[(i, "mlp")], (i, "mlp_ad"))
-        h = y + mo
-        caches.append({"ln1": c1, "attn": ca, "attn_ad": caa, "ln2": c2, "mlp": cm, "mlp_ad": cma})
+        h, c = block_forward(e, m, i, h, masks[i])
+        caches.append(c)
     hf, cf = _ln_fwd(e, h, m.lnf_g, m.lnf_b)
     return e.mm(hf, emb.T), {"blocks": caches, "lnf": cf}
 
 
 def model_backward(e: Emul, m: O.OModel, cache, d_logits):
-    """sf/autograd.py:165-196."""
+    """sf/autograd.py:184-196."""
     grads = {}
     emb = e.rd(m.emb)
     dh = O.layernorm_backward(e.mm(e.rd(d_logits), emb), cache["lnf"])
-    adapter, bitfit = m.peft == "adapter", m.peft == "bitfit"
     for i in reversed(range(m.dims.n_layers)):
-        c, lw, lora, prefix = cache["blocks"][i], m.layers[i], O._layer_lora(m, i), f"layers.{i}."
-        dm = dh
-        if adapter:
-            dm = adapter_backward(e, dh, m.adapters[(i, "mlp")], c["mlp_ad"], grads, f"{prefix}mlp_adapter")
-        dh2 = mlp_backward(e, e.rd(dm), c["mlp"], lw, lora, m.dims, grads, prefix, bitfit)
-        dy = dh + O.layernorm_backward(dh2, c["ln2"])
-        da = dy
-        if adapter:
-            da = adapter_backward(e, dy, m.adapters[(i, "attn")], c["attn_ad"], grads, f"{prefix}attn_adapter")
-        dh1 = mha_backward(e, e.rd(da), c["attn"], lw, lora, m.dims, grads, prefix, bitfit)
-        dh = dy + O.layernorm_backward(dh1, c["ln1"])
+        dh = block_backward(e, m, i, cache["blocks"][i], dh, grads)
     for name, p in O.trainable_params(m).items():
         if name not in grads:
             grads[name] = np.zeros_like(p)

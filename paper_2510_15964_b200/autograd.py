@@ -59,7 +59,8 @@ class FlatGrads(dict):
         self.views, self.scale = views, scale
 
 
-# diagnostics (tools/): when a dict, mlp_backward records its bf16 dO and dz under "<prefix>dO" / "<prefix>dz"
+# diagnostics and teacher-forced tests: when a dict, block_backward records its fp32 d_out under "<prefix>d_out"
+# and mlp_backward its bf16 dO and dz under "<prefix>dO" / "<prefix>dz"
 DEBUG_TAPS: dict | None = None
 
 CG_LAYERS = 2  # layers whose LoRA / BitFit column reductions share one lx_colgrad_group launch (4: no gain)
@@ -287,6 +288,8 @@ def block_backward(d_out, model: M.Model, layer: int, cache, masks, grads: dict,
     bitfit = model.peft_method == "bitfit"
     lora = {t: model.lora[(layer, t)] for t in model.lora_targets} if model.peft_method == "lora" else {}
     prefix = f"layers.{layer}."
+    if DEBUG_TAPS is not None:
+        DEBUG_TAPS[f"{prefix}d_out"] = d_out.clone()
     adapter = model.peft_method == "adapter"
     if d_out_bf16 is None:
         d_out_bf16 = d_out.to(torch.bfloat16)

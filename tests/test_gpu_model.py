@@ -83,22 +83,26 @@ def check_grads(grads, ref: dict, tol: float = 1e-2):
     """Every gradient tensor within max|dev - ref| / max|ref| <= tol; all-zero references (inactive
     neuron blocks, unreached parameters) exactly zero on the device; inactive columns of w1.lora_b /
     w2.lora_a / b1 exactly zero; bk (exactly 0 by softmax shift invariance) bounded absolutely by tol *
-    max|g_bv|. Returns the worst relative error."""
-    worst = 0.0
+    max|g_bv|. Returns the worst relative error; a failure lists every tensor's error."""
+    errs, bad = {}, []
     for n, v in ref.items():
         gr = grads[n].detach().float().cpu().numpy()
         if np.abs(v).max() == 0:
-            assert float(np.abs(gr).max()) == 0, n
+            if float(np.abs(gr).max()) != 0:
+                bad.append((n, "nonzero where the reference is 0"))
             continue
         if n.endswith(".bk"):
-            assert np.abs(gr - v).max() <= tol * np.abs(ref[n[:-2] + "bv"]).max(), n
+            if np.abs(gr - v).max() > tol * np.abs(ref[n[:-2] + "bv"]).max():
+                bad.append((n, "bk absolute bound"))
             continue
         if n.endswith("w1.lora_b") or n.endswith("w2.lora_a") or n.endswith(".b1"):
-            assert np.all(gr[v == 0] == 0), n  # inactive neuron blocks untouched (sf/autograd.py:89-90)
-        e = rel(gr, v)
-        worst = max(worst, e)
-        assert e <= tol, (n, e)
-    return worst
+            if not np.all(gr[v == 0] == 0):  # inactive neuron blocks untouched (sf/autograd.py:89-90)
+                bad.append((n, "inactive block written"))
+        errs[n] = rel(gr, v)
+        if errs[n] > tol:
+            bad.append((n, errs[n]))
+    assert not bad, (bad, sorted(errs.items(), key=lambda kv: -kv[1])[:12])
+    return max(errs.values(), default=0.0)
 
 
 @pytest.mark.parametrize("peft", ["lora", "adapter", "bitfit"])
@@ -322,8 +326,12 @@ def test_cfg1_end_to_end_predicted_mode(dev):
     autograd tests do. Device vs oracle on the device-chosen masks (sf/harness.py:401-417):
       * logits and loss within 1e-2 of the float32 oracle;
       * every layer's masks equal the oracle predictor's on the device's own predictor inputs (ties excepted);
-      * every LoRA gradient within 1e-2 of the bf16 rounding-point oracle given the device's masks and ReLU
-        decisions, and within 1e-1 of float32 (sanity)."""
+      * per layer, teacher-forced: the block's output from the device's input, and the block's LoRA gradients
+        from the device's incoming gradient, within 1e-2 of the bf16 rounding-point oracle (given the device's
+        masks and ReLU decisions) -- each layer is checked on its own, so rounding differences do not compound
+        over the 12 layers;
+      * end to end, the LoRA gradients within 5e-2 of the same oracle (compounded over 12 layers)."""
+    from oracle import bf16_emul as E
     from paper_2510_15964_b200 import autograd as AG, harness as HN, model as M, predictor as P
 
     dims = O.Dims(768, 12, 3072, 256, 12, 50272, 16, 16)
@@ -340,7 +348,12 @@ def test_cfg1_end_to_end_predicted_mode(dev):
     prov = HN.PredictedProvider(m, preds, P.PredictorTrainConfig())
     toks = rng.integers(0, dims.vocab, size=dims.seq_len + 1)
     logits, cache = M.model_forward(m, toks[None, :-1], prov)
-    grads = AG.model_backward(m, cache, M.loss_backward(logits, toks[None, 1:]))
+    AG.DEBUG_TAPS = {}
+    try:
+        grads = AG.model_backward(m, cache, M.loss_backward(logits, toks[None, 1:]))
+        taps = AG.DEBUG_TAPS
+    finally:
+        AG.DEBUG_TAPS = None
     ids = list(m.pool)
     ref = predictor_masks_on_device_inputs(cache, preds, om.pool, 0)
     masks = []
@@ -356,5 +369,16 @@ def test_cfg1_end_to_end_predicted_mode(dev):
     lg, c32 = O.model_forward(om, toks[:-1], masks)
     assert rel(logits[0], lg) < 1e-2
     assert abs(M.loss_forward(logits, toks[None, 1:]) - O.loss_forward(lg, toks[1:])) < 1e-2 * O.loss_forward(lg, toks[1:])
-    check_grads(grads, emulated(om, toks, masks, device_relu(cache))[1])
-    check_grads(grads, O.model_backward(om, c32, O.loss_backward(lg, toks[1:])), tol=1e-1)
+    # per-layer teacher forcing
+    e = E.Emul(relu=device_relu(cache))
+    ins = [c["ln1"]["x"].cpu().numpy() for c in cache["blocks"]] + [cache["lnf"]["x"].cpu().numpy()]
+    worst_fwd = worst_bwd = 0.0
+    for i in range(dims.n_layers):
+        y, ce = E.block_forward(e, om, i, ins[i], masks[i])
+        worst_fwd = max(worst_fwd, rel(ins[i + 1] - ins[i], y - ins[i]))  # the block's contribution
+        gl = {}
+        E.block_backward(e, om, i, ce, taps[f"layers.{i}.d_out"].cpu().numpy(), gl)
+        worst_bwd = max(worst_bwd, check_grads({n: grads[n] for n in gl}, gl))
+    assert worst_fwd < 1e-2, worst_fwd
+    # end to end (compounded through 12 layers)
+    check_grads(grads, emulated(om, toks, masks, device_relu(cache))[1], tol=5e-2)
