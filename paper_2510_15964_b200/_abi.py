@@ -48,6 +48,9 @@ SIGNATURES: dict[str, list] = {
     "lx_bsattn_fwd_tc": [_P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _I, _P, _P],
     "lx_bsattn_bwd_tc": [_P, _I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P],
     "lx_debug_set_attn_trace": [_P],
+    "lx_adapter_ws_floats": [_I, _I],
+    "lx_adapter_fwd": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P],
+    "lx_adapter_bwd": [_P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _F, _P, _P, _P, _P, _P],
     "lx_layernorm_fwd": [_P, _P, _P, _I, _I, _P, _P, _F, _P, _I, _P, _P, _I, _I, _P, _P],
     "lx_cross_entropy": [_P, _I, _I, _P, _F, _P, _P, _P],
     "lx_adam_step": [_P, _P, _P, _P, _LL, _D, _D, _D, _D, _I, _P],
@@ -60,7 +63,8 @@ SIGNATURES: dict[str, list] = {
     "lx_block_activity": [_P, _I, _I, _I, _I, _P, _P],
     "lx_weighted_bce": [_P, _I, _I, _I, _P, _F, _P, _I, _P, _P],
 }
-RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_group_ws_floats": _LL, "lx_rowproj_ws_bytes": _LL, "lx_exact_mass_smem": C.c_size_t}
+RESTYPES = {"lx_last_error": C.c_char_p, "lx_colgrad_group_ws_floats": _LL, "lx_rowproj_ws_bytes": _LL, "lx_exact_mass_smem": C.c_size_t,
+            "lx_adapter_ws_floats": _LL}
 
 
 
@@ -102,7 +106,7 @@ def lib() -> C.CDLL:
     return _lib
 
 
-_NON_STATUS = ("lx_abi_version", "lx_device_sm_count", "lx_gemm_set_cta_pair", "lx_exact_mass_smem")
+_NON_STATUS = ("lx_abi_version", "lx_device_sm_count", "lx_gemm_set_cta_pair", "lx_exact_mass_smem", "lx_adapter_ws_floats")
 
 
 # Kernel-time probe (bench.py's roofline): when a dict {symbol: list}, every call of a listed symbol is

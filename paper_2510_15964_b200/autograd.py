@@ -143,13 +143,24 @@ def layernorm_backward(dy, cache, accumulate_into: torch.Tensor | None = None, w
 
 
 def adapter_backward(dy, ad: M.AdapterLayer, cache, grads: dict, prefix: str):
-    """sf/autograd.py:69-75 (fp32)."""
-    _acc(grads, f"{prefix}.w_up", cache["h"].t() @ dy)
-    _acc(grads, f"{prefix}.b_up", dy.sum(0))
-    dh = (dy @ ad.w_up.t()) * (cache["z"] > 0)
-    _acc(grads, f"{prefix}.w_down", cache["x"].t() @ dh)
-    _acc(grads, f"{prefix}.b_down", dh.sum(0))
-    return dy + dh @ ad.w_down.t()
+    """sf/autograd.py:69-75 on the fp32 adapter kernels (csrc/adapter.cu): one row pass (dh, dx) and one
+    deterministic column reduction for the four gradients. Returns dx fp32."""
+    dy = dy.float().reshape(-1, ad.w_up.shape[1]).contiguous()
+    M, d = dy.shape
+    r = ad.w_down.shape[1]
+    dev = dy.device
+    dh = torch.empty(M, r, dtype=torch.float32, device=dev)
+    dx = torch.empty_like(dy)
+    ws = torch.empty(int(_abi.lib().lx_adapter_ws_floats(d, r)), dtype=torch.float32, device=dev)
+    g = {k: torch.empty_like(getattr(ad, k)) for k in ("w_down", "b_down", "w_up", "b_up")}
+    x = cache["x"]
+    _abi.call("lx_adapter_bwd", dy.data_ptr(), d, x.data_ptr(), x.stride(0), M, d, r, cache["z"].data_ptr(),
+              ad.w_down.data_ptr(), ad.w_up.data_ptr(), dh.data_ptr(), dx.data_ptr(), d, ws.data_ptr(), 1.0,
+              g["w_down"].data_ptr(), g["b_down"].data_ptr(), g["w_up"].data_ptr(), g["b_up"].data_ptr(),
+              _abi.stream_handle(dev))
+    for k, v in g.items():
+        _acc(grads, f"{prefix}.{k}", v)
+    return dx
 
 
 def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims: M.ModelDims, grads: dict,

@@ -495,10 +495,16 @@ def layernorm_forward(x, gamma, beta, eps: float = 1e-5, x_small_spec=None, delt
 
 
 def adapter_forward(x: torch.Tensor, ad: AdapterLayer):
-    """x + relu(x Wd + bd) Wu + bu (sf/model.py:315-319); fp32."""
-    z = torch.addmm(ad.b_down, x, ad.w_down)
-    h = torch.relu(z)
-    return x + torch.addmm(ad.b_up, h, ad.w_up), {"x": x, "z": z, "h": h}
+    """x + relu(x Wd + bd) Wu + bu (sf/model.py:315-319) on the fp32 adapter kernel (csrc/adapter.cu); the cache
+    keeps x, the pre-activation z and h = relu(z)."""
+    x = x.float().contiguous()
+    M, d = x.shape
+    r = ad.w_down.shape[1]
+    z = torch.empty(M, r, dtype=torch.float32, device=x.device)
+    out = torch.empty_like(x)
+    _abi.call("lx_adapter_fwd", x.data_ptr(), d, M, d, r, ad.w_down.data_ptr(), ad.b_down.data_ptr(), ad.w_up.data_ptr(),
+              ad.b_up.data_ptr(), z.data_ptr(), out.data_ptr(), d, _abi.stream_handle(x.device))
+    return out, {"x": x, "z": z, "h": torch.relu(z)}
 
 
 def resolve_head_patterns(head_patterns, model_or_dpool, n_items: int, n_heads: int, device):
