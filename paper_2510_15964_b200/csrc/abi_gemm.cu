@@ -110,6 +110,13 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   return launch_check("gemm_sm100 (cta pair)");
 }
 
+// N-side packed gathers (fc1, fc2 input-grad): wide CTA-pair tiles (256 rows x up to 512 columns, the width chosen on
+// the device so the tiles fit in one round of pairs) unless LX_GEMM_WIDE=0 or a pair mode is forced. Halves the
+// L2 -> SM bytes per FLOP of the 128 x 256 single-CTA tile and avoids a second, mostly empty round of tiles.
+static bool wide_pairs() {
+  static const bool on = [] { const char* e = getenv("LX_GEMM_WIDE"); return !(e && e[0] == '0'); }();
+  return on && g_cta_pair == 0;
+}
 // dense / packed B: pick the CTA-pair engine when enabled (B boxes are then BN/2 rows on the N side)
 // tb1: B boxes for 1-CTA 256-wide tiles; tb2: 128-row boxes (pair, BN 256); tb4: 64-row boxes (pair, BN 128)
 template <int BMODE, int EPI>
@@ -120,6 +127,19 @@ static int launch_gemm_auto(const CUtensorMap& ta, const CUtensorMap& tb1, const
   if (g_cta_pair == 3) return launch_gemm<BMODE, EPI, 128, 1>(ta, tb2, args, st);  // single CTA, 128 x 128 tiles
   return launch_gemm<BMODE, EPI, 256, 1>(ta, tb1, args, st);
 }
+
+template <int EPI>
+static int launch_packed_n(const CUtensorMap& ta, const uint16_t* wp, int n_items, int d, int d_ff, const CUtensorMap& tb,
+                           const CUtensorMap& tb2, const CUtensorMap& tb4, const GemmArgs& args, cudaStream_t st) {
+  if (wide_pairs()) {
+    CUtensorMap tb32;
+    int rc = make_tmap_bf16_2d(&tb32, wp, d, (uint64_t)n_items * d_ff, d, kBK, 32);
+    if (rc) return rc;
+    return launch_gemm<kPackedN, EPI, 512, 2>(ta, tb32, args, st);
+  }
+  return launch_gemm_auto<kPackedN, EPI>(ta, tb, tb2, tb4, args, st);
+}
+
 
 static GemmArgs base_args(int n_items, int rows, int n_dense, int k_dense) {
   GemmArgs a;
@@ -271,8 +291,8 @@ int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int bl
     CUtensorMap tb2, tb4;
     if ((rc = mlp_tmap_b(&tb2, w1_t, w1_packed, n_items, d, d_ff, blk, true, 128))) return rc;
     if ((rc = mlp_tmap_b(&tb4, w1_t, w1_packed, n_items, d, d_ff, blk, true, 64))) return rc;
-    return apply_relu ? launch_gemm_auto<kPackedN, kEpiFc1>(ta, tb, tb2, tb4, args, stream)
-                      : launch_gemm_auto<kPackedN, kEpiFc1Raw>(ta, tb, tb2, tb4, args, stream);
+    return apply_relu ? launch_packed_n<kEpiFc1>(ta, w1_packed, n_items, d, d_ff, tb, tb2, tb4, args, stream)
+                      : launch_packed_n<kEpiFc1Raw>(ta, w1_packed, n_items, d, d_ff, tb, tb2, tb4, args, stream);
   }
   return apply_relu ? launch_gemm<kNGather, kEpiFc1, 256>(ta, tb, args, stream)
                     : launch_gemm<kNGather, kEpiFc1Raw, 256>(ta, tb, args, stream);
@@ -337,7 +357,7 @@ int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_
     CUtensorMap tb2, tb4;
     if ((rc = mlp_tmap_b(&tb2, w2, w2_packed, n_items, d, d_ff, blk, true, 128))) return rc;
     if ((rc = mlp_tmap_b(&tb4, w2, w2_packed, n_items, d, d_ff, blk, true, 64))) return rc;
-    return launch_gemm_auto<kPackedN, kEpiDa>(ta, tb, tb2, tb4, args, stream);
+    return launch_packed_n<kEpiDa>(ta, w2_packed, n_items, d, d_ff, tb, tb2, tb4, args, stream);
   }
   return launch_gemm<kNGather, kEpiDa, 256>(ta, tb, args, stream);
 }

@@ -102,13 +102,13 @@ constexpr int kStgPitch = 80;  // bytes per staged row: 64 B of bf16 + 16 B pad 
 
 template <int BN, int CTAS = 1>
 struct GemmSmem {
-  static constexpr int kStages = CTAS == 2 ? (BN >= 256 ? 5 : 7) : (BN >= 256 ? 3 : 5);
+  static constexpr int kStages = CTAS == 2 ? (BN > 256 ? 3 : BN >= 256 ? 5 : 7) : (BN >= 256 ? 3 : 5);
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = (BN / CTAS) * kBK * 2;  // this CTA's share of the B tile
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOff = kStages * kStageBytes;
   static constexpr int kMiscOff = kBarOff + (2 * kStages + 4) * 8;
-  static constexpr int kEpiOff = (kMiscOff + 16 + 4 * (kMaxItems + 1) + 127) / 128 * 128;
+  static constexpr int kEpiOff = (kMiscOff + 16 + 4 * (kMaxItems + 2) + 127) / 128 * 128;  // + prefix, tile width
   static constexpr int kEpiBytes = BN * 4 + BN * kMaxR * 4;
   static constexpr int kStgOff = kEpiOff + kEpiBytes;  // per epilogue warp: 32 rows x kStgPitch
   static constexpr int kTotal = kStgOff + kEpiWarps * 32 * kStgPitch + 1024;  // + alignment slack
@@ -122,14 +122,20 @@ struct TileInfo {
   int k_total;   // K extent (elements)
 };
 
+// Wide pair tiles (CTAS = 2, BN = 512, N-side gathers): one accumulator of up to 512 columns per CTA, tile width
+// w (a multiple of 64, chosen per launch on the device from the counts: the narrowest w whose tiles fit in one
+// round of CTA pairs), computed as two cta_group::2 MMAs (N = min(w, 256), then the rest).
 template <int BMODE, int BN>
-LX_DEV int item_n_tiles(const GemmArgs& a, int cnt) {
-  if (is_ng<BMODE>()) return (cnt * a.blk + BN - 1) / BN;
+LX_DEV int item_n_tiles(const GemmArgs& a, int cnt, int wsel = 0) {
+  if (is_ng<BMODE>()) {
+    const int w = wsel ? wsel : BN;
+    return (cnt * a.blk + w - 1) / w;
+  }
   return (a.n_dense + BN - 1) / BN;
 }
 
 template <int BMODE, int BN>
-LX_DEV TileInfo decode_tile(const GemmArgs& a, const int* prefix, const int* cnts, int m_tiles, int t) {
+LX_DEV TileInfo decode_tile(const GemmArgs& a, const int* prefix, const int* cnts, int m_tiles, int t, int wsel = 0) {
   // m_tiles counts tiles of kBM * CTAS rows (the caller's choice)
   int lo = 0, hi = a.n_items;  // largest item with prefix[item] <= t
   while (hi - lo > 1) {
@@ -146,7 +152,9 @@ LX_DEV TileInfo decode_tile(const GemmArgs& a, const int* prefix, const int* cnt
   // an item's active columns are split into equal-width tiles (multiples of 16, <= BN): no short last
   // tile whose CTA idles while the full ones finish
   int w = BN;
-  if (is_ng<BMODE>()) {
+  if (is_ng<BMODE>() && wsel) {
+    w = wsel;  // wide pair tiles: uniform width chosen for the launch
+  } else if (is_ng<BMODE>()) {
     const int nt_item = (n_total + BN - 1) / BN;
     const int q = a.blk > 16 ? a.blk : 16;  // whole neuron blocks (gather boxes are per block)
     if (nt_item > 0) w = min(BN, ((n_total + nt_item - 1) / nt_item + q - 1) / q * q);
@@ -163,6 +171,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, GemmArgs args) {
   static_assert(CTAS == 1 || (BMODE == kDense || BMODE == kPackedN || BMODE == kPackedK), "CTA pairs: dense / packed B only");
   using L = GemmSmem<BN, CTAS>;
+  constexpr bool kWide = BN > 256;  // wide pair tiles (CTAS == 2, N-side gathers)
+  static_assert(!kWide || (CTAS == 2 && is_ng<BMODE>()), "wide tiles: CTA pairs over N-side gathers only");
+  constexpr int kAccBufs = 2 * BN <= 512 ? 2 : 1;  // TMEM accumulators (double-buffered when two fit)
   constexpr int TM = kBM * CTAS;  // rows per (pair) tile
   constexpr int BNC = BN / CTAS;  // this CTA's share of the N tile
   constexpr int S = L::kStages;
@@ -174,6 +185,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kMiscOff);
   int* prefix = reinterpret_cast<int*>(smem + L::kMiscOff + 16);
+  int* wsel_s = prefix + kMaxItems + 1;
   float* s_bias = reinterpret_cast<float*>(smem + L::kEpiOff);
   float* s_w = s_bias + BN;
 
@@ -199,12 +211,27 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   // prologue above overlaps the predecessor kernel's tail (programmatic dependent launch)
   pdl_wait_trigger();
   // ---- tile table: prefix[b] = first tile index of item b (counts are device-resident)
+  // counts -> shared memory in one parallel round trip (the epilogue's staging area is free until the first tile)
+  int* s_cnt = reinterpret_cast<int*>(smem + L::kEpiOff);
+  if (BMODE != kDense)
+    for (int b = threadIdx.x; b < args.n_items; b += blockDim.x) s_cnt[b] = __ldg(args.counts + b);
+  __syncthreads();
   if (threadIdx.x == 0) {
+    int wsel = 0;
+    if (kWide) {  // narrowest multiple-of-64 width whose tiles fit in one round of pairs (else the widest)
+      const int pairs = gridDim.x / CTAS;
+      for (wsel = 64; wsel < BN; wsel += 64) {
+        int tot = 0;
+        for (int b = 0; b < args.n_items; ++b) tot += m_tiles * item_n_tiles<BMODE, BN>(args, s_cnt[b], wsel);
+        if (tot <= pairs) break;
+      }
+    }
+    *wsel_s = wsel;
     int acc = 0;
     for (int b = 0; b < args.n_items; ++b) {
       prefix[b] = acc;
-      int cnt = (BMODE == kDense) ? 0 : __ldg(args.counts + b);
-      acc += m_tiles * item_n_tiles<BMODE, BN>(args, cnt);
+      int cnt = (BMODE == kDense) ? 0 : s_cnt[b];
+      acc += m_tiles * item_n_tiles<BMODE, BN>(args, cnt, wsel);
     }
     prefix[args.n_items] = acc;
   }
@@ -214,6 +241,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int n_tiles_total = prefix[args.n_items];
+  const int wsel = *wsel_s;
 
   // counts are needed by every role to decode tiles; read through L1 per decode.
   const int* cnts = args.counts;
@@ -225,7 +253,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     int stage = 0;
     uint32_t phase = 0;
     for (int t = t0; t < n_tiles_total; t += t_step) {
-      TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t);
+      TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t, wsel);
       const int row0 = ti.item * args.rows_per_item + ti.mt * TM + rank * kBM;
       const int* ids = args.ids + (size_t)ti.item * args.ids_stride;
       int my_row = 0;  // kNGather: this lane's gathered W row (block id * blk), lane < nb
@@ -247,6 +275,24 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         mbar_wait(empty + stage, phase ^ 1);
         if (CTAS == 2) {
           // pair: this CTA's A rows and half of B; bytes of both halves counted on the leader's barrier
+          if (kWide) {
+            // N split as two cta_group::2 MMAs: n1 = min(w, 256) columns, then n2; each CTA holds n1/2 + n2/2
+            // rows of B (rows n0 + rank n1/2 .., then n0 + n1 + rank n2/2 ..), loaded as 32-row boxes
+            const int nm = (ti.n_cols + 63) / 64 * 64, n1 = nm < 256 ? nm : 256, n2 = nm - n1;
+            if (lane == 0) {
+              if (leader) mbar_arrive_expect_tx(full + stage, 2 * (L::kABytes + (n1 / 2 + n2 / 2) * 128));
+              tma_load_2d_cg2(sa, &tmap_a, full + stage, ks * kBK, row0, pol_w);
+              const int b0 = ti.item * args.packed_stride + ti.n0;
+              for (int r0 = 0; r0 < n1 / 2; r0 += 32)
+                tma_load_2d_cg2(sb + r0 * 128, &tmap_b, full + stage, ks * kBK, b0 + rank * (n1 / 2) + r0, pol_w);
+              for (int r0 = 0; r0 < n2 / 2; r0 += 32)
+                tma_load_2d_cg2(sb + 128 * 128 + r0 * 128, &tmap_b, full + stage, ks * kBK, b0 + n1 + rank * (n2 / 2) + r0,
+                                pol_w);
+            }
+            __syncwarp();
+            if (++stage == S) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if (lane == 0) {
             if (leader) mbar_arrive_expect_tx(full + stage, 2 * (L::kABytes + L::kBBytes));
             tma_load_2d_cg2(sa, &tmap_a, full + stage, ks * kBK, row0, pol_w);
@@ -298,15 +344,18 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       uint32_t phase = 0;
       int it = 0;
       for (int t = t0; t < n_tiles_total; t += t_step, ++it) {
-        TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t);
-        const int buf = it & 1;
-        const uint32_t use_phase = (it >> 1) & 1;
+        TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t, wsel);
+        const int buf = kAccBufs == 2 ? (it & 1) : 0;
+        const uint32_t use_phase = kAccBufs == 2 ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(tempty + buf, use_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
         // pairs always run the full N (each CTA holds BN/2 of B; columns past n_cols are discarded)
         int n_mma = (is_ng<BMODE>() && CTAS == 1) ? ((ti.n_cols + 15) / 16) * 16 : BN;
+        const int nm_w = (ti.n_cols + 63) / 64 * 64, n1_w = nm_w < 256 ? nm_w : 256, n2_w = nm_w - n1_w;
+        if (kWide) n_mma = n1_w;
         const uint32_t idesc = make_idesc_bf16(TM, n_mma, false, is_kg<BMODE>());
+        const uint32_t idesc2 = make_idesc_bf16(TM, n2_w > 0 ? n2_w : 16, false, false);
         for (int ks = 0; ks < ti.k_stages; ++ks) {
           mbar_wait(full + stage, phase);
           if (ks == 0 && it < 3) gemm_stamp(2 + 4 * it);
@@ -320,6 +369,8 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             uint64_t db = is_kg<BMODE>() ? make_sdesc(sb + kk * 2048, kBK * 128, 1024) : make_sdesc(sb + kk * 32, 16, 1024);
             if (CTAS == 2) mma_bf16_ss_cg2(d_tmem, da, db, idesc, (ks | kk) != 0);
             else mma_bf16_ss(d_tmem, da, db, idesc, (ks | kk) != 0);
+            if (kWide && n2_w > 0)  // second N part: B rows at +128 rows of this CTA's stage, accumulator columns 256..
+              mma_bf16_ss_cg2(d_tmem + 256, da, make_sdesc(sb + 128 * 128 + kk * 32, 16, 1024), idesc2, (ks | kk) != 0);
           }
           if (CTAS == 2) mma_commit_cg2(empty + stage);
           else mma_commit(empty + stage);
@@ -340,8 +391,8 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     uint8_t* stg = smem + L::kStgOff + (warp - 2) * 32 * kStgPitch;
     int it = 0;
     for (int t = t0; t < n_tiles_total; t += t_step, ++it) {
-      TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t);
-      const int buf = it & 1;
+      TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t, wsel);
+      const int buf = kAccBufs == 2 ? (it & 1) : 0;
       const int* ids = args.ids + (size_t)ti.item * args.ids_stride;
       const int local_row = ti.mt * TM + rank * kBM + r_in_tile;
       const bool row_ok = local_row < args.rows_per_item;
@@ -373,7 +424,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           if (q < r) xr[q] = __ldg(args.lora_x + grow * r + q) * args.lora_scale;
       }
 
-      mbar_wait(tfull + buf, (it >> 1) & 1);
+      mbar_wait(tfull + buf, kAccBufs == 2 ? ((it >> 1) & 1) : (it & 1));
       if (ep_tid == 0 && it < 3) gemm_stamp(4 + 4 * it);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;

@@ -25,7 +25,7 @@ if "--pair" in sys.argv:  # GEMM engine variant (lx_gemm_set_cta_pair): 0 single
     from paper_2510_15964_b200 import _abi
 
     _abi.lib().lx_gemm_set_cta_pair(int(sys.argv[sys.argv.index("--pair") + 1]))
-model, state, prov = bench.build_workload(cfg, dev, 0, 0.85, 0.5)
+model, state, prov = bench.build_workload(cfg, dev, 0, 0.85, 0.75)
 eng = FinetuneEngine(model, state, prov, lr=1e-4)
 tok = torch.randint(0, cfg["V"], (cfg["B"], cfg["s"] + 1), device=dev)
 if graph:
