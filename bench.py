@@ -424,9 +424,14 @@ def run_ours(args, cfg, rank, world, dist):
     roof, kernels = None, None
     if rank == 0:
         snap = StateSnapshot(state)  # rank-0-only probes below must not leave rank 0's state diverged
+        eng.graph = eng.static_loss = None  # the step graph's memory pool back before the eager probe / dense steps
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
         sync_saved, eng.grad_sync = eng.grad_sync, None  # rank-0-only probe step: no collective
         roof, kernels = kernel_probe(model, eng, tok_dev, peaks, args.config)
         eng.grad_sync = sync_saved
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
         if not args.skip_dense:
             # dense reference points on the same box: (a) same engine, every head/block dense; (b) torch cuBLAS/SDPA
             dprov = HN.DenseProvider(model)
@@ -435,7 +440,8 @@ def run_ours(args, cfg, rank, world, dist):
             deng.capture(tok_dev, warmup=1)
             extra["dense_same_kernels_ms"] = round(time_graph(deng, max(3, args.steps // 2), None, dev), 3)
             extra["speedup_vs_dense_same_kernels"] = round(extra["dense_same_kernels_ms"] / ms, 3)
-            del deng
+            del deng, dprov
+            torch.cuda.synchronize()
             torch.cuda.empty_cache()
             if args.peft == "lora":
                 try:

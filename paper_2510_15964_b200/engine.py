@@ -95,6 +95,8 @@ class FinetuneEngine:
         dh, dh_bf = AG.layernorm_backward(d_hf, cf, want_bf16=True)
         cg = None
         side = self._cg_stream()
+        if side is not None:  # fork the side stream from this (possibly capturing) stream, so the join below is legal
+            side.wait_stream(torch.cuda.current_stream())  # even when no column reduction runs on it (adapter)
         sync = self.grad_sync
         # buckets only where every trainable is written by the column reductions (LoRA, BitFit); the adapter's
         # torch-op gradients are copied in at the end and reduced by finish()
@@ -159,6 +161,7 @@ class FinetuneEngine:
         """Capture forward+backward+grad-reduction (not Adam, whose bias correction depends on
         the step count) into one CUDA graph; Adam runs as a handful of elementwise kernels."""
         self.static_tokens = example_tokens.to(self.model.device, torch.int64).clone()
+        torch.cuda.empty_cache()  # eager steps' cached blocks back to the driver: the graph pool is separate
         if hasattr(self.provider, "timing"):
             self.provider.timing = False  # no timing events inside a graph
         side = torch.cuda.Stream()

@@ -550,6 +550,7 @@ QKV_SLOT = {"wq": 0, "wk": 1, "wv": 2}
 # LX_NO_PACK=1: MLP GEMMs gather the active neuron blocks straight from W (one TMA box per block)
 # instead of streaming item-packed copies (experiments)
 _NO_PACK = __import__("os").environ.get("LX_NO_PACK", "0") == "1"
+_PACK_CACHE_BYTES = float(__import__("os").environ.get("LX_PACK_CACHE_GB", "48")) * 2**30
 
 
 def _qkv_lora(lora: dict, d: int):
@@ -637,10 +638,13 @@ def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, c
     d, f, blk = dims.d_model, dims.d_ff, dims.blk_size
     nm = lower_mask(neuron_mask, dims.n_blk, blk, B, x2.device)
     ad1, ad2 = lora.get("w1"), lora.get("w2")
-    # active rows of W1^T and W2 packed per item once per layer; reused by the backward's input-grads
+    # active rows of W1^T and W2 packed per item once per layer; kept for the backward's input-grads unless the
+    # packs of all layers would exceed LX_PACK_CACHE_GB (capacity [B, d_ff, d] per weight: 137 GB at OPT-6.7B,
+    # B = 16), in which case the backward re-packs its layer (mlp_backward)
     pack = not _NO_PACK
     w1p = neuron_ops.pack_active_rows(lw.mlp.w1_t, nm) if pack else None
     w2p = neuron_ops.pack_active_rows(lw.mlp.w2, nm) if pack else None
+    keep = pack and dims.n_layers * 2 * B * f * d * 2 <= _PACK_CACHE_BYTES
     lp = lw.lora_pack
     if ad1 is None:
         ax1 = None
@@ -667,7 +671,8 @@ def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, c
             counter.add(s * (d + n_act // max(B, 1)) * ad1.rank * B)
         if ad2 is not None:
             counter.add(s * (n_act // max(B, 1) + d) * ad2.rank * B)
-    return out, {"x": x2, "a": hid, "mask": nm, "ax1": ax1, "ax2": ax2, "n_items": B, "s": s, "w1p": w1p, "w2p": w2p}
+    return out, {"x": x2, "a": hid, "mask": nm, "ax1": ax1, "ax2": ax2, "n_items": B, "s": s,
+                 "w1p": w1p if keep else None, "w2p": w2p if keep else None, "repack": pack and not keep}
 
 
 def block_forward(x, model: Model, layer: int, masks, counter=None):

@@ -382,3 +382,23 @@ def test_cfg1_end_to_end_predicted_mode(dev):
     assert worst_fwd < 1e-2, worst_fwd
     # end to end (compounded through 12 layers)
     check_grads(grads, emulated(om, toks, masks, device_relu(cache))[1], tol=5e-2)
+
+
+def test_repacked_backward_equals_cached_packs(dev, monkeypatch):
+    """When the packed active weight rows of all layers would exceed LX_PACK_CACHE_GB, the forward drops them and
+    the backward re-packs its layer: bit-identical gradients to the cached-pack path."""
+    import bench
+    from paper_2510_15964_b200 import model as M
+    from paper_2510_15964_b200.engine import FinetuneEngine
+
+    cfg = dict(d=256, H=4, d_ff=1024, L=2, V=128, B=2, s=128, blk=16, attn_blk=32, r=8)
+    tok = torch.randint(0, cfg["V"], (cfg["B"], cfg["s"] + 1), generator=torch.Generator().manual_seed(5)).to(dev)
+    out = []
+    for limit in (M._PACK_CACHE_BYTES, 0.0):
+        monkeypatch.setattr(M, "_PACK_CACHE_BYTES", limit)
+        m, st, prov = bench.build_workload(cfg, dev, 8, 0.5, 0.5)
+        eng = FinetuneEngine(m, st, prov, lr=1e-3)
+        eng._step(tok)
+        torch.cuda.synchronize()
+        out.append(eng.flat_grad.clone())
+    assert torch.equal(out[0], out[1])
