@@ -62,6 +62,12 @@ int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void
 int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, int N, int K, void* out, int ldo,
               int out_f32, const float* resid, const float* bias, const float* lora_x, const float* lora_w,
               long long w_sr, long long w_sc, int r, float scaling, lx_stream_t stream);
+/* Same with the weight as stored for x @ W (torch.addmm layout): b [K, N] row-major, row stride ldb.
+ * The frozen Q/K/V/O projections and the LM head's input-grad (sf/model.py:340-342,354,449-450;
+ * sf/autograd.py:127-162) run on this and on lx_linear (the input-grads take W itself as b_t). */
+int lx_linear_kn(const uint16_t* a, int lda, const uint16_t* b, int ldb, int M, int N, int K, void* out, int ldo,
+                 int out_f32, const float* resid, const float* bias, const float* lora_x, const float* lora_w,
+                 long long w_sr, long long w_sc, int r, float scaling, lx_stream_t stream);
 
 /* ------------------------------------------------------------------ K1 mask build
  * approx_mlp_scores + predict_mlp_mask + active_columns

@@ -31,6 +31,7 @@ SIGNATURES: dict[str, list] = {
     "lx_debug_set_gemm_trace": [_P],
     "lx_gemm_bf16_tn": [_P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _I, _P],
     "lx_linear": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _P, _P, _P, _P, _LL, _LL, _I, _F, _P],
+    "lx_linear_kn": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _P, _P, _P, _P, _LL, _LL, _I, _F, _P],
     "lx_predict_mlp_mask": [_P, _I, _I, _I, _P, _I, _I, _F, _I, _P, _P, _P, _P, _P, _P],
     "lx_mask_compact": [_P, _I, _I, _I, _P, _P, _P, _P],
     "lx_predict_attention_patterns": [_P, _I, _I, _I, _P, _I, _I, _I, _F, _D, _I, _P, _P, _I, _I, _P, _P, _P, _P],

@@ -1,4 +1,5 @@
 // C-ABI: generic tcgen05 GEMM and the neuron-sparse MLP GEMMs (K2).
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -78,13 +79,41 @@ int make_tmap_bf16_2d_sw(CUtensorMap* map, const void* ptr, uint64_t inner, uint
 // first stage by ~1.4k cycles and costs more than its halved B traffic saves (tools/gemm_trace.py).
 static int g_cta_pair = 0;
 
-template <int BMODE, int EPI, int BN, int CTAS = 1>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
-  auto kern = gemm_sm100_kernel<BMODE, EPI, BN, CTAS>;
+template <int BMODE, int EPI, int BN, int CTAS = 1, int CL = 1>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args_in, cudaStream_t st) {
+  static const int spin = [] { const char* e = getenv("LX_GEMM_SPIN"); return e ? atoi(e) : 0; }();
+  GemmArgs args = args_in;
+  args.spin = spin;
+  auto kern = gemm_sm100_kernel<BMODE, EPI, BN, CTAS, CL>;
   constexpr int smem = GemmSmem<BN, CTAS>::kTotal;
+  constexpr int kCl = CTAS * CL;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+  static int grid = 0;  // persistent grid: every CTA (cluster) resident at once
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    grid = num_sms() / kCl * kCl;
+    if (attr_err == cudaSuccess && kCl > 2) {
+      // clusters of 4 must fit inside a GPC: size the grid by how many the device can hold at once
+      cfg.gridDim = dim3(grid);
+      int n = 0;
+      attr_err = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+      if (attr_err == cudaSuccess && n > 0) grid = std::min(grid, n * kCl);
+    }
+  });
   LX_CHECK_CUDA(attr_err);
   LX_REQUIRE(args.n_items >= 1 && args.n_items <= kMaxItems, LX_ERR_UNSUPPORTED, "n_items must be in [1, %d]", kMaxItems);
   LX_REQUIRE(args.lora_r >= 0 && args.lora_r <= kMaxR, LX_ERR_UNSUPPORTED, "LoRA rank must be <= %d", kMaxR);
@@ -92,20 +121,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
     launch_k(kern, num_sms(), kGemmThreads, smem, st, ta, tb, args);
     return launch_check("gemm_sm100");
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(num_sms() & ~1);
-  cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.gridDim = dim3(grid);
   LX_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, args));
   return launch_check("gemm_sm100 (cta pair)");
 }
@@ -125,6 +141,7 @@ static int launch_gemm_auto(const CUtensorMap& ta, const CUtensorMap& tb1, const
   if (g_cta_pair == 2) return launch_gemm<BMODE, EPI, 128, 2>(ta, tb4, args, st);
   if (g_cta_pair == 1) return launch_gemm<BMODE, EPI, 256, 2>(ta, tb2, args, st);
   if (g_cta_pair == 3) return launch_gemm<BMODE, EPI, 128, 1>(ta, tb2, args, st);  // single CTA, 128 x 128 tiles
+  if (g_cta_pair == 4) return launch_gemm<BMODE, EPI, 256, 2, 2>(ta, tb4, args, st);  // two pairs, B multicast
   return launch_gemm<BMODE, EPI, 256, 1>(ta, tb1, args, st);
 }
 
@@ -190,7 +207,7 @@ int lx_debug_set_gemm_trace(unsigned long long* buf) {
 
 int lx_gemm_set_cta_pair(int mode) {
   const int prev = g_cta_pair;
-  g_cta_pair = (mode >= 1 && mode <= 3) ? mode : 0;
+  g_cta_pair = (mode >= 1 && mode <= 5) ? mode : 0;
   return prev;
 }
 
@@ -220,23 +237,14 @@ int lx_gemm_bf16_tn(const uint16_t* a, int lda, const uint16_t* b, int ldb, void
                   : launch_gemm_auto<kDense, kEpiStoreBF16>(ta, tb, tb2, tb4, args, stream);
 }
 
-int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, int N, int K, void* out, int ldo,
-              int out_f32, const float* resid, const float* bias, const float* lora_x, const float* lora_w,
-              long long w_sr, long long w_sc, int r, float scaling, lx_stream_t stream) {
+static int linear_impl(const uint16_t* a, int lda, const uint16_t* b, int ldb, bool b_kn, int M, int N, int K, void* out,
+                       int ldo, int out_f32, const float* resid, const float* bias, const float* lora_x,
+                       const float* lora_w, long long w_sr, long long w_sc, int r, float scaling, cudaStream_t stream) {
   LX_REQUIRE(M > 0 && N > 0 && K > 0, LX_ERR_SHAPE, "linear: empty shape");
   LX_REQUIRE(!resid || out_f32, LX_ERR_SHAPE, "linear: residual add needs fp32 output");
-  // tile width: 128x256 tiles unless that leaves fewer than ~3 tiles per SM, then 128x128
-  // (more tiles per persistent CTA -> epilogues overlap the next tile's mainloop, smaller tail wave)
-  static int forced_bn = [] { const char* e = getenv("LX_LINEAR_BN"); return e ? atoi(e) : 0; }();
-  const long long tiles256 = (long long)((M + kBM - 1) / kBM) * ((N + 255) / 256);
-  // measured (tools/linear_probe.py): 128-wide tiles are A-operand smem-bound with 1-SM MMA, so 256
-  // wins even at 1.7 waves; LX_LINEAR_BN=128 keeps the variant reachable for experiments
-  (void)tiles256;
-  const int bn = forced_bn ? forced_bn : 256;
   CUtensorMap ta, tb;
   int rc;
   if ((rc = make_tmap_bf16_2d(&ta, a, K, M, lda, kBK, kBM))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, b_t, K, N, ldb, kBK, bn))) return rc;
   GemmArgs args = base_args(1, M, N, K);
   args.out = out;
   args.ldo = ldo;
@@ -249,8 +257,43 @@ int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, i
   args.w_sc = w_sc;
   args.lora_r = (lora_x && lora_w) ? r : 0;
   args.lora_scale = scaling;
+  // engine: wide CTA pairs (256 x 512 tiles, tcgen05 floor in the mainloop) when they fill at least half of the
+  // pairs, else single-CTA 128 x 256 tiles (small M: more, shorter tiles); lx_gemm_set_cta_pair forces a variant
+  const long long wide_tiles = (long long)((M + 255) / 256) * ((N + 511) / 512);
+  const bool wide = g_cta_pair == 5 || (g_cta_pair == 0 && wide_tiles * 4 >= num_sms());
+  if (b_kn) {  // B [K, N] row-major: MN-major 64 x 64 atoms
+    if ((rc = make_tmap_bf16_2d(&tb, b, N, K, ldb, kBK, 64))) return rc;
+    return wide ? launch_gemm<kDenseMN, kEpiFc2, 512, 2>(ta, tb, args, stream)
+                : launch_gemm<kDenseMN, kEpiFc2, 256>(ta, tb, args, stream);
+  }
+  if (wide) {  // 32-row B boxes
+    if ((rc = make_tmap_bf16_2d(&tb, b, K, N, ldb, kBK, 32))) return rc;
+    return launch_gemm<kDense, kEpiFc2, 512, 2>(ta, tb, args, stream);
+  }
+  if (g_cta_pair == 1 || g_cta_pair == 4) {  // CTA pairs (B half = 128-row boxes), or two pairs multicasting B
+    if ((rc = make_tmap_bf16_2d(&tb, b, K, N, ldb, kBK, g_cta_pair == 4 ? 64 : 128))) return rc;
+    return g_cta_pair == 4 ? launch_gemm<kDense, kEpiFc2, 256, 2, 2>(ta, tb, args, stream)
+                           : launch_gemm<kDense, kEpiFc2, 256, 2>(ta, tb, args, stream);
+  }
+  static int forced_bn = [] { const char* e = getenv("LX_LINEAR_BN"); return e ? atoi(e) : 0; }();
+  const int bn = forced_bn == 128 ? 128 : 256;
+  if ((rc = make_tmap_bf16_2d(&tb, b, K, N, ldb, kBK, bn))) return rc;
   return bn == 128 ? launch_gemm<kDense, kEpiFc2, 128>(ta, tb, args, stream)
                    : launch_gemm<kDense, kEpiFc2, 256>(ta, tb, args, stream);
+}
+
+int lx_linear(const uint16_t* a, int lda, const uint16_t* b_t, int ldb, int M, int N, int K, void* out, int ldo,
+              int out_f32, const float* resid, const float* bias, const float* lora_x, const float* lora_w,
+              long long w_sr, long long w_sc, int r, float scaling, lx_stream_t stream) {
+  return linear_impl(a, lda, b_t, ldb, false, M, N, K, out, ldo, out_f32, resid, bias, lora_x, lora_w, w_sr, w_sc, r,
+                     scaling, stream);
+}
+
+int lx_linear_kn(const uint16_t* a, int lda, const uint16_t* b, int ldb, int M, int N, int K, void* out, int ldo,
+                 int out_f32, const float* resid, const float* bias, const float* lora_x, const float* lora_w,
+                 long long w_sr, long long w_sc, int r, float scaling, lx_stream_t stream) {
+  return linear_impl(a, lda, b, ldb, true, M, N, K, out, ldo, out_f32, resid, bias, lora_x, lora_w, w_sr, w_sc, r,
+                     scaling, stream);
 }
 
 // B-operand tensor map of an MLP GEMM: gathered blocks of the full weight, or the item-packed copy.
@@ -326,7 +369,9 @@ int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_
   args.lora_scale = scaling;
   args.out_f32 = out_f32;
   args.resid = resid;
-  if (w2_packed) return launch_gemm_auto<kPackedK, kEpiFc2>(ta, tb, tb, tb, args, stream);
+  if (w2_packed) {
+    return launch_gemm_auto<kPackedK, kEpiFc2>(ta, tb, tb, tb, args, stream);
+  }
   return launch_gemm<kKGather, kEpiFc2, 256>(ta, tb, args, stream);
 }
 
@@ -385,7 +430,9 @@ int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d,
   args.w_sc = r;
   args.lora_r = (dax1 && a1_lora) ? r : 0;
   args.out_f32 = out_f32;
-  if (w1_packed) return launch_gemm_auto<kPackedK, kEpiDx>(ta, tb, tb, tb, args, stream);
+  if (w1_packed) {
+    return launch_gemm_auto<kPackedK, kEpiDx>(ta, tb, tb, tb, args, stream);
+  }
   return launch_gemm<kKGather, kEpiDx, 256>(ta, tb, args, stream);
 }
 

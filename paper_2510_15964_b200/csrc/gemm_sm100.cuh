@@ -5,6 +5,7 @@
 //
 // B operand modes (the neuron-sparse MLP of sf/neuron_ops.py:75-95):
 //   kDense   : B is K-major [N, K] (row n contiguous along K).
+//   kDenseMN : B is MN-major [K, N] (the torch.addmm weight layout), loaded as 64-column atoms.
 //   kNGather : B is K-major [d_ff, K]; the item's packed N columns are its
 //              active neuron blocks (ids[b][*]), each a contiguous run of `blk`
 //              rows of W1^T (fc1) or W2 (fc2 input-grad). One TMA box per block.
@@ -23,6 +24,14 @@
 // leader's full barrier; the MMA commits multicast to both CTAs' empty / accumulator barriers;
 // both CTAs' epilogue warps release the leader's accumulator barrier. Each CTA's TMEM holds its
 // 128 rows x BN columns, so the epilogue is the 1-CTA one.
+//
+// Wide pairs (CTAS = 2, BN = 512): a 256 x w tile (w <= 512) as two cta_group::2 MMAs per K step into one
+// 512-column accumulator. Per SM and K stage: 48 KB in, 8.4 MFLOP, which keeps the mainloop at the tcgen05
+// floor (~1040 cycles per 64-deep stage measured, tools/dense_trace.py) where the 128 x 256 single-CTA tile
+// (48 KB per 4.2 MFLOP) and the 256 x 256 pair run at ~70% of it. The epilogue is not overlapped (no second
+// accumulator), so it is kept to convert + store when there is no bias / LoRA term.
+// CL = 2 (two pairs per cluster sharing the B tile, multicast): measured no faster than pairs and the
+// 4-CTA clusters only fit 132 SMs; kept for tests / experiments (lx_gemm_set_cta_pair(4)).
 #pragma once
 #include "ptx.cuh"
 
@@ -31,11 +40,15 @@ namespace lx {
 // kPackedN / kPackedK: the same two gathers, but over an item-packed copy of the active rows
 // ([n_items, packed_stride, K|N], built once per layer by lx_pack_active_rows): one 256-row box
 // (N side) or four 64x64 boxes (K side) per stage instead of one 2 KB box per neuron block.
-enum BMode : int { kDense = 0, kNGather = 1, kKGather = 2, kPackedN = 3, kPackedK = 4 };
+enum BMode : int { kDense = 0, kNGather = 1, kKGather = 2, kPackedN = 3, kPackedK = 4, kDenseMN = 5 };
 template <int BMODE>
 LX_DEV constexpr bool is_ng() { return BMODE == kNGather || BMODE == kPackedN; }
 template <int BMODE>
 LX_DEV constexpr bool is_kg() { return BMODE == kKGather || BMODE == kPackedK; }
+template <int BMODE>
+LX_DEV constexpr bool is_dense() { return BMODE == kDense || BMODE == kDenseMN; }  // no counts, N / K from args
+template <int BMODE>
+LX_DEV constexpr bool b_mn() { return is_kg<BMODE>() || BMODE == kDenseMN; }  // B is MN-major [K, N] (64-col atoms)
 enum EpiKind : int {
   kEpiStoreF32 = 0,   // C (fp32)
   kEpiStoreBF16 = 1,  // C (bf16)
@@ -94,6 +107,7 @@ struct GemmArgs {
   int out_f32;          // store fp32 instead of bf16 (any epilogue except kEpiMask)
   const float* resid;   // fp32 [rows, ldo]: out = resid + value (fused residual add; requires out_f32)
   int packed_stride;    // kPacked*: rows per item in the packed weight copy
+  int spin;             // producer / MMA issuer poll (test_wait) instead of try_wait (set by the launcher)
   int a_k_split;        // kDense: A's K coordinate is k - a_k_split for k >= a_k_split (0: off). With B =
                         // [W_hi | W_lo] (segments a_k_split wide) one GEMM computes A W_hi + A W_lo.
 };
@@ -131,7 +145,8 @@ LX_DEV int item_n_tiles(const GemmArgs& a, int cnt, int wsel = 0) {
     const int w = wsel ? wsel : BN;
     return (cnt * a.blk + w - 1) / w;
   }
-  return (a.n_dense + BN - 1) / BN;
+  const int w = wsel ? wsel : BN;
+  return (a.n_dense + w - 1) / w;
 }
 
 template <int BMODE, int BN>
@@ -147,12 +162,12 @@ LX_DEV TileInfo decode_tile(const GemmArgs& a, const int* prefix, const int* cnt
   int local = t - prefix[lo];
   ti.mt = local % m_tiles;
   ti.nt = local / m_tiles;
-  int cnt = BMODE == kDense ? 0 : __ldg(cnts + lo);
+  int cnt = is_dense<BMODE>() ? 0 : __ldg(cnts + lo);
   int n_total = is_ng<BMODE>() ? cnt * a.blk : a.n_dense;
   // an item's active columns are split into equal-width tiles (multiples of 16, <= BN): no short last
   // tile whose CTA idles while the full ones finish
   int w = BN;
-  if (is_ng<BMODE>() && wsel) {
+  if (wsel) {
     w = wsel;  // wide pair tiles: uniform width chosen for the launch
   } else if (is_ng<BMODE>()) {
     const int nt_item = (n_total + BN - 1) / BN;
@@ -166,15 +181,25 @@ LX_DEV TileInfo decode_tile(const GemmArgs& a, const int* prefix, const int* cnt
   return ti;
 }
 
-template <int BMODE, int EPI, int BN, int CTAS = 1>
+template <int BMODE, int EPI, int BN, int CTAS = 1, int CL = 1>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, GemmArgs args) {
-  static_assert(CTAS == 1 || (BMODE == kDense || BMODE == kPackedN || BMODE == kPackedK), "CTA pairs: dense / packed B only");
+  static_assert(CTAS == 1 || (is_dense<BMODE>() || BMODE == kPackedN || BMODE == kPackedK), "CTA pairs: dense / packed B only");
+  static_assert(BMODE != kDenseMN || CTAS == 1 || BN > 256, "MN-major dense B: single CTA or wide pairs");
   using L = GemmSmem<BN, CTAS>;
   constexpr bool kWide = BN > 256;  // wide pair tiles (CTAS == 2, N-side gathers)
-  static_assert(!kWide || (CTAS == 2 && is_ng<BMODE>()), "wide tiles: CTA pairs over N-side gathers only");
+  static_assert(!kWide || (CTAS == 2 && (is_dense<BMODE>() || BMODE == kPackedN || BMODE == kPackedK)),
+                "wide tiles: CTA pairs, dense / packed B only");
+  // wide-tile width granularity: whole 32-row boxes per CTA half (N side), whole 64-column atoms (K side)
+  constexpr int kWq = b_mn<BMODE>() ? 128 : 64;
   constexpr int kAccBufs = 2 * BN <= 512 ? 2 : 1;  // TMEM accumulators (double-buffered when two fit)
+  static_assert(CL == 1 || (CTAS == 2 && !kWide), "pair clusters: CTA pairs, 256-column tiles");
   constexpr int TM = kBM * CTAS;  // rows per (pair) tile
+  // CL = 2: a cluster of two CTA pairs takes two adjacent row tiles of the same B tile; each CTA loads half of
+  // its B half and multicasts it to the matching CTA of the other pair (half the L2 -> SM bytes for B)
+  constexpr int TMc = TM * CL;  // rows per cluster tile
+  constexpr int kCluster = CTAS * CL;
+  const bool kSpin = args.spin != 0;  // producer / MMA issuer poll their barriers instead of try_wait
   constexpr int BNC = BN / CTAS;  // this CTA's share of the N tile
   constexpr int S = L::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -191,16 +216,17 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const uint32_t rank = CTAS == 2 ? cluster_ctarank() : 0;
-  const bool leader = rank == 0;
-  const int m_tiles = (args.rows_per_item + TM - 1) / TM;
-  const int t0 = blockIdx.x / CTAS, t_step = gridDim.x / CTAS;
+  const uint32_t rank = CTAS == 2 ? cluster_ctarank() : 0;  // rank * kBM: this CTA's rows in the cluster tile
+  const uint32_t prank = rank & 1, pidx = rank >> 1;       // rank in the pair, pair in the cluster
+  const bool leader = prank == 0;
+  const int m_tiles = (args.rows_per_item + TMc - 1) / TMc;
+  const int t0 = blockIdx.x / kCluster, t_step = gridDim.x / kCluster;
 
   if (warp == 0 && lane == 0) {
     gemm_stamp(0);
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
-    for (int i = 0; i < S; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+    for (int i = 0; i < S; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, CL); }
     for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, kEpiWarps * CTAS); }
     fence_mbar_init();
   }
@@ -213,14 +239,14 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   // ---- tile table: prefix[b] = first tile index of item b (counts are device-resident)
   // counts -> shared memory in one parallel round trip (the epilogue's staging area is free until the first tile)
   int* s_cnt = reinterpret_cast<int*>(smem + L::kEpiOff);
-  if (BMODE != kDense)
+  if (!is_dense<BMODE>())
     for (int b = threadIdx.x; b < args.n_items; b += blockDim.x) s_cnt[b] = __ldg(args.counts + b);
   __syncthreads();
   if (threadIdx.x == 0) {
     int wsel = 0;
     if (kWide) {  // narrowest multiple-of-64 width whose tiles fit in one round of pairs (else the widest)
-      const int pairs = gridDim.x / CTAS;
-      for (wsel = 64; wsel < BN; wsel += 64) {
+      const int pairs = gridDim.x / kCluster;
+      for (wsel = kWq; wsel < BN; wsel += kWq) {
         int tot = 0;
         for (int b = 0; b < args.n_items; ++b) tot += m_tiles * item_n_tiles<BMODE, BN>(args, s_cnt[b], wsel);
         if (tot <= pairs) break;
@@ -230,7 +256,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     int acc = 0;
     for (int b = 0; b < args.n_items; ++b) {
       prefix[b] = acc;
-      int cnt = (BMODE == kDense) ? 0 : s_cnt[b];
+      int cnt = is_dense<BMODE>() ? 0 : s_cnt[b];
       acc += m_tiles * item_n_tiles<BMODE, BN>(args, cnt, wsel);
     }
     prefix[args.n_items] = acc;
@@ -254,7 +280,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     uint32_t phase = 0;
     for (int t = t0; t < n_tiles_total; t += t_step) {
       TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t, wsel);
-      const int row0 = ti.item * args.rows_per_item + ti.mt * TM + rank * kBM;
+      const int row0 = ti.item * args.rows_per_item + ti.mt * TMc + rank * kBM;
       const int* ids = args.ids + (size_t)ti.item * args.ids_stride;
       int my_row = 0;  // kNGather: this lane's gathered W row (block id * blk), lane < nb
       int nb_n = 0;
@@ -272,22 +298,34 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           const int j = lane / (BN / 64);
           if (j < nb_k) my_k_row = __ldg(ids + kb0 + j) * args.blk;
         }
-        mbar_wait(empty + stage, phase ^ 1);
+        if (kSpin) mbar_spin(empty + stage, phase ^ 1);
+        else mbar_wait(empty + stage, phase ^ 1);
         if (CTAS == 2) {
           // pair: this CTA's A rows and half of B; bytes of both halves counted on the leader's barrier
           if (kWide) {
             // N split as two cta_group::2 MMAs: n1 = min(w, 256) columns, then n2; each CTA holds n1/2 + n2/2
             // rows of B (rows n0 + rank n1/2 .., then n0 + n1 + rank n2/2 ..), loaded as 32-row boxes
-            const int nm = (ti.n_cols + 63) / 64 * 64, n1 = nm < 256 ? nm : 256, n2 = nm - n1;
+            const int nm = (ti.n_cols + kWq - 1) / kWq * kWq, n1 = nm < 256 ? nm : 256, n2 = nm - n1;
             if (lane == 0) {
               if (leader) mbar_arrive_expect_tx(full + stage, 2 * (L::kABytes + (n1 / 2 + n2 / 2) * 128));
-              tma_load_2d_cg2(sa, &tmap_a, full + stage, ks * kBK, row0, pol_w);
-              const int b0 = ti.item * args.packed_stride + ti.n0;
-              for (int r0 = 0; r0 < n1 / 2; r0 += 32)
-                tma_load_2d_cg2(sb + r0 * 128, &tmap_b, full + stage, ks * kBK, b0 + rank * (n1 / 2) + r0, pol_w);
-              for (int r0 = 0; r0 < n2 / 2; r0 += 32)
-                tma_load_2d_cg2(sb + 128 * 128 + r0 * 128, &tmap_b, full + stage, ks * kBK, b0 + n1 + rank * (n2 / 2) + r0,
-                                pol_w);
+              const int ak =
+                  (is_dense<BMODE>() && args.a_k_split && ks * kBK >= args.a_k_split) ? ks * kBK - args.a_k_split : ks * kBK;
+              tma_load_2d_cg2(sa, &tmap_a, full + stage, ak, row0, pol_w);
+              if (!b_mn<BMODE>()) {  // K-major B (dense, packed N side): 32-row boxes
+                const int b0 = ti.item * args.packed_stride + ti.n0;
+                for (int r0 = 0; r0 < n1 / 2; r0 += 32)
+                  tma_load_2d_cg2(sb + r0 * 128, &tmap_b, full + stage, ks * kBK, b0 + prank * (n1 / 2) + r0, pol_w);
+                for (int r0 = 0; r0 < n2 / 2; r0 += 32)
+                  tma_load_2d_cg2(sb + 128 * 128 + r0 * 128, &tmap_b, full + stage, ks * kBK, b0 + n1 + prank * (n2 / 2) + r0,
+                                  pol_w);
+              } else {  // MN-major B ([64 K rows] x 64-column atoms of 8 KB)
+                const int k0 = ti.item * args.packed_stride + ks * kBK;
+                for (int c0 = 0; c0 < n1 / 2; c0 += 64)
+                  tma_load_2d_cg2(sb + c0 / 64 * (kBK * 128), &tmap_b, full + stage, ti.n0 + prank * (n1 / 2) + c0, k0, pol_w);
+                for (int c0 = 0; c0 < n2 / 2; c0 += 64)
+                  tma_load_2d_cg2(sb + 128 * 128 + c0 / 64 * (kBK * 128), &tmap_b, full + stage, ti.n0 + n1 + prank * (n2 / 2) + c0,
+                                  k0, pol_w);
+              }
             }
             __syncwarp();
             if (++stage == S) { stage = 0; phase ^= 1; }
@@ -295,14 +333,33 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           }
           if (lane == 0) {
             if (leader) mbar_arrive_expect_tx(full + stage, 2 * (L::kABytes + L::kBBytes));
-            tma_load_2d_cg2(sa, &tmap_a, full + stage, ks * kBK, row0, pol_w);
-            if (BMODE == kDense) tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.n0 + rank * BNC, pol_w);
-            if (BMODE == kPackedN)
-              tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.item * args.packed_stride + ti.n0 + rank * BNC, pol_w);
-            if (BMODE == kPackedK)
-              for (int a = 0; a < BNC / 64; ++a)
-                tma_load_2d_cg2(sb + a * (kBK * 128), &tmap_b, full + stage, ti.n0 + rank * BNC + a * 64,
-                                ti.item * args.packed_stride + ks * kBK, pol_w);
+            const int ak =
+                (is_dense<BMODE>() && args.a_k_split && ks * kBK >= args.a_k_split) ? ks * kBK - args.a_k_split : ks * kBK;
+            tma_load_2d_cg2(sa, &tmap_a, full + stage, ak, row0, pol_w);
+            if (CL == 1) {
+              if (BMODE == kDense) tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.n0 + prank * BNC, pol_w);
+              if (BMODE == kPackedN)
+                tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.item * args.packed_stride + ti.n0 + prank * BNC,
+                                pol_w);
+              if (BMODE == kPackedK)
+                for (int a = 0; a < BNC / 64; ++a)
+                  tma_load_2d_cg2(sb + a * (kBK * 128), &tmap_b, full + stage, ti.n0 + prank * BNC + a * 64,
+                                  ti.item * args.packed_stride + ks * kBK, pol_w);
+            } else {
+              // quarter of the B tile: rows (K-major) / 64-column atoms (MN-major) [pidx * BNC/2, +BNC/2) of this
+              // CTA's half, to this CTA and its counterpart in the other pair
+              const uint16_t mc = (uint16_t)((1u << prank) | (1u << (prank + 2)));
+              const int nq = ti.n0 + prank * BNC + pidx * (BNC / 2);
+              if (BMODE == kDense)
+                tma_load_2d_cg2_mc(sb + pidx * (BNC / 2) * 128, &tmap_b, full + stage, ks * kBK, nq, mc, pol_w);
+              if (BMODE == kPackedN)
+                tma_load_2d_cg2_mc(sb + pidx * (BNC / 2) * 128, &tmap_b, full + stage, ks * kBK,
+                                   ti.item * args.packed_stride + nq, mc, pol_w);
+              if (BMODE == kPackedK)
+                for (int a = 0; a < BNC / 128; ++a)
+                  tma_load_2d_cg2_mc(sb + (pidx * (BNC / 128) + a) * (kBK * 128), &tmap_b, full + stage, nq + a * 64,
+                                     ti.item * args.packed_stride + ks * kBK, mc, pol_w);
+            }
           }
           __syncwarp();
           if (++stage == S) { stage = 0; phase ^= 1; }
@@ -310,15 +367,18 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         }
         if (lane == 0) {
           uint32_t bytes = L::kABytes;
-          if (BMODE == kDense || BMODE == kPackedN || BMODE == kPackedK) bytes += BN * kBK * 2;
+          if (is_dense<BMODE>() || BMODE == kPackedN || BMODE == kPackedK) bytes += BN * kBK * 2;
           else if (BMODE == kNGather) bytes += nb_n * args.blk * kBK * 2;
           else bytes += nb_k * (BN / 64) * args.blk * 128;
           mbar_arrive_expect_tx(full + stage, bytes);
-          const int ak = (BMODE == kDense && args.a_k_split && ks * kBK >= args.a_k_split) ? ks * kBK - args.a_k_split : ks * kBK;
+          const int ak = (is_dense<BMODE>() && args.a_k_split && ks * kBK >= args.a_k_split) ? ks * kBK - args.a_k_split : ks * kBK;
           tma_load_2d(sa, &tmap_a, full + stage, ak, row0);
           if (BMODE == kDense) tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.n0, pol_w);
           if (BMODE == kPackedN)  // rows [nt*BN, nt*BN+BN) of this item's packed copy, one box
             tma_load_2d_hint(sb, &tmap_b, full + stage, ks * kBK, ti.item * args.packed_stride + ti.n0, pol_w);
+          if (BMODE == kDenseMN)  // 64 K-rows x BN columns: one box per 64-column atom
+            for (int a = 0; a < BN / 64; ++a)
+              tma_load_2d_hint(sb + a * (kBK * 128), &tmap_b, full + stage, ti.n0 + a * 64, ks * kBK, pol_w);
           if (BMODE == kPackedK)  // 64 packed K-rows x BN columns: one box per 64-column atom
             for (int a = 0; a < BN / 64; ++a)
               tma_load_2d_hint(sb + a * (kBK * 128), &tmap_b, full + stage, ti.n0 + a * 64,
@@ -352,12 +412,13 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         const uint32_t d_tmem = tmem_base + buf * BN;
         // pairs always run the full N (each CTA holds BN/2 of B; columns past n_cols are discarded)
         int n_mma = (is_ng<BMODE>() && CTAS == 1) ? ((ti.n_cols + 15) / 16) * 16 : BN;
-        const int nm_w = (ti.n_cols + 63) / 64 * 64, n1_w = nm_w < 256 ? nm_w : 256, n2_w = nm_w - n1_w;
+        const int nm_w = (ti.n_cols + kWq - 1) / kWq * kWq, n1_w = nm_w < 256 ? nm_w : 256, n2_w = nm_w - n1_w;
         if (kWide) n_mma = n1_w;
-        const uint32_t idesc = make_idesc_bf16(TM, n_mma, false, is_kg<BMODE>());
-        const uint32_t idesc2 = make_idesc_bf16(TM, n2_w > 0 ? n2_w : 16, false, false);
+        const uint32_t idesc = make_idesc_bf16(TM, n_mma, false, b_mn<BMODE>());
+        const uint32_t idesc2 = make_idesc_bf16(TM, n2_w > 0 ? n2_w : 16, false, b_mn<BMODE>());
         for (int ks = 0; ks < ti.k_stages; ++ks) {
-          mbar_wait(full + stage, phase);
+          if (kSpin) mbar_spin(full + stage, phase);
+          else mbar_wait(full + stage, phase);
           if (ks == 0 && it < 3) gemm_stamp(2 + 4 * it);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
@@ -366,18 +427,21 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           kk_n = (kk_n + 15) / 16;
           for (int kk = 0; kk < kk_n; ++kk) {
             uint64_t da = make_sdesc(sa + kk * 32, 16, 1024);
-            uint64_t db = is_kg<BMODE>() ? make_sdesc(sb + kk * 2048, kBK * 128, 1024) : make_sdesc(sb + kk * 32, 16, 1024);
+            uint64_t db = b_mn<BMODE>() ? make_sdesc(sb + kk * 2048, kBK * 128, 1024) : make_sdesc(sb + kk * 32, 16, 1024);
             if (CTAS == 2) mma_bf16_ss_cg2(d_tmem, da, db, idesc, (ks | kk) != 0);
             else mma_bf16_ss(d_tmem, da, db, idesc, (ks | kk) != 0);
-            if (kWide && n2_w > 0)  // second N part: B rows at +128 rows of this CTA's stage, accumulator columns 256..
-              mma_bf16_ss_cg2(d_tmem + 256, da, make_sdesc(sb + 128 * 128 + kk * 32, 16, 1024), idesc2, (ks | kk) != 0);
+            if (kWide && n2_w > 0)  // second N part: this CTA's B half at +16 KB of the stage, accumulator columns 256..
+              mma_bf16_ss_cg2(d_tmem + 256, da,
+                              b_mn<BMODE>() ? make_sdesc(sb + 128 * 128 + kk * 2048, kBK * 128, 1024)
+                                             : make_sdesc(sb + 128 * 128 + kk * 32, 16, 1024),
+                              idesc2, (ks | kk) != 0);
           }
-          if (CTAS == 2) mma_commit_cg2(empty + stage);
+          if (CTAS == 2) mma_commit_cg2(empty + stage, CL == 2 ? 0xF : 0x3);  // frees the stage in both pairs
           else mma_commit(empty + stage);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
         if (it < 3) gemm_stamp(3 + 4 * it);
-        if (CTAS == 2) mma_commit_cg2(tfull + buf);  // also fine with no MMA issued (arrives at once)
+        if (CTAS == 2) mma_commit_cg2(tfull + buf, (uint16_t)(3u << (2 * pidx)));  // this pair (also with no MMA)
         else if (ti.k_stages > 0) mma_commit(tfull + buf);
         else mbar_arrive(tfull + buf);
       }
@@ -394,14 +458,17 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       TileInfo ti = decode_tile<BMODE, BN>(args, prefix, cnts, m_tiles, t, wsel);
       const int buf = kAccBufs == 2 ? (it & 1) : 0;
       const int* ids = args.ids + (size_t)ti.item * args.ids_stride;
-      const int local_row = ti.mt * TM + rank * kBM + r_in_tile;
+      const int local_row = ti.mt * TMc + rank * kBM + r_in_tile;
       const bool row_ok = local_row < args.rows_per_item;
       const size_t grow = (size_t)ti.item * args.rows_per_item + local_row;
       const int r = args.lora_r;
       constexpr bool kLora = EPI == kEpiFc1 || EPI == kEpiFc1Raw || EPI == kEpiFc2 || EPI == kEpiDa || EPI == kEpiDx;
 
-      // stage per-column bias / LoRA column factors for this tile
-      if (kLora) {
+      // stage per-column bias / LoRA column factors for this tile (skipped when there are none: the plain
+      // product's epilogue is then convert + store only)
+      const int r_even = (r + 1) & ~1;  // the paired FMA below reads factor pairs (q, q + 1)
+      const bool cols = kLora && (args.bias != nullptr || (r > 0 && args.lora_w != nullptr));
+      if (cols) {
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
         for (int c = ep_tid; c < BN; c += 32 * kEpiWarps) {
           int j = ti.n0 + c;
@@ -409,11 +476,20 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           if (is_ng<BMODE>()) oc = (c < ti.n_cols) ? __ldg(ids + j / args.blk) * args.blk + j % args.blk : 0;
           bool ok = c < ti.n_cols;
           s_bias[c] = (ok && args.bias) ? __ldg(args.bias + oc) : 0.f;
-          for (int q = 0; q < kMaxR; ++q)
-            s_w[c * kMaxR + q] =
+          for (int q = 0; q < r_even; ++q)  // column pairs interleaved: [c/2][q][c&1] for the paired FMA below
+            s_w[(c >> 1) * 2 * kMaxR + 2 * q + (c & 1)] =
                 (ok && q < r && args.lora_w) ? __ldg(args.lora_w + q * args.w_sr + (long long)oc * args.w_sc) : 0.f;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      }
+      // staged bf16 stores: lane l writes rows 8p + l/4 (p = 0..3) of this warp's 32, 16 B at column 8(l%4)
+      __nv_bfloat16* st_row[4];
+#pragma unroll
+      for (int pss = 0; pss < 4; ++pss) {
+        const int lrow = ti.mt * TMc + rank * kBM + quad * 32 + pss * 8 + (lane >> 2);
+        st_row[pss] = lrow < args.rows_per_item ? reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                                      ((size_t)ti.item * args.rows_per_item + lrow) * args.ldo + 8 * (lane & 3)
+                                                : nullptr;
       }
       float xr[kMaxR];
 #pragma unroll
@@ -430,18 +506,21 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;
       const int n_chunks = (ti.n_cols + 31) / 32;
       constexpr int kHalf = BN / 64;  // 32-column chunks per column half
-      for (int ch = col_half * kHalf; ch < min(n_chunks, (col_half + 1) * kHalf); ++ch) {
-        uint32_t raw[32];
+      const int ch_lo = col_half * kHalf, ch_hi = min(n_chunks, (col_half + 1) * kHalf);
+      // software-pipelined: chunk ch + 1's TMEM load is in flight while chunk ch is processed
+      uint32_t raw[32];
+      if (ti.k_stages > 0 && ch_lo < ch_hi) tmem_ld_32x32b_x32(t_row + ch_lo * 32, raw);
+      for (int ch = ch_lo; ch < ch_hi; ++ch) {
+        float v[32];
         if (ti.k_stages > 0) {
-          tmem_ld_32x32b_x32(t_row + ch * 32, raw);
-          tmem_ld_wait();
+          tmem_ld_wait_regs(raw);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
+          if (ch + 1 < ch_hi) tmem_ld_32x32b_x32(t_row + (ch + 1) * 32, raw);
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) raw[i] = 0u;
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
         }
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
         const int c0 = ch * 32;
         const int nv = min(32, ti.n_cols - c0);
         const int j0 = ti.n0 + c0;  // packed / dense column of v[0]
@@ -463,25 +542,25 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           }
           continue;
         }
-        if (kLora && r == 0) {
+        if (kLora && cols && r == 0) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] += s_bias[c0 + i];
-        } else if (kLora) {
+        } else if (kLora && cols) {
+          // two columns per fma.rn.f32x2 (FFMA2): same per-column operation order as scalar fmaf, half the issue
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float* w = s_w + (c0 + i) * kMaxR;
-            float acc = v[i] + s_bias[c0 + i];
+          for (int i = 0; i < 32; i += 2) {
+            const float* w = s_w + (c0 + i) * kMaxR;  // pair (c0+i, c0+i+1), c0 + i even
+            float a0 = v[i] + s_bias[c0 + i], a1 = v[i + 1] + s_bias[c0 + i + 1];
 #pragma unroll
-            for (int q = 0; q < kMaxR; q += 4) {
+            for (int q = 0; q < kMaxR; q += 2) {
               if (q < r) {
-                float4 wq = *reinterpret_cast<const float4*>(w + q);
-                acc = fmaf(xr[q], wq.x, acc);
-                acc = fmaf(xr[q + 1], wq.y, acc);
-                acc = fmaf(xr[q + 2], wq.z, acc);
-                acc = fmaf(xr[q + 3], wq.w, acc);
+                float4 wq = *reinterpret_cast<const float4*>(w + 2 * q);  // (q,c) (q,c+1) (q+1,c) (q+1,c+1)
+                ffma2(a0, a1, xr[q], xr[q], wq.x, wq.y);
+                ffma2(a0, a1, xr[q + 1], xr[q + 1], wq.z, wq.w);
               }
             }
-            v[i] = acc;
+            v[i] = a0;
+            v[i + 1] = a1;
           }
         }
         if (EPI == kEpiFc1) {
@@ -555,13 +634,10 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           __syncwarp();
 #pragma unroll
           for (int pss = 0; pss < 4; ++pss) {
-            const int rr = pss * 8 + (lane >> 2), q = lane & 3;
-            const int lrow = ti.mt * TM + rank * kBM + quad * 32 + rr;
-            if (lrow < args.rows_per_item) {
-              const uint4 val = *reinterpret_cast<const uint4*>(stg + rr * kStgPitch + 16 * q);
-              __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) +
-                                 ((size_t)ti.item * args.rows_per_item + lrow) * args.ldo + j0 + 8 * q;
-              *reinterpret_cast<uint4*>(o) = val;
+            if (st_row[pss]) {
+              const uint4 val =
+                  *reinterpret_cast<const uint4*>(stg + (pss * 8 + (lane >> 2)) * kStgPitch + 16 * (lane & 3));
+              *reinterpret_cast<uint4*>(st_row[pss] + j0) = val;
             }
           }
           __syncwarp();

@@ -15,6 +15,8 @@
 // row splits on mma.sync (see colgrad_group_kernel below).
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -243,6 +245,86 @@ __global__ void __launch_bounds__(32 * kRpWarps, 2) rowproj_mma2_kernel(const __
       for (int w = 0; w < kRpWarps; ++w) v += s_red[w][rr][q];
       y[((size_t)item * s + row) * ldy + q] = v * scale;
       if (yb) yb[((size_t)item * s + row) * ldyb + q] = __float2bfloat16_rn(v * scale);
+    }
+  }
+}
+
+// Dense-K variant for K <= kRpsMaxK (the projections' LoRA down-products, K = d): the CTA's 16 rows of X are
+// fetched with one 1-D bulk copy per row into shared memory (rows padded to K + 32 elements: the lanes' 16-byte
+// fragment reads of rows g, g + 8 fall in distinct bank groups), so all of the CTA's X is in flight at once
+// instead of kRpU 32-k blocks per warp round trip; the MMAs then read A fragments from shared memory and the
+// hi/lo W pack from L1/L2 as above. Same k-slot mapping, same fixed-order warp reduction (identical results).
+constexpr int kRpsMaxK = 4096;
+template <int NT>
+__global__ void __launch_bounds__(32 * kRpWarps, 2) rowproj_smem_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int rows,
+                                                           int K, int Kp, int r, float scale,
+                                                           const __nv_bfloat16* __restrict__ wp, float* __restrict__ y,
+                                                           int ldy, __nv_bfloat16* __restrict__ yb, int ldyb) {
+  constexpr int RP = 8 * NT;
+  extern __shared__ __align__(128) uint8_t rps_smem[];
+  __shared__ float s_red[kRpWarps][16][RP + 1];
+  __shared__ __align__(8) uint64_t bar;
+  const int pitch = K + 32;  // elements
+  __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(rps_smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int row0 = blockIdx.x * 16;
+  const int nr = min(16, rows - row0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait_trigger();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bar, (uint32_t)nr * K * 2);
+    for (int i = 0; i < nr; ++i) bulk_load_1d(sx + (size_t)i * pitch, x + (size_t)(row0 + i) * ldx, K * 2, &bar);
+  }
+  // rows past the end (last CTA): zero in shared memory, never read from global
+  for (int i = nr + warp; i < 16; i += kRpWarps)
+    for (int c = lane * 8; c < K; c += 256) *reinterpret_cast<uint4*>(sx + (size_t)i * pitch + c) = make_uint4(0u, 0u, 0u, 0u);
+  const __nv_bfloat16* wh = wp + (size_t)g * Kp;
+  const __nv_bfloat16* wl = wh + (size_t)RP * Kp;
+  float acc[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const __nv_bfloat16* xa = sx + (size_t)g * pitch + 8 * t;
+  const __nv_bfloat16* xbp = xa + (size_t)8 * pitch;
+  for (int k0 = warp * 32; k0 < K; k0 += 32 * kRpWarps) {
+    const uint4 va = *reinterpret_cast<const uint4*>(xa + k0);
+    const uint4 vb = *reinterpret_cast<const uint4*>(xbp + k0);
+    const uint32_t a0[4] = {va.x, vb.x, va.y, vb.y};
+    const uint32_t a1[4] = {va.z, vb.z, va.w, vb.w};
+    const int kw = k0 + 8 * t;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const uint4 vh = __ldg(reinterpret_cast<const uint4*>(wh + (size_t)n * 8 * Kp + kw));
+      const uint4 vl = __ldg(reinterpret_cast<const uint4*>(wl + (size_t)n * 8 * Kp + kw));
+      mma16816_rp(acc[n], a0, vh.x, vh.y);
+      mma16816_rp(acc[n], a0, vl.x, vl.y);
+      mma16816_rp(acc[n], a1, vh.z, vh.w);
+      mma16816_rp(acc[n], a1, vl.z, vl.w);
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    const int q = n * 8 + t * 2;
+    s_red[warp][g][q] = acc[n][0];
+    s_red[warp][g][q + 1] = acc[n][1];
+    s_red[warp][g + 8][q] = acc[n][2];
+    s_red[warp][g + 8][q + 1] = acc[n][3];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 16 * RP; e += 32 * kRpWarps) {
+    const int rr = e / RP, q = e % RP, row = row0 + rr;
+    if (q < r && row < rows) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < kRpWarps; ++w) v += s_red[w][rr][q];
+      y[(size_t)row * ldy + q] = v * scale;
+      if (yb) yb[(size_t)row * ldyb + q] = __float2bfloat16_rn(v * scale);
     }
   }
 }
@@ -682,6 +764,21 @@ int lx_rowproj_packed(const uint16_t* x, int ldx, int n_items, int s, int K, con
   auto* ybf = reinterpret_cast<__nv_bfloat16*>(yb);
   const int items = counts ? n_items : 1, rows = counts ? s : n_items * s;
   dim3 grid((rows + 15) / 16, items);
+  static const bool use_smem = [] { const char* e = getenv("LX_ROWPROJ_SMEM"); return !(e && e[0] == '0'); }();
+  if (!counts && use_smem && K <= kRpsMaxK && K % 8 == 0 && ldx % 8 == 0) {
+    // dense K: X rows staged in shared memory by bulk copies (rowproj_smem_kernel)
+    const size_t smem = (size_t)16 * (K + 32) * 2;
+    if (RP == 8) {
+      static cudaError_t a = cudaFuncSetAttribute(rowproj_smem_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      LX_CHECK_CUDA(a);
+      launch_k(rowproj_smem_kernel<1>, grid, 32 * kRpWarps, smem, stream, xb, ldx, rows, K, K_full, r, scale, wp, y, ldy, ybf, ldyb);
+    } else {
+      static cudaError_t a = cudaFuncSetAttribute(rowproj_smem_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      LX_CHECK_CUDA(a);
+      launch_k(rowproj_smem_kernel<2>, grid, 32 * kRpWarps, smem, stream, xb, ldx, rows, K, K_full, r, scale, wp, y, ldy, ybf, ldyb);
+    }
+    return launch_check("rowproj_smem");
+  }
   if (RP == 8)
     launch_k(rowproj_mma2_kernel<1>, grid, 32 * kRpWarps, 0, stream, xb, ldx, rows, K, K_full, r, scale, counts, counts ? blk : 1, wp,
                                                                0, counts ? ids : nullptr, counts ? K / blk : 0, y, ldy, ybf, ldyb);

@@ -86,8 +86,27 @@ LX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 #endif
 }
+// pure polling (no suspend / wake latency), for the single-thread MMA issuer and TMA producer loops
+LX_DEV void mbar_spin(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_SPIN:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra LAB_SPIN;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 
 // ---------------------------------------------------------------- TMA
+// (d0, d1) = (a0 * b0 + d0, a1 * b1 + d1), one fma.rn.f32x2 (FFMA2): per lane identical to fmaf
+LX_DEV void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rd, {%0, %1};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rd;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "+f"(d0), "+f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
 LX_DEV void tma_prefetch_desc(const void* desc) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");
 }
@@ -137,9 +156,21 @@ LX_DEV void tma_load_2d_cg2(void* smem_dst, const void* desc, uint64_t* bar, int
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "l"(hint)
       : "memory");
 }
-// Arrive (release, cluster scope) on the leader CTA's copy of this barrier.
+// Same, multicast: the box lands at this smem offset in every CTA of `mask` (cluster ranks); each
+// destination's bytes are counted on the barrier of that destination's pair leader.
+LX_DEV void tma_load_2d_cg2_mc(void* smem_dst, const void* desc, uint64_t* bar, int32_t c0, int32_t c1, uint16_t mask,
+                               uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "h"(mask), "l"(hint)
+      : "memory");
+}
+// Arrive on the leader CTA's copy of this barrier. Default (CTA-scope release) semantics: the epilogue's
+// accumulator hand-back orders TMEM reads via tcgen05.fence::before_thread_sync, not memory; a cluster-scope
+// release here compiles to MEMBAR.ALL.GPU and made every tile's hand-back wait for its global stores to drain.
 LX_DEV void mbar_arrive_leader(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask) : "memory");
 }
 template <uint32_t kCols>
 LX_DEV void tmem_alloc_cg2(uint32_t* dst_smem) {  // one warp in each CTA of the pair (same warp id)
@@ -158,13 +189,13 @@ LX_DEV void mma_bf16_ss_cg2(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, u
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
 }
-// Arrive on this barrier offset in BOTH CTAs of the pair once the issued MMAs complete.
-LX_DEV void mma_commit_cg2(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
-          smem_u32(bar))
-      : "memory");
+// Arrive on this barrier offset in every CTA of `mask` (cluster ranks; the pair: 3 << its first rank) once
+// the issued MMAs complete.
+LX_DEV void mma_commit_cg2(uint64_t* bar, uint16_t mask = 3) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
 }
 // L2 cache-policy descriptors (createpolicy): weights are re-read by many CTAs.
 LX_DEV uint64_t policy_evict_last() {
@@ -235,6 +266,17 @@ LX_DEV void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 LX_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait, with the loaded registers as operands: no use of them can be scheduled above the wait (loads
+// issued ahead of the registers' consumer, software-pipelined epilogues)
+LX_DEV void tmem_ld_wait_regs(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+                 "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+                 "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
 
 // ---------------------------------------------------------------- UMMA descriptors
 // Shared-memory matrix descriptor (PTX "matrix descriptor", sm_100 version 1).

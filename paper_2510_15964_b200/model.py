@@ -534,15 +534,24 @@ def resolve_head_patterns(head_patterns, model_or_dpool, n_items: int, n_heads: 
 
 
 def linear(a: torch.Tensor, b_t: torch.Tensor, out_f32: bool = False, resid: torch.Tensor | None = None, bias=None,
-           lora_x=None, lora_w=None, w_sr: int = 0, w_sc: int = 0, r: int = 0, scaling: float = 1.0) -> torch.Tensor:
+           lora_x=None, lora_w=None, w_sr: int = 0, w_sc: int = 0, r: int = 0, scaling: float = 1.0, *,
+           kn: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
     """out = (resid) + a @ b_t^T + bias + scaling * lora_x . w on the tcgen05 GEMM (fused epilogue).
-    a bf16 [M, K] (any row stride), b_t bf16 [N, K] (K-major weight)."""
+    a bf16 [M, K] (any row stride), b_t bf16 [N, K] (K-major weight), or with kn=True the weight as
+    stored for a @ W: [K, N] (any row stride). bias fp32 [N]. `out` (optional) receives the result."""
     M, K = a.shape
-    N = b_t.shape[0]
-    out = torch.empty(M, N, dtype=torch.float32 if (out_f32 or resid is not None) else torch.bfloat16, device=a.device)
-    _abi.call("lx_linear", a.data_ptr(), a.stride(0), b_t.data_ptr(), b_t.stride(0), M, N, K, out.data_ptr(), out.stride(0),
-              int(out.dtype == torch.float32), _abi.ptr(resid), _abi.ptr(bias), _abi.ptr(lora_x), _abi.ptr(lora_w), w_sr,
-              w_sc, r if lora_x is not None else 0, float(scaling), _abi.stream_handle(a.device))
+    N = b_t.shape[1] if kn else b_t.shape[0]
+    if (b_t.shape[0] if kn else b_t.shape[1]) != K or b_t.stride(1) != 1 or a.stride(1) != 1:
+        raise ShapeError(f"linear shapes disagree: {tuple(a.shape)} x {tuple(b_t.shape)} (kn={kn})")
+    dt = torch.float32 if (out_f32 or resid is not None) else torch.bfloat16
+    if out is None:
+        out = torch.empty(M, N, dtype=dt, device=a.device)
+    elif out.dtype != dt or tuple(out.shape) != (M, N) or out.stride(1) != 1:
+        raise ShapeError(f"linear output {tuple(out.shape)} {out.dtype} does not match [{M}, {N}] {dt}")
+    _abi.call("lx_linear_kn" if kn else "lx_linear", a.data_ptr(), a.stride(0), b_t.data_ptr(), b_t.stride(0), M, N, K,
+              out.data_ptr(), out.stride(0), int(out.dtype == torch.float32), _abi.ptr(resid), _abi.ptr(bias),
+              _abi.ptr(lora_x), _abi.ptr(lora_w), w_sr, w_sc, r if lora_x is not None else 0, float(scaling),
+              _abi.stream_handle(a.device))
     return out
 
 

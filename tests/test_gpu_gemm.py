@@ -21,9 +21,10 @@ def rel(a, b):
     return ((a - b).abs().max() / b.abs().max().clamp_min(1e-30)).item()
 
 
-@pytest.fixture(params=[0, 1, 2], ids=["single_cta", "cta_pair_256", "cta_pair_128"])
+@pytest.fixture(params=[0, 1, 2, 4, 5], ids=["single_cta", "cta_pair_256", "cta_pair_128", "pair_cluster_mc", "wide_pair"])
 def engine(request):
-    """All GEMM engine variants: single-CTA tiles and CTA pairs (tcgen05.mma.cta_group::2), N 256 / 128."""
+    """All GEMM engine variants: single-CTA tiles, CTA pairs (tcgen05.mma.cta_group::2) with N 256 / 128, and
+    clusters of two pairs multicasting the B tile (mode 4)."""
     from paper_2510_15964_b200 import _abi
 
     prev = _abi.lib().lx_gemm_set_cta_pair(request.param)
@@ -183,9 +184,11 @@ def test_lora_skinny_kernels(gather, r, w_layout):
 
 
 @pytest.mark.parametrize("M,N,K,r,mode", [(4096, 6144, 2048, 16, "bf16"), (300, 520, 200, 8, "f32"), (512, 2048, 2048, 8, "resid"),
-                                          (256, 256, 64, 0, "bf16")])
-def test_linear_fused_epilogue(M, N, K, r, mode):
-    """lx_linear: out = (resid) + A B^T + bias + s * lora_x . w  (lora_linear_forward's fused dense product)."""
+                                          (256, 256, 64, 0, "bf16"), (4096, 2048, 2112, 0, "bf16"), (1000, 1000, 320, 3, "f32")])
+@pytest.mark.parametrize("kn", [False, True], ids=["b_nk", "b_kn"])
+def test_linear_fused_epilogue(M, N, K, r, mode, kn, engine):
+    """lx_linear / lx_linear_kn: out = (resid) + A B^T + bias + s * lora_x . w (lora_linear_forward's fused
+    dense product), weight K-major [N, K] or as stored for x @ W ([K, N], the projections' layout)."""
     from paper_2510_15964_b200 import model as Mo
 
     dev = _dev()
@@ -196,8 +199,11 @@ def test_linear_fused_epilogue(M, N, K, r, mode):
     lx = torch.randn(M, max(r, 1), generator=g).to(dev)
     lw = torch.randn(max(r, 1), N, generator=g).to(dev) * 0.1
     resid = torch.randn(M, N, generator=g).to(dev) if mode == "resid" else None
-    out = Mo.linear(a, bt, out_f32=mode != "bf16", resid=resid, bias=bias, lora_x=lx if r else None, lora_w=lw if r else None,
-                    w_sr=N, w_sc=1, r=r, scaling=0.5)
+    w = bt.t().contiguous() if kn else bt
+    if kn and N % 8:
+        pytest.skip("[K, N] weight rows need N % 8 == 0 (16-byte TMA row stride)")
+    out = Mo.linear(a, w, out_f32=mode != "bf16", resid=resid, bias=bias, lora_x=lx if r else None, lora_w=lw if r else None,
+                    w_sr=N, w_sc=1, r=r, scaling=0.5, kn=kn)
     ref = a.float() @ bt.float().T + bias
     if r:
         ref = ref + 0.5 * lx @ lw
