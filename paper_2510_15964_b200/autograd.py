@@ -5,7 +5,7 @@ input-grad runs the tcgen05 gather-GEMMs over the forward's index lists, the
 LoRA / BitFit gradients are deterministic skinny reductions over the packed
 active columns (inactive rows/columns stay exactly 0, sf/autograd.py:89-90),
 attention gradients flow through the block-sparse backward kernels only. The
-dense projection input-grads are library GEMMs (cuBLAS); the q/k/v LoRA term
+dense projection input-grads are plain library GEMMs (model.proj_t); the q/k/v LoRA term
 rides in the same GEMM by K-extension ([dqkv | dAx] x [W_qkv^T ; A^T]). Gradients are sums over the batch items (the
 reference harness sums per-item gradients and divides by the batch size,
 sf/harness.py:413-415).
@@ -236,7 +236,7 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
     g = _bf16(d_out.reshape(-1, d)).contiguous()
     # output projection: d_heads = g Wo^T (+ LoRA(wo) fused), grads of wo's LoRA / bias
     ad_o = lora.get("wo")
-    d_heads = torch.mm(g, lw.wo.t())  # plain library GEMM (cuBLAS), bf16
+    d_heads = M.proj_t(g, lw.wo)  # bf16
     dax_o = None
     if ad_o is not None:
         dax_o = rowproj(g, B, s, d, ad_o.b, 1, d, ad_o.rank, scale=ad_o.scaling)
@@ -273,10 +273,10 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
                 rowproj(dqkv[:, sl * d : (sl + 1) * d], B, s, d, ad.b, 1, d, r, scale=ad.scaling,
                         out=dax[:, j * r : (j + 1) * r])
     if ext:
-        dx = torch.mm(dqkv_full, lw.wqkv_ext[:d, :].t())
+        dx = M.proj_t(dqkv_full, lw.wqkv_ext[:d, :])
     else:
-        # dx = dqkv W_qkv^T (cuBLAS) + dax A_cat^T (rank-n*r update)
-        dx = torch.mm(dqkv, lw.wqkv.t())
+        # dx = dqkv W_qkv^T + dax A_cat^T (rank-n*r update)
+        dx = M.proj_t(dqkv, lw.wqkv)
         if tq:
             dx.addmm_(dax.to(torch.bfloat16), cache["a_cat"].t().to(torch.bfloat16))
     for j, t in enumerate(tq):

@@ -158,6 +158,12 @@ static int launch_packed_n(const CUtensorMap& ta, const uint16_t* wp, int n_item
 }
 
 
+// float32-faithful predictor GEMMs (hi/lo weight pair, one A read per K stage): 256 x 128 CTA-pair tiles
+int gemm_dual_launch(bool mask_epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
+  return mask_epi ? launch_gemm<kDenseDual, kEpiMask, 256, 2>(ta, tb, args, st)
+                  : launch_gemm<kDenseDual, kEpiStoreF32, 256, 2>(ta, tb, args, st);
+}
+
 static GemmArgs base_args(int n_items, int rows, int n_dense, int k_dense) {
   GemmArgs a;
   memset(&a, 0, sizeof(a));

@@ -40,13 +40,16 @@ namespace lx {
 // kPackedN / kPackedK: the same two gathers, but over an item-packed copy of the active rows
 // ([n_items, packed_stride, K|N], built once per layer by lx_pack_active_rows): one 256-row box
 // (N side) or four 64x64 boxes (K side) per stage instead of one 2 KB box per neuron block.
-enum BMode : int { kDense = 0, kNGather = 1, kKGather = 2, kPackedN = 3, kPackedK = 4, kDenseMN = 5 };
+// kDenseDual: K-major B holding a bf16 hi/lo pair [W_hi | W_lo] (the lo half at K offset args.dual_k): each stage
+// loads A once and B's hi and lo boxes, and issues two MMAs into one accumulator (A W_hi + A W_lo), so the
+// float32-faithful predictor GEMMs read A once instead of once per term. CTA pairs, N tile = BN / 2.
+enum BMode : int { kDense = 0, kNGather = 1, kKGather = 2, kPackedN = 3, kPackedK = 4, kDenseMN = 5, kDenseDual = 6 };
 template <int BMODE>
 LX_DEV constexpr bool is_ng() { return BMODE == kNGather || BMODE == kPackedN; }
 template <int BMODE>
 LX_DEV constexpr bool is_kg() { return BMODE == kKGather || BMODE == kPackedK; }
 template <int BMODE>
-LX_DEV constexpr bool is_dense() { return BMODE == kDense || BMODE == kDenseMN; }  // no counts, N / K from args
+LX_DEV constexpr bool is_dense() { return BMODE == kDense || BMODE == kDenseMN || BMODE == kDenseDual; }  // no counts
 template <int BMODE>
 LX_DEV constexpr bool b_mn() { return is_kg<BMODE>() || BMODE == kDenseMN; }  // B is MN-major [K, N] (64-col atoms)
 enum EpiKind : int {
@@ -110,6 +113,7 @@ struct GemmArgs {
   int spin;             // producer / MMA issuer poll (test_wait) instead of try_wait (set by the launcher)
   int a_k_split;        // kDense: A's K coordinate is k - a_k_split for k >= a_k_split (0: off). With B =
                         // [W_hi | W_lo] (segments a_k_split wide) one GEMM computes A W_hi + A W_lo.
+  int dual_k;           // kDenseDual: K coordinate of W_lo in B (k_dense = the K extent of A and of each half)
 };
 
 constexpr int kStgPitch = 80;  // bytes per staged row: 64 B of bf16 + 16 B pad (conflict-free 16 B writes)
@@ -145,7 +149,7 @@ LX_DEV int item_n_tiles(const GemmArgs& a, int cnt, int wsel = 0) {
     const int w = wsel ? wsel : BN;
     return (cnt * a.blk + w - 1) / w;
   }
-  const int w = wsel ? wsel : BN;
+  const int w = wsel ? wsel : (BMODE == kDenseDual ? BN / 2 : BN);
   return (a.n_dense + w - 1) / w;
 }
 
@@ -166,7 +170,7 @@ LX_DEV TileInfo decode_tile(const GemmArgs& a, const int* prefix, const int* cnt
   int n_total = is_ng<BMODE>() ? cnt * a.blk : a.n_dense;
   // an item's active columns are split into equal-width tiles (multiples of 16, <= BN): no short last
   // tile whose CTA idles while the full ones finish
-  int w = BN;
+  int w = BMODE == kDenseDual ? BN / 2 : BN;
   if (wsel) {
     w = wsel;  // wide pair tiles: uniform width chosen for the launch
   } else if (is_ng<BMODE>()) {
@@ -338,6 +342,11 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             tma_load_2d_cg2(sa, &tmap_a, full + stage, ak, row0, pol_w);
             if (CL == 1) {
               if (BMODE == kDense) tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.n0 + prank * BNC, pol_w);
+              if (BMODE == kDenseDual) {  // this CTA's BNC/2 rows of the N tile, hi then lo
+                tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.n0 + prank * (BNC / 2), pol_w);
+                tma_load_2d_cg2(sb + (BNC / 2) * 128, &tmap_b, full + stage, args.dual_k + ks * kBK, ti.n0 + prank * (BNC / 2),
+                                pol_w);
+              }
               if (BMODE == kPackedN)
                 tma_load_2d_cg2(sb, &tmap_b, full + stage, ks * kBK, ti.item * args.packed_stride + ti.n0 + prank * BNC,
                                 pol_w);
@@ -411,7 +420,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
         // pairs always run the full N (each CTA holds BN/2 of B; columns past n_cols are discarded)
-        int n_mma = (is_ng<BMODE>() && CTAS == 1) ? ((ti.n_cols + 15) / 16) * 16 : BN;
+        int n_mma = (is_ng<BMODE>() && CTAS == 1) ? ((ti.n_cols + 15) / 16) * 16 : (BMODE == kDenseDual ? BN / 2 : BN);
         const int nm_w = (ti.n_cols + kWq - 1) / kWq * kWq, n1_w = nm_w < 256 ? nm_w : 256, n2_w = nm_w - n1_w;
         if (kWide) n_mma = n1_w;
         const uint32_t idesc = make_idesc_bf16(TM, n_mma, false, b_mn<BMODE>());
@@ -430,6 +439,8 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             uint64_t db = b_mn<BMODE>() ? make_sdesc(sb + kk * 2048, kBK * 128, 1024) : make_sdesc(sb + kk * 32, 16, 1024);
             if (CTAS == 2) mma_bf16_ss_cg2(d_tmem, da, db, idesc, (ks | kk) != 0);
             else mma_bf16_ss(d_tmem, da, db, idesc, (ks | kk) != 0);
+            if (BMODE == kDenseDual)  // + A W_lo: the lo rows follow the hi rows in this CTA's B half
+              mma_bf16_ss_cg2(d_tmem, da, make_sdesc(sb + (BNC / 2) * 128 + kk * 32, 16, 1024), idesc, 1);
             if (kWide && n2_w > 0)  // second N part: this CTA's B half at +16 KB of the stage, accumulator columns 256..
               mma_bf16_ss_cg2(d_tmem + 256, da,
                               b_mn<BMODE>() ? make_sdesc(sb + 128 * 128 + kk * 2048, kBK * 128, 1024)

@@ -13,10 +13,19 @@
 //   OR over items (batch scope), nearest-cell upsample, integer coverage counts
 //   per pool pattern and the fp64 (mass/total >= tau - 1e-9) selection with the
 //   fewest-blocks / pool-order tie-break.
+#include <cstdlib>
 #include "common.cuh"
 #include "gemm_sm100.cuh"
 
 namespace lx {
+
+int gemm_dual_launch(bool mask_epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st);
+// LX_PRED_DUAL=0: the k_terms 2 scoring GEMMs as one K-extended GEMM (A re-read per term) instead of the dual
+// hi/lo CTA-pair engine (measurements)
+static bool pred_dual() {
+  static const bool on = [] { const char* e = getenv("LX_PRED_DUAL"); return !(e && e[0] == '0'); }();
+  return on;
+}
 
 constexpr int kCompactMaxWords = 512;  // n_blk <= 16384 neuron blocks
 
@@ -265,6 +274,27 @@ int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint
   const int bn = tiles256 < num_sms() ? 128 : 256;
   CUtensorMap ta, tb;
   int rc;
+  if (k_terms == 2 && pred_dual()) {
+    // h [M, d] read once per K stage against W_hi and W_lo (two MMAs into one accumulator), 256 x 128 pair tiles
+    if ((rc = make_tmap_bf16_2d(&ta, h, d, (uint64_t)n_items * s, d, kBK, kBM))) return rc;
+    if ((rc = make_tmap_bf16_2d(&tb, wa_t, 2 * d, n_blk, 2 * d, kBK, 64))) return rc;
+    GemmArgs args;
+    memset(&args, 0, sizeof(args));
+    args.n_items = n_items;
+    args.rows_per_item = s;
+    args.n_dense = n_blk;
+    args.k_dense = d;
+    args.dual_k = d;
+    args.blk = 16;
+    args.out = scores_dump;
+    args.ldo = n_blk;
+    args.thr = threshold;
+    args.bits = bits_ws;
+    args.bits_stride = words;
+    args.lora_scale = 1.f;
+    if ((rc = gemm_dual_launch(true, ta, tb, args, stream))) return rc;
+    return lx_mask_compact(bits_ws, n_items, n_blk, scope_batch, counts, ids, pos, stream);
+  }
   // k_terms 2: h [M, d] x [W_hi | W_lo]; 3: [x_hi | x_lo] [M, 2d] x [W_hi | W_lo | W_hi] (A's K wraps at d)
   const int a_cols = k_terms == 3 ? 2 * d : d, kt = k_terms * d;
   if ((rc = make_tmap_bf16_2d(&ta, h, a_cols, (uint64_t)n_items * s, a_cols, kBK, kBM))) return rc;
@@ -309,9 +339,31 @@ int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, i
   LX_REQUIRE(tau > 0 && tau <= 1, LX_ERR_SHAPE, "coverage tau must be in (0, 1]");
   LX_REQUIRE(k_terms >= 1 && k_terms <= 3 && (k_terms == 1 || d % 64 == 0), LX_ERR_SHAPE,
              "predict_attention_patterns: k_terms %d (1..3; split terms need d %% 64 == 0)", k_terms);
+  int rc;
+  if (k_terms == 2 && pred_dual()) {
+    // x_small [B*m, d] read once per K stage against W_hi and W_lo: B*m <= 256 rows fit one pair tile, so every
+    // weight row is streamed from HBM once
+    CUtensorMap ta, tb;
+    if ((rc = make_tmap_bf16_2d(&ta, x_small, d, (uint64_t)n_items * m, d, kBK, kBM))) return rc;
+    if ((rc = make_tmap_bf16_2d(&tb, wqk_t, 2 * d, 2 * H * r, 2 * d, kBK, 64))) return rc;
+    GemmArgs args;
+    memset(&args, 0, sizeof(args));
+    args.n_items = 1;
+    args.rows_per_item = n_items * m;
+    args.n_dense = 2 * H * r;
+    args.k_dense = d;
+    args.dual_k = d;
+    args.blk = 16;
+    args.out = proj_ws;
+    args.ldo = 2 * H * r;
+    args.out_f32 = 1;
+    args.lora_scale = 1.f;
+    rc = gemm_dual_launch(false, ta, tb, args, stream);
+  } else {
   // k_terms 2: x_small [M, d] x [W_hi | W_lo]; 3: [x_hi | x_lo] [M, 2d] x [W_hi | W_lo | W_hi]
-  int rc = lx_gemm_bf16_tn(x_small, k_terms == 3 ? 2 * d : d, wqk_t, k_terms * d, proj_ws, 2 * H * r, 1, n_items * m,
+  rc = lx_gemm_bf16_tn(x_small, k_terms == 3 ? 2 * d : d, wqk_t, k_terms * d, proj_ws, 2 * H * r, 1, n_items * m,
                            2 * H * r, k_terms * d, k_terms > 1 ? d : 0, stream);
+  }
   if (rc) return rc;
   dim3 grid(H, scope_batch ? 1 : n_items);
   const size_t smem = sizeof(float) * 2 * m * (r + 4);

@@ -573,6 +573,28 @@ def _qkv_lora(lora: dict, d: int):
     return tq, a_cat, r
 
 
+# The dense projections are plain library GEMMs (bias in the cuBLAS addmm). LX_PROJ_ENGINE=1 runs them on the
+# tcgen05 engine instead (lx_linear_kn / lx_linear, fp32 bias in the epilogue): measured 13% slower per GEMM inside
+# the cfg3 step (56.9 vs 49.7 us forward, 52.0 vs 46.0 us input-grad; +0.6 ms per step), so not default.
+_PROJ_CUBLAS = __import__("os").environ.get("LX_PROJ_ENGINE", "0") != "1"
+
+
+def _proj(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor, bias16=None) -> torch.Tensor:
+    """bf16 a @ w + bias for a projection weight stored [K, N] (sf/model.py:340-354): cuBLAS addmm with the bf16
+    bias, or (LX_PROJ_ENGINE=1) the tcgen05 engine with the fp32 bias in the epilogue (lx_linear_kn)."""
+    if _PROJ_CUBLAS:
+        return torch.addmm(bias16, a, w)
+    return linear(a, w, bias=bias, kn=True)
+
+
+def proj_t(a: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """bf16 a @ w^T for a projection weight stored [N, K] row-major (the input-grads dx = dy W^T,
+    sf/autograd.py:127-162): cuBLAS, or (LX_PROJ_ENGINE=1) lx_linear with w as the K-major operand."""
+    if _PROJ_CUBLAS:
+        return torch.mm(a, w.t())
+    return linear(a, w)
+
+
 def _bias_bf16(lw: LayerWeights, name: str, frozen: bool) -> torch.Tensor:
     """bf16 copy of a projection bias for the cuBLAS addmm; frozen biases (every PEFT method but BitFit)
     are converted once per storage instead of once per step."""
@@ -589,8 +611,8 @@ def _bias_bf16(lw: LayerWeights, name: str, frozen: bool) -> torch.Tensor:
 def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: ModelDims, counter=None, *, dpool=None,
                 x_ext=None, frozen_bias: bool = False):
     """Block-sparse multi-head attention (sf/model.py:322-360). x: LN1 output bf16 [B, s, d] (or [s, d]).
-    The dense projections are plain library GEMMs (cuBLAS, bias in the addmm); each LoRA delta
-    s*(xA)B is a rank-r cuBLAS update of its column slice with xA from the skinny rowproj kernel.
+    The dense projections are plain library GEMMs (_proj: cuBLAS, bias in the addmm); the q/k/v LoRA deltas
+    ride in the same GEMM by K-extension ([x | xA] x [W ; s B]), else each is a rank-r update of its column slice.
     Returns (out bf16 [B*s, d] = O Wo + bo (+ LoRA), cache); the cache holds O and the row LSE
     instead of probabilities. The residual add is fused into the next LayerNorm kernel."""
     x2, B, s = _items(x)
@@ -602,15 +624,15 @@ def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: Mode
     ext = bool(tq) and x_ext is not None and lp is not None and lp["kx"] > 0 and lp["tq"] == tuple(tq)
     # the concatenated A is only an operand of the unfused path (the fused one reads the packs)
     tq, a_cat, r = _qkv_lora(lora, d) if not ext else (tq, None, lora[tq[0]].rank)
-    bqkv16 = _bias_bf16(lw, "bqkv", frozen_bias)
+    bqkv16 = _bias_bf16(lw, "bqkv", frozen_bias) if _PROJ_CUBLAS else None
     ax = None
     if ext:
         # K-extended projection: x_ext = [x | xA_cat] (bf16 LoRA columns written by the rowproj), W_ext rows d.. = s*B
         kx = lp["kx"]
         ax = rowproj_packed(x_ext, B, s, d, lp["a_qkv"], kx, out_bf16=x_ext[:, d:])  # fp32 [M, n*r] for the LoRA grads
-        qkv = torch.addmm(bqkv16, x_ext, lw.wqkv_ext[: d + kx, : 3 * d])
+        qkv = _proj(x_ext, lw.wqkv_ext[: d + kx, : 3 * d], lw.bqkv, bqkv16)
     else:
-        qkv = torch.addmm(bqkv16, x2, lw.wqkv)  # bf16 [M, 3d]
+        qkv = _proj(x2, lw.wqkv, lw.bqkv, bqkv16)  # bf16 [M, 3d]
     if tq and not ext:
         ax = rowproj(x2, B, s, d, a_cat, a_cat.shape[1], 1, a_cat.shape[1])  # fp32 [M, n*r] (kept for the LoRA grads)
         axb = ax.to(torch.bfloat16)
@@ -622,7 +644,7 @@ def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: Mode
     if counter is not None:
         nnz = sum(dp_nnz(dp, int(i)) for i in pidx.flatten().tolist()) * (B if stride == 0 else 1)
         counter.add(2 * nnz * dims.attn_blk * dims.attn_blk * hd)
-    out = torch.addmm(_bias_bf16(lw, "bo", frozen_bias), o, lw.wo)  # bf16 [M, d]
+    out = _proj(o, lw.wo, lw.bo, _bias_bf16(lw, "bo", frozen_bias) if _PROJ_CUBLAS else None)  # bf16 [M, d]
     ad_o = lora.get("wo")
     ax_o = None
     if ad_o is not None:
