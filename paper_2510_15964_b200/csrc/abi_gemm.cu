@@ -85,7 +85,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   GemmArgs args = args_in;
   args.spin = spin;
   auto kern = gemm_sm100_kernel<BMODE, EPI, BN, CTAS, CL>;
-  constexpr int smem = GemmSmem<BN, CTAS>::kTotal;
+  constexpr int smem = GemmSmemFor<BMODE, BN, CTAS>::kTotal;
   constexpr int kCl = CTAS * CL;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kGemmThreads);

@@ -118,19 +118,24 @@ struct GemmArgs {
 
 constexpr int kStgPitch = 80;  // bytes per staged row: 64 B of bf16 + 16 B pad (conflict-free 16 B writes)
 
-template <int BN, int CTAS = 1>
+// LEAN (the dual predictor GEMMs: no bias / LoRA columns to stage): one more pipeline stage in place of the
+// LoRA column-factor area, i.e. more bytes in flight per SM for the HBM-streamed weights
+template <int BN, int CTAS = 1, bool LEAN = false>
 struct GemmSmem {
-  static constexpr int kStages = CTAS == 2 ? (BN > 256 ? 3 : BN >= 256 ? 5 : 7) : (BN >= 256 ? 3 : 5);
+  static constexpr int kStages = (CTAS == 2 ? (BN > 256 ? 3 : BN >= 256 ? 5 : 7) : (BN >= 256 ? 3 : 5)) + (LEAN ? 1 : 0);
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = (BN / CTAS) * kBK * 2;  // this CTA's share of the B tile
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOff = kStages * kStageBytes;
   static constexpr int kMiscOff = kBarOff + (2 * kStages + 4) * 8;
   static constexpr int kEpiOff = (kMiscOff + 16 + 4 * (kMaxItems + 2) + 127) / 128 * 128;  // + prefix, tile width
-  static constexpr int kEpiBytes = BN * 4 + BN * kMaxR * 4;
+  static constexpr int kEpiBytes = BN * 4 + (LEAN ? 0 : BN * kMaxR * 4);
   static constexpr int kStgOff = kEpiOff + kEpiBytes;  // per epilogue warp: 32 rows x kStgPitch
   static constexpr int kTotal = kStgOff + kEpiWarps * 32 * kStgPitch + 1024;  // + alignment slack
 };
+
+template <int BMODE, int BN, int CTAS>
+using GemmSmemFor = GemmSmem<BN, CTAS, BMODE == kDenseDual>;
 
 struct TileInfo {
   int item, mt, nt;
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, GemmArgs args) {
   static_assert(CTAS == 1 || (is_dense<BMODE>() || BMODE == kPackedN || BMODE == kPackedK), "CTA pairs: dense / packed B only");
   static_assert(BMODE != kDenseMN || CTAS == 1 || BN > 256, "MN-major dense B: single CTA or wide pairs");
-  using L = GemmSmem<BN, CTAS>;
+  using L = GemmSmemFor<BMODE, BN, CTAS>;
   constexpr bool kWide = BN > 256;  // wide pair tiles (CTAS == 2, N-side gathers)
   static_assert(!kWide || (CTAS == 2 && (is_dense<BMODE>() || BMODE == kPackedN || BMODE == kPackedK)),
                 "wide tiles: CTA pairs, dense / packed B only");
@@ -238,8 +243,11 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     if (CTAS == 2) tmem_alloc_cg2<512>(tmem_slot);
     else tmem_alloc<512>(tmem_slot);
   }
-  // prologue above overlaps the predecessor kernel's tail (programmatic dependent launch)
-  pdl_wait_trigger();
+  // prologue above overlaps the predecessor kernel's tail (programmatic dependent launch). kDenseDual: B (the
+  // frozen predictor weights) does not depend on the predecessor, so the first stages' B boxes are issued before
+  // the grid-dependency wait (below, after the cluster barrier that makes the leader's barriers valid)
+  constexpr bool kPreB = BMODE == kDenseDual && CL == 1;
+  if (!kPreB) pdl_wait_trigger();
   // ---- tile table: prefix[b] = first tile index of item b (counts are device-resident)
   // counts -> shared memory in one parallel round trip (the epilogue's staging area is free until the first tile)
   int* s_cnt = reinterpret_cast<int*>(smem + L::kEpiOff);
@@ -272,6 +280,23 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   const uint32_t tmem_base = *tmem_slot;
   const int n_tiles_total = prefix[args.n_items];
   const int wsel = *wsel_s;
+  int n_pre = 0;  // kPreB: stages of the first tile whose B boxes (and expect-tx) are already issued
+  if (kPreB) {
+    if (warp == 0 && t0 < n_tiles_total) {
+      const TileInfo ti = decode_tile<BMODE, BN>(args, prefix, args.counts, m_tiles, t0, wsel);
+      n_pre = min(S, ti.k_stages);
+      if (lane == 0) {
+        const uint64_t pol = policy_evict_last();
+        for (int ks = 0; ks < n_pre; ++ks) {
+          uint8_t* sb = smem + ks * L::kStageBytes + L::kABytes;
+          if (leader) mbar_arrive_expect_tx(full + ks, 2 * (L::kABytes + L::kBBytes));
+          tma_load_2d_cg2(sb, &tmap_b, full + ks, ks * kBK, ti.n0 + prank * (BNC / 2), pol);
+          tma_load_2d_cg2(sb + (BNC / 2) * 128, &tmap_b, full + ks, args.dual_k + ks * kBK, ti.n0 + prank * (BNC / 2), pol);
+        }
+      }
+    }
+    pdl_wait_trigger();
+  }
 
   // counts are needed by every role to decode tiles; read through L1 per decode.
   const int* cnts = args.counts;
@@ -335,7 +360,9 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             if (++stage == S) { stage = 0; phase ^= 1; }
             continue;
           }
-          if (lane == 0) {
+          if (lane == 0 && n_pre > 0) {  // kPreB: B and the expect-tx of this stage were issued before the wait
+            tma_load_2d_cg2(sa, &tmap_a, full + stage, ks * kBK, row0, pol_w);
+          } else if (lane == 0) {
             if (leader) mbar_arrive_expect_tx(full + stage, 2 * (L::kABytes + L::kBBytes));
             const int ak =
                 (is_dense<BMODE>() && args.a_k_split && ks * kBK >= args.a_k_split) ? ks * kBK - args.a_k_split : ks * kBK;
@@ -371,6 +398,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             }
           }
           __syncwarp();
+          if (n_pre > 0) --n_pre;
           if (++stage == S) { stage = 0; phase ^= 1; }
           continue;
         }
@@ -516,7 +544,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;
       const int n_chunks = (ti.n_cols + 31) / 32;
-      constexpr int kHalf = BN / 64;  // 32-column chunks per column half
+      constexpr int kHalf = (BMODE == kDenseDual ? BN / 2 : BN) / 64;  // 32-column chunks per column half
       const int ch_lo = col_half * kHalf, ch_hi = min(n_chunks, (col_half + 1) * kHalf);
       // software-pipelined: chunk ch + 1's TMEM load is in flight while chunk ch is processed
       uint32_t raw[32];
