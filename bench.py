@@ -306,7 +306,7 @@ def kernel_probe(model, engine, tok_dev, peaks: dict, config: str) -> tuple[dict
     only) and credit algorithmic units per launch:
       fc GEMMs   2 * s * d * sum_b counts_b * blk FLOPs
       attention  fwd 4 * sum_(b,h) nnz * attn_blk^2 * hd, bwd 8 * (...) FLOPs (reference MAC convention)
-      K1 mask    HBM bytes: MLP = M*d*2 (h2) + n_blk*d*2 (W_a) + outputs; attention = B*m*d*2 + 2*H*r*d*2.
+      K1 mask    HBM bytes: MLP = M*d*2 (h2) + n_blk*d*4 (fp32 W_a) + outputs; attention = B*m*d*2 + 2*H*r*d*4.
     Returns (dominant kernel's roofline object, per-kernel list)."""
     import torch
 
@@ -340,8 +340,9 @@ def kernel_probe(model, engine, tok_dev, peaks: dict, config: str) -> tuple[dict
         "lx_neuron_fc2_dgrad": ("tensor", fc_fl[::-1]), "lx_neuron_fc1_dgrad": ("tensor", fc_fl[::-1]),
         "lx_bsattn_fwd_tc": ("tensor", [4.0 * n * ab * ab * hd for n in att_nnz]),
         "lx_bsattn_bwd_tc": ("tensor", [8.0 * n * ab * ab * hd for n in att_nnz[::-1]]),
-        "lx_predict_mlp_mask": ("hbm", [float(B * s * d * 2 + dims.n_blk * d * 2 + 4 * B * (2 * dims.n_blk + 1))] * L),
-        "lx_predict_attention_patterns": ("hbm", [float(B * m * d * 2 + 2 * dims.n_heads * r_pred * d * 2 + 4 * B * dims.n_heads)] * L),
+        "lx_predict_mlp_mask": ("hbm", [float(B * s * d * 2 + dims.n_blk * d * 4 + 4 * B * (2 * dims.n_blk + 1))] * L),
+        # the predictor weights are float32 (sf/predictor.py): 4 B each, streamed as a bf16 hi/lo pair
+        "lx_predict_attention_patterns": ("hbm", [float(B * m * d * 2 + 2 * dims.n_heads * r_pred * d * 4 + 4 * B * dims.n_heads)] * L),
     }
     traffic_db = {}
     prof = ROOT / "profiles" / "r02_ncu_traffic.json"
@@ -370,6 +371,21 @@ def kernel_probe(model, engine, tok_dev, peaks: dict, config: str) -> tuple[dict
                                              else "HBM copy bandwidth"))
     dom["timing"] = "CUDA events around each launch of one eager step (all layers) on the launching stream, mean"
     return dom, out
+
+
+def k1_summary(kernels) -> dict | None:
+    """K1 (predictor scoring + exposer aggregation -> masks / patterns) per layer: both calls' time and algorithmic
+    HBM bytes (fp32 predictor weights, bf16 activations, index outputs) -> achieved GB/s against the HBM peak."""
+    k = [x for x in kernels or [] if x["kernel"].startswith("lx_predict")]
+    if not k:
+        return None
+    us = sum(x["ms_per_launch"] for x in k) * 1e3
+    by = sum(x["bytes_per_launch"] for x in k)
+    tr = [x.get("traffic") for x in k]
+    return {"calls": [x["kernel"] for x in k], "us_per_layer": round(us, 2), "bytes_per_layer": by,
+            "achieved": round(by / (us * 1e-6) / 1e9, 1), "unit": "GB/s", "peak": k[0]["peak"],
+            "frac": round(by / (us * 1e-6) / 1e9 / k[0]["peak"], 4),
+            "traffic": sum(tr) if all(t is not None for t in tr) else None}
 
 
 def run_ours(args, cfg, rank, world, dist):
@@ -495,6 +511,7 @@ def run_ours(args, cfg, rank, world, dist):
         "final_loss": round(losses[-1], 5),
         "clocks": clk.summary(),
         "roofline": roof,
+        "k1": k1_summary(kernels),
         "kernels": kernels,
         "cpu_baseline": cpu,
         **extra,
