@@ -254,24 +254,37 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   if (!is_dense<BMODE>())
     for (int b = threadIdx.x; b < args.n_items; b += blockDim.x) s_cnt[b] = __ldg(args.counts + b);
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
+    // warp-parallel: lane L tests the width (L + 1) * kWq, then a warp scan builds the item prefix
     int wsel = 0;
     if (kWide) {  // narrowest multiple-of-64 width whose tiles fit in one round of pairs (else the widest)
       const int pairs = gridDim.x / kCluster;
-      for (wsel = kWq; wsel < BN; wsel += kWq) {
+      const int w_l = ((int)lane + 1) * kWq;
+      bool fits = false;
+      if (w_l < BN) {
         int tot = 0;
-        for (int b = 0; b < args.n_items; ++b) tot += m_tiles * item_n_tiles<BMODE, BN>(args, s_cnt[b], wsel);
-        if (tot <= pairs) break;
+        for (int b = 0; b < args.n_items; ++b) tot += m_tiles * item_n_tiles<BMODE, BN>(args, s_cnt[b], w_l);
+        fits = tot <= pairs;
       }
+      const uint32_t fit_mask = __ballot_sync(0xffffffffu, fits);
+      wsel = fit_mask ? (__ffs(fit_mask)) * kWq : BN;
     }
-    *wsel_s = wsel;
-    int acc = 0;
-    for (int b = 0; b < args.n_items; ++b) {
-      prefix[b] = acc;
-      int cnt = is_dense<BMODE>() ? 0 : s_cnt[b];
-      acc += m_tiles * item_n_tiles<BMODE, BN>(args, cnt, wsel);
+    if (lane == 0) *wsel_s = wsel;
+    int carry = 0;
+    for (int b0 = 0; b0 < args.n_items; b0 += 32) {
+      const int b = b0 + (int)lane;
+      const int cnt = (b < args.n_items && !is_dense<BMODE>()) ? s_cnt[b] : 0;
+      const int nt = b < args.n_items ? m_tiles * item_n_tiles<BMODE, BN>(args, cnt, wsel) : 0;
+      int inc = nt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if ((int)lane >= o) inc += t;
+      }
+      if (b < args.n_items) prefix[b] = carry + inc - nt;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    prefix[args.n_items] = acc;
+    if (lane == 0) prefix[args.n_items] = carry;
   }
   tc_fence_before();
   __syncthreads();
