@@ -127,7 +127,9 @@ struct GemmSmem {
   static constexpr int kBBytes = (BN / CTAS) * kBK * 2;  // this CTA's share of the B tile
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOff = kStages * kStageBytes;
-  static constexpr int kMiscOff = kBarOff + (2 * kStages + 4) * 8;
+  // wide pair tiles re-cut the same ring into more, smaller stages when the launch's tile width is below BN
+  static constexpr int kMaxStg = (CTAS == 2 && BN > 256) ? 8 : kStages;
+  static constexpr int kMiscOff = kBarOff + (2 * kMaxStg + 4) * 8;
   static constexpr int kEpiOff = (kMiscOff + 16 + 4 * (kMaxItems + 2) + 127) / 128 * 128;  // + prefix, tile width
   static constexpr int kEpiBytes = BN * 4 + (LEAN ? 0 : BN * kMaxR * 4);
   static constexpr int kStgOff = kEpiOff + kEpiBytes;  // per epilogue warp: 32 rows x kStgPitch
@@ -210,12 +212,12 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   constexpr int kCluster = CTAS * CL;
   const bool kSpin = args.spin != 0;  // producer / MMA issuer poll their barriers instead of try_wait
   constexpr int BNC = BN / CTAS;  // this CTA's share of the N tile
-  constexpr int S = L::kStages;
+  constexpr int S0 = L::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
-  uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
+  uint64_t* empty = full + L::kMaxStg;
+  uint64_t* tfull = empty + L::kMaxStg;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kMiscOff);
   int* prefix = reinterpret_cast<int*>(smem + L::kMiscOff + 16);
@@ -235,7 +237,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     gemm_stamp(0);
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
-    for (int i = 0; i < S; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, CL); }
+    for (int i = 0; i < L::kMaxStg; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, CL); }
     for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, kEpiWarps * CTAS); }
     fence_mbar_init();
   }
@@ -293,6 +295,10 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   const uint32_t tmem_base = *tmem_slot;
   const int n_tiles_total = prefix[args.n_items];
   const int wsel = *wsel_s;
+  // pipeline ring: wide pairs hold A (16 KB) + this CTA's half of a wsel-wide B tile (64 B per column) per stage,
+  // so a narrower launch width gives more stages in flight over the same shared memory (latency-bound mainloop)
+  const int stage_bytes = (kWide && wsel) ? L::kABytes + 64 * wsel : L::kStageBytes;
+  const int S = kWide ? min(L::kMaxStg, (S0 * L::kStageBytes) / stage_bytes) : S0;
   int n_pre = 0;  // kPreB: stages of the first tile whose B boxes (and expect-tx) are already issued
   if (kPreB) {
     if (warp == 0 && t0 < n_tiles_total) {
@@ -301,7 +307,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       if (lane == 0) {
         const uint64_t pol = policy_evict_last();
         for (int ks = 0; ks < n_pre; ++ks) {
-          uint8_t* sb = smem + ks * L::kStageBytes + L::kABytes;
+          uint8_t* sb = smem + ks * stage_bytes + L::kABytes;
           if (leader) mbar_arrive_expect_tx(full + ks, 2 * (L::kABytes + L::kBBytes));
           tma_load_2d_cg2(sb, &tmap_b, full + ks, ks * kBK, ti.n0 + prank * (BNC / 2), pol);
           tma_load_2d_cg2(sb + (BNC / 2) * 128, &tmap_b, full + ks, args.dual_k + ks * kBK, ti.n0 + prank * (BNC / 2), pol);
@@ -331,7 +337,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         if ((int)lane < nb_n) my_row = __ldg(ids + ti.n0 / args.blk + lane) * args.blk;
       }
       for (int ks = 0; ks < ti.k_stages; ++ks) {
-        uint8_t* sa = smem + stage * L::kStageBytes;
+        uint8_t* sa = smem + stage * stage_bytes;
         uint8_t* sb = sa + L::kABytes;
         int nb_k = 0, my_k_row = 0;
         if (BMODE == kKGather) {
@@ -471,7 +477,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           else mbar_wait(full + stage, phase);
           if (ks == 0 && it < 3) gemm_stamp(2 + 4 * it);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t sa = smem_u32(smem + stage * stage_bytes);
           const uint32_t sb = sa + L::kABytes;
           int kk_n = min(kBK, ti.k_total - ks * kBK);
           kk_n = (kk_n + 15) / 16;
