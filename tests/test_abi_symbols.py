@@ -45,3 +45,16 @@ def test_error_mapping_without_gpu():
     with pytest.raises(E.LayoutError):  # gather_rows must be a power of two in [16, 128]
         _abi.call("lx_bsattn_fwd_tc", None, 192, 1, 128, 1, 64, None, 0, None, 48, 0.125, None, 64, None, None)
     assert issubclass(E.LayoutError, ValueError) and issubclass(E.MaskError, ValueError)
+
+
+def test_integration_bindings_match_the_abi_table():
+    """Every ctypes binding shown in INTEGRATION.md has the argument types of the package's own table."""
+    from paper_2510_15964_b200 import _abi
+
+    text = (ROOT / "INTEGRATION.md").read_text()
+    alias = {"P": _abi._P, "I": _abi._I, "F": _abi._F, "D": _abi._D, "C.c_longlong": _abi._LL}
+    found = re.findall(r"_lib\.(lx_\w+)\.argtypes = \[([^\]]*)\]", text)
+    assert len(found) >= 10
+    for name, args in found:
+        types = [alias[a.strip()] for a in args.split(",")]
+        assert types == list(_abi.SIGNATURES[name]), name
