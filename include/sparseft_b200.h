@@ -246,13 +246,14 @@ int lx_debug_set_attn_trace(unsigned long long* buf);
  * adapter_forward / adapter_backward (sf/model.py:76-83,315-319; sf/autograd.py:69-75), fp32 like the reference.
  * x fp32 [M, d] (row stride ldx), w_down [d, r], b_down [r], w_up [r, d], b_up [d]; r in {8, 16}.
  * fwd: out = x + relu(x w_down + b_down) w_up + b_up (row stride ldo); z = x w_down + b_down fp32 [M, r] is kept
- *      for the backward.
+ *      for the backward. resid (optional, fp32, row stride ldr): out = resid + (that), the block's residual add
+ *      (sf/model.py:420-427) fused.
  * bwd: dh = (dy w_up^T) * (z > 0) (fp32 [M, r] out), dx = dy + dh w_down^T (row stride lddx); the gradients of
  *      w_down, b_down, w_up, b_up summed over the rows (fixed order) times `scale`; ws: lx_adapter_ws_floats(d, r)
  *      floats. */
 long long lx_adapter_ws_floats(int d, int r);
 int lx_adapter_fwd(const float* x, int ldx, int M, int d, int r, const float* w_down, const float* b_down, const float* w_up,
-                   const float* b_up, float* z, float* out, int ldo, lx_stream_t stream);
+                   const float* b_up, float* z, float* out, int ldo, const float* resid, int ldr, lx_stream_t stream);
 int lx_adapter_bwd(const float* dy, int ldy, const float* x, int ldx, int M, int d, int r, const float* z,
                    const float* w_down, const float* w_up, float* dh, float* dx, int lddx, float* ws, float scale,
                    float* g_w_down, float* g_b_down, float* g_w_up, float* g_b_up, lx_stream_t stream);

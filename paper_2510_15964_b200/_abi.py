@@ -50,7 +50,7 @@ SIGNATURES: dict[str, list] = {
     "lx_bsattn_bwd_tc": [_P, _I, _I, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P],
     "lx_debug_set_attn_trace": [_P],
     "lx_adapter_ws_floats": [_I, _I],
-    "lx_adapter_fwd": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P],
+    "lx_adapter_fwd": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _I, _P],
     "lx_adapter_bwd": [_P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _F, _P, _P, _P, _P, _P],
     "lx_layernorm_fwd": [_P, _P, _P, _I, _I, _P, _P, _F, _P, _I, _P, _P, _I, _I, _P, _P],
     "lx_cross_entropy": [_P, _I, _I, _P, _F, _P, _P, _P],

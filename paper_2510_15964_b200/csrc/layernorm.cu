@@ -99,7 +99,14 @@ __global__ void __launch_bounds__(kLnThreads) ln_bwd_kernel(const void* __restri
   const size_t row = blockIdx.x;
   const float mu = mean[row], is = istd[row];
   const int nv = d / 4;
-  float4 gv[kLnMaxVec], xh[kLnMaxVec];
+  float4 gv[kLnMaxVec], xh[kLnMaxVec], cur[kLnMaxVec];
+  float4* o = reinterpret_cast<float4*>(dx + row * d);
+  // the accumulator row is loaded with the inputs (one DRAM round trip per row, not two around the block sums)
+#pragma unroll
+  for (int i = 0; i < kLnMaxVec; ++i) {
+    const int c = threadIdx.x + i * kLnThreads;
+    cur[i] = c < nv ? o[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
   for (int i = 0; i < kLnMaxVec; ++i) {
@@ -130,15 +137,14 @@ __global__ void __launch_bounds__(kLnThreads) ln_bwd_kernel(const void* __restri
   for (int i = 0; i < kLnMaxVec; ++i) {
     int c = threadIdx.x + i * kLnThreads;
     if (c < nv) {
-      float4* o = reinterpret_cast<float4*>(dx + row * d) + c;
-      float4 cur = *o;
-      cur.x += is * (gv[i].x - mg - xh[i].x * mgx);
-      cur.y += is * (gv[i].y - mg - xh[i].y * mgx);
-      cur.z += is * (gv[i].z - mg - xh[i].z * mgx);
-      cur.w += is * (gv[i].w - mg - xh[i].w * mgx);
-      *o = cur;
+      cur[i].x += is * (gv[i].x - mg - xh[i].x * mgx);
+      cur[i].y += is * (gv[i].y - mg - xh[i].y * mgx);
+      cur[i].z += is * (gv[i].z - mg - xh[i].z * mgx);
+      cur[i].w += is * (gv[i].w - mg - xh[i].w * mgx);
+      o[c] = cur[i];
       if (dx_bf16)  // bf16 copy of the updated residual gradient: the next GEMMs' operand
-        *reinterpret_cast<uint2*>(dx_bf16 + row * d + 4 * c) = make_uint2(pack_bf16x2(cur.x, cur.y), pack_bf16x2(cur.z, cur.w));
+        *reinterpret_cast<uint2*>(dx_bf16 + row * d + 4 * c) =
+            make_uint2(pack_bf16x2(cur[i].x, cur[i].y), pack_bf16x2(cur[i].z, cur[i].w));
     }
   }
 }

@@ -494,16 +494,21 @@ def layernorm_forward(x, gamma, beta, eps: float = 1e-5, x_small_spec=None, delt
                "y_ext": y_ext if ext_cols else None}
 
 
-def adapter_forward(x: torch.Tensor, ad: AdapterLayer):
+def adapter_forward(x: torch.Tensor, ad: AdapterLayer, resid: torch.Tensor | None = None):
     """x + relu(x Wd + bd) Wu + bu (sf/model.py:315-319) on the fp32 adapter kernel (csrc/adapter.cu); the cache
-    keeps x, the pre-activation z and h = relu(z)."""
+    keeps x, the pre-activation z and h = relu(z). With `resid` (fp32 [M, d]) the result is resid + adapter(x): the
+    block's residual add (sf/model.py:420-427) fused into the kernel's store."""
     x = x.float().contiguous()
     M, d = x.shape
     r = ad.w_down.shape[1]
     z = torch.empty(M, r, dtype=torch.float32, device=x.device)
     out = torch.empty_like(x)
+    rs = resid.reshape(M, d) if resid is not None else None
+    if rs is not None and (rs.dtype != torch.float32 or rs.stride(1) != 1):
+        raise ShapeError("adapter residual must be fp32 with unit column stride")
     _abi.call("lx_adapter_fwd", x.data_ptr(), d, M, d, r, ad.w_down.data_ptr(), ad.b_down.data_ptr(), ad.w_up.data_ptr(),
-              ad.b_up.data_ptr(), z.data_ptr(), out.data_ptr(), d, _abi.stream_handle(x.device))
+              ad.b_up.data_ptr(), z.data_ptr(), out.data_ptr(), d, _abi.ptr(rs), rs.stride(0) if rs is not None else 0,
+              _abi.stream_handle(x.device))
     return out, {"x": x, "z": z, "h": torch.relu(z)}
 
 
@@ -733,8 +738,9 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
                           frozen_bias=model.peft_method != "bitfit")
     caa = None
     if adapter:
-        att, caa = adapter_forward(att.float(), model.adapters[(layer, "attn")])
-        h2, c2 = layernorm_forward(x2 + att, lw.ln2_g, lw.ln2_b)
+        # y = x + adapter(attn): the residual add fused into the adapter kernel's store
+        y_att, caa = adapter_forward(att, model.adapters[(layer, "attn")], resid=x2)
+        h2, c2 = layernorm_forward(y_att.view(B, s, d), lw.ln2_g, lw.ln2_b)
     else:
         # y = x + attn fused into the LN2 kernel (fp32 y returned as the LN cache input)
         h2, c2 = layernorm_forward(x2, lw.ln2_g, lw.ln2_b, delta=att)
@@ -745,8 +751,8 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
     mo, cm = mlp_forward(h2v, lw, lora, nm, model.dims, counter, out_f32=adapter)
     cma = None
     if adapter:
-        mo, cma = adapter_forward(mo, model.adapters[(layer, "mlp")])
-        out = (y + mo).view(B, s, d)
+        out, cma = adapter_forward(mo, model.adapters[(layer, "mlp")], resid=y)
+        out = out.view(B, s, d)
     else:
         out = PendingResidual(y.view(B, s, d), mo)
     cache = {"ln1": c1, "attn": ca, "attn_adapter": caa, "ln2": c2, "mlp": cm, "mlp_adapter": cma,

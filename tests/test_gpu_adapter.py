@@ -45,6 +45,10 @@ def test_adapter_kernels_match_float64(dev, M, d, r):
     assert rel(grads["a.b_up"], DY.sum(0)) < 1e-5
     assert rel(grads["a.w_down"], X.t() @ dh) < 1e-5
     assert rel(grads["a.b_down"], dh.sum(0)) < 1e-5
+    res = torch.randn(M, d, generator=g).to(dev)
+    out_r, _ = M_.adapter_forward(x, ad, resid=res)  # fused residual add: bitwise resid + out
+    torch.cuda.synchronize()
+    assert torch.equal(out_r, res + out)
     grads2 = {}
     AG.adapter_backward(dy, ad, cache, grads2, "a")
     for k in grads:

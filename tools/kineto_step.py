@@ -17,7 +17,7 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 import bench  # noqa: E402
 from paper_2510_15964_b200.engine import FinetuneEngine  # noqa: E402
 
-args = [a for a in sys.argv[1:] if not a.startswith("--") and not a.isdigit()]
+args = [a for i, a in enumerate(sys.argv[1:]) if not a.startswith("--") and not a.isdigit() and sys.argv[i] != "--peft"]
 cfg = bench.CONFIGS[args[0] if args else "cfg3"]
 graph = "--graph" in sys.argv
 dev = torch.device("cuda", 0)
@@ -25,7 +25,8 @@ if "--pair" in sys.argv:  # GEMM engine variant (lx_gemm_set_cta_pair): 0 single
     from paper_2510_15964_b200 import _abi
 
     _abi.lib().lx_gemm_set_cta_pair(int(sys.argv[sys.argv.index("--pair") + 1]))
-model, state, prov = bench.build_workload(cfg, dev, 0, 0.85, 0.75)
+peft = sys.argv[sys.argv.index("--peft") + 1] if "--peft" in sys.argv else "lora"
+model, state, prov = bench.build_workload(cfg, dev, 0, 0.85, 0.75, peft=peft)
 eng = FinetuneEngine(model, state, prov, lr=1e-4)
 tok = torch.randint(0, cfg["V"], (cfg["B"], cfg["s"] + 1), device=dev)
 if graph:
