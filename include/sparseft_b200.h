@@ -81,7 +81,8 @@ int lx_linear_kn(const uint16_t* a, int lda, const uint16_t* b, int ldb, int M, 
  *          3: h = [x_hi | x_lo] bf16 [n_items*s, 2d] and wa_t = [W_hi | W_lo | W_hi]: an fp32 x and fp32 W
  *             (the reference-API call on host float32 inputs). Split terms need d % 64 == 0.
  * scope_batch: 0 = per-item masks (sf/harness.py:204-211), 1 = OR over items (sf/predictor.py:132-136)
- * bits_ws: uint32 [n_items, ceil(n_blk/32)] workspace
+ * bits_ws: uint32 [n_items, ceil(s/32), ceil(n_blk/32)] workspace: one word per (32-token group, 32 blocks), each
+ *          stored exactly once by the scoring GEMM (no memset, no atomics); the compaction ORs the groups
  * counts: int32 [n_items]; ids: int32 [n_items, n_blk] ascending active block ids;
  * pos:    int32 [n_items, n_blk] packed position of each block or -1
  * scores_dump: optional fp32 [n_items*s, n_blk] copy of S_hat (parity tests) */

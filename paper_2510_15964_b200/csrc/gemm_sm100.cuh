@@ -105,8 +105,9 @@ struct GemmArgs {
   const __nv_bfloat16* act;  // kEpiDa: packed relu output a (same layout as out)
   int ld_act;
   float thr;            // kEpiMask
-  uint32_t* bits;       // kEpiMask: [n_items, bits_stride] words
+  uint32_t* bits;       // kEpiMask: [n_items, bits_slots, bits_stride] words: slot t = rows [32t, 32t + 32) of the item
   int bits_stride;
+  int bits_slots;       // ceil(rows_per_item / 32); every (slot, word) is stored exactly once (no atomics, no memset)
   int out_f32;          // store fp32 instead of bf16 (any epilogue except kEpiMask)
   const float* resid;   // fp32 [rows, ldo]: out = resid + value (fused residual add; requires out_f32)
   int packed_stride;    // kPacked*: rows per item in the packed weight copy
@@ -591,7 +592,10 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             uint32_t bal = __ballot_sync(0xffffffffu, act);
             if (bal) word |= 1u << i;
           }
-          if (lane == 0 && word) atomicOr(args.bits + (size_t)ti.item * args.bits_stride + j0 / 32, word);
+          // this warp's 32 rows are one slot: a plain store of the word (the compaction ORs the slots)
+          const int slot = (ti.mt * TMc + rank * kBM + quad * 32) / 32;
+          if (lane == 0 && slot < args.bits_slots)
+            args.bits[((size_t)ti.item * args.bits_slots + slot) * args.bits_stride + j0 / 32] = word;
           if (args.out && row_ok) {
             float* o = reinterpret_cast<float*>(args.out) + grow * args.ldo + j0;
 #pragma unroll

@@ -1,11 +1,12 @@
 // K1 — predictor scoring + prolonged-range aggregation -> compacted index lists.
 //
 // MLP (sf/predictor.py:121-139, sf/neuron_ops.py:67-72):
-//   S = h * Wa_hat on tcgen05 (gemm_sm100, kEpiMask epilogue): each tile ORs
-//   (S > thr) over its rows with warp ballots and publishes one 32-bit word per
-//   (item, 32 blocks) with atomicOr (idempotent => deterministic). A compaction
-//   kernel turns the bitmask into ascending active-block ids, counts and the
-//   inverse map pos[item][blk] (packed position or -1).
+//   S = h * Wa_hat on tcgen05 (gemm_sm100, kEpiMask epilogue): each epilogue warp ORs
+//   (S > thr) over its 32 rows with ballots and stores one 32-bit word per
+//   (item, 32-row group, 32 blocks) -- every word stored exactly once, so no memset and
+//   no atomics. The compaction kernel ORs an item's groups and turns the bitmask into
+//   ascending active-block ids, counts and the inverse map pos[item][blk] (packed
+//   position or -1): two launches per call.
 // Attention (sf/predictor.py:62-118, sf/exposer.py:71-85):
 //   [Q_hat | K_hat] = X_small * [Wq_hat | Wk_hat] for every head at once (one
 //   tcgen05 GEMM), then one CTA per (item, head): S_hat = Q_hat K_hat^T (fp32),
@@ -32,8 +33,10 @@ constexpr int kCompactMaxWords = 512;  // n_blk <= 16384 neuron blocks
 // bits -> ascending active ids, counts and the inverse map, one CTA per item, fully parallel:
 // per-word popcounts, one warp's exclusive scan over the words, then one thread per block writes
 // its id at (word prefix + popc of the lower bits of its word). No serial per-bit loop.
+// bits [n_items, n_slots, words]: an item's mask is the OR of its slots (the scoring GEMM's 32-row groups)
 __global__ void mask_compact_kernel(const uint32_t* __restrict__ bits, int n_items, int n_blk, int scope_batch,
-                                    int32_t* __restrict__ counts, int32_t* __restrict__ ids, int32_t* __restrict__ pos) {
+                                    int n_slots, int32_t* __restrict__ counts, int32_t* __restrict__ ids,
+                                    int32_t* __restrict__ pos) {
   pdl_wait_trigger();
   const int item = blockIdx.x;
   const int words = (n_blk + 31) / 32;
@@ -42,11 +45,9 @@ __global__ void mask_compact_kernel(const uint32_t* __restrict__ bits, int n_ite
   __shared__ int s_total;
   for (int w = threadIdx.x; w < words; w += blockDim.x) {
     uint32_t v = 0;
-    if (scope_batch) {
-      for (int b = 0; b < n_items; ++b) v |= bits[(size_t)b * words + w];
-    } else {
-      v = bits[(size_t)item * words + w];
-    }
+    const int b0 = scope_batch ? 0 : item, b1 = scope_batch ? n_items : item + 1;
+    for (int b = b0; b < b1; ++b)
+      for (int t = 0; t < n_slots; ++t) v |= bits[((size_t)b * n_slots + t) * words + w];
     if (w == words - 1 && (n_blk & 31)) v &= (1u << (n_blk & 31)) - 1u;
     s_v[w] = v;
   }
@@ -256,7 +257,13 @@ int lx_mask_compact(const uint32_t* bits, int n_items, int n_blk, int scope_batc
                     int32_t* pos, lx_stream_t stream) {
   LX_REQUIRE(n_items >= 1 && n_blk >= 1, LX_ERR_SHAPE, "mask_compact: empty shape");
   LX_REQUIRE(n_blk <= 32 * kCompactMaxWords, LX_ERR_UNSUPPORTED, "mask_compact: n_blk %d > %d", n_blk, 32 * kCompactMaxWords);
-  launch_k(mask_compact_kernel, n_items, 512, 0, stream, bits, n_items, n_blk, scope_batch, counts, ids, pos);
+  launch_k(mask_compact_kernel, n_items, 512, 0, stream, bits, n_items, n_blk, scope_batch, 1, counts, ids, pos);
+  return launch_check("mask_compact");
+}
+
+static int mask_compact_slots(const uint32_t* bits, int n_items, int n_blk, int scope_batch, int n_slots, int32_t* counts,
+                              int32_t* ids, int32_t* pos, cudaStream_t stream) {
+  launch_k(mask_compact_kernel, n_items, 512, 0, stream, bits, n_items, n_blk, scope_batch, n_slots, counts, ids, pos);
   return launch_check("mask_compact");
 }
 
@@ -268,7 +275,7 @@ int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint
              "predict_mlp_mask: k_terms %d (1..3; split terms need d %% %d == 0)", k_terms, kBK);
   LX_REQUIRE(n_items <= kMaxItems, LX_ERR_UNSUPPORTED, "too many items");
   const int words = (n_blk + 31) / 32;
-  LX_CHECK_CUDA(cudaMemsetAsync(bits_ws, 0, sizeof(uint32_t) * n_items * words, stream));
+  const int slots = (s + 31) / 32;  // bits_ws: [n_items, slots, words], every word stored by the GEMM (no memset)
   // 128-wide tiles when 256-wide ones would leave SMs idle (n_blk = 512: 64 tiles at B = 8 x 512 tokens)
   const long long tiles256 = (long long)n_items * ((s + kBM - 1) / kBM) * ((n_blk + 255) / 256);
   const int bn = tiles256 < num_sms() ? 128 : 256;
@@ -291,9 +298,10 @@ int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint
     args.thr = threshold;
     args.bits = bits_ws;
     args.bits_stride = words;
+    args.bits_slots = slots;
     args.lora_scale = 1.f;
     if ((rc = gemm_dual_launch(true, ta, tb, args, stream))) return rc;
-    return lx_mask_compact(bits_ws, n_items, n_blk, scope_batch, counts, ids, pos, stream);
+    return mask_compact_slots(bits_ws, n_items, n_blk, scope_batch, slots, counts, ids, pos, stream);
   }
   // k_terms 2: h [M, d] x [W_hi | W_lo]; 3: [x_hi | x_lo] [M, 2d] x [W_hi | W_lo | W_hi] (A's K wraps at d)
   const int a_cols = k_terms == 3 ? 2 * d : d, kt = k_terms * d;
@@ -312,6 +320,7 @@ int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint
   args.thr = threshold;
   args.bits = bits_ws;
   args.bits_stride = words;
+  args.bits_slots = slots;
   args.lora_scale = 1.f;
   if (bn == 128) {
     auto kern = gemm_sm100_kernel<kDense, kEpiMask, 128>;
@@ -327,7 +336,7 @@ int lx_predict_mlp_mask(const uint16_t* h, int n_items, int s, int d, const uint
     launch_k(kern, num_sms(), kGemmThreads, smem, stream, ta, tb, args);
   }
   if ((rc = launch_check("mlp mask gemm"))) return rc;
-  return lx_mask_compact(bits_ws, n_items, n_blk, scope_batch, counts, ids, pos, stream);
+  return mask_compact_slots(bits_ws, n_items, n_blk, scope_batch, slots, counts, ids, pos, stream);
 }
 
 int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, int d, const uint16_t* wqk_t, int H,

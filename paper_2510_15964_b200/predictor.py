@@ -203,7 +203,7 @@ def mlp_masks(h: torch.Tensor, n_items: int, s: int, params: MlpPredictorParams,
     wa = params.packed_t(dev, terms)
     n_blk = wa.shape[0]
     words = (n_blk + 31) // 32
-    bits = torch.empty(n_items, words, dtype=torch.int32, device=dev)
+    bits = torch.empty(n_items, (s + 31) // 32, words, dtype=torch.int32, device=dev)  # per 32-row slot, all stored
     counts = torch.empty(n_items, dtype=torch.int32, device=dev)
     ids = torch.empty(n_items, n_blk, dtype=torch.int32, device=dev)  # tail zeroed by the compaction kernel
     pos = torch.empty(n_items, n_blk, dtype=torch.int32, device=dev)

@@ -22,7 +22,7 @@ wqk = (torch.randn(2 * H * r, 2 * d, device=dev, generator=g) * 0.05).to(torch.b
 proj = torch.empty(B * m, 2 * H * r, device=dev)
 h = torch.randn(B * s, d, device=dev, generator=g).to(torch.bfloat16)
 wa = (torch.randn(n_blk, 2 * d, device=dev, generator=g) * 0.05).to(torch.bfloat16)
-bits = torch.zeros(B * 16, dtype=torch.int32, device=dev)
+bits = torch.zeros(B * (s // 32) * 16, dtype=torch.int32, device=dev)
 counts = torch.zeros(B, dtype=torch.int32, device=dev)
 ids = torch.zeros(B, n_blk, dtype=torch.int32, device=dev)
 pos = torch.zeros(B, n_blk, dtype=torch.int32, device=dev)
