@@ -149,6 +149,10 @@ int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d,
  * order, into packed [n_items, d_ff, d] rows [0, counts[b]*blk) (sf/neuron_ops.py:67-72 columns). */
 int lx_pack_active_rows(const uint16_t* w, int d_ff, int d, int blk, int n_items, const int32_t* counts,
                         const int32_t* ids, uint16_t* packed, lx_stream_t stream);
+/* The same for two weights with the same masks (W1^T and W2 of one layer) in one launch; w_b / packed_b may be NULL. */
+int lx_pack_active_rows2(const uint16_t* w_a, const uint16_t* w_b, int d_ff, int d, int blk, int n_items,
+                         const int32_t* counts, const int32_t* ids, uint16_t* packed_a, uint16_t* packed_b,
+                         lx_stream_t stream);
 
 /* Skinny LoRA row projection: Y[M, r] (row stride ldy) = scale * X[M, K] W, K optionally gathered per item.
  *   X bf16 row stride ldx; W(k, q) = w[k_orig*w_sk + q*w_sq]; k_orig = k (dense, counts==NULL) or

@@ -39,6 +39,7 @@ SIGNATURES: dict[str, list] = {
     "lx_neuron_fc2": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _P, _I, _P, _P, _P],
     "lx_neuron_fc2_dgrad": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P],
     "lx_pack_active_rows": [_P, _I, _I, _I, _I, _P, _P, _P, _P],
+    "lx_pack_active_rows2": [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P],
     "lx_neuron_fc1_dgrad": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P],
     "lx_rowproj": [_P, _I, _I, _I, _I, _P, _LL, _LL, _I, _F, _P, _P, _I, _P, _I, _P, _P],
     "lx_rowproj_ws_bytes": [_I, _I, _I, _I],

@@ -24,7 +24,7 @@ from . import _abi
 from . import model as M
 from .block_sparse import attention_backward
 from .errors import GradientError
-from .neuron_ops import colgrad_group, colgrad_problem, pack_active_rows, rowproj, rowproj_packed
+from .neuron_ops import colgrad_group, colgrad_problem, pack_active_rows2, rowproj, rowproj_packed
 
 
 def check_gradient_set(grads: dict, model: M.Model) -> None:
@@ -194,7 +194,7 @@ def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims
         cg.add(f"{prefix}w2.lora_b", (r2, d), cache["ax2"], dO, d, r2, ad2.scaling, d, 1)
     w1p, w2p = cache.get("w1p"), cache.get("w2p")
     if cache.get("repack"):  # the forward did not keep its packs (memory): re-pack this layer's active rows
-        w1p, w2p = pack_active_rows(lw.mlp.w1_t, nm), pack_active_rows(lw.mlp.w2, nm)
+        w1p, w2p = pack_active_rows2(lw.mlp.w1_t, lw.mlp.w2, nm)
     dz = torch.empty_like(a)
     _abi.call("lx_neuron_fc2_dgrad", dO.data_ptr(), B, s, d, f, blk, lw.mlp.w2.data_ptr(), nm.counts.data_ptr(),
               nm.ids.data_ptr(), _abi.ptr(dax2), _abi.ptr(ad2.a if ad2 else None), ad2.rank if ad2 else 0, a.data_ptr(),

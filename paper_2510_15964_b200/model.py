@@ -678,8 +678,7 @@ def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, c
     # packs of all layers would exceed LX_PACK_CACHE_GB (capacity [B, d_ff, d] per weight: 137 GB at OPT-6.7B,
     # B = 16), in which case the backward re-packs its layer (mlp_backward)
     pack = not _NO_PACK
-    w1p = neuron_ops.pack_active_rows(lw.mlp.w1_t, nm) if pack else None
-    w2p = neuron_ops.pack_active_rows(lw.mlp.w2, nm) if pack else None
+    w1p, w2p = neuron_ops.pack_active_rows2(lw.mlp.w1_t, lw.mlp.w2, nm) if pack else (None, None)
     keep = pack and dims.n_layers * 2 * B * f * d * 2 <= _PACK_CACHE_BYTES
     lp = lw.lora_pack
     if ad1 is None:

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _abi
-from .errors import MaskError
+from .errors import MaskError, ShapeError
 
 
 def block_slices(d_ff: int, blk_size: int) -> list[slice]:
@@ -219,6 +219,18 @@ def neuron_matmul_fwd2(hidden: ActiveHidden, weights: LayeredWeights, mask, coun
     if counter is not None:
         counter.add(s * int(nm.counts.sum()) * hidden.blk_size * d)
     return res
+
+
+def pack_active_rows2(w_a: torch.Tensor, w_b: torch.Tensor, masks: NeuronMasks) -> tuple[torch.Tensor, torch.Tensor]:
+    """pack_active_rows of two [d_ff, d] weights under the same masks (W1^T and W2 of a layer) in one launch."""
+    d_ff, d = w_a.shape
+    if tuple(w_b.shape) != (d_ff, d) or w_b.dtype != w_a.dtype:
+        raise ShapeError("pack_active_rows2: the two weights must have the same shape and dtype")
+    pa = torch.empty(masks.n_items, d_ff, d, dtype=w_a.dtype, device=w_a.device)
+    pb = torch.empty_like(pa)
+    _abi.call("lx_pack_active_rows2", w_a.data_ptr(), w_b.data_ptr(), d_ff, d, masks.blk, masks.n_items,
+              masks.counts.data_ptr(), masks.ids.data_ptr(), pa.data_ptr(), pb.data_ptr(), _abi.stream_handle(w_a.device))
+    return pa, pb
 
 
 def pack_active_rows(w: torch.Tensor, masks: NeuronMasks) -> torch.Tensor:
