@@ -20,6 +20,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
+// VEC = float4 per thread, ceil(d / 4 / 256): registers (and so resident CTAs) sized to the row, not to the max d
+template <int VEC>
 __global__ void __launch_bounds__(kLnThreads) ln_fwd_kernel(const float* __restrict__ x, int d, const float* __restrict__ g,
                                                              const float* __restrict__ b, float eps,
                                                              __nv_bfloat16* __restrict__ y, int ldy, float* __restrict__ mean_out,
@@ -32,10 +34,10 @@ __global__ void __launch_bounds__(kLnThreads) ln_fwd_kernel(const float* __restr
   const size_t row = blockIdx.x;
   const float4* xr = reinterpret_cast<const float4*>(x + row * d);
   const int nv = d / 4;
-  float4 v[kLnMaxVec];
+  float4 v[VEC];
   float sum = 0.f;
 #pragma unroll
-  for (int i = 0; i < kLnMaxVec; ++i) {
+  for (int i = 0; i < VEC; ++i) {
     int c = threadIdx.x + i * kLnThreads;
     v[i] = c < nv ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
     if (delta && c < nv) {  // fused residual add: y = x + delta (sf/model.py:420, 427), y kept in fp32
@@ -51,7 +53,7 @@ __global__ void __launch_bounds__(kLnThreads) ln_fwd_kernel(const float* __restr
   const float mu = block_sum(sum, red) / d;
   float sq = 0.f;
 #pragma unroll
-  for (int i = 0; i < kLnMaxVec; ++i) {
+  for (int i = 0; i < VEC; ++i) {
     int c = threadIdx.x + i * kLnThreads;
     if (c < nv) {
       float a = v[i].x - mu, bb = v[i].y - mu, cc = v[i].z - mu, dd = v[i].w - mu;
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(kLnThreads) ln_fwd_kernel(const float* __restr
   const float4* g4 = reinterpret_cast<const float4*>(g);
   const float4* b4 = reinterpret_cast<const float4*>(b);
 #pragma unroll
-  for (int i = 0; i < kLnMaxVec; ++i) {
+  for (int i = 0; i < VEC; ++i) {
     int c = threadIdx.x + i * kLnThreads;
     if (c < nv) {
       float4 gg = g4[c], bb = b4[c];
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(kLnThreads) ln_fwd_kernel(const float* __restr
   }
 }
 
-template <bool kF32>
+template <bool kF32, int VEC>
 __global__ void __launch_bounds__(kLnThreads) ln_bwd_kernel(const void* __restrict__ dy_, const float* __restrict__ x,
                                                              const float* __restrict__ g, const float* __restrict__ mean,
                                                              const float* __restrict__ istd, int d,
@@ -99,17 +101,17 @@ __global__ void __launch_bounds__(kLnThreads) ln_bwd_kernel(const void* __restri
   const size_t row = blockIdx.x;
   const float mu = mean[row], is = istd[row];
   const int nv = d / 4;
-  float4 gv[kLnMaxVec], xh[kLnMaxVec], cur[kLnMaxVec];
+  float4 gv[VEC], xh[VEC], cur[VEC];
   float4* o = reinterpret_cast<float4*>(dx + row * d);
   // the accumulator row is loaded with the inputs (one DRAM round trip per row, not two around the block sums)
 #pragma unroll
-  for (int i = 0; i < kLnMaxVec; ++i) {
+  for (int i = 0; i < VEC; ++i) {
     const int c = threadIdx.x + i * kLnThreads;
     cur[i] = c < nv ? o[c] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-  for (int i = 0; i < kLnMaxVec; ++i) {
+  for (int i = 0; i < VEC; ++i) {
     int c = threadIdx.x + i * kLnThreads;
     gv[i] = xh[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (c < nv) {
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(kLnThreads) ln_bwd_kernel(const void* __restri
   const float mg = block_sum(s1, red) / d;
   const float mgx = block_sum(s2, red) / d;
 #pragma unroll
-  for (int i = 0; i < kLnMaxVec; ++i) {
+  for (int i = 0; i < VEC; ++i) {
     int c = threadIdx.x + i * kLnThreads;
     if (c < nv) {
       cur[i].x += is * (gv[i].x - mg - xh[i].x * mgx);
@@ -339,10 +341,11 @@ int lx_layernorm_fwd(const float* x, const uint16_t* delta, float* resid_out, in
     else ln_fwd_warp<16>(x, delta, resid_out, M, d, gamma, beta, eps, y, ldy, mean, inv_std, s, m_small, x_small, stream);
     return launch_check("layernorm_fwd");
   }
-  launch_k(ln_fwd_kernel, M, kLnThreads, 0, stream, x, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), ldy, mean,
-           inv_std,
-                                              s > 0 ? s : 1, m_small, reinterpret_cast<__nv_bfloat16*>(x_small),
-                                              reinterpret_cast<const __nv_bfloat16*>(delta), resid_out);
+  const int vec = (d / 4 + kLnThreads - 1) / kLnThreads;  // block kernel: float4 per thread
+  auto kf = vec <= 4 ? ln_fwd_kernel<4> : vec <= 6 ? ln_fwd_kernel<6> : ln_fwd_kernel<8>;
+  launch_k(kf, M, kLnThreads, 0, stream, x, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), ldy, mean, inv_std,
+           s > 0 ? s : 1, m_small, reinterpret_cast<__nv_bfloat16*>(x_small), reinterpret_cast<const __nv_bfloat16*>(delta),
+           resid_out);
   return launch_check("layernorm_fwd");
 }
 
@@ -357,10 +360,10 @@ int lx_layernorm_bwd(const void* dy, int dy_is_f32, const float* x, const float*
     else ln_bwd_warp<16>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
     return launch_check("layernorm_bwd");
   }
-  if (dy_is_f32)
-    launch_k(ln_bwd_kernel<true>, M, kLnThreads, 0, stream, dy, x, gamma, mean, inv_std, d, dx_accum, ob);
-  else
-    launch_k(ln_bwd_kernel<false>, M, kLnThreads, 0, stream, dy, x, gamma, mean, inv_std, d, dx_accum, ob);
+  const int vec = (d / 4 + kLnThreads - 1) / kLnThreads;
+  auto kb = dy_is_f32 ? (vec <= 4 ? ln_bwd_kernel<true, 4> : vec <= 6 ? ln_bwd_kernel<true, 6> : ln_bwd_kernel<true, 8>)
+                      : (vec <= 4 ? ln_bwd_kernel<false, 4> : vec <= 6 ? ln_bwd_kernel<false, 6> : ln_bwd_kernel<false, 8>);
+  launch_k(kb, M, kLnThreads, 0, stream, dy, x, gamma, mean, inv_std, d, dx_accum, ob);
   return launch_check("layernorm_bwd");
 }
 

@@ -370,7 +370,7 @@ def test_adam_step_kernel():
     assert np.abs(p.cpu().numpy() - pr).max() <= 1e-7
 
 
-@pytest.mark.parametrize("d", [768, 1024, 2048])
+@pytest.mark.parametrize("d", [768, 1024, 2048, 4096, 5120])
 @pytest.mark.parametrize("with_delta", [False, True])
 def test_layernorm_fwd_kernel(d, with_delta):
     """lx_layernorm_fwd (csrc/layernorm.cu) vs torch fp32 (sf/model.py:307-312): fused residual add
@@ -404,3 +404,37 @@ def test_layernorm_fwd_kernel(d, with_delta):
     idx = torch.tensor([(i * s) // m_small for i in range(m_small)], device=dev)
     want = y.view(n_items, s, d)[:, idx].reshape(-1, d)
     assert torch.equal(xs, want)
+
+
+@pytest.mark.parametrize("d", [768, 2048, 4096, 5120])
+@pytest.mark.parametrize("dy_f32", [False, True])
+def test_layernorm_bwd_kernel(d, dy_f32):
+    """lx_layernorm_bwd (warp kernel up to d = 2048, block kernel above): dx_accum += LN'(dy) against torch autograd
+    of layer_norm in float64, and the bf16 copy of the updated accumulator."""
+    from paper_2510_15964_b200 import _abi
+
+    dev = _dev()
+    g = torch.Generator(device="cpu").manual_seed(d)
+    M = 1000
+    x = torch.randn(M, d, generator=g).to(dev)
+    gamma = (1 + 0.1 * torch.randn(d, generator=g)).to(dev)
+    beta = torch.zeros(d, device=dev)
+    dy = torch.randn(M, d, generator=g).to(dev)
+    dy_in = dy if dy_f32 else dy.to(torch.bfloat16)
+    acc0 = torch.randn(M, d, generator=g).to(dev)
+    acc = acc0.clone()
+    y = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
+    mean, istd = torch.empty(M, device=dev), torch.empty(M, device=dev)
+    st = _abi.stream_handle(dev)
+    _abi.call("lx_layernorm_fwd", x.data_ptr(), None, None, M, d, gamma.data_ptr(), beta.data_ptr(), 1e-5, y.data_ptr(), d,
+              mean.data_ptr(), istd.data_ptr(), 0, 0, None, st)
+    ob = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
+    _abi.call("lx_layernorm_bwd", dy_in.data_ptr(), int(dy_f32), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
+              istd.data_ptr(), M, d, acc.data_ptr(), ob.data_ptr(), st)
+    torch.cuda.synchronize()
+    xd = x.double().requires_grad_(True)
+    out = torch.nn.functional.layer_norm(xd, (d,), gamma.double(), beta.double(), 1e-5)
+    out.backward(dy_in.double())
+    ref = acc0.double() + xd.grad
+    assert rel(acc, ref) < 1e-4
+    assert torch.equal(ob, acc.to(torch.bfloat16))
