@@ -279,6 +279,17 @@ int lx_adam_step(float* params, const float* grads, double* m, double* v, long l
 int lx_cross_entropy(const float* logits, int rows, int V, const int64_t* targets, float inv_s, float* row_loss,
                      uint16_t* grad_bf16, lx_stream_t stream);
 
+/* The tied LM head + loss_forward + loss_backward without fp32 logits (sf/model.py:449-472): a tcgen05 logits GEMM
+ * hf [rows, d] x emb^T (emb bf16 [V, d]) whose epilogue keeps, per row and 256-column segment, m = max l and
+ * z = sum exp(l - m), stores bf16 exp(l - m) into g [rows, ldg] and the target's fp32 logit; a combine kernel forms
+ * row_loss[r] = logsumexp(l_r) - l_r[t_r] and the per-segment factors; a rescale pass turns g in place into
+ * bf16((softmax(l_r) - onehot(t_r)) * inv_s) -- the operand of the d_hf = g emb GEMM.
+ * stats_ws: float [rows, 2 * nseg]; coef_ws: float [rows, nseg]; tl_ws: float [rows]; nseg = lx_lm_head_ce_nseg(V). */
+int lx_lm_head_ce_nseg(int V);
+int lx_lm_head_ce(const uint16_t* hf, int ld_hf, int rows, int d, const uint16_t* emb, int V, const int64_t* targets,
+                  float inv_s, uint16_t* g, int ldg, float* stats_ws, float* coef_ws, float* tl_ws, float* row_loss,
+                  lx_stream_t stream);
+
 /* layernorm_backward (sf/autograd.py:61-66): dx_accum += LN'(dy), dy bf16 or fp32 (dy_is_f32);
  * optionally also writes bf16(dx_accum) to dx_bf16 (the next GEMM's operand). */
 int lx_layernorm_bwd(const void* dy, int dy_is_f32, const float* x, const float* gamma, const float* mean,

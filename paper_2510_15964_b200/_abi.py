@@ -40,6 +40,8 @@ SIGNATURES: dict[str, list] = {
     "lx_neuron_fc2_dgrad": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P],
     "lx_pack_active_rows": [_P, _I, _I, _I, _I, _P, _P, _P, _P],
     "lx_pack_active_rows2": [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P],
+    "lx_lm_head_ce_nseg": [_I],
+    "lx_lm_head_ce": [_P, _I, _I, _I, _P, _I, _P, _F, _P, _I, _P, _P, _P, _P, _P],
     "lx_neuron_fc1_dgrad": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P],
     "lx_rowproj": [_P, _I, _I, _I, _I, _P, _LL, _LL, _I, _F, _P, _P, _I, _P, _I, _P, _P],
     "lx_rowproj_ws_bytes": [_I, _I, _I, _I],
@@ -108,7 +110,8 @@ def lib() -> C.CDLL:
     return _lib
 
 
-_NON_STATUS = ("lx_abi_version", "lx_device_sm_count", "lx_gemm_set_cta_pair", "lx_exact_mass_smem", "lx_adapter_ws_floats")
+_NON_STATUS = ("lx_abi_version", "lx_device_sm_count", "lx_gemm_set_cta_pair", "lx_exact_mass_smem", "lx_adapter_ws_floats",
+               "lx_lm_head_ce_nseg")
 
 
 # Kernel-time probe (bench.py's roofline): when a dict {symbol: list}, every call of a listed symbol is

@@ -164,6 +164,68 @@ int gemm_dual_launch(bool mask_epi, const CUtensorMap& ta, const CUtensorMap& tb
                   : launch_gemm<kDenseDual, kEpiStoreF32, 256, 2>(ta, tb, args, st);
 }
 
+// ---- LM head + cross-entropy without fp32 logits (sf/model.py:449-472)
+// combine: per row, lse = M + log sum_t z_t 2^((m_t - M) log2 e) over the logits GEMM's segment stats (fixed order:
+// lane-strided partial sums, then a butterfly), loss = lse - l_target, and per segment the factor
+// c_t = exp(m_t - lse) * inv_s that turns the stored bf16 exp(l - m_t) into the softmax / s. One warp per row.
+__global__ void __launch_bounds__(256) ce_combine_kernel(const float2* __restrict__ stats, int nseg, const float* __restrict__ tl,
+                                                         int rows, float inv_s, float* __restrict__ row_loss,
+                                                         float* __restrict__ coef) {
+  pdl_wait_trigger();
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float2* st = stats + (size_t)row * nseg;
+  float mx = -INFINITY;
+  for (int k = lane; k < nseg; k += 32) mx = fmaxf(mx, st[k].x);
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float z = 0.f;
+  for (int k = lane; k < nseg; k += 32) {
+    const float2 p = st[k];
+    if (p.y > 0.f) z += p.y * __expf(p.x - mx);
+  }
+  for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+  const float lse = mx + __logf(z);
+  for (int k = lane; k < nseg; k += 32) {
+    const float2 p = st[k];
+    coef[(size_t)row * nseg + k] = p.y > 0.f ? __expf(p.x - lse) * inv_s : 0.f;
+  }
+  if (lane == 0) row_loss[row] = lse - tl[row];
+}
+
+// rescale in place: g[r, j] = bf16(float(g[r, j]) * c[r, j / seg] - (j == target[r]) * inv_s), 8 columns per thread
+__global__ void __launch_bounds__(256) ce_rescale_kernel(__nv_bfloat16* __restrict__ g, int ldg, int rows, int V,
+                                                         const float* __restrict__ coef, int nseg, int seg,
+                                                         const int64_t* __restrict__ tgt, float inv_s) {
+  pdl_wait_trigger();
+  const int v8 = (V + 7) / 8;
+  const long long n = (long long)rows * v8;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(e / v8), j0 = (int)(e % v8) * 8;
+    const float c = __ldg(coef + (size_t)row * nseg + j0 / seg);
+    const long long t = __ldg(tgt + row);
+    __nv_bfloat16* p = g + (size_t)row * ldg + j0;
+    if (j0 + 8 <= V) {
+      uint4 w = *reinterpret_cast<const uint4*>(p);
+      uint32_t* u = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float a = __bfloat162float(__ushort_as_bfloat16((unsigned short)(u[k] & 0xffffu))) * c;
+        float b = __bfloat162float(__ushort_as_bfloat16((unsigned short)(u[k] >> 16))) * c;
+        if (j0 + 2 * k == t) a -= inv_s;
+        if (j0 + 2 * k + 1 == t) b -= inv_s;
+        u[k] = pack_bf16x2(a, b);
+      }
+      *reinterpret_cast<uint4*>(p) = w;
+    } else {
+      for (int k = 0; j0 + k < V; ++k) {
+        float a = __bfloat162float(p[k]) * c;
+        if (j0 + k == t) a -= inv_s;
+        p[k] = __float2bfloat16_rn(a);
+      }
+    }
+  }
+}
+
 static GemmArgs base_args(int n_items, int rows, int n_dense, int k_dense) {
   GemmArgs a;
   memset(&a, 0, sizeof(a));
@@ -482,6 +544,35 @@ int lx_neuron_fc1_dgrad(const uint16_t* dz, int ld_h, int n_items, int s, int d,
 int lx_pack_active_rows(const uint16_t* w, int d_ff, int d, int blk, int n_items, const int32_t* counts,
                         const int32_t* ids, uint16_t* packed, lx_stream_t stream) {
   return lx_pack_active_rows2(w, nullptr, d_ff, d, blk, n_items, counts, ids, packed, nullptr, stream);
+}
+
+int lx_lm_head_ce_nseg(int V) { return 2 * ((V + 511) / 512); }  // two 256-column halves per 512-wide tile
+
+int lx_lm_head_ce(const uint16_t* hf, int ld_hf, int rows, int d, const uint16_t* emb, int V, const int64_t* targets,
+                  float inv_s, uint16_t* g, int ldg, float* stats_ws, float* coef_ws, float* tl_ws, float* row_loss,
+                  lx_stream_t stream) {
+  LX_REQUIRE(rows >= 1 && d >= 1 && V >= 1, LX_ERR_SHAPE, "lm_head_ce: empty shape");
+  LX_REQUIRE(ldg >= V && ldg % 8 == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0, LX_ERR_SHAPE,
+             "lm_head_ce: gradient rows need ldg >= V, a multiple of 8, 16-byte aligned");
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_tmap_bf16_2d(&ta, hf, d, rows, ld_hf, kBK, kBM))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, emb, d, V, d, kBK, 32))) return rc;  // wide pair tiles: 32-row B boxes
+  const int nseg = lx_lm_head_ce_nseg(V);
+  GemmArgs args = base_args(1, rows, V, d);
+  args.out = g;
+  args.ldo = ldg;
+  args.ce_tgt = targets;
+  args.ce_stats = reinterpret_cast<float2*>(stats_ws);
+  args.ce_tl = tl_ws;
+  args.ce_nseg = nseg;
+  if ((rc = launch_gemm<kDense, kEpiCe, 512, 2>(ta, tb, args, stream))) return rc;
+  launch_k(ce_combine_kernel, (rows + 7) / 8, 256, 0, stream, reinterpret_cast<const float2*>(stats_ws), nseg,
+           (const float*)tl_ws, rows, inv_s, row_loss, coef_ws);
+  if ((rc = launch_check("ce_combine"))) return rc;
+  launch_k(ce_rescale_kernel, 8 * num_sms(), 256, 0, stream, reinterpret_cast<__nv_bfloat16*>(g), ldg, rows, V,
+           (const float*)coef_ws, nseg, 256, targets, inv_s);
+  return launch_check("ce_rescale");
 }
 
 int lx_pack_active_rows2(const uint16_t* w_a, const uint16_t* w_b, int d_ff, int d, int blk, int n_items,

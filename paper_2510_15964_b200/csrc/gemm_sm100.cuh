@@ -61,6 +61,8 @@ enum EpiKind : int {
   kEpiDx = 5,         // acc + dax1[row]·A1[c,:]                  -> bf16
   kEpiMask = 6,       // OR_rows(acc > thr) per column -> bitmask words (+ optional fp32 dump)
   kEpiFc1Raw = 7,     // acc + b1[c] + s*ax1[row]·B1[:,c] (no ReLU)  -> bf16 packed (neuron_matmul_fwd1 API)
+  kEpiCe = 8,         // LM-head logits l: per (row, BN/2-column segment) m = max l and z = sum exp(l - m) -> ce_stats,
+                      // bf16 exp(l - m) -> out, the target's fp32 logit -> ce_tl (no fp32 logits are stored)
 };
 
 // Debug-only phase trace (lx_debug_set_gemm_trace): per CTA 32 clock64 stamps, NULL in production.
@@ -108,6 +110,10 @@ struct GemmArgs {
   uint32_t* bits;       // kEpiMask: [n_items, bits_slots, bits_stride] words: slot t = rows [32t, 32t + 32) of the item
   int bits_stride;
   int bits_slots;       // ceil(rows_per_item / 32); every (slot, word) is stored exactly once (no atomics, no memset)
+  const int64_t* ce_tgt;  // kEpiCe: target id per row
+  float2* ce_stats;       // kEpiCe: [rows, ce_nseg] (segment max, sum of exp(l - max)), segments of BN/2 columns
+  float* ce_tl;           // kEpiCe: [rows] fp32 logit of the target
+  int ce_nseg;
   int out_f32;          // store fp32 instead of bf16 (any epilogue except kEpiMask)
   const float* resid;   // fp32 [rows, ldo]: out = resid + value (fused residual add; requires out_f32)
   int packed_stride;    // kPacked*: rows per item in the packed weight copy
@@ -259,8 +265,8 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   __syncthreads();
   if (warp == 0) {
     // warp-parallel: lane L tests the width (L + 1) * kWq, then a warp scan builds the item prefix
-    int wsel = 0;
-    if (kWide) {  // narrowest multiple-of-64 width whose tiles fit in one round of pairs (else the widest)
+    int wsel = (kWide && EPI == kEpiCe) ? BN : 0;  // CE segments are BN / 2 columns: full-width tiles
+    if (kWide && EPI != kEpiCe) {  // narrowest multiple-of-64 width whose tiles fit in one round of pairs (else the widest)
       const int pairs = gridDim.x / kCluster;
       const int w_l = ((int)lane + 1) * kWq;
       bool fits = false;
@@ -568,6 +574,21 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       const int ch_lo = col_half * kHalf, ch_hi = min(n_chunks, (col_half + 1) * kHalf);
       // software-pipelined: chunk ch + 1's TMEM load is in flight while chunk ch is processed
       uint32_t raw[32];
+      // kEpiCe: max of this row's logits over the column half (its segment); exp / sum / store in the chunk loop
+      float ce_m = -INFINITY, ce_z = 0.f, ce_tlv = 0.f;
+      bool ce_has_t = false;
+      long long ce_tcol = -1;
+      if (EPI == kEpiCe) {
+        if (row_ok) ce_tcol = args.ce_tgt[grow] - ti.n0;
+        for (int ch = ch_lo; ch < ch_hi; ++ch) {
+          tmem_ld_32x32b_x32(t_row + ch * 32, raw);
+          tmem_ld_wait_regs(raw);
+          const int nvm = min(32, ti.n_cols - ch * 32);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < nvm) ce_m = fmaxf(ce_m, __uint_as_float(raw[i]));
+        }
+      }
       if (ti.k_stages > 0 && ch_lo < ch_hi) tmem_ld_32x32b_x32(t_row + ch_lo * 32, raw);
       for (int ch = ch_lo; ch < ch_hi; ++ch) {
         float v[32];
@@ -583,6 +604,19 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         const int c0 = ch * 32;
         const int nv = min(32, ti.n_cols - c0);
         const int j0 = ti.n0 + c0;  // packed / dense column of v[0]
+        if (EPI == kEpiCe) {
+          const float ml = ce_m * 1.4426950408889634f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (c0 + i == ce_tcol) {
+              ce_tlv = v[i];
+              ce_has_t = true;
+            }
+            const float e = i < nv ? ex2(fmaf(v[i], 1.4426950408889634f, -ml)) : 0.f;
+            ce_z += e;
+            v[i] = e;
+          }
+        }
 
         if (EPI == kEpiMask) {
           uint32_t word = 0;
@@ -718,6 +752,10 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
               if (i < nv) o[i] = __float2bfloat16_rn(v[i]);
           }
         }
+      }
+      if (EPI == kEpiCe && row_ok) {
+        args.ce_stats[grow * args.ce_nseg + (ti.n0 + col_half * (BN / 2)) / (BN / 2)] = make_float2(ce_m, ce_z);
+        if (ce_has_t) args.ce_tl[grow] = ce_tlv;
       }
       // release the accumulator buffer to the MMA warp
       tc_fence_before();

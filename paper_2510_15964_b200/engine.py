@@ -16,12 +16,38 @@ import torch
 from . import autograd as AG, model as M
 
 
+# LX_LMHEAD_FUSED=0: fp32 logits from cuBLAS + the CE kernel (the round-1 path) instead of the fused-epilogue logits
+# GEMM (lx_lm_head_ce), for measurements
+_LMHEAD_FUSED = __import__("os").environ.get("LX_LMHEAD_FUSED", "1") != "0"
+
+
 def lm_head_loss_and_grad(hf: torch.Tensor, emb: torch.Tensor, targets: torch.Tensor, s: int, chunk: int = 4096):
     """Mean CE over positions (per-item mean, then batch mean) and d(sum of per-item losses)/d hf.
-    hf bf16 [M, d]; emb bf16 [V, d]; targets int64 [M]. Returns (loss fp32 scalar tensor, d_hf fp32 [M, d])."""
+    hf bf16 [M, d]; emb bf16 [V, d]; targets int64 [M]. Returns (loss fp32 scalar tensor, d_hf fp32 [M, d]).
+    Default: no fp32 logits exist -- the logits GEMM's epilogue keeps per-segment softmax statistics and stores
+    bf16 exp(l - m_seg), a combine kernel forms the loss, a rescale pass turns that into the bf16 gradient
+    (lx_lm_head_ce), and d_hf = g emb is one library GEMM."""
     from . import _abi
 
     Mr, V = hf.shape[0], emb.shape[0]
+    if _LMHEAD_FUSED:
+        dev = hf.device
+        nseg = _abi.lib().lx_lm_head_ce_nseg(V)
+        ldg = (V + 7) // 8 * 8
+        d_hf = torch.empty(Mr, hf.shape[1], dtype=torch.float32, device=dev)
+        row_loss = torch.empty(Mr, dtype=torch.float32, device=dev)
+        tg = targets.contiguous()
+        for r0 in range(0, Mr, chunk):
+            r1 = min(Mr, r0 + chunk)
+            g = torch.empty(r1 - r0, ldg, dtype=torch.bfloat16, device=dev)
+            stats = torch.empty(r1 - r0, 2 * nseg, dtype=torch.float32, device=dev)
+            coef = torch.empty(r1 - r0, nseg, dtype=torch.float32, device=dev)
+            tl = torch.empty(r1 - r0, dtype=torch.float32, device=dev)
+            _abi.call("lx_lm_head_ce", hf[r0:r1].data_ptr(), hf.stride(0), r1 - r0, hf.shape[1], emb.data_ptr(), V,
+                      tg[r0:r1].data_ptr(), 1.0 / s, g.data_ptr(), ldg, stats.data_ptr(), coef.data_ptr(), tl.data_ptr(),
+                      row_loss[r0:].data_ptr(), _abi.stream_handle(dev))
+            d_hf[r0:r1] = M._mm_f32(g[:, :V], emb)
+        return row_loss.mean(), d_hf
     d_hf = torch.empty(Mr, hf.shape[1], dtype=torch.float32, device=hf.device)
     row_loss = torch.empty(Mr, dtype=torch.float32, device=hf.device)
     tg = targets.contiguous()

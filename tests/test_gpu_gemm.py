@@ -234,6 +234,46 @@ def test_cross_entropy_kernel():
     assert rel(d_hf, ref_dhf) < 1e-2
 
 
+@pytest.mark.parametrize("rows,d,V,scale", [(192, 128, 1000, 0.3), (700, 768, 50272, 0.05), (4096, 2048, 50272, 0.03),
+                                          (300, 256, 517, 2.0)])
+def test_lm_head_fused_ce(rows, d, V, scale):
+    """lx_lm_head_ce (logits GEMM with the CE epilogue, combine, rescale) vs float64 torch (sf/model.py:449-472):
+    per-row losses at 1e-5 relative (fp32 statistics), the bf16 gradient g = (softmax - onehot) / s at 1e-2 with
+    the one-hot on the target column only, and d_hf = g emb through the engine's helper at 1e-2. Ragged V
+    (not a multiple of the 512-column tile or of 8), targets on the first and last columns, wide logits."""
+    from paper_2510_15964_b200 import _abi
+    from paper_2510_15964_b200.engine import lm_head_loss_and_grad
+
+    dev = _dev()
+    g0 = torch.Generator(device="cpu").manual_seed(rows + V)
+    hf = torch.randn(rows, d, generator=g0).to(dev, torch.bfloat16)
+    emb = (torch.randn(V, d, generator=g0) * scale).to(dev, torch.bfloat16)
+    tgt = torch.randint(0, V, (rows,), generator=g0).to(dev)
+    tgt[0], tgt[1] = 0, V - 1
+    s = 37
+    nseg = _abi.lib().lx_lm_head_ce_nseg(V)
+    ldg = (V + 7) // 8 * 8
+    gbuf = torch.empty(rows, ldg, dtype=torch.bfloat16, device=dev)
+    stats = torch.empty(rows, 2 * nseg, device=dev)
+    coef = torch.empty(rows, nseg, device=dev)
+    tl = torch.empty(rows, device=dev)
+    row_loss = torch.empty(rows, device=dev)
+    _abi.call("lx_lm_head_ce", hf.data_ptr(), d, rows, d, emb.data_ptr(), V, tgt.data_ptr(), 1.0 / s, gbuf.data_ptr(), ldg,
+              stats.data_ptr(), coef.data_ptr(), tl.data_ptr(), row_loss.data_ptr(), _abi.stream_handle(dev))
+    torch.cuda.synchronize()
+    logits = hf.double() @ emb.double().T
+    ref_loss = torch.nn.functional.cross_entropy(logits, tgt, reduction="none")
+    ref_g = (torch.softmax(logits, dim=1) - torch.nn.functional.one_hot(tgt, V).double()) / s
+    assert (row_loss.double() - ref_loss).abs().max().item() < 1e-5 * ref_loss.abs().max().item()
+    gv = gbuf[:, :V]
+    assert rel(gv.float(), ref_g) < 1e-2
+    assert torch.equal(gv[:, 0].float() < 0, tgt == 0)
+    loss, d_hf = lm_head_loss_and_grad(hf, emb, tgt, s)
+    torch.cuda.synchronize()
+    assert abs(float(loss) - float(ref_loss.mean())) < 1e-5 * float(ref_loss.mean())
+    assert rel(d_hf, ref_g @ emb.double()) < 1e-2
+
+
 def test_cross_entropy_kernel_persistent_rows():
     """More rows than the persistent CE grid (2 CTAs per SM) at the OPT vocabulary (V % 1024 != 0):
     every row's loss and gradient vs torch fp32, so rows handled on a CTA's second and later passes
