@@ -255,21 +255,24 @@ __global__ void __launch_bounds__(32 * kRpWarps, 2) rowproj_mma2_kernel(const __
 // instead of kRpU 32-k blocks per warp round trip; the MMAs then read A fragments from shared memory and the
 // hi/lo W pack from L1/L2 as above. Same k-slot mapping, same fixed-order warp reduction (identical results).
 constexpr int kRpsMaxK = 4096;
-template <int NT>
+// RG row groups of 16 per CTA share every W fragment load (RG = 2 halves the W pack re-reads from L2, which at
+// 16 rows per CTA were as many bytes as X itself); X smem is 16 * RG rows of K + 32 elements.
+template <int NT, int RG>
 __global__ void __launch_bounds__(32 * kRpWarps, 2) rowproj_smem_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int rows,
                                                            int K, int Kp, int r, float scale,
                                                            const __nv_bfloat16* __restrict__ wp, float* __restrict__ y,
                                                            int ldy, __nv_bfloat16* __restrict__ yb, int ldyb) {
   constexpr int RP = 8 * NT;
+  constexpr int TR = 16 * RG;  // rows per CTA
   extern __shared__ __align__(128) uint8_t rps_smem[];
-  __shared__ float s_red[kRpWarps][16][RP + 1];
+  __shared__ float s_red[kRpWarps][TR][RP + 1];
   __shared__ __align__(8) uint64_t bar;
   const int pitch = K + 32;  // elements
   __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(rps_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int row0 = blockIdx.x * 16;
-  const int nr = min(16, rows - row0);
+  const int row0 = blockIdx.x * TR;
+  const int nr = min(TR, rows - row0);
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -281,43 +284,53 @@ __global__ void __launch_bounds__(32 * kRpWarps, 2) rowproj_smem_kernel(const __
     for (int i = 0; i < nr; ++i) bulk_load_1d(sx + (size_t)i * pitch, x + (size_t)(row0 + i) * ldx, K * 2, &bar);
   }
   // rows past the end (last CTA): zero in shared memory, never read from global
-  for (int i = nr + warp; i < 16; i += kRpWarps)
+  for (int i = nr + warp; i < TR; i += kRpWarps)
     for (int c = lane * 8; c < K; c += 256) *reinterpret_cast<uint4*>(sx + (size_t)i * pitch + c) = make_uint4(0u, 0u, 0u, 0u);
   const __nv_bfloat16* wh = wp + (size_t)g * Kp;
   const __nv_bfloat16* wl = wh + (size_t)RP * Kp;
-  float acc[NT][4];
+  float acc[RG][NT][4];
 #pragma unroll
-  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+  for (int q = 0; q < RG; ++q)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[q][n][0] = acc[q][n][1] = acc[q][n][2] = acc[q][n][3] = 0.f;
   __syncthreads();
   mbar_wait(&bar, 0);
-  const __nv_bfloat16* xa = sx + (size_t)g * pitch + 8 * t;
-  const __nv_bfloat16* xbp = xa + (size_t)8 * pitch;
   for (int k0 = warp * 32; k0 < K; k0 += 32 * kRpWarps) {
-    const uint4 va = *reinterpret_cast<const uint4*>(xa + k0);
-    const uint4 vb = *reinterpret_cast<const uint4*>(xbp + k0);
-    const uint32_t a0[4] = {va.x, vb.x, va.y, vb.y};
-    const uint32_t a1[4] = {va.z, vb.z, va.w, vb.w};
+    uint32_t a0[RG][4], a1[RG][4];
+#pragma unroll
+    for (int q = 0; q < RG; ++q) {
+      const __nv_bfloat16* xa = sx + (size_t)(16 * q + g) * pitch + 8 * t;
+      const uint4 va = *reinterpret_cast<const uint4*>(xa + k0);
+      const uint4 vb = *reinterpret_cast<const uint4*>(xa + (size_t)8 * pitch + k0);
+      a0[q][0] = va.x; a0[q][1] = vb.x; a0[q][2] = va.y; a0[q][3] = vb.y;
+      a1[q][0] = va.z; a1[q][1] = vb.z; a1[q][2] = va.w; a1[q][3] = vb.w;
+    }
     const int kw = k0 + 8 * t;
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
       const uint4 vh = __ldg(reinterpret_cast<const uint4*>(wh + (size_t)n * 8 * Kp + kw));
       const uint4 vl = __ldg(reinterpret_cast<const uint4*>(wl + (size_t)n * 8 * Kp + kw));
-      mma16816_rp(acc[n], a0, vh.x, vh.y);
-      mma16816_rp(acc[n], a0, vl.x, vl.y);
-      mma16816_rp(acc[n], a1, vh.z, vh.w);
-      mma16816_rp(acc[n], a1, vl.z, vl.w);
+#pragma unroll
+      for (int q = 0; q < RG; ++q) {
+        mma16816_rp(acc[q][n], a0[q], vh.x, vh.y);
+        mma16816_rp(acc[q][n], a0[q], vl.x, vl.y);
+        mma16816_rp(acc[q][n], a1[q], vh.z, vh.w);
+        mma16816_rp(acc[q][n], a1[q], vl.z, vl.w);
+      }
     }
   }
 #pragma unroll
-  for (int n = 0; n < NT; ++n) {
-    const int q = n * 8 + t * 2;
-    s_red[warp][g][q] = acc[n][0];
-    s_red[warp][g][q + 1] = acc[n][1];
-    s_red[warp][g + 8][q] = acc[n][2];
-    s_red[warp][g + 8][q + 1] = acc[n][3];
-  }
+  for (int q = 0; q < RG; ++q)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int c = n * 8 + t * 2;
+      s_red[warp][16 * q + g][c] = acc[q][n][0];
+      s_red[warp][16 * q + g][c + 1] = acc[q][n][1];
+      s_red[warp][16 * q + g + 8][c] = acc[q][n][2];
+      s_red[warp][16 * q + g + 8][c + 1] = acc[q][n][3];
+    }
   __syncthreads();
-  for (int e = threadIdx.x; e < 16 * RP; e += 32 * kRpWarps) {
+  for (int e = threadIdx.x; e < TR * RP; e += 32 * kRpWarps) {
     const int rr = e / RP, q = e % RP, row = row0 + rr;
     if (q < r && row < rows) {
       float v = 0.f;
@@ -766,19 +779,22 @@ int lx_rowproj_packed(const uint16_t* x, int ldx, int n_items, int s, int K, con
   dim3 grid((rows + 15) / 16, items);
   static const bool use_smem = [] { const char* e = getenv("LX_ROWPROJ_SMEM"); return !(e && e[0] == '0'); }();
   if (!counts && use_smem && K <= kRpsMaxK && K % 8 == 0 && ldx % 8 == 0) {
-    // dense K: X rows staged in shared memory by bulk copies (rowproj_smem_kernel)
-    const size_t smem = (size_t)16 * (K + 32) * 2;
-    if (RP == 8) {
-      static cudaError_t a = cudaFuncSetAttribute(rowproj_smem_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    // dense K: X rows staged in shared memory by bulk copies (rowproj_smem_kernel), 32 rows per CTA when they fit
+    const bool two = (size_t)32 * (K + 32) * 2 <= 160 * 1024;
+    const dim3 g2((rows + (two ? 31 : 15)) / (two ? 32 : 16));
+    const size_t smem = (size_t)(two ? 32 : 16) * (K + 32) * 2;
+    auto launch = [&](auto kern) -> int {
+      static cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
       LX_CHECK_CUDA(a);
-      launch_k(rowproj_smem_kernel<1>, grid, 32 * kRpWarps, smem, stream, xb, ldx, rows, K, K_full, r, scale, wp, y, ldy, ybf, ldyb);
-    } else {
-      static cudaError_t a = cudaFuncSetAttribute(rowproj_smem_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      LX_CHECK_CUDA(a);
-      launch_k(rowproj_smem_kernel<2>, grid, 32 * kRpWarps, smem, stream, xb, ldx, rows, K, K_full, r, scale, wp, y, ldy, ybf, ldyb);
-    }
+      launch_k(kern, g2, 32 * kRpWarps, smem, stream, xb, ldx, rows, K, K_full, r, scale, wp, y, ldy, ybf, ldyb);
+      return LX_OK;
+    };
+    int rc = RP == 8 ? (two ? launch(rowproj_smem_kernel<1, 2>) : launch(rowproj_smem_kernel<1, 1>))
+                     : (two ? launch(rowproj_smem_kernel<2, 2>) : launch(rowproj_smem_kernel<2, 1>));
+    if (rc) return rc;
     return launch_check("rowproj_smem");
   }
+
   if (RP == 8)
     launch_k(rowproj_mma2_kernel<1>, grid, 32 * kRpWarps, 0, stream, xb, ldx, rows, K, K_full, r, scale, counts, counts ? blk : 1, wp,
                                                                0, counts ? ids : nullptr, counts ? K / blk : 0, y, ldy, ybf, ldyb);

@@ -301,13 +301,15 @@ def test_cross_entropy_kernel_persistent_rows():
 
 @pytest.mark.parametrize("gather", [False, True])
 @pytest.mark.parametrize("r,rp", [(8, 8), (16, 16), (4, 8), (12, 16)])
-def test_rowproj_packed_and_pack_params(gather, r, rp):
+@pytest.mark.parametrize("K", [1024, 4096])
+def test_rowproj_packed_and_pack_params(gather, r, rp, K):
     """lx_pack_params (fp32 LoRA factor -> bf16 hi/lo pack) feeding lx_rowproj_packed, dense and gathered
-    through the item's active block ids, with the optional bf16 copy of Y (K-extended GEMM columns)."""
+    through the item's active block ids, with the optional bf16 copy of Y (K-extended GEMM columns). K 1024:
+    32-row CTAs with a ragged last CTA; K 4096: the 16-row variant."""
     from paper_2510_15964_b200 import _abi, neuron_ops as N
 
     dev = _dev()
-    n_items, s, K, blk = 3, 300, 1024, 16
+    n_items, s, blk = 3, 300, 16
     n_blk = K // blk
     masks, counts, ids = _masks(n_items, n_blk, 0.4, seed=r + rp)
     g = torch.Generator(device="cpu").manual_seed(r)
