@@ -783,15 +783,21 @@ int lx_rowproj_packed(const uint16_t* x, int ldx, int n_items, int s, int K, con
     const bool two = (size_t)32 * (K + 32) * 2 <= 160 * 1024;
     const dim3 g2((rows + (two ? 31 : 15)) / (two ? 32 : 16));
     const size_t smem = (size_t)(two ? 32 : 16) * (K + 32) * 2;
-    auto launch = [&](auto kern) -> int {
-      static cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      LX_CHECK_CUDA(a);
-      launch_k(kern, g2, 32 * kRpWarps, smem, stream, xb, ldx, rows, K, K_full, r, scale, wp, y, ldy, ybf, ldyb);
-      return LX_OK;
-    };
-    int rc = RP == 8 ? (two ? launch(rowproj_smem_kernel<1, 2>) : launch(rowproj_smem_kernel<1, 1>))
-                     : (two ? launch(rowproj_smem_kernel<2, 2>) : launch(rowproj_smem_kernel<2, 1>));
-    if (rc) return rc;
+    // the dynamic shared-memory opt-in is per kernel: set it once for each of the four instantiations
+    static const cudaError_t attr = [] {
+      cudaError_t e = cudaFuncSetAttribute(rowproj_smem_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(rowproj_smem_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(rowproj_smem_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(rowproj_smem_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      return e;
+    }();
+    LX_CHECK_CUDA(attr);
+    auto kern = RP == 8 ? (two ? rowproj_smem_kernel<1, 2> : rowproj_smem_kernel<1, 1>)
+                        : (two ? rowproj_smem_kernel<2, 2> : rowproj_smem_kernel<2, 1>);
+    launch_k(kern, g2, 32 * kRpWarps, smem, stream, xb, ldx, rows, K, K_full, r, scale, wp, y, ldy, ybf, ldyb);
     return launch_check("rowproj_smem");
   }
 
