@@ -567,6 +567,54 @@ _NO_PACK = __import__("os").environ.get("LX_NO_PACK", "0") == "1"
 _PACK_CACHE_BYTES = float(__import__("os").environ.get("LX_PACK_CACHE_GB", "48")) * 2**30
 
 
+# LX_SIDE_ROWPROJ=0: the LoRA down-projections of the LN outputs (x A_qkv, h2 A1) on the main stream instead of an
+# auxiliary stream beside the attention-predictor / MLP-mask chains they do not depend on
+_SIDE_ROWPROJ = __import__("os").environ.get("LX_SIDE_ROWPROJ", "1") != "0"
+_AUX_STREAMS: dict = {}
+
+
+def _aux_stream(device):
+    if not _SIDE_ROWPROJ:
+        return None
+    key = torch.device(device).index
+    if key not in _AUX_STREAMS:
+        _AUX_STREAMS[key] = torch.cuda.Stream(device=device)
+    return _AUX_STREAMS[key]
+
+
+def _side_call(fn, inputs, device):
+    """Run fn() on the auxiliary stream after everything queued so far; returns a handle for _side_join. Inputs
+    made on the main stream are recorded on the side stream (allocator safety); captured into a CUDA graph as a
+    fork / join like the engine's other side stream."""
+    side = _aux_stream(device)
+    if side is None:
+        return (fn(), None)
+    main = torch.cuda.current_stream(device)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        out = fn()
+    for t in inputs:
+        t.record_stream(side)
+    return (out, side)
+
+
+def _side_join(handle):
+    """The result of a _side_call, with the main stream ordered after it."""
+    out, side = handle
+    if side is not None:
+        main = torch.cuda.current_stream(out.device)
+        main.wait_stream(side)
+        out.record_stream(main)
+    return out
+
+
+def _qkv_ext_ready(lw, lora: dict, x_ext) -> bool:
+    """The q/k/v LoRA rides in the projection GEMM by K-extension (mha_forward's ext path)."""
+    tq = [t for t in ("wq", "wk", "wv") if t in lora]
+    lp = lw.lora_pack
+    return bool(tq) and x_ext is not None and lp is not None and lp["kx"] > 0 and lp["tq"] == tuple(tq)
+
+
 def _qkv_lora(lora: dict, d: int):
     """Targets among wq/wk/wv and their concatenated A [d, n*r] (sf/model.py:292-304): one rowproj
     computes x A for all of them."""
@@ -614,7 +662,7 @@ def _bias_bf16(lw: LayerWeights, name: str, frozen: bool) -> torch.Tensor:
 
 
 def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: ModelDims, counter=None, *, dpool=None,
-                x_ext=None, frozen_bias: bool = False):
+                x_ext=None, frozen_bias: bool = False, ax_pre=None):
     """Block-sparse multi-head attention (sf/model.py:322-360). x: LN1 output bf16 [B, s, d] (or [s, d]).
     The dense projections are plain library GEMMs (_proj: cuBLAS, bias in the addmm); the q/k/v LoRA deltas
     ride in the same GEMM by K-extension ([x | xA] x [W ; s B]), else each is a rank-r update of its column slice.
@@ -626,7 +674,7 @@ def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: Mode
     pidx, stride = resolve_head_patterns(head_patterns, dp, B, H, x2.device)
     tq = [t for t in ("wq", "wk", "wv") if t in lora]
     lp = lw.lora_pack
-    ext = bool(tq) and x_ext is not None and lp is not None and lp["kx"] > 0 and lp["tq"] == tuple(tq)
+    ext = _qkv_ext_ready(lw, lora, x_ext)
     # the concatenated A is only an operand of the unfused path (the fused one reads the packs)
     tq, a_cat, r = _qkv_lora(lora, d) if not ext else (tq, None, lora[tq[0]].rank)
     bqkv16 = _bias_bf16(lw, "bqkv", frozen_bias) if _PROJ_CUBLAS else None
@@ -634,7 +682,10 @@ def mha_forward(x, lw: LayerWeights, lora: dict, head_patterns, pool, dims: Mode
     if ext:
         # K-extended projection: x_ext = [x | xA_cat] (bf16 LoRA columns written by the rowproj), W_ext rows d.. = s*B
         kx = lp["kx"]
-        ax = rowproj_packed(x_ext, B, s, d, lp["a_qkv"], kx, out_bf16=x_ext[:, d:])  # fp32 [M, n*r] for the LoRA grads
+        if ax_pre is not None:  # launched on the auxiliary stream right after LN1 (block_forward)
+            ax = _side_join(ax_pre)
+        else:
+            ax = rowproj_packed(x_ext, B, s, d, lp["a_qkv"], kx, out_bf16=x_ext[:, d:])  # fp32 [M, n*r] for the grads
         qkv = _proj(x_ext, lw.wqkv_ext[: d + kx, : 3 * d], lw.bqkv, bqkv16)
     else:
         qkv = _proj(x2, lw.wqkv, lw.bqkv, bqkv16)  # bf16 [M, 3d]
@@ -666,7 +717,7 @@ def dp_nnz(dp: DevicePool, i: int) -> int:
 
 
 def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, counter=None, *, resid=None,
-                out_f32: bool = False):
+                out_f32: bool = False, ax1_pre=None):
     """ReLU MLP restricted to active neuron blocks (sf/model.py:363-400) on the tcgen05
     gather-GEMMs with bias / LoRA / ReLU fused in the epilogues. x: LN2 output bf16.
     With `resid` (fp32) the fc2 epilogue returns resid + MLP (the block's residual add)."""
@@ -683,6 +734,8 @@ def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, c
     lp = lw.lora_pack
     if ad1 is None:
         ax1 = None
+    elif ax1_pre is not None:  # launched on the auxiliary stream right after LN2 (block_forward)
+        ax1 = _side_join(ax1_pre)
     elif lp is not None and lp.get("a1") is not None:
         ax1 = rowproj_packed(x2, B, s, d, lp["a1"], ad1.rank)
     else:
@@ -725,6 +778,11 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
     kx = lw.lora_pack["kx"] if (model.peft_method == "lora" and lw.lora_pack is not None) else 0
     h1, c1 = layernorm_forward(x, lw.ln1_g, lw.ln1_b, x_small_spec=spec, ext_cols=kx)
     h1v = h1.view(B, s, d)
+    # the q/k/v LoRA down-projection x A_qkv only needs LN1's output: it runs beside the attention predictor
+    ax_pre = None
+    if not static and _qkv_ext_ready(lw, lora, c1["y_ext"]):
+        ye, lp = c1["y_ext"], lw.lora_pack
+        ax_pre = _side_call(lambda: rowproj_packed(ye, B, s, d, lp["a_qkv"], lp["kx"], out_bf16=ye[:, d:]), [ye], h1.device)
     if static:
         hp = masks.head_patterns
     elif spec is not None:
@@ -734,7 +792,7 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
     adapter = model.peft_method == "adapter"
     x2 = c1["x"]  # the block input (materialised by LN1 when x was a pending residual)
     att, ca = mha_forward(h1v, lw, lora, hp, model.pool, model.dims, counter, dpool=model.dpool, x_ext=c1["y_ext"],
-                          frozen_bias=model.peft_method != "bitfit")
+                          frozen_bias=model.peft_method != "bitfit", ax_pre=ax_pre)
     caa = None
     if adapter:
         # y = x + adapter(attn): the residual add fused into the adapter kernel's store
@@ -745,9 +803,15 @@ def block_forward(x, model: Model, layer: int, masks, counter=None):
         h2, c2 = layernorm_forward(x2, lw.ln2_g, lw.ln2_b, delta=att)
     y = c2["x"]
     h2v = h2.view(B, s, d)
+    # the w1 LoRA down-projection h2 A1 only needs LN2's output: it runs beside the MLP-mask prediction
+    ax1_pre = None
+    lp = lw.lora_pack
+    if not static and "w1" in lora and lp is not None and lp.get("a1") is not None:
+        r1 = lora["w1"].rank
+        ax1_pre = _side_call(lambda: rowproj_packed(h2, B, s, d, lp["a1"], r1), [h2], h1.device)
     nm = masks.neuron_mask if static else masks.mlp_mask(layer, h2v)
     # the MLP's residual add (y + MLP) is deferred into the next LayerNorm: fc2 stores bf16 only
-    mo, cm = mlp_forward(h2v, lw, lora, nm, model.dims, counter, out_f32=adapter)
+    mo, cm = mlp_forward(h2v, lw, lora, nm, model.dims, counter, out_f32=adapter, ax1_pre=ax1_pre)
     cma = None
     if adapter:
         out, cma = adapter_forward(mo, model.adapters[(layer, "mlp")], resid=y)
