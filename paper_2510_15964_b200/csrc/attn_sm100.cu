@@ -980,8 +980,10 @@ struct AttnDkdvPP {
   static constexpr int kOffRing = kKV * 2 * kT;
   static constexpr int kOffL = kOffRing + kSt * 2 * kT;          // lse [kSt][128], delta [kSt][128]
   static constexpr int kStgPitch = 144;                          // staging row: 128 B of bf16 + 16 B pad
-  static constexpr int kOffStg = kOffL + 2 * kSt * kAT * 4;      // [8 warps][32 rows][kStgPitch]
-  static constexpr int kOffBar = kOffStg + 8 * 32 * kStgPitch;
+  // HD 128 stages 16 rows per warp at a time (two rounds), so the kernel fits in 227 KB of shared memory
+  static constexpr int kStgRows = HD == 64 ? 32 : 16;
+  static constexpr int kOffStg = kOffL + 2 * kSt * kAT * 4;      // [8 warps][kStgRows rows][kStgPitch]
+  static constexpr int kOffBar = kOffStg + 8 * kStgRows * kStgPitch;
   static constexpr int kTotal = kOffBar + 512 + 1024;
 };
 
@@ -1260,9 +1262,11 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
       // dK / dV rows -> bf16 through a per-warp staging tile, stored as full 128-byte row segments
       const uint32_t tcol = (wg == 0 ? t_dk : t_dv) + lane_base;
       const float mul = wg == 0 ? scale : 1.f;
-      uint8_t* stg = sm + L::kOffStg + (warp - 2) * 32 * L::kStgPitch;
+      uint8_t* stg = sm + L::kOffStg + (warp - 2) * L::kStgRows * L::kStgPitch;
+      constexpr int kRounds = 32 / L::kStgRows;
 #pragma unroll
       for (int cp = 0; cp < HD / 64; ++cp) {
+        uint4 pk[8];  // this lane's row: 64 columns as bf16
 #pragma unroll
         for (int c2 = 0; c2 < 2; ++c2) {
           uint32_t ov[32];
@@ -1273,23 +1277,30 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
             float f[8];
 #pragma unroll
             for (int k2 = 0; k2 < 8; ++k2) f[k2] = n > 0 ? __uint_as_float(ov[8 * i + k2]) * mul : 0.f;
-            *reinterpret_cast<uint4*>(stg + lane * L::kStgPitch + c2 * 64 + 16 * i) =
-                make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
-                           pack_bf16x2(f[6], f[7]));
+            pk[4 * c2 + i] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                        pack_bf16x2(f[6], f[7]));
           }
         }
-        __syncwarp();
 #pragma unroll
-        for (int pass = 0; pass < 8; ++pass) {  // lane -> row pass*4 + lane/8, 16-byte piece lane%8
-          const int rr = pass * 4 + (lane >> 3), piece = lane & 7;
-          const int key = kt * kAT + quad * 32 + rr;
-          if (key < s) {
-            const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * L::kStgPitch + piece * 16);
-            *reinterpret_cast<uint4*>(dkv + ((size_t)row_base + key) * ld_dkv + (wg + 1) * d_model + h * HD + cp * 64 +
-                                      piece * 8) = v;
+        for (int rd = 0; rd < kRounds; ++rd) {
+          if ((int)lane / L::kStgRows == rd) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              *reinterpret_cast<uint4*>(stg + (lane % L::kStgRows) * L::kStgPitch + 16 * i) = pk[i];
           }
+          __syncwarp();
+#pragma unroll
+          for (int pass = 0; pass < L::kStgRows / 4; ++pass) {  // lane -> row pass*4 + lane/8, 16-byte piece lane%8
+            const int rr = pass * 4 + (lane >> 3), piece = lane & 7;
+            const int key = kt * kAT + quad * 32 + rd * L::kStgRows + rr;
+            if (key < s) {
+              const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * L::kStgPitch + piece * 16);
+              *reinterpret_cast<uint4*>(dkv + ((size_t)row_base + key) * ld_dkv + (wg + 1) * d_model + h * HD + cp * 64 +
+                                        piece * 8) = v;
+            }
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
       tc_fence_before();
       asm volatile("bar.sync 1, 256;" ::: "memory");  // every epilogue thread has drained TMEM
@@ -1663,7 +1674,7 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
   LX_CHECK_CUDA(a2);
   dim3 grid(nt, H, n_items);
   const float sl2 = scale * 1.4426950408889634f;
-  // the ping-pong kernels' rings + staging fit in shared memory for HD 64; HD 128 keeps the 2-CTA kernels
+  // the dK/dV ping-pong kernel's rings + staging fit in shared memory for HD 64; HD 128 keeps the 2-CTA kernel
   static const bool old_bwd = getenv("LX_ATTN_BWD_OLD") != nullptr || AttnDkdvPP<HD>::kTotal > 227 * 1024;
   if (old_bwd) {
     launch_k(bsattn_dkdv_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, tm_g, tm_do_g, gu, s, H, H * HD, pidx, item_stride,
@@ -1677,7 +1688,9 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
              reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, (const int4*)desc_kv);
   }
   if ((rc = launch_check("bsattn_dkdv_tc"))) return rc;
-  if (old_bwd || AttnDqPP<HD>::kTotal > 227 * 1024) {
+  // the dQ ping-pong kernel fits at HD 128 too (1 Q/dO buffer, 2-stage K/V ring: 215 KB), whichever dK/dV ran
+  static const bool old_dq = getenv("LX_ATTN_BWD_OLD") != nullptr || AttnDqPP<HD>::kTotal > 227 * 1024;
+  if (old_dq) {
     launch_k(bsattn_dq_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, tm_g, gu, s, H, H * HD, pidx, item_stride, tables128,
              scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, (const float*)kbar);
   } else {
