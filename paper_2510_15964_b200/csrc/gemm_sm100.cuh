@@ -252,11 +252,8 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     if (CTAS == 2) tmem_alloc_cg2<512>(tmem_slot);
     else tmem_alloc<512>(tmem_slot);
   }
-  // prologue above overlaps the predecessor kernel's tail (programmatic dependent launch). kDenseDual: B (the
-  // frozen predictor weights) does not depend on the predecessor, so the first stages' B boxes are issued before
-  // the grid-dependency wait (below, after the cluster barrier that makes the leader's barriers valid)
-  constexpr bool kPreB = BMODE == kDenseDual && CL == 1;
-  if (!kPreB) pdl_wait_trigger();
+  // prologue above overlaps the predecessor kernel's tail (programmatic dependent launch)
+  pdl_wait_trigger();
   // ---- tile table: prefix[b] = first tile index of item b (counts are device-resident)
   // counts -> shared memory in one parallel round trip (the epilogue's staging area is free until the first tile)
   int* s_cnt = reinterpret_cast<int*>(smem + L::kEpiOff);
@@ -306,23 +303,6 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   // so a narrower launch width gives more stages in flight over the same shared memory (latency-bound mainloop)
   const int stage_bytes = (kWide && wsel) ? L::kABytes + 64 * wsel : L::kStageBytes;
   const int S = kWide ? min(L::kMaxStg, (S0 * L::kStageBytes) / stage_bytes) : S0;
-  int n_pre = 0;  // kPreB: stages of the first tile whose B boxes (and expect-tx) are already issued
-  if (kPreB) {
-    if (warp == 0 && t0 < n_tiles_total) {
-      const TileInfo ti = decode_tile<BMODE, BN>(args, prefix, args.counts, m_tiles, t0, wsel);
-      n_pre = min(S, ti.k_stages);
-      if (lane == 0) {
-        const uint64_t pol = policy_evict_last();
-        for (int ks = 0; ks < n_pre; ++ks) {
-          uint8_t* sb = smem + ks * stage_bytes + L::kABytes;
-          if (leader) mbar_arrive_expect_tx(full + ks, 2 * (L::kABytes + L::kBBytes));
-          tma_load_2d_cg2(sb, &tmap_b, full + ks, ks * kBK, ti.n0 + prank * (BNC / 2), pol);
-          tma_load_2d_cg2(sb + (BNC / 2) * 128, &tmap_b, full + ks, args.dual_k + ks * kBK, ti.n0 + prank * (BNC / 2), pol);
-        }
-      }
-    }
-    pdl_wait_trigger();
-  }
 
   // counts are needed by every role to decode tiles; read through L1 per decode.
   const int* cnts = args.counts;
@@ -386,9 +366,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             if (++stage == S) { stage = 0; phase ^= 1; }
             continue;
           }
-          if (lane == 0 && n_pre > 0) {  // kPreB: B and the expect-tx of this stage were issued before the wait
-            tma_load_2d_cg2(sa, &tmap_a, full + stage, ks * kBK, row0, pol_w);
-          } else if (lane == 0) {
+          if (lane == 0) {
             if (leader) mbar_arrive_expect_tx(full + stage, 2 * (L::kABytes + L::kBBytes));
             const int ak =
                 (is_dense<BMODE>() && args.a_k_split && ks * kBK >= args.a_k_split) ? ks * kBK - args.a_k_split : ks * kBK;
@@ -424,7 +402,6 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             }
           }
           __syncwarp();
-          if (n_pre > 0) --n_pre;
           if (++stage == S) { stage = 0; phase ^= 1; }
           continue;
         }
