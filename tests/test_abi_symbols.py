@@ -58,3 +58,16 @@ def test_integration_bindings_match_the_abi_table():
     for name, args in found:
         types = [alias[a.strip()] for a in args.split(",")]
         assert types == list(_abi.SIGNATURES[name]), name
+
+
+def test_bench_counts_every_kernel_call_of_the_step():
+    """bench.py's gpu_launches counts kernels per C-ABI call: every entry point the fine-tune step calls
+    (engine, model, autograd, neuron_ops, predictor, block_sparse, dp) has a kernel count."""
+    import bench
+
+    names = set()
+    for mod in ("engine", "model", "autograd", "neuron_ops", "predictor", "block_sparse", "dp"):
+        names |= set(re.findall(r'_abi\.call\(\s*"(lx_\w+)"', (ROOT / "paper_2510_15964_b200" / f"{mod}.py").read_text()))
+    debug = {"lx_debug_set_gemm_trace", "lx_debug_set_attn_trace"}
+    missing = sorted(n for n in names - debug if n not in bench.KERNELS_PER_CALL)
+    assert not missing, missing
