@@ -160,7 +160,21 @@ LX_DEV float warp_sum(float v) {
   return v;
 }
 
-template <int VEC>
+// Row sum over the TPR threads that own a row. TPR 64 (d = 2048: 8 float4 per lane instead of 16, so ~60 instead of
+// ~120 registers and twice the rows in flight per SM): the two warps' partial sums meet in shared memory behind a
+// 64-thread named barrier (id 1 + row slot), added in warp order (deterministic). k selects the slot pair of the
+// first / second reduction of a row, so a partner still reading slot k of this row never races the next write.
+template <int TPR>
+LX_DEV float row_sum(float v, float* red, int k) {
+  v = warp_sum(v);
+  if (TPR == 32) return v;
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[k * 8 + warp] = v;
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp >> 1)) : "memory");
+  return red[k * 8 + (warp & ~1)] + red[k * 8 + (warp | 1)];
+}
+
+template <int VEC, int TPR>
 __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const float* __restrict__ x, int M, int d,
                                                           const float* __restrict__ g, const float* __restrict__ b,
                                                           float eps, __nv_bfloat16* __restrict__ y, int ldy,
@@ -169,24 +183,26 @@ __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const float* __restric
                                                           const __nv_bfloat16* __restrict__ delta,
                                                           float* __restrict__ resid_out) {
   pdl_wait_trigger();
-  const int lane = threadIdx.x & 31;
+  constexpr int RPC = 256 / TPR;  // rows per CTA pass
+  __shared__ float red[16];
+  const int lane = threadIdx.x % TPR;
   const int nv = d / 4;
 #pragma unroll 1
-  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < M; row += gridDim.x * 8) {
+  for (int row = blockIdx.x * RPC + (int)threadIdx.x / TPR; row < M; row += gridDim.x * RPC) {
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * d);
   const uint2* dr = delta ? reinterpret_cast<const uint2*>(delta + (size_t)row * d) : nullptr;
   float4 v[VEC];
   uint2 dv[VEC];
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
-    const int c = lane + 32 * i;
+    const int c = lane + TPR * i;
     v[i] = c < nv ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
     dv[i] = (dr && c < nv) ? __ldg(dr + c) : make_uint2(0u, 0u);
   }
   float sum = 0.f;
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
-    const int c = lane + 32 * i;
+    const int c = lane + TPR * i;
     if (dr && c < nv) {  // fused residual add: y = x + delta (sf/model.py:420, 427), y kept in fp32
       v[i].x += bf16_bits_to_float(dv[i].x & 0xffff);
       v[i].y += bf16_bits_to_float(dv[i].x >> 16);
@@ -196,17 +212,17 @@ __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const float* __restric
     }
     sum += (v[i].x + v[i].y) + (v[i].z + v[i].w);
   }
-  const float mu = warp_sum(sum) / d;
+  const float mu = row_sum<TPR>(sum, red, 0) / d;
   float sq = 0.f;
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
-    const int c = lane + 32 * i;
+    const int c = lane + TPR * i;
     if (c < nv) {
       const float a = v[i].x - mu, bb = v[i].y - mu, cc = v[i].z - mu, dd = v[i].w - mu;
       sq += (a * a + bb * bb) + (cc * cc + dd * dd);
     }
   }
-  const float istd = 1.0f / sqrtf(warp_sum(sq) / d + eps);
+  const float istd = 1.0f / sqrtf(row_sum<TPR>(sq, red, 1) / d + eps);
   if (lane == 0) {
     mean_out[row] = mu;
     istd_out[row] = istd;
@@ -221,7 +237,7 @@ __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const float* __restric
   const float4* b4 = reinterpret_cast<const float4*>(b);
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
-    const int c = lane + 32 * i;
+    const int c = lane + TPR * i;
     if (c < nv) {
       const float4 gg = __ldg(g4 + c), bb = __ldg(b4 + c);
       const uint2 pk = make_uint2(pack_bf16x2((v[i].x - mu) * istd * gg.x + bb.x, (v[i].y - mu) * istd * gg.y + bb.y),
@@ -233,29 +249,31 @@ __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const float* __restric
   }
 }
 
-template <bool kF32, int VEC>
+template <bool kF32, int VEC, int TPR>
 __global__ void __launch_bounds__(256) ln_bwd_warp_kernel(const void* __restrict__ dy_, const float* __restrict__ x,
                                                           const float* __restrict__ g, const float* __restrict__ mean,
                                                           const float* __restrict__ istd, int M, int d,
                                                           float* __restrict__ dx, __nv_bfloat16* __restrict__ dx_bf16) {
   pdl_wait_trigger();
-  const int lane = threadIdx.x & 31;
+  constexpr int RPC = 256 / TPR;
+  __shared__ float red[16];
+  const int lane = threadIdx.x % TPR;
   const int nv = d / 4;
 #pragma unroll 1
-  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < M; row += gridDim.x * 8) {
+  for (int row = blockIdx.x * RPC + (int)threadIdx.x / TPR; row < M; row += gridDim.x * RPC) {
   const float mu = __ldg(mean + row), is = __ldg(istd + row);
   float4* o = reinterpret_cast<float4*>(dx + (size_t)row * d);
   float4 cur[VEC];  // the accumulator row is loaded with the inputs: one round trip per row
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
-    const int c = lane + 32 * i;
+    const int c = lane + TPR * i;
     cur[i] = c < nv ? o[c] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   float4 gv[VEC], xh[VEC];
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
-    const int c = lane + 32 * i;
+    const int c = lane + TPR * i;
     float4 dy = make_float4(0.f, 0.f, 0.f, 0.f), xx = dy, gg = dy;
     if (c < nv) {
       if (kF32) {
@@ -274,10 +292,10 @@ __global__ void __launch_bounds__(256) ln_bwd_warp_kernel(const void* __restrict
     s1 += (gv[i].x + gv[i].y) + (gv[i].z + gv[i].w);
     s2 += (gv[i].x * xh[i].x + gv[i].y * xh[i].y) + (gv[i].z * xh[i].z + gv[i].w * xh[i].w);
   }
-  const float mg = warp_sum(s1) / d, mgx = warp_sum(s2) / d;
+  const float mg = row_sum<TPR>(s1, red, 0) / d, mgx = row_sum<TPR>(s2, red, 1) / d;
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
-    const int c = lane + 32 * i;
+    const int c = lane + TPR * i;
     if (c < nv) {
       cur[i].x += is * (gv[i].x - mg - xh[i].x * mgx);
       cur[i].y += is * (gv[i].y - mg - xh[i].y * mgx);
@@ -294,30 +312,29 @@ __global__ void __launch_bounds__(256) ln_bwd_warp_kernel(const void* __restrict
 
 // persistent grid for the warp-per-row kernels: as many 8-row CTAs as fit at once (no partial last wave)
 template <typename K>
-static int ln_grid(K kern, int M) {
+static int ln_grid(K kern, int M, int rows_per_cta = 8) {
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
-  const int ctas = (M + 7) / 8;
+  const int ctas = (M + rows_per_cta - 1) / rows_per_cta;
   return ctas < per_sm * num_sms() ? ctas : per_sm * num_sms();
 }
 
-template <int VEC>
+template <int VEC, int TPR = 32>
 static void ln_fwd_warp(const float* x, const uint16_t* delta, float* resid_out, int M, int d, const float* gamma,
                         const float* beta, float eps, uint16_t* y, int ldy, float* mean, float* inv_std, int s, int m_small,
                         uint16_t* x_small, cudaStream_t st) {
-  launch_k(ln_fwd_warp_kernel<VEC>, ln_grid(ln_fwd_warp_kernel<VEC>, M), 256, 0, st, x, M, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), ldy, mean,
+  auto kern = ln_fwd_warp_kernel<VEC, TPR>;
+  launch_k(kern, ln_grid(kern, M, 256 / TPR), 256, 0, st, x, M, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), ldy, mean,
                                                        inv_std, s > 0 ? s : 1, m_small,
                                                        reinterpret_cast<__nv_bfloat16*>(x_small),
                                                        reinterpret_cast<const __nv_bfloat16*>(delta), resid_out);
 }
 
-template <int VEC>
+template <int VEC, int TPR = 32>
 static void ln_bwd_warp(const void* dy, int dy_is_f32, const float* x, const float* gamma, const float* mean,
                         const float* inv_std, int M, int d, float* dx, __nv_bfloat16* ob, cudaStream_t st) {
-  if (dy_is_f32)
-    launch_k(ln_bwd_warp_kernel<true, VEC>, ln_grid(ln_bwd_warp_kernel<true, VEC>, M), 256, 0, st, dy, x, gamma, mean, inv_std, M, d, dx, ob);
-  else
-    launch_k(ln_bwd_warp_kernel<false, VEC>, ln_grid(ln_bwd_warp_kernel<false, VEC>, M), 256, 0, st, dy, x, gamma, mean, inv_std, M, d, dx, ob);
+  auto kern = dy_is_f32 ? ln_bwd_warp_kernel<true, VEC, TPR> : ln_bwd_warp_kernel<false, VEC, TPR>;
+  launch_k(kern, ln_grid(kern, M, 256 / TPR), 256, 0, st, dy, x, gamma, mean, inv_std, M, d, dx, ob);
 }
 
 }  // namespace lx
@@ -338,7 +355,7 @@ int lx_layernorm_fwd(const float* x, const uint16_t* delta, float* resid_out, in
   if (per_lane <= 16) {
     if (per_lane <= 4) ln_fwd_warp<4>(x, delta, resid_out, M, d, gamma, beta, eps, y, ldy, mean, inv_std, s, m_small, x_small, stream);
     else if (per_lane <= 8) ln_fwd_warp<8>(x, delta, resid_out, M, d, gamma, beta, eps, y, ldy, mean, inv_std, s, m_small, x_small, stream);
-    else ln_fwd_warp<16>(x, delta, resid_out, M, d, gamma, beta, eps, y, ldy, mean, inv_std, s, m_small, x_small, stream);
+    else ln_fwd_warp<8, 64>(x, delta, resid_out, M, d, gamma, beta, eps, y, ldy, mean, inv_std, s, m_small, x_small, stream);
     return launch_check("layernorm_fwd");
   }
   const int vec = (d / 4 + kLnThreads - 1) / kLnThreads;  // block kernel: float4 per thread
@@ -357,7 +374,7 @@ int lx_layernorm_bwd(const void* dy, int dy_is_f32, const float* x, const float*
   if (per_lane <= 16) {
     if (per_lane <= 4) ln_bwd_warp<4>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
     else if (per_lane <= 8) ln_bwd_warp<8>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
-    else ln_bwd_warp<16>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
+    else ln_bwd_warp<8, 64>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
     return launch_check("layernorm_bwd");
   }
   const int vec = (d / 4 + kLnThreads - 1) / kLnThreads;
