@@ -331,6 +331,12 @@ static int ln_tpr() {
   return t;
 }
 
+// LX_LN_BLOCK=1: the one-CTA-per-row block kernels for 2048 < d <= 4096 as well (measurements)
+static bool ln_block() {
+  static const bool b = [] { const char* e = getenv("LX_LN_BLOCK"); return e && e[0] == '1'; }();
+  return b;
+}
+
 template <int VEC, int TPR = 32>
 static void ln_fwd_warp(const float* x, const uint16_t* delta, float* resid_out, int M, int d, const float* gamma,
                         const float* beta, float eps, uint16_t* y, int ldy, float* mean, float* inv_std, int s, int m_small,
@@ -372,6 +378,10 @@ int lx_layernorm_fwd(const float* x, const uint16_t* delta, float* resid_out, in
     else ln_fwd_warp<4, 128>(x, delta, resid_out, M, d, gamma, beta, eps, y, ldy, mean, inv_std, s, m_small, x_small, stream);
     return launch_check("layernorm_fwd");
   }
+  if (d <= 4096 && !ln_block()) {  // cfg4: four warps per row, 8 float4 per lane
+    ln_fwd_warp<8, 128>(x, delta, resid_out, M, d, gamma, beta, eps, y, ldy, mean, inv_std, s, m_small, x_small, stream);
+    return launch_check("layernorm_fwd");
+  }
   const int vec = (d / 4 + kLnThreads - 1) / kLnThreads;  // block kernel: float4 per thread
   auto kf = vec <= 4 ? ln_fwd_kernel<4> : vec <= 6 ? ln_fwd_kernel<6> : ln_fwd_kernel<8>;
   launch_k(kf, M, kLnThreads, 0, stream, x, d, gamma, beta, eps, reinterpret_cast<__nv_bfloat16*>(y), ldy, mean, inv_std,
@@ -391,6 +401,10 @@ int lx_layernorm_bwd(const void* dy, int dy_is_f32, const float* x, const float*
     else if (ln_tpr() == 64) ln_bwd_warp<8, 64>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
     else if (ln_tpr() == 256) ln_bwd_warp<2, 256>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
     else ln_bwd_warp<4, 128>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
+    return launch_check("layernorm_bwd");
+  }
+  if (d <= 4096 && !ln_block()) {
+    ln_bwd_warp<8, 128>(dy, dy_is_f32, x, gamma, mean, inv_std, M, d, dx_accum, ob, stream);
     return launch_check("layernorm_bwd");
   }
   const int vec = (d / 4 + kLnThreads - 1) / kLnThreads;
