@@ -1319,6 +1319,368 @@ bsattn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
   }
 }
 
+// ============================================================================ backward dK/dV, two unit streams
+// At sparse layouts most units (key tile, head, item) hold one or two query tiles, so the ping-pong kernel above
+// runs one serial chain per unit (K/V -> S -> P -> dV, dP -> dS -> dK -> drain) with one of its warpgroups idle.
+// Here a CTA runs two INDEPENDENT unit streams, each a full pipeline of its own: producer warp, MMA-issuer warp, a
+// 4-warp epilogue group, its own K/V buffer, Q/dO ring, S/dP TMEM buffer and dK/dV accumulators (HD 64: TMEM
+// S/dP at 128 w, dV / dK at 256 + 128 w). The two chains meet only at the tensor core and the MUFU, which
+// interleave them. The CTA's units are ordered by entry count (largest first) and dealt greedily to the stream
+// with the smaller load (entries + 1 per unit), so the streams finish together; each unit's dK/dV sums run in
+// entry order (deterministic). An empty unit is written as zeros by its epilogue group alone.
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kDsThreads = 384;  // warps 0/1 stream-0 producer/MMA, 2-5 and 6-9 epilogue groups, 10/11 stream-1
+constexpr int kDsSortMax = 64;   // units per CTA dealt by entry count; beyond, units alternate between streams
+template <int HD>
+struct AttnDkdvDs {
+  static constexpr int kT = kAT * 128;                       // one 128 x 64 bf16 tile
+  static constexpr int kSt = 2;                              // Q/dO ring stages per stream
+  static constexpr int kStgRows = 16;                        // drain staging rows per warp (two rounds)
+  static constexpr int kStgPitch = 144;
+  static constexpr int kOffRing = 2 * kT;                    // per stream: [K|V] [ring] [lse|delta] [staging]
+  static constexpr int kOffL = kOffRing + kSt * 2 * kT;
+  static constexpr int kOffStg = kOffL + 2 * kSt * kAT * 4;
+  static constexpr int kStream = kOffStg + 4 * kStgRows * kStgPitch;  // 107 KB, a multiple of 1024
+  static constexpr int kOffBar = 2 * kStream;
+  static constexpr int kTotal = kOffBar + 512 + 1024;
+  static_assert(kStream % 1024 == 0, "stream 1's tiles must stay 1024-aligned for SWIZZLE_128B");
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kDsThreads, 1)
+bsattn_dkdv_ds_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                      const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_do_g, int gu, int s, int H,
+                      int n_units, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
+                      float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
+                      __nv_bfloat16* __restrict__ dkv, int ld_dkv, const int4* __restrict__ desc) {
+  static_assert(HD == 64, "two streams' S/dP buffers and dK/dV accumulators fill TMEM at HD 64");
+  using L = AttnDkdvDs<HD>;
+  const int d_model = H * HD;
+  const int nkt = (s + kAT - 1) / kAT;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ int s_list[2][kDsSortMax];
+  __shared__ int s_cnt[2];
+  uint8_t* sm = align_smem_1024(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
+  // per stream w, at bars + 16 w: kv_full, kv_empty, qd_full[2], qd_empty[2], s_full, p_ready (4 warps), dp_full,
+  // ds_ready (4 warps), acc_full, acc_empty (1 arrival after the group's drain barrier)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+  uint64_t* sMaskAll = bars + 40;  // [2][kSt]
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_g);
+    tma_prefetch_desc(&tm_do_g);
+    for (int w = 0; w < 2; ++w) {
+      uint64_t* b = bars + 16 * w;
+      for (int i = 0; i < 6; ++i) mbar_init(b + i, 1);
+      mbar_init(b + 6, 1);
+      mbar_init(b + 7, 4);
+      mbar_init(b + 8, 1);
+      mbar_init(b + 9, 4);
+      mbar_init(b + 10, 1);
+      mbar_init(b + 11, 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  pdl_wait_trigger();
+  const int G = gridDim.x;
+  const int n_mine = n_units > (int)blockIdx.x ? (n_units - (int)blockIdx.x + G - 1) / G : 0;
+  const bool dealt = n_mine <= kDsSortMax;
+  if (threadIdx.x == 0 && dealt) {
+    int cnt[kDsSortMax], ord[kDsSortMax];
+    for (int k = 0; k < n_mine; ++k) {  // insertion sort by entry count, descending (ties keep index order)
+      const int nk = __ldg(desc + blockIdx.x + k * G).y;
+      int i = k;
+      while (i > 0 && cnt[i - 1] < nk) {
+        cnt[i] = cnt[i - 1];
+        ord[i] = ord[i - 1];
+        --i;
+      }
+      cnt[i] = nk;
+      ord[i] = k;
+    }
+    int load0 = 0, load1 = 0, c0 = 0, c1 = 0;
+    for (int i = 0; i < n_mine; ++i) {  // greedy: to the stream with the smaller load (stream 0 on ties)
+      const int u = blockIdx.x + ord[i] * G;
+      if (load0 <= load1) {
+        s_list[0][c0++] = u;
+        load0 += cnt[i] + 1;
+      } else {
+        s_list[1][c1++] = u;
+        load1 += cnt[i] + 1;
+      }
+    }
+    s_cnt[0] = c0;
+    s_cnt[1] = c1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int tab_nt = __ldg(tables), tab_per = __ldg(tables + 6);
+  // stream w's i-th unit and its count
+  auto n_stream = [&](int w) { return dealt ? s_cnt[w] : (n_mine + 1 - w) / 2; };
+  auto unit = [&](int w, int i, int& item, int& h, int& kt, const int32_t*& ents, int& e0, int& n) {
+    const int u = dealt ? s_list[w][i] : (int)blockIdx.x + (2 * i + w) * G;
+    const int4 dd = __ldg(desc + u);
+    kt = u % nkt;
+    h = (u / nkt) % H;
+    item = u / (nkt * H);
+    e0 = dd.x;
+    n = dd.y;
+    ents = desc_entries(tables, tab_nt, tab_per, dd.z, true);
+  };
+
+  if (warp < 2 || warp >= 10) {
+    const int w = warp >= 10 ? 1 : 0;
+    uint64_t* b = bars + 16 * w;
+    uint64_t *kv_full = b, *kv_empty = b + 1, *qd_full = b + 2, *qd_empty = b + 4, *s_full = b + 6, *p_ready = b + 7,
+             *dp_full = b + 8, *ds_ready = b + 9, *acc_full = b + 10, *acc_empty = b + 11;
+    uint8_t* smw = sm + w * L::kStream;
+    uint64_t* sMask = sMaskAll + w * L::kSt;
+    float* sL = reinterpret_cast<float*>(smw + L::kOffL);
+    float* sD = sL + L::kSt * kAT;
+    const int nu = n_stream(w);
+    if ((warp & 1) == 0) {
+      // ================= producer of stream w: K/V per non-empty unit, then its Q/dO tiles (+ lse / delta rows)
+      int g = 0, kvn = 0;
+      for (int i = 0; i < nu; ++i) {
+        int item, h, kt, e0, n;
+        const int32_t* ents;
+        unit(w, i, item, h, kt, ents, e0, n);
+        if (n == 0) continue;
+        const int row_base = item * s;
+        mbar_wait(kv_empty, (kvn & 1) ^ 1);
+        ++kvn;
+        if (lane == 0) {
+          mbar_arrive_expect_tx(kv_full, 2 * L::kT);
+          tma_load_2d(smw, &tm_qkv, kv_full, d_model + h * HD, row_base + kt * kAT);
+          tma_load_2d(smw + L::kT, &tm_qkv, kv_full, 2 * d_model + h * HD, row_base + kt * kAT);
+        }
+        const float* lse_b = lse + ((size_t)item * H + h) * s;
+        const float* del_b = delta + ((size_t)item * H + h) * s;
+        const int nsub = kAT / gu;
+        for (int e = 0; e < n; ++e, ++g) {
+          const int st = g % L::kSt;
+          mbar_wait(qd_empty + st, ((g / L::kSt) & 1) ^ 1);
+          const int32_t* ent = ents + (size_t)(e0 + e) * kEntryInts;
+          if (lane == 0) {
+            sMask[st] = ent_mask(ent);
+            uint8_t* sq = smw + L::kOffRing + st * 2 * L::kT;
+            mbar_arrive_expect_tx(qd_full + st, 2 * L::kT + 2 * kAT * 4);
+            tma_load_gather(sq, &tm_g, qd_full + st, h * HD, row_base, ent, gu, nsub);
+            tma_load_gather(sq + L::kT, &tm_do_g, qd_full + st, h * HD, row_base, ent, gu, nsub);
+            for (int k = 0; k < nsub; ++k) {
+              const int q0 = __ldg(ent + 2 + k) * gu;
+              bulk_load_1d(sL + st * kAT + k * gu, lse_b + q0, gu * 4, qd_full + st);
+              bulk_load_1d(sD + st * kAT + k * gu, del_b + q0, gu * 4, qd_full + st);
+            }
+          }
+          __syncwarp();
+        }
+      }
+    } else if (lane == 0) {
+      // ================= MMA issuer of stream w: per entry S^T = K Q^T | [p_ready] dV += P^T dO, dP^T = V dO^T |
+      // [ds_ready] dK += dS^T Q, then the next entry's S into the freed buffer
+      const uint32_t id_s = make_idesc_bf16(kAT, kAT, false, false);
+      const uint32_t id_g = make_idesc_bf16(kAT, HD, false, true);
+      const uint32_t tb = tmem + w * kAT, t_dv = tmem + 2 * kAT + w * 2 * HD, t_dk = t_dv + HD;
+      const uint32_t sk = smem_u32(smw), sv = sk + L::kT;
+      int g = 0, kvn = 0, accn = 0;
+      for (int i = 0; i < nu; ++i) {
+        int item, h, kt, e0, n;
+        const int32_t* ents;
+        unit(w, i, item, h, kt, ents, e0, n);
+        if (n == 0) continue;
+        mbar_wait(kv_full, kvn & 1);
+        ++kvn;
+        for (int j = 0; j < n; ++j) {
+          const int gg = g + j, st = gg % L::kSt;
+          const uint32_t sq = smem_u32(smw + L::kOffRing + st * 2 * L::kT), sdo = sq + L::kT;
+          mbar_wait(qd_full + st, (gg / L::kSt) & 1);
+          tc_fence_after();
+          for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(tb, desc_kmajor(sk, kk), desc_kmajor(sq, kk), id_s, kk != 0);
+          mma_commit(s_full);
+          if (j == 0) {
+            mbar_wait(acc_empty, (accn & 1) ^ 1);  // this stream's previous unit has been drained
+            tc_fence_after();
+          }
+          mbar_wait(p_ready, gg & 1);
+          tc_fence_after();
+          for (int kk = 0; kk < kAT / 16; ++kk) mma_bf16_ts(t_dv, tb + kk * 8, desc_mnmajor(sdo, kk), id_g, (j | kk) != 0);
+          for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(tb, desc_kmajor(sv, kk), desc_kmajor(sdo, kk), id_s, kk != 0);
+          mma_commit(dp_full);
+          if (j + 1 == n) mma_commit(kv_empty);  // K and V are read by S and dP only
+          mbar_wait(ds_ready, gg & 1);
+          tc_fence_after();
+          for (int kk = 0; kk < kAT / 16; ++kk) mma_bf16_ts(t_dk, tb + kk * 8, desc_mnmajor(sq, kk), id_g, (j | kk) != 0);
+          mma_commit(qd_empty + st);
+        }
+        mma_commit(acc_full);
+        ++accn;
+        g += n;
+      }
+    }
+  } else {
+    // ================= epilogue group wg = stream wg; thread = key row
+    const int wg = (warp - 2) >> 2, quad = warp & 3;
+    uint64_t* b = bars + 16 * wg;
+    uint64_t *qd_full = b + 2, *s_full = b + 6, *p_ready = b + 7, *dp_full = b + 8, *ds_ready = b + 9,
+             *acc_full = b + 10, *acc_empty = b + 11;
+    uint8_t* smw = sm + wg * L::kStream;
+    const uint64_t* sMask = sMaskAll + wg * L::kSt;
+    const float* sL = reinterpret_cast<const float*>(smw + L::kOffL);
+    const float* sD = sL + L::kSt * kAT;
+    const int kr = quad * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const uint32_t tb = tmem + wg * kAT + lane_base;
+    const int cj = kr >> 4;
+    const int nu = n_stream(wg);
+    int g = 0, accn = 0;
+    for (int i = 0; i < nu; ++i) {
+      int item, h, kt, e0, n;
+      const int32_t* ents;
+      unit(wg, i, item, h, kt, ents, e0, n);
+      for (int j = 0; j < n; ++j) {
+        const int gg = g + j, st = gg % L::kSt;
+        const float* l2 = sL + st * kAT;
+        const float* dl = sD + st * kAT;
+        mbar_wait(qd_full + st, (gg / L::kSt) & 1);
+        const uint64_t mask = sMask[st];
+        uint32_t mrow = 0;  // bit q16: cell (query group q16, this thread's key group) is active
+#pragma unroll
+        for (int q16 = 0; q16 < 8; ++q16) mrow |= (uint32_t)((mask >> (q16 * 8 + cj)) & 1ull) << q16;
+        mbar_wait(s_full, gg & 1);
+        tc_fence_after();
+        uint32_t pp[4][16];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t sv_[2][32];
+          tmem_ld_32x32b_x32(tb + h2 * 64, sv_[0]);
+          tmem_ld_32x32b_x32(tb + h2 * 64 + 32, sv_[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const int c = h2 * 2 + c2;
+#pragma unroll
+            for (int u2 = 0; u2 < 16; ++u2) {
+              const int qi = c * 32 + 2 * u2;
+              const float2 nl = mul2(*reinterpret_cast<const float2*>(l2 + qi), make_float2(-kLog2e, -kLog2e));
+              const float2 x = fma2(make_float2(__uint_as_float(sv_[c2][2 * u2]), __uint_as_float(sv_[c2][2 * u2 + 1])),
+                                    make_float2(scale_log2, scale_log2), nl);
+              const uint32_t pk = pack_bf16x2(ex2(x.x), ex2(x.y));
+              pp[c][u2] = (mrow >> (c * 2 + (u2 >> 3))) & 1u ? pk : 0u;
+            }
+            tmem_st_32x32b_x16(tb + c * 16, pp[c]);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_ready);
+        mbar_wait(dp_full, gg & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t dv_[2][32];
+          tmem_ld_32x32b_x32(tb + h2 * 64, dv_[0]);
+          tmem_ld_32x32b_x32(tb + h2 * 64 + 32, dv_[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const int c = h2 * 2 + c2;
+            uint32_t dd[16];
+#pragma unroll
+            for (int u2 = 0; u2 < 16; ++u2) {
+              const int qi = c * 32 + 2 * u2;
+              const float2 pf = bf16x2_unpack(pp[c][u2]);
+              const float2 t = sub2(make_float2(__uint_as_float(dv_[c2][2 * u2]), __uint_as_float(dv_[c2][2 * u2 + 1])),
+                                    *reinterpret_cast<const float2*>(dl + qi));
+              const float2 r2 = mul2(pf, t);
+              dd[u2] = pack_bf16x2(r2.x, r2.y);
+            }
+            tmem_st_32x32b_x16(tb + c * 16, dd);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ds_ready);
+      }
+      g += n;
+      // ---- unit drain: dK (scaled) into column block 1, dV into block 2, through 16-row staging
+      if (n > 0) {
+        mbar_wait(acc_full, accn & 1);
+        tc_fence_after();
+      }
+      const int row_base = item * s;
+      uint8_t* stg = smw + L::kOffStg + quad * L::kStgRows * L::kStgPitch;
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        const uint32_t tcol = tmem + 2 * kAT + wg * 2 * HD + (which == 0 ? HD : 0) + lane_base;
+        const float mul = which == 0 ? scale : 1.f;
+        uint4 pk[8];
+        if (n > 0) {
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            uint32_t ov[32];
+            tmem_ld_32x32b_x32(tcol + c2 * 32, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float f[8];
+#pragma unroll
+              for (int k2 = 0; k2 < 8; ++k2) f[k2] = __uint_as_float(ov[8 * q + k2]) * mul;
+              pk[4 * c2 + q] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                          pack_bf16x2(f[6], f[7]));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) pk[q] = make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int rd = 0; rd < 32 / L::kStgRows; ++rd) {
+          if ((int)lane / L::kStgRows == rd) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              *reinterpret_cast<uint4*>(stg + (lane % L::kStgRows) * L::kStgPitch + 16 * q) = pk[q];
+          }
+          __syncwarp();
+#pragma unroll
+          for (int pass = 0; pass < L::kStgRows / 4; ++pass) {
+            const int rr = pass * 4 + (lane >> 3), piece = lane & 7;
+            const int key = kt * kAT + quad * 32 + rd * L::kStgRows + rr;
+            if (key < s) {
+              const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * L::kStgPitch + piece * 16);
+              *reinterpret_cast<uint4*>(dkv + ((size_t)row_base + key) * ld_dkv + (which + 1) * d_model + h * HD +
+                                        piece * 8) = v;
+            }
+          }
+          __syncwarp();
+        }
+      }
+      if (n > 0) {
+        tc_fence_before();
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");  // the group has drained its accumulators
+        if ((threadIdx.x & 127) == 0) mbar_arrive(acc_empty);
+        ++accn;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // ============================================================================ backward dQ, ping-pong
 // Same structure as the dK/dV kernel over query-tile units (CSR walk over key tiles): WG w takes the
 // unit's entries e = w, w + 2, ... with its own S/dP TMEM buffer; per entry the MMA issuer computes
@@ -1644,6 +2006,347 @@ bsattn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
   }
 }
 
+// ============================================================================ backward dQ, two unit streams
+// The dQ counterpart of bsattn_dkdv_ds_kernel: two independent pipelines per CTA over query-tile units (producer,
+// MMA issuer and 4-warp epilogue group each; TMEM S/dP at 128 w, dQ at 256 + 64 w), units dealt by entry count.
+// Per entry: S = Q K^T | [p_done] dP = dO V^T over S | [ds_ready] dQ += dS K (dS as bf16 over dP). A stream's
+// group owns whole units, so the bf16 row-sum residual eps of dS (see bsattn_dq_tc_kernel) is a per-thread sum.
+template <int HD>
+struct AttnDqDs {
+  static constexpr int kT = kAT * 128;
+  static constexpr int kSt = 2;                                // K/V ring stages per stream
+  static constexpr int kStgPitch = 80;                         // staging row: 64 B of bf16 + 16 B pad
+  static constexpr int kOffRing = 2 * kT;                      // per stream: [Q|dO] [ring] [kbar] [staging]
+  static constexpr int kOffKbar = kOffRing + kSt * 2 * kT;
+  static constexpr int kOffStg = kOffKbar + 64 * 4;
+  static constexpr int kStream = (kOffStg + 4 * 32 * kStgPitch + 1023) / 1024 * 1024;
+  static constexpr int kOffBar = 2 * kStream;
+  static constexpr int kTotal = kOffBar + 512 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kDsThreads, 1)
+bsattn_dq_ds_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                    const __grid_constant__ CUtensorMap tm_g, int gu, int s, int H,
+                    int n_units, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
+                    float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
+                    __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ kbar_g, const int4* __restrict__ desc) {
+  static_assert(HD == 64, "two streams' S/dP buffers and dQ accumulators fit TMEM at HD 64");
+  using L = AttnDqDs<HD>;
+  const int d_model = H * HD;
+  const int nqt = (s + kAT - 1) / kAT;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ int s_list[2][kDsSortMax];
+  __shared__ int s_cnt[2];
+  uint8_t* sm = align_smem_1024(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
+  // per stream w, at bars + 16 w: q_full, q_empty, kv_full[2], kv_empty[2], s_full, p_done (4 warps), dp_full,
+  // ds_ready (4 warps), acc_full, acc_empty
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+  uint64_t* sMaskAll = bars + 40;  // [2][kSt]
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_g);
+    for (int w = 0; w < 2; ++w) {
+      uint64_t* b = bars + 16 * w;
+      for (int i = 0; i < 6; ++i) mbar_init(b + i, 1);
+      mbar_init(b + 6, 1);
+      mbar_init(b + 7, 4);
+      mbar_init(b + 8, 1);
+      mbar_init(b + 9, 4);
+      mbar_init(b + 10, 1);
+      mbar_init(b + 11, 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  pdl_wait_trigger();
+  const int G = gridDim.x;
+  const int n_mine = n_units > (int)blockIdx.x ? (n_units - (int)blockIdx.x + G - 1) / G : 0;
+  const bool dealt = n_mine <= kDsSortMax;
+  if (threadIdx.x == 0 && dealt) {
+    int cnt[kDsSortMax], ord[kDsSortMax];
+    for (int k = 0; k < n_mine; ++k) {
+      const int nk = __ldg(desc + blockIdx.x + k * G).y;
+      int i = k;
+      while (i > 0 && cnt[i - 1] < nk) {
+        cnt[i] = cnt[i - 1];
+        ord[i] = ord[i - 1];
+        --i;
+      }
+      cnt[i] = nk;
+      ord[i] = k;
+    }
+    int load0 = 0, load1 = 0, c0 = 0, c1 = 0;
+    for (int i = 0; i < n_mine; ++i) {
+      const int u = blockIdx.x + ord[i] * G;
+      if (load0 <= load1) {
+        s_list[0][c0++] = u;
+        load0 += cnt[i] + 1;
+      } else {
+        s_list[1][c1++] = u;
+        load1 += cnt[i] + 1;
+      }
+    }
+    s_cnt[0] = c0;
+    s_cnt[1] = c1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int tab_nt = __ldg(tables), tab_per = __ldg(tables + 6);
+  auto n_stream = [&](int w) { return dealt ? s_cnt[w] : (n_mine + 1 - w) / 2; };
+  auto unit_id = [&](int w, int i) { return dealt ? s_list[w][i] : (int)blockIdx.x + (2 * i + w) * G; };
+  auto unit = [&](int w, int i, int& item, int& h, int& qt, const int32_t*& ents, int& e0, int& n) {
+    const int u = unit_id(w, i);
+    const int4 dd = __ldg(desc + u);
+    qt = u % nqt;
+    h = (u / nqt) % H;
+    item = u / (nqt * H);
+    e0 = dd.x;
+    n = dd.y;
+    ents = desc_entries(tables, tab_nt, tab_per, dd.z, false);
+  };
+
+  if (warp < 2 || warp >= 10) {
+    const int w = warp >= 10 ? 1 : 0;
+    uint64_t* b = bars + 16 * w;
+    uint64_t *q_full = b, *q_empty = b + 1, *kv_full = b + 2, *kv_empty = b + 4, *s_full = b + 6, *p_done = b + 7,
+             *dp_full = b + 8, *ds_ready = b + 9, *acc_full = b + 10, *acc_empty = b + 11;
+    uint8_t* smw = sm + w * L::kStream;
+    uint64_t* sMask = sMaskAll + w * L::kSt;
+    const int nu = n_stream(w);
+    if ((warp & 1) == 0) {
+      // ================= producer of stream w: Q/dO per non-empty unit, then its K/V tiles
+      if (lane == 0) {
+        int g = 0, qn = 0;
+        for (int i = 0; i < nu; ++i) {
+          int item, h, qt, e0, n;
+          const int32_t* ents;
+          unit(w, i, item, h, qt, ents, e0, n);
+          if (n == 0) continue;
+          const int row_base = item * s;
+          mbar_wait(q_empty, (qn & 1) ^ 1);
+          ++qn;
+          mbar_arrive_expect_tx(q_full, 2 * L::kT);
+          tma_load_2d(smw, &tm_qkv, q_full, h * HD, row_base + qt * kAT);
+          tma_load_2d(smw + L::kT, &tm_do, q_full, h * HD, row_base + qt * kAT);
+          for (int e = 0; e < n; ++e, ++g) {
+            const int st = g % L::kSt;
+            mbar_wait(kv_empty + st, ((g / L::kSt) & 1) ^ 1);
+            const int32_t* ent = ents + (size_t)(e0 + e) * kEntryInts;
+            uint8_t* skv = smw + L::kOffRing + st * 2 * L::kT;
+            sMask[st] = ent_mask(ent);
+            mbar_arrive_expect_tx(kv_full + st, 2 * L::kT);
+            tma_load_gather(skv, &tm_g, kv_full + st, d_model + h * HD, row_base, ent, gu, kAT / gu);
+            tma_load_gather(skv + L::kT, &tm_g, kv_full + st, 2 * d_model + h * HD, row_base, ent, gu, kAT / gu);
+          }
+        }
+      }
+    } else if (lane == 0) {
+      // ================= MMA issuer of stream w
+      const uint32_t id_s = make_idesc_bf16(kAT, kAT, false, false);
+      const uint32_t id_g = make_idesc_bf16(kAT, HD, false, true);
+      const uint32_t tb = tmem + w * kAT, t_dq = tmem + 2 * kAT + w * HD;
+      const uint32_t sq = smem_u32(smw), sdo = sq + L::kT;
+      int g = 0, qn = 0, accn = 0;
+      for (int i = 0; i < nu; ++i) {
+        int item, h, qt, e0, n;
+        const int32_t* ents;
+        unit(w, i, item, h, qt, ents, e0, n);
+        if (n == 0) continue;
+        mbar_wait(q_full, qn & 1);
+        ++qn;
+        for (int j = 0; j < n; ++j) {
+          const int gg = g + j, st = gg % L::kSt;
+          const uint32_t sk = smem_u32(smw + L::kOffRing + st * 2 * L::kT), sv = sk + L::kT;
+          mbar_wait(kv_full + st, (gg / L::kSt) & 1);
+          tc_fence_after();
+          for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(tb, desc_kmajor(sq, kk), desc_kmajor(sk, kk), id_s, kk != 0);
+          mma_commit(s_full);
+          if (j == 0) {
+            mbar_wait(acc_empty, (accn & 1) ^ 1);  // this stream's previous dQ has been drained
+            tc_fence_after();
+          }
+          mbar_wait(p_done, gg & 1);
+          tc_fence_after();
+          for (int kk = 0; kk < HD / 16; ++kk) mma_bf16_ss(tb, desc_kmajor(sdo, kk), desc_kmajor(sv, kk), id_s, kk != 0);
+          mma_commit(dp_full);
+          if (j + 1 == n) mma_commit(q_empty);  // Q and dO are read by S and dP only
+          mbar_wait(ds_ready, gg & 1);
+          tc_fence_after();
+          for (int kk = 0; kk < kAT / 16; ++kk) mma_bf16_ts(t_dq, tb + kk * 8, desc_mnmajor(sk, kk), id_g, (j | kk) != 0);
+          mma_commit(kv_empty + st);
+        }
+        mma_commit(acc_full);
+        ++accn;
+        g += n;
+      }
+    }
+  } else {
+    // ================= epilogue group wg = stream wg; thread = query row
+    const int wg = (warp - 2) >> 2, quad = warp & 3;
+    uint64_t* b = bars + 16 * wg;
+    uint64_t *kv_full = b + 2, *s_full = b + 6, *p_done = b + 7, *dp_full = b + 8, *ds_ready = b + 9, *acc_full = b + 10,
+             *acc_empty = b + 11;
+    uint8_t* smw = sm + wg * L::kStream;
+    const uint64_t* sMask = sMaskAll + wg * L::kSt;
+    float* kbar = reinterpret_cast<float*>(smw + L::kOffKbar);
+    uint8_t* stg = smw + L::kOffStg + quad * 32 * L::kStgPitch;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const uint32_t tb = tmem + wg * kAT + lane_base;
+    const uint32_t t_dq = tmem + 2 * kAT + wg * HD + lane_base;
+    const int ci = r >> 4;
+    const int nu = n_stream(wg);
+    // this thread's row terms (lse, delta) and kbar component of the stream's next unit, loaded one unit ahead
+    float l2n = 0.f, dln = 0.f, kbn = 0.f;
+    auto row_terms = [&](int i) {
+      if (i >= nu) return;
+      const int u = unit_id(wg, i);
+      const int qt_ = u % nqt, h_ = (u / nqt) % H, it_ = u / (nqt * H), row_ = qt_ * kAT + r;
+      const size_t lr = ((size_t)it_ * H + h_) * s + (row_ < s ? row_ : 0);
+      l2n = __ldg(lse + lr);
+      dln = __ldg(delta + lr);
+      if (r < HD) kbn = __ldg(kbar_g + ((size_t)it_ * H + h_) * HD + r);
+    };
+    row_terms(0);
+    int g = 0, accn = 0;
+    for (int i = 0; i < nu; ++i) {
+      int item, h, qt, e0, n;
+      const int32_t* ents;
+      unit(wg, i, item, h, qt, ents, e0, n);
+      const float l2 = l2n * 1.4426950408889634f, dl = dln, kb = kbn;
+      row_terms(i + 1);
+      float2 eps2 = make_float2(0.f, 0.f);  // bf16 dS row sum, even / odd columns
+      for (int j = 0; j < n; ++j) {
+        const int gg = g + j, st = gg % L::kSt;
+        mbar_wait(kv_full + st, (gg / L::kSt) & 1);
+        const uint32_t mrow = (uint32_t)(sMask[st] >> (ci * 8)) & 0xffu;
+        mbar_wait(s_full, gg & 1);
+        tc_fence_after();
+        uint32_t pp[4][16];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t sv_[2][32];
+          tmem_ld_32x32b_x32(tb + h2 * 64, sv_[0]);
+          tmem_ld_32x32b_x32(tb + h2 * 64 + 32, sv_[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const int c = h2 * 2 + c2;
+#pragma unroll
+            for (int u2 = 0; u2 < 16; ++u2) {
+              const float2 x = fma2(make_float2(__uint_as_float(sv_[c2][2 * u2]), __uint_as_float(sv_[c2][2 * u2 + 1])),
+                                    make_float2(scale_log2, scale_log2), make_float2(-l2, -l2));
+              const uint32_t pk = pack_bf16x2(ex2(x.x), ex2(x.y));
+              pp[c][u2] = (mrow >> (c * 2 + (u2 >> 3))) & 1u ? pk : 0u;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_done);
+        mbar_wait(dp_full, gg & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t dv_[2][32];
+          tmem_ld_32x32b_x32(tb + h2 * 64, dv_[0]);
+          tmem_ld_32x32b_x32(tb + h2 * 64 + 32, dv_[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const int c = h2 * 2 + c2;
+            uint32_t dd[16];
+#pragma unroll
+            for (int u2 = 0; u2 < 16; ++u2) {
+              const float2 pf = bf16x2_unpack(pp[c][u2]);
+              const float2 t = sub2(make_float2(__uint_as_float(dv_[c2][2 * u2]), __uint_as_float(dv_[c2][2 * u2 + 1])),
+                                    make_float2(dl, dl));
+              const float2 r2 = mul2(pf, t);
+              dd[u2] = pack_bf16x2(r2.x, r2.y);
+              eps2 = add2(eps2, bf16x2_unpack(dd[u2]));
+            }
+            tmem_st_32x32b_x16(tb + c * 16, dd);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ds_ready);
+      }
+      g += n;
+      // ---- unit drain: dQ rows with the common-mode correction, through the staging tile (64-byte row segments)
+      const int row_base = item * s;
+      const float eps = eps2.x + eps2.y;
+      if (n > 0) {
+        if (r < HD) kbar[r] = kb;  // mean key of (item, h), bsattn_prep_kernel
+        mbar_wait(acc_full, accn & 1);
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+        tc_fence_after();
+      }
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        const int col0 = c * 32;
+        uint32_t ov[32];
+        if (n > 0) {
+          tmem_ld_32x32b_x32(t_dq + col0, ov);
+          tmem_ld_wait();
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float f[8];
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2)
+            f[k2] = n > 0 ? (__uint_as_float(ov[8 * q + k2]) - eps * kbar[col0 + 8 * q + k2]) * scale : 0.f;
+          *reinterpret_cast<uint4*>(stg + lane * L::kStgPitch + 16 * q) =
+              make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int pass = 0; pass < 4; ++pass) {
+          const int rr = pass * 8 + (lane >> 2), piece = lane & 3;
+          const int qrow = qt * kAT + quad * 32 + rr;
+          if (qrow < s)
+            *reinterpret_cast<uint4*>(dq + ((size_t)row_base + qrow) * ld_dq + h * HD + col0 + piece * 8) =
+                *reinterpret_cast<const uint4*>(stg + rr * L::kStgPitch + piece * 16);
+        }
+        __syncwarp();
+      }
+      if (n > 0) {
+        tc_fence_before();
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");  // TMEM drained, kbar reusable
+        if ((threadIdx.x & 127) == 0) mbar_arrive(acc_empty);
+        ++accn;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// LX_ATTN_DKDV_DS=0: the entry-alternating dK/dV ping-pong kernel at HD 64 instead of the two-stream one
+static bool dkdv_ds() {
+  static const bool on = [] { const char* e = getenv("LX_ATTN_DKDV_DS"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
+// LX_ATTN_DQ_DS=0: the entry-alternating dQ ping-pong kernel at HD 64 instead of the two-stream one
+static bool dq_ds() {
+  static const bool on = [] { const char* e = getenv("LX_ATTN_DQ_DS"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
 template <int HD>
 static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* o, const uint16_t* d_o, int ld_o, int n_items, int s,
                          int H, const int32_t* pidx, int item_stride, const int32_t* tables128, int gu, float scale,
@@ -1679,6 +2382,13 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
   if (old_bwd) {
     launch_k(bsattn_dkdv_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, tm_g, tm_do_g, gu, s, H, H * HD, pidx, item_stride,
              tables128, scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d);
+  } else if (HD == 64 && dkdv_ds()) {
+    constexpr int smem_ds = AttnDkdvDs<64>::kTotal;
+    static cudaError_t a5 = cudaFuncSetAttribute(bsattn_dkdv_ds_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ds);
+    LX_CHECK_CUDA(a5);
+    launch_k(bsattn_dkdv_ds_kernel<64>, std::min(n_units, num_sms()), kDsThreads, smem_ds, st, tm_qkv, tm_do, tm_g, tm_do_g,
+             gu, s, H, n_units, pidx, item_stride, tables128, scale, sl2, lse, delta,
+             reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, (const int4*)desc_kv);
   } else {
     constexpr int smem_pp = AttnDkdvPP<HD>::kTotal;
     static cudaError_t a3 = cudaFuncSetAttribute(bsattn_dkdv_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pp);
@@ -1690,7 +2400,14 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
   if ((rc = launch_check("bsattn_dkdv_tc"))) return rc;
   // the dQ ping-pong kernel fits at HD 128 too (1 Q/dO buffer, 2-stage K/V ring: 215 KB), whichever dK/dV ran
   static const bool old_dq = getenv("LX_ATTN_BWD_OLD") != nullptr || AttnDqPP<HD>::kTotal > 227 * 1024;
-  if (old_dq) {
+  if (HD == 64 && !old_dq && dq_ds()) {
+    constexpr int smem_dq = AttnDqDs<64>::kTotal;
+    static cudaError_t a6 = cudaFuncSetAttribute(bsattn_dq_ds_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_dq);
+    LX_CHECK_CUDA(a6);
+    launch_k(bsattn_dq_ds_kernel<64>, std::min(n_units, num_sms()), kDsThreads, smem_dq, st, tm_qkv, tm_do, tm_g, gu, s, H,
+             n_units, pidx, item_stride, tables128, scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d,
+             (const float*)kbar, (const int4*)desc_q);
+  } else if (old_dq) {
     launch_k(bsattn_dq_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, tm_g, gu, s, H, H * HD, pidx, item_stride, tables128,
              scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, (const float*)kbar);
   } else {

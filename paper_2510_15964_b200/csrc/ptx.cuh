@@ -107,6 +107,32 @@ LX_DEV void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1) 
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
 
+// two-lane fp32 ops (FADD2 / FMUL2 / FFMA2): per lane identical to the scalar op, half the issue
+#define LX_F32X2_OP(name, op)                                                                                     \
+  LX_DEV float2 name(float2 a, float2 b) {                                                                       \
+    float2 r;                                                                                                    \
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t" op                  \
+        " rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"                                                            \
+        : "=f"(r.x), "=f"(r.y)                                                                                   \
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));                                                               \
+    return r;                                                                                                    \
+  }
+LX_F32X2_OP(add2, "add.rn.f32x2")
+LX_F32X2_OP(sub2, "sub.rn.f32x2")
+LX_F32X2_OP(mul2, "mul.rn.f32x2")
+#undef LX_F32X2_OP
+// bf16x2 -> (low, high) as fp32: one shift and one mask
+LX_DEV float2 bf16x2_unpack(uint32_t v) { return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u)); }
+// (a0 * b0 + c0, a1 * b1 + c1)
+LX_DEV float2 fma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+
 LX_DEV void tma_prefetch_desc(const void* desc) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");
 }
