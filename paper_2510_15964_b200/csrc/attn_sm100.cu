@@ -37,6 +37,11 @@ LX_DEV void trace_stamp(int slot) {
   }
 }
 
+LX_DEV void trace_put(int slot, unsigned long long v) {
+  unsigned long long* t = g_attn_trace;
+  if (t != nullptr) t[(blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z)) * 32 + slot] = v;
+}
+
 // Gathered 128-tile tables (patterns.tables128_from_grids): header [nt, P, s, attn_blk, gu, nsub, per, 0];
 // per pattern row_ptr[nt+1] col_ptr[nt+1] csr[nt*nt][10] csc[nt*nt][10]. A CSR entry of query tile i is one
 // gathered key tile: nsub = 128 / gu units of gu consecutive keys (entry[2 + k] = unit id of slot k, padding
@@ -1352,7 +1357,7 @@ bsattn_dkdv_ds_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
                       const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_do_g, int gu, int s, int H,
                       int n_units, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                       float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
-                      __nv_bfloat16* __restrict__ dkv, int ld_dkv, const int4* __restrict__ desc) {
+                      __nv_bfloat16* __restrict__ dkv, int ld_dkv, const int4* __restrict__ desc, int deal) {
   static_assert(HD == 64, "two streams' S/dP buffers and dK/dV accumulators fill TMEM at HD 64");
   using L = AttnDkdvDs<HD>;
   const int d_model = H * HD;
@@ -1360,6 +1365,7 @@ bsattn_dkdv_ds_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
   extern __shared__ uint8_t smem_raw[];
   __shared__ int s_list[2][kDsSortMax];
   __shared__ int s_cnt[2];
+  __shared__ int s_n[kDsSortMax], s_ord[kDsSortMax];  // entry counts of this CTA's units, their sorted order
   uint8_t* sm = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
   // per stream w, at bars + 16 w: kv_full, kv_empty, qd_full[2], qd_empty[2], s_full, p_ready (4 warps), dp_full,
@@ -1387,40 +1393,47 @@ bsattn_dkdv_ds_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
   pdl_wait_trigger();
+  if (threadIdx.x == 0) trace_stamp(6);
   const int G = gridDim.x;
   const int n_mine = n_units > (int)blockIdx.x ? (n_units - (int)blockIdx.x + G - 1) / G : 0;
-  const bool dealt = n_mine <= kDsSortMax;
-  if (threadIdx.x == 0 && dealt) {
-    int cnt[kDsSortMax], ord[kDsSortMax];
-    for (int k = 0; k < n_mine; ++k) {  // insertion sort by entry count, descending (ties keep index order)
-      const int nk = __ldg(desc + blockIdx.x + k * G).y;
-      int i = k;
-      while (i > 0 && cnt[i - 1] < nk) {
-        cnt[i] = cnt[i - 1];
-        ord[i] = ord[i - 1];
-        --i;
+  const bool dealt = deal && n_mine <= kDsSortMax;
+  if (dealt) {
+    // the CTA's units by entry count, descending (ties by index): each thread ranks one unit, then thread 0 deals
+    // them in that order to the stream with the smaller load (entries + 1 per unit; stream 0 on ties)
+    const int k = threadIdx.x;
+    const int nk = k < n_mine ? __ldg(desc + blockIdx.x + k * G).y : 0;
+    if (k < n_mine) s_n[k] = nk;
+    __syncthreads();
+    if (k < n_mine) {
+      int rank = 0;
+      for (int j = 0; j < n_mine; ++j) {
+        const int nj = s_n[j];
+        rank += (nj > nk) | (nj == nk && j < k);
       }
-      cnt[i] = nk;
-      ord[i] = k;
+      s_ord[rank] = k;
     }
-    int load0 = 0, load1 = 0, c0 = 0, c1 = 0;
-    for (int i = 0; i < n_mine; ++i) {  // greedy: to the stream with the smaller load (stream 0 on ties)
-      const int u = blockIdx.x + ord[i] * G;
-      if (load0 <= load1) {
-        s_list[0][c0++] = u;
-        load0 += cnt[i] + 1;
-      } else {
-        s_list[1][c1++] = u;
-        load1 += cnt[i] + 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int load0 = 0, load1 = 0, c0 = 0, c1 = 0;
+      for (int i = 0; i < n_mine; ++i) {
+        const int kk = s_ord[i];
+        if (load0 <= load1) {
+          s_list[0][c0++] = blockIdx.x + kk * G;
+          load0 += s_n[kk] + 1;
+        } else {
+          s_list[1][c1++] = blockIdx.x + kk * G;
+          load1 += s_n[kk] + 1;
+        }
       }
+      s_cnt[0] = c0;
+      s_cnt[1] = c1;
     }
-    s_cnt[0] = c0;
-    s_cnt[1] = c1;
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) trace_stamp(0);
 
   const int tab_nt = __ldg(tables), tab_per = __ldg(tables + 6);
   // stream w's i-th unit and its count
@@ -1671,6 +1684,10 @@ bsattn_dkdv_ds_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_c
         if ((threadIdx.x & 127) == 0) mbar_arrive(acc_empty);
         ++accn;
       }
+    }
+    if ((threadIdx.x & 127) == 0) {
+      trace_stamp(0 + 1 + wg);
+      trace_put(0 + 3 + wg, ((unsigned long long)nu << 32) | (unsigned)g);
     }
   }
   tc_fence_before();
@@ -2030,7 +2047,7 @@ bsattn_dq_ds_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
                     const __grid_constant__ CUtensorMap tm_g, int gu, int s, int H,
                     int n_units, const int32_t* __restrict__ pidx, int item_stride, const int32_t* __restrict__ tables,
                     float scale, float scale_log2, const float* __restrict__ lse, const float* __restrict__ delta,
-                    __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ kbar_g, const int4* __restrict__ desc) {
+                    __nv_bfloat16* __restrict__ dq, int ld_dq, const float* __restrict__ kbar_g, const int4* __restrict__ desc, int deal) {
   static_assert(HD == 64, "two streams' S/dP buffers and dQ accumulators fit TMEM at HD 64");
   using L = AttnDqDs<HD>;
   const int d_model = H * HD;
@@ -2038,6 +2055,7 @@ bsattn_dq_ds_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
   extern __shared__ uint8_t smem_raw[];
   __shared__ int s_list[2][kDsSortMax];
   __shared__ int s_cnt[2];
+  __shared__ int s_n[kDsSortMax], s_ord[kDsSortMax];  // entry counts of this CTA's units, their sorted order
   uint8_t* sm = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
   // per stream w, at bars + 16 w: q_full, q_empty, kv_full[2], kv_empty[2], s_full, p_done (4 warps), dp_full,
@@ -2064,40 +2082,47 @@ bsattn_dq_ds_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
   pdl_wait_trigger();
+  if (threadIdx.x == 0) trace_stamp(7);
   const int G = gridDim.x;
   const int n_mine = n_units > (int)blockIdx.x ? (n_units - (int)blockIdx.x + G - 1) / G : 0;
-  const bool dealt = n_mine <= kDsSortMax;
-  if (threadIdx.x == 0 && dealt) {
-    int cnt[kDsSortMax], ord[kDsSortMax];
-    for (int k = 0; k < n_mine; ++k) {
-      const int nk = __ldg(desc + blockIdx.x + k * G).y;
-      int i = k;
-      while (i > 0 && cnt[i - 1] < nk) {
-        cnt[i] = cnt[i - 1];
-        ord[i] = ord[i - 1];
-        --i;
+  const bool dealt = deal && n_mine <= kDsSortMax;
+  if (dealt) {
+    // the CTA's units by entry count, descending (ties by index): each thread ranks one unit, then thread 0 deals
+    // them in that order to the stream with the smaller load (entries + 1 per unit; stream 0 on ties)
+    const int k = threadIdx.x;
+    const int nk = k < n_mine ? __ldg(desc + blockIdx.x + k * G).y : 0;
+    if (k < n_mine) s_n[k] = nk;
+    __syncthreads();
+    if (k < n_mine) {
+      int rank = 0;
+      for (int j = 0; j < n_mine; ++j) {
+        const int nj = s_n[j];
+        rank += (nj > nk) | (nj == nk && j < k);
       }
-      cnt[i] = nk;
-      ord[i] = k;
+      s_ord[rank] = k;
     }
-    int load0 = 0, load1 = 0, c0 = 0, c1 = 0;
-    for (int i = 0; i < n_mine; ++i) {
-      const int u = blockIdx.x + ord[i] * G;
-      if (load0 <= load1) {
-        s_list[0][c0++] = u;
-        load0 += cnt[i] + 1;
-      } else {
-        s_list[1][c1++] = u;
-        load1 += cnt[i] + 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int load0 = 0, load1 = 0, c0 = 0, c1 = 0;
+      for (int i = 0; i < n_mine; ++i) {
+        const int kk = s_ord[i];
+        if (load0 <= load1) {
+          s_list[0][c0++] = blockIdx.x + kk * G;
+          load0 += s_n[kk] + 1;
+        } else {
+          s_list[1][c1++] = blockIdx.x + kk * G;
+          load1 += s_n[kk] + 1;
+        }
       }
+      s_cnt[0] = c0;
+      s_cnt[1] = c1;
     }
-    s_cnt[0] = c0;
-    s_cnt[1] = c1;
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) trace_stamp(8);
 
   const int tab_nt = __ldg(tables), tab_per = __ldg(tables + 6);
   auto n_stream = [&](int w) { return dealt ? s_cnt[w] : (n_mine + 1 - w) / 2; };
@@ -2326,6 +2351,10 @@ bsattn_dq_ds_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
         ++accn;
       }
     }
+    if ((threadIdx.x & 127) == 0) {
+      trace_stamp(8 + 1 + wg);
+      trace_put(8 + 3 + wg, ((unsigned long long)nu << 32) | (unsigned)g);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -2338,6 +2367,12 @@ bsattn_dq_ds_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_con
 // LX_ATTN_DKDV_DS=0: the entry-alternating dK/dV ping-pong kernel at HD 64 instead of the two-stream one
 static bool dkdv_ds() {
   static const bool on = [] { const char* e = getenv("LX_ATTN_DKDV_DS"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
+// LX_ATTN_DS_DEAL=0: the two-stream kernels alternate a CTA's units between the streams instead of dealing them
+static int ds_deal() {
+  static const int on = [] { const char* e = getenv("LX_ATTN_DS_DEAL"); return !(e && e[0] == '0'); }();
   return on;
 }
 
@@ -2388,7 +2423,7 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
     LX_CHECK_CUDA(a5);
     launch_k(bsattn_dkdv_ds_kernel<64>, std::min(n_units, num_sms()), kDsThreads, smem_ds, st, tm_qkv, tm_do, tm_g, tm_do_g,
              gu, s, H, n_units, pidx, item_stride, tables128, scale, sl2, lse, delta,
-             reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, (const int4*)desc_kv);
+             reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, (const int4*)desc_kv, ds_deal());
   } else {
     constexpr int smem_pp = AttnDkdvPP<HD>::kTotal;
     static cudaError_t a3 = cudaFuncSetAttribute(bsattn_dkdv_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pp);
@@ -2406,7 +2441,7 @@ static int launch_bwd_tc(const uint16_t* qkv, int ld, int ld_d, const uint16_t* 
     LX_CHECK_CUDA(a6);
     launch_k(bsattn_dq_ds_kernel<64>, std::min(n_units, num_sms()), kDsThreads, smem_dq, st, tm_qkv, tm_do, tm_g, gu, s, H,
              n_units, pidx, item_stride, tables128, scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d,
-             (const float*)kbar, (const int4*)desc_q);
+             (const float*)kbar, (const int4*)desc_q, ds_deal());
   } else if (old_dq) {
     launch_k(bsattn_dq_tc_kernel<HD>, grid, 192, smem, st, tm_qkv, tm_do, tm_g, gu, s, H, H * HD, pidx, item_stride, tables128,
              scale, sl2, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), ld_d, (const float*)kbar);
