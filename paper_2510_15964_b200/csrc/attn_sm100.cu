@@ -870,10 +870,14 @@ __global__ void __launch_bounds__(256) bsattn_prep_kernel(const __nv_bfloat16* _
                                                           int nb_delta, int nb_kbar) {
   pdl_wait_trigger();
   const int d = H * HD;
-  if ((int)blockIdx.x < nb_delta) {
+  // block roles: [descriptors | kbar | delta]; the short latency-bound roles are scheduled first, under the
+  // bandwidth-bound delta blocks
+  const int nb_desc = (int)gridDim.x - nb_delta - nb_kbar;
+  if ((int)blockIdx.x >= nb_desc + nb_kbar) {
+    const int bdx = blockIdx.x - nb_desc - nb_kbar;
     constexpr int G = HD / 8;  // lanes per head
     constexpr int kIt = 8;     // 16 B chunks per lane per pass (2048 columns)
-    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int row = (bdx * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= n_rows_total) return;
     const int n_it = (d + 255) / 256;
@@ -910,20 +914,27 @@ __global__ void __launch_bounds__(256) bsattn_prep_kernel(const __nv_bfloat16* _
     }
     return;
   }
-  if ((int)blockIdx.x < nb_delta + nb_kbar) {
+  if ((int)blockIdx.x >= nb_desc) {
     // kbar of (item, h) over the item's first min(s, 128) keys: any fixed vector is exact for the dQ
     // identity sum_j dS_ij (k_j - kbar) = sum_j dS_ij k_j; the first tile's mean estimates the common mode.
     // 16-byte loads: thread t reads chunk t % (HD / 8) of rows t / (HD / 8), + 256 / (HD / 8), ...
     __shared__ float part[256 / (HD / 8)][HD];
     constexpr int CH = HD / 8, RS = 256 / CH;
-    const int ih = blockIdx.x - nb_delta, item = ih / H, h = ih % H;
+    const int ih = blockIdx.x - nb_desc, item = ih / H, h = ih % H;
     const int ch = threadIdx.x % CH, r0 = threadIdx.x / CH;
     const int nr = s < kAT ? s : kAT;
     const __nv_bfloat16* kp = qkv + (size_t)item * s * ldq + d + h * HD + ch * 8;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int r = r0; r < nr; r += RS) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(kp + (size_t)r * ldq));
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    constexpr int kLd = (kAT + RS - 1) / RS;  // rows per thread: all loads issued before the sums
+    uint4 v[kLd];
+#pragma unroll
+    for (int i = 0; i < kLd; ++i) {
+      const int r = r0 + i * RS;
+      v[i] = r < nr ? __ldg(reinterpret_cast<const uint4*>(kp + (size_t)r * ldq)) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int i = 0; i < kLd; ++i) {
+      const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const __nv_bfloat162 p2 = *reinterpret_cast<const __nv_bfloat162*>(&w[q]);
@@ -941,7 +952,7 @@ __global__ void __launch_bounds__(256) bsattn_prep_kernel(const __nv_bfloat16* _
     }
     return;
   }
-  const int u = (blockIdx.x - nb_delta - nb_kbar) * blockDim.x + threadIdx.x;
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n_units) return;
   const int nt = __ldg(tables), per = __ldg(tables + 6);
   const int t = u % nt, h = (u / nt) % H, item = u / (nt * H);
