@@ -13,7 +13,7 @@ CALLS = {
     "lx_neuron_fc2_dgrad": ["gemm_sm100_kernel<3, 4, 512, 2, 1>"],
     "lx_neuron_fc1_dgrad": ["gemm_sm100_kernel<4, 5, 256, 1, 1>"],
     "lx_bsattn_fwd_tc": ["bsattn_fwd_tc_kernel<64>"],
-    "lx_bsattn_bwd_tc": ["bsattn_prep_kernel<64>", "bsattn_dkdv_pp_kernel<64>", "bsattn_dq_pp_kernel<64>"],
+    "lx_bsattn_bwd_tc": ["bsattn_prep_kernel<64>", "bsattn_dkdv_ds_kernel<64>", "bsattn_dq_ds_kernel<64>"],
     "lx_predict_mlp_mask": ["gemm_sm100_kernel<6, 6, 256, 2, 1>", "mask_compact_kernel"],
     "lx_predict_attention_patterns": ["gemm_sm100_kernel<6, 0, 256, 2, 1>", "attn_pattern_kernel"],
 }
