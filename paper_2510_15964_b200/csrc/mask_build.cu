@@ -100,7 +100,9 @@ __device__ __forceinline__ bool pool_member(int kind, int p, int i, int j) {
 constexpr int kMaxPool = 16;
 constexpr int kMaxM = 64;
 
-__global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items, int m, int H, int r, float frac,
+// two blocks per SM (register cap, full shared-memory carveout): the (item, head) blocks are latency chains, and
+// one resident block per SM ran the 256 blocks at cfg3 in two waves
+__global__ void __launch_bounds__(256, 2) attn_pattern_kernel(const float* __restrict__ proj, int n_items, int m, int H, int r, float frac,
                                     double tau, int n_b, const int32_t* __restrict__ pool_kind,
                                     const int32_t* __restrict__ pool_param, int n_pool, int scope_batch,
                                     int32_t* __restrict__ pattern_idx, float* __restrict__ dump) {
@@ -127,7 +129,26 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
   }
   for (int item = item0; item < item1; ++item) {
     __syncthreads();
-    if (vec) {
+    if (vec && blockDim.x % (r / 4) == 0) {
+      // thread -> (row, float4 column): no index division in the loop; batches of 8 loads before any store
+      const int r4 = r / 4, rp = blockDim.x / r4, t4 = threadIdx.x % r4, nrow = 2 * m;
+      for (int base = threadIdx.x / r4; base < nrow; base += 8 * rp) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int row = base + u * rp;
+          if (row < nrow) {
+            const int which = row >= m, i = which ? row - m : row;
+            v[u] = __ldg(reinterpret_cast<const float4*>(proj + (size_t)(item * m + i) * ldp + (which ? H + h : h) * r) + t4);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int row = base + u * rp;
+          if (row < nrow) reinterpret_cast<float4*>(s_qk + row * rs)[t4] = v[u];
+        }
+      }
+    } else if (vec) {
       // float4 loads, issued in batches of 8 before any store (one round trip per batch)
       const int r4 = r / 4, nq = 2 * m * r4;
       for (int e0 = threadIdx.x; e0 < nq; e0 += 8 * blockDim.x) {
@@ -159,6 +180,39 @@ __global__ void attn_pattern_kernel(const float* __restrict__ proj, int n_items,
     // S_hat = (X Wq)(X Wk)^T  (sf/predictor.py:74-76): warp w takes rows i = w, w + n_warps, ..., lane j a
     // column; q_i is a warp broadcast, k_j rows are conflict-free (row stride rs = r + 4 / r + 1). Four
     // partial sums over t mod 4 combined in a fixed order: deterministic.
+    if (vec) {
+      // two rows per pass (i, i + n_warps): each k_j float4 feeds both, twice the independent FMA chains; per
+      // (i, j) the same four partial sums in the same order as the one-row loop below
+      for (int i = warp; i < m; i += 2 * n_warps) {
+        const int i2 = i + n_warps < m ? i + n_warps : i;
+        const float* qr = s_qk + i * rs;
+        const float* qr2 = s_qk + i2 * rs;
+        for (int j = lane; j < m; j += 32) {
+          const float* kr = s_qk + (m + j) * rs;
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
+#pragma unroll 8
+          for (int t = 0; t < r; t += 4) {
+            const float4 k4 = *reinterpret_cast<const float4*>(kr + t);
+            const float4 q4 = *reinterpret_cast<const float4*>(qr + t), p4 = *reinterpret_cast<const float4*>(qr2 + t);
+            a0 = fmaf(q4.x, k4.x, a0);
+            a1 = fmaf(q4.y, k4.y, a1);
+            a2 = fmaf(q4.z, k4.z, a2);
+            a3 = fmaf(q4.w, k4.w, a3);
+            b0 = fmaf(p4.x, k4.x, b0);
+            b1 = fmaf(p4.y, k4.y, b1);
+            b2 = fmaf(p4.z, k4.z, b2);
+            b3 = fmaf(p4.w, k4.w, b3);
+          }
+          const float acc = (a0 + a1) + (a2 + a3), acc2 = (b0 + b1) + (b2 + b3);
+          s_hat[i * m + j] = acc;
+          if (dump) dump[((size_t)item * H + h) * mm + i * m + j] = acc;
+          if (i2 != i) {
+            s_hat[i2 * m + j] = acc2;
+            if (dump) dump[((size_t)item * H + h) * mm + i2 * m + j] = acc2;
+          }
+        }
+      }
+    } else
     for (int i = warp; i < m; i += n_warps) {
       const float* qr = s_qk + i * rs;
       for (int j = lane; j < m; j += 32) {
@@ -377,7 +431,13 @@ int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, i
   dim3 grid(H, scope_batch ? 1 : n_items);
   const size_t smem = sizeof(float) * 2 * m * (r + 4);
   LX_REQUIRE(smem <= 200 * 1024, LX_ERR_UNSUPPORTED, "predictor rank %d x m %d exceeds shared memory", r, m);
-  static cudaError_t attr = cudaFuncSetAttribute(attn_pattern_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  static cudaError_t attr = [] {
+    cudaError_t e = cudaFuncSetAttribute(attn_pattern_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_pattern_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    return e;
+  }();
   LX_CHECK_CUDA(attr);
   launch_k(attn_pattern_kernel, grid, 256, smem, stream, proj_ws, n_items, m, H, r, threshold_frac, tau, n_b, pool_kind,
                                                      pool_param, n_pool, scope_batch, pattern_idx, scores_dump);
