@@ -66,7 +66,7 @@ CONFIGS = {
 KERNELS_PER_CALL = {
     "lx_gemm_bf16_tn": 1, "lx_linear": 1, "lx_linear_kn": 1, "lx_cross_entropy": 1, "lx_adam_step": 1, "lx_predict_mlp_mask": 2, "lx_mask_compact": 1,
     "lx_predict_attention_patterns": 2, "lx_neuron_fc1": 1, "lx_neuron_fc2": 1, "lx_neuron_fc2_dgrad": 1, "lx_neuron_fc1_dgrad": 1,
-    "lx_rowproj": 2, "lx_rowproj_packed": 1, "lx_pack_params": 1, "lx_pack_active_rows": 1, "lx_pack_active_rows2": 1, "lx_lm_head_ce": 3, "lx_colgrad_group": 3,
+    "lx_rowproj": 2, "lx_rowproj_packed": 1, "lx_rowproj_packed_seg": 1, "lx_pack_params": 1, "lx_pack_active_rows": 1, "lx_pack_active_rows2": 1, "lx_lm_head_ce": 3, "lx_colgrad_group": 3,
     "lx_bsattn_fwd": 1, "lx_bsattn_bwd": 3, "lx_bsattn_fwd_tc": 1, "lx_bsattn_bwd_tc": 3, "lx_layernorm_fwd": 1,
     "lx_layernorm_bwd": 1, "lx_adapter_fwd": 1, "lx_adapter_bwd": 3,
 }

@@ -168,6 +168,14 @@ int lx_rowproj_packed(const uint16_t* x, int ldx, int n_items, int s, int K, con
                       int r, float scale, const int32_t* counts, const int32_t* ids, int blk, float* y, int ldy,
                       uint16_t* yb, int ldyb, lx_stream_t stream);
 
+/* lx_rowproj_packed over n_seg independent dense-K problems in one launch (segment k: x + k*x_seg, wpack +
+ * k*w_seg, y + k*y_seg, yb + k*yb_seg, element offsets; n_rows rows each). The q/k/v LoRA input-grad projections
+ * dAx_t = dqkv[:, slot_t] B_t^T of one layer (lora_linear_backward, sf/autograd.py:48-58), whose slots, packs and
+ * output columns are equally spaced. K <= 4096. */
+int lx_rowproj_packed_seg(const uint16_t* x, int ldx, long long x_seg, int n_rows, int K, const uint16_t* wpack,
+                          long long w_seg, int K_full, int RP, int r, float scale, float* y, int ldy, int y_seg, uint16_t* yb,
+                          int ldyb, int yb_seg, int n_seg, lx_stream_t stream);
+
 /* Parameter packing after the optimizer step (sf/autograd.py:203-225 updates the fp32 trainables):
  *   dst[i*dst_sr + j*dst_sc] = bf16(scale * src[i*src_sr + j*src_sc]),  i < rows, j < cols (element strides);
  *   lo_off != 0 also writes the bf16 residual at dst + lo_off (hi/lo split of an fp32 factor).

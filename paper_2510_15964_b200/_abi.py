@@ -46,6 +46,7 @@ SIGNATURES: dict[str, list] = {
     "lx_rowproj": [_P, _I, _I, _I, _I, _P, _LL, _LL, _I, _F, _P, _P, _I, _P, _I, _P, _P],
     "lx_rowproj_ws_bytes": [_I, _I, _I, _I],
     "lx_rowproj_packed": [_P, _I, _I, _I, _I, _P, _I, _I, _I, _F, _P, _P, _I, _P, _I, _P, _I, _P],
+    "lx_rowproj_packed_seg": [_P, _I, _LL, _I, _I, _P, _LL, _I, _I, _I, _F, _P, _I, _I, _P, _I, _I, _I, _P],
     "lx_pack_params": [_P, _I, _P],
     "lx_colgrad_group_ws_floats": [_P, _I, _I, _I],
     "lx_colgrad_group": [_P, _I, _I, _I, _P, _P],

@@ -24,7 +24,7 @@ from . import _abi
 from . import model as M
 from .block_sparse import attention_backward
 from .errors import GradientError
-from .neuron_ops import colgrad_group, colgrad_problem, pack_active_rows2, rowproj, rowproj_packed
+from .neuron_ops import colgrad_group, colgrad_problem, pack_active_rows2, rowproj, rowproj_packed, rowproj_packed_seg
 
 
 def check_gradient_set(grads: dict, model: M.Model) -> None:
@@ -264,7 +264,15 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
     dax = None
     if tq:
         dax = torch.empty(B * s, len(tq) * r, dtype=torch.float32, device=dev)
-        for j, t in enumerate(tq):
+        slots = [M.QKV_SLOT[t] for t in tq]
+        bq = lw.lora_pack.get("b_qkv") if ext else None
+        one = (bq is not None and len({lora[t].scaling for t in tq}) == 1
+               and all(b - a == slots[1] - slots[0] for a, b in zip(slots, slots[1:])))
+        if one:
+            # every target's dAx_t = dqkv[:, slot_t] B_t^T * s in one launch (equally spaced slots / packs / columns)
+            rowproj_packed_seg(dqkv[:, slots[0] * d :], (slots[1] - slots[0]) * d if len(tq) > 1 else 0,
+                                          d, bq, r, lora[tq[0]].scaling, dax, r, dqkv_full[:, 3 * d :], r, len(tq))
+        for j, t in ([] if one else enumerate(tq)):
             ad, sl = lora[t], M.QKV_SLOT[t]
             if ext:
                 rowproj_packed(dqkv[:, sl * d : (sl + 1) * d], B, s, d, lw.lora_pack["b"][t], r, scale=ad.scaling,

@@ -261,7 +261,13 @@ template <int NT, int RG>
 __global__ void __launch_bounds__(32 * kRpWarps, 2) rowproj_smem_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int rows,
                                                            int K, int Kp, int r, float scale,
                                                            const __nv_bfloat16* __restrict__ wp, float* __restrict__ y,
-                                                           int ldy, __nv_bfloat16* __restrict__ yb, int ldyb) {
+                                                           int ldy, __nv_bfloat16* __restrict__ yb, int ldyb,
+                                                           long long seg_x, long long seg_w, int seg_y, int seg_yb) {
+  // blockIdx.y = segment: independent problems at fixed element offsets (lx_rowproj_packed_seg)
+  x += blockIdx.y * seg_x;
+  wp += blockIdx.y * seg_w;
+  y += blockIdx.y * seg_y;
+  if (yb) yb += blockIdx.y * seg_yb;
   constexpr int RP = 8 * NT;
   constexpr int TR = 16 * RG;  // rows per CTA
   extern __shared__ __align__(128) uint8_t rps_smem[];
@@ -706,6 +712,21 @@ static long long cg_ws_floats(const lx_colgrad_problem& q, int n_items, int s, i
 
 using namespace lx;
 
+// the dynamic shared-memory opt-in of rowproj_smem_kernel is per instantiation: set once for all four
+static cudaError_t rowproj_smem_attr() {
+  static const cudaError_t attr = [] {
+    cudaError_t e = cudaFuncSetAttribute(rowproj_smem_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(rowproj_smem_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(rowproj_smem_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(rowproj_smem_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    return e;
+  }();
+  return attr;
+}
+
 extern "C" {
 
 long long lx_rowproj_ws_bytes(int n_items, int K, int r, int gathered) {
@@ -783,21 +804,11 @@ int lx_rowproj_packed(const uint16_t* x, int ldx, int n_items, int s, int K, con
     const bool two = (size_t)32 * (K + 32) * 2 <= 160 * 1024;
     const dim3 g2((rows + (two ? 31 : 15)) / (two ? 32 : 16));
     const size_t smem = (size_t)(two ? 32 : 16) * (K + 32) * 2;
-    // the dynamic shared-memory opt-in is per kernel: set it once for each of the four instantiations
-    static const cudaError_t attr = [] {
-      cudaError_t e = cudaFuncSetAttribute(rowproj_smem_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(rowproj_smem_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(rowproj_smem_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(rowproj_smem_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      return e;
-    }();
+    const cudaError_t attr = rowproj_smem_attr();
     LX_CHECK_CUDA(attr);
     auto kern = RP == 8 ? (two ? rowproj_smem_kernel<1, 2> : rowproj_smem_kernel<1, 1>)
                         : (two ? rowproj_smem_kernel<2, 2> : rowproj_smem_kernel<2, 1>);
-    launch_k(kern, g2, 32 * kRpWarps, smem, stream, xb, ldx, rows, K, K_full, r, scale, wp, y, ldy, ybf, ldyb);
+    launch_k(kern, g2, 32 * kRpWarps, smem, stream, xb, ldx, rows, K, K_full, r, scale, wp, y, ldy, ybf, ldyb, 0LL, 0LL, 0, 0);
     return launch_check("rowproj_smem");
   }
 
@@ -808,6 +819,28 @@ int lx_rowproj_packed(const uint16_t* x, int ldx, int n_items, int s, int K, con
     launch_k(rowproj_mma2_kernel<2>, grid, 32 * kRpWarps, 0, stream, xb, ldx, rows, K, K_full, r, scale, counts, counts ? blk : 1, wp,
                                                                0, counts ? ids : nullptr, counts ? K / blk : 0, y, ldy, ybf, ldyb);
   return launch_check("rowproj_packed");
+}
+
+int lx_rowproj_packed_seg(const uint16_t* x, int ldx, long long x_seg, int n_rows, int K, const uint16_t* wpack,
+                          long long w_seg, int K_full, int RP, int r, float scale, float* y, int ldy, int y_seg, uint16_t* yb,
+                          int ldyb, int yb_seg, int n_seg, lx_stream_t stream) {
+  LX_REQUIRE(RP == 8 || RP == 16, LX_ERR_UNSUPPORTED, "rowproj_packed_seg: RP must be 8 or 16");
+  LX_REQUIRE(r >= 1 && r <= RP && n_seg >= 1 && n_seg <= 65535 && n_rows >= 1, LX_ERR_SHAPE,
+             "rowproj_packed_seg: rank %d / segments %d / rows %d", r, n_seg, n_rows);
+  LX_REQUIRE(ldy >= r && (!yb || ldyb >= r), LX_ERR_SHAPE, "rowproj_packed_seg: output stride < r");
+  LX_REQUIRE(K % 16 == 0 && K <= K_full && K <= kRpsMaxK && ldx % 8 == 0 && x_seg % 8 == 0 && w_seg % 8 == 0 &&
+                 (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(wpack) & 15) == 0,
+             LX_ERR_SHAPE, "rowproj_packed_seg: dense K (%% 16, <= %d) with 16-byte aligned rows, segments and pack", kRpsMaxK);
+  LX_CHECK_CUDA(rowproj_smem_attr());
+  const bool two = (size_t)32 * (K + 32) * 2 <= 160 * 1024;
+  const dim3 g2((n_rows + (two ? 31 : 15)) / (two ? 32 : 16), n_seg);
+  const size_t smem = (size_t)(two ? 32 : 16) * (K + 32) * 2;
+  auto kern = RP == 8 ? (two ? rowproj_smem_kernel<1, 2> : rowproj_smem_kernel<1, 1>)
+                      : (two ? rowproj_smem_kernel<2, 2> : rowproj_smem_kernel<2, 1>);
+  launch_k(kern, g2, 32 * kRpWarps, smem, stream, reinterpret_cast<const __nv_bfloat16*>(x), ldx, n_rows, K, K_full, r, scale,
+           reinterpret_cast<const __nv_bfloat16*>(wpack), y, ldy, reinterpret_cast<__nv_bfloat16*>(yb), ldyb, x_seg, w_seg,
+           y_seg, yb_seg);
+  return launch_check("rowproj_packed_seg");
 }
 
 int lx_pack_params(const lx_pack_segment* segs, int n_segs, lx_stream_t stream) {

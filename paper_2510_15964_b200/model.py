@@ -392,12 +392,16 @@ def ensure_lora_packs(model: Model) -> bool:
                 lw.wqkv_ext, lw.wqkv = ext, ext[:d, : 3 * d]
             ext, ld = lw.wqkv_ext, 3 * d + kx
             a_qkv = torch.zeros(2, kx, d, dtype=torch.bfloat16, device=dev)
+            # the q/k/v B packs side by side ([n_t][2][RP][d]): equally spaced for the one-launch input-grad projection
+            b_qkv = torch.zeros(len(tq), 2, _rp(r), d, dtype=torch.bfloat16, device=dev)
+            lp["b_qkv"] = b_qkv
             for j, t in enumerate(tq):
                 ad, sl = lora[t], QKV_SLOT[t]
                 seg(ad.a, 1, r, r, d, a_qkv, j * r * d, d, 1, kx * d)  # rowproj pack rows j*r..
                 seg(ad.b, d, 1, r, d, ext, (d + j * r) * ld + sl * d, ld, 1, 0, ad.scaling)  # s * B_j rows
                 seg(ad.a, r, 1, d, r, ext, 3 * d + j * r, ld, 1, 0)  # A_j columns (input-grad GEMM)
-                lp["b"][t] = pack_b(ad.b, d)
+                seg(ad.b, d, 1, r, d, b_qkv[j], 0, d, 1, _rp(r) * d)  # pack_b(ad.b, d) into slot j
+                lp["b"][t] = b_qkv[j]
             lp["a_qkv"] = a_qkv
         if "w1" in lora and lora["w1"].rank <= 16:
             lp["a1"] = pack_a(lora["w1"].a, d)

@@ -273,6 +273,16 @@ def rowproj_packed(x2: torch.Tensor, n_items: int, s: int, K: int, wpack: torch.
     return y
 
 
+def rowproj_packed_seg(x2: torch.Tensor, x_seg: int, K: int, wpacks: torch.Tensor, r: int, scale: float, y: torch.Tensor,
+                       y_seg: int, yb: torch.Tensor | None, yb_seg: int, n_seg: int) -> None:
+    """n_seg dense rowproj_packed problems in one launch: Y_k = scale * X_k W_k with X_k = x2 columns offset by
+    k * x_seg, W_k = wpacks[k] ([n_seg][2][RP][K_full]), Y_k / yb_k at column offsets k * y_seg / k * yb_seg."""
+    _abi.call("lx_rowproj_packed_seg", x2.data_ptr(), x2.stride(0), int(x_seg), x2.shape[0], K, wpacks.data_ptr(),
+              wpacks[0].numel() if n_seg > 1 else 0, wpacks.shape[3], wpacks.shape[2], r, float(scale), y.data_ptr(),
+              y.stride(0), y_seg, _abi.ptr(yb), yb.stride(0) if yb is not None else 0, yb_seg, n_seg,
+              _abi.stream_handle(x2.device))
+
+
 def colgrad_problem(p: torch.Tensor | None, x2: torch.Tensor, ncols: int, r: int, scale: float, out: torch.Tensor,
                     g_sq: int, g_sc: int, masks: NeuronMasks | None = None, blk: int = 1):
     """One G(q, c) = scale * sum_rows P[row, q] X[row, c] problem (c original column) for colgrad_group.

@@ -480,3 +480,27 @@ def test_layernorm_bwd_kernel(d, dy_f32):
     ref = acc0.double() + xd.grad
     assert rel(acc, ref) < 1e-4
     assert torch.equal(ob, acc.to(torch.bfloat16))
+
+
+def test_rowproj_packed_seg_matches_per_segment():
+    """lx_rowproj_packed_seg (q/k/v LoRA input-grad projections in one launch) gives the bits of one
+    lx_rowproj_packed call per segment, on strided column slices of a fused [M, 3d + kx] operand."""
+    from paper_2510_15964_b200 import neuron_ops as N
+
+    dev = _dev()
+    M_, d, r, n_t = 1000, 512, 8, 2
+    g = torch.Generator().manual_seed(11)
+    xfull = (torch.randn(M_, 3 * d + 16, generator=g) * 0.5).to(dev, torch.bfloat16)
+    packs = (torch.randn(n_t, 2, 8, d, generator=g) * 0.1).to(dev, torch.bfloat16)
+    slots = [0, 2]
+    y = torch.full((M_, n_t * r), float("nan"), device=dev)
+    yb = torch.full((M_, 3 * d + 16), 7.0, dtype=torch.bfloat16, device=dev)
+    N.rowproj_packed_seg(xfull[:, slots[0] * d:], (slots[1] - slots[0]) * d, d, packs, r, 0.5, y, r, yb[:, 3 * d:], r, n_t)
+    ref = torch.empty(M_, n_t * r, device=dev)
+    refb = torch.full_like(yb, 7.0)
+    for j, sl in enumerate(slots):
+        N.rowproj_packed(xfull[:, sl * d:(sl + 1) * d], 1, M_, d, packs[j], r, scale=0.5, out=ref[:, j * r:(j + 1) * r],
+                         out_bf16=refb[:, 3 * d + j * r:3 * d + (j + 1) * r])
+    torch.cuda.synchronize()
+    assert torch.equal(y, ref)
+    assert torch.equal(yb, refb)
