@@ -132,7 +132,8 @@ def sweep_mlp(args, timer, peak):
         def bwd():
             a = state["hid"].values
             _abi.call("lx_neuron_fc2_dgrad", dO.data_ptr(), B, s, d, f, blk, lw.w2.data_ptr(), nm.counts.data_ptr(),
-                      nm.ids.data_ptr(), 0, 0, 0, a.data_ptr(), dz.data_ptr(), a.stride(0), state["w2p"].data_ptr(), st)
+                      nm.ids.data_ptr(), 0, 0, 0, a.data_ptr(), dz.data_ptr(), a.stride(0), state["w2p"].data_ptr(), None,
+                      st)
             _abi.call("lx_neuron_fc1_dgrad", dz.data_ptr(), dz.stride(0), B, s, d, f, blk, lw.w1_t.data_ptr(),
                       nm.counts.data_ptr(), nm.ids.data_ptr(), 0, 0, 0, dx.data_ptr(), 0, state["w1p"].data_ptr(), st)
 

@@ -118,11 +118,13 @@ int lx_predict_attention_patterns(const uint16_t* x_small, int n_items, int m, i
 
 /* neuron_matmul_fwd1 + b1 + scaling*(x A1) B1[:,cols] (+ ReLU if apply_relu)
  *   (sf/neuron_ops.py:75-82, sf/model.py:376-386)
- * ax1: fp32 [M, r] = x A1 (from lx_rowproj); b1_lora: fp32 [r, d_ff] */
+ * ax1: fp32 [M, r] = x A1 (from lx_rowproj); b1_lora: fp32 [r, d_ff]
+ * relu_bits (optional, apply_relu, ld_h % 16 == 0): also writes relu'(z) = (bf16 a > 0) as bits, uint16 [M, ld_h/16]
+ * (bit j%16 of word j/16 of a row = packed column j), the mask mlp_backward applies (sf/autograd.py:101). */
 int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w1_t,
                   const int32_t* counts, const int32_t* ids, const float* b1, const float* ax1, const float* b1_lora,
                   int r, float scaling, int apply_relu, uint16_t* a_out, int ld_h, const uint16_t* w1_packed,
-                  lx_stream_t stream);
+                  uint16_t* relu_bits, lx_stream_t stream);
 
 /* neuron_matmul_fwd2 + b2 + scaling*(a A2[cols]) B2   (sf/neuron_ops.py:85-95, sf/model.py:388-395)
  * ax2: fp32 [M, r]; b2_lora: fp32 [r, d]. out bf16, or fp32 (out_f32) with optional fused residual
@@ -133,10 +135,12 @@ int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_
                   lx_stream_t stream);
 
 /* mlp_backward input-grad through fc2 and ReLU   (sf/autograd.py:97-106)
- * dz = (dO W2[cols]^T + dax2 A2[cols]^T) * (a > 0); dax2 fp32 [M,r] (already scaled); a2: fp32 [d_ff, r] */
+ * dz = (dO W2[cols]^T + dax2 A2[cols]^T) * (a > 0); dax2 fp32 [M,r] (already scaled); a2: fp32 [d_ff, r]
+ * relu_bits (optional): lx_neuron_fc1's bits of (a > 0), read instead of the bf16 a (16x fewer epilogue bytes). */
 int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
                         const int32_t* counts, const int32_t* ids, const float* dax2, const float* a2_lora, int r,
-                        const uint16_t* a, uint16_t* dz, int ld_h, const uint16_t* w2_packed, lx_stream_t stream);
+                        const uint16_t* a, uint16_t* dz, int ld_h, const uint16_t* w2_packed, const uint16_t* relu_bits,
+                        lx_stream_t stream);
 
 /* mlp_backward input-grad through fc1   (sf/autograd.py:112-120)
  * dx = dz W1[:,cols]^T + dax1 A1^T; dax1 fp32 [M,r] (already scaled); a1: fp32 [d, r] */

@@ -35,9 +35,9 @@ SIGNATURES: dict[str, list] = {
     "lx_predict_mlp_mask": [_P, _I, _I, _I, _P, _I, _I, _F, _I, _P, _P, _P, _P, _P, _P],
     "lx_mask_compact": [_P, _I, _I, _I, _P, _P, _P, _P],
     "lx_predict_attention_patterns": [_P, _I, _I, _I, _P, _I, _I, _I, _F, _D, _I, _P, _P, _I, _I, _P, _P, _P, _P],
-    "lx_neuron_fc1": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _I, _P, _I, _P, _P],
+    "lx_neuron_fc1": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _I, _P, _I, _P, _P, _P],
     "lx_neuron_fc2": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _F, _P, _I, _P, _P, _P],
-    "lx_neuron_fc2_dgrad": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P],
+    "lx_neuron_fc2_dgrad": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _P],
     "lx_pack_active_rows": [_P, _I, _I, _I, _I, _P, _P, _P, _P],
     "lx_pack_active_rows2": [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P],
     "lx_lm_head_ce_nseg": [_I],

@@ -198,7 +198,7 @@ def mlp_backward(d_out, cache, lw: M.LayerWeights, lora: dict, neuron_mask, dims
     dz = torch.empty_like(a)
     _abi.call("lx_neuron_fc2_dgrad", dO.data_ptr(), B, s, d, f, blk, lw.mlp.w2.data_ptr(), nm.counts.data_ptr(),
               nm.ids.data_ptr(), _abi.ptr(dax2), _abi.ptr(ad2.a if ad2 else None), ad2.rank if ad2 else 0, a.data_ptr(),
-              dz.data_ptr(), a.stride(0), _abi.ptr(w2p), st)
+              dz.data_ptr(), a.stride(0), _abi.ptr(w2p), _abi.ptr(cache.get("relu_bits")), st)
     if DEBUG_TAPS is not None:
         DEBUG_TAPS[f"{prefix}dO"], DEBUG_TAPS[f"{prefix}dz"] = dO, dz
     if ad2 is not None:

@@ -413,7 +413,7 @@ static int mlp_tmap_b(CUtensorMap* tb, const uint16_t* w, const uint16_t* wp, in
 int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w1_t,
                   const int32_t* counts, const int32_t* ids, const float* b1, const float* ax1, const float* b1_lora,
                   int r, float scaling, int apply_relu, uint16_t* a_out, int ld_h, const uint16_t* w1_packed,
-                  lx_stream_t stream) {
+                  uint16_t* relu_bits, lx_stream_t stream) {
   int rc;
   if ((rc = check_blk(blk))) return rc;
   LX_REQUIRE(d_ff % blk == 0, LX_ERR_MASK, "d_ff %d not a multiple of blk %d on the device path", d_ff, blk);
@@ -421,6 +421,10 @@ int lx_neuron_fc1(const uint16_t* x, int n_items, int s, int d, int d_ff, int bl
   if ((rc = make_tmap_bf16_2d(&ta, x, d, (uint64_t)n_items * s, d, kBK, kBM))) return rc;
   if ((rc = mlp_tmap_b(&tb, w1_t, w1_packed, n_items, d, d_ff, blk, true))) return rc;
   GemmArgs args = base_args(n_items, s, 0, d);
+  LX_REQUIRE(!relu_bits || (apply_relu && ld_h % 16 == 0), LX_ERR_SHAPE,
+             "neuron_fc1: relu bits need apply_relu and ld_h %% 16 == 0");
+  args.relu_bits = relu_bits;
+  args.ld_bits = ld_h / 16;
   args.counts = counts;
   args.ids = ids;
   args.ids_stride = d_ff / blk;
@@ -482,7 +486,8 @@ int lx_neuron_fc2(const uint16_t* a, int ld_h, int n_items, int s, int d, int d_
 
 int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_ff, int blk, const uint16_t* w2,
                         const int32_t* counts, const int32_t* ids, const float* dax2, const float* a2_lora, int r,
-                        const uint16_t* a, uint16_t* dz, int ld_h, const uint16_t* w2_packed, lx_stream_t stream) {
+                        const uint16_t* a, uint16_t* dz, int ld_h, const uint16_t* w2_packed, const uint16_t* relu_bits,
+                        lx_stream_t stream) {
   int rc;
   if ((rc = check_blk(blk))) return rc;
   CUtensorMap ta, tb;
@@ -503,6 +508,9 @@ int lx_neuron_fc2_dgrad(const uint16_t* d_out, int n_items, int s, int d, int d_
   args.lora_r = (dax2 && a2_lora) ? r : 0;
   args.act = reinterpret_cast<const __nv_bfloat16*>(a);
   args.ld_act = ld_h;
+  LX_REQUIRE(!relu_bits || ld_h % 16 == 0, LX_ERR_SHAPE, "neuron_fc2_dgrad: relu bits need ld_h %% 16 == 0");
+  args.relu_bits = const_cast<uint16_t*>(relu_bits);
+  args.ld_bits = ld_h / 16;
   if (w2_packed) {
     CUtensorMap tb2, tb4;
     if ((rc = mlp_tmap_b(&tb2, w2, w2_packed, n_items, d, d_ff, blk, true, 128))) return rc;

@@ -121,6 +121,8 @@ struct GemmArgs {
   int a_k_split;        // kDense: A's K coordinate is k - a_k_split for k >= a_k_split (0: off). With B =
                         // [W_hi | W_lo] (segments a_k_split wide) one GEMM computes A W_hi + A W_lo.
   int dual_k;           // kDenseDual: K coordinate of W_lo in B (k_dense = the K extent of A and of each half)
+  uint16_t* relu_bits;  // kEpiFc1 writes / kEpiDa reads relu'(z) = (bf16 a > 0) as bits: row-major [rows][ld_bits]
+  int ld_bits;          // uint16 words per row (16 columns each; tiles start at multiples of 16 columns)
 };
 
 constexpr int kStgPitch = 80;  // bytes per staged row: 64 B of bf16 + 16 B pad (conflict-free 16 B writes)
@@ -542,13 +544,29 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           if (q < r) xr[q] = __ldg(args.lora_x + grow * r + q) * args.lora_scale;
       }
 
+      const int n_chunks = (ti.n_cols + 31) / 32;
+      constexpr int kHalf = (BMODE == kDenseDual ? BN / 2 : BN) / 64;  // 32-column chunks per column half
+      const int ch_lo = col_half * kHalf, ch_hi = min(n_chunks, (col_half + 1) * kHalf);
+      // kEpiDa with relu bits: this row's relu'(z) words for every chunk of its column half (2 B per 16 columns),
+      // loaded before the accumulator wait, so their latency hides under the tile's mainloop; rb[0] is the
+      // current chunk's word (the array shifts down one per chunk)
+      constexpr int kRb = EPI == kEpiDa ? kHalf : 1;
+      uint32_t rb[kRb];
+      const bool use_bits = EPI == kEpiDa && args.relu_bits != nullptr;
+#pragma unroll
+      for (int k = 0; k < kRb; ++k) {
+        rb[k] = 0u;
+        const int ch = ch_lo + k;
+        if (use_bits && row_ok && ch < ch_hi) {
+          const uint16_t* bp = args.relu_bits + grow * args.ld_bits + (ti.n0 + ch * 32) / 16;
+          rb[k] = (uint32_t)__ldg(bp) | ((ch * 32 + 16 < ti.n_cols) ? (uint32_t)__ldg(bp + 1) << 16 : 0u);
+        }
+      }
+
       mbar_wait(tfull + buf, kAccBufs == 2 ? ((it >> 1) & 1) : (it & 1));
       if (ep_tid == 0 && it < 3) gemm_stamp(4 + 4 * it);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;
-      const int n_chunks = (ti.n_cols + 31) / 32;
-      constexpr int kHalf = (BMODE == kDenseDual ? BN / 2 : BN) / 64;  // 32-column chunks per column half
-      const int ch_lo = col_half * kHalf, ch_hi = min(n_chunks, (col_half + 1) * kHalf);
       // software-pipelined: chunk ch + 1's TMEM load is in flight while chunk ch is processed
       uint32_t raw[32];
       // kEpiCe: max of this row's logits over the column half (its segment); exp / sum / store in the chunk loop
@@ -640,7 +658,28 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
         }
-        if (EPI == kEpiDa) {
+        if (EPI == kEpiFc1 && args.relu_bits != nullptr && row_ok) {
+          // relu'(z) of the stored bf16 activation: nonzero with the sign bit clear
+          uint32_t word = 0;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint32_t pk = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+            const uint32_t lo = pk & 0xffffu, hi = pk >> 16;
+            word |= (uint32_t)(2 * i < nv && lo != 0u && (lo & 0x8000u) == 0u) << (2 * i);
+            word |= (uint32_t)(2 * i + 1 < nv && hi != 0u && (hi & 0x8000u) == 0u) << (2 * i + 1);
+          }
+          uint16_t* bp = args.relu_bits + grow * args.ld_bits + j0 / 16;
+          bp[0] = (uint16_t)(word & 0xffffu);
+          if (nv > 16) bp[1] = (uint16_t)(word >> 16);
+        }
+
+        if (EPI == kEpiDa && use_bits) {
+          const uint32_t word = rb[0];
+#pragma unroll
+          for (int k = 0; k + 1 < kRb; ++k) rb[k] = rb[k + 1];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = ((word >> i) & 1u) ? v[i] : 0.f;
+        } else if (EPI == kEpiDa) {
           if (row_ok) {
             const __nv_bfloat16* ap = args.act + grow * args.ld_act + j0;
             uint32_t aw[16];

@@ -744,9 +744,12 @@ def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, c
         ax1 = rowproj_packed(x2, B, s, d, lp["a1"], ad1.rank)
     else:
         ax1 = rowproj(x2, B, s, d, ad1.a, ad1.rank, 1, ad1.rank)
+    # relu'(z) as bits beside the bf16 activation: the fc2 input-grad epilogue reads 1/16 of the bytes
+    relu_bits = torch.empty(B * s, f // 16, dtype=torch.int16, device=x2.device) if f % 16 == 0 else None
     hid = neuron_ops.neuron_matmul_fwd1(x2.view(B, s, d), lw.mlp, nm, blk, counter, bias=lw.b1, ax=ax1,
                                         lora_b=ad1.b if ad1 else None, lora_r=ad1.rank if ad1 else 0,
-                                        scaling=ad1.scaling if ad1 else 1.0, relu=True, w_packed=w1p)
+                                        scaling=ad1.scaling if ad1 else 1.0, relu=True, w_packed=w1p,
+                                        relu_bits=relu_bits)
     if ad2 is None:
         ax2 = None
     elif lp is not None and lp.get("a2") is not None:
@@ -763,7 +766,7 @@ def mlp_forward(x, lw: LayerWeights, lora: dict, neuron_mask, dims: ModelDims, c
             counter.add(s * (d + n_act // max(B, 1)) * ad1.rank * B)
         if ad2 is not None:
             counter.add(s * (n_act // max(B, 1) + d) * ad2.rank * B)
-    return out, {"x": x2, "a": hid, "mask": nm, "ax1": ax1, "ax2": ax2, "n_items": B, "s": s,
+    return out, {"x": x2, "a": hid, "mask": nm, "ax1": ax1, "ax2": ax2, "n_items": B, "s": s, "relu_bits": relu_bits,
                  "w1p": w1p if keep else None, "w2p": w2p if keep else None, "repack": pack and not keep}
 
 

@@ -181,9 +181,10 @@ def _check_device_blk(d_ff: int, blk: int) -> None:
 
 
 def neuron_matmul_fwd1(x, weights: LayeredWeights, mask, blk_size: int, counter=None, *, bias=None, ax=None, lora_b=None,
-                       lora_r=0, scaling=1.0, relu=False, out=None, w_packed=None) -> ActiveHidden:
+                       lora_r=0, scaling=1.0, relu=False, out=None, w_packed=None, relu_bits=None) -> ActiveHidden:
     """x @ W1[:, cols] over active column blocks (sf/neuron_ops.py:75-82) on the tcgen05
-    N-gather GEMM. Optional fused epilogue (used by mlp_forward): + bias[cols] + scaling*ax B[:,cols], ReLU."""
+    N-gather GEMM. Optional fused epilogue (used by mlp_forward): + bias[cols] + scaling*ax B[:,cols], ReLU.
+    `relu_bits` (int16 [M, d_ff/16], with relu): also receives relu'(z) as bits for lx_neuron_fc2_dgrad."""
     d_ff, d = weights.w1_t.shape
     _check_device_blk(d_ff, blk_size)
     x2, B, s = _as_items(x.to(torch.bfloat16))
@@ -191,7 +192,7 @@ def neuron_matmul_fwd1(x, weights: LayeredWeights, mask, blk_size: int, counter=
     vals = out if out is not None else torch.empty(B * s, d_ff, dtype=torch.bfloat16, device=x2.device)
     _abi.call("lx_neuron_fc1", x2.data_ptr(), B, s, d, d_ff, blk_size, weights.w1_t.data_ptr(), nm.counts.data_ptr(),
               nm.ids.data_ptr(), _abi.ptr(bias), _abi.ptr(ax), _abi.ptr(lora_b), lora_r, float(scaling), int(relu),
-              vals.data_ptr(), d_ff, _abi.ptr(w_packed), _abi.stream_handle(x2.device))
+              vals.data_ptr(), d_ff, _abi.ptr(w_packed), _abi.ptr(relu_bits), _abi.stream_handle(x2.device))
     if counter is not None:
         counter.add(s * d * int(nm.counts.sum()) * blk_size)
     return ActiveHidden(vals, nm, blk_size, d_ff, B)

@@ -41,7 +41,7 @@ def test_error_mapping_without_gpu():
         pytest.skip("extension not built")
     with pytest.raises(E.UnsupportedError):
         _abi.call("lx_neuron_fc1", None, 1, 16, 64, 64, 24, None, None, None, None, None, None, 0, 1.0, 1, None, 64, None,
-                  None)
+                  None, None)
     with pytest.raises(E.LayoutError):  # gather_rows must be a power of two in [16, 128]
         _abi.call("lx_bsattn_fwd_tc", None, 192, 1, 128, 1, 64, None, 0, None, 48, 0.125, None, 64, None, None)
     assert issubclass(E.LayoutError, ValueError) and issubclass(E.MaskError, ValueError)

@@ -102,14 +102,21 @@ def test_neuron_mlp_gemms(n_items, s, d, d_ff, blk, density, r, packed, engine):
             _abi.call("lx_pack_active_rows", src.data_ptr(), d_ff, d, blk, n_items, cnt_d.data_ptr(), ids_d.data_ptr(),
                       dst.data_ptr(), st)
         WP1, WP2 = w1p.data_ptr(), w2p.data_ptr()
+    bits = torch.zeros(M, ld_h // 16, device=dev, dtype=torch.int16) if ld_h % 16 == 0 else None
     _abi.call("lx_neuron_fc1", x.data_ptr(), n_items, s, d, d_ff, blk, w1t.data_ptr(), cnt_d.data_ptr(), ids_d.data_ptr(),
-              b1.data_ptr(), P(ax1), P(B1), r, scaling, 1, a.data_ptr(), ld_h, WP1, st)
+              b1.data_ptr(), P(ax1), P(B1), r, scaling, 1, a.data_ptr(), ld_h, WP1, _abi.ptr(bits), st)
     out = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
     _abi.call("lx_neuron_fc2", a.data_ptr(), ld_h, n_items, s, d, d_ff, blk, w2.data_ptr(), cnt_d.data_ptr(), ids_d.data_ptr(),
               b2.data_ptr(), P(ax2), P(B2), r, scaling, out.data_ptr(), 0, None, WP2, st)
     dz = torch.zeros(M, ld_h, device=dev, dtype=torch.bfloat16)
     _abi.call("lx_neuron_fc2_dgrad", d_out.data_ptr(), n_items, s, d, d_ff, blk, w2.data_ptr(), cnt_d.data_ptr(),
-              ids_d.data_ptr(), P(dax2), P(A2), r, a.data_ptr(), dz.data_ptr(), ld_h, WP2, st)
+              ids_d.data_ptr(), P(dax2), P(A2), r, a.data_ptr(), dz.data_ptr(), ld_h, WP2, None, st)
+    if bits is not None:  # relu'(z) from fc1's bits instead of the bf16 activation: the same dz bits
+        dz_b = torch.zeros_like(dz)
+        _abi.call("lx_neuron_fc2_dgrad", d_out.data_ptr(), n_items, s, d, d_ff, blk, w2.data_ptr(), cnt_d.data_ptr(),
+                  ids_d.data_ptr(), P(dax2), P(A2), r, a.data_ptr(), dz_b.data_ptr(), ld_h, WP2, bits.data_ptr(), st)
+        torch.cuda.synchronize()
+        assert torch.equal(dz_b, dz)
     dx = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
     _abi.call("lx_neuron_fc1_dgrad", dz.data_ptr(), ld_h, n_items, s, d, d_ff, blk, w1t.data_ptr(), cnt_d.data_ptr(),
               ids_d.data_ptr(), P(dax1), P(A1), r, dx.data_ptr(), 0, WP1, st)

@@ -24,11 +24,12 @@ out = torch.empty(B * s, d, device=dev, dtype=torch.bfloat16)
 resid = torch.randn(B * s, d, device=dev)
 st = _abi.stream_handle()
 buf = torch.zeros(160, 32, dtype=torch.int64, device=dev)
+bits = torch.zeros(B * s, f // 16, dtype=torch.int16, device=dev)
 
 
 def fc1():
     _abi.call("lx_neuron_fc1", x.data_ptr(), B, s, d, f, blk, w1t.data_ptr(), nm.counts.data_ptr(), nm.ids.data_ptr(),
-              None, None, None, 0, 1.0, 1, h.data_ptr(), f, w1p.data_ptr(), st)
+              None, None, None, 0, 1.0, 1, h.data_ptr(), f, w1p.data_ptr(), bits.data_ptr(), st)
 
 
 def fc2():
@@ -36,9 +37,24 @@ def fc2():
               None, None, None, 0, 1.0, out.data_ptr(), 0, None, w2p.data_ptr(), st)
 
 
+dz = torch.empty(B * s, f, device=dev, dtype=torch.bfloat16)
+dxo = torch.empty(B * s, d, device=dev, dtype=torch.bfloat16)
+
+
+def fc2_dgrad():  # dz = (dO W2[cols]^T) * relu'(a), a = fc1's output h
+    _abi.call("lx_neuron_fc2_dgrad", out.data_ptr(), B, s, d, f, blk, w2.data_ptr(), nm.counts.data_ptr(),
+              nm.ids.data_ptr(), None, None, 0, h.data_ptr(), dz.data_ptr(), f, w2p.data_ptr(),
+              bits.data_ptr() if "--bits" in sys.argv else None, st)
+
+
+def fc1_dgrad():  # dx = dz W1[:, cols]^T
+    _abi.call("lx_neuron_fc1_dgrad", dz.data_ptr(), f, B, s, d, f, blk, w1t.data_ptr(), nm.counts.data_ptr(),
+              nm.ids.data_ptr(), None, None, 0, dxo.data_ptr(), 0, w1p.data_ptr(), st)
+
+
 for pair in ((0,) if "--default" in sys.argv else (2, 1, 0)):
     _abi.lib().lx_gemm_set_cta_pair(pair)
-    for name, fn in (("fc1", fc1), ("fc2", fc2)):
+    for name, fn in (("fc1", fc1), ("fc2", fc2), ("fc2_dgrad", fc2_dgrad), ("fc1_dgrad", fc1_dgrad)):
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
