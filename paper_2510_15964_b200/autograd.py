@@ -24,7 +24,8 @@ from . import _abi
 from . import model as M
 from .block_sparse import attention_backward
 from .errors import GradientError
-from .neuron_ops import colgrad_group, colgrad_problem, pack_active_rows2, rowproj, rowproj_packed, rowproj_packed_seg
+from .neuron_ops import (ROWPROJ_SEG_MAX_K, colgrad_group, colgrad_problem, pack_active_rows2, rowproj, rowproj_packed,
+                         rowproj_packed_seg)
 
 
 def check_gradient_set(grads: dict, model: M.Model) -> None:
@@ -266,7 +267,7 @@ def mha_backward(d_out, cache, lw: M.LayerWeights, lora: dict, dims: M.ModelDims
         dax = torch.empty(B * s, len(tq) * r, dtype=torch.float32, device=dev)
         slots = [M.QKV_SLOT[t] for t in tq]
         bq = lw.lora_pack.get("b_qkv") if ext else None
-        one = (bq is not None and len({lora[t].scaling for t in tq}) == 1
+        one = (bq is not None and d <= ROWPROJ_SEG_MAX_K and len({lora[t].scaling for t in tq}) == 1
                and all(b - a == slots[1] - slots[0] for a, b in zip(slots, slots[1:])))
         if one:
             # every target's dAx_t = dqkv[:, slot_t] B_t^T * s in one launch (equally spaced slots / packs / columns)

@@ -274,6 +274,9 @@ def rowproj_packed(x2: torch.Tensor, n_items: int, s: int, K: int, wpack: torch.
     return y
 
 
+ROWPROJ_SEG_MAX_K = 4096  # lx_rowproj_packed_seg stages X rows in shared memory (kRpsMaxK in csrc/lora.cu)
+
+
 def rowproj_packed_seg(x2: torch.Tensor, x_seg: int, K: int, wpacks: torch.Tensor, r: int, scale: float, y: torch.Tensor,
                        y_seg: int, yb: torch.Tensor | None, yb_seg: int, n_seg: int) -> None:
     """n_seg dense rowproj_packed problems in one launch: Y_k = scale * X_k W_k with X_k = x2 columns offset by

@@ -402,3 +402,23 @@ def test_repacked_backward_equals_cached_packs(dev, monkeypatch):
         torch.cuda.synchronize()
         out.append(eng.flat_grad.clone())
     assert torch.equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("peft", ["lora", "adapter", "bitfit"])
+def test_engine_step_wide_model(dev, peft):
+    """One engine step at cfg5's width (d = 5120, hd 128): the branches taken only above the staged-row limits
+    (q/k/v LoRA input-grads per target instead of one segmented launch, block LayerNorm kernels, head-dim-128
+    attention) run, and the loss and every gradient are finite."""
+    import bench
+    from paper_2510_15964_b200.engine import FinetuneEngine
+
+    cfg = dict(d=5120, H=40, d_ff=20480, L=1, V=256, B=1, s=256, blk=16, attn_blk=128, r=8)
+    model, state, prov = bench.build_workload(cfg, dev, 3, 0.85, 0.75, peft=peft)
+    eng = FinetuneEngine(model, state, prov, lr=1e-4)
+    tok = torch.randint(0, cfg["V"], (cfg["B"], cfg["s"] + 1), generator=torch.Generator().manual_seed(2)).to(dev)
+    before = state.flat.clone()
+    loss = float(eng.step(tok))
+    torch.cuda.synchronize()
+    assert np.isfinite(loss)
+    assert torch.isfinite(state.flat).all()
+    assert not torch.equal(state.flat, before)
