@@ -256,12 +256,14 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   }
   // prologue above overlaps the predecessor kernel's tail (programmatic dependent launch)
   pdl_wait_trigger();
+  if (threadIdx.x == 0) gemm_stamp(14);
   // ---- tile table: prefix[b] = first tile index of item b (counts are device-resident)
   // counts -> shared memory in one parallel round trip (the epilogue's staging area is free until the first tile)
   int* s_cnt = reinterpret_cast<int*>(smem + L::kEpiOff);
   if (!is_dense<BMODE>())
     for (int b = threadIdx.x; b < args.n_items; b += blockDim.x) s_cnt[b] = __ldg(args.counts + b);
   __syncthreads();
+  if (threadIdx.x == 0) gemm_stamp(15);
   if (warp == 0) {
     // warp-parallel: lane L tests the width (L + 1) * kWq, then a warp scan builds the item prefix
     int wsel = (kWide && EPI == kEpiCe) ? BN : 0;  // CE segments are BN / 2 columns: full-width tiles
@@ -294,10 +296,12 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     }
     if (lane == 0) prefix[args.n_items] = carry;
   }
+  if (threadIdx.x == 0) gemm_stamp(16);
   tc_fence_before();
   __syncthreads();
   if (CTAS == 2) cluster_sync();  // both CTAs' barriers initialised before any cross-CTA signal
   tc_fence_after();
+  if (threadIdx.x == 0) gemm_stamp(17);
   const uint32_t tmem_base = *tmem_slot;
   const int n_tiles_total = prefix[args.n_items];
   const int wsel = *wsel_s;
@@ -563,6 +567,13 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         }
       }
 
+      // kEpiFc1 relu bits: a full column half of 8 full chunks at a 256-column boundary is collected in registers
+      // and written as two 16-byte stores (per-chunk 2-byte stores cost a partial-sector write each)
+      constexpr int kBw = (EPI == kEpiFc1 && kHalf == 8) ? 8 : 1;
+      uint32_t bw[kBw];
+      const bool bits_vec = kBw == 8 && args.relu_bits != nullptr && row_ok && (args.ld_bits % 8) == 0 &&
+                            ((ti.n0 + ch_lo * 32) % 256) == 0 && ch_hi - ch_lo == 8 && ch_hi * 32 <= ti.n_cols;
+
       mbar_wait(tfull + buf, kAccBufs == 2 ? ((it >> 1) & 1) : (it & 1));
       if (ep_tid == 0 && it < 3) gemm_stamp(4 + 4 * it);
       tc_fence_after();
@@ -658,21 +669,35 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
         }
-        if (EPI == kEpiFc1 && args.relu_bits != nullptr && row_ok) {
-          // relu'(z) of the stored bf16 activation: nonzero with the sign bit clear
-          uint32_t word = 0;
+        // kEpiFc1 relu bits from the packed bf16 words pk[16] of this chunk (see relu_bits in GemmArgs)
+        auto relu_bits_store = [&](const uint32_t* pk) {
+          if (!(EPI == kEpiFc1 && args.relu_bits != nullptr && row_ok)) return;
+          // per bf16 half: a > 0 by one bf16x2 compare (1.0 / 0.0 per half: bit 7 of each half), two bits per pair
+          uint32_t m2[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const uint32_t pk = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-            const uint32_t lo = pk & 0xffffu, hi = pk >> 16;
-            word |= (uint32_t)(2 * i < nv && lo != 0u && (lo & 0x8000u) == 0u) << (2 * i);
-            word |= (uint32_t)(2 * i + 1 < nv && hi != 0u && (hi & 0x8000u) == 0u) << (2 * i + 1);
+            const __nv_bfloat162 gt = __hgt2(*reinterpret_cast<const __nv_bfloat162*>(&pk[i]), __float2bfloat162_rn(0.f));
+            const uint32_t g = *reinterpret_cast<const uint32_t*>(&gt);
+            m2[i] = ((g >> 7) & 1u) | ((g >> 22) & 2u);
           }
-          uint16_t* bp = args.relu_bits + grow * args.ld_bits + j0 / 16;
-          bp[0] = (uint16_t)(word & 0xffffu);
-          if (nv > 16) bp[1] = (uint16_t)(word >> 16);
-        }
-
+#pragma unroll
+          for (int i = 0; i < 8; ++i) m2[i] = m2[2 * i] | (m2[2 * i + 1] << 2);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) m2[i] = m2[2 * i] | (m2[2 * i + 1] << 4);
+#pragma unroll
+          for (int i = 0; i < 2; ++i) m2[i] = m2[2 * i] | (m2[2 * i + 1] << 8);
+          uint32_t word = m2[0] | (m2[1] << 16);
+          if (nv < 32) word &= (1u << nv) - 1u;
+          if (bits_vec) {  // collected, stored as 32 contiguous bytes after the last chunk
+#pragma unroll
+            for (int k = 0; k + 1 < kBw; ++k) bw[k] = bw[k + 1];
+            bw[kBw - 1] = word;
+          } else {
+            uint16_t* bp = args.relu_bits + grow * args.ld_bits + j0 / 16;
+            bp[0] = (uint16_t)(word & 0xffffu);
+            if (nv > 16) bp[1] = (uint16_t)(word >> 16);
+          }
+        };
         if (EPI == kEpiDa && use_bits) {
           const uint32_t word = rb[0];
 #pragma unroll
@@ -739,6 +764,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
           uint32_t p[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) p[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+          relu_bits_store(p);
           uint8_t* mine = stg + lane * kStgPitch;
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -759,14 +785,26 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             uint32_t p[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) p[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+            relu_bits_store(p);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
               *reinterpret_cast<uint4*>(o + 8 * i) = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
           } else {
+            uint32_t p[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) p[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+            relu_bits_store(p);
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               if (i < nv) o[i] = __float2bfloat16_rn(v[i]);
           }
+        }
+      }
+      if constexpr (kBw == 8) {
+        if (bits_vec) {
+          uint4* bp = reinterpret_cast<uint4*>(args.relu_bits + grow * args.ld_bits + (ti.n0 + ch_lo * 32) / 16);
+          bp[0] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+          bp[1] = make_uint4(bw[4], bw[5], bw[6], bw[7]);
         }
       }
       if (EPI == kEpiCe && row_ok) {

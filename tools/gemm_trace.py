@@ -29,7 +29,8 @@ bits = torch.zeros(B * s, f // 16, dtype=torch.int16, device=dev)
 
 def fc1():
     _abi.call("lx_neuron_fc1", x.data_ptr(), B, s, d, f, blk, w1t.data_ptr(), nm.counts.data_ptr(), nm.ids.data_ptr(),
-              None, None, None, 0, 1.0, 1, h.data_ptr(), f, w1p.data_ptr(), bits.data_ptr(), st)
+              None, None, None, 0, 1.0, 1, h.data_ptr(), f, w1p.data_ptr(), bits.data_ptr() if "--bits" in sys.argv else None,
+              st)
 
 
 def fc2():
@@ -94,6 +95,8 @@ for pair in ((0,) if "--default" in sys.argv else (2, 1, 0)):
         rel = np.where(t > 0, t - base, 0)
         print(f"{name} pair={pair}: {us:.1f} us/launch (graph {us_graph:.1f}), CTAs with a tile {act.sum()}; lifetime mean "
               f"{(t[:, 1] - t[:, 0]).mean():.0f} cyc")
+        pro = [np.median(rel[act, k]) for k in (14, 15, 16, 17)]
+        print(f"   prologue: pdl wait {pro[0]:.0f}  counts {pro[1]:.0f}  width/prefix {pro[2]:.0f}  cluster sync {pro[3]:.0f}")
         for i in range(2):
             sel = t[:, 2 + 4 * i] > 0
             if not sel.any():
