@@ -254,6 +254,9 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     if (CTAS == 2) tmem_alloc_cg2<512>(tmem_slot);
     else tmem_alloc<512>(tmem_slot);
   }
+  // pairs: arrive on the cluster barrier now (barrier inits released), wait once the tile table is built, so
+  // the peer handshake overlaps the PDL wait and the prologue instead of following it
+  if (CTAS == 2) cluster_arrive();
   // prologue above overlaps the predecessor kernel's tail (programmatic dependent launch)
   pdl_wait_trigger();
   if (threadIdx.x == 0) gemm_stamp(14);
@@ -299,7 +302,7 @@ gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   if (threadIdx.x == 0) gemm_stamp(16);
   tc_fence_before();
   __syncthreads();
-  if (CTAS == 2) cluster_sync();  // both CTAs' barriers initialised before any cross-CTA signal
+  if (CTAS == 2) cluster_wait();  // both CTAs' barriers initialised before any cross-CTA signal
   tc_fence_after();
   if (threadIdx.x == 0) gemm_stamp(17);
   const uint32_t tmem_base = *tmem_slot;
